@@ -70,15 +70,28 @@ def rank_caps(dims, j: int, r: int, p: int):
     return ell, min(int(r), ell)
 
 
+def canonical_signs(u: np.ndarray) -> np.ndarray:
+    """DESIGN reading R4b: the thin SVD fixes singular vectors only up to sign; we
+    fix it so that the entry of largest magnitude of each column of U_hat = Q U_B(:,1:r)
+    is positive (first such row on ties).  Needed because in Alg 3 the next sketch
+    G_(rho_j) Omega depends on the basis of the shrunk core.  Returns the +-1 vector."""
+    idx = np.argmax(np.abs(u), axis=0)
+    s = np.sign(u[idx, np.arange(u.shape[1])])
+    s[s == 0] = 1.0
+    return s
+
+
 def randsvd(xm: np.ndarray, r: int, p: int, omega: np.ndarray):
     """Alg 1 RandSVD(X, r, p, Omega).  Returns (U_hat, Sigma_hat, V_hat^T)
-    plus the diagnostics (Q, B, U_B, all singular values of B)."""
+    plus the diagnostics (Q, B, U_B, all singular values of B).  Signs per reading R4b."""
     y = xm @ omega                                        # line 1: Y = X Omega
     q, _ = np.linalg.qr(y, mode="reduced")                # line 2: Y = QR (Householder, LAPACK)
     b = q.T @ xm                                          # line 3: B = Q^T X
     ub, s, vt = np.linalg.svd(b, full_matrices=False)     # line 4: thin SVD of B
     u = q @ ub[:, :r]                                     # line 5: U_hat = Q U_B(:, 1:r)
-    return u, s[:r], vt[:r, :], dict(q=q, b=b, ub=ub, s_all=s)   # line 6
+    sg = canonical_signs(u)
+    u, vt = u * sg[None, :], vt[:r, :] * sg[:, None]      # (U, V) -> (U D, V D), D = diag(+-1)
+    return u, s[:r], vt, dict(q=q, b=b, ub=ub, s_all=s)   # line 6
 
 
 def _omega_for(seed, j, ncols, ell, k0=0):
@@ -171,7 +184,9 @@ def adapt_range_finder(xm: np.ndarray, tau_sq: float, b: int, seed: int, mode: i
     ok = np.nonzero(norm2 - cums <= tau_sq)[0]
     r = int(ok[0]) + 1 if ok.size else k
     info.update(r=r, s=s)
-    return q @ ub[:, :r], s[:r, None] * vt[:r, :], info
+    a = q @ ub[:, :r]
+    sg = canonical_signs(a)                               # reading R4b
+    return a * sg[None, :], (s[:r, None] * vt[:r, :]) * sg[:, None], info
 
 
 def _mode_tols(eps, d, mode_tol):
@@ -251,8 +266,9 @@ def sthosvd(x: np.ndarray, ranks, order=None) -> TuckerResult:
     for j in order:
         u, s, vt = np.linalg.svd(unfold(g, j), full_matrices=False)
         r = ranks[j]
-        factors[j] = u[:, :r]
-        g = fold(s[:r, None] * vt[:r, :], j, g.shape)
+        sg = canonical_signs(u[:, :r])
+        factors[j] = u[:, :r] * sg[None, :]
+        g = fold((s[:r, None] * vt[:r, :]) * sg[:, None], j, g.shape)
     return TuckerResult(g, factors, tuple(ranks), tuple(ranks), order, -1)
 
 
