@@ -1,0 +1,290 @@
+#!/usr/bin/env python3
+"""Benchmark of the randomized Tucker hot path (BASELINE.json metric
+"R-HOSVD/R-STHOSVD Gelem/s; sketch/TTM % of HBM roofline, 1/2/4/8 GPUs").
+
+Step = one R-STHOSVD (Alg 3) of BASELINE configs[3] (C4): 800x800x800 fp32 orthogonally
+decomposable tensor, r=(50,50,50), p=10, rho=[1,2,3], seed 0, resident in HBM
+(2.05 GB > 126 MB L2, so every step streams from HBM; no flush needed).
+With --gpus N>1 (torchrun) the tensor is sharded along mode 3 (strong scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--algo sthosvd|hosvd]
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §8 for every field).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+I = 800
+RANKS = (50, 50, 50)
+P = 10
+ORDER = (0, 1, 2)
+SEED = 0
+DATA_SEED = 4
+N_ELEM = I * I * I
+BYTES_X = N_ELEM * 4
+METRIC = "R-STHOSVD Gelem/s (C4 800^3 fp32, r=50, p=10)"
+
+
+def workload_config(algo, n):
+    return {"workload": f"C4 odeco 800x800x800 fp32 R-{algo.upper()} r=(50,50,50) p=10 rho=[1,2,3] seed=0",
+            "algorithm": f"R-{algo.upper()}", "dims": [I, I, I], "dtype": "fp32", "ranks": list(RANKS), "p": P,
+            "order": [1, 2, 3], "parallelism": f"mode-3 slabs x{n}" if n > 1 else "single GPU",
+            "l2": "input 2.05 GB > 126 MB L2: every step streams X from HBM (no flush needed)",
+            "data": "synthetic (workloads.odeco, data seed 4)"}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        return float(m["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (clocks line of B200_PROFILING.md)."""
+
+    def __init__(self, idx):
+        self.idx = idx
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            t = [x.strip() for x in line.split(",")]
+            if len(t) < 9:
+                continue
+            try:
+                sm.append(float(t[1]))
+                smax = max(smax, float(t[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, t[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def oracle_sample_input(slabs: int):
+    import numpy as np
+    from workloads import odeco
+    x = odeco(I, seed=DATA_SEED, dtype=np.float32, device="cpu", slabs=(0, slabs)).numpy()
+    return x.reshape((I, I, slabs), order="F")
+
+
+def cpu_oracle_sample(slabs: int = 300, x=None):
+    """The oracle (oracle/, fp64 numpy) as it stands on a bounded sample of the workload:
+    R-STHOSVD of the first `slabs` mode-3 slabs of C4 (800 x 800 x slabs), same ranks."""
+    import oracle as O
+    x = oracle_sample_input(slabs) if x is None else x
+    t0 = time.perf_counter()
+    O.r_sthosvd(x, (50, 50, min(50, slabs)), P, SEED, ORDER)
+    dt = time.perf_counter() - t0
+    return x.size / dt / 1e9, dt, f"oracle r_sthosvd on C4[:, :, :{slabs}] (800x800x{slabs}, {x.size} elem)"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count()
+    slabs = 100
+    x = oracle_sample_input(slabs)
+    vals = []
+    for _ in range(args.warmup):
+        cpu_oracle_sample(slabs, x)
+    for _ in range(args.steps):
+        v, dt, sample = cpu_oracle_sample(slabs, x)
+        vals.append((v, dt))
+    v = statistics.median([a for a, _ in vals])
+    ms = statistics.median([b for _, b in vals]) * 1e3
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "Gelem/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args.algo, args.gpus),
+            "cpu_baseline": {"value": v, "unit": "Gelem/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--algo", default="sthosvd", choices=["sthosvd", "hosvd"])
+    ap.add_argument("--flags", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1905_07311_b200.rtucker import Context, RESULT_HOST
+    from workloads import odeco
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    assert world == args.gpus or world == 1, "launch N>1 with torchrun --nproc-per-node N"
+
+    # ---- input: C4, sharded along mode 3 when world > 1
+    ext = [I // world + (1 if r < I % world else 0) for r in range(world)]
+    off = sum(ext[:rank])
+    x = odeco(I, seed=DATA_SEED, dtype=np.float32, device=f"cuda:{local}", slabs=(off, off + ext[rank]))
+    shard = (off, ext[rank]) if world > 1 else None
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream()  # the library enqueues every kernel of a step on this stream
+    ctx = Context(local, stream=stream, group=dist.group.WORLD if world > 1 else None)
+
+    def step(inp, flags=0):
+        if args.algo == "sthosvd":
+            return ctx.sthosvd(inp, (I, I, I), RANKS, P, SEED, ORDER, flags | args.flags, shard=shard)
+        return ctx.hosvd(inp, (I, I, I), RANKS, P, SEED, flags | args.flags, shard=shard)
+
+    for _ in range(args.warmup):
+        step(x).free()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, barrier + sync on both sides, CUDA events on the ctx stream
+    ctx.set_profiling(True)
+    ctx.phase_times(reset=True)
+    clocks = Clocks(local)
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.launches
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    results = []
+    for _ in range(args.steps):
+        results.append(step(x))
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launches - l0
+    ms_local = e0.elapsed_time(e1) / args.steps
+    clk = clocks.stop()
+    phases = ctx.phase_times(reset=True)
+    ctx.set_profiling(False)
+    for r in results:
+        r.free()
+    ms = ms_local
+    if world > 1:
+        t = torch.tensor([ms_local], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = N_ELEM / (ms * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel: the mode-1 sketch (reads X once)
+    hbm, peak_src = peaks()
+    sk_ms, sk_n = phases.get(("sketch", 0), (0.0, 0))
+    bp_ms, bp_n = phases.get(("bpass", 0), (0.0, 0))
+    dom = "sketch_mode1"
+    t_kernel = sk_ms / max(sk_n, 1)
+    algo_bytes = BYTES_X // world + 0  # X read once; Y (800x60 fp64) is negligible
+    achieved = algo_bytes / (t_kernel * 1e-3) / 1e9 if t_kernel > 0 else 0.0
+    step_phase_ms = {f"{k[0]}{k[1] + 1}": round(v[0] / max(v[1], 1), 4) for k, v in sorted(phases.items())}
+
+    # ---- end-to-end through the public API with HOST buffers (H2D + D2H inside the region)
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty(x.numel(), dtype=torch.float32, pin_memory=True)
+        xh.copy_(x)
+        del x
+        torch.cuda.empty_cache()
+        step(xh, RESULT_HOST).free()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d2h = 0
+        for _ in range(args.steps):
+            r = step(xh, RESULT_HOST)
+            s = r.s
+            d2h = sum(int(s.dims[k]) * int(s.ranks[k]) * 8 for k in range(3)) + int(np.prod([s.ranks[k] for k in range(3)])) * 8
+            r.free()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / args.steps
+        if world > 1:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": N_ELEM / dt / 1e9, "unit": "Gelem/s", "h2d_bytes_per_step": BYTES_X // world,
+               "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3}
+
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline:
+            v, dt, sample = cpu_oracle_sample(300)
+            cpu = {"value": v, "unit": "Gelem/s", "cores": os.cpu_count(), "kind": "oracle", "sample": sample,
+                   "seconds": dt}
+        line = {
+            "metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(args.algo, world),
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms": t_kernel,
+                         "bpass_mode1_ms": bp_ms / max(bp_n, 1)},
+            "phase_ms": step_phase_ms,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

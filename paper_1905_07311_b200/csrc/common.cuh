@@ -1,0 +1,149 @@
+// Shared host/device plumbing for librtucker (no method arithmetic here).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string>
+#include <vector>
+#include <stdexcept>
+
+#include "../../include/rtucker.h"
+
+namespace rt {
+
+constexpr int kMaxModes = RTUCKER_MAX_MODES;
+
+// Error carried through the orchestrator as an exception and mapped to a status code
+// at the C boundary.
+struct Error : std::runtime_error {
+  rtucker_status code;
+  Error(rtucker_status c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+#define RT_REQUIRE(cond, msg)                                                          \
+  do {                                                                                 \
+    if (!(cond)) throw ::rt::Error(RTUCKER_EINVAL, std::string(msg));                  \
+  } while (0)
+
+#define RT_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      char b_[512];                                                                    \
+      snprintf(b_, sizeof b_, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_),  \
+               __FILE__, __LINE__);                                                    \
+      throw ::rt::Error(e_ == cudaErrorMemoryAllocation ? RTUCKER_ENOMEM : RTUCKER_ECUDA, \
+                        b_);                                                           \
+    }                                                                                  \
+  } while (0)
+
+struct Comm;  // comm.cpp
+
+// Phase timing (measurement only): CUDA events recorded on the context stream around
+// each step of the path; resolved lazily by rtucker_phase_times().
+enum Phase { PH_SKETCH = 0, PH_QR = 1, PH_BPASS = 2, PH_EIG = 3, PH_SHRINK = 4, PH_OTHER = 5, PH_COUNT = 6 };
+
+struct PhaseEvent {
+  int slot;  // phase * kMaxModes + position of the mode in the processing order
+  cudaEvent_t a, b;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int rank = 0, nranks = 1;
+  Comm *comm = nullptr;
+  uint64_t launches = 0;
+  int num_sms = 148;
+  std::string last_error;
+  bool profiling = false;
+  std::vector<PhaseEvent> events;
+  double phase_ms[PH_COUNT * kMaxModes] = {0};
+  int64_t phase_n[PH_COUNT * kMaxModes] = {0};
+};
+
+// RAII scope that records a start/stop event pair when profiling is on.
+struct PhaseScope {
+  Ctx &c;
+  PhaseEvent ev{};
+  bool on, open = false;
+  int pos;
+  PhaseScope(Ctx &ctx, int phase, int position) : c(ctx), on(ctx.profiling), pos(position) { start(phase); }
+  void start(int phase) {
+    if (!on) return;
+    ev.slot = phase * kMaxModes + (pos < kMaxModes ? pos : kMaxModes - 1);
+    cudaEventCreate(&ev.a);
+    cudaEventCreate(&ev.b);
+    cudaEventRecord(ev.a, c.stream);
+    open = true;
+  }
+  void stop() {
+    if (!on || !open) return;
+    cudaEventRecord(ev.b, c.stream);
+    c.events.push_back(ev);
+    open = false;
+  }
+  void next(int phase) {
+    stop();
+    start(phase);
+  }
+  ~PhaseScope() { stop(); }
+};
+
+// Count every library kernel launch (reported as gpu_launches by bench.py).
+#define RT_LAUNCH(ctx, kern, grid, block, smem, ...)                                   \
+  do {                                                                                 \
+    kern<<<(grid), (block), (smem), (ctx).stream>>>(__VA_ARGS__);                      \
+    (ctx).launches++;                                                                  \
+    RT_CUDA(cudaGetLastError());                                                       \
+  } while (0)
+
+// Stream-ordered device buffer (cudaMallocAsync on the context stream).
+template <typename T>
+struct DevBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(Ctx &c, size_t count) { alloc(c, count); }
+  void alloc(Ctx &c, size_t count) {
+    release();
+    s = c.stream;
+    n = count;
+    if (count) RT_CUDA(cudaMallocAsync((void **)&p, count * sizeof(T), s));
+  }
+  void zero() {
+    if (n) RT_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  T *release_ownership() {
+    T *q = p;
+    p = nullptr;
+    n = 0;
+    return q;
+  }
+  void release() {
+    if (p) cudaFreeAsync(p, s);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf &) = delete;
+  DevBuf &operator=(const DevBuf &) = delete;
+  DevBuf(DevBuf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf &operator=(DevBuf &&o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+};
+
+inline int64_t prod(const int64_t *d, int n) {
+  int64_t p = 1;
+  for (int i = 0; i < n; ++i) p *= d[i];
+  return p;
+}
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace rt

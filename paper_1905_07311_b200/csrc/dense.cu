@@ -1,0 +1,346 @@
+// Dense fixed-rank algorithms: R-STHOSVD (Alg 3) and R-HOSVD (Alg 2,
+// P:158-171), single GPU or sharded along the last mode, plus the
+// measurement helper rel_error.  No host synchronisation on the fixed-rank path.
+#include <cstring>
+
+#include "comm.h"
+#include "kernels_extra.h"
+#include "orchestrate.h"
+
+namespace rt {
+
+namespace {
+
+struct Policy {
+  bool mul_f64;  // fp64 products
+  DT store;      // precision of B and of the shrunk intermediates
+};
+
+Policy policy_for(DT in, uint32_t flags) {
+  const uint32_t acc = flags & RTUCKER_ACCUM_MASK;
+  const bool f64 = in == DT::F64 || acc == RTUCKER_ACCUM_FP64;
+  return Policy{f64, f64 ? DT::F64 : DT::F32};
+}
+
+void check_ranks(const DenseIn &in, const int64_t *ranks, int p) {
+  RT_REQUIRE(p >= 0, "p must be >= 0");
+  for (int k = 0; k < in.d; ++k)
+    RT_REQUIRE(ranks[k] >= 1 && ranks[k] <= in.gdims[k], "r_n must lie in [1, I_n]");
+}
+
+void fill_header(rtucker_result *r, const DenseIn &in, const int32_t *ord, uint64_t seed, uint32_t flags) {
+  for (int k = 0; k < in.d; ++k) {
+    r->dims[k] = in.gdims[k];
+    r->order[k] = ord[k];
+  }
+  r->seed = seed;
+  r->flags = flags;
+}
+
+// Sketch of the sharded last mode: local rows are complete; gather the row blocks of
+// all ranks into Y (I_glob x ell, column-major).  normsq gets the global ||G||^2.
+void sketch_last_sharded(Ctx &c, const DenseIn &in, const void *G, DT gt, const int64_t *cur, int ell,
+                         uint64_t seed, bool mulf64, double *Y, double *normsq) {
+  const int d = in.d, n = d - 1;
+  const ModeView v = mode_view(cur, d, n);  // v.I = local extent
+  const int64_t ext = v.I;
+  // exchange (offset, extent) of every rank
+  DevBuf<double> meta(c, 2), all(c, 2 * (size_t)c.nranks);
+  double hm[2] = {(double)in.offset, (double)ext};
+  RT_CUDA(cudaMemcpyAsync(meta.p, hm, sizeof hm, cudaMemcpyHostToDevice, c.stream));
+  allgather_f64(c, meta.p, all.p, 2);
+  std::vector<double> ha(2 * c.nranks);
+  RT_CUDA(cudaMemcpyAsync(ha.data(), all.p, sizeof(double) * 2 * c.nranks, cudaMemcpyDeviceToHost, c.stream));
+  RT_CUDA(cudaStreamSynchronize(c.stream));
+  int64_t maxext = 0;
+  std::vector<int64_t> offs(c.nranks), exts(c.nranks);
+  for (int r = 0; r < c.nranks; ++r) {
+    offs[r] = (int64_t)ha[2 * r];
+    exts[r] = (int64_t)ha[2 * r + 1];
+    maxext = std::max(maxext, exts[r]);
+  }
+  DevBuf<double> yl(c, (size_t)maxext * ell + 1);
+  yl.zero();
+  DevBuf<double> ytmp(c, (size_t)ext * ell);
+  sketch_dense(c, G, gt, v, n, ell, 0, seed, 0, mulf64, ytmp.p, yl.p + (size_t)maxext * ell);
+  RT_CUDA(cudaMemcpy2DAsync(yl.p, maxext * sizeof(double), ytmp.p, ext * sizeof(double), ext * sizeof(double),
+                            ell, cudaMemcpyDeviceToDevice, c.stream));
+  RT_CUDA(cudaMemcpyAsync(normsq, yl.p + (size_t)maxext * ell, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+  allreduce_sum_f64(c, normsq, 1);
+  DevBuf<double> g(c, (size_t)c.nranks * (maxext * ell + 1));
+  allgather_f64(c, yl.p, g.p, (size_t)maxext * ell + 1);
+  // drop the per-rank norm slot: blocks are (maxext*ell + 1) long
+  DevBuf<double> gp(c, (size_t)c.nranks * maxext * ell);
+  RT_CUDA(cudaMemcpy2DAsync(gp.p, maxext * ell * sizeof(double), g.p, (maxext * ell + 1) * sizeof(double),
+                            maxext * ell * sizeof(double), c.nranks, cudaMemcpyDeviceToDevice, c.stream));
+  DevBuf<int64_t> doffs(c, c.nranks), dexts(c, c.nranks);
+  RT_CUDA(cudaMemcpyAsync(doffs.p, offs.data(), sizeof(int64_t) * c.nranks, cudaMemcpyHostToDevice, c.stream));
+  RT_CUDA(cudaMemcpyAsync(dexts.p, exts.data(), sizeof(int64_t) * c.nranks, cudaMemcpyHostToDevice, c.stream));
+  rows_scatter(c, gp.p, c.nranks, maxext, ell, doffs.p, dexts.p, in.gdims[n], Y);
+  RT_CUDA(cudaStreamSynchronize(c.stream));  // host vectors above go out of scope
+}
+
+void copy_residuals(Ctx &c, rtucker_result *r, const double *scal, int d, int first_mode) {
+  for (int k = 0; k < d; ++k)
+    RT_CUDA(cudaMemcpyAsync(&r->mode_residual_sq[k], scal + 2 * k + 1, sizeof(double), cudaMemcpyDeviceToHost,
+                            c.stream));
+  RT_CUDA(cudaMemcpyAsync(&r->norm_sq, scal + 2 * first_mode, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+}
+
+}  // namespace
+
+rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ranks, int p, uint64_t seed,
+                            const int32_t *order, uint32_t flags) {
+  DenseIn in;
+  prepare_dense(c, X, in);
+  check_ranks(in, ranks, p);
+  int32_t ord[kMaxModes];
+  check_order(order, in.d, ord, in.gdims, in.sharded);
+  const Policy pol = policy_for(in.dt, flags);
+  const int d = in.d;
+  ResultGuard rg{c, new_result(d)};
+  rtucker_result *res = rg.r;
+  fill_header(res, in, ord, seed, flags);
+
+  int64_t cur[kMaxModes], gcur[kMaxModes];
+  memcpy(cur, in.ldims, sizeof cur);
+  memcpy(gcur, in.gdims, sizeof gcur);
+  const void *G = in.ptr;
+  DT gt = in.dt;
+  DevBuf<unsigned char> gown;
+  DevBuf<double> scal(c, 2 * (size_t)d);
+  scal.zero();
+
+  for (int jj = 0; jj < d; ++jj) {
+    const int n = ord[jj];
+    int ell, rr;
+    rank_caps(gcur, d, n, ranks[n], p, flags & RTUCKER_STRICT, ell, rr);
+    const ModeView v = mode_view(cur, d, n);
+    const bool last_sharded = in.sharded && n == d - 1;
+    const int64_t Ig = gcur[n];
+
+    // ---- line 2 of Alg 3 / line 1 of Alg 1: Y = G_(n) Omega_n   (+ ||G||^2)
+    DevBuf<double> Y(c, (size_t)Ig * ell + 1);
+    {
+      PhaseScope ps(c, PH_SKETCH, jj);
+      if (!last_sharded) {
+        sketch_dense(c, G, gt, v, n, ell, 0, seed, col_offset_for(in, cur, n), pol.mul_f64, Y.p, Y.p + Ig * ell);
+        allreduce_sum_f64(c, Y.p, (size_t)Ig * ell + 1);
+        RT_CUDA(cudaMemcpyAsync(scal.p + 2 * n, Y.p + Ig * ell, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+      } else {
+        sketch_last_sharded(c, in, G, gt, cur, ell, seed, pol.mul_f64, Y.p, scal.p + 2 * n);
+      }
+    }
+    // ---- Alg 1 line 2: thin QR
+    DevBuf<double> Q(c, (size_t)Ig * ell);
+    {
+      PhaseScope ps(c, PH_QR, jj);
+      householder_qr(c, Y.p, Ig, ell, Q.p);
+    }
+    Y.release();
+    // ---- Alg 1 line 3: B = Q^T G_(n)   (+ Gram B B^T)
+    DevBuf<unsigned char> B(c, (size_t)v.L * ell * v.R * dt_size(pol.store));
+    DevBuf<double> gram(c, (size_t)ell * ell);
+    PhaseScope ps_b(c, PH_BPASS, jj);
+    if (!last_sharded) {
+      ttm_dense(c, G, gt, v, Q.p, Ig, ell, B.p, pol.store, pol.mul_f64, gram.p);
+      allreduce_sum_f64(c, gram.p, (size_t)ell * ell);
+    } else {
+      ttm_dense(c, G, gt, v, Q.p + in.offset, Ig, ell, B.p, pol.store, pol.mul_f64, nullptr);
+      allreduce_sum(c, B.p, (size_t)v.L * ell, pol.store == DT::F64);
+      DevBuf<double> b64;
+      const double *bp = (const double *)B.p;
+      if (pol.store != DT::F64) {
+        b64.alloc(c, (size_t)v.L * ell);
+        convert(c, B.p, pol.store, b64.p, DT::F64, v.L * ell);
+        bp = b64.p;
+      }
+      gemm_small(c, true, bp, v.L, bp, v.L, gram.p, ell, ell, ell, v.L);
+    }
+    ps_b.next(PH_EIG);
+    // ---- Alg 1 line 4: thin SVD of B through the eigenpairs of its Gram
+    DevBuf<double> w(c, ell), V(c, (size_t)ell * ell);
+    sym_eig(c, gram.p, ell, w.p, V.p);
+    // ---- Alg 1 line 5: A_n = Q U_B(:, 1:r)
+    double *A = nullptr;
+    RT_CUDA(cudaMallocAsync((void **)&A, sizeof(double) * Ig * rr, c.stream));
+    res->factors[n] = A;
+    gemm_small(c, false, Q.p, Ig, V.p, ell, A, Ig, Ig, rr, ell);
+    canonical_signs(c, A, Ig, rr, V.p, ell, ell);  // reading R4b (shrink uses the signed U_B)
+    residual_from_eigs(c, w.p, rr, scal.p + 2 * n, scal.p + 2 * n + 1);
+    ps_b.next(PH_SHRINK);
+    // ---- Alg 3 line 6: G_(n) <- Sigma_hat V_hat^T = U_B(:, 1:r)^T B
+    const ModeView vb{v.L, ell, v.R};
+    DevBuf<unsigned char> Gn(c, (size_t)v.L * rr * v.R * dt_size(pol.store));
+    ttm_dense(c, B.p, pol.store, vb, V.p, ell, rr, Gn.p, pol.store, pol.mul_f64, nullptr);
+    gown = std::move(Gn);
+    G = gown.p;
+    gt = pol.store;
+    cur[n] = rr;
+    gcur[n] = rr;
+    if (last_sharded) cur[n] = rr;  // core is replicated from here on
+    res->ranks[n] = rr;
+    res->ell[n] = ell;
+  }
+  const int64_t ncore = prod(cur, d);
+  RT_CUDA(cudaMallocAsync(&res->core, sizeof(double) * ncore, c.stream));
+  convert(c, G, gt, res->core, DT::F64, ncore);
+  copy_residuals(c, res, scal.p, d, ord[0]);
+  finish_result(c, res, flags);
+  return rg.release();
+}
+
+rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ranks, int p, uint64_t seed,
+                          uint32_t flags) {
+  DenseIn in;
+  prepare_dense(c, X, in);
+  check_ranks(in, ranks, p);
+  const Policy pol = policy_for(in.dt, flags);
+  const int d = in.d;
+  int32_t ord[kMaxModes];
+  for (int k = 0; k < d; ++k) ord[k] = k;
+  ResultGuard rg{c, new_result(d)};
+  rtucker_result *res = rg.r;
+  fill_header(res, in, ord, seed, flags);
+  const bool want_core = !(flags & RTUCKER_NO_CORE);
+  DevBuf<double> scal(c, 2 * (size_t)d);
+  scal.zero();
+  // B_1 = Q_1^T X_(1) is kept so that the core chain starts from U_B1^T B_1 (unsharded).
+  const bool keep_b1 = want_core && !in.sharded && d > 1;
+  DevBuf<unsigned char> B1;
+  DevBuf<double> U1;
+  int ell1 = 0;
+
+  for (int n = 0; n < d; ++n) {
+    int ell, rr;
+    rank_caps(in.gdims, d, n, ranks[n], p, flags & RTUCKER_STRICT, ell, rr);
+    const ModeView v = mode_view(in.ldims, d, n);
+    const bool last_sharded = in.sharded && n == d - 1;
+    const int64_t Ig = in.gdims[n];
+    DevBuf<double> Y(c, (size_t)Ig * ell + 1);
+    PhaseScope ps(c, PH_SKETCH, n);
+    if (!last_sharded) {
+      sketch_dense(c, in.ptr, in.dt, v, n, ell, 0, seed, col_offset_for(in, in.ldims, n), pol.mul_f64, Y.p,
+                   Y.p + Ig * ell);
+      allreduce_sum_f64(c, Y.p, (size_t)Ig * ell + 1);
+      RT_CUDA(cudaMemcpyAsync(scal.p + 2 * n, Y.p + Ig * ell, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
+    } else {
+      sketch_last_sharded(c, in, in.ptr, in.dt, in.ldims, ell, seed, pol.mul_f64, Y.p, scal.p + 2 * n);
+    }
+    ps.next(PH_QR);
+    DevBuf<double> Q(c, (size_t)Ig * ell);
+    householder_qr(c, Y.p, Ig, ell, Q.p);
+    DevBuf<double> gram(c, (size_t)ell * ell);
+    ps.next(PH_BPASS);
+    if (!last_sharded) {
+      if (n == 0 && keep_b1) {
+        B1.alloc(c, (size_t)v.L * ell * v.R * dt_size(pol.store));
+        ttm_dense(c, in.ptr, in.dt, v, Q.p, Ig, ell, B1.p, pol.store, pol.mul_f64, gram.p);
+      } else {
+        ttm_dense(c, in.ptr, in.dt, v, Q.p, Ig, ell, nullptr, pol.store, pol.mul_f64, gram.p);  // Gram only
+      }
+      allreduce_sum_f64(c, gram.p, (size_t)ell * ell);
+    } else {
+      // B_d = Q_d^T X_(d) sums over the sharded index: partial B, then allreduce (fp64)
+      DevBuf<double> Bd(c, (size_t)v.L * ell);
+      ttm_dense(c, in.ptr, in.dt, v, Q.p + in.offset, Ig, ell, Bd.p, DT::F64, true, nullptr);
+      allreduce_sum_f64(c, Bd.p, (size_t)v.L * ell);
+      gemm_small(c, true, Bd.p, v.L, Bd.p, v.L, gram.p, ell, ell, ell, v.L);
+    }
+    ps.next(PH_EIG);
+    DevBuf<double> w(c, ell), V(c, (size_t)ell * ell);
+    sym_eig(c, gram.p, ell, w.p, V.p);
+    double *A = nullptr;
+    RT_CUDA(cudaMallocAsync((void **)&A, sizeof(double) * Ig * rr, c.stream));
+    res->factors[n] = A;
+    gemm_small(c, false, Q.p, Ig, V.p, ell, A, Ig, Ig, rr, ell);
+    canonical_signs(c, A, Ig, rr, V.p, ell, ell);  // reading R4b (shrink uses the signed U_B)
+    residual_from_eigs(c, w.p, rr, scal.p + 2 * n, scal.p + 2 * n + 1);
+    if (n == 0 && keep_b1) {
+      U1.alloc(c, (size_t)ell * rr);
+      RT_CUDA(cudaMemcpyAsync(U1.p, V.p, sizeof(double) * ell * rr, cudaMemcpyDeviceToDevice, c.stream));
+      ell1 = ell;
+    }
+    res->ranks[n] = rr;
+    res->ell[n] = ell;
+  }
+  if (want_core) {
+    PhaseScope ps(c, PH_SHRINK, 0);
+    // G = X x_1 A_1^T ... x_d A_d^T (Alg 2 line 5)
+    int64_t cur[kMaxModes];
+    memcpy(cur, in.ldims, sizeof cur);
+    DevBuf<unsigned char> g0, g1;
+    const void *G = in.ptr;
+    DT gt = in.dt;
+    int start = 0;
+    if (keep_b1) {  // G <- U_B1(:, 1:r1)^T B_1  (= A_1^T X_(1))
+      const ModeView vb{1, ell1, prod(cur + 1, d - 1)};
+      g0.alloc(c, (size_t)res->ranks[0] * vb.R * dt_size(pol.store));
+      ttm_dense(c, B1.p, pol.store, vb, U1.p, ell1, (int)res->ranks[0], g0.p, pol.store, pol.mul_f64, nullptr);
+      G = g0.p;
+      gt = pol.store;
+      cur[0] = res->ranks[0];
+      start = 1;
+    }
+    for (int n = start; n < d; ++n) {
+      const ModeView v = mode_view(cur, d, n);
+      const bool last_sharded = in.sharded && n == d - 1;
+      const int rr = (int)res->ranks[n];
+      DevBuf<unsigned char> &dst = (G == g0.p) ? g1 : g0;
+      dst.alloc(c, (size_t)v.L * rr * v.R * dt_size(last_sharded ? DT::F64 : pol.store));
+      if (!last_sharded) {
+        ttm_dense(c, G, gt, v, (const double *)res->factors[n], in.gdims[n], rr, dst.p, pol.store, pol.mul_f64,
+                  nullptr);
+        gt = pol.store;
+      } else {
+        ttm_dense(c, G, gt, v, (const double *)res->factors[n] + in.offset, in.gdims[n], rr, dst.p, DT::F64, true,
+                  nullptr);
+        allreduce_sum_f64(c, (double *)dst.p, (size_t)v.L * rr);
+        gt = DT::F64;
+      }
+      G = dst.p;
+      cur[n] = rr;
+    }
+    const int64_t ncore = prod(cur, d);
+    RT_CUDA(cudaMallocAsync(&res->core, sizeof(double) * ncore, c.stream));
+    convert(c, G, gt, res->core, DT::F64, ncore);
+  }
+  copy_residuals(c, res, scal.p, d, 0);
+  finish_result(c, res, flags);
+  return rg.release();
+}
+
+// ||X - [G; A_1..A_d]||_F / ||X||_F: expand the core mode by mode (fp64) and take
+// the squared difference with X on the device.  Unsharded inputs only.
+double run_rel_error(Ctx &c, const rtucker_dense_desc *X, const rtucker_result *res) {
+  DenseIn in;
+  prepare_dense(c, X, in);
+  RT_REQUIRE(!in.sharded, "rel_error: unsharded inputs only");
+  RT_REQUIRE(res->d == in.d, "rel_error: mode count mismatch");
+  RT_REQUIRE(res->memory == RTUCKER_DEVICE && res->core, "rel_error: needs a device-resident dense result");
+  const int d = in.d;
+  int64_t cur[kMaxModes];
+  for (int k = 0; k < d; ++k) cur[k] = res->ranks[k];
+  DevBuf<double> a, b;
+  const double *G = (const double *)res->core;
+  for (int n = 0; n < d; ++n) {
+    const ModeView v = mode_view(cur, d, n);
+    DevBuf<double> &dst = (G == a.p) ? b : a;
+    dst.alloc(c, (size_t)v.L * in.gdims[n] * v.R);
+    ttm_expand(c, G, DT::F64, v, (const double *)res->factors[n], in.gdims[n], in.gdims[n], dst.p);
+    G = dst.p;
+    cur[n] = in.gdims[n];
+  }
+  const int64_t N = prod(in.gdims, d);
+  DevBuf<double> s(c, 2);
+  diff_sumsq(c, in.ptr, in.dt, G, N, s.p);
+  sumsq(c, in.ptr, in.dt, N, s.p + 1);
+  double h[2];
+  RT_CUDA(cudaMemcpyAsync(h, s.p, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+  RT_CUDA(cudaStreamSynchronize(c.stream));
+  RT_REQUIRE(h[1] > 0.0, "rel_error: ||X|| = 0");
+  if (!std::isfinite(h[0]) || !std::isfinite(h[1])) throw Error(RTUCKER_ENUMERIC, "rel_error: non-finite norm");
+  return std::sqrt(h[0] / h[1]);
+}
+
+}  // namespace rt

@@ -1,0 +1,80 @@
+// Host-side launchers of the librtucker kernels (one translation unit per family).
+#pragma once
+#include "common.cuh"
+
+namespace rt {
+
+enum class DT { F32 = 0, F64 = 1 };
+inline size_t dt_size(DT t) { return t == DT::F32 ? 4 : 8; }
+
+// (L, I, R) view of mode n of a first-mode-fastest tensor: element (l, i, r) at
+// l + L*(i + I*r); unfolding column c = l + L*r.
+struct ModeView {
+  int64_t L, I, R;
+};
+inline ModeView mode_view(const int64_t *dims, int d, int n) {
+  ModeView v{1, dims[n], 1};
+  for (int k = 0; k < n; ++k) v.L *= dims[k];
+  for (int k = n + 1; k < d; ++k) v.R *= dims[k];
+  return v;
+}
+
+// ---- sketch.cu ---------------------------------------------------------------------
+// Y (I x ell, fp64 col-major) = X_(n) Omega_n(:, k0:k0+ell) with Omega rows indexed by
+// c + col_offset (global column).  normsq (optional, device scalar) <- ||X||_F^2.
+// mul_f64: multiply in fp64 (else fp32 products with fp64 accumulation every 32 terms).
+void sketch_dense(Ctx &c, const void *X, DT in, ModeView v, int mode, int ell, int64_t k0,
+                  uint64_t seed, int64_t col_offset, bool mul_f64, double *Y, double *normsq);
+
+// Generates Omega rows for given columns (debug / parity).
+void omega_rows(Ctx &c, DT out, uint64_t seed, int mode, const int64_t *cols, int64_t n,
+                int ell, int64_t k0, void *dst);
+void philox_raw(Ctx &c, const uint32_t *ctr, int64_t n, uint32_t k0, uint32_t k1, uint32_t *out);
+
+// ---- ttm.cu ------------------------------------------------------------------------
+// out = X x_n A^T with A (I x J, fp64 col-major, leading dim lda): out(l, j, r) = sum_i A[i,j] X(l,i,r).
+// out may be null (Gram-only pass).  gram (optional, J x J fp64) <- B_(n) B_(n)^T of the
+// (stored-precision) output.
+void ttm_dense(Ctx &c, const void *X, DT in, ModeView v, const double *A, int64_t lda, int J,
+               void *out, DT outT, bool mul_f64, double *gram);
+
+// Gram of the mode-n unfolding of B (mode size v.I): gram (v.I x v.I, fp64).
+void mode_gram(Ctx &c, const void *B, DT t, ModeView v, double *gram);
+
+// ---- linalg.cu ---------------------------------------------------------------------
+void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q);
+// w descending; sweeps (optional, device int) <- Jacobi sweeps used
+void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps = nullptr);
+// Sign convention of reading R4b: for each column k < r of A (m x r) make the entry of
+// largest magnitude positive (first on ties); the same sign is applied to column k of U
+// (ell x r, leading dim ldu) so that the shrink U^T B stays consistent.
+void canonical_signs(Ctx &c, double *A, int64_t m, int r, double *U, int64_t ldu, int ell);
+// C (m x n) = op(A) (m x k) * B (k x n), fp64 col-major with leading dims.
+void gemm_small(Ctx &c, bool transA, const double *A, int64_t lda, const double *B, int64_t ldb,
+                double *C, int64_t ldc, int64_t m, int64_t n, int64_t k);
+void convert(Ctx &c, const void *src, DT s, void *dst, DT d, int64_t n);
+void sumsq(Ctx &c, const void *X, DT t, int64_t n, double *out);             // deterministic
+void diff_sumsq(Ctx &c, const void *X, DT t, const double *Y, int64_t n, double *out);
+void sum_vec(Ctx &c, const double *x, int64_t n, double *out);             // out = sum x
+void sub_scalar(Ctx &c, const double *a, const double *b, double *out);   // out = a - b
+
+// ---- sparse.cu ---------------------------------------------------------------------
+struct CooDev {
+  int d;
+  int64_t dims[kMaxModes];
+  int64_t nnz;
+  const int32_t *idx[kMaxModes];
+  const void *vals;
+  DT vt;
+};
+// Y (I_n x ell, fp64) = G_(n) Omega_n for a COO tensor.
+void sketch_coo(Ctx &c, const CooDev &g, int mode, int ell, uint64_t seed, double *Y);
+// Strong-RRQR (CPQR + maxvol, eta) on Q (m x l): sel sorted (device int64), A (m x l).
+void srrqr(Ctx &c, const double *Q, int64_t m, int l, double eta, int64_t *sel, double *A,
+           int *swaps_host);
+// Keep entries whose mode-n index is in sel (sorted, length l) and renumber it.
+// Returns new nnz (host sync).
+int64_t coo_select(Ctx &c, const CooDev &in, int mode, const int64_t *sel, int l,
+                   int32_t *const *out_idx, void *out_vals);
+
+}  // namespace rt

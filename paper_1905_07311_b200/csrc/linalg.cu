@@ -1,0 +1,119 @@
+// Small dense linear algebra on the device, fp64 (latency-bound steps of the path):
+//   (householder_qr and sym_eig live in smallla.cu)
+//   gemm_small      A_n = Q U_B(:, 1:r) (Alg 1 line 5) and friends
+//   reductions      deterministic two-stage sums (norms, residuals)
+#include "kernels.h"
+
+namespace rt {
+
+namespace {
+
+
+__device__ __forceinline__ double warp_sum(double v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// C = op(A) B, one thread per output element (small sizes only).
+__global__ void gemm_small_kernel(bool transA, const double *__restrict__ A, int64_t lda,
+                                  const double *__restrict__ B, int64_t ldb, double *__restrict__ C,
+                                  int64_t ldc, int64_t m, int64_t n, int64_t k) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % m, j = e / m;
+    double s = 0.0;
+    if (transA)
+      for (int64_t t = 0; t < k; ++t) s += A[t + lda * i] * B[t + ldb * j];
+    else
+      for (int64_t t = 0; t < k; ++t) s += A[i + lda * t] * B[t + ldb * j];
+    C[i + ldc * j] = s;
+  }
+}
+
+template <typename S, typename D>
+__global__ void convert_kernel(const S *__restrict__ s, D *__restrict__ d, int64_t n) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    d[e] = (D)s[e];
+}
+
+constexpr int kRedBlocks = 1024;
+
+template <typename T>
+__global__ void sumsq_stage1(const T *__restrict__ x, const double *__restrict__ y, int64_t n,
+                             double *__restrict__ part) {
+  __shared__ double sred[8];
+  double s = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const double v = (double)x[e] - (y ? y[e] : 0.0);
+    s += v * v;
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sred[k];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void sum_vec_kernel(const double *__restrict__ x, int64_t n, double *__restrict__ out) {
+  __shared__ double sred[32];
+  double s = 0.0;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) s += x[e];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sred[k];
+    *out = t;
+  }
+}
+
+__global__ void sub_scalar_kernel(const double *a, const double *b, double *out) { *out = *a - *b; }
+
+}  // namespace
+
+void gemm_small(Ctx &c, bool transA, const double *A, int64_t lda, const double *B, int64_t ldb,
+                double *C, int64_t ldc, int64_t m, int64_t n, int64_t k) {
+  const int g = std::max(1, std::min(2048, ceil_div(m * n, 256)));
+  RT_LAUNCH(c, gemm_small_kernel, g, 256, 0, transA, A, lda, B, ldb, C, ldc, m, n, k);
+}
+
+void convert(Ctx &c, const void *src, DT s, void *dst, DT d, int64_t n) {
+  const int g = std::max(1, std::min(4096, ceil_div(n, 256)));
+  if (s == DT::F32 && d == DT::F64)
+    RT_LAUNCH(c, (convert_kernel<float, double>), g, 256, 0, (const float *)src, (double *)dst, n);
+  else if (s == DT::F64 && d == DT::F32)
+    RT_LAUNCH(c, (convert_kernel<double, float>), g, 256, 0, (const double *)src, (float *)dst, n);
+  else
+    RT_CUDA(cudaMemcpyAsync(dst, src, n * dt_size(s), cudaMemcpyDeviceToDevice, c.stream));
+}
+
+static void sumsq_impl(Ctx &c, const void *X, DT t, const double *Y, int64_t n, double *out) {
+  DevBuf<double> part(c, kRedBlocks);
+  if (t == DT::F32)
+    RT_LAUNCH(c, sumsq_stage1<float>, kRedBlocks, 256, 0, (const float *)X, Y, n, part.p);
+  else
+    RT_LAUNCH(c, sumsq_stage1<double>, kRedBlocks, 256, 0, (const double *)X, Y, n, part.p);
+  sum_vec(c, part.p, kRedBlocks, out);
+}
+
+void sumsq(Ctx &c, const void *X, DT t, int64_t n, double *out) { sumsq_impl(c, X, t, nullptr, n, out); }
+
+void diff_sumsq(Ctx &c, const void *X, DT t, const double *Y, int64_t n, double *out) {
+  sumsq_impl(c, X, t, Y, n, out);
+}
+
+void sum_vec(Ctx &c, const double *x, int64_t n, double *out) {
+  RT_LAUNCH(c, sum_vec_kernel, 1, 1024, 0, x, n, out);
+}
+
+void sub_scalar(Ctx &c, const double *a, const double *b, double *out) {
+  RT_LAUNCH(c, sub_scalar_kernel, 1, 1, 0, a, b, out);
+}
+
+}  // namespace rt

@@ -1,0 +1,73 @@
+// Auxiliary device kernels for the orchestrator (layout moves and expansion products).
+#include "kernels_extra.h"
+
+namespace rt {
+
+namespace {
+
+// out(l, j, r) = sum_{i<I} M[j + ldm*i] * X(l, i, r), M is J x I column-major (fp64).
+// Used to expand a Tucker core (measurement helper rtucker_rel_error) where J is large
+// and I (a rank) is small.
+template <typename Tin>
+__global__ void ttm_expand_kernel(const Tin *__restrict__ X, int64_t L, int64_t I, int64_t R,
+                                  const double *__restrict__ M, int64_t ldm, int64_t J,
+                                  double *__restrict__ out) {
+  const int64_t n = L * J * R;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = e % L;
+    const int64_t t = e / L;
+    const int64_t j = t % J, r = t / J;
+    double s = 0.0;
+    for (int64_t i = 0; i < I; ++i) s += M[j + ldm * i] * (double)X[l + L * (i + I * r)];
+    out[e] = s;
+  }
+}
+
+// Allgathered row blocks [rank][ext][ell] (each block column-major ext x ell) ->
+// column-major (I x ell) with rank blocks at row offsets off[rank].
+__global__ void rows_scatter_kernel(const double *__restrict__ g, int nranks, int64_t ext,
+                                    int ell, const int64_t *__restrict__ offs,
+                                    const int64_t *__restrict__ exts, int64_t I,
+                                    double *__restrict__ Y) {
+  const int64_t n = (int64_t)nranks * ext * ell;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t rk = e / (ext * ell);
+    const int64_t t = e % (ext * ell);
+    const int64_t i = t % ext, k = t / ext;
+    if (i < exts[rk]) Y[offs[rk] + i + I * k] = g[e];
+  }
+}
+
+__global__ void sum_first_kernel(const double *__restrict__ w, int r, const double *__restrict__ nsq,
+                                 double *__restrict__ out) {
+  double s = 0.0;
+  for (int i = 0; i < r; ++i) s += w[i];
+  *out = *nsq - s;
+}
+
+}  // namespace
+
+void ttm_expand(Ctx &c, const void *X, DT in, ModeView v, const double *M, int64_t ldm, int64_t J,
+                double *out) {
+  const int64_t n = v.L * J * v.R;
+  const int g = std::max(1, std::min(8192, ceil_div(n, 256)));
+  if (in == DT::F64)
+    RT_LAUNCH(c, ttm_expand_kernel<double>, g, 256, 0, (const double *)X, v.L, v.I, v.R, M, ldm, J, out);
+  else
+    RT_LAUNCH(c, ttm_expand_kernel<float>, g, 256, 0, (const float *)X, v.L, v.I, v.R, M, ldm, J, out);
+}
+
+void rows_scatter(Ctx &c, const double *g, int nranks, int64_t ext, int ell, const int64_t *offs,
+                  const int64_t *exts, int64_t I, double *Y) {
+  const int64_t n = (int64_t)nranks * ext * ell;
+  const int gr = std::max(1, std::min(4096, ceil_div(n, 256)));
+  RT_LAUNCH(c, rows_scatter_kernel, gr, 256, 0, g, nranks, ext, ell, offs, exts, I, Y);
+}
+
+void residual_from_eigs(Ctx &c, const double *w, int r, const double *normsq, double *out) {
+  RT_LAUNCH(c, sum_first_kernel, 1, 1, 0, w, r, normsq, out);
+}
+
+}  // namespace rt

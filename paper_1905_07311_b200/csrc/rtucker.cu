@@ -1,0 +1,366 @@
+// librtucker: C ABI (include/rtucker.h) and the host orchestrator of the randomized
+// Tucker algorithms.  Every arithmetic step runs in the kernels of sketch.cu, ttm.cu,
+// linalg.cu, sparse.cu; this file only sequences them, validates arguments, manages
+// workspace (stream-ordered allocations) and the collectives of the sharded path.
+#include <cmath>
+#include <cstring>
+#include <algorithm>
+#include <numeric>
+#include <functional>
+
+#include "comm.h"
+#include "kernels_extra.h"
+#include "orchestrate.h"
+
+using namespace rt;
+
+struct rtucker_ctx {
+  Ctx c;
+};
+
+namespace rt {
+
+// ---------------------------------------------------------------- argument checks --
+static DT to_dt(rtucker_dtype t) {
+  if (t == RTUCKER_F32) return DT::F32;
+  if (t == RTUCKER_F64) return DT::F64;
+  throw Error(RTUCKER_EINVAL, "dtype must be RTUCKER_F32 or RTUCKER_F64");
+}
+
+void prepare_dense(Ctx &c, const rtucker_dense_desc *X, DenseIn &in) {
+  RT_REQUIRE(X != nullptr, "null tensor descriptor");
+  if (X->d > kMaxModes) throw Error(RTUCKER_EUNSUPPORTED, "d > RTUCKER_MAX_MODES");
+  RT_REQUIRE(X->d >= 1, "d must be >= 1");
+  RT_REQUIRE(X->data != nullptr, "null tensor data");
+  in.dt = to_dt(X->dtype);
+  in.d = X->d;
+  for (int k = 0; k < in.d; ++k) {
+    RT_REQUIRE(X->dims[k] >= 1, "every dim must be >= 1");
+    in.gdims[k] = X->dims[k];
+    in.ldims[k] = X->dims[k];
+  }
+  in.sharded = X->shard_extent > 0 && (X->shard_extent != X->dims[in.d - 1] || c.nranks > 1);
+  in.offset = 0;
+  if (X->shard_extent > 0) {
+    RT_REQUIRE(X->shard_offset >= 0 && X->shard_offset + X->shard_extent <= X->dims[in.d - 1],
+               "shard range outside the last mode");
+    in.ldims[in.d - 1] = X->shard_extent;
+    in.offset = X->shard_offset;
+  }
+  RT_REQUIRE(!in.sharded || c.nranks > 1, "a partial shard needs a multi-rank context");
+  const int64_t n = prod(in.ldims, in.d);
+  if (X->memory == RTUCKER_HOST) {
+    in.owned.alloc(c, n * dt_size(in.dt));
+    RT_CUDA(cudaMemcpyAsync(in.owned.p, X->data, n * dt_size(in.dt), cudaMemcpyHostToDevice, c.stream));
+    in.ptr = in.owned.p;
+  } else {
+    in.ptr = X->data;
+  }
+}
+
+void check_order(const int32_t *order, int d, int32_t *out, const int64_t *dims, bool sharded) {
+  if (order) {
+    bool seen[kMaxModes] = {false};
+    for (int k = 0; k < d; ++k) {
+      RT_REQUIRE(order[k] >= 0 && order[k] < d && !seen[order[k]], "order is not a permutation");
+      seen[order[k]] = true;
+      out[k] = order[k];
+    }
+  } else {
+    // process the largest modes first, ties by ascending index
+    std::iota(out, out + d, 0);
+    std::stable_sort(out, out + d, [&](int a, int b) { return dims[a] > dims[b]; });
+    if (sharded) {  // sharded dense runs process the sharded last mode last
+      std::stable_partition(out, out + d, [&](int a) { return a != d - 1; });
+    }
+  }
+  RT_REQUIRE(!sharded || out[d - 1] == d - 1, "a sharded tensor must be processed with its last mode last");
+}
+
+// l_n = min(r_n + p, I_n, prod others) on the current dims (reading R5).
+void rank_caps(const int64_t *dims, int d, int n, int64_t r, int p, bool strict, int &ell, int &rr) {
+  int64_t others = 1;
+  for (int k = 0; k < d; ++k)
+    if (k != n) others *= dims[k];
+  const int64_t cap = std::min<int64_t>(dims[n], others);
+  int64_t e = r + p;
+  if (e > cap) {
+    RT_REQUIRE(!strict, "r_n + p exceeds min(I_n, prod_{k!=n} I_k) (RTUCKER_STRICT)");
+    e = cap;
+  }
+  ell = (int)e;
+  rr = (int)std::min<int64_t>(r, e);
+}
+
+// --------------------------------------------------------------------- result ------
+rtucker_result *new_result(int d) {
+  rtucker_result *r = nullptr;
+  if (cudaMallocHost((void **)&r, sizeof(rtucker_result)) != cudaSuccess)
+    throw Error(RTUCKER_ENOMEM, "cudaMallocHost(result)");
+  memset(r, 0, sizeof *r);
+  r->d = d;
+  r->dtype = RTUCKER_F64;
+  r->memory = RTUCKER_DEVICE;
+  return r;
+}
+
+void free_result(Ctx &c, rtucker_result *r) {
+  if (!r) return;
+  auto fr = [&](void *p) {
+    if (!p) return;
+    if (r->memory == RTUCKER_HOST) cudaFreeHost(p);
+    else cudaFreeAsync(p, c.stream);
+  };
+  fr(r->core);
+  for (int k = 0; k < kMaxModes; ++k) {
+    fr(r->factors[k]);
+    fr(r->core_idx[k]);
+    fr(r->selection[k]);
+  }
+  fr(r->core_vals);
+  cudaFreeHost(r);
+}
+
+// Moves device result buffers to pinned host memory when RTUCKER_RESULT_HOST is set.
+void finish_result(Ctx &c, rtucker_result *r, uint32_t flags) {
+  if (!(flags & RTUCKER_RESULT_HOST)) return;
+  auto mv = [&](void *&p, size_t bytes) {
+    if (!p) return;
+    void *h = nullptr;
+    RT_CUDA(cudaMallocHost(&h, std::max<size_t>(bytes, 1)));
+    RT_CUDA(cudaMemcpyAsync(h, p, bytes, cudaMemcpyDeviceToHost, c.stream));
+    RT_CUDA(cudaFreeAsync(p, c.stream));
+    p = h;
+  };
+  const size_t vs = r->dtype == RTUCKER_F64 ? 8 : 4;
+  int64_t core_n = 1;
+  for (int k = 0; k < r->d; ++k) core_n *= r->ranks[k];
+  if (r->core) mv(r->core, core_n * vs);
+  for (int k = 0; k < r->d; ++k) {
+    if (r->factors[k]) mv(r->factors[k], (size_t)r->dims[k] * r->ranks[k] * 8);
+    if (r->core_idx[k]) mv(*(void **)&r->core_idx[k], r->core_nnz * 4);
+    if (r->selection[k]) mv(*(void **)&r->selection[k], r->ranks[k] * 8);
+  }
+  if (r->core_vals) mv(r->core_vals, r->core_nnz * vs);
+  r->memory = RTUCKER_HOST;
+  RT_CUDA(cudaStreamSynchronize(c.stream));
+}
+
+}  // namespace rt
+
+// ======================================================================= C ABI ======
+static rtucker_status guard(rtucker_ctx *ctx, const std::function<void()> &fn) {
+  try {
+    fn();
+    if (ctx) ctx->c.last_error.clear();
+    return RTUCKER_OK;
+  } catch (const Error &e) {
+    if (ctx) ctx->c.last_error = e.what();
+    return e.code;
+  } catch (const std::exception &e) {
+    if (ctx) ctx->c.last_error = e.what();
+    return RTUCKER_ECUDA;
+  }
+}
+
+extern "C" {
+
+const char *rtucker_version(void) { return "rtucker 0.1 (sm_100a)"; }
+
+rtucker_status rtucker_memcpy(rtucker_ctx *ctx, void *dst, const void *src, size_t bytes, int kind) {
+  if (!ctx || (!dst && bytes) || (!src && bytes) || kind < 0 || kind > 4) return RTUCKER_EINVAL;
+  return guard(ctx, [&] {
+    if (bytes) RT_CUDA(cudaMemcpyAsync(dst, src, bytes, (cudaMemcpyKind)kind, ctx->c.stream));
+  });
+}
+
+rtucker_status rtucker_sync(rtucker_ctx *ctx) {
+  if (!ctx) return RTUCKER_EINVAL;
+  return guard(ctx, [&] { RT_CUDA(cudaStreamSynchronize(ctx->c.stream)); });
+}
+
+rtucker_status rtucker_set_profiling(rtucker_ctx *ctx, int enabled) {
+  if (!ctx) return RTUCKER_EINVAL;
+  ctx->c.profiling = enabled != 0;
+  return RTUCKER_OK;
+}
+
+rtucker_status rtucker_phase_times(rtucker_ctx *ctx, double *ms, int64_t *counts, int reset) {
+  if (!ctx) return RTUCKER_EINVAL;
+  return guard(ctx, [&] {
+    Ctx &c = ctx->c;
+    RT_CUDA(cudaStreamSynchronize(c.stream));
+    for (auto &e : c.events) {
+      float t = 0.f;
+      RT_CUDA(cudaEventElapsedTime(&t, e.a, e.b));
+      c.phase_ms[e.slot] += t;
+      c.phase_n[e.slot] += 1;
+      cudaEventDestroy(e.a);
+      cudaEventDestroy(e.b);
+    }
+    c.events.clear();
+    if (ms) memcpy(ms, c.phase_ms, sizeof c.phase_ms);
+    if (counts) memcpy(counts, c.phase_n, sizeof c.phase_n);
+    if (reset) {
+      memset(c.phase_ms, 0, sizeof c.phase_ms);
+      memset(c.phase_n, 0, sizeof c.phase_n);
+    }
+  });
+}
+
+rtucker_status rtucker_ctx_create(int device, void *cuda_stream, const void *nccl_unique_id, int rank,
+                                  int nranks, rtucker_ctx **out) {
+  if (!out) return RTUCKER_EINVAL;
+  *out = nullptr;
+  if (nranks < 1 || rank < 0 || rank >= nranks) return RTUCKER_EINVAL;
+  if (nranks > 1 && !nccl_unique_id) return RTUCKER_EINVAL;
+  rtucker_ctx *ctx = new rtucker_ctx;
+  rtucker_status st = guard(ctx, [&] {
+    RT_CUDA(cudaSetDevice(device));
+    ctx->c.device = device;
+    if (cuda_stream) {
+      ctx->c.stream = (cudaStream_t)cuda_stream;
+    } else {
+      RT_CUDA(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+      ctx->c.own_stream = true;
+    }
+    RT_CUDA(cudaDeviceGetAttribute(&ctx->c.num_sms, cudaDevAttrMultiProcessorCount, device));
+    ctx->c.rank = rank;
+    ctx->c.nranks = nranks;
+    if (nranks > 1) ctx->c.comm = comm_create(nccl_unique_id, rank, nranks);
+  });
+  if (st != RTUCKER_OK) {
+    delete ctx;
+    return st;
+  }
+  *out = ctx;
+  return RTUCKER_OK;
+}
+
+void rtucker_ctx_destroy(rtucker_ctx *ctx) {
+  if (!ctx) return;
+  cudaStreamSynchronize(ctx->c.stream);
+  comm_destroy(ctx->c.comm);
+  if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+  delete ctx;
+}
+
+rtucker_status rtucker_ctx_set_stream(rtucker_ctx *ctx, void *cuda_stream) {
+  if (!ctx || !cuda_stream) return RTUCKER_EINVAL;
+  if (ctx->c.own_stream) {
+    cudaStreamSynchronize(ctx->c.stream);
+    cudaStreamDestroy(ctx->c.stream);
+    ctx->c.own_stream = false;
+  }
+  ctx->c.stream = (cudaStream_t)cuda_stream;
+  return RTUCKER_OK;
+}
+
+const char *rtucker_last_error(const rtucker_ctx *ctx) {
+  return ctx ? ctx->c.last_error.c_str() : "null context";
+}
+
+uint64_t rtucker_launch_count(const rtucker_ctx *ctx) { return ctx ? ctx->c.launches : 0; }
+
+rtucker_status rtucker_nccl_unique_id(void *out128) {
+  if (!out128) return RTUCKER_EINVAL;
+  return guard(nullptr, [&] { nccl_unique_id(out128); });
+}
+
+rtucker_status rtucker_hosvd(rtucker_ctx *ctx, const rtucker_dense_desc *X, const int64_t *ranks,
+                             int32_t p, uint64_t seed, uint32_t flags, rtucker_result **out) {
+  if (!ctx || !out || !ranks) return RTUCKER_EINVAL;
+  *out = nullptr;
+  return guard(ctx, [&] { *out = run_hosvd(ctx->c, X, ranks, p, seed, flags); });
+}
+
+rtucker_status rtucker_sthosvd(rtucker_ctx *ctx, const rtucker_dense_desc *X, const int64_t *ranks,
+                               int32_t p, uint64_t seed, const int32_t *order, uint32_t flags,
+                               rtucker_result **out) {
+  if (!ctx || !out || !ranks) return RTUCKER_EINVAL;
+  *out = nullptr;
+  return guard(ctx, [&] { *out = run_sthosvd(ctx->c, X, ranks, p, seed, order, flags); });
+}
+
+rtucker_status rtucker_adaptive(rtucker_ctx *ctx, const rtucker_dense_desc *X, double tol, int32_t block,
+                                const double *mode_tol, const int32_t *order, uint64_t seed,
+                                uint32_t flags, rtucker_result **out) {
+  if (!ctx || !out) return RTUCKER_EINVAL;
+  *out = nullptr;
+  return guard(ctx, [&] { *out = run_adaptive(ctx->c, X, tol, block, mode_tol, order, seed, flags); });
+}
+
+rtucker_status rtucker_sparse_sthosvd(rtucker_ctx *ctx, const rtucker_coo_desc *X, const int64_t *ranks,
+                                      int32_t p, uint64_t seed, const int32_t *order, double eta,
+                                      uint32_t flags, rtucker_result **out) {
+  if (!ctx || !out || !ranks) return RTUCKER_EINVAL;
+  *out = nullptr;
+  return guard(ctx, [&] { *out = run_sparse_sthosvd(ctx->c, X, ranks, p, seed, order, eta, flags); });
+}
+
+void rtucker_result_free(rtucker_ctx *ctx, rtucker_result *res) {
+  if (!ctx || !res) return;
+  free_result(ctx->c, res);
+}
+
+rtucker_status rtucker_rel_error(rtucker_ctx *ctx, const rtucker_dense_desc *X, const rtucker_result *res,
+                                 double *out) {
+  if (!ctx || !res || !out) return RTUCKER_EINVAL;
+  return guard(ctx, [&] { *out = run_rel_error(ctx->c, X, res); });
+}
+
+rtucker_status rtucker_debug_sketch(rtucker_ctx *ctx, const rtucker_dense_desc *X, int32_t mode, int32_t ell,
+                                    int64_t k0, uint64_t seed, uint32_t flags, double *Y_out) {
+  if (!ctx || !Y_out) return RTUCKER_EINVAL;
+  return guard(ctx, [&] {
+    DenseIn in;
+    prepare_dense(ctx->c, X, in);
+    RT_REQUIRE(mode >= 0 && mode < in.d, "mode out of range");
+    RT_REQUIRE(ell >= 1 && k0 >= 0, "ell >= 1 and k0 >= 0 required");
+    const bool f64 = in.dt == DT::F64 || (flags & RTUCKER_ACCUM_MASK) == RTUCKER_ACCUM_FP64;
+    sketch_dense(ctx->c, in.ptr, in.dt, mode_view(in.ldims, in.d, mode), mode, ell, k0, seed,
+                 col_offset_for(in, in.ldims, mode), f64, Y_out, nullptr);
+  });
+}
+
+rtucker_status rtucker_debug_omega(rtucker_ctx *ctx, rtucker_dtype dtype, uint64_t seed, int32_t mode,
+                                   const int64_t *cols, int64_t n, int32_t ell, int64_t k0, void *out) {
+  if (!ctx || !cols || !out || n < 0 || ell < 1 || k0 < 0) return RTUCKER_EINVAL;
+  return guard(ctx, [&] { omega_rows(ctx->c, to_dt(dtype), seed, mode, cols, n, ell, k0, out); });
+}
+
+rtucker_status rtucker_debug_philox(rtucker_ctx *ctx, const uint32_t *ctr, int64_t n, uint32_t key0,
+                                    uint32_t key1, uint32_t *out) {
+  if (!ctx || !ctr || !out || n < 0) return RTUCKER_EINVAL;
+  return guard(ctx, [&] { philox_raw(ctx->c, ctr, n, key0, key1, out); });
+}
+
+rtucker_status rtucker_debug_qr(rtucker_ctx *ctx, int64_t m, int32_t n, const double *Y, double *Q) {
+  if (!ctx || !Y || !Q || n < 1 || m < n) return RTUCKER_EINVAL;
+  return guard(ctx, [&] { householder_qr(ctx->c, Y, m, n, Q); });
+}
+
+rtucker_status rtucker_debug_eig(rtucker_ctx *ctx, int32_t n, const double *A, double *w, double *V,
+                                 int32_t *sweeps_out) {
+  if (!ctx || !A || !w || !V || n < 1) return RTUCKER_EINVAL;
+  return guard(ctx, [&] {
+    DevBuf<int> sw(ctx->c, 1);
+    sym_eig(ctx->c, A, n, w, V, sw.p);
+    int h = 0;
+    RT_CUDA(cudaMemcpyAsync(&h, sw.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->c.stream));
+    RT_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    if (sweeps_out) *sweeps_out = h;
+  });
+}
+
+rtucker_status rtucker_debug_srrqr(rtucker_ctx *ctx, int64_t m, int32_t l, const double *Q, double eta,
+                                   int64_t *sel, double *A, int32_t *swaps_out) {
+  if (!ctx || !Q || !sel || !A || l < 1 || m < l || !(eta >= 1.0)) return RTUCKER_EINVAL;
+  return guard(ctx, [&] {
+    int sw = 0;
+    srrqr(ctx->c, Q, m, l, eta, sel, A, &sw);
+    if (swaps_out) *swaps_out = sw;
+  });
+}
+
+}  // extern "C"

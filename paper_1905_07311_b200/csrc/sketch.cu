@@ -1,0 +1,242 @@
+// Dense mode-n sketch Y = X_(n) Omega_n (Alg 1 line 1; Alg 2 line 2, Alg 3 line 2)
+// without materialising the unfolding, Omega generated on the fly.
+//
+// SIMT kernel (the tensor-core 3xTF32 variant lives in sketch_tc.cu).  Each CTA owns a
+// tile of TI rows i and a contiguous range of unfolding columns c = l + L*r; it streams
+// CK columns at a time: X tile -> smem (coalesced along the contiguous index of the
+// (L, I, R) view), Omega chunk generated into smem, register-blocked 4x4 FMAs.  Per-CTA
+// partial Y tiles are summed in a fixed order by reduce_splits (deterministic).
+// The squared Frobenius norm of X is fused in (each element is read exactly once).
+#include "kernels.h"
+#include "philox.cuh"
+
+namespace rt {
+
+namespace {
+
+constexpr int kThreads = 256;
+template <int LP> constexpr int chunk_cols() { return LP >= 32 ? 32 : 16; }  // columns per chunk
+
+template <typename Tin, typename Tmul, int LP>
+__global__ void __launch_bounds__(kThreads) sketch_simt_kernel(
+    const Tin *__restrict__ X, int64_t L, int64_t I, int64_t R, int64_t cols_per_split,
+    uint64_t seed, int mode, int ell, int64_t k0, int64_t col_offset,
+    double *__restrict__ partial, double *__restrict__ norm_partial) {
+  constexpr int TI = 4096 / LP;   // rows per tile
+  constexpr int NK = LP / 4;      // k-groups
+  constexpr int kCK = chunk_cols<LP>();
+  __shared__ __align__(16) Tmul sX[kCK][TI];
+  __shared__ __align__(16) Tmul sO[kCK][LP];
+  __shared__ double sred[kThreads / 32];
+
+  const int tid = threadIdx.x;
+  const int tk = tid % NK, ti = tid / NK;
+  const int64_t i0 = (int64_t)blockIdx.x * TI;
+  const int64_t C = L * R;
+  const int64_t cbeg = (int64_t)blockIdx.y * cols_per_split;
+  const int64_t cend = min(C, cbeg + cols_per_split);
+
+  // Philox blocks that cover global sketch columns [k0, k0 + ell).
+  const int64_t jb0 = k0 >> 2;
+  const int nb = (int)(((k0 + ell - 1) >> 2) - jb0 + 1);
+
+  // zero the padding columns of the Omega tile once
+  for (int e = tid; e < kCK * LP; e += kThreads) sO[e / LP][e % LP] = Tmul(0);
+
+  double accd[4][4];
+  Tmul acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) { accd[a][b] = 0.0; acc[a][b] = Tmul(0); }
+  double nsq = 0.0;
+
+  for (int64_t c0 = cbeg; c0 < cend; c0 += kCK) {
+    __syncthreads();
+    const int64_t l0 = c0 % L, rb = c0 / L;  // one 64-bit divide per chunk
+    // ---- X tile: (ii, cc) -> X[l + L*(i + I*r)] with c = l + L*r
+    for (int e = tid; e < kCK * TI; e += kThreads) {
+      int ii, cc;
+      if (L == 1) { ii = e % TI; cc = e / TI; } else { cc = e % kCK; ii = e / kCK; }
+      const int64_t i = i0 + ii, c = c0 + cc;
+      Tmul x = Tmul(0);
+      if (i < I && c < cend) {
+        int64_t off;
+        if (L == 1) {
+          off = i + I * c;
+        } else {
+          int64_t l = l0 + cc, r = rb;
+          while (l >= L) { l -= L; ++r; }
+          off = l + L * (i + I * r);
+        }
+        const Tin xv = __ldg(X + off);
+        x = (Tmul)xv;
+        nsq += (double)xv * (double)xv;
+      }
+      sX[cc][ii] = x;
+    }
+    // ---- Omega chunk: rows c0..c0+CK, columns k0..k0+ell (Philox block granularity)
+    for (int e = tid; e < kCK * nb; e += kThreads) {
+      const int cc = e / nb, jb = e % nb;
+      const int64_t c = c0 + cc;
+      if (c >= cend) continue;
+      const uint4 w = omega_words(seed, mode, 0, (uint64_t)(c + col_offset), (uint32_t)(jb0 + jb));
+      Normal4<Tmul> z(w);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t kk = 4 * (jb0 + jb) + q - k0;
+        if (kk >= 0 && kk < ell) sO[cc][kk] = z.v[q];
+      }
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int cc = 0; cc < kCK; ++cc) {
+      Tmul a[4], b[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { a[q] = sX[cc][ti * 4 + q]; b[q] = sO[cc][tk * 4 + q]; }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+    }
+    // flush the chunk sum (<= 32 products) into the fp64 accumulators
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) { accd[p][q] += (double)acc[p][q]; acc[p][q] = Tmul(0); }
+  }
+  // ---- per-CTA partial: partial[split][k*I + i]
+  double *dst = partial + (int64_t)blockIdx.y * I * ell;
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int64_t i = i0 + ti * 4 + p;
+    if (i >= I) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = tk * 4 + q;
+      if (k < ell) dst[(int64_t)k * I + i] = accd[p][q];
+    }
+  }
+  if (norm_partial) {
+    for (int o = 16; o; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
+    if ((tid & 31) == 0) sred[tid >> 5] = nsq;
+    __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kThreads / 32; ++w) s += sred[w];
+      norm_partial[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+    }
+  }
+}
+
+// Y[e] = sum_s partial[s*n + e], fixed order.
+__global__ void reduce_splits_kernel(const double *__restrict__ partial, int nsplit, int64_t n,
+                                     double *__restrict__ Y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < nsplit; ++k) s += partial[(int64_t)k * n + e];
+    Y[e] = s;
+  }
+}
+
+template <typename Tout>
+__global__ void omega_rows_kernel(uint64_t seed, int mode, const int64_t *__restrict__ cols,
+                                  int64_t n, int ell, int64_t k0, Tout *__restrict__ out) {
+  const int64_t jb0 = k0 >> 2;
+  const int nb = (int)(((k0 + ell - 1) >> 2) - jb0 + 1);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * nb;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / nb;
+    const int jb = (int)(e % nb);
+    const uint4 w = omega_words(seed, mode, 0, (uint64_t)cols[i], (uint32_t)(jb0 + jb));
+    Normal4<Tout> z(w);
+    for (int q = 0; q < 4; ++q) {
+      const int64_t kk = 4 * (jb0 + jb) + q - k0;
+      if (kk >= 0 && kk < ell) out[i + n * kk] = z.v[q];
+    }
+  }
+}
+
+__global__ void philox_raw_kernel(const uint32_t *__restrict__ ctr, int64_t n, uint32_t k0,
+                                  uint32_t k1, uint32_t *__restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint4 c = make_uint4(ctr[4 * e], ctr[4 * e + 1], ctr[4 * e + 2], ctr[4 * e + 3]);
+    uint4 w = philox4x32_10(c, k0, k1);
+    out[4 * e] = w.x; out[4 * e + 1] = w.y; out[4 * e + 2] = w.z; out[4 * e + 3] = w.w;
+  }
+}
+
+template <typename Tin, typename Tmul, int LP>
+void launch_sketch(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int64_t k0, uint64_t seed,
+                   int64_t col_offset, double *Y, double *normsq) {
+  constexpr int TI = 4096 / LP;
+  constexpr int kCK = chunk_cols<LP>();
+  const int gx = ceil_div(v.I, TI);
+  const int64_t C = v.L * v.R;
+  // enough CTAs for ~4 per SM, each with at least 4 chunks of columns
+  int64_t target = std::max<int64_t>(1, (int64_t)c.num_sms * 4 / gx);
+  int64_t maxsplit = std::max<int64_t>(1, C / (4 * kCK));
+  int64_t nsplit = std::min<int64_t>(target, maxsplit);
+  int64_t cps = ((C + nsplit - 1) / nsplit + kCK - 1) / kCK * kCK;
+  nsplit = (C + cps - 1) / cps;
+  DevBuf<double> part(c, (size_t)nsplit * v.I * ell);
+  DevBuf<double> npart;
+  if (normsq) npart.alloc(c, (size_t)nsplit * gx);
+  dim3 grid(gx, (unsigned)nsplit);
+  RT_LAUNCH(c, (sketch_simt_kernel<Tin, Tmul, LP>), grid, kThreads, 0, X, v.L, v.I, v.R, cps,
+            seed, mode, ell, k0, col_offset, part.p, normsq ? npart.p : nullptr);
+  const int64_t n = v.I * ell;
+  RT_LAUNCH(c, reduce_splits_kernel, ceil_div(n, 256) > 1024 ? 1024 : ceil_div(n, 256), 256, 0,
+            part.p, (int)nsplit, n, Y);
+  if (normsq) sum_vec(c, npart.p, (int64_t)nsplit * gx, normsq);
+}
+
+template <typename Tin, typename Tmul>
+void sketch_dispatch(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int64_t k0,
+                     uint64_t seed, int64_t col_offset, double *Y, double *normsq) {
+  // Column blocks of <= 64 sketch columns; the norm is fused into the first block only.
+  for (int kb = 0; kb < ell; kb += 64) {
+    const int e = std::min(64, ell - kb);
+    double *Yb = Y + (int64_t)kb * v.I;
+    double *ns = kb == 0 ? normsq : nullptr;
+    if (e <= 16)
+      launch_sketch<Tin, Tmul, 16>(c, X, v, mode, e, k0 + kb, seed, col_offset, Yb, ns);
+    else if (e <= 32)
+      launch_sketch<Tin, Tmul, 32>(c, X, v, mode, e, k0 + kb, seed, col_offset, Yb, ns);
+    else
+      launch_sketch<Tin, Tmul, 64>(c, X, v, mode, e, k0 + kb, seed, col_offset, Yb, ns);
+  }
+}
+
+}  // namespace
+
+void sketch_dense(Ctx &c, const void *X, DT in, ModeView v, int mode, int ell, int64_t k0,
+                  uint64_t seed, int64_t col_offset, bool mul_f64, double *Y, double *normsq) {
+  if (in == DT::F64)
+    sketch_dispatch<double, double>(c, (const double *)X, v, mode, ell, k0, seed, col_offset, Y,
+                                    normsq);
+  else if (mul_f64)
+    sketch_dispatch<float, double>(c, (const float *)X, v, mode, ell, k0, seed, col_offset, Y,
+                                   normsq);
+  else
+    sketch_dispatch<float, float>(c, (const float *)X, v, mode, ell, k0, seed, col_offset, Y,
+                                  normsq);
+}
+
+void omega_rows(Ctx &c, DT out, uint64_t seed, int mode, const int64_t *cols, int64_t n, int ell,
+                int64_t k0, void *dst) {
+  const int g = std::max(1, std::min(4096, ceil_div(n * ((ell + 7) / 4), 256)));
+  if (out == DT::F64)
+    RT_LAUNCH(c, omega_rows_kernel<double>, g, 256, 0, seed, mode, cols, n, ell, k0, (double *)dst);
+  else
+    RT_LAUNCH(c, omega_rows_kernel<float>, g, 256, 0, seed, mode, cols, n, ell, k0, (float *)dst);
+}
+
+void philox_raw(Ctx &c, const uint32_t *ctr, int64_t n, uint32_t k0, uint32_t k1, uint32_t *out) {
+  const int g = std::max(1, std::min(4096, ceil_div(n, 256)));
+  RT_LAUNCH(c, philox_raw_kernel, g, 256, 0, ctr, n, k0, k1, out);
+}
+
+}  // namespace rt

@@ -1,0 +1,293 @@
+// Mode-n products out = X x_n A^T used for
+//   the B-pass   B = Q^T X_(n)            (Alg 1 line 3)  + fused Gram B B^T (fp64)
+//   the shrink   G_(n) <- U_B(:,1:r)^T B  (= Sigma_hat V_hat^T, Alg 3 line 6)
+//   the core chain G = X x_1 A_1^T ... x_d A_d^T (Alg 2 line 5).
+// SIMT kernel: each CTA walks tiles of TP output columns p = l + L*r (grid-stride), streams
+// the mode-n index i in chunks of CI through smem (X tile coalesced along the contiguous
+// index, A chunk), 4x4 register blocks, fp64 accumulation (fp32 products are flushed into
+// fp64 every CI terms).  The optional Gram of the produced tile is accumulated per CTA in
+// fp64 and reduced in a fixed order (deterministic).
+#include "kernels.h"
+
+namespace rt {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kCI = 32;
+
+template <typename Tin, typename Tout, typename Tmul, int JP, bool STORE, bool GRAM>
+__global__ void __launch_bounds__(kThreads) ttm_simt_kernel(
+    const Tin *__restrict__ X, int64_t L, int64_t I, int64_t R, const double *__restrict__ A, int64_t lda,
+    int J, int64_t Jst, Tout *__restrict__ out, double *__restrict__ gram_partial) {
+  // J: active output columns of this launch (<= JP); Jst: size of the output mode
+  // (stride of r in the output layout; > J when the caller blocks over j).
+  constexpr int TP = 4096 / JP;
+  constexpr int NJ = JP / 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Tmul *sX = reinterpret_cast<Tmul *>(smem_raw);   // [kCI][TP]
+  Tmul *sA = sX + kCI * TP;                         // [kCI][JP]
+  double *sB = reinterpret_cast<double *>(smem_raw); // [TP][JP+1] (after the main loop)
+
+  const int tid = threadIdx.x;
+  const int tj = tid % NJ, tp = tid / NJ;
+  const int64_t P = L * R;
+  const int64_t ntiles = (P + TP - 1) / TP;
+
+  double g[GRAM ? (JP * JP + kThreads - 1) / kThreads : 1];
+  if (GRAM) {
+#pragma unroll
+    for (int e = 0; e < (JP * JP + kThreads - 1) / kThreads; ++e) g[e] = 0.0;
+  }
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t p0 = tile * TP;
+    double accd[4][4];
+    Tmul acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) { accd[a][b] = 0.0; acc[a][b] = Tmul(0); }
+
+    const int64_t pl0 = p0 % L, pr0 = p0 / L;  // one 64-bit divide per tile
+    for (int64_t i0 = 0; i0 < I; i0 += kCI) {
+      __syncthreads();
+      for (int e = tid; e < kCI * TP; e += kThreads) {
+        int ii, pp;
+        if (L == 1) { ii = e % kCI; pp = e / kCI; } else { pp = e % TP; ii = e / TP; }
+        const int64_t i = i0 + ii, p = p0 + pp;
+        Tmul x = Tmul(0);
+        if (i < I && p < P) {
+          int64_t off;
+          if (L == 1) {
+            off = i + I * p;
+          } else {
+            int64_t l = pl0 + pp, r = pr0;
+            while (l >= L) { l -= L; ++r; }
+            off = l + L * (i + I * r);
+          }
+          x = (Tmul)__ldg(X + off);
+        }
+        sX[ii * TP + pp] = x;
+      }
+      for (int e = tid; e < kCI * JP; e += kThreads) {
+        const int ii = e / JP, j = e % JP;
+        const int64_t i = i0 + ii;
+        sA[ii * JP + j] = (i < I && j < J) ? (Tmul)__ldg(A + i + lda * j) : Tmul(0);
+      }
+      __syncthreads();
+#pragma unroll 8
+      for (int ii = 0; ii < kCI; ++ii) {
+        Tmul a[4], b[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { a[q] = sX[ii * TP + tp * 4 + q]; b[q] = sA[ii * JP + tj * 4 + q]; }
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc[p][q] = fma(a[p], b[q], acc[p][q]);
+      }
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) { accd[p][q] += (double)acc[p][q]; acc[p][q] = Tmul(0); }
+    }
+    // ---- epilogue: stage the tile (rounded to the stored precision) in smem
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int pp = tp * 4 + p, j = tj * 4 + q;
+        const bool valid = (p0 + pp < P) && (j < J);
+        sB[pp * (JP + 1) + j] = valid ? (double)(Tout)accd[p][q] : 0.0;
+      }
+    __syncthreads();
+    if (STORE) {
+      // out(l, j, r) at l + L*(j + J*r); coalesce along l (L > 1) or j (L == 1)
+      for (int e = tid; e < TP * JP; e += kThreads) {
+        int pp, j;
+        if (L == 1) { j = e % JP; pp = e / JP; } else { pp = e % TP; j = e / TP; }
+        const int64_t p = p0 + pp;
+        if (p < P && j < J) {
+          int64_t off;
+          if (L == 1) {
+            off = j + Jst * p;
+          } else {
+            int64_t l = pl0 + pp, r = pr0;
+            while (l >= L) { l -= L; ++r; }
+            off = l + L * (j + Jst * r);
+          }
+          out[off] = (Tout)sB[pp * (JP + 1) + j];
+        }
+      }
+    }
+    if (GRAM) {
+#pragma unroll
+      for (int e = 0; e < (JP * JP + kThreads - 1) / kThreads; ++e) {
+        const int idx = tid + e * kThreads;
+        if (idx < JP * JP) {
+          const int j1 = idx / JP, j2 = idx % JP;
+          double s = 0.0;
+          for (int pp = 0; pp < TP; ++pp) s = fma(sB[pp * (JP + 1) + j1], sB[pp * (JP + 1) + j2], s);
+          g[e] += s;
+        }
+      }
+    }
+  }
+  if (GRAM) {
+#pragma unroll
+    for (int e = 0; e < (JP * JP + kThreads - 1) / kThreads; ++e) {
+      const int idx = tid + e * kThreads;
+      if (idx < JP * JP) gram_partial[(int64_t)blockIdx.x * JP * JP + idx] = g[e];
+    }
+  }
+}
+
+// gram[j1 + J*j2] = sum_b partial[b][j1*JP + j2] (fixed order)
+__global__ void gram_reduce_kernel(const double *__restrict__ partial, int nblk, int JP, int J,
+                                   double *__restrict__ gram) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < J * J; e += gridDim.x * blockDim.x) {
+    const int j1 = e % J, j2 = e / J;
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += partial[(int64_t)b * JP * JP + j1 * JP + j2];
+    gram[e] = s;
+  }
+}
+
+template <typename Tin, typename Tout, typename Tmul, int JP>
+void launch_ttm(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t lda, int J, int64_t Jst,
+                Tout *out, double *gram) {
+  constexpr int TP = 4096 / JP;
+  const int64_t P = v.L * v.R;
+  const int64_t ntiles = (P + TP - 1) / TP;
+  const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)c.num_sms * 4));
+  const size_t sm_main = (size_t)kCI * (TP + JP) * sizeof(Tmul);
+  const size_t sm_epi = (size_t)TP * (JP + 1) * sizeof(double);
+  const size_t smem = std::max(sm_main, sm_epi);
+  DevBuf<double> part;
+  if (gram) part.alloc(c, (size_t)nblk * JP * JP);
+#define RT_TTM_CASE(ST, GR)                                                                   \
+  do {                                                                                        \
+    auto k = ttm_simt_kernel<Tin, Tout, Tmul, JP, ST, GR>;                                    \
+    RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    RT_LAUNCH(c, k, nblk, kThreads, smem, X, v.L, v.I, v.R, A, lda, J, Jst, out, part.p);     \
+  } while (0)
+  if (out && gram) RT_TTM_CASE(true, true);
+  else if (out) RT_TTM_CASE(true, false);
+  else RT_TTM_CASE(false, true);
+#undef RT_TTM_CASE
+  if (gram) RT_LAUNCH(c, gram_reduce_kernel, ceil_div((int64_t)J * J, 256), 256, 0, part.p, nblk, JP, J, gram);
+}
+
+// Gram of the mode-n unfolding of a (stored) tensor B with mode size J:
+// gram[j1 + J*j2] = sum_{l,r} B(l, j1, r) B(l, j2, r), computed per 64 x 64 block pair.
+constexpr int kGB = 64;
+template <typename T>
+__global__ void __launch_bounds__(kThreads) mode_gram_kernel(const T *__restrict__ B, int64_t L, int64_t J,
+                                                             int64_t R, int jb1, int jb2,
+                                                             double *__restrict__ partial) {
+  constexpr int TPc = 32;
+  __shared__ double s1[TPc][kGB + 1], s2[TPc][kGB + 1];
+  const int tid = threadIdx.x;
+  const int64_t P = L * R;
+  double acc[kGB * kGB / kThreads];
+#pragma unroll
+  for (int e = 0; e < kGB * kGB / kThreads; ++e) acc[e] = 0.0;
+  for (int64_t p0 = (int64_t)blockIdx.x * TPc; p0 < P; p0 += (int64_t)gridDim.x * TPc) {
+    __syncthreads();
+    for (int e = tid; e < TPc * kGB; e += kThreads) {
+      int pp, j;
+      if (L == 1) { j = e % kGB; pp = e / kGB; } else { pp = e % TPc; j = e / TPc; }
+      const int64_t p = p0 + pp;
+      const int64_t j1 = (int64_t)jb1 * kGB + j, j2 = (int64_t)jb2 * kGB + j;
+      double a = 0.0, b = 0.0;
+      if (p < P) {
+        const int64_t l = p % L, r = p / L;
+        if (j1 < J) a = (double)B[l + L * (j1 + J * r)];
+        if (j2 < J) b = (double)B[l + L * (j2 + J * r)];
+      }
+      s1[pp][j] = a;
+      s2[pp][j] = b;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < kGB * kGB / kThreads; ++e) {
+      const int idx = tid + e * kThreads;
+      const int a = idx / kGB, b = idx % kGB;
+      double s = 0.0;
+#pragma unroll 8
+      for (int pp = 0; pp < TPc; ++pp) s = fma(s1[pp][a], s2[pp][b], s);
+      acc[e] += s;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < kGB * kGB / kThreads; ++e)
+    partial[(int64_t)blockIdx.x * kGB * kGB + tid + e * kThreads] = acc[e];
+}
+
+__global__ void mode_gram_reduce_kernel(const double *__restrict__ partial, int nblk, int jb1, int jb2, int64_t J,
+                                        double *__restrict__ gram) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kGB * kGB; e += gridDim.x * blockDim.x) {
+    const int a = e / kGB, b = e % kGB;
+    const int64_t j1 = (int64_t)jb1 * kGB + a, j2 = (int64_t)jb2 * kGB + b;
+    if (j1 >= J || j2 >= J) continue;
+    double s = 0.0;
+    for (int k = 0; k < nblk; ++k) s += partial[(int64_t)k * kGB * kGB + e];
+    gram[j1 + J * j2] = s;
+    gram[j2 + J * j1] = s;
+  }
+}
+
+template <typename T>
+void mode_gram_t(Ctx &c, const T *B, ModeView v, double *gram) {
+  const int64_t P = v.L * v.R;
+  const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((P + 31) / 32, (int64_t)c.num_sms * 2));
+  const int nb = ceil_div(v.I, kGB);
+  DevBuf<double> part(c, (size_t)nblk * kGB * kGB);
+  for (int b1 = 0; b1 < nb; ++b1)
+    for (int b2 = b1; b2 < nb; ++b2) {
+      RT_LAUNCH(c, mode_gram_kernel<T>, nblk, kThreads, 0, B, v.L, v.I, v.R, b1, b2, part.p);
+      RT_LAUNCH(c, mode_gram_reduce_kernel, 16, 256, 0, part.p, nblk, b1, b2, v.I, gram);
+    }
+}
+
+template <typename Tin, typename Tout, typename Tmul>
+void ttm_dispatch(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t lda, int J, Tout *out,
+                  double *gram) {
+  if (J <= 16) return launch_ttm<Tin, Tout, Tmul, 16>(c, X, v, A, lda, J, J, out, gram);
+  if (J <= 32) return launch_ttm<Tin, Tout, Tmul, 32>(c, X, v, A, lda, J, J, out, gram);
+  if (J <= 64) return launch_ttm<Tin, Tout, Tmul, 64>(c, X, v, A, lda, J, J, out, gram);
+  // J > 64: blocks of 64 output columns, then the Gram of the stored output
+  DevBuf<Tout> tmp;
+  Tout *o = out;
+  if (!o) {
+    tmp.alloc(c, (size_t)v.L * J * v.R);
+    o = tmp.p;
+  }
+  for (int j0 = 0; j0 < J; j0 += 64)
+    launch_ttm<Tin, Tout, Tmul, 64>(c, X, v, A + lda * j0, lda, std::min(64, J - j0), J, o + v.L * j0, nullptr);
+  if (gram) mode_gram_t<Tout>(c, o, ModeView{v.L, J, v.R}, gram);
+}
+
+}  // namespace
+
+void mode_gram(Ctx &c, const void *B, DT t, ModeView v, double *gram) {
+  if (t == DT::F64) mode_gram_t<double>(c, (const double *)B, v, gram);
+  else mode_gram_t<float>(c, (const float *)B, v, gram);
+}
+
+void ttm_dense(Ctx &c, const void *X, DT in, ModeView v, const double *A, int64_t lda, int J,
+               void *out, DT outT, bool mul_f64, double *gram) {
+  RT_REQUIRE(out || gram, "ttm: nothing to compute");
+  if (in == DT::F64) {
+    RT_REQUIRE(outT == DT::F64, "ttm: fp64 input needs fp64 output");
+    ttm_dispatch<double, double, double>(c, (const double *)X, v, A, lda, J, (double *)out, gram);
+  } else if (outT == DT::F64 || mul_f64) {
+    RT_REQUIRE(outT == DT::F64, "ttm: fp64 products imply fp64 output");
+    ttm_dispatch<float, double, double>(c, (const float *)X, v, A, lda, J, (double *)out, gram);
+  } else {
+    ttm_dispatch<float, float, float>(c, (const float *)X, v, A, lda, J, (float *)out, gram);
+  }
+}
+
+}  // namespace rt

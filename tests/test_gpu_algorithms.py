@@ -1,0 +1,211 @@
+"""End-to-end GPU parity of R-STHOSVD / R-HOSVD through the C ABI against the CPU oracle
+on the same seeded inputs (DESIGN §5 criteria):
+  fp64 data: approximation distance delta <= 1e-12, |e_gpu - e_or| <= max(1e-12 e, 1e-14)
+  fp32 data: delta <= 1e-5, |e_gpu - e_or| / e_or <= 1e-5 (BASELINE north_star)."""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle as O
+from workloads import hilbert, tucker_c2, odeco, exact_rank, to_first_mode_fastest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1905_07311_b200.rtucker import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def _run(ctx, algo, x, ranks, p, seed, order=None, flags=0, device=True):
+    import torch
+    from paper_1905_07311_b200.rtucker import RESULT_HOST
+    xin = torch.as_tensor(to_first_mode_fastest(x), device="cuda") if device else x
+    if algo == "sthosvd":
+        return ctx.sthosvd(xin, x.shape, ranks, p, seed, order, flags | RESULT_HOST).numpy()
+    return ctx.hosvd(xin, x.shape, ranks, p, seed, flags | RESULT_HOST).numpy()
+
+
+def _oracle(algo, x, ranks, p, seed, order=None):
+    if algo == "sthosvd":
+        return O.r_sthosvd(x, ranks, p, seed, order)
+    return O.r_hosvd(x, ranks, p, seed)
+
+
+def _check(x, g, o, fp64):
+    delta = O.approx_distance(x, (g.core, g.factors), (o.core, o.factors))
+    eg = O.rel_error(x, g.core, g.factors)
+    eo = O.rel_error(x, o.core, o.factors)
+    if fp64:
+        assert delta <= 1e-12, delta
+        assert abs(eg - eo) <= max(1e-12 * eo, 1e-14), (eg, eo)
+    else:
+        assert delta <= 1e-5, delta
+        assert abs(eg - eo) <= 1e-5 * eo, (eg, eo)
+    for a in g.factors:
+        assert np.linalg.norm(a.T @ a - np.eye(a.shape[1])) <= 1e-12 * a.shape[1]
+    return delta, eg, eo
+
+
+FP64_CASES = [
+    ("C1", lambda: hilbert((50, 50, 50), "shifted"), (5, 5, 5), 5, (0, 1, 2)),
+    ("C3", lambda: hilbert((25,) * 5, "shifted"), (5,) * 5, 5, (0, 1, 2, 3, 4)),
+    ("paper25^5", lambda: hilbert((25,) * 5, "paper"), (5,) * 5, 5, None),
+    ("ragged", lambda: np.asfortranarray(np.random.default_rng(3).standard_normal((37, 19, 41))),
+     (7, 3, 11), 4, (2, 0, 1)),
+    ("d4_wide_ell", lambda: hilbert((70, 9, 13, 11), "paper"), (40, 3, 5, 4), 25, None),
+]
+
+
+@pytest.mark.parametrize("algo", ["sthosvd", "hosvd"])
+@pytest.mark.parametrize("name,make,ranks,p,order", FP64_CASES, ids=[c[0] for c in FP64_CASES])
+def test_fp64_parity(ctx, algo, name, make, ranks, p, order):
+    x = make()
+    g = _run(ctx, algo, x, ranks, p, seed=0, order=order)
+    o = _oracle(algo, x, ranks, p, 0, order)
+    assert g.ranks == o.ranks and g.ell == o.ell
+    _check(x, g, o, True)
+    if algo == "sthosvd":
+        assert g.order == o.order
+        # per-mode residuals ||G_prev||^2 - ||G_next||^2 (sum = ||X||^2 - ||G||^2)
+        for j in range(x.ndim):
+            assert abs(g.mode_residual_sq[j] - o.mode_residual_sq[j]) <= 1e-12 * g.norm_sq
+        assert abs(g.norm_sq - float(np.sum(x * x))) <= 1e-13 * g.norm_sq
+
+
+FP32_CASES = [
+    ("C2", lambda: tucker_c2(), (20, 20, 40), 10, None),
+    ("C3_f32", lambda: hilbert((25,) * 5, "shifted", dtype=np.float32), (5,) * 5, 5, (0, 1, 2, 3, 4)),
+    ("C1_f32", lambda: hilbert((50, 50, 50), "shifted", dtype=np.float32), (5, 5, 5), 5, (0, 1, 2)),
+    ("odeco96", lambda: odeco(96, seed=4, dtype=np.float32), (12, 12, 12), 10, (0, 1, 2)),
+]
+
+
+@pytest.mark.parametrize("algo", ["sthosvd", "hosvd"])
+@pytest.mark.parametrize("name,make,ranks,p,order", FP32_CASES, ids=[c[0] for c in FP32_CASES])
+def test_fp32_parity(ctx, algo, name, make, ranks, p, order):
+    x = make()
+    g = _run(ctx, algo, x, ranks, p, seed=1, order=order)
+    o = _oracle(algo, x, ranks, p, 1, order)
+    _check(x, g, o, False)
+
+
+def test_fp32_fp64_policy_is_tighter(ctx):
+    from paper_1905_07311_b200.rtucker import ACCUM_FP64
+    x = hilbert((25,) * 5, "shifted", dtype=np.float32)
+    g = _run(ctx, "sthosvd", x, (5,) * 5, 5, 0, (0, 1, 2, 3, 4), flags=ACCUM_FP64)
+    o = _oracle("sthosvd", x, (5,) * 5, 5, 0, (0, 1, 2, 3, 4))
+    delta, eg, eo = _check(x, g, o, False)
+    assert delta <= 1e-9 and abs(eg - eo) <= 1e-9 * eo
+
+
+def test_all_orders_c2_shape(ctx):
+    x = exact_rank((16, 12, 20), (3, 4, 5), seed=5)
+    for order in itertools.permutations(range(3)):
+        g = _run(ctx, "sthosvd", x, (3, 4, 5), 2, 4, order)
+        o = _oracle("sthosvd", x, (3, 4, 5), 2, 4, order)
+        _check(x, g, o, True)
+        assert O.rel_error(x, g.core, g.factors) <= 1e-12        # exact recovery
+
+
+def test_exact_recovery_p0(ctx):
+    x = exact_rank((50, 50, 50), (5, 5, 5), seed=7)
+    for algo in ("sthosvd", "hosvd"):
+        g = _run(ctx, algo, x, (5, 5, 5), 0, 0)
+        assert O.rel_error(x, g.core, g.factors) <= 1e-12
+
+
+def test_host_input_and_determinism(ctx):
+    """Host (numpy) input gives the bit-identical result of the device input; reruns are
+    bit-identical (fixed-order reductions, no float atomics)."""
+    x = hilbert((40, 30, 20), "paper")
+    a = _run(ctx, "sthosvd", x, (4, 4, 4), 5, 2, device=True)
+    b = _run(ctx, "sthosvd", x, (4, 4, 4), 5, 2, device=False)
+    c = _run(ctx, "sthosvd", x, (4, 4, 4), 5, 2, device=True)
+    np.testing.assert_array_equal(a.core, b.core)
+    np.testing.assert_array_equal(a.core, c.core)
+    for fa, fb in zip(a.factors, c.factors):
+        np.testing.assert_array_equal(fa, fb)
+
+
+def test_rel_error_on_device(ctx):
+    import torch
+    x = hilbert((50, 50, 50), "shifted")
+    xd = torch.as_tensor(to_first_mode_fastest(x), device="cuda")
+    r = ctx.sthosvd(xd, x.shape, (5, 5, 5), 5, 0, (0, 1, 2))
+    e = ctx.rel_error(xd, x.shape, r)
+    h = r.numpy()
+    assert abs(e - O.rel_error(x, h.core, h.factors)) <= 1e-12
+
+
+def test_rank_clamp_and_strict(ctx):
+    from paper_1905_07311_b200.rtucker import RTuckerError, STRICT
+    x = hilbert((8, 6, 5), "paper")
+    g = _run(ctx, "sthosvd", x, (5, 5, 5), 5, 0, (0, 1, 2))   # l clamped to the current caps
+    o = _oracle("sthosvd", x, (5, 5, 5), 5, 0, (0, 1, 2))
+    assert g.ell == o.ell
+    _check(x, g, o, True)
+    with pytest.raises(RTuckerError) as e:
+        _run(ctx, "sthosvd", x, (5, 5, 5), 5, 0, (0, 1, 2), flags=STRICT)
+    assert e.value.name == "EINVAL"
+
+
+def test_invalid_arguments(ctx):
+    from paper_1905_07311_b200.rtucker import RTuckerError
+    x = hilbert((6, 5, 4), "paper")
+    bad = [dict(ranks=(0, 2, 2)), dict(ranks=(7, 2, 2)), dict(p=-1), dict(order=(0, 0, 1)), dict(order=(0, 1, 3))]
+    for kw in bad:
+        args = dict(ranks=(2, 2, 2), p=1, order=None)
+        args.update(kw)
+        with pytest.raises(RTuckerError) as e:
+            ctx.sthosvd(x, x.shape, args["ranks"], args["p"], 0, args["order"])
+        assert e.value.name == "EINVAL", kw
+    with pytest.raises(RTuckerError) as e:
+        ctx.sthosvd(np.zeros(9 * 2 ** 0), (1,) * 9, (1,) * 9, 0)
+    assert e.value.name == "EUNSUPPORTED"
+
+
+def test_order_one_and_two_mode(ctx):
+    """d=1 and d=2 (RandSVD of a matrix, Alg 1)."""
+    rng = np.random.default_rng(4)
+    m = (rng.standard_normal((90, 8)) @ rng.standard_normal((8, 70))) + 1e-6 * rng.standard_normal((90, 70))
+    m = np.asfortranarray(m)
+    for algo in ("sthosvd", "hosvd"):
+        g = _run(ctx, algo, m, (8, 8), 4, 3, (0, 1) if algo == "sthosvd" else None)
+        o = _oracle(algo, m, (8, 8), 4, 3, (0, 1) if algo == "sthosvd" else None)
+        _check(m, g, o, True)
+    v = np.asfortranarray(rng.standard_normal(33))
+    g = _run(ctx, "sthosvd", v, (1,), 0, 0)
+    assert abs(O.rel_error(v, g.core, g.factors)) <= 1e-14
+
+
+@pytest.mark.slow
+def test_c4_full_size_rsthosvd(ctx):
+    """BASELINE configs[3] at full size (800^3 fp32, r=50, p=10, rho=[1,2,3]) in bench.py's
+    launch configuration, against the full oracle run on the same bits."""
+    import torch
+    xd = odeco(800, seed=4, dtype=np.float32, device="cuda")
+    from paper_1905_07311_b200.rtucker import RESULT_HOST
+    g = ctx.sthosvd(xd, (800, 800, 800), (50, 50, 50), 10, 0, (0, 1, 2), RESULT_HOST).numpy()
+    x = xd.cpu().numpy().reshape((800, 800, 800), order="F")
+    del xd
+    torch.cuda.empty_cache()
+    o = O.r_sthosvd(x, (50, 50, 50), 10, 0, (0, 1, 2))
+    nx2 = float(np.sum(x.astype(np.float64) ** 2))
+    # STHOSVD identity for both (orthonormal factors): e^2 = 1 - ||G||^2/||X||^2
+    eg = np.sqrt(max(0.0, 1 - np.sum(g.core ** 2) / nx2))
+    eo = np.sqrt(max(0.0, 1 - np.sum(o.core ** 2) / nx2))
+    assert abs(eg - eo) <= 1e-5 * eo, (eg, eo)
+    # delta via the factor algebra: ||Xg - Xo||^2 = ||Gg||^2 + ||Go||^2 - 2 <Gg, Go x_j (Ag_j^T Ao_j)>
+    t = o.core
+    for j in range(3):
+        t = O.mode_product(t, g.factors[j].T @ o.factors[j], j)
+    d2 = np.sum(g.core ** 2) + np.sum(o.core ** 2) - 2 * np.sum(g.core * t)
+    assert np.sqrt(max(d2, 0.0) / nx2) <= 1e-5

@@ -1,0 +1,125 @@
+"""GPU parity of the individual kernels through the C ABI against the CPU oracle
+(or, for the QR / eig / srrqr steps, against LAPACK on the same fp64 inputs)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from oracle.philox import philox4x32_10
+from workloads import hilbert, tucker_c2, to_first_mode_fastest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1905_07311_b200.rtucker import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def test_philox_words_bit_exact(ctx):
+    rng = np.random.default_rng(0)
+    n = 100000
+    ctr = rng.integers(0, 2 ** 32, size=(n, 4), dtype=np.uint64).astype(np.uint32)
+    for key in [(0, 0), (0xFFFFFFFF, 0xFFFFFFFF), (0xA4093822, 0x299F31D0)]:
+        got = ctx.debug_philox(ctr, *key)
+        ref = np.stack(philox4x32_10([ctr[:, i].astype(np.uint64) for i in range(4)],
+                                     [np.uint64(key[0]), np.uint64(key[1])]), axis=1)
+        np.testing.assert_array_equal(got, ref)
+
+
+@pytest.mark.parametrize("k0,ell", [(0, 64), (5, 7), (3, 1), (60, 10)])
+def test_omega_fp64(ctx, k0, ell):
+    cols = np.concatenate([np.arange(20000), np.array([2 ** 32 + 5, 2 ** 40 + 123])]).astype(np.int64)
+    got = ctx.debug_omega(cols, ell, seed=0x1234567890ABCDEF, mode=3, k0=k0, dtype="f64")
+    ref = O.omega_rows(0x1234567890ABCDEF, 3, cols, ell, k0=k0)
+    np.testing.assert_allclose(got, ref, rtol=1e-13, atol=1e-13)
+
+
+def test_omega_fp32(ctx):
+    cols = np.arange(1_000_000, dtype=np.int64)
+    got = ctx.debug_omega(cols, 4, seed=7, mode=1, dtype="f32").astype(np.float64)
+    ref = O.omega_rows(7, 1, cols, 4)
+    d = got - ref
+    assert np.sqrt(np.mean(d * d)) <= 3e-7
+    assert np.max(np.abs(d)) <= 2e-5
+
+
+def _sketch_ref(x, mode, ell, seed, k0=0):
+    xm = O.unfold(np.asarray(x, dtype=np.float64), mode)
+    return xm @ O.omega_rows(seed, mode, np.arange(xm.shape[1]), ell, k0=k0)
+
+
+CASES = [
+    ("hilbert50", lambda: hilbert((50, 50, 50), "shifted"), [10, 64, 70]),
+    ("ragged", lambda: np.asfortranarray(np.random.default_rng(1).standard_normal((37, 41, 29))), [13, 33]),
+    ("hilbert25^5", lambda: hilbert((25,) * 5, "shifted"), [10]),
+    ("c2_f32", lambda: tucker_c2(), [30, 50]),
+    ("hilbert25^5_f32", lambda: hilbert((25,) * 5, "shifted", dtype=np.float32), [10]),
+]
+
+
+@pytest.mark.parametrize("name,make,ells", CASES, ids=[c[0] for c in CASES])
+def test_sketch_all_modes(ctx, name, make, ells):
+    x = make()
+    tol = 1e-13 if x.dtype == np.float64 else 2e-6
+    for mode in range(x.ndim):
+        for ell in ells:
+            ell = min(ell, x.shape[mode] * 4)
+            got = ctx.debug_sketch(x, x.shape, mode, ell, seed=11)
+            ref = _sketch_ref(x, mode, ell, 11)
+            err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+            assert err <= tol, (name, mode, ell, err)
+
+
+def test_sketch_fp32_with_fp64_policy(ctx):
+    from paper_1905_07311_b200.rtucker import ACCUM_FP64
+    x = hilbert((25,) * 5, "shifted", dtype=np.float32)
+    got = ctx.debug_sketch(x, x.shape, 2, 10, seed=3, flags=ACCUM_FP64)
+    ref = _sketch_ref(x, 2, 10, 3)
+    assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 1e-13
+
+
+def test_sketch_block_offset(ctx):
+    """Adaptive blocks continue the global column index k (reading R3)."""
+    x = np.asfortranarray(np.random.default_rng(2).standard_normal((30, 20, 10)))
+    got = ctx.debug_sketch(x, x.shape, 1, 6, seed=9, k0=13)
+    ref = _sketch_ref(x, 1, 6, 9, k0=13)
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("m,n", [(800, 60), (50, 10), (25, 10), (1000, 1), (64, 64), (4096, 15)])
+def test_householder_qr(ctx, m, n):
+    rng = np.random.default_rng(m + n)
+    y = rng.standard_normal((m, n)) * np.logspace(0, -9, n)[None, :]
+    q = ctx.debug_qr(y)
+    assert np.linalg.norm(q.T @ q - np.eye(n)) <= 1e-13 * n
+    qr, _ = np.linalg.qr(y)
+    assert np.linalg.norm(q @ q.T - qr @ qr.T, 2) <= 1e-10
+    # rank-deficient sketch: exact rank 3 with 10 columns
+    if m >= 10 and n >= 10:
+        y = rng.standard_normal((m, 3)) @ rng.standard_normal((3, 10))
+        q = ctx.debug_qr(y)
+        assert np.linalg.norm(q.T @ q - np.eye(10)) <= 1e-12
+        assert np.linalg.norm(y - q @ (q.T @ y)) <= 1e-12 * np.linalg.norm(y)
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 10, 30, 60, 64, 65])
+def test_sym_eig(ctx, n):
+    rng = np.random.default_rng(n)
+    u, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.sort(np.logspace(0, -12, n) * (1 + 0.1 * rng.random(n)))[::-1]
+    a = (u * lam) @ u.T
+    a = (a + a.T) / 2
+    w, v = ctx.debug_eig(a)
+    print(f"n={n} jacobi sweeps={ctx.last_sweeps}")
+    assert ctx.last_sweeps < 40
+    wr = np.sort(np.linalg.eigvalsh(a))[::-1]
+    np.testing.assert_allclose(w, wr, rtol=0, atol=1e-15 * n)
+    assert np.all(np.diff(w) <= 0)
+    assert np.linalg.norm(v.T @ v - np.eye(n)) <= 1e-13 * n
+    assert np.linalg.norm(a @ v - v * w[None, :]) <= 1e-14 * n

@@ -94,7 +94,7 @@ def tucker_c2(seed: int = 2, dims=(64, 64, 400), core=(40, 40, 40), noise: float
 
 
 def odeco(I: int = 800, R: int | None = None, seed: int = 4, noise: float = 1e-4,
-          dtype=np.float32, device=None, third: int | None = None):
+          dtype=np.float32, device=None, third: int | None = None, slabs=None):
     """Orthogonally decomposable 3-mode tensor (BASELINE configs[3]):
     X0 = sum_{i<=R} sigma_i u_i o v_i o w_i, sigma_i = i^-1.5, Haar U, V (I x R) and W
     (third x R); X = X0 + E with E iid N(0, (noise*||X0||_F/sqrt(N))^2).
@@ -102,8 +102,9 @@ def odeco(I: int = 800, R: int | None = None, seed: int = 4, noise: float = 1e-4
     device=None: numpy fp64 construction, returns a logical-shape numpy array.
     device='cuda'/'cpu' torch device: builds slab-wise with torch (fp32 matmuls, no TF32)
     and returns a flat first-mode-fastest torch tensor of `dtype` on that device; the
-    noise is drawn with a torch generator seeded by `seed` (so bits differ from the numpy
-    variant; parity tests feed the same bits to both implementations).
+    noise of mode-3 slab c is drawn with a torch generator seeded by seed*1000003 + c (so
+    bits differ from the numpy variant; parity tests feed the same bits to both
+    implementations).  slabs=(lo, hi) builds only mode-3 slabs lo..hi-1 (a shard).
     """
     R = I if R is None else R
     K = I if third is None else third
@@ -128,21 +129,23 @@ def odeco(I: int = 800, R: int | None = None, seed: int = 4, noise: float = 1e-4
         Vt = torch.as_tensor(V.T.copy(), dtype=torch.float32, device=tdev)
         Wt = torch.as_tensor(W, dtype=torch.float32, device=tdev)
         tdt = torch.float32 if dtype in (np.float32, "float32") else torch.float64
-        out = torch.empty(K, I, I, dtype=tdt, device=tdev)  # [c][b][a]: a fastest
+        lo, hi = (0, K) if slabs is None else (int(slabs[0]), int(slabs[1]))
+        out = torch.empty(hi - lo, I, I, dtype=tdt, device=tdev)  # [c][b][a]: a fastest
         n_el = I * I * K
         std = noise * math.sqrt(float(np.sum(sig ** 2))) / math.sqrt(n_el)
         gen = torch.Generator(device=tdev)
-        gen.manual_seed(int(seed))
         chunk = 64
-        for c0 in range(0, K, chunk):
-            c1 = min(K, c0 + chunk)
+        for c0 in range(lo, hi, chunk):
+            c1 = min(hi, c0 + chunk)
             # slab[c] (a x b) = (U diag(sig*W[c,:])) V^T ; stored transposed so a is fastest
             scl = Wt[c0:c1]                                   # (cc, R)
             left = Us[None, :, :] * scl[:, None, :]           # (cc, I, R)
             slab = torch.matmul(left, Vt[None])               # (cc, I(a), I(b))
             slab = slab.transpose(1, 2)                       # (cc, b, a)
-            noise_t = torch.randn(slab.shape, generator=gen, device=tdev, dtype=torch.float32)
-            out[c0:c1] = (slab + std * noise_t).to(tdt)
+            for c in range(c0, c1):                           # per-slab noise stream: any slab
+                gen.manual_seed(int(seed) * 1_000_003 + c)    # range reproduces the same bits
+                nz = torch.randn((I, I), generator=gen, device=tdev, dtype=torch.float32)
+                out[c - lo] = (slab[c - c0] + std * nz).to(tdt)
         return out.reshape(-1)
     finally:
         torch.backends.cuda.matmul.allow_tf32 = prev
