@@ -67,9 +67,18 @@ typedef enum { RTUCKER_DEVICE = 0, RTUCKER_HOST = 1 } rtucker_memory;
 
 /* Flags (bitmask). */
 #define RTUCKER_STRICT            (1u << 0)  /* error instead of clamping l_n */
-#define RTUCKER_ACCUM_AUTO        (0u << 1)  /* fp32 data: fp64 chunk accumulation, fp32 intermediates */
-#define RTUCKER_ACCUM_FP64        (1u << 1)  /* fp32 data: fp64 arithmetic and fp64 intermediates */
-#define RTUCKER_ACCUM_FAST        (2u << 1)  /* fp32 data: tensor-core 3xTF32 passes where available */
+/* Precision policy for fp32 data (fp64 data always computes in fp64).  Every policy
+ * accumulates sums in fp64 (fp32 partial products are flushed into fp64 accumulators
+ * every few dozen terms); norms, Grams, QR and eigensolves are fp64 throughout.
+ *   AUTO    FP64 when max_n l_n <= 12, else HYBRID
+ *   FP64    fp64 products; B and every shrunk intermediate stored in fp64
+ *   FAST    fp32 (or 3xTF32 tensor-core) products; B and intermediates stored in fp32
+ *   HYBRID  FAST products on the fp32 input, B and intermediates stored in fp64 (later
+ *           passes therefore run in fp64) */
+#define RTUCKER_ACCUM_AUTO        (0u << 1)
+#define RTUCKER_ACCUM_FP64        (1u << 1)
+#define RTUCKER_ACCUM_FAST        (2u << 1)
+#define RTUCKER_ACCUM_HYBRID      (3u << 1)
 #define RTUCKER_ACCUM_MASK        (3u << 1)
 #define RTUCKER_ADAPT_NO_TRUNCATE (1u << 3)  /* adaptive: keep the block basis (no post-truncation) */
 #define RTUCKER_ADAPT_HOSVD       (1u << 4)  /* adaptive: Alg 4 (modes independent) instead of Alg 5 */

@@ -11,15 +11,31 @@ namespace rt {
 
 namespace {
 
+// Precision policy for the passes (include/rtucker.h flags).  Passes over fp64
+// data always multiply in fp64.  For fp32 data:
+//   FP64    fp64 products, fp64 B and intermediates
+//   FAST    fp32 products (flushed into fp64 accumulators), fp32 B and intermediates
+//   HYBRID  fp32 products on the fp32 input X, fp64 B and intermediates (so every later
+//           pass runs in fp64)
+//   AUTO    FP64 while max l <= 12 (2l/4 flop/B under the DFMA ridge), else HYBRID
 struct Policy {
-  bool mul_f64;  // fp64 products
+  bool mul_f64;  // fp64 products when reading fp32 data
   DT store;      // precision of B and of the shrunk intermediates
 };
 
-Policy policy_for(DT in, uint32_t flags) {
-  const uint32_t acc = flags & RTUCKER_ACCUM_MASK;
-  const bool f64 = in == DT::F64 || acc == RTUCKER_ACCUM_FP64;
-  return Policy{f64, f64 ? DT::F64 : DT::F32};
+Policy policy_for(DT in, uint32_t flags, int max_ell) {
+  uint32_t acc = flags & RTUCKER_ACCUM_MASK;
+  if (in == DT::F64) return Policy{true, DT::F64};
+  if (acc == RTUCKER_ACCUM_AUTO) acc = max_ell <= 12 ? RTUCKER_ACCUM_FP64 : RTUCKER_ACCUM_HYBRID;
+  if (acc == RTUCKER_ACCUM_FP64) return Policy{true, DT::F64};
+  if (acc == RTUCKER_ACCUM_HYBRID) return Policy{false, DT::F64};
+  return Policy{false, DT::F32};
+}
+
+int max_ell(const DenseIn &in, const int64_t *ranks, int p) {
+  int64_t m = 1;
+  for (int k = 0; k < in.d; ++k) m = std::max<int64_t>(m, std::min<int64_t>(ranks[k] + p, in.gdims[k]));
+  return (int)m;
 }
 
 void check_ranks(const DenseIn &in, const int64_t *ranks, int p) {
@@ -96,7 +112,7 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
   check_ranks(in, ranks, p);
   int32_t ord[kMaxModes];
   check_order(order, in.d, ord, in.gdims, in.sharded);
-  const Policy pol = policy_for(in.dt, flags);
+  const Policy pol = policy_for(in.dt, flags, max_ell(in, ranks, p));
   const int d = in.d;
   ResultGuard rg{c, new_result(d)};
   rtucker_result *res = rg.r;
@@ -195,7 +211,7 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
   DenseIn in;
   prepare_dense(c, X, in);
   check_ranks(in, ranks, p);
-  const Policy pol = policy_for(in.dt, flags);
+  const Policy pol = policy_for(in.dt, flags, max_ell(in, ranks, p));
   const int d = in.d;
   int32_t ord[kMaxModes];
   for (int k = 0; k < d; ++k) ord[k] = k;

@@ -26,6 +26,12 @@ inline ModeView mode_view(const int64_t *dims, int d, int n) {
 void sketch_dense(Ctx &c, const void *X, DT in, ModeView v, int mode, int ell, int64_t k0,
                   uint64_t seed, int64_t col_offset, bool mul_f64, double *Y, double *normsq);
 
+// sketch_tc.cu: tcgen05 3xTF32 variant for fp32 data with L == 1 (MN-major rows); returns
+// false when the shape is outside its envelope.
+bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0, uint64_t seed,
+                  int64_t col_offset, double *Y, double *normsq);
+bool sketch_tc_enabled();
+
 // Generates Omega rows for given columns (debug / parity).
 void omega_rows(Ctx &c, DT out, uint64_t seed, int mode, const int64_t *cols, int64_t n,
                 int ell, int64_t k0, void *dst);

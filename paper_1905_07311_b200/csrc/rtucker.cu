@@ -225,6 +225,12 @@ rtucker_status rtucker_ctx_create(int device, void *cuda_stream, const void *ncc
       ctx->c.own_stream = true;
     }
     RT_CUDA(cudaDeviceGetAttribute(&ctx->c.num_sms, cudaDevAttrMultiProcessorCount, device));
+    // keep freed stream-ordered workspace in the pool between calls (no re-mapping of the
+    // large B / shrunk-core buffers on every decomposition)
+    cudaMemPool_t pool;
+    RT_CUDA(cudaDeviceGetMemPool(&pool, device));
+    uint64_t thr = UINT64_MAX;
+    RT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     ctx->c.rank = rank;
     ctx->c.nranks = nranks;
     if (nranks > 1) ctx->c.comm = comm_create(nccl_unique_id, rank, nranks);

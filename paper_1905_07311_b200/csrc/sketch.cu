@@ -9,6 +9,7 @@
 // The squared Frobenius norm of X is fused in (each element is read exactly once).
 #include "kernels.h"
 #include "philox.cuh"
+#include <type_traits>
 
 namespace rt {
 
@@ -201,6 +202,9 @@ void sketch_dispatch(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int64_
     const int e = std::min(64, ell - kb);
     double *Yb = Y + (int64_t)kb * v.I;
     double *ns = kb == 0 ? normsq : nullptr;
+    if constexpr (std::is_same<Tin, float>::value && std::is_same<Tmul, float>::value) {
+      if (sketch_tc_mn(c, X, v, mode, e, k0 + kb, seed, col_offset, Yb, ns)) continue;
+    }
     if (e <= 16)
       launch_sketch<Tin, Tmul, 16>(c, X, v, mode, e, k0 + kb, seed, col_offset, Yb, ns);
     else if (e <= 32)

@@ -1,0 +1,340 @@
+// Tensor-core (tcgen05, 3xTF32) mode-n sketch Y = X_(n) Omega_n (Alg 1 line 1) for
+// fp32 data whose mode-n rows are the contiguous index (L == 1: mode 1, or any mode whose
+// lower modes are all 1), i.e. X_(n) is stored column-major I x C and the MMA A operand
+// is MN-major.  Omega is generated on the fly into shared memory; it is never read
+// from HBM.
+//
+// Layout of one CTA (persistent, one per SM, split-K over the unfolding columns c):
+//   warp 0      TMA producer: per stage, boxes of 256 rows x 8 columns of X into a staging
+//               buffer (plain row-major [c][i] tiles)
+//   warp 1      TMEM allocation + MMA issuer (one elected thread)
+//   warps 2-9   workers: split X = hi + lo (hi = tf32 truncation, lo = X - hi exact) and
+//               write both TRANSPOSED into K-major operand tiles (the tensor core reads
+//               tf32 operands K-major only: an MN-major tf32 A measured as all-zero output
+//               on this B200, scripts/dbg/tc_probe.cu), generate Omega(c0:c0+8, k0:k0+N)
+//               with Philox4x32-10 + Box-Muller (fp32, DESIGN reading R3) as hi/lo K-major
+//               tiles, accumulate ||X||^2; after the last stage: TMEM -> fp64 partial Y.
+//   The accumulator of M-tile mt (rows 128 mt ..) lives in TMEM columns [mt N, mt N + N):
+//   3 MMAs per M-tile and stage, D += Xhi*Ohi + Xhi*Olo + Xlo*Ohi (M=128, N, K=8), fp32
+//   accumulation in TMEM (BASELINE "3xTF32"; the dropped Xlo*Olo term is 2^-22 relative).
+//   K-major no-swizzle operand tile (rows r, 8 K): byte (r/8)*256 + (k/4)*128 + (r%8)*16 + (k%4)*4.
+// Per-CTA partial sketches are reduced in a fixed order by the caller (deterministic).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "kernels.h"
+#include "philox.cuh"
+#include "tc.cuh"
+
+namespace rt {
+
+namespace {
+
+constexpr int kBK = 8;               // unfolding columns per stage (= MMA K for tf32)
+constexpr int kWorkers = 8;          // worker warps
+constexpr int kThreads = 32 * (2 + kWorkers);
+
+struct SketchTcParams {
+  int64_t I, C;          // rows, unfolding columns
+  int64_t cps;           // columns per CTA (multiple of kBK)
+  int NT;                // M-tiles of 128 rows
+  int nbox, BR;          // TMA boxes per stage and rows per box (nbox * BR >= I, BR <= 256)
+  int NSS, NSO;          // staging stages (TMA depth), operand stages
+  int ell;               // valid sketch columns (<= N)
+  int64_t k0;            // first global sketch column
+  uint64_t seed;
+  int mode;
+  int64_t col_offset;    // global unfolding-column offset of this shard
+  double *partial;       // [grid][ell][I]
+  double *norm_partial;  // [grid] or null
+};
+
+__device__ __forceinline__ int kmaj_off(int r, int k) {  // byte offset in a K-major tile
+  return (r >> 3) * 256 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4;
+}
+
+template <int N>
+__global__ void __launch_bounds__(kThreads, 1)
+    sketch_tc_mn_kernel(const __grid_constant__ CUtensorMap tmap, const SketchTcParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // offsets from smem_raw (kept as shared-window pointers so that the compiler emits LDS/STS)
+  const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
+  unsigned char *base = smem_raw + pad;
+  const int NT = p.NT, NSS = p.NSS, NSO = p.NSO;
+  const int sbytes = p.nbox * p.BR * kBK * 4;      // staging (raw X) per stage
+  const int abytes = NT * 128 * kBK * 4;           // one operand plane (all M-tiles)
+  const int obytes = N * kBK * 4;                  // one Omega tile
+  unsigned char *hb = base;                        // [NSO][abytes]  X hi (K-major)
+  unsigned char *lb = hb + (size_t)NSO * abytes;   // [NSO][abytes]  X lo
+  unsigned char *ohb = lb + (size_t)NSO * abytes;  // [NSO][obytes]
+  unsigned char *olb = ohb + (size_t)NSO * obytes; // [NSO][obytes]
+  unsigned char *sb = olb + (size_t)NSO * obytes;  // [NSS][sbytes]
+  uint64_t *full = (uint64_t *)(sb + (size_t)NSS * sbytes);
+  uint64_t *sfree = full + NSS;
+  uint64_t *ready = sfree + NSS;
+  uint64_t *empty = ready + NSO;
+  uint64_t *done = empty + NSO;
+  uint32_t *tslot = (uint32_t *)(done + 1);
+  double *wsum = (double *)(tslot + 2);            // [kWorkers]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t cbeg = (int64_t)blockIdx.x * p.cps;
+  const int64_t cend = min(p.C, cbeg + p.cps);
+  const int nst = (int)((cend - cbeg + kBK - 1) / kBK);
+  const uint32_t tcols = NT * N <= 32 ? 32 : NT * N <= 64 ? 64 : NT * N <= 128 ? 128 : NT * N <= 256 ? 256 : 512;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSS; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&sfree[s], 32 * kWorkers);
+    }
+    for (int s = 0; s < NSO; ++s) {
+      tc::mbar_init(&ready[s], 32 * kWorkers);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(done, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, tcols);
+  // Omega tiles: columns n >= ell stay zero for the whole kernel
+  for (int e = threadIdx.x; e < 2 * NSO * obytes / 4; e += kThreads) ((float *)ohb)[e] = 0.f;
+  tc::fence_proxy_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------- TMA producer
+    if (lane == 0 && nst > 0) {
+      tc::tma_prefetch_desc(&tmap);
+      const uint32_t bytes = (uint32_t)sbytes;
+      const int boxb = p.BR * kBK * 4;
+      for (int it = 0; it < nst; ++it) {
+        const int s = it % NSS;
+        if (it >= NSS) tc::mbar_wait(&sfree[s], ((it / NSS) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&full[s], bytes);
+        const int c0 = (int)(cbeg + (int64_t)it * kBK);
+        unsigned char *dst = sb + (size_t)s * sbytes;
+        for (int b = 0; b < p.nbox; ++b) tc::tma_load_2d(dst + b * boxb, &tmap, &full[s], p.BR * b, c0);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------- MMA issuer
+    if (lane == 0 && nst > 0) {
+      constexpr uint32_t idesc = tc::idesc_tf32(128, N, false, false);
+      for (int it = 0; it < nst; ++it) {
+        const int s = it % NSO;
+        tc::mbar_wait(&ready[s], (it / NSO) & 1);
+        tc::tc_fence_after();
+        const uint32_t ha = tc::smem_u32(hb + (size_t)s * abytes);
+        const uint32_t la = tc::smem_u32(lb + (size_t)s * abytes);
+        const uint64_t bh = tc::smem_desc(tc::smem_u32(ohb + (size_t)s * obytes), 128, 256, tc::kSwNone);
+        const uint64_t bl = tc::smem_desc(tc::smem_u32(olb + (size_t)s * obytes), 128, 256, tc::kSwNone);
+        for (int mt = 0; mt < NT; ++mt) {
+          const uint64_t ah = tc::smem_desc(ha + mt * 128 * kBK * 4, 128, 256, tc::kSwNone);
+          const uint64_t al = tc::smem_desc(la + mt * 128 * kBK * 4, 128, 256, tc::kSwNone);
+          const uint32_t d = tmem + mt * N;
+          tc::mma_tf32(d, ah, bh, idesc, it > 0 ? 1u : 0u);
+          tc::mma_tf32(d, ah, bl, idesc, 1u);
+          tc::mma_tf32(d, al, bh, idesc, 1u);
+        }
+        tc::mma_commit(&empty[s]);
+      }
+      tc::mma_commit(done);
+    }
+  } else {
+    // ------------------------------------------------------------- workers
+    const int wt = threadIdx.x - 64;  // 0 .. 32*kWorkers-1
+    const int64_t jb0 = p.k0 >> 2;
+    const int nb = (int)(((p.k0 + p.ell - 1) >> 2) - jb0 + 1);
+    const int rows_st = min(NT * 128, p.nbox * p.BR);  // operand rows filled from staging
+    double nsq = 0.0;
+    for (int it = 0; it < nst; ++it) {
+      const int so = it % NSO, ss = it % NSS;
+      const int64_t c0 = cbeg + (int64_t)it * kBK;
+      // the MMAs of this operand slot's previous use must have finished reading it
+      if (it >= NSO) tc::mbar_wait(&empty[so], ((it / NSO) & 1) ^ 1);
+      // Omega(c0 .. c0+7, k0 .. k0+ell) -> hi/lo K-major tiles (rows n, K = c)
+      float *oh = (float *)(ohb + (size_t)so * obytes), *ol = (float *)(olb + (size_t)so * obytes);
+      for (int t = wt; t < kBK * nb; t += 32 * kWorkers) {
+        const int kk = t & (kBK - 1), jb = t >> 3;
+        const int64_t c = c0 + kk;
+        const bool valid = c < cend;
+        const uint4 w = omega_words(p.seed, p.mode, 0, (uint64_t)(c + p.col_offset), (uint32_t)(jb0 + jb));
+        Normal4<float> z(w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t n = 4 * (jb0 + jb) + q - p.k0;
+          if (n >= 0 && n < p.ell) {
+            const float v = valid ? z.v[q] : 0.f;
+            const float hi = tc::tf32_hi(v);
+            const int off = kmaj_off((int)n, kk) >> 2;
+            oh[off] = hi;
+            ol[off] = v - hi;
+          }
+        }
+      }
+      // X staging [box][c][BR rows] -> hi / lo K-major tiles (rows i, K = c); rows >= I are
+      // zero-filled by the TMA, rows beyond the staging extent are never read by a valid D row
+      tc::mbar_wait(&full[ss], (it / NSS) & 1);
+      const float *st = (const float *)(sb + (size_t)ss * sbytes);
+      unsigned char *hs = hb + (size_t)so * abytes, *ls = lb + (size_t)so * abytes;
+      float acc = 0.f;
+      int box = 0, r = wt;
+      while (r >= p.BR) { r -= p.BR; ++box; }
+      for (int i = wt; i < rows_st; i += 32 * kWorkers) {
+        const float *src = st + box * (p.BR * kBK) + r;
+#pragma unroll
+        for (int cq = 0; cq < 2; ++cq) {
+          float x[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) x[u] = src[(4 * cq + u) * p.BR];
+          float4 h, l;
+          h.x = tc::tf32_hi(x[0]); h.y = tc::tf32_hi(x[1]); h.z = tc::tf32_hi(x[2]); h.w = tc::tf32_hi(x[3]);
+          l.x = x[0] - h.x; l.y = x[1] - h.y; l.z = x[2] - h.z; l.w = x[3] - h.w;
+          const int off = (i >> 3) * 256 + cq * 128 + (i & 7) * 16;
+          *(float4 *)(hs + off) = h;
+          *(float4 *)(ls + off) = l;
+          acc = fmaf(x[0], x[0], fmaf(x[1], x[1], fmaf(x[2], x[2], fmaf(x[3], x[3], acc))));
+        }
+        r += 32 * kWorkers;
+        while (r >= p.BR) { r -= p.BR; ++box; }
+      }
+      nsq += (double)acc;
+      tc::mbar_arrive(&sfree[ss]);       // staging slot may be refilled
+      tc::fence_proxy_async_smem();
+      tc::mbar_arrive(&ready[so]);
+    }
+    // ---- epilogue: TMEM -> fp64 partial[blockIdx.x][k * I + i]
+    const int q4 = warp & 3;              // TMEM lane quadrant of this warp
+    const int half = (warp - 2) >> 2;     // 0 / 1: which 32 of the N columns
+    if (nst > 0) {
+      tc::mbar_wait(done, 0);
+      tc::tc_fence_after();
+    }
+    double *dst = p.partial + (int64_t)blockIdx.x * p.ell * p.I;
+    if (half * 32 < N) {
+      for (int mt = 0; mt < NT; ++mt) {
+        uint32_t r[32];
+        if (nst > 0) tc::tmem_ld32(tmem + ((uint32_t)(32 * q4) << 16) + mt * N + half * 32, r);
+        const int64_t i = (int64_t)mt * 128 + 32 * q4 + lane;
+        if (i < p.I) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int k = half * 32 + j;
+            if (k < p.ell) dst[(int64_t)k * p.I + i] = nst > 0 ? (double)__uint_as_float(r[j]) : 0.0;
+          }
+        }
+      }
+    }
+    if (p.norm_partial) {
+      for (int o = 16; o; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
+      if (lane == 0) wsum[warp - 2] = nsq;
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (p.norm_partial && threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kWorkers; ++w) s += wsum[w];
+    p.norm_partial[blockIdx.x] = s;
+  }
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, tcols);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    RT_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q));
+    if (!ptr || q != cudaDriverEntryPointSuccess) throw Error(RTUCKER_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    fn = (PFN_cuTensorMapEncodeTiled_v12000)ptr;
+  }
+  return fn;
+}
+
+__global__ void reduce_partials_kernel(const double *__restrict__ partial, int nsplit, int64_t n,
+                                       double *__restrict__ Y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < nsplit; ++k) s += partial[(int64_t)k * n + e];
+    Y[e] = s;
+  }
+}
+
+template <int N>
+void launch(Ctx &c, const CUtensorMap &tm, SketchTcParams &p, int grid, size_t smem) {
+  auto k = sketch_tc_mn_kernel<N>;
+  RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  RT_LAUNCH(c, k, grid, kThreads, smem, tm, p);
+}
+
+}  // namespace
+
+bool sketch_tc_enabled() {
+  static const bool off = getenv("RTUCKER_NO_TC") != nullptr;
+  return !off;
+}
+
+// Y (I x ell fp64, column-major) = X_(n) Omega(:, k0:k0+ell) for fp32 X with L == 1.
+// Returns false when the shape is outside this kernel's envelope (caller falls back).
+bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0, uint64_t seed,
+                  int64_t col_offset, double *Y, double *normsq) {
+  if (!sketch_tc_enabled() || v.L != 1 || (v.I % 4) != 0 || ell > 64 || ell < 1) return false;
+  const int N = ell <= 32 ? 32 : 64;
+  const int NT = (int)((v.I + 127) / 128);
+  if (NT * N > 512 || (((uintptr_t)X) & 15) != 0) return false;
+  const int64_t C = v.R;
+  if (C > (int64_t)INT32_MAX - 64) return false;
+  SketchTcParams p{};
+  p.I = v.I;
+  p.C = C;
+  p.NT = NT;
+  p.nbox = (int)((v.I + 255) / 256);
+  p.BR = (int)(((v.I + p.nbox - 1) / p.nbox + 7) / 8 * 8);
+  const size_t sbytes = (size_t)p.nbox * p.BR * kBK * 4, abytes = (size_t)NT * 128 * kBK * 4,
+               obytes = (size_t)N * kBK * 4;
+  const size_t budget = 220 * 1024;
+  p.NSO = 2;
+  const size_t fixed = 1024 + 2 * p.NSO * (abytes + obytes) + 512;
+  if (fixed + 2 * sbytes > budget) return false;
+  p.NSS = (int)std::min<size_t>(4, (budget - fixed) / sbytes);
+  const size_t smem = fixed + p.NSS * sbytes;
+  const int64_t nchunks = (C + kBK - 1) / kBK;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(c.num_sms, nchunks / 4));
+  p.cps = ((nchunks + grid - 1) / grid) * kBK;
+  const int g = (int)((C + p.cps - 1) / p.cps);
+  p.ell = ell;
+  p.k0 = k0;
+  p.seed = seed;
+  p.mode = mode;
+  p.col_offset = col_offset;
+  DevBuf<double> part(c, (size_t)g * ell * v.I);
+  DevBuf<double> npart;
+  if (normsq) npart.alloc(c, g);
+  p.partial = part.p;
+  p.norm_partial = normsq ? npart.p : nullptr;
+
+  CUtensorMap tm;
+  cuuint64_t dims[2] = {(cuuint64_t)v.I, (cuuint64_t)C};
+  cuuint64_t strides[1] = {(cuuint64_t)v.I * 4};
+  cuuint32_t box[2] = {(cuuint32_t)p.BR, kBK};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)X, dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(RTUCKER_ECUDA, "cuTensorMapEncodeTiled failed for the sketch operand");
+  if (N == 32) launch<32>(c, tm, p, g, smem);
+  else launch<64>(c, tm, p, g, smem);
+  const int64_t n = v.I * ell;
+  RT_LAUNCH(c, reduce_partials_kernel, (int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, part.p, g, n, Y);
+  if (normsq) sum_vec(c, npart.p, g, normsq);
+  return true;
+}
+
+}  // namespace rt

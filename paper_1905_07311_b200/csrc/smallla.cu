@@ -11,7 +11,7 @@
 //  sym_eig          eigenpairs of the l x l Gram B B^T (thin SVD of B, Alg 1 line 4)
 //                   by one-sided (Hestenes) Jacobi on the Gram itself: each warp owns one
 //                   column pair of the round-robin ordering, so a round needs a single CTA
-//                   barrier.  Relative stopping test |g_pq| <= tol sqrt(g_pp g_qq).
+//                   barrier.
 //  canonical_signs  the sign convention of DESIGN reading R4b.
 #include <cooperative_groups.h>
 
@@ -35,14 +35,34 @@ constexpr int kQRT = 512;  // threads per CTA
 constexpr int kNW = kQRT / 32;
 constexpr int kMaxN = 64;  // columns handled by the cluster kernel
 
-// Sum over the cluster of slot `idx` of the message buffers: lane k reads CTA k's value,
-// then a butterfly (identical order in every warp of every CTA => identical results).
-__device__ __forceinline__ double cluster_sum(cg::cluster_group &cl, double *buf, int idx, int ncta, int lane) {
-  double v = 0.0;
-  for (int k = lane; k < ncta; k += 32) v += cl.map_shared_rank(buf, k)[idx];
-  return warp_sum(v);
+constexpr int kMaxCTA = 16;
+
+// Cluster-wide sums of slots [s0, s1) of every CTA's message buffer `buf`: all threads
+// gather the remote slots into `gat` in one parallel sweep (one DSMEM round trip), then
+// slot s is summed over CTAs 0..ncta-1 in that fixed order, so every CTA derives
+// bit-identical values.  Ends with a CTA barrier; `tot` holds the sums.
+__device__ __forceinline__ void cluster_allsum(cg::cluster_group &cl, double *buf, double *gat, double *tot,
+                                               int s0, int s1, int ncta) {
+  const int w = s1 - s0;
+  for (int e = threadIdx.x; e < ncta * w; e += kQRT) {
+    const int k = e / w, s = s0 + e % w;
+    gat[k * 2 * kMaxN + s] = cl.map_shared_rank(buf, k)[s];
+  }
+  __syncthreads();
+  for (int s = s0 + (int)threadIdx.x; s < s1; s += kQRT) {
+    double v = 0.0;
+    for (int k = 0; k < ncta; ++k) v += gat[k * 2 * kMaxN + s];
+    tot[s] = v;
+  }
+  __syncthreads();
 }
 
+// Householder QR of the m x n sketch with its rows split over the CTAs of a cluster (row
+// slab of W and Q in each CTA's shared memory).  Per column j: partial dots x_j^T w_c and
+// the row-j entries -> one cluster barrier -> gathered, summed in fixed order -> every CTA
+// forms the same reflector v = x_j + sign(alpha) ||x_j|| e_j, beta = 1/(||x|| (||x|| + |alpha|))
+// and updates its rows; v^T w_c = x_j^T w_c + (v_0 - alpha) w_c[j].  Q = H_0 .. H_{n-1} [I; 0]
+// is then accumulated backwards the same way.
 __global__ void __launch_bounds__(kQRT) qr_cluster_kernel(const double *__restrict__ Y, int64_t m, int n,
                                                           int rows, double *__restrict__ Q) {
   extern __shared__ double sm[];
@@ -55,8 +75,10 @@ __global__ void __launch_bounds__(kQRT) qr_cluster_kernel(const double *__restri
   const int nloc = left <= 0 ? 0 : (left < rows ? (int)left : rows);
   double *W = sm;                        // rows x n (column-major, ld = rows)
   double *Qs = W + (size_t)rows * n;     // rows x n
-  double *msg = Qs + (size_t)rows * n;   // [2][kMaxN][2]: (partial dot, row-j entry)
-  double *beta = msg + 4 * kMaxN;        // [kMaxN]
+  double *msg = Qs + (size_t)rows * n;   // [2 parity][2 kMaxN]: (partial dot, row-j entry)
+  double *gat = msg + 4 * kMaxN;         // [kMaxCTA][2 kMaxN]
+  double *tot = gat + 2 * kMaxN * kMaxCTA;  // [2 kMaxN]
+  double *beta = tot + 2 * kMaxN;        // [kMaxN]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   for (int e = tid; e < rows * n; e += kQRT) {
@@ -71,7 +93,6 @@ __global__ void __launch_bounds__(kQRT) qr_cluster_kernel(const double *__restri
     const int jl = j - r0i;                   // local index of row j (owner: 0 <= jl < nloc)
     const bool owner = jl >= 0 && jl < nloc;
     const int i0 = max(jl, 0);                // local rows with global index >= j
-    // partial x_j^T w_c over local rows >= j (c = j gives ||x_j||^2) and w_c[j] (owner)
     for (int c = j + warp; c < n; c += kNW) {
       double d = 0.0;
       for (int i = i0 + lane; i < nloc; i += 32) d += W[i + rows * j] * W[i + rows * c];
@@ -82,9 +103,9 @@ __global__ void __launch_bounds__(kQRT) qr_cluster_kernel(const double *__restri
       }
     }
     cl.sync();
-    const double nrm2 = cluster_sum(cl, buf, 2 * j, ncta, lane);
-    const double alpha = cluster_sum(cl, buf, 2 * j + 1, ncta, lane);
-    const double nrm = sqrt(nrm2);
+    cluster_allsum(cl, buf, gat, tot, 2 * j, 2 * n, ncta);
+    const double nrm = sqrt(tot[2 * j]);
+    const double alpha = tot[2 * j + 1];
     double b = 0.0, v0 = 0.0;
     if (nrm > 0.0) {
       v0 = alpha + (alpha >= 0.0 ? nrm : -nrm);
@@ -92,17 +113,14 @@ __global__ void __launch_bounds__(kQRT) qr_cluster_kernel(const double *__restri
     }
     if (tid == 0) beta[j] = b;
     if (b != 0.0) {
-      for (int c = j + 1 + warp; c < n; c += kNW) {
-        const double D = cluster_sum(cl, buf, 2 * c, ncta, lane);
-        const double R = cluster_sum(cl, buf, 2 * c + 1, ncta, lane);
-        const double f = b * (D + (v0 - alpha) * R);   // beta * v^T w_c
-        for (int i = i0 + lane; i < nloc; i += 32) {
-          const double vi = (i == jl) ? v0 : W[i + rows * j];
-          W[i + rows * c] -= f * vi;
-        }
+      const int nr = nloc - i0, nc = n - j - 1;
+      for (int e = tid; e < nr * nc; e += kQRT) {
+        const int i = i0 + e % nr, c = j + 1 + e / nr;
+        const double f = b * (tot[2 * c] + (v0 - alpha) * tot[2 * c + 1]);  // beta v^T w_c
+        const double vi = (i == jl) ? v0 : W[i + rows * j];
+        W[i + rows * c] -= f * vi;
       }
     }
-    __syncthreads();
     if (owner && tid == 0) W[jl + rows * j] = v0;  // store v in place (v_j = v0)
     __syncthreads();
   }
@@ -124,12 +142,14 @@ __global__ void __launch_bounds__(kQRT) qr_cluster_kernel(const double *__restri
       double d = 0.0;
       for (int i = i0 + lane; i < nloc; i += 32) d += W[i + rows * j] * Qs[i + rows * c];
       d = warp_sum(d);
-      if (lane == 0) buf[2 * c] = d;
+      if (lane == 0) buf[c] = d;
     }
     cl.sync();
-    for (int c = j + warp; c < n; c += kNW) {
-      const double f = b * cluster_sum(cl, buf, 2 * c, ncta, lane);
-      for (int i = i0 + lane; i < nloc; i += 32) Qs[i + rows * c] -= f * W[i + rows * j];
+    cluster_allsum(cl, buf, gat, tot, j, n, ncta);
+    const int nr = nloc - i0, nc = n - j;
+    for (int e = tid; e < nr * nc; e += kQRT) {
+      const int i = i0 + e % nr, c = j + e / nr;
+      Qs[i + rows * c] -= b * tot[c] * W[i + rows * j];
     }
     __syncthreads();
   }
@@ -203,6 +223,9 @@ __global__ void __launch_bounds__(kQRG) qr_global_kernel(double *__restrict__ W,
 }
 
 // ------------------------------------------------------- one-sided Jacobi eig -------
+#ifndef RT_EIG_PROBE
+#define RT_EIG_PROBE(k)
+#endif
 constexpr int kEigT = 1024;
 
 // Pair k of round t of the round-robin tournament on np (even) indices.
@@ -213,60 +236,147 @@ __device__ __forceinline__ void rr_pair(int k, int t, int np, int &p, int &q) {
   if (p > q) { const int s = p; p = q; q = s; }
 }
 
-// M <- M J, V <- V J on column pairs until the columns of M = G V are orthogonal; then
-// G V = V diag(lambda) with lambda_k = v_k^T m_k.
+// One-sided (Hestenes) Jacobi on the Gram itself: M <- M J, V <- V J on column pairs
+// until the columns of M = G V are mutually orthogonal; then G V = V diag(lambda) with
+// lambda_k = v_k^T m_k.  Round-robin ordering (pair table precomputed in shared memory);
+// each pair of a round is owned by a group of kL lanes (8 for np <= 64, so a warp handles
+// 4 pairs and the dot product needs 3 shuffle levels); one CTA barrier per round.  The
+// squared column norms a_k are carried from round to round with the exact update
+// a_p' = a_p - t g, a_q' = a_q + t g and recomputed at every sweep start (dgesvj
+// practice), so a round reduces only g = m_p.m_q.  A pair is skipped when
+// g^2 <= tol^2 a_p a_q (relative test; tol ~ sqrt(n) eps, just above the rounding of g, so
+// the angle left between converged columns is <= tol lambda_q / lambda_p).
+template <int kL, bool kSmem>
 __global__ void __launch_bounds__(kEigT) jacobi_kernel(const double *__restrict__ Ain, int n, double *__restrict__ w,
                                                        double *__restrict__ Vout, double *__restrict__ gws,
                                                        double tol, int max_sweeps, int *__restrict__ info) {
   extern __shared__ double esm[];
   const int np = n + (n & 1);
-  double *M = gws ? gws : esm;                // np x np, column-major
-  double *V = M + (size_t)np * np;
-  double *lam = V + (size_t)np * np;          // np
+  double *__restrict__ M = kSmem ? esm : gws;   // np x np, column-major
+  double *__restrict__ V = M + (size_t)np * np;
+  double *__restrict__ lam = V + (size_t)np * np;  // np (column norms^2 during the sweeps)
+  short2 *ptab = reinterpret_cast<short2 *>(kSmem ? (lam + np) : esm);  // [(np-1) * np/2]
   __shared__ int sconv;
+  __shared__ double sfro[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int NW = kEigT / 32;
-
-  for (int e = tid; e < np * np; e += kEigT) {
-    const int i = e % np, j = e / np;
-    M[e] = (i < n && j < n) ? 0.5 * (Ain[i + n * j] + Ain[j + n * i]) : 0.0;
-    V[e] = (i == j) ? 1.0 : 0.0;
-  }
-  __syncthreads();
+  const int nthr = blockDim.x, nw = nthr >> 5;
+  constexpr int kGroups = 32 / kL;                 // pairs per warp
+  const int sub = lane / kL, gl = lane % kL;       // group within warp, lane within group
+  const unsigned gmask = (kL == 32) ? 0xffffffffu : (((1u << kL) - 1u) << (sub * kL));
   const int npairs = np / 2;
+
+  double fro = 0.0;
+  for (int e = tid; e < np * np; e += nthr) {
+    const int i = e % np, j = e / np;
+    const double v = (i < n && j < n) ? 0.5 * (Ain[i + (size_t)n * j] + Ain[j + (size_t)n * i]) : 0.0;
+    M[e] = v;
+    V[e] = (i == j) ? 1.0 : 0.0;
+    fro = fma(v, v, fro);
+  }
+  for (int e = tid; e < (np - 1) * npairs; e += nthr) {
+    int p, q;
+    rr_pair(e % npairs, e / npairs, np, p, q);
+    ptab[e] = make_short2((short)p, (short)q);
+  }
+  fro = warp_sum(fro);
+  if (lane == 0) sfro[warp] = fro;
+  __syncthreads();
+  double f2 = 0.0;
+  for (int k = 0; k < nw; ++k) f2 += sfro[k];
+  const double tol2 = tol * tol;
+  const int kstride = kGroups * nw;
   int sweeps = 0;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    // column norms^2 (fresh every sweep)
+    for (int k = warp; k < np; k += nw) {
+      double d = 0.0;
+      for (int r = lane; r < np; r += 32) { const double x = M[r + (size_t)np * k]; d = fma(x, x, d); }
+      d = warp_sum(d);
+      if (lane == 0) lam[k] = d;
+    }
     if (tid == 0) sconv = 1;
     __syncthreads();
     for (int t = 0; t < np - 1; ++t) {
-      for (int k = warp; k < npairs; k += NW) {
-        int p, q;
-        rr_pair(k, t, np, p, q);
-        double a = 0.0, b = 0.0, g = 0.0;
-        for (int r = lane; r < np; r += 32) {
-          const double mp = M[r + np * p], mq = M[r + np * q];
-          a = fma(mp, mp, a);
-          b = fma(mq, mq, b);
-          g = fma(mp, mq, g);
+      const short2 *row = ptab + t * npairs;
+      for (int k0 = warp * kGroups; k0 < npairs; k0 += kstride) {
+        const int k = k0 + sub;
+        const bool act = k < npairs;
+        const short2 pq = row[act ? k : 0];
+        const int p = pq.x, q = pq.y;
+        double *__restrict__ mp = M + (size_t)np * p;
+        double *__restrict__ mq = M + (size_t)np * q;
+        RT_EIG_PROBE(0);
+        constexpr int kR = (kL == 8) ? 8 : 1;   // rows per lane held in registers (np <= 64)
+        double xp[kR], xq[kR];
+        double g = 0.0;
+        if (kL == 8) {
+#pragma unroll
+          for (int u = 0; u < kR; ++u) {
+            const int r = gl + kL * u;
+            xp[u] = r < np ? mp[r] : 0.0;
+            xq[u] = r < np ? mq[r] : 0.0;
+          }
+          double pr[kR];
+#pragma unroll
+          for (int u = 0; u < kR; ++u) pr[u] = xp[u] * xq[u];   // independent products, then a tree
+#pragma unroll
+          for (int h = kR / 2; h; h >>= 1)
+#pragma unroll
+            for (int u = 0; u < h; ++u) pr[u] += pr[u + h];
+          g = pr[0];
+        } else {
+          for (int r = gl; r < np; r += kL) g = fma(mp[r], mq[r], g);
         }
-        a = warp_sum(a);
-        b = warp_sum(b);
-        g = warp_sum(g);
-        if (g == 0.0 || fabs(g) <= tol * sqrt(a * b)) continue;  // warp-uniform
-        if (lane == 0) sconv = 0;
-        const double zeta = (b - a) / (2.0 * g);
-        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double c = rsqrt(1.0 + tt * tt), s = tt * c;
-        for (int r = lane; r < np; r += 32) {
-          const double mp = M[r + np * p], mq = M[r + np * q];
-          M[r + np * p] = c * mp - s * mq;
-          M[r + np * q] = s * mp + c * mq;
-          const double vp = V[r + np * p], vq = V[r + np * q];
-          V[r + np * p] = c * vp - s * vq;
-          V[r + np * q] = s * vp + c * vq;
+#pragma unroll
+        for (int o = kL / 2; o; o >>= 1) g += __shfl_xor_sync(gmask, g, o, kL);
+        const double a = lam[p], b = lam[q];
+        const bool rot = act && g != 0.0 && g * g > tol2 * a * b;
+        RT_EIG_PROBE(1);
+        if (rot) {  // group-uniform
+          if (gl == 0) sconv = 0;
+          const double zeta = (b - a) / (2.0 * g);
+          const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double c = rsqrt(fma(tt, tt, 1.0)), s = tt * c;
+          RT_EIG_PROBE(2);
+          double *__restrict__ vp = V + (size_t)np * p;
+          double *__restrict__ vq = V + (size_t)np * q;
+          if (kL == 8) {
+            double yp[kR], yq[kR];
+#pragma unroll
+            for (int u = 0; u < kR; ++u) {
+              const int r = gl + kL * u;
+              yp[u] = r < np ? vp[r] : 0.0;
+              yq[u] = r < np ? vq[r] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kR; ++u) {
+              const int r = gl + kL * u;
+              if (r < np) {
+                mp[r] = c * xp[u] - s * xq[u];
+                mq[r] = s * xp[u] + c * xq[u];
+                vp[r] = c * yp[u] - s * yq[u];
+                vq[r] = s * yp[u] + c * yq[u];
+              }
+            }
+          } else {
+            for (int r = gl; r < np; r += kL) {
+              const double x = mp[r], y = mq[r];
+              const double u = vp[r], z = vq[r];
+              mp[r] = c * x - s * y;
+              mq[r] = s * x + c * y;
+              vp[r] = c * u - s * z;
+              vq[r] = s * u + c * z;
+            }
+          }
+          if (gl == 0) {  // exact for the exact angle; refreshed every sweep
+            lam[p] = a - tt * g;
+            lam[q] = b + tt * g;
+          }
+          RT_EIG_PROBE(3);
         }
       }
       __syncthreads();
+      RT_EIG_PROBE(4);
     }
     sweeps = sweep + 1;
     const int done = sconv;
@@ -275,15 +385,15 @@ __global__ void __launch_bounds__(kEigT) jacobi_kernel(const double *__restrict_
   }
   if (tid == 0 && info) *info = sweeps;
   // lambda_k = v_k^T m_k
-  for (int k = warp; k < np; k += NW) {
+  for (int k = warp; k < np; k += nw) {
     double d = 0.0;
-    for (int r = lane; r < np; r += 32) d = fma(V[r + np * k], M[r + np * k], d);
+    for (int r = lane; r < np; r += 32) d = fma(V[r + (size_t)np * k], M[r + (size_t)np * k], d);
     d = warp_sum(d);
     if (lane == 0) lam[k] = d;
   }
   __syncthreads();
   // sort descending (ties by index), drop the padding index
-  for (int i = tid; i < n; i += kEigT) {
+  for (int i = tid; i < n; i += nthr) {
     const double di = lam[i];
     int rank = 0;
     for (int j = 0; j < n; ++j) {
@@ -291,7 +401,7 @@ __global__ void __launch_bounds__(kEigT) jacobi_kernel(const double *__restrict_
       if (dj > di || (dj == di && j < i)) ++rank;
     }
     w[rank] = di;
-    for (int r = 0; r < n; ++r) Vout[r + (int64_t)n * rank] = V[r + np * i];
+    for (int r = 0; r < n; ++r) Vout[r + (int64_t)n * rank] = V[r + (size_t)np * i];
   }
 }
 
@@ -350,7 +460,8 @@ void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
     if (n > kMaxN) break;
     if (forced > 0 && ncta != forced) continue;
     const int rows = (int)((m + ncta - 1) / ncta);
-    const size_t smem = sizeof(double) * ((size_t)2 * rows * n + 5 * kMaxN);
+    if (forced == 0 && rows > 256 && ncta < 16) continue;  // keep per-CTA slabs short (latency)
+    const size_t smem = sizeof(double) * ((size_t)2 * rows * n + (7 + 2 * kMaxCTA) * kMaxN);
     if (smem > 200 * 1024) continue;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ncta);
@@ -381,16 +492,21 @@ void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
 
 void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps) {
   const int np = n + (n & 1);
-  const size_t need = sizeof(double) * (2 * (size_t)np * np + np);
-  const double tol = 1e-15;
-  const int max_sweeps = 30;
-  DevBuf<double> ws;
+  const size_t tab = sizeof(short2) * (size_t)(np - 1) * (np / 2) + 16;
+  const size_t need = sizeof(double) * (2 * (size_t)np * np + np) + tab;
+  const double tol = 3e-15 * std::sqrt((double)n);
+  const int max_sweeps = 40;
+  const int thr = np <= 64 ? std::max(64, ((np / 2) * 8 + 31) / 32 * 32) : kEigT;
   if (need <= 200 * 1024) {
-    RT_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
-    RT_LAUNCH(c, jacobi_kernel, 1, kEigT, need, A, n, w, V, (double *)nullptr, tol, max_sweeps, sweeps);
-  } else {
-    ws.alloc(c, need / sizeof(double) + 1);
-    RT_LAUNCH(c, jacobi_kernel, 1, kEigT, 0, A, n, w, V, ws.p, tol, max_sweeps, sweeps);
+#define RT_EIG(KL)                                                                                   \
+  RT_CUDA(cudaFuncSetAttribute(jacobi_kernel<KL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need)); \
+  RT_LAUNCH(c, (jacobi_kernel<KL, true>), 1, thr, need, A, n, w, V, (double *)nullptr, tol, max_sweeps, sweeps)
+    if (np <= 64) { RT_EIG(8); } else { RT_EIG(32); }
+#undef RT_EIG
+  } else {  // matrices and vectors in global memory, pair table in shared memory
+    DevBuf<double> ws(c, 2 * (size_t)np * np + np);
+    RT_CUDA(cudaFuncSetAttribute(jacobi_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab));
+    RT_LAUNCH(c, (jacobi_kernel<32, false>), 1, kEigT, tab, A, n, w, V, ws.p, tol, max_sweeps, sweeps);
   }
 }
 

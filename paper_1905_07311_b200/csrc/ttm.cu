@@ -143,15 +143,19 @@ __global__ void __launch_bounds__(kThreads) ttm_simt_kernel(
   }
 }
 
-// gram[j1 + J*j2] = sum_b partial[b][j1*JP + j2] (fixed order)
+// gram[j1 + J*j2] = sum_b partial[b][j1*JP + j2]: one CTA per entry, fixed-shape tree
+// (deterministic).
 __global__ void gram_reduce_kernel(const double *__restrict__ partial, int nblk, int JP, int J,
                                    double *__restrict__ gram) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < J * J; e += gridDim.x * blockDim.x) {
-    const int j1 = e % J, j2 = e / J;
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += partial[(int64_t)b * JP * JP + j1 * JP + j2];
-    gram[e] = s;
-  }
+  __shared__ double sred[4];
+  const int e = blockIdx.x;
+  const int j1 = e % J, j2 = e / J;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) s += partial[(int64_t)b * JP * JP + j1 * JP + j2];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) gram[e] = (sred[0] + sred[1]) + (sred[2] + sred[3]);
 }
 
 template <typename Tin, typename Tout, typename Tmul, int JP>
@@ -176,7 +180,7 @@ void launch_ttm(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t lda, 
   else if (out) RT_TTM_CASE(true, false);
   else RT_TTM_CASE(false, true);
 #undef RT_TTM_CASE
-  if (gram) RT_LAUNCH(c, gram_reduce_kernel, ceil_div((int64_t)J * J, 256), 256, 0, part.p, nblk, JP, J, gram);
+  if (gram) RT_LAUNCH(c, gram_reduce_kernel, J * J, 128, 0, part.p, nblk, JP, J, gram);
 }
 
 // Gram of the mode-n unfolding of a (stored) tensor B with mode size J:

@@ -24,6 +24,7 @@ STRICT = 1 << 0
 ACCUM_AUTO = 0 << 1
 ACCUM_FP64 = 1 << 1
 ACCUM_FAST = 2 << 1
+ACCUM_HYBRID = 3 << 1
 ADAPT_NO_TRUNCATE = 1 << 3
 ADAPT_HOSVD = 1 << 4
 RESULT_HOST = 1 << 5

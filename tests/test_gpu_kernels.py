@@ -123,3 +123,19 @@ def test_sym_eig(ctx, n):
     assert np.all(np.diff(w) <= 0)
     assert np.linalg.norm(v.T @ v - np.eye(n)) <= 1e-13 * n
     assert np.linalg.norm(a @ v - v * w[None, :]) <= 1e-14 * n
+
+
+@pytest.mark.parametrize("shape,ell,k0", [((800, 800, 40), 60, 0), ((800, 300, 7), 10, 0), ((96, 1001, 3), 64, 0),
+                                          ((800, 200, 11), 5, 10), ((128, 64, 8), 33, 4)])
+def test_sketch_tc_mode1(ctx, shape, ell, k0):
+    """Mode-1 fp32 sketch (the tcgen05 3xTF32 path: L == 1, I % 4 == 0) against the fp64
+    oracle product on the same fp32 bits, incl. ragged column counts and block offsets k0.
+    Tolerance: fp32 accumulation in TMEM over a CTA's column range (a few hundred to a few
+    thousand terms, relative error ~ sqrt(K) u32) -> 1e-5 relative."""
+    rng = np.random.default_rng(sum(shape) + ell)
+    x = np.asfortranarray(rng.standard_normal(shape).astype(np.float32))
+    got = ctx.debug_sketch(x, x.shape, 0, ell, seed=5, k0=k0)
+    ref = _sketch_ref(x, 0, ell, 5, k0=k0)
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    colerr = np.max(np.linalg.norm(got - ref, axis=0) / np.linalg.norm(ref, axis=0))
+    assert err <= 1e-5 and colerr <= 2e-5, (err, colerr)
