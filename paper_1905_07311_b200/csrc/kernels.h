@@ -31,6 +31,8 @@ void sketch_dense(Ctx &c, const void *X, DT in, ModeView v, int mode, int ell, i
 bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0, uint64_t seed,
                   int64_t col_offset, double *Y, double *normsq);
 bool sketch_tc_enabled();
+// bpass_tc.cu: B = Q^T X_(n) (B[k + ell c]) for fp32 X with L == 1 on tcgen05 (3xTF32).
+bool bpass_tc_mn(Ctx &c, const float *X, ModeView v, const double *Q, int64_t ldq, int ell, void *B, bool out_f64);
 
 // Generates Omega rows for given columns (debug / parity).
 void omega_rows(Ctx &c, DT out, uint64_t seed, int mode, const int64_t *cols, int64_t n,

@@ -5,15 +5,18 @@
 // from HBM.
 //
 // Layout of one CTA (persistent, one per SM, split-K over the unfolding columns c):
-//   warp 0      TMA producer: per stage, boxes of 256 rows x 8 columns of X into a staging
-//               buffer (plain row-major [c][i] tiles)
-//   warp 1      TMEM allocation + MMA issuer (one elected thread)
-//   warps 2-9   workers: split X = hi + lo (hi = tf32 truncation, lo = X - hi exact) and
-//               write both TRANSPOSED into K-major operand tiles (the tensor core reads
-//               tf32 operands K-major only: an MN-major tf32 A measured as all-zero output
-//               on this B200, scripts/dbg/tc_probe.cu), generate Omega(c0:c0+8, k0:k0+N)
-//               with Philox4x32-10 + Box-Muller (fp32, DESIGN reading R3) as hi/lo K-major
-//               tiles, accumulate ||X||^2; after the last stage: TMEM -> fp64 partial Y.
+//   warp 0       TMA producer: per stage, nbox boxes of BR rows x 8 columns of X into a
+//                staging buffer (plain [c][i] tiles), NSS stages deep
+//   warp 1       TMEM allocation + MMA issuer (one elected thread)
+//   warps 2-5    Omega generators: Omega(c0:c0+8, k0:k0+N) with Philox4x32-10 + Box-Muller
+//                (fp32, DESIGN reading R3), one Philox block per thread and stage, split into
+//                hi/lo tf32 K-major tiles (NSG stages deep, so the long RNG dependency chain
+//                runs ahead of the X pipeline)
+//   warps 6-13   X workers: split X = hi + lo (hi = tf32 truncation, lo = X - hi exact) and
+//                write both TRANSPOSED into K-major operand tiles (the tensor core reads tf32
+//                operands K-major only: MN-major tf32 A or B measured as all-zero output on
+//                this B200, scripts/dbg/tc_probe.cu); accumulate ||X||^2; after the last
+//                stage: TMEM -> fp64 partial Y.
 //   The accumulator of M-tile mt (rows 128 mt ..) lives in TMEM columns [mt N, mt N + N):
 //   3 MMAs per M-tile and stage, D += Xhi*Ohi + Xhi*Olo + Xlo*Ohi (M=128, N, K=8), fp32
 //   accumulation in TMEM (BASELINE "3xTF32"; the dropped Xlo*Olo term is 2^-22 relative).
@@ -31,15 +34,17 @@ namespace rt {
 namespace {
 
 constexpr int kBK = 8;               // unfolding columns per stage (= MMA K for tf32)
-constexpr int kWorkers = 8;          // worker warps
-constexpr int kThreads = 32 * (2 + kWorkers);
+constexpr int kGen = 4;              // Omega generator warps
+constexpr int kWorkers = 8;          // X worker warps
+constexpr int kThreads = 32 * (2 + kGen + kWorkers);
+constexpr int kNSG = 4;              // Omega stages
 
 struct SketchTcParams {
   int64_t I, C;          // rows, unfolding columns
   int64_t cps;           // columns per CTA (multiple of kBK)
   int NT;                // M-tiles of 128 rows
   int nbox, BR;          // TMA boxes per stage and rows per box (nbox * BR >= I, BR <= 256)
-  int NSS, NSO;          // staging stages (TMA depth), operand stages
+  int NSS, NSO;          // staging stages (TMA depth), X operand stages
   int ell;               // valid sketch columns (<= N)
   int64_t k0;            // first global sketch column
   uint64_t seed;
@@ -63,17 +68,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int NT = p.NT, NSS = p.NSS, NSO = p.NSO;
   const int sbytes = p.nbox * p.BR * kBK * 4;      // staging (raw X) per stage
   const int abytes = NT * 128 * kBK * 4;           // one operand plane (all M-tiles)
-  const int obytes = N * kBK * 4;                  // one Omega tile
+  constexpr int obytes = N * kBK * 4;              // one Omega tile
   unsigned char *hb = base;                        // [NSO][abytes]  X hi (K-major)
   unsigned char *lb = hb + (size_t)NSO * abytes;   // [NSO][abytes]  X lo
-  unsigned char *ohb = lb + (size_t)NSO * abytes;  // [NSO][obytes]
-  unsigned char *olb = ohb + (size_t)NSO * obytes; // [NSO][obytes]
-  unsigned char *sb = olb + (size_t)NSO * obytes;  // [NSS][sbytes]
+  unsigned char *ohb = lb + (size_t)NSO * abytes;  // [kNSG][obytes]
+  unsigned char *olb = ohb + (size_t)kNSG * obytes;// [kNSG][obytes]
+  unsigned char *sb = olb + (size_t)kNSG * obytes; // [NSS][sbytes]
   uint64_t *full = (uint64_t *)(sb + (size_t)NSS * sbytes);
   uint64_t *sfree = full + NSS;
-  uint64_t *ready = sfree + NSS;
-  uint64_t *empty = ready + NSO;
-  uint64_t *done = empty + NSO;
+  uint64_t *xready = sfree + NSS;
+  uint64_t *xempty = xready + NSO;
+  uint64_t *oready = xempty + NSO;
+  uint64_t *oempty = oready + kNSG;
+  uint64_t *done = oempty + kNSG;
   uint32_t *tslot = (uint32_t *)(done + 1);
   double *wsum = (double *)(tslot + 2);            // [kWorkers]
 
@@ -89,15 +96,19 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_init(&sfree[s], 32 * kWorkers);
     }
     for (int s = 0; s < NSO; ++s) {
-      tc::mbar_init(&ready[s], 32 * kWorkers);
-      tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&xready[s], 32 * kWorkers);
+      tc::mbar_init(&xempty[s], 1);
+    }
+    for (int s = 0; s < kNSG; ++s) {
+      tc::mbar_init(&oready[s], 32 * kGen);
+      tc::mbar_init(&oempty[s], 1);
     }
     tc::mbar_init(done, 1);
     tc::fence_barrier_init();
   }
   if (warp == 1) tc::tmem_alloc(tslot, tcols);
   // Omega tiles: columns n >= ell stay zero for the whole kernel
-  for (int e = threadIdx.x; e < 2 * NSO * obytes / 4; e += kThreads) ((float *)ohb)[e] = 0.f;
+  for (int e = threadIdx.x; e < 2 * kNSG * obytes / 4; e += kThreads) ((float *)ohb)[e] = 0.f;
   tc::fence_proxy_async_smem();
   tc::tc_fence_before();
   __syncthreads();
@@ -124,13 +135,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0 && nst > 0) {
       constexpr uint32_t idesc = tc::idesc_tf32(128, N, false, false);
       for (int it = 0; it < nst; ++it) {
-        const int s = it % NSO;
-        tc::mbar_wait(&ready[s], (it / NSO) & 1);
+        const int s = it % NSO, g = it % kNSG;
+        tc::mbar_wait(&oready[g], (it / kNSG) & 1);
+        tc::mbar_wait(&xready[s], (it / NSO) & 1);
         tc::tc_fence_after();
         const uint32_t ha = tc::smem_u32(hb + (size_t)s * abytes);
         const uint32_t la = tc::smem_u32(lb + (size_t)s * abytes);
-        const uint64_t bh = tc::smem_desc(tc::smem_u32(ohb + (size_t)s * obytes), 128, 256, tc::kSwNone);
-        const uint64_t bl = tc::smem_desc(tc::smem_u32(olb + (size_t)s * obytes), 128, 256, tc::kSwNone);
+        const uint64_t bh = tc::smem_desc(tc::smem_u32(ohb + (size_t)g * obytes), 128, 256, tc::kSwNone);
+        const uint64_t bl = tc::smem_desc(tc::smem_u32(olb + (size_t)g * obytes), 128, 256, tc::kSwNone);
         for (int mt = 0; mt < NT; ++mt) {
           const uint64_t ah = tc::smem_desc(ha + mt * 128 * kBK * 4, 128, 256, tc::kSwNone);
           const uint64_t al = tc::smem_desc(la + mt * 128 * kBK * 4, 128, 256, tc::kSwNone);
@@ -139,25 +151,22 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc::mma_tf32(d, ah, bl, idesc, 1u);
           tc::mma_tf32(d, al, bh, idesc, 1u);
         }
-        tc::mma_commit(&empty[s]);
+        tc::mma_commit(&xempty[s]);
+        tc::mma_commit(&oempty[g]);
       }
       tc::mma_commit(done);
     }
-  } else {
-    // ------------------------------------------------------------- workers
-    const int wt = threadIdx.x - 64;  // 0 .. 32*kWorkers-1
+  } else if (warp < 2 + kGen) {
+    // ------------------------------------------------------------- Omega generators
+    const int gt = threadIdx.x - 64;  // 0 .. 32*kGen-1
     const int64_t jb0 = p.k0 >> 2;
     const int nb = (int)(((p.k0 + p.ell - 1) >> 2) - jb0 + 1);
-    const int rows_st = min(NT * 128, p.nbox * p.BR);  // operand rows filled from staging
-    double nsq = 0.0;
     for (int it = 0; it < nst; ++it) {
-      const int so = it % NSO, ss = it % NSS;
+      const int g = it % kNSG;
       const int64_t c0 = cbeg + (int64_t)it * kBK;
-      // the MMAs of this operand slot's previous use must have finished reading it
-      if (it >= NSO) tc::mbar_wait(&empty[so], ((it / NSO) & 1) ^ 1);
-      // Omega(c0 .. c0+7, k0 .. k0+ell) -> hi/lo K-major tiles (rows n, K = c)
-      float *oh = (float *)(ohb + (size_t)so * obytes), *ol = (float *)(olb + (size_t)so * obytes);
-      for (int t = wt; t < kBK * nb; t += 32 * kWorkers) {
+      if (it >= kNSG) tc::mbar_wait(&oempty[g], ((it / kNSG) & 1) ^ 1);
+      float *oh = (float *)(ohb + (size_t)g * obytes), *ol = (float *)(olb + (size_t)g * obytes);
+      for (int t = gt; t < kBK * nb; t += 32 * kGen) {
         const int kk = t & (kBK - 1), jb = t >> 3;
         const int64_t c = c0 + kk;
         const bool valid = c < cend;
@@ -175,6 +184,18 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
+      tc::fence_proxy_async_smem();
+      tc::mbar_arrive(&oready[g]);
+    }
+  } else {
+    // ------------------------------------------------------------- X workers
+    const int wt = threadIdx.x - 32 * (2 + kGen);  // 0 .. 32*kWorkers-1
+    const int rows_st = min(NT * 128, p.nbox * p.BR);  // operand rows filled from staging
+    double nsq = 0.0;
+    for (int it = 0; it < nst; ++it) {
+      const int so = it % NSO, ss = it % NSS;
+      // the MMAs of this operand slot's previous use must have finished reading it
+      if (it >= NSO) tc::mbar_wait(&xempty[so], ((it / NSO) & 1) ^ 1);
       // X staging [box][c][BR rows] -> hi / lo K-major tiles (rows i, K = c); rows >= I are
       // zero-filled by the TMA, rows beyond the staging extent are never read by a valid D row
       tc::mbar_wait(&full[ss], (it / NSS) & 1);
@@ -185,30 +206,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       while (r >= p.BR) { r -= p.BR; ++box; }
       for (int i = wt; i < rows_st; i += 32 * kWorkers) {
         const float *src = st + box * (p.BR * kBK) + r;
+        float x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = src[u * p.BR];
 #pragma unroll
         for (int cq = 0; cq < 2; ++cq) {
-          float x[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) x[u] = src[(4 * cq + u) * p.BR];
           float4 h, l;
-          h.x = tc::tf32_hi(x[0]); h.y = tc::tf32_hi(x[1]); h.z = tc::tf32_hi(x[2]); h.w = tc::tf32_hi(x[3]);
-          l.x = x[0] - h.x; l.y = x[1] - h.y; l.z = x[2] - h.z; l.w = x[3] - h.w;
+          h.x = tc::tf32_hi(x[4 * cq]); h.y = tc::tf32_hi(x[4 * cq + 1]);
+          h.z = tc::tf32_hi(x[4 * cq + 2]); h.w = tc::tf32_hi(x[4 * cq + 3]);
+          l.x = x[4 * cq] - h.x; l.y = x[4 * cq + 1] - h.y; l.z = x[4 * cq + 2] - h.z; l.w = x[4 * cq + 3] - h.w;
           const int off = (i >> 3) * 256 + cq * 128 + (i & 7) * 16;
           *(float4 *)(hs + off) = h;
           *(float4 *)(ls + off) = l;
-          acc = fmaf(x[0], x[0], fmaf(x[1], x[1], fmaf(x[2], x[2], fmaf(x[3], x[3], acc))));
         }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = fmaf(x[u], x[u], acc);
         r += 32 * kWorkers;
         while (r >= p.BR) { r -= p.BR; ++box; }
       }
       nsq += (double)acc;
       tc::mbar_arrive(&sfree[ss]);       // staging slot may be refilled
       tc::fence_proxy_async_smem();
-      tc::mbar_arrive(&ready[so]);
+      tc::mbar_arrive(&xready[so]);
     }
     // ---- epilogue: TMEM -> fp64 partial[blockIdx.x][k * I + i]
-    const int q4 = warp & 3;              // TMEM lane quadrant of this warp
-    const int half = (warp - 2) >> 2;     // 0 / 1: which 32 of the N columns
+    const int q4 = warp & 3;                       // TMEM lane quadrant of this warp
+    const int half = (warp - 2 - kGen) >> 2;       // 0 / 1: which 32 of the N columns
     if (nst > 0) {
       tc::mbar_wait(done, 0);
       tc::tc_fence_after();
@@ -216,21 +239,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     double *dst = p.partial + (int64_t)blockIdx.x * p.ell * p.I;
     if (half * 32 < N) {
       for (int mt = 0; mt < NT; ++mt) {
-        uint32_t r[32];
-        if (nst > 0) tc::tmem_ld32(tmem + ((uint32_t)(32 * q4) << 16) + mt * N + half * 32, r);
+        uint32_t rr[32];
+        if (nst > 0) tc::tmem_ld32(tmem + ((uint32_t)(32 * q4) << 16) + mt * N + half * 32, rr);
         const int64_t i = (int64_t)mt * 128 + 32 * q4 + lane;
         if (i < p.I) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int k = half * 32 + j;
-            if (k < p.ell) dst[(int64_t)k * p.I + i] = nst > 0 ? (double)__uint_as_float(r[j]) : 0.0;
+            if (k < p.ell) dst[(int64_t)k * p.I + i] = nst > 0 ? (double)__uint_as_float(rr[j]) : 0.0;
           }
         }
       }
     }
     if (p.norm_partial) {
       for (int o = 16; o; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
-      if (lane == 0) wsum[warp - 2] = nsq;
+      if (lane == 0) wsum[warp - 2 - kGen] = nsq;
     }
   }
   tc::tc_fence_before();
@@ -276,6 +299,8 @@ void launch(Ctx &c, const CUtensorMap &tm, SketchTcParams &p, int grid, size_t s
 
 }  // namespace
 
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() { return encode_fn(); }
+
 bool sketch_tc_enabled() {
   static const bool off = getenv("RTUCKER_NO_TC") != nullptr;
   return !off;
@@ -301,7 +326,7 @@ bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t
                obytes = (size_t)N * kBK * 4;
   const size_t budget = 220 * 1024;
   p.NSO = 2;
-  const size_t fixed = 1024 + 2 * p.NSO * (abytes + obytes) + 512;
+  const size_t fixed = 1024 + 2 * p.NSO * abytes + 2 * kNSG * obytes + 512;
   if (fixed + 2 * sbytes > budget) return false;
   p.NSS = (int)std::min<size_t>(4, (budget - fixed) / sbytes);
   const size_t smem = fixed + p.NSS * sbytes;

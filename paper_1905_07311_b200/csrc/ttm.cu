@@ -280,9 +280,13 @@ void mode_gram(Ctx &c, const void *B, DT t, ModeView v, double *gram) {
   else mode_gram_t<float>(c, (const float *)B, v, gram);
 }
 
+bool ttm_dense_tc(Ctx &c, const void *X, DT in, ModeView v, const double *A, int64_t lda, int J, void *out, DT outT,
+                  bool mul_f64, double *gram);
+
 void ttm_dense(Ctx &c, const void *X, DT in, ModeView v, const double *A, int64_t lda, int J,
                void *out, DT outT, bool mul_f64, double *gram) {
   RT_REQUIRE(out || gram, "ttm: nothing to compute");
+  if (ttm_dense_tc(c, X, in, v, A, lda, J, out, outT, mul_f64, gram)) return;
   if (in == DT::F64) {
     RT_REQUIRE(outT == DT::F64, "ttm: fp64 input needs fp64 output");
     ttm_dispatch<double, double, double>(c, (const double *)X, v, A, lda, J, (double *)out, gram);
@@ -292,6 +296,15 @@ void ttm_dense(Ctx &c, const void *X, DT in, ModeView v, const double *A, int64_
   } else {
     ttm_dispatch<float, float, float>(c, (const float *)X, v, A, lda, J, (float *)out, gram);
   }
+}
+
+bool ttm_dense_tc(Ctx &c, const void *X, DT in, ModeView v, const double *A, int64_t lda, int J, void *out, DT outT,
+                  bool mul_f64, double *gram) {
+  // tensor-core B-pass (fp32 data, FAST products, mode with L == 1, B stored), Gram from B
+  if (in != DT::F32 || mul_f64 || !out || v.L != 1) return false;
+  if (!bpass_tc_mn(c, (const float *)X, v, A, lda, J, out, outT == DT::F64)) return false;
+  if (gram) mode_gram(c, out, outT, ModeView{1, J, v.R}, gram);
+  return true;
 }
 
 }  // namespace rt

@@ -4,8 +4,9 @@
 #include <cstdint>
 #include "../../paper_1905_07311_b200/csrc/tc.cuh"
 using namespace rt;
-__global__ void probe(const float *A, const float *B, float *D, int mode) {
-  __shared__ __align__(1024) unsigned char sa[4096];
+__global__ void probe(const float *A, const float *B, float *D, int mode, int var) {
+  extern __shared__ __align__(1024) unsigned char dyn[];
+  unsigned char *sa = dyn + ((1024u - ((uint32_t)__cvta_generic_to_shared(dyn) & 1023u)) & 1023u);
   __shared__ __align__(1024) unsigned char sb[1024];
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
@@ -34,6 +35,49 @@ __global__ void probe(const float *A, const float *B, float *D, int mode) {
     int n = idx % 32, k = idx / 32;
     *(float *)(sb + (n / 8) * 256 + (k / 4) * 128 + (n % 8) * 16 + (k % 4) * 4) = B[n + 32 * k];
   }
+  if (mode == 9) {  // B MN-major no swizzle: (n/4)*128 + k*16 + (n%4)*4
+    for (int idx = t; idx < 32 * 8; idx += blockDim.x) {
+      int n = idx % 32, k = idx / 32;
+      *(float *)(sb + (n / 4) * 128 + k * 16 + (n % 4) * 4) = B[n + 32 * k];
+    }
+  }
+  if (mode == 10) {  // B MN-major SW128 atom: row k (128 B) holds n 0..31, chunk j = n/4 swizzled
+    for (int idx = t; idx < 32 * 8; idx += blockDim.x) {
+      int n = idx % 32, k = idx / 32;
+      *(float *)(sb + k * 128 + (((n / 4) ^ (k % 8)) * 16) + (n % 4) * 4) = B[n + 32 * k];
+    }
+  }
+  if (mode >= 9) {  // A K-major no swizzle
+    for (int idx = t; idx < 128 * 8; idx += blockDim.x) {
+      int m = idx % 128, k = idx / 128;
+      *(float *)(sa + (m / 8) * 256 + (k / 4) * 128 + (m % 8) * 16 + (k % 4) * 4) = A[m + 128 * k];
+    }
+  }
+  for (int idx = t; idx < 190 * 1024 / 4; idx += blockDim.x) ((float *)sa)[idx] = 0.f;
+  __syncthreads();
+  if (mode == 13 && var < 2) {  // A K-major SW128, K slice 0
+    for (int idx = t; idx < 128 * 32; idx += blockDim.x) {
+      int m = idx % 128, k = idx / 128;
+      float v = (k < 8) ? A[m + 128 * k] : 1e30f;
+      *(float *)(sa + m * 128 + (((k / 4) ^ (m % 8)) * 16) + (k % 4) * 4) = v;
+    }
+  }
+  if (mode == 13 && var >= 2) {  // A K-major SW32: row m = 32 B, chunk j ^ ((m >> 2) & 1)
+    for (int idx = t; idx < 128 * 8; idx += blockDim.x) {
+      int m = idx % 128, k = idx / 128;
+      *(float *)(sa + m * 32 + (((k / 4) ^ ((m >> 2) & 1)) * 16) + (k % 4) * 4) = A[m + 128 * k];
+    }
+  }
+  if (mode == 11 || mode == 12) {  // A K-major SW128: row m = 128 B (32 k), chunk j ^ (m % 8); K slice 1 = k 8..15
+    for (int idx = t; idx < 128 * 32; idx += blockDim.x) {
+      int m = idx % 128, k = idx / 128;
+      float v = (k >= 8 && k < 16) ? A[m + 128 * (k - 8)] : 1e30f;
+      if (mode == 12) v = (k == 8) ? 1.0f + 0x1p-11f + 0x1p-13f : 0.f;
+      *(float *)(sa + m * 128 + (((k / 4) ^ (m % 8)) * 16) + (k % 4) * 4) = v;
+    }
+    if (mode == 12) for (int idx = t; idx < 32 * 8; idx += blockDim.x) { int n = idx % 32, k = idx / 32;
+      *(float *)(sb + (n / 8) * 256 + (k / 4) * 128 + (n % 8) * 16 + (k % 4) * 4) = (k == 0) ? 1.f : 0.f; }
+  }
   if (t == 0) { tc::mbar_init(&bar, 1); tc::fence_barrier_init(); }
   if (warp == 0) tc::tmem_alloc(&slot, 64);
   tc::fence_proxy_async_smem();
@@ -50,7 +94,23 @@ __global__ void probe(const float *A, const float *B, float *D, int mode) {
     if (mode == 5) ad = tc::smem_desc(tc::smem_u32(sa), 1024, 128, tc::kSwNone);
     if (mode == 6) ad = tc::smem_desc(tc::smem_u32(sa), 128, 1024, tc::kSwNone);
     if (mode == 7) ad = tc::smem_desc(tc::smem_u32(sa), 1024, 1024, tc::kSw128);
-    if (mode != 3 && mode != 8) tc::mma_tf32(tm, ad, bd, tc::idesc_tf32(128, 32, mode != 4, false), 0);
+    if (mode >= 9) {
+      ad = tc::smem_desc(tc::smem_u32(sa), 128, 256, tc::kSwNone);
+      bd = mode == 9 ? tc::smem_desc(tc::smem_u32(sb), 1024, 128, tc::kSwNone) : tc::smem_desc(tc::smem_u32(sb), 1024, 1024, tc::kSw128);
+      tc::mma_tf32(tm, ad, bd, tc::idesc_tf32(128, 32, false, true), 0);
+    }
+    if (mode == 13) {
+      if (var == 0) ad = tc::smem_desc(tc::smem_u32(sa), 16, 1024, tc::kSw128);
+      if (var == 1) ad = tc::smem_desc(tc::smem_u32(sa), 0, 1024, tc::kSw128);
+      if (var == 2) ad = tc::smem_desc(tc::smem_u32(sa), 16, 256, tc::kSw32);
+      if (var == 3) ad = tc::smem_desc(tc::smem_u32(sa), 0, 256, tc::kSw32);
+      tc::mma_tf32(tm, ad, bd, tc::idesc_tf32(128, 32, false, false), 0);
+    }
+    if (mode == 11 || mode == 12) {
+      ad = tc::smem_desc(tc::smem_u32(sa) + 32, 16, 1024, tc::kSw128);
+      tc::mma_tf32(tm, ad, bd, tc::idesc_tf32(128, 32, false, false), 0);
+    }
+    if (mode != 3 && mode != 8 && mode < 9 && mode != 13) tc::mma_tf32(tm, ad, bd, tc::idesc_tf32(128, 32, mode != 4, false), 0);
     tc::mma_commit(&bar);
   }
   if (mode == 8) {
@@ -86,20 +146,22 @@ __global__ void probe(const float *A, const float *B, float *D, int mode) {
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tm, 64);
 }
-int main() {
+int main(int argc, char **argv) {
   float hA[128 * 8], hB[32 * 8], hD[128 * 32], ref[128 * 32];
   for (int i = 0; i < 128 * 8; ++i) hA[i] = (float)((i * 7) % 13) - 6.f;
   for (int i = 0; i < 32 * 8; ++i) hB[i] = (float)((i * 5) % 11) - 5.f;
   for (int m = 0; m < 128; ++m) for (int n = 0; n < 32; ++n) { double s = 0; for (int k = 0; k < 8; ++k) s += hA[m + 128 * k] * hB[n + 32 * k]; ref[m + 128 * n] = s; }
   float *A, *B, *D; cudaMalloc(&A, sizeof hA); cudaMalloc(&B, sizeof hB); cudaMalloc(&D, sizeof hD);
   cudaMemcpy(A, hA, sizeof hA, cudaMemcpyHostToDevice); cudaMemcpy(B, hB, sizeof hB, cudaMemcpyHostToDevice);
-  for (int mode = 4; mode < 9; mode += 4) {
+  for (int mode = atoi(argv[1]); mode <= atoi(argv[1]); ++mode) {
     cudaMemset(D, 0, sizeof hD);
-    probe<<<1, 128>>>(A, B, D, mode);
+    cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    probe<<<1, 128, 200 * 1024>>>(A, B, D, mode, argc > 2 ? atoi(argv[2]) : 0);
     cudaError_t e = cudaDeviceSynchronize();
     cudaMemcpy(hD, D, sizeof hD, cudaMemcpyDeviceToHost);
     double maxerr = 0, maxref = 0; int bad = 0;
     for (int i = 0; i < 128 * 32; ++i) { double d = fabs(hD[i] - ref[i]); if (d > maxerr) maxerr = d; if (fabs(ref[i]) > maxref) maxref = fabs(ref[i]); if (d > 1e-3) ++bad; }
+    if (mode == 12) { printf("trunc test: D[0]=%.9g (1=truncation, %.9g=round-nearest)\n", hD[0], 1.0 + 1.0 / 1024); continue; }
     printf("mode %d err=%s maxerr=%g maxref=%g bad=%d  D[0..3]=%g %g %g %g ref=%g %g %g %g D[128]=%g ref=%g\n", mode, cudaGetErrorString(e), maxerr, maxref, bad,
            hD[0], hD[1], hD[2], hD[3], ref[0], ref[1], ref[2], ref[3], hD[128], ref[128]);
   }
