@@ -113,12 +113,12 @@ __global__ void __launch_bounds__(kQRT) qr_cluster_kernel(const double *__restri
     }
     if (tid == 0) beta[j] = b;
     if (b != 0.0) {
-      const int nr = nloc - i0, nc = n - j - 1;
-      for (int e = tid; e < nr * nc; e += kQRT) {
-        const int i = i0 + e % nr, c = j + 1 + e / nr;
+      for (int c = j + 1 + warp; c < n; c += kNW) {      // warp per column, lanes over rows
         const double f = b * (tot[2 * c] + (v0 - alpha) * tot[2 * c + 1]);  // beta v^T w_c
-        const double vi = (i == jl) ? v0 : W[i + rows * j];
-        W[i + rows * c] -= f * vi;
+        for (int i = i0 + lane; i < nloc; i += 32) {
+          const double vi = (i == jl) ? v0 : W[i + rows * j];
+          W[i + rows * c] -= f * vi;
+        }
       }
     }
     if (owner && tid == 0) W[jl + rows * j] = v0;  // store v in place (v_j = v0)
@@ -146,10 +146,9 @@ __global__ void __launch_bounds__(kQRT) qr_cluster_kernel(const double *__restri
     }
     cl.sync();
     cluster_allsum(cl, buf, gat, tot, j, n, ncta);
-    const int nr = nloc - i0, nc = n - j;
-    for (int e = tid; e < nr * nc; e += kQRT) {
-      const int i = i0 + e % nr, c = j + e / nr;
-      Qs[i + rows * c] -= b * tot[c] * W[i + rows * j];
+    for (int c = j + warp; c < n; c += kNW) {
+      const double f = b * tot[c];
+      for (int i = i0 + lane; i < nloc; i += 32) Qs[i + rows * c] -= f * W[i + rows * j];
     }
     __syncthreads();
   }
@@ -225,6 +224,7 @@ __global__ void __launch_bounds__(kQRG) qr_global_kernel(double *__restrict__ W,
 // ------------------------------------------------------- one-sided Jacobi eig -------
 #ifndef RT_EIG_PROBE
 #define RT_EIG_PROBE(k)
+#define RT_EIG_PROBE_INIT()
 #endif
 constexpr int kEigT = 1024;
 
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kEigT) jacobi_kernel(const double *__restrict_
   double *__restrict__ M = kSmem ? esm : gws;   // np x np, column-major
   double *__restrict__ V = M + (size_t)np * np;
   double *__restrict__ lam = V + (size_t)np * np;  // np (column norms^2 during the sweeps)
-  short2 *ptab = reinterpret_cast<short2 *>(kSmem ? (lam + np) : esm);  // [(np-1) * np/2]
+  short2 *ptab = reinterpret_cast<short2 *>(lam + np);  // [(np-1) * np/2], shared-memory variant only
   __shared__ int sconv;
   __shared__ double sfro[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -264,6 +264,7 @@ __global__ void __launch_bounds__(kEigT) jacobi_kernel(const double *__restrict_
   const int sub = lane / kL, gl = lane % kL;       // group within warp, lane within group
   const unsigned gmask = (kL == 32) ? 0xffffffffu : (((1u << kL) - 1u) << (sub * kL));
   const int npairs = np / 2;
+  RT_EIG_PROBE_INIT();
 
   double fro = 0.0;
   for (int e = tid; e < np * np; e += nthr) {
@@ -273,11 +274,12 @@ __global__ void __launch_bounds__(kEigT) jacobi_kernel(const double *__restrict_
     V[e] = (i == j) ? 1.0 : 0.0;
     fro = fma(v, v, fro);
   }
-  for (int e = tid; e < (np - 1) * npairs; e += nthr) {
-    int p, q;
-    rr_pair(e % npairs, e / npairs, np, p, q);
-    ptab[e] = make_short2((short)p, (short)q);
-  }
+  if (kSmem)
+    for (int e = tid; e < (np - 1) * npairs; e += nthr) {
+      int p, q;
+      rr_pair(e % npairs, e / npairs, np, p, q);
+      ptab[e] = make_short2((short)p, (short)q);
+    }
   fro = warp_sum(fro);
   if (lane == 0) sfro[warp] = fro;
   __syncthreads();
@@ -301,8 +303,14 @@ __global__ void __launch_bounds__(kEigT) jacobi_kernel(const double *__restrict_
       for (int k0 = warp * kGroups; k0 < npairs; k0 += kstride) {
         const int k = k0 + sub;
         const bool act = k < npairs;
-        const short2 pq = row[act ? k : 0];
-        const int p = pq.x, q = pq.y;
+        int p, q;
+        if (kSmem) {
+          const short2 pq = row[act ? k : 0];
+          p = pq.x;
+          q = pq.y;
+        } else {
+          rr_pair(act ? k : 0, t, np, p, q);
+        }
         double *__restrict__ mp = M + (size_t)np * p;
         double *__restrict__ mq = M + (size_t)np * q;
         RT_EIG_PROBE(0);
@@ -503,10 +511,9 @@ void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps) 
   RT_LAUNCH(c, (jacobi_kernel<KL, true>), 1, thr, need, A, n, w, V, (double *)nullptr, tol, max_sweeps, sweeps)
     if (np <= 64) { RT_EIG(8); } else { RT_EIG(32); }
 #undef RT_EIG
-  } else {  // matrices and vectors in global memory, pair table in shared memory
+  } else {  // matrices and vectors in global memory, pairs computed on the fly
     DevBuf<double> ws(c, 2 * (size_t)np * np + np);
-    RT_CUDA(cudaFuncSetAttribute(jacobi_kernel<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab));
-    RT_LAUNCH(c, (jacobi_kernel<32, false>), 1, kEigT, tab, A, n, w, V, ws.p, tol, max_sweeps, sweeps);
+    RT_LAUNCH(c, (jacobi_kernel<32, false>), 1, kEigT, 0, A, n, w, V, ws.p, tol, max_sweeps, sweeps);
   }
 }
 

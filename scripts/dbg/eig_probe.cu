@@ -3,6 +3,7 @@
 __device__ long long g_probe[8];
 __shared__ long long s_probe[8];
 #define RT_EIG_PROBE(k) do { if (threadIdx.x == 0) { long long t_ = clock64(); if (k == 0) s_probe[7] = t_; else s_probe[k] += t_ - s_probe[7]; s_probe[7] = t_; if (k == 4) for (int i_ = 1; i_ < 5; ++i_) g_probe[i_] = s_probe[i_]; } } while (0)
+#define RT_EIG_PROBE_INIT() do { if (threadIdx.x < 8) s_probe[threadIdx.x] = 0; } while (0)
 #include "../../paper_1905_07311_b200/csrc/smallla.cu"
 #include <vector>
 #include <cmath>
