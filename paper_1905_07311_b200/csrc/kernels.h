@@ -76,7 +76,8 @@ struct CooDev {
   DT vt;
 };
 // Y (I_n x ell, fp64) = G_(n) Omega_n for a COO tensor.
-void sketch_coo(Ctx &c, const CooDev &g, int mode, int ell, uint64_t seed, double *Y);
+// normals_f64: fp64 Box-Muller normals (else fp32 normals; products and sums in fp64).
+void sketch_coo(Ctx &c, const CooDev &g, int mode, int ell, uint64_t seed, bool normals_f64, double *Y);
 // Strong-RRQR (CPQR + maxvol, eta) on Q (m x l): sel sorted (device int64), A (m x l).
 void srrqr(Ctx &c, const double *Q, int64_t m, int l, double eta, int64_t *sel, double *A,
            int *swaps_host);

@@ -1,0 +1,114 @@
+"""GPU parity of SP-STHOSVD (Alg 6; sRRQR per DESIGN reading R9) through the C ABI
+against the CPU oracle on the same COO inputs: selections S_j equal, core
+entries bit-exact copies of the input values, oblique factors A_j = Q (P^T Q)^-1 close
+(they do not depend on the QR basis), and Thm 5.1's structure (A_j[S_j,:] = I, |A| <= eta)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from workloads import superdiagonal, sparse_zipf
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1905_07311_b200.rtucker import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def _run(ctx, idx, vals, dims, ranks, p, seed=0, order=None, eta=2.0, device=True, flags=0):
+    import torch
+    from paper_1905_07311_b200.rtucker import RESULT_HOST
+    if device:
+        it = torch.as_tensor(np.ascontiguousarray(idx, dtype=np.int32), device="cuda")
+        vt = torch.as_tensor(np.ascontiguousarray(vals), device="cuda")
+        return ctx.sparse_sthosvd(it, vt, dims, ranks, p, seed, order, eta, flags | RESULT_HOST).numpy()
+    return ctx.sparse_sthosvd(np.ascontiguousarray(idx, dtype=np.int32), np.ascontiguousarray(vals), dims, ranks, p,
+                              seed, order, eta, flags | RESULT_HOST).numpy()
+
+
+def _check(g, o, eta, a_tol):
+    d = len(o.selections)
+    for j in range(d):
+        assert list(g.selections[j]) == list(o.selections[j]), (j, g.selections[j], o.selections[j])
+        a = g.factors[j]
+        np.testing.assert_allclose(a[np.asarray(o.selections[j])], np.eye(a.shape[1]), atol=1e-10)
+        assert np.max(np.abs(a)) <= eta * (1 + 1e-9)
+        err = np.linalg.norm(a - o.factors[j]) / np.linalg.norm(o.factors[j])
+        assert err <= a_tol, (j, err)
+    assert tuple(g.nnz_history) == tuple(o.nnz_history)
+    # core: same entries (bit-exact values), compare as sorted coordinate lists
+    gk = np.lexsort(g.core_idx[::-1])
+    ok = np.lexsort(o.core_idx[::-1])
+    np.testing.assert_array_equal(g.core_idx[:, gk], o.core_idx[:, ok])
+    np.testing.assert_array_equal(g.core_vals[gk], np.asarray(o.core_vals)[ok])
+
+
+def test_superdiagonal_spec_example(ctx):
+    """Superdiagonal 5^3 with (5,4,3,2,1), r=(2,2,2), p=2 -> the 4x4x4 leading sub-tensor."""
+    x = superdiagonal([5, 4, 3, 2, 1])
+    idx = np.array(np.nonzero(x))
+    vals = x[tuple(idx)]
+    g = _run(ctx, idx, vals, x.shape, (2, 2, 2), 2, seed=0)
+    o = O.sp_sthosvd(idx, vals, x.shape, (2, 2, 2), 2, seed=0)
+    _check(g, o, 2.0, 1e-10)
+    assert g.ranks == (4, 4, 4)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_zipf_small_scale(ctx, dtype):
+    """BASELINE configs[4] at 1/100 of the draws (Zipf(1.1) indices, 1+Poisson(2) counts)."""
+    idx, vals = sparse_zipf(ndraws=500_000)
+    vals = vals.astype(dtype)
+    dims = (8000, 8000, 200000, 1200)
+    g = _run(ctx, idx, vals, dims, (10, 10, 10, 10), 5, seed=0)
+    o = O.sp_sthosvd(idx, vals, dims, (10, 10, 10, 10), 5, seed=0)
+    # fp32 values -> fp32 normals on the GPU (fp64 products/sums), the oracle draws fp64
+    # normals: Y agrees to ~1e-7 relative, so A to ~1e-5
+    _check(g, o, 2.0, 1e-9 if dtype == np.float64 else 1e-4)
+    assert g.order == (2, 0, 1, 3)
+
+
+def test_host_input_order_and_eta(ctx):
+    rng = np.random.default_rng(3)
+    dims = (40, 30, 25)
+    n = 3000
+    idx = np.array([rng.integers(0, d_, n) for d_ in dims])
+    key = np.ravel_multi_index(idx, dims)
+    _, first = np.unique(key, return_index=True)
+    idx = idx[:, np.sort(first)]
+    vals = rng.random(idx.shape[1])
+    for order, eta in [((1, 2, 0), 2.0), ((0, 1, 2), 1.1)]:
+        g = _run(ctx, idx, vals, dims, (4, 3, 5), 3, seed=7, order=order, eta=eta, device=False)
+        o = O.sp_sthosvd(idx, vals, dims, (4, 3, 5), 3, seed=7, order=order, eta=eta)
+        _check(g, o, eta, 1e-9)
+        assert g.swaps == tuple(o.swaps)
+
+
+def test_srrqr_on_oracle_q(ctx):
+    """N9 fed the oracle's Q reproduces the oracle's selection exactly (SURVEY c.4)."""
+    rng = np.random.default_rng(11)
+    for I, ell in [(200, 15), (5000, 15), (64, 8)]:
+        q, _ = np.linalg.qr(rng.standard_normal((I, ell)) * np.exp(-0.02 * np.arange(I))[:, None])
+        sel, a, swaps = ctx.debug_srrqr(q, 2.0)
+        osel, oswaps = O.srrqr_select(q, 2.0)
+        assert list(sel) == list(osel) and swaps == oswaps
+        np.testing.assert_allclose(a, O.oblique_factor(q, osel), rtol=0, atol=1e-10)
+
+
+def test_sparse_invalid(ctx):
+    from paper_1905_07311_b200.rtucker import RTuckerError
+    idx = np.array([[0, 1, 2], [0, 1, 2], [0, 1, 2]])
+    vals = np.array([1.0, 2.0, 3.0])
+    for kw in (dict(ranks=(2, 1, 1), p=1), dict(eta=0.5)):   # r + p >= min(I, prod others)
+        a = dict(ranks=(1, 1, 1), p=0, eta=2.0)
+        a.update(kw)
+        with pytest.raises(RTuckerError) as e:
+            _run(ctx, idx, vals, (3, 3, 3), a["ranks"], a["p"], eta=a["eta"], device=False)
+        assert e.value.name == "EINVAL", kw
