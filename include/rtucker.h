@@ -222,6 +222,12 @@ rtucker_status rtucker_debug_qr(rtucker_ctx *ctx, int64_t m, int32_t n, const do
 rtucker_status rtucker_debug_eig(rtucker_ctx *ctx, int32_t n, const double *A, double *w, double *V,
                                  int32_t *sweeps_out /* host, may be NULL */);
 
+/* Eigenpairs of a symmetric positive semidefinite Gram (the hot-path eigensolver): pivoted
+ * Cholesky + one-sided Jacobi on the factor.  Eigenvalues descending in w; eigenvectors in V
+ * accurate to ~eps * sqrt(w_0 / w_k) (DEVICE pointers). */
+rtucker_status rtucker_debug_gram_eig(rtucker_ctx *ctx, int32_t n, const double *A, double *w, double *V,
+                                      int32_t *sweeps_out /* host, may be NULL */);
+
 /* Strong-RRQR row selection (DESIGN reading R9) of an m x l orthonormal fp64 Q:
  * sel (l, sorted ascending, DEVICE int64) and A = Q Q[sel,:]^{-1} (m x l, DEVICE). */
 rtucker_status rtucker_debug_srrqr(rtucker_ctx *ctx, int64_t m, int32_t l, const double *Q,

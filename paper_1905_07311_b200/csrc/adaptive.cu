@@ -104,7 +104,7 @@ ModeOut adapt_mode(Ctx &c, const void *G, DT gt, const int64_t *cur, int d, int 
     sumsq(c, W.p, DT::F64, I * bb, scal.p);
     const double wn = std::sqrt(fetch(c, scal.p));
     if (wn <= floor_abs) break;  // range exhausted: the block is discarded
-    householder_qr(c, W.p, I, bb, Q.p + (size_t)I * k);
+    householder_qr(c, W.p, I, bb, Q.p + (size_t)I * k);  // the basis of Q is the core basis with ADAPT_NO_TRUNCATE
     ps.next(PH_BPASS);
     // B_i = Q_i^T G_(n) written into rows k..k+bb of B (L, cap, R) via a strided TTM
     DevBuf<double> gram(c, (size_t)bb * bb);
@@ -138,7 +138,7 @@ ModeOut adapt_mode(Ctx &c, const void *G, DT gt, const int64_t *cur, int d, int 
   PhaseScope ps(c, PH_EIG, n);
   DevBuf<double> gram(c, (size_t)k * k), w(c, k), U(c, (size_t)k * k);
   mode_gram(c, B.p, store, vb, gram.p);
-  sym_eig(c, gram.p, k, w.p, U.p);
+  sym_eig(c, gram.p, k, w.p, U.p);  // r not known yet: accurate tail needed
   std::vector<double> hw(k);
   RT_CUDA(cudaMemcpyAsync(hw.data(), w.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c.stream));
   RT_CUDA(cudaStreamSynchronize(c.stream));

@@ -151,7 +151,7 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
     DevBuf<double> Q(c, (size_t)Ig * ell);
     {
       PhaseScope ps(c, PH_QR, jj);
-      householder_qr(c, Y.p, Ig, ell, Q.p);
+      thin_qr(c, Y.p, Ig, ell, Q.p);
     }
     Y.release();
     // ---- Alg 1 line 3: B = Q^T G_(n)   (+ Gram B B^T)
@@ -176,7 +176,7 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
     ps_b.next(PH_EIG);
     // ---- Alg 1 line 4: thin SVD of B through the eigenpairs of its Gram
     DevBuf<double> w(c, ell), V(c, (size_t)ell * ell);
-    sym_eig(c, gram.p, ell, w.p, V.p);
+    gram_eig(c, gram.p, ell, w.p, V.p, nullptr, rr);
     // ---- Alg 1 line 5: A_n = Q U_B(:, 1:r)
     double *A = nullptr;
     RT_CUDA(cudaMallocAsync((void **)&A, sizeof(double) * Ig * rr, c.stream));
@@ -245,7 +245,7 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
     }
     ps.next(PH_QR);
     DevBuf<double> Q(c, (size_t)Ig * ell);
-    householder_qr(c, Y.p, Ig, ell, Q.p);
+    thin_qr(c, Y.p, Ig, ell, Q.p);
     DevBuf<double> gram(c, (size_t)ell * ell);
     ps.next(PH_BPASS);
     if (!last_sharded) {
@@ -265,7 +265,7 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
     }
     ps.next(PH_EIG);
     DevBuf<double> w(c, ell), V(c, (size_t)ell * ell);
-    sym_eig(c, gram.p, ell, w.p, V.p);
+    gram_eig(c, gram.p, ell, w.p, V.p, nullptr, rr);
     double *A = nullptr;
     RT_CUDA(cudaMallocAsync((void **)&A, sizeof(double) * Ig * rr, c.stream));
     res->factors[n] = A;

@@ -50,9 +50,17 @@ void ttm_dense(Ctx &c, const void *X, DT in, ModeView v, const double *A, int64_
 void mode_gram(Ctx &c, const void *B, DT t, ModeView v, double *gram);
 
 // ---- linalg.cu ---------------------------------------------------------------------
-void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q);
+// gate (device int, optional): the kernels return immediately when *gate == 0.
+void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q, const int *gate = nullptr);
+// Hot-path thin QR: CholeskyQR2, with Householder recomputation when ill-conditioned.
+void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q);
 // w descending; sweeps (optional, device int) <- Jacobi sweeps used
-void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps = nullptr);
+// gate (device int, optional): the kernel returns immediately when *gate == 0.
+void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps = nullptr, const int *gate = nullptr);
+// PSD Gram: pivoted Cholesky + one-sided Jacobi on the factor; eigenvectors accurate to
+// ~eps sqrt(w_0 / w_k).  When the r_need-th eigenvalue is below 1e-8 w_0 the unpreconditioned
+// sym_eig recomputes the result (device-side gate, no host sync).  n > 64 uses sym_eig.
+void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps = nullptr, int r_need = 1 << 30);
 // Sign convention of reading R4b: for each column k < r of A (m x r) make the entry of
 // largest magnitude positive (first on ties); the same sign is applied to column k of U
 // (ell x r, leading dim ldu) so that the shrink U^T B stays consistent.

@@ -343,7 +343,7 @@ rtucker_status rtucker_debug_philox(rtucker_ctx *ctx, const uint32_t *ctr, int64
 
 rtucker_status rtucker_debug_qr(rtucker_ctx *ctx, int64_t m, int32_t n, const double *Y, double *Q) {
   if (!ctx || !Y || !Q || n < 1 || m < n) return RTUCKER_EINVAL;
-  return guard(ctx, [&] { householder_qr(ctx->c, Y, m, n, Q); });
+  return guard(ctx, [&] { thin_qr(ctx->c, Y, m, n, Q); });
 }
 
 rtucker_status rtucker_debug_eig(rtucker_ctx *ctx, int32_t n, const double *A, double *w, double *V,
@@ -352,6 +352,19 @@ rtucker_status rtucker_debug_eig(rtucker_ctx *ctx, int32_t n, const double *A, d
   return guard(ctx, [&] {
     DevBuf<int> sw(ctx->c, 1);
     sym_eig(ctx->c, A, n, w, V, sw.p);
+    int h = 0;
+    RT_CUDA(cudaMemcpyAsync(&h, sw.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->c.stream));
+    RT_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    if (sweeps_out) *sweeps_out = h;
+  });
+}
+
+rtucker_status rtucker_debug_gram_eig(rtucker_ctx *ctx, int32_t n, const double *A, double *w, double *V,
+                                      int32_t *sweeps_out) {
+  if (!ctx || !A || !w || !V || n < 1) return RTUCKER_EINVAL;
+  return guard(ctx, [&] {
+    DevBuf<int> sw(ctx->c, 1);
+    gram_eig(ctx->c, A, n, w, V, sw.p, 1);
     int h = 0;
     RT_CUDA(cudaMemcpyAsync(&h, sw.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->c.stream));
     RT_CUDA(cudaStreamSynchronize(ctx->c.stream));

@@ -64,7 +64,9 @@ __device__ __forceinline__ void cluster_allsum(cg::cluster_group &cl, double *bu
 // and updates its rows; v^T w_c = x_j^T w_c + (v_0 - alpha) w_c[j].  Q = H_0 .. H_{n-1} [I; 0]
 // is then accumulated backwards the same way.
 __global__ void __launch_bounds__(kQRT) qr_cluster_kernel(const double *__restrict__ Y, int64_t m, int n,
-                                                          int rows, double *__restrict__ Q) {
+                                                          int rows, double *__restrict__ Q,
+                                                          const int *__restrict__ gate) {
+  if (gate && *gate == 0) return;  // uniform across the cluster
   extern __shared__ double sm[];
   cg::cluster_group cl = cg::this_cluster();
   const int ncta = (int)cl.num_blocks();
@@ -163,7 +165,8 @@ __global__ void __launch_bounds__(kQRT) qr_cluster_kernel(const double *__restri
 // with I_n ~ 1e5): same reflectors, one CTA, W and Q in global memory.
 constexpr int kQRG = 1024;
 __global__ void __launch_bounds__(kQRG) qr_global_kernel(double *__restrict__ W, int64_t m, int n,
-                                                         double *__restrict__ Q) {
+                                                         double *__restrict__ Q, const int *__restrict__ gate) {
+  if (gate && *gate == 0) return;
   extern __shared__ double gsm[];
   double *sbeta = gsm, *sdot = gsm + n;
   __shared__ double sred[kQRG / 32];
@@ -247,9 +250,11 @@ __device__ __forceinline__ void rr_pair(int k, int t, int np, int &p, int &q) {
 // g^2 <= tol^2 a_p a_q (relative test; tol ~ sqrt(n) eps, just above the rounding of g, so
 // the angle left between converged columns is <= tol lambda_q / lambda_p).
 template <int kL, bool kSmem>
-__global__ void __launch_bounds__(kEigT) jacobi_kernel(const double *__restrict__ Ain, int n, double *__restrict__ w,
+__global__ void __launch_bounds__(kL == 8 ? 256 : (kL == 16 ? 512 : kEigT)) jacobi_kernel(const double *__restrict__ Ain, int n, double *__restrict__ w,
                                                        double *__restrict__ Vout, double *__restrict__ gws,
-                                                       double tol, int max_sweeps, int *__restrict__ info) {
+                                                       double tol, int max_sweeps, int *__restrict__ info,
+                                                       const int *__restrict__ gate) {
+  if (gate && *gate == 0) return;  // the preconditioned solver's result was accurate enough
   extern __shared__ double esm[];
   const int np = n + (n & 1);
   double *__restrict__ M = kSmem ? esm : gws;   // np x np, column-major
@@ -314,10 +319,10 @@ __global__ void __launch_bounds__(kEigT) jacobi_kernel(const double *__restrict_
         double *__restrict__ mp = M + (size_t)np * p;
         double *__restrict__ mq = M + (size_t)np * q;
         RT_EIG_PROBE(0);
-        constexpr int kR = (kL == 8) ? 8 : 1;   // rows per lane held in registers (np <= 64)
+        constexpr int kR = (kL < 32) ? 64 / kL : 1;   // rows per lane held in registers (np <= 64)
         double xp[kR], xq[kR];
         double g = 0.0;
-        if (kL == 8) {
+        if (kL < 32) {
 #pragma unroll
           for (int u = 0; u < kR; ++u) {
             const int r = gl + kL * u;
@@ -348,7 +353,7 @@ __global__ void __launch_bounds__(kEigT) jacobi_kernel(const double *__restrict_
           RT_EIG_PROBE(2);
           double *__restrict__ vp = V + (size_t)np * p;
           double *__restrict__ vq = V + (size_t)np * q;
-          if (kL == 8) {
+          if (kL < 32) {
             double yp[kR], yq[kR];
 #pragma unroll
             for (int u = 0; u < kR; ++u) {
@@ -413,6 +418,254 @@ __global__ void __launch_bounds__(kEigT) jacobi_kernel(const double *__restrict_
   }
 }
 
+// Eigenpairs of a PSD Gram G (n <= 64), preconditioned one-sided Jacobi (Drmac-Veselic
+// style): pivoted Cholesky P^T G P = L L^T (diagonal pivoting, ties to the smallest index,
+// stops at rank when the largest remaining diagonal is <= n eps max diag(G)), then one-sided
+// Jacobi orthogonalises the columns of M = L (M J = U Sigma), so P^T G P = U Sigma^2 U^T:
+// lambda_k = |m_k|^2 and v_k = P m_k / |m_k|.  The pivoted factor is already close to
+// column-orthogonal, so the Jacobi needs a handful of sweeps instead of the 13-25 sweeps of
+// Jacobi on G itself; no rotation matrix is accumulated.  Eigenvectors are accurate to
+// ~eps sigma_1 / sigma_k, i.e. for the leading part of the spectrum that the truncation keeps.
+constexpr int kGramT = 256;
+__global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restrict__ Ain, int n, double *__restrict__ w,
+                                                          double *__restrict__ Vout, double tol, int max_sweeps,
+                                                          int *__restrict__ info, int r_need, int *__restrict__ refine) {
+  extern __shared__ double gsm2[];
+  const int np = n + (n & 1);
+  double *G = gsm2;                     // np x np working copy (column-major)
+  double *M = G + np * np;              // L, then M J
+  double *lam = M + np * np;            // np
+  int *perm = reinterpret_cast<int *>(lam + np);
+  short2 *ptab = reinterpret_cast<short2 *>(perm + np + (np & 1));
+  __shared__ int sconv, spiv, srank;
+  __shared__ double sdmax;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nw = kGramT / 32;
+  constexpr int kL = 8, kGroups = 4, kR = 8;
+  const int sub = lane / kL, gl = lane % kL;
+  const unsigned gmask = 0xFFu << (sub * kL);
+  const int npairs = np / 2;
+  for (int e = tid; e < np * np; e += kGramT) {
+    const int i = e % np, j = e / np;
+    G[e] = (i < n && j < n) ? 0.5 * (Ain[i + (size_t)n * j] + Ain[j + (size_t)n * i]) : 0.0;
+    M[e] = 0.0;
+  }
+  for (int i = tid; i < np; i += kGramT) perm[i] = i;
+  for (int e = tid; e < (np - 1) * npairs; e += kGramT) {
+    int p, q;
+    rr_pair(e % npairs, e / npairs, np, p, q);
+    ptab[e] = make_short2((short)p, (short)q);
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double m = 0.0;
+    for (int i = lane; i < n; i += 32) m = fmax(m, G[i + np * i]);
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) { sdmax = m; srank = n; }
+  }
+  __syncthreads();
+  const double thresh = n * 2.2e-16 * sdmax;
+  // ---- pivoted Cholesky (right-looking), L stored in M (column-major, lower)
+  for (int k = 0; k < n; ++k) {
+    if (warp == 0) {  // pivot: largest remaining diagonal, first index on ties
+      double bv = -1.0;
+      int bi = n;
+      for (int i = k + lane; i < n; i += 32) {
+        const double v = G[i + np * i];
+        if (v > bv) { bv = v; bi = i; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+      }
+      if (lane == 0) {
+        spiv = bi;
+        if (!(bv > thresh)) srank = k;
+      }
+    }
+    __syncthreads();
+    if (srank <= k) break;  // rank reached: the remaining columns of L are zero
+    const int p = spiv;
+    if (p != k) {  // symmetric swap of G rows/cols k <-> p, rows of L computed so far, perm
+      for (int j = tid; j < n; j += kGramT) {
+        double t = G[k + np * j]; G[k + np * j] = G[p + np * j]; G[p + np * j] = t;
+      }
+      __syncthreads();
+      for (int i = tid; i < n; i += kGramT) {
+        double t = G[i + np * k]; G[i + np * k] = G[i + np * p]; G[i + np * p] = t;
+      }
+      for (int j = tid; j < k; j += kGramT) {
+        double t = M[k + np * j]; M[k + np * j] = M[p + np * j]; M[p + np * j] = t;
+      }
+      if (tid == 0) { int t = perm[k]; perm[k] = perm[p]; perm[p] = t; }
+      __syncthreads();
+    }
+    const double lkk = sqrt(G[k + np * k]);
+    for (int i = k + tid; i < n; i += kGramT) M[i + np * k] = (i == k) ? lkk : G[i + np * k] / lkk;
+    __syncthreads();
+    for (int e = tid; e < (n - k - 1) * (n - k - 1); e += kGramT) {
+      const int i = k + 1 + e % (n - k - 1), j = k + 1 + e / (n - k - 1);
+      G[i + np * j] -= M[i + np * k] * M[j + np * k];
+    }
+    __syncthreads();
+  }
+  // ---- one-sided Jacobi on the columns of M
+  const double tol2 = tol * tol;
+  int sweeps = 0;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    for (int k = warp; k < np; k += nw) {
+      double d = 0.0;
+      for (int r = lane; r < np; r += 32) { const double x = M[r + np * k]; d = fma(x, x, d); }
+      d = warp_sum(d);
+      if (lane == 0) lam[k] = d;
+    }
+    if (tid == 0) sconv = 1;
+    __syncthreads();
+    for (int t = 0; t < np - 1; ++t) {
+      const short2 *row = ptab + t * npairs;
+      for (int k0 = warp * kGroups; k0 < npairs; k0 += kGroups * nw) {
+        const int k = k0 + sub;
+        const bool act = k < npairs;
+        const short2 pq = row[act ? k : 0];
+        double *__restrict__ mp = M + np * pq.x;
+        double *__restrict__ mq = M + np * pq.y;
+        double xp[kR], xq[kR], pr[kR];
+#pragma unroll
+        for (int u = 0; u < kR; ++u) {
+          const int r = gl + kL * u;
+          xp[u] = r < np ? mp[r] : 0.0;
+          xq[u] = r < np ? mq[r] : 0.0;
+          pr[u] = xp[u] * xq[u];
+        }
+#pragma unroll
+        for (int h = kR / 2; h; h >>= 1)
+#pragma unroll
+          for (int u = 0; u < h; ++u) pr[u] += pr[u + h];
+        double g = pr[0];
+#pragma unroll
+        for (int o = kL / 2; o; o >>= 1) g += __shfl_xor_sync(gmask, g, o, kL);
+        const double a = lam[pq.x], b = lam[pq.y];
+        if (act && g != 0.0 && g * g > tol2 * a * b) {  // group-uniform
+          if (gl == 0) sconv = 0;
+          const double zeta = (b - a) / (2.0 * g);
+          const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double c = rsqrt(fma(tt, tt, 1.0)), s = tt * c;
+#pragma unroll
+          for (int u = 0; u < kR; ++u) {
+            const int r = gl + kL * u;
+            if (r < np) {
+              mp[r] = c * xp[u] - s * xq[u];
+              mq[r] = s * xp[u] + c * xq[u];
+            }
+          }
+          if (gl == 0) {
+            lam[pq.x] = a - tt * g;
+            lam[pq.y] = b + tt * g;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    sweeps = sweep + 1;
+    const int done = sconv;
+    __syncthreads();
+    if (done) break;
+  }
+  if (tid == 0 && info) *info = sweeps;
+  for (int k = warp; k < np; k += nw) {  // exact column norms
+    double d = 0.0;
+    for (int r = lane; r < np; r += 32) { const double x = M[r + np * k]; d = fma(x, x, d); }
+    d = warp_sum(d);
+    if (lane == 0) lam[k] = d;
+  }
+  __syncthreads();
+  // sort descending (ties by index), drop the padding column, v_k = P m_k / |m_k|
+  for (int i = tid; i < n; i += kGramT) {
+    const double di = lam[i];
+    int rank = 0;
+    for (int j = 0; j < np; ++j) {
+      const double dj = lam[j];
+      if (j != i && (dj > di || (dj == di && j < i))) ++rank;
+    }
+    if (rank >= n) continue;
+    w[rank] = di;
+    const double inv = di > 0.0 ? 1.0 / sqrt(di) : 0.0;
+    for (int r = 0; r < n; ++r) Vout[perm[r] + (int64_t)n * rank] = M[r + np * i] * inv;
+  }
+  // v_k from a normalised column is accurate to ~eps sqrt(lambda_0 / lambda_k): request the
+  // unpreconditioned solver when the wanted rank reaches lambda_k < 1e-8 lambda_0
+  if (refine) {
+    __syncthreads();  // w (global) written above by the sorting threads
+    if (tid == 0) *refine = (w[r_need - 1] >= 1e-8 * w[0]) ? 0 : 1;
+  }
+}
+
+// ------------------------------------------------------------- CholeskyQR2 ----------
+// Thin QR of a well-conditioned tall sketch in 2 x (Gram, Cholesky, Y R^{-1}) passes
+// (Yamamoto et al.'s CholeskyQR2; orthogonality ~eps while kappa(Y) < ~1e7).  The Cholesky
+// flags ill-conditioning (a pivot d_k < 1e-13 of its original diagonal, i.e. a column that is
+// numerically in the span of the previous ones); the Householder kernel then recomputes Q
+// (device-side gate, no host sync).  Only the range of Q enters the method (B = Q^T X and
+// A = Q U_B, or the oblique factor Q Q_S^{-1}), and both routes span range(Y).
+__global__ void __launch_bounds__(256) chol_inv_kernel(const double *__restrict__ G, int n, double *__restrict__ Rinv,
+                                                       int *__restrict__ bad) {
+  extern __shared__ double cs[];
+  double *R = cs;              // n x n, row-major upper (R[k*n + j])
+  double *diag0 = R + n * n;   // original diagonal
+  __shared__ int sbad;
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    R[e] = 0.5 * (G[i + n * j] + G[j + n * i]);
+  }
+  for (int i = tid; i < n; i += blockDim.x) diag0[i] = G[i + n * i];
+  if (tid == 0) sbad = 0;
+  __syncthreads();
+  // right-looking Cholesky G = R^T R (upper R), 16 x 16 thread tiling of the trailing update
+  for (int k = 0; k < n; ++k) {
+    const double d = R[k * n + k];
+    if (!(d > 1e-13 * diag0[k] && d > 0.0)) {  // uniform
+      if (tid == 0) sbad = 1;
+      break;
+    }
+    const double inv = rsqrt(d);
+    for (int i = k + 1 + ty; i < n; i += 16)
+      for (int j = i + tx; j < n; j += 16) R[i * n + j] -= (R[k * n + i] * inv) * (R[k * n + j] * inv);
+    __syncthreads();
+    for (int j = k + 1 + tid; j < n; j += blockDim.x) R[k * n + j] *= inv;
+    if (tid == 0) R[k * n + k] = d * inv;
+    __syncthreads();
+  }
+  if (sbad) {
+    if (tid == 0) *bad = 1;
+    return;
+  }
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e / n, j = e - i * n;
+    Rinv[i + n * j] = (j >= i) ? R[e] : 0.0;  // R itself (column-major upper)
+  }
+}
+
+// Q = Y R^{-1} by forward substitution, one row of Y per thread (x R = y), R in shared memory.
+__global__ void __launch_bounds__(128) trsm_rows_kernel(const double *__restrict__ Y, int64_t m, int n,
+                                                        const double *__restrict__ Rg, double *__restrict__ Q,
+                                                        const int *__restrict__ bad) {
+  if (*bad) return;
+  extern __shared__ double rs[];
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) rs[e] = Rg[e];
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+    double x[64];
+    for (int j = 0; j < n; ++j) {
+      double s = Y[i + m * j];
+      for (int t = 0; t < j; ++t) s = fma(-x[t], rs[t + n * j], s);
+      x[j] = s / rs[j + n * j];
+      Q[i + m * j] = x[j];
+    }
+  }
+}
+
 // One CTA per column k: argmax |A[:, k]| (first index on ties); flip A[:, k] and U[:, k]
 // when that entry is negative (DESIGN reading R4b).
 __global__ void canonical_signs_kernel(double *__restrict__ A, int64_t m, double *__restrict__ U, int64_t ldu,
@@ -455,7 +708,7 @@ void canonical_signs(Ctx &c, double *A, int64_t m, int r, double *U, int64_t ldu
   RT_LAUNCH(c, canonical_signs_kernel, r, 256, 0, A, m, U, ldu, ell);
 }
 
-void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
+void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q, const int *gate) {
   RT_REQUIRE(m >= n && n >= 1, "qr: need m >= n >= 1");
   RT_REQUIRE(n <= 4096, "qr: more than 4096 columns is not supported");
   // smallest cluster whose row slabs fit in shared memory (RTUCKER_QR_NCTA forces a size,
@@ -486,7 +739,7 @@ void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
     RT_CUDA(cudaFuncSetAttribute(qr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (ncta > 8)
       RT_CUDA(cudaFuncSetAttribute(qr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    RT_CUDA(cudaLaunchKernelEx(&cfg, qr_cluster_kernel, Y, m, n, rows, Q));
+    RT_CUDA(cudaLaunchKernelEx(&cfg, qr_cluster_kernel, Y, m, n, rows, Q, gate));
     c.launches++;
     return;
   }
@@ -495,10 +748,44 @@ void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
   const size_t smem = sizeof(double) * 2 * (size_t)n;
   if (smem > 48 * 1024)
     RT_CUDA(cudaFuncSetAttribute(qr_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  RT_LAUNCH(c, qr_global_kernel, 1, kQRG, smem, W.p, m, n, Q);
+  RT_LAUNCH(c, qr_global_kernel, 1, kQRG, smem, W.p, m, n, Q, gate);
 }
 
-void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps) {
+void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps, int r_need) {
+  const int np = n + (n & 1);
+  if (np > 64) return sym_eig(c, A, n, w, V, sweeps);
+  const size_t need = sizeof(double) * (2 * (size_t)np * np + np) + sizeof(int) * (np + 1) +
+                      sizeof(short2) * (size_t)(np - 1) * (np / 2) + 64;
+  DevBuf<int> refine(c, 1);
+  RT_CUDA(cudaFuncSetAttribute(gram_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+  RT_LAUNCH(c, gram_eig_kernel, 1, kGramT, need, A, n, w, V, 3e-15 * std::sqrt((double)n), 40, sweeps,
+            std::max(1, std::min(r_need, n)), refine.p);
+  sym_eig(c, A, n, w, V, nullptr, refine.p);  // no-op unless the gate asks for it
+}
+
+void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
+  RT_REQUIRE(m >= n && n >= 1, "qr: need m >= n >= 1");
+  // sketches whose rows fit a 16-CTA cluster: Householder directly (latency-bound either way);
+  // tall sketches (sparse modes, I_n ~ 1e5): CholeskyQR2 with the Householder fallback
+  if (n > 64 || m <= 16 * 256) return householder_qr(c, Y, m, n, Q, nullptr);
+  DevBuf<double> G(c, (size_t)n * n), Ri(c, (size_t)n * n), Q1(c, (size_t)m * n);
+  DevBuf<int> bad(c, 1);
+  bad.zero();
+  const size_t csm = sizeof(double) * ((size_t)n * n + n);
+  RT_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+  const double *src = Y;
+  for (int pass = 0; pass < 2; ++pass) {
+    double *dst = pass == 0 ? Q1.p : Q;
+    mode_gram(c, src, DT::F64, ModeView{m, n, 1}, G.p);
+    RT_LAUNCH(c, chol_inv_kernel, 1, 256, csm, G.p, n, Ri.p, bad.p);
+    RT_LAUNCH(c, trsm_rows_kernel, std::max(1, std::min(c.num_sms * 8, ceil_div(m, 128))), 128,
+              sizeof(double) * n * n, src, m, n, Ri.p, dst, bad.p);
+    src = dst;
+  }
+  householder_qr(c, Y, m, n, Q, bad.p);  // runs only when a Cholesky pass flagged
+}
+
+void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps, const int *gate) {
   const int np = n + (n & 1);
   const size_t tab = sizeof(short2) * (size_t)(np - 1) * (np / 2) + 16;
   const size_t need = sizeof(double) * (2 * (size_t)np * np + np) + tab;
@@ -508,12 +795,12 @@ void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps) 
   if (need <= 200 * 1024) {
 #define RT_EIG(KL)                                                                                   \
   RT_CUDA(cudaFuncSetAttribute(jacobi_kernel<KL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need)); \
-  RT_LAUNCH(c, (jacobi_kernel<KL, true>), 1, thr, need, A, n, w, V, (double *)nullptr, tol, max_sweeps, sweeps)
+  RT_LAUNCH(c, (jacobi_kernel<KL, true>), 1, thr, need, A, n, w, V, (double *)nullptr, tol, max_sweeps, sweeps, gate)
     if (np <= 64) { RT_EIG(8); } else { RT_EIG(32); }
 #undef RT_EIG
   } else {  // matrices and vectors in global memory, pairs computed on the fly
     DevBuf<double> ws(c, 2 * (size_t)np * np + np);
-    RT_LAUNCH(c, (jacobi_kernel<32, false>), 1, kEigT, 0, A, n, w, V, ws.p, tol, max_sweeps, sweeps);
+    RT_LAUNCH(c, (jacobi_kernel<32, false>), 1, kEigT, 0, A, n, w, V, ws.p, tol, max_sweeps, sweeps, gate);
   }
 }
 

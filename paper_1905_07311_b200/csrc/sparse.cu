@@ -520,7 +520,7 @@ rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int6
       PhaseScope ps(c, PH_SKETCH, jj);
       sketch_coo(c, g, n, ell, seed, nf64, Y.p);
       ps.next(PH_QR);
-      householder_qr(c, Y.p, I, ell, Q.p);
+      thin_qr(c, Y.p, I, ell, Q.p);
     }
     double *A = nullptr;
     RT_CUDA(cudaMallocAsync((void **)&A, sizeof(double) * I * ell, c.stream));

@@ -242,9 +242,99 @@ __global__ void mode_gram_reduce_kernel(const double *__restrict__ partial, int 
   }
 }
 
+// Gram of the mode-n unfolding for J <= 64 (fp64 DFMA, register-tiled): 256 threads in 4
+// groups of 64; a group owns every 4th column of the CTA's chunk and each of its threads an
+// 8 x 8 tile of the 64 x 64 Gram; columns p = l + L r are staged 32 at a time in shared
+// memory (coalesced along l, or along j when L == 1).  Per-CTA partials are summed in a
+// fixed order by gram_reduce2_kernel (deterministic).
+constexpr int kGP = 32;  // columns per staged chunk
+template <typename T>
+__global__ void __launch_bounds__(256) gram64_kernel(const T *__restrict__ B, int64_t L, int J, int64_t R,
+                                                     int64_t pchunk, double *__restrict__ partial) {
+  __shared__ double sB[kGP][65];
+  const int tid = threadIdx.x, grp = tid >> 6, t = tid & 63;
+  const int ta = t >> 3, tb = t & 7;  // tile rows 8ta.., cols 8tb..
+  const int64_t P = L * R;
+  const int64_t pbeg = (int64_t)blockIdx.x * pchunk, pend = min(P, pbeg + pchunk);
+  double acc[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) acc[a][b] = 0.0;
+  for (int64_t p0 = pbeg; p0 < pend; p0 += kGP) {
+    __syncthreads();
+    const int np_ = (int)((pend - p0) < kGP ? (pend - p0) : kGP);
+    if (L == 1) {  // columns contiguous: B[j + J p]
+      const T *src = B + p0 * J;
+      for (int e = tid; e < kGP * 64; e += 256) {
+        const int pp = e >> 6, j = e & 63;
+        sB[pp][j] = (pp < np_ && j < J) ? (double)src[(int64_t)pp * J + j] : 0.0;
+      }
+    } else {
+      const int64_t l0 = p0 % L, r0 = p0 / L;
+      for (int e = tid; e < kGP * 64; e += 256) {
+        const int pp = e % kGP, j = e / kGP;
+        double v = 0.0;
+        if (pp < np_ && j < J) {
+          int64_t l = l0 + pp, r = r0;
+          while (l >= L) { l -= L; ++r; }
+          v = (double)B[l + L * (j + (int64_t)J * r)];
+        }
+        sB[pp][j] = v;
+      }
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int pp = grp; pp < kGP; pp += 4) {
+      double x[8], y[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) { x[u] = sB[pp][8 * ta + u]; y[u] = sB[pp][8 * tb + u]; }
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
+    }
+  }
+  // combine the 4 groups in a fixed order into the CTA partial [64 x 64] (global, L2)
+  for (int g = 0; g < 4; ++g) {
+    __syncthreads();
+    if (grp == g) {
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          const int64_t o = (int64_t)blockIdx.x * 4096 + (8 * ta + a) * 64 + 8 * tb + b;
+          partial[o] = (g == 0 ? 0.0 : partial[o]) + acc[a][b];
+        }
+    }
+  }
+}
+
+__global__ void gram_reduce2_kernel(const double *__restrict__ partial, int nblk, int J, double *__restrict__ gram) {
+  __shared__ double sred[4];
+  const int e = blockIdx.x;
+  const int j1 = e % J, j2 = e / J;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) s += partial[(int64_t)b * 4096 + j1 * 64 + j2];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) gram[e] = (sred[0] + sred[1]) + (sred[2] + sred[3]);
+}
+
 template <typename T>
 void mode_gram_t(Ctx &c, const T *B, ModeView v, double *gram) {
   const int64_t P = v.L * v.R;
+  if (v.I <= 64) {
+    const int64_t nchunk = (P + kGP - 1) / kGP;
+    const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>(nchunk, (int64_t)c.num_sms * 3));
+    const int64_t pchunk = ((nchunk + nblk - 1) / nblk) * kGP;
+    const int g = (int)((P + pchunk - 1) / pchunk);
+    DevBuf<double> part(c, (size_t)std::max(g, 1) * 4096);
+    RT_LAUNCH(c, gram64_kernel<T>, g, 256, 0, B, v.L, (int)v.I, v.R, pchunk, part.p);
+    RT_LAUNCH(c, gram_reduce2_kernel, (int)(v.I * v.I), 128, 0, part.p, g, (int)v.I, gram);
+    return;
+  }
   const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>((P + 31) / 32, (int64_t)c.num_sms * 2));
   const int nb = ceil_div(v.I, kGB);
   DevBuf<double> part(c, (size_t)nblk * kGB * kGB);

@@ -38,7 +38,7 @@ EXPORTED = [
     "rtucker_adaptive", "rtucker_sparse_sthosvd", "rtucker_result_free", "rtucker_memcpy", "rtucker_sync",
     "rtucker_rel_error", "rtucker_debug_sketch", "rtucker_debug_omega", "rtucker_debug_philox",
     "rtucker_debug_qr", "rtucker_debug_eig", "rtucker_debug_srrqr", "rtucker_set_profiling",
-    "rtucker_phase_times",
+    "rtucker_phase_times", "rtucker_debug_gram_eig",
 ]
 PHASES = ("sketch", "qr", "bpass", "eig", "shrink", "other")
 
@@ -108,6 +108,7 @@ def load_library(path: str = LIB_PATH):
         "rtucker_debug_qr": (C.c_int, [P, I64, I32, P, P]),
         "rtucker_debug_eig": (C.c_int, [P, I32, P, P, P, C.POINTER(I32)]),
         "rtucker_debug_srrqr": (C.c_int, [P, I64, I32, P, D, P, P, C.POINTER(I32)]),
+        "rtucker_debug_gram_eig": (C.c_int, [P, I32, P, P, P, C.POINTER(I32)]),
         "rtucker_set_profiling": (C.c_int, [P, C.c_int]),
         "rtucker_phase_times": (C.c_int, [P, P, P, C.c_int]),
     }
@@ -443,6 +444,20 @@ class Context:
         sw = C.c_int32()
         self._enter()
         self._check(self.lib.rtucker_debug_eig(self.h, n, at.data_ptr(), w.data_ptr(), v.data_ptr(), C.byref(sw)))
+        self.sync()
+        self.last_sweeps = int(sw.value)
+        return w.cpu().numpy(), v.cpu().numpy().reshape((n, n), order="F")
+
+    def debug_gram_eig(self, a: np.ndarray):
+        """Hot-path PSD eigensolver (pivoted Cholesky + one-sided Jacobi)."""
+        torch = _torch()
+        n = a.shape[0]
+        at = torch.as_tensor(np.asfortranarray(a, dtype=np.float64).ravel(order="F"), device="cuda")
+        w = torch.empty(n, dtype=torch.float64, device="cuda")
+        v = torch.empty_like(at)
+        sw = C.c_int32()
+        self._enter()
+        self._check(self.lib.rtucker_debug_gram_eig(self.h, n, at.data_ptr(), w.data_ptr(), v.data_ptr(), C.byref(sw)))
         self.sync()
         self.last_sweeps = int(sw.value)
         return w.cpu().numpy(), v.cpu().numpy().reshape((n, n), order="F")

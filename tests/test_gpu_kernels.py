@@ -139,3 +139,32 @@ def test_sketch_tc_mode1(ctx, shape, ell, k0):
     err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     colerr = np.max(np.linalg.norm(got - ref, axis=0) / np.linalg.norm(ref, axis=0))
     assert err <= 1e-5 and colerr <= 2e-5, (err, colerr)
+
+
+@pytest.mark.parametrize("kind,n,k", [("c4like", 60, 50), ("hilbert", 60, 5), ("rankdef", 40, 7), ("small", 10, 5),
+                                      ("odd", 33, 20), ("one", 1, 1)])
+def test_gram_eig(ctx, kind, n, k):
+    """Hot-path PSD eigensolver (pivoted Cholesky + one-sided Jacobi on the factor) against
+    LAPACK eigh: leading eigenvalues to ~1e-12 relative, the leading-k projector to the
+    accuracy the gap allows, orthonormal leading eigenvectors."""
+    rng = np.random.default_rng(n + k)
+    if kind == "c4like" or kind in ("small", "odd", "one"):
+        u, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        lam = np.arange(1, n + 1) ** -3.0
+        a = (u * lam) @ u.T
+    elif kind == "hilbert":
+        a = 1.0 / (np.arange(n)[:, None] + np.arange(n)[None, :] + 1.0)
+    else:
+        b = rng.standard_normal((n, k)) @ rng.standard_normal((k, 300))
+        a = b @ b.T
+    a = (a + a.T) / 2
+    w, v = ctx.debug_gram_eig(a)
+    assert ctx.last_sweeps <= 20
+    we, ve = np.linalg.eigh(a)
+    o = np.argsort(-we)
+    we, ve = we[o], ve[:, o]
+    np.testing.assert_allclose(w[:k], we[:k], rtol=1e-11, atol=1e-14 * we[0])
+    gap = we[k - 1] - (we[k] if k < n else 0.0)
+    p1, p2 = v[:, :k] @ v[:, :k].T, ve[:, :k] @ ve[:, :k].T
+    assert np.linalg.norm(p1 - p2, 2) <= 1e-13 * we[0] / gap + 1e-12
+    assert np.linalg.norm(v[:, :k].T @ v[:, :k] - np.eye(k)) <= 1e-12
