@@ -204,6 +204,13 @@ rtucker_status rtucker_debug_sketch(rtucker_ctx *ctx, const rtucker_dense_desc *
                                     int32_t ell, int64_t k0, uint64_t seed, uint32_t flags,
                                     double *Y_out);
 
+/* B = A^T X_(mode) stored (L, J, R) in fp64 (out, DEVICE, may be NULL) and/or its Gram
+ * B_(mode) B_(mode)^T (gram, J x J, DEVICE, may be NULL); A is I_mode x J fp64 column-major
+ * (DEVICE).  The B-pass of Alg 1 line 3 with fp64 storage (HYBRID / FP64 products per
+ * flags). */
+rtucker_status rtucker_debug_ttm(rtucker_ctx *ctx, const rtucker_dense_desc *X, int32_t mode, const double *A,
+                                 int32_t J, uint32_t flags, double *out, double *gram);
+
 /* Omega rows: out[i + n*k] = Omega_mode[cols[i], k0 + k] for i < n, k < ell in `dtype`
  * precision (DEVICE pointers; cols int64). */
 rtucker_status rtucker_debug_omega(rtucker_ctx *ctx, rtucker_dtype dtype, uint64_t seed,

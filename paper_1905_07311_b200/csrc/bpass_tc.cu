@@ -5,16 +5,20 @@
 // i_out I/4, c_out C/8) writes the canonical no-swizzle K-major layout (8 rows x 16 B core
 // matrices, LBO = 128 B along K, SBO = 1024 B along M) straight from HBM.
 //
-//   warp 0       TMA producer: per stage (32 values of i) the X box (256 c x 32 i, 32 KB) and
+//   warp 0       TMA producer: per stage (32 values of i) the X box (128 c x 32 i, 16 KB) and
 //                the pre-split Q chunk (hi/lo, 64 k x 32 i, 16 KB, bulk copy from L2)
-//   warp 1       TMEM allocation + MMA issuer: per stage and M-tile (128 c), 4 k-steps x 3
-//                MMAs D += Xhi Qhi + Xhi Qlo + Xlo Qhi (M=128, N=64, K=8); two TMEM
-//                accumulator buffers (2 x 128 columns) so the epilogue of unit u overlaps
-//                the MMAs of unit u+1
-//   warps 2-5    epilogue: TMEM -> B (fp32 or fp64), one thread per column c
-//   warps 6-13   split workers: X = hi + lo in place (hi = tf32 truncation, lo to a buffer of
-//                the same layout; elementwise, layout-agnostic)
-// A work unit is 256 consecutive columns c; CTAs are persistent and stride over units.
+//   warp 1       TMEM allocation + MMA issuer: per stage 4 k-steps x 3 MMAs
+//                D = Xhi Qhi + Xhi Qlo + Xlo Qhi (M=128, N=64, K=8) into a FRESH accumulator
+//                (two TMEM buffers of 64 columns, alternating per stage)
+//   warps 2-5    epilogue: per stage, TMEM -> registers, added into fp64 running sums (one
+//                row c per thread, 64 doubles); after a unit's last stage B(c, :) is stored.
+//                fp32 accumulation therefore spans only the 32 terms of one stage: summing the
+//                whole I = 800 terms in TMEM gave a B error of 6e-6 relative at C4, which moved
+//                the rank-50 eigen-subspace of the Gram (gap ~5e-7 of lambda_1) and the C4
+//                relative error by 1e-2
+//   warps 6-9    split workers: X = hi + lo in place (both rounded to the tf32 grid, DESIGN
+//                R15; lo to a buffer of the same layout; elementwise, layout-agnostic)
+// A work unit is 128 consecutive columns c; CTAs are persistent and stride over units.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -27,12 +31,12 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();  // sketch_tc.cu
 
 namespace {
 
-constexpr int kUnit = 256;            // columns per work unit (2 M-tiles)
+constexpr int kUnit = 128;            // columns per work unit (1 M-tile)
 constexpr int kKC = 32;               // values of i per stage
-constexpr int kXBytes = kUnit * kKC * 4;   // 32 KB
+constexpr int kXBytes = kUnit * kKC * 4;   // 16 KB
 constexpr int kQBytes = 64 * kKC * 4;      // one Q plane chunk, 8 KB
-constexpr int kNS = 2;
-constexpr int kEpi = 4, kSplit = 8;
+constexpr int kNS = 4;
+constexpr int kEpi = 4, kSplit = 4;
 constexpr int kThreads = 32 * (2 + kEpi + kSplit);
 
 struct BpassParams {
@@ -77,7 +81,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc::fence_barrier_init();
   }
-  if (warp == 1) tc::tmem_alloc(tslot, 256);
+  if (warp == 1) tc::tmem_alloc(tslot, 128);
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
@@ -93,11 +97,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t u = blockIdx.x + (it / p.nkc) * gridDim.x;
         const int kc = (int)(it % p.nkc);
         tc::mbar_arrive_expect_tx(&full[s], kXBytes + 2 * kQBytes);
-        // X box: i_in 0..3, c_in 0..7, i_out 8 kc .. +8, c_out 32 u .. +32
+        // X box: i_in 0..3, c_in 0..7, i_out 8 kc .. +8, c_out 16 u .. +16
         asm volatile(
             "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, "
             "%5}], [%6];" ::"r"(tc::smem_u32(xb + s * kXBytes)),
-            "l"(&tmap), "r"(0), "r"(0), "r"(8 * kc), "r"((int)(32 * u)), "r"(tc::smem_u32(&full[s]))
+            "l"(&tmap), "r"(0), "r"(0), "r"(8 * kc), "r"((int)(16 * u)), "r"(tc::smem_u32(&full[s]))
             : "memory");
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -112,58 +116,66 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc = tc::idesc_tf32(128, 64, false, false);
       for (int64_t it = 0; it < nst; ++it) {
         const int s = (int)(it % kNS);
-        const int64_t ui = it / p.nkc;        // local unit index
-        const int kc = (int)(it % p.nkc);
-        const int ab = (int)(ui & 1);          // accumulator buffer
-        if (kc == 0 && ui >= 2) tc::mbar_wait(&accempty[ab], (uint32_t)(((ui / 2) & 1) ^ 1));
+        const int ab = (int)(it & 1);          // accumulator buffer
+        if (it >= 2) tc::mbar_wait(&accempty[ab], (uint32_t)(((it / 2) & 1) ^ 1));
         tc::mbar_wait(&ready[s], (uint32_t)((it / kNS) & 1));
         tc::tc_fence_after();
         const uint32_t xa = tc::smem_u32(xb + s * kXBytes), la = tc::smem_u32(lb + s * kXBytes);
         const uint32_t qh = tc::smem_u32(qb + s * 2 * kQBytes), ql = qh + kQBytes;
-        for (int mt = 0; mt < 2; ++mt) {
-          const uint32_t d = tmem + ab * 128 + mt * 64;
-          for (int ks = 0; ks < kKC / 8; ++ks) {
-            const uint64_t ah = tc::smem_desc(xa + mt * 16384 + ks * 256, 128, 1024, tc::kSwNone);
-            const uint64_t al = tc::smem_desc(la + mt * 16384 + ks * 256, 128, 1024, tc::kSwNone);
-            const uint64_t bh = tc::smem_desc(qh + ks * 256, 128, 1024, tc::kSwNone);
-            const uint64_t bl = tc::smem_desc(ql + ks * 256, 128, 1024, tc::kSwNone);
-            tc::mma_tf32(d, ah, bh, idesc, (kc | ks) ? 1u : 0u);
-            tc::mma_tf32(d, ah, bl, idesc, 1u);
-            tc::mma_tf32(d, al, bh, idesc, 1u);
-          }
+        const uint32_t d = tmem + ab * 64;
+        for (int ks = 0; ks < kKC / 8; ++ks) {
+          const uint64_t ah = tc::smem_desc(xa + ks * 256, 128, 1024, tc::kSwNone);
+          const uint64_t al = tc::smem_desc(la + ks * 256, 128, 1024, tc::kSwNone);
+          const uint64_t bh = tc::smem_desc(qh + ks * 256, 128, 1024, tc::kSwNone);
+          const uint64_t bl = tc::smem_desc(ql + ks * 256, 128, 1024, tc::kSwNone);
+          tc::mma_tf32(d, ah, bh, idesc, ks ? 1u : 0u);
+          tc::mma_tf32(d, ah, bl, idesc, 1u);
+          tc::mma_tf32(d, al, bh, idesc, 1u);
         }
         tc::mma_commit(&empty[s]);
-        if (kc == p.nkc - 1) tc::mma_commit(&accfull[ab]);
+        tc::mma_commit(&accfull[ab]);
       }
     }
   } else if (warp < 2 + kEpi) {
     // ------------------------------------------------------------- epilogue
-    const int q4 = warp & 3;  // TMEM lane quadrant
-    for (int64_t ui = 0; ui < nmine; ++ui) {
-      const int ab = (int)(ui & 1);
-      const int64_t u = blockIdx.x + ui * gridDim.x;
-      tc::mbar_wait(&accfull[ab], (uint32_t)((ui / 2) & 1));
+    const int q4 = warp & 3;  // TMEM lane quadrant = rows 32 q4 .. of the M-tile
+    double acc[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+    for (int64_t it = 0; it < nst; ++it) {
+      const int ab = (int)(it & 1);
+      tc::mbar_wait(&accfull[ab], (uint32_t)((it / 2) & 1));
       tc::tc_fence_after();
-      for (int mt = 0; mt < 2; ++mt) {
-        const int64_t c = u * kUnit + mt * 128 + 32 * q4 + lane;
+      {
         uint32_t r[32];
-        for (int h = 0; h < 2; ++h) {
-          tc::tmem_ld32(tmem + ((uint32_t)(32 * q4) << 16) + ab * 128 + mt * 64 + h * 32, r);
-          if (c < p.C) {
-            if (kF64) {
-              double *dst = (double *)p.B + c * p.ell + h * 32;
-              const int nk = min(32, p.ell - h * 32);
-              for (int j = 0; j < nk; ++j) dst[j] = (double)__uint_as_float(r[j]);
-            } else {
-              float *dst = (float *)p.B + c * p.ell + h * 32;
-              const int nk = min(32, p.ell - h * 32);
-              for (int j = 0; j < nk; ++j) dst[j] = __uint_as_float(r[j]);
-            }
-          }
-        }
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * q4) << 16) + ab * 64, r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[j] += (double)__uint_as_float(r[j]);
+        tc::tmem_ld32(tmem + ((uint32_t)(32 * q4) << 16) + ab * 64 + 32, r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[32 + j] += (double)__uint_as_float(r[j]);
       }
       tc::tc_fence_before();
       tc::mbar_arrive(&accempty[ab]);
+      if ((int)(it % p.nkc) == p.nkc - 1) {  // unit complete: store B(c, :) and reset
+        const int64_t u = blockIdx.x + (it / p.nkc) * gridDim.x;
+        const int64_t c = u * kUnit + 32 * q4 + lane;
+        if (c < p.C) {
+          if (kF64) {
+            double *dst = (double *)p.B + c * p.ell;
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+              if (j < p.ell) dst[j] = acc[j];
+          } else {
+            float *dst = (float *)p.B + c * p.ell;
+#pragma unroll
+            for (int j = 0; j < 64; ++j)
+              if (j < p.ell) dst[j] = (float)acc[j];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+      }
     }
   } else {
     // ------------------------------------------------------------- split workers
@@ -178,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float4 x = xv[e];
         float4 h, l;
         h.x = tc::tf32_hi(x.x); h.y = tc::tf32_hi(x.y); h.z = tc::tf32_hi(x.z); h.w = tc::tf32_hi(x.w);
-        l.x = x.x - h.x; l.y = x.y - h.y; l.z = x.z - h.z; l.w = x.w - h.w;
+        l.x = tc::tf32_lo(x.x, h.x); l.y = tc::tf32_lo(x.y, h.y); l.z = tc::tf32_lo(x.z, h.z); l.w = tc::tf32_lo(x.w, h.w);
         xv[e] = h;
         lv[e] = l;
       }
@@ -190,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (warp == 1) {
     tc::tc_fence_after();
-    tc::tmem_dealloc(tmem, 256);
+    tc::tmem_dealloc(tmem, 128);
   }
 }
 
@@ -209,7 +221,7 @@ __global__ void prep_q_kernel(const double *__restrict__ Q, int64_t ldq, int64_t
     const int off = ((k >> 3) * 1024 + (ii >> 2) * 128 + (k & 7) * 16 + (ii & 3) * 4) >> 2;
     float *dst = out + (size_t)kc * 2 * 64 * kKC;
     dst[off] = hi;
-    dst[64 * kKC + off] = v - hi;
+    dst[64 * kKC + off] = tc::tf32_lo(v, hi);
   }
 }
 
@@ -218,7 +230,8 @@ __global__ void prep_q_kernel(const double *__restrict__ Q, int64_t ldq, int64_t
 // B = Q^T X_(n) for fp32 X with L == 1 (B[k + ell c]); Q fp64 I x ell (ld = ldq).  Returns
 // false outside the kernel's envelope (caller falls back to the SIMT TTM).
 bool bpass_tc_mn(Ctx &c, const float *X, ModeView v, const double *Q, int64_t ldq, int ell, void *B, bool out_f64) {
-  if (!sketch_tc_enabled() || v.L != 1 || (v.I % 4) != 0 || (v.R % 8) != 0 || ell > 64 || ell < 1) return false;
+  static const bool off = getenv("RTUCKER_NO_TC_BPASS") != nullptr;
+  if (off || !sketch_tc_enabled() || v.L != 1 || (v.I % 4) != 0 || (v.R % 8) != 0 || ell > 64 || ell < 1) return false;
   if ((((uintptr_t)X) & 15) != 0 || v.R / 8 > (int64_t)INT32_MAX / 2) return false;
   BpassParams p{};
   p.I = v.I;
@@ -238,7 +251,7 @@ bool bpass_tc_mn(Ctx &c, const float *X, ModeView v, const double *Q, int64_t ld
   const uint64_t C = (uint64_t)v.R, I = (uint64_t)v.I;
   cuuint64_t dims[4] = {4, 8, I / 4, C / 8};
   cuuint64_t strides[3] = {I * 4, 16, I * 32};  // bytes of dims 1..3
-  cuuint32_t box[4] = {4, 8, kKC / 4, kUnit / 8};
+  cuuint32_t box[4] = {4, 8, kKC / 4, kUnit / 8};  // 4 x 8 x 8 x 16 = 128 c x 32 i
   cuuint32_t es[4] = {1, 1, 1, 1};
   CUresult r = tensor_map_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void *)X, dims, strides, box, es,
                                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,

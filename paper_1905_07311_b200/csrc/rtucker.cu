@@ -329,6 +329,20 @@ rtucker_status rtucker_debug_sketch(rtucker_ctx *ctx, const rtucker_dense_desc *
   });
 }
 
+rtucker_status rtucker_debug_ttm(rtucker_ctx *ctx, const rtucker_dense_desc *X, int32_t mode, const double *A,
+                                 int32_t J, uint32_t flags, double *out, double *gram) {
+  if (!ctx || !A || J < 1 || (!out && !gram)) return RTUCKER_EINVAL;
+  return guard(ctx, [&] {
+    DenseIn in;
+    prepare_dense(ctx->c, X, in);
+    RT_REQUIRE(mode >= 0 && mode < in.d, "mode out of range");
+    const ModeView v = mode_view(in.ldims, in.d, mode);
+    const uint32_t acc = flags & RTUCKER_ACCUM_MASK;
+    const bool f64 = in.dt == DT::F64 || acc == RTUCKER_ACCUM_FP64;
+    ttm_dense(ctx->c, in.ptr, in.dt, v, A, v.I, J, out, DT::F64, f64, gram);
+  });
+}
+
 rtucker_status rtucker_debug_omega(rtucker_ctx *ctx, rtucker_dtype dtype, uint64_t seed, int32_t mode,
                                    const int64_t *cols, int64_t n, int32_t ell, int64_t k0, void *out) {
   if (!ctx || !cols || !out || n < 0 || ell < 1 || k0 < 0) return RTUCKER_EINVAL;

@@ -12,7 +12,7 @@
 //                (fp32, DESIGN reading R3), one Philox block per thread and stage, split into
 //                hi/lo tf32 K-major tiles (NSG stages deep, so the long RNG dependency chain
 //                runs ahead of the X pipeline)
-//   warps 6-13   X workers: split X = hi + lo (hi = tf32 truncation, lo = X - hi exact) and
+//   warps 6-13   X workers: split X = hi + lo (both rounded to the tf32 grid, R15) and
 //                write both TRANSPOSED into K-major operand tiles (the tensor core reads tf32
 //                operands K-major only: MN-major tf32 A or B measured as all-zero output on
 //                this B200, scripts/dbg/tc_probe.cu); accumulate ||X||^2; after the last
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float hi = tc::tf32_hi(v);
             const int off = kmaj_off((int)n, kk) >> 2;
             oh[off] = hi;
-            ol[off] = v - hi;
+            ol[off] = tc::tf32_lo(v, hi);
           }
         }
       }
@@ -214,7 +214,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           float4 h, l;
           h.x = tc::tf32_hi(x[4 * cq]); h.y = tc::tf32_hi(x[4 * cq + 1]);
           h.z = tc::tf32_hi(x[4 * cq + 2]); h.w = tc::tf32_hi(x[4 * cq + 3]);
-          l.x = x[4 * cq] - h.x; l.y = x[4 * cq + 1] - h.y; l.z = x[4 * cq + 2] - h.z; l.w = x[4 * cq + 3] - h.w;
+          l.x = tc::tf32_lo(x[4 * cq], h.x); l.y = tc::tf32_lo(x[4 * cq + 1], h.y);
+          l.z = tc::tf32_lo(x[4 * cq + 2], h.z); l.w = tc::tf32_lo(x[4 * cq + 3], h.w);
           const int off = (i >> 3) * 256 + cq * 128 + (i & 7) * 16;
           *(float4 *)(hs + off) = h;
           *(float4 *)(ls + off) = l;
@@ -310,7 +311,8 @@ bool sketch_tc_enabled() {
 // Returns false when the shape is outside this kernel's envelope (caller falls back).
 bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0, uint64_t seed,
                   int64_t col_offset, double *Y, double *normsq) {
-  if (!sketch_tc_enabled() || v.L != 1 || (v.I % 4) != 0 || ell > 64 || ell < 1) return false;
+  static const bool off = getenv("RTUCKER_NO_TC_SKETCH") != nullptr;
+  if (off || !sketch_tc_enabled() || v.L != 1 || (v.I % 4) != 0 || ell > 64 || ell < 1) return false;
   const int N = ell <= 32 ? 32 : 64;
   const int NT = (int)((v.I + 127) / 128);
   if (NT * N > 512 || (((uintptr_t)X) & 15) != 0) return false;

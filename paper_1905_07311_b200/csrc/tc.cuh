@@ -127,10 +127,16 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn, bool 
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-// fp32 -> (hi, lo) with hi = x truncated to the tf32 grid (10 explicit mantissa bits) and
-// lo = x - hi exact in fp32; the tensor core then sees hi exactly, whatever its own
-// fp32->tf32 conversion does.
-__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+// fp32 -> tf32 grid (10 explicit mantissa bits), round to nearest (ties away from zero).
+// The tensor core itself TRUNCATES fp32 operands to tf32 (measured: scripts/dbg/tc_probe.cu
+// mode 14), which biases every product toward zero; splitting x = hi + lo with both parts
+// rounded to the tf32 grid gives operands the tensor core reads exactly and an unbiased
+// residual |x - hi - lo| <= 2^-22 |x|.
+__device__ __forceinline__ float tf32_rn(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+__device__ __forceinline__ float tf32_hi(float x) { return tf32_rn(x); }
+__device__ __forceinline__ float tf32_lo(float x, float hi) { return tf32_rn(x - hi); }
 
 }  // namespace tc
 }  // namespace rt

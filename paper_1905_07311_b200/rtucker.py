@@ -38,7 +38,7 @@ EXPORTED = [
     "rtucker_adaptive", "rtucker_sparse_sthosvd", "rtucker_result_free", "rtucker_memcpy", "rtucker_sync",
     "rtucker_rel_error", "rtucker_debug_sketch", "rtucker_debug_omega", "rtucker_debug_philox",
     "rtucker_debug_qr", "rtucker_debug_eig", "rtucker_debug_srrqr", "rtucker_set_profiling",
-    "rtucker_phase_times", "rtucker_debug_gram_eig",
+    "rtucker_phase_times", "rtucker_debug_gram_eig", "rtucker_debug_ttm",
 ]
 PHASES = ("sketch", "qr", "bpass", "eig", "shrink", "other")
 
@@ -109,6 +109,7 @@ def load_library(path: str = LIB_PATH):
         "rtucker_debug_eig": (C.c_int, [P, I32, P, P, P, C.POINTER(I32)]),
         "rtucker_debug_srrqr": (C.c_int, [P, I64, I32, P, D, P, P, C.POINTER(I32)]),
         "rtucker_debug_gram_eig": (C.c_int, [P, I32, P, P, P, C.POINTER(I32)]),
+        "rtucker_debug_ttm": (C.c_int, [P, C.POINTER(DenseDesc), I32, P, I32, U32, P, P]),
         "rtucker_set_profiling": (C.c_int, [P, C.c_int]),
         "rtucker_phase_times": (C.c_int, [P, P, P, C.c_int]),
     }
@@ -405,6 +406,22 @@ class Context:
                                                   int(flags), y.data_ptr()))
         self.sync()
         return y.cpu().numpy().reshape((int(dims[mode]), int(ell)), order="F")
+
+    def debug_ttm(self, x, dims, mode, a, flags=0, want_out=True, want_gram=True):
+        """B = A^T X_(mode) as (L, J, R) fp64 and its Gram (J x J)."""
+        torch = _torch()
+        desc, keep = self.dense_desc(x, dims)
+        at = torch.as_tensor(np.asfortranarray(a, dtype=np.float64).ravel(order="F"), device="cuda")
+        J = a.shape[1]
+        L = int(np.prod(dims[:mode], dtype=np.int64))
+        R = int(np.prod(dims[mode + 1:], dtype=np.int64))
+        out = torch.empty(L * J * R, dtype=torch.float64, device="cuda") if want_out else None
+        g = torch.empty(J * J, dtype=torch.float64, device="cuda") if want_gram else None
+        self._check(self.lib.rtucker_debug_ttm(self.h, C.byref(desc), int(mode), at.data_ptr(), int(J), int(flags),
+                                               out.data_ptr() if out is not None else None,
+                                               g.data_ptr() if g is not None else None))
+        self.sync()
+        return (out, g.cpu().numpy().reshape((J, J), order="F") if g is not None else None)
 
     def debug_omega(self, cols, ell, seed=0, mode=0, k0=0, dtype="f64"):
         torch = _torch()

@@ -55,6 +55,15 @@ __global__ void probe(const float *A, const float *B, float *D, int mode, int va
   }
   for (int idx = t; idx < 190 * 1024 / 4; idx += blockDim.x) ((float *)sa)[idx] = 0.f;
   __syncthreads();
+  if (mode == 14) {  // truncation test, K-major no swizzle: A(0,0) = 1+2^-11+2^-13, B(n,0) = 1
+    for (int idx = t; idx < 128 * 8; idx += blockDim.x) {
+      int m = idx % 128, k = idx / 128;
+      float v = (m == 0 && k == 0) ? 1.0f + 0x1p-11f + 0x1p-13f : ((m == 1 && k == 0) ? -(1.0f + 0x1p-11f + 0x1p-13f) : 0.f);
+      *(float *)(sa + (m / 8) * 256 + (k / 4) * 128 + (m % 8) * 16 + (k % 4) * 4) = v;
+    }
+    for (int idx = t; idx < 32 * 8; idx += blockDim.x) { int n = idx % 32, k = idx / 32;
+      *(float *)(sb + (n / 8) * 256 + (k / 4) * 128 + (n % 8) * 16 + (k % 4) * 4) = (k == 0) ? 1.f : 0.f; }
+  }
   if (mode == 13 && var < 2) {  // A K-major SW128, K slice 0
     for (int idx = t; idx < 128 * 32; idx += blockDim.x) {
       int m = idx % 128, k = idx / 128;
@@ -99,6 +108,10 @@ __global__ void probe(const float *A, const float *B, float *D, int mode, int va
       bd = mode == 9 ? tc::smem_desc(tc::smem_u32(sb), 1024, 128, tc::kSwNone) : tc::smem_desc(tc::smem_u32(sb), 1024, 1024, tc::kSw128);
       tc::mma_tf32(tm, ad, bd, tc::idesc_tf32(128, 32, false, true), 0);
     }
+    if (mode == 14) {
+      ad = tc::smem_desc(tc::smem_u32(sa), 128, 256, tc::kSwNone);
+      tc::mma_tf32(tm, ad, bd, tc::idesc_tf32(128, 32, false, false), 0);
+    }
     if (mode == 13) {
       if (var == 0) ad = tc::smem_desc(tc::smem_u32(sa), 16, 1024, tc::kSw128);
       if (var == 1) ad = tc::smem_desc(tc::smem_u32(sa), 0, 1024, tc::kSw128);
@@ -110,7 +123,7 @@ __global__ void probe(const float *A, const float *B, float *D, int mode, int va
       ad = tc::smem_desc(tc::smem_u32(sa) + 32, 16, 1024, tc::kSw128);
       tc::mma_tf32(tm, ad, bd, tc::idesc_tf32(128, 32, false, false), 0);
     }
-    if (mode != 3 && mode != 8 && mode < 9 && mode != 13) tc::mma_tf32(tm, ad, bd, tc::idesc_tf32(128, 32, mode != 4, false), 0);
+    if (mode != 3 && mode != 8 && mode < 9 && mode != 13 && mode != 14) tc::mma_tf32(tm, ad, bd, tc::idesc_tf32(128, 32, mode != 4, false), 0);
     tc::mma_commit(&bar);
   }
   if (mode == 8) {
@@ -161,6 +174,7 @@ int main(int argc, char **argv) {
     cudaMemcpy(hD, D, sizeof hD, cudaMemcpyDeviceToHost);
     double maxerr = 0, maxref = 0; int bad = 0;
     for (int i = 0; i < 128 * 32; ++i) { double d = fabs(hD[i] - ref[i]); if (d > maxerr) maxerr = d; if (fabs(ref[i]) > maxref) maxref = fabs(ref[i]); if (d > 1e-3) ++bad; }
+    if (mode == 14) { printf("trunc test: D[0]=%.9g D[1]=%.9g (1=truncation, %.9g=round-nearest)\n", hD[0], hD[1], 1.0 + 1.0 / 1024); continue; }
     if (mode == 12) { printf("trunc test: D[0]=%.9g (1=truncation, %.9g=round-nearest)\n", hD[0], 1.0 + 1.0 / 1024); continue; }
     printf("mode %d err=%s maxerr=%g maxref=%g bad=%d  D[0..3]=%g %g %g %g ref=%g %g %g %g D[128]=%g ref=%g\n", mode, cudaGetErrorString(e), maxerr, maxref, bad,
            hD[0], hD[1], hD[2], hD[3], ref[0], ref[1], ref[2], ref[3], hD[128], ref[128]);
