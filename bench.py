@@ -54,6 +54,33 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def fp64_peak_tflops():
+    """fp64 FMA peak derived from the measured DFMA issue rate (64 DFMA/clk/SM,
+    scripts/dbg/lat_probe2.cu on this pool's B200) x SMs x 2 flop x max SM clock."""
+    try:
+        import torch
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+    except Exception:
+        sms = 148
+    mhz = 1965.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", mhz))
+    except Exception:
+        pass
+    return sms * 64 * 2 * mhz * 1e6 / 1e12, f"derived: {sms} SMs x 64 DFMA/clk (measured) x 2 x {mhz:.0f} MHz"
+
+
+def load_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
+    captures (profiles/traffic.json, written by scripts/ncu_traffic.py); {} if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return {k: v["bytes_per_launch"] for k, v in json.load(f).items()}
+    except Exception:
+        return {}
+
+
 class Clocks:
     """nvidia-smi sampling during the timed region (clocks line of B200_PROFILING.md)."""
 
@@ -227,15 +254,39 @@ def main():
         ms = float(t.item())
     value = N_ELEM / (ms * 1e-3) / 1e9
 
-    # ---- roofline of the dominant kernel: the mode-1 sketch (reads X once)
+    # ---- rooflines: per-kernel algorithmic work / event-timed duration
     hbm, peak_src = peaks()
-    sk_ms, sk_n = phases.get(("sketch", 0), (0.0, 0))
-    bp_ms, bp_n = phases.get(("bpass", 0), (0.0, 0))
-    dom = "sketch_mode1"
-    t_kernel = sk_ms / max(sk_n, 1)
-    algo_bytes = BYTES_X // world + 0  # X read once; Y (800x60 fp64) is negligible
-    achieved = algo_bytes / (t_kernel * 1e-3) / 1e9 if t_kernel > 0 else 0.0
+    fp64_peak, fp64_src = fp64_peak_tflops()
     step_phase_ms = {f"{k[0]}{k[1] + 1}": round(v[0] / max(v[1], 1), 4) for k, v in sorted(phases.items())}
+    traffic = load_traffic()
+    kernels = []
+    sk_ms, sk_n = phases.get(("sketch", 0), (0.0, 0))
+    if sk_n:
+        t_k = sk_ms / sk_n
+        algo = BYTES_X // world  # X read once (Omega never touches HBM; Y partials stay in L2)
+        ach = algo / (t_k * 1e-3) / 1e9
+        kernels.append({"kernel": "sketch_tc_mn_kernel (mode-1 sketch, tcgen05 3xTF32)", "bound": "hbm",
+                        "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                        "traffic": traffic.get("sketch_tc_mn_kernel"), "ms": t_k,
+                        "algorithmic": f"{algo} B per launch (800^3 fp32 read once)"})
+    bp_ms, bp_n = phases.get(("bpass", 0), (0.0, 0))
+    if bp_n and args.algo == "sthosvd":
+        t_k = bp_ms / bp_n
+        flops = 2.0 * (RANKS[0] + P) * N_ELEM / world  # B = Q^T X_(1): 2 l flop per element (fp64 products)
+        ach = flops / (t_k * 1e-3) / 1e12
+        kernels.append({"kernel": "ttm_dfma_kernel (mode-1 B-pass + fp64 Gram, HYBRID policy)", "bound": "alu",
+                        "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
+                        "traffic": traffic.get("ttm_dfma_kernel<float, 1, 1>"), "ms": t_k,
+                        "algorithmic": f"{flops:.4g} fp64 flop per launch (2 l N, l = 60)",
+                        "peak_source": fp64_src})
+    dom = max(kernels, key=lambda k: k["ms"]) if kernels else None
+    roofline = None
+    if dom:
+        roofline = {k: dom[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
+        roofline["kernel"] = dom["kernel"]
+        roofline["kernel_ms"] = dom["ms"]
+        roofline["algorithmic"] = dom["algorithmic"]
+        roofline["peak_source"] = dom.get("peak_source", peak_src)
 
     # ---- end-to-end through the public API with HOST buffers (H2D + D2H inside the region)
     e2e = None
@@ -274,10 +325,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(args.algo, world),
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": algo_bytes, "kernel_ms": t_kernel,
-                         "bpass_mode1_ms": bp_ms / max(bp_n, 1)},
+            "roofline": roofline, "kernels": kernels,
             "phase_ms": step_phase_ms,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         }

@@ -69,7 +69,7 @@ T fetch(Ctx &c, const T *dev) {
 // AdaptRangeFinder on the mode-n unfolding of G (dims cur), threshold tau2 = tau^2.
 ModeOut adapt_mode(Ctx &c, const void *G, DT gt, const int64_t *cur, int d, int n, double tau2, int block,
                    uint64_t seed, double floor_abs, bool mul_f64, DT store, bool truncate, bool want_core,
-                   double *gnorm2_dev) {
+                   double *gnorm2_dev, bool fp32_data) {
   const ModeView v = mode_view(cur, d, n);
   const int64_t I = v.I;
   int64_t others = v.L * v.R;
@@ -90,7 +90,7 @@ ModeOut adapt_mode(Ctx &c, const void *G, DT gt, const int64_t *cur, int d, int 
     DevBuf<double> W(c, (size_t)I * bb);
     {
       PhaseScope ps(c, PH_SKETCH, n);
-      sketch_dense(c, G, gt, v, n, bb, k, seed, 0, mul_f64, W.p, nullptr);
+      sketch_dense(c, G, gt, v, n, bb, k, seed, 0, mul_f64, W.p, nullptr, fp32_data);
     }
     PhaseScope ps(c, PH_QR, n);
     if (k > 0) {  // W <- (I - Q Q^T) W, twice (re-orthogonalisation)
@@ -241,7 +241,7 @@ rtucker_result *run_adaptive(Ctx &c, const rtucker_dense_desc *X, double tol, in
     const int64_t *dims = hosvd ? in.gdims : cur;
     const bool mulf = f64 || st == DT::F64;
     ModeOut mo = adapt_mode(c, src, st, dims, d, n, tau2, block, seed, floor_abs, mulf, store, truncate, !hosvd,
-                            scal.p + 1);
+                            scal.p + 1, in.dt == DT::F32 && !f64);
     res->factors[n] = mo.A;
     res->ranks[n] = mo.r;
     res->ell[n] = mo.k;

@@ -56,7 +56,7 @@ void fill_header(rtucker_result *r, const DenseIn &in, const int32_t *ord, uint6
 // Sketch of the sharded last mode: local rows are complete; gather the row blocks of
 // all ranks into Y (I_glob x ell, column-major).  normsq gets the global ||G||^2.
 void sketch_last_sharded(Ctx &c, const DenseIn &in, const void *G, DT gt, const int64_t *cur, int ell,
-                         uint64_t seed, bool mulf64, double *Y, double *normsq) {
+                         uint64_t seed, bool mulf64, double *Y, double *normsq, bool n32) {
   const int d = in.d, n = d - 1;
   const ModeView v = mode_view(cur, d, n);  // v.I = local extent
   const int64_t ext = v.I;
@@ -78,7 +78,7 @@ void sketch_last_sharded(Ctx &c, const DenseIn &in, const void *G, DT gt, const 
   DevBuf<double> yl(c, (size_t)maxext * ell + 1);
   yl.zero();
   DevBuf<double> ytmp(c, (size_t)ext * ell);
-  sketch_dense(c, G, gt, v, n, ell, 0, seed, 0, mulf64, ytmp.p, yl.p + (size_t)maxext * ell);
+  sketch_dense(c, G, gt, v, n, ell, 0, seed, 0, mulf64, ytmp.p, yl.p + (size_t)maxext * ell, n32);
   RT_CUDA(cudaMemcpy2DAsync(yl.p, maxext * sizeof(double), ytmp.p, ext * sizeof(double), ext * sizeof(double),
                             ell, cudaMemcpyDeviceToDevice, c.stream));
   RT_CUDA(cudaMemcpyAsync(normsq, yl.p + (size_t)maxext * ell, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
@@ -140,11 +140,13 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
     {
       PhaseScope ps(c, PH_SKETCH, jj);
       if (!last_sharded) {
-        sketch_dense(c, G, gt, v, n, ell, 0, seed, col_offset_for(in, cur, n), pol.mul_f64, Y.p, Y.p + Ig * ell);
+        sketch_dense(c, G, gt, v, n, ell, 0, seed, col_offset_for(in, cur, n), pol.mul_f64, Y.p, Y.p + Ig * ell,
+                     in.dt == DT::F32 && !pol.mul_f64);
         allreduce_sum_f64(c, Y.p, (size_t)Ig * ell + 1);
         RT_CUDA(cudaMemcpyAsync(scal.p + 2 * n, Y.p + Ig * ell, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
       } else {
-        sketch_last_sharded(c, in, G, gt, cur, ell, seed, pol.mul_f64, Y.p, scal.p + 2 * n);
+        sketch_last_sharded(c, in, G, gt, cur, ell, seed, pol.mul_f64, Y.p, scal.p + 2 * n,
+                            in.dt == DT::F32 && !pol.mul_f64);
       }
     }
     // ---- Alg 1 line 2: thin QR
@@ -237,11 +239,12 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
     PhaseScope ps(c, PH_SKETCH, n);
     if (!last_sharded) {
       sketch_dense(c, in.ptr, in.dt, v, n, ell, 0, seed, col_offset_for(in, in.ldims, n), pol.mul_f64, Y.p,
-                   Y.p + Ig * ell);
+                   Y.p + Ig * ell, in.dt == DT::F32 && !pol.mul_f64);
       allreduce_sum_f64(c, Y.p, (size_t)Ig * ell + 1);
       RT_CUDA(cudaMemcpyAsync(scal.p + 2 * n, Y.p + Ig * ell, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
     } else {
-      sketch_last_sharded(c, in, in.ptr, in.dt, in.ldims, ell, seed, pol.mul_f64, Y.p, scal.p + 2 * n);
+      sketch_last_sharded(c, in, in.ptr, in.dt, in.ldims, ell, seed, pol.mul_f64, Y.p, scal.p + 2 * n,
+                          in.dt == DT::F32 && !pol.mul_f64);
     }
     ps.next(PH_QR);
     DevBuf<double> Q(c, (size_t)Ig * ell);

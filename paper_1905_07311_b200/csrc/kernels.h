@@ -23,8 +23,12 @@ inline ModeView mode_view(const int64_t *dims, int d, int n) {
 // Y (I x ell, fp64 col-major) = X_(n) Omega_n(:, k0:k0+ell) with Omega rows indexed by
 // c + col_offset (global column).  normsq (optional, device scalar) <- ||X||_F^2.
 // mul_f64: multiply in fp64 (else fp32 products with fp64 accumulation every 32 terms).
+// Normals (reading R3): products in fp32 (FAST) draw fp32 normals; products in fp64 draw fp64
+// normals unless normals_f32 (fp32 input under the HYBRID policy, whose later passes run in
+// fp64 on fp64 intermediates but keep the fp32 data's Omega).
 void sketch_dense(Ctx &c, const void *X, DT in, ModeView v, int mode, int ell, int64_t k0,
-                  uint64_t seed, int64_t col_offset, bool mul_f64, double *Y, double *normsq);
+                  uint64_t seed, int64_t col_offset, bool mul_f64, double *Y, double *normsq,
+                  bool normals_f32 = false);
 
 // sketch_tc.cu: tcgen05 3xTF32 variant for fp32 data with L == 1 (MN-major rows); returns
 // false when the shape is outside its envelope.

@@ -194,6 +194,137 @@ void launch_sketch(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int64_t 
   if (normsq) sum_vec(c, npart.p, (int64_t)nsplit * gx, normsq);
 }
 
+// ------------------------------------------------------------ fp64-product sketch ----
+// Y[i, k] = sum_p X(l, i, r) Omega(p, k), p = l + L r, with fp64 products and sums (X fp32
+// or fp64; normals fp32 or fp64 per reading R3).  A CTA owns 128 rows x 64 sketch columns
+// and a contiguous range of p (split-K); thread (ti, tk) the rows ti + 16 u (u < 8) and the
+// columns 4 tk .. 4 tk + 3.  X and Omega are staged 16 values of p at a time (Omega
+// generated into shared memory: ceil(I/128) row tiles regenerate it, 0.5 normals per element
+// at most); partials per split are summed in a fixed order (deterministic).
+constexpr int kSP = 16;  // p per chunk
+template <typename Tin, typename TN>
+__global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict__ X, int64_t L, int64_t I, int64_t R,
+                                                          int64_t cols_per_split, uint64_t seed, int mode, int ell,
+                                                          int64_t k0, int64_t col_offset, double *__restrict__ partial,
+                                                          double *__restrict__ norm_partial) {
+  __shared__ double Xs[kSP][128 + 1];
+  __shared__ __align__(16) double Os[kSP][64];
+  __shared__ double sred[8];
+  const int tid = threadIdx.x, ti = tid & 15, tk = tid >> 4;
+  const int64_t i0 = (int64_t)blockIdx.x * 128;
+  const int64_t P = L * R;
+  const int64_t pbeg = (int64_t)blockIdx.y * cols_per_split, pend = min(P, pbeg + cols_per_split);
+  const int64_t jb0 = k0 >> 2;
+  const int nb = (int)(((k0 + ell - 1) >> 2) - jb0 + 1);
+  double acc[8][4];
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+  double nsq = 0.0;
+  for (int e = tid; e < kSP * 64; e += 256) Os[e >> 6][e & 63] = 0.0;
+  for (int64_t p0 = pbeg; p0 < pend; p0 += kSP) {
+    __syncthreads();
+    // X chunk: rows i0.., columns p0.. (fp64)
+    if (L == 1) {  // X[i + I p]: coalesced along i
+      for (int e = tid; e < kSP * 128; e += 256) {
+        const int ii = e & 127, pp = e >> 7;
+        const int64_t i = i0 + ii, p = p0 + pp;
+        double v = 0.0;
+        if (i < I && p < pend) {
+          v = (double)X[i + I * p];
+          nsq = fma(v, v, nsq);
+        }
+        Xs[pp][ii] = v;
+      }
+    } else {  // coalesced along p (= l)
+      const int64_t pl0 = p0 % L, pr0 = p0 / L;
+      for (int e = tid; e < kSP * 128; e += 256) {
+        const int pp = e % kSP, ii = e / kSP;
+        const int64_t i = i0 + ii, p = p0 + pp;
+        double v = 0.0;
+        if (i < I && p < pend) {
+          int64_t l = pl0 + pp, r = pr0;
+          while (l >= L) { l -= L; ++r; }
+          v = (double)X[l + L * (i + I * r)];
+          nsq = fma(v, v, nsq);
+        }
+        Xs[pp][ii] = v;
+      }
+    }
+    // Omega chunk: rows p0.., columns k0.. (Philox block granularity)
+    for (int e = tid; e < kSP * nb; e += 256) {
+      const int pp = e / nb, jb = e % nb;
+      const int64_t p = p0 + pp;
+      if (p >= pend) continue;
+      const uint4 w = omega_words(seed, mode, 0, (uint64_t)(p + col_offset), (uint32_t)(jb0 + jb));
+      Normal4<TN> z(w);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t kk = 4 * (jb0 + jb) + q - k0;
+        if (kk >= 0 && kk < ell) Os[pp][kk] = (double)z.v[q];
+      }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int pp = 0; pp < kSP; ++pp) {
+      double a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = Xs[pp][ti + 16 * u];
+      const double2 b01 = *reinterpret_cast<const double2 *>(&Os[pp][4 * tk]);
+      const double2 b23 = *reinterpret_cast<const double2 *>(&Os[pp][4 * tk + 2]);
+      const double b[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[u][q] = fma(a[u], b[q], acc[u][q]);
+    }
+  }
+  double *dst = partial + (int64_t)blockIdx.y * I * ell;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int64_t i = i0 + ti + 16 * u;
+    if (i >= I) continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = 4 * tk + q;
+      if (k < ell) dst[(int64_t)k * I + i] = acc[u][q];
+    }
+  }
+  if (norm_partial) {
+    for (int o = 16; o; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
+    if ((tid & 31) == 0) sred[tid >> 5] = nsq;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < 8; ++w) t += sred[w];
+      norm_partial[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+  }
+}
+
+template <typename Tin, typename TN>
+void launch_sketch_dfma(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int64_t k0, uint64_t seed,
+                        int64_t col_offset, double *Y, double *normsq) {
+  const int gx = ceil_div(v.I, 128);
+  const int64_t P = v.L * v.R;
+  int64_t target = std::max<int64_t>(1, (int64_t)c.num_sms * 3 / gx);
+  int64_t maxsplit = std::max<int64_t>(1, P / (4 * kSP));
+  int64_t nsplit = std::min<int64_t>(target, maxsplit);
+  int64_t cps = ((P + nsplit - 1) / nsplit + kSP - 1) / kSP * kSP;
+  nsplit = (P + cps - 1) / cps;
+  DevBuf<double> part(c, (size_t)nsplit * v.I * ell);
+  DevBuf<double> npart;
+  if (normsq) npart.alloc(c, (size_t)nsplit * gx);
+  dim3 grid(gx, (unsigned)nsplit);
+  RT_LAUNCH(c, (sketch_dfma_kernel<Tin, TN>), grid, 256, 0, X, v.L, v.I, v.R, cps, seed, mode, ell, k0, col_offset,
+            part.p, normsq ? npart.p : nullptr);
+  const int64_t n = v.I * ell;
+  RT_LAUNCH(c, reduce_splits_kernel, ceil_div(n, 256) > 1024 ? 1024 : ceil_div(n, 256), 256, 0, part.p, (int)nsplit, n,
+            Y);
+  if (normsq) sum_vec(c, npart.p, (int64_t)nsplit * gx, normsq);
+}
+
 template <typename Tin, typename Tmul>
 void sketch_dispatch(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int64_t k0,
                      uint64_t seed, int64_t col_offset, double *Y, double *normsq) {
@@ -217,16 +348,24 @@ void sketch_dispatch(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int64_
 }  // namespace
 
 void sketch_dense(Ctx &c, const void *X, DT in, ModeView v, int mode, int ell, int64_t k0,
-                  uint64_t seed, int64_t col_offset, bool mul_f64, double *Y, double *normsq) {
-  if (in == DT::F64)
-    sketch_dispatch<double, double>(c, (const double *)X, v, mode, ell, k0, seed, col_offset, Y,
-                                    normsq);
-  else if (mul_f64)
-    sketch_dispatch<float, double>(c, (const float *)X, v, mode, ell, k0, seed, col_offset, Y,
-                                   normsq);
-  else
-    sketch_dispatch<float, float>(c, (const float *)X, v, mode, ell, k0, seed, col_offset, Y,
-                                  normsq);
+                  uint64_t seed, int64_t col_offset, bool mul_f64, double *Y, double *normsq, bool normals_f32) {
+  if (in == DT::F64 || mul_f64) {
+    // fp64 products: DFMA kernel in column blocks of <= 64 (norm fused into the first block)
+    for (int kb = 0; kb < ell; kb += 64) {
+      const int e = std::min(64, ell - kb);
+      double *Yb = Y + (int64_t)kb * v.I;
+      double *ns = kb == 0 ? normsq : nullptr;
+      if (in == DT::F64) {
+        if (normals_f32) launch_sketch_dfma<double, float>(c, (const double *)X, v, mode, e, k0 + kb, seed, col_offset, Yb, ns);
+        else launch_sketch_dfma<double, double>(c, (const double *)X, v, mode, e, k0 + kb, seed, col_offset, Yb, ns);
+      } else {  // fp32 data with the FP64 policy
+        if (normals_f32) launch_sketch_dfma<float, float>(c, (const float *)X, v, mode, e, k0 + kb, seed, col_offset, Yb, ns);
+        else launch_sketch_dfma<float, double>(c, (const float *)X, v, mode, e, k0 + kb, seed, col_offset, Yb, ns);
+      }
+    }
+    return;
+  }
+  sketch_dispatch<float, float>(c, (const float *)X, v, mode, ell, k0, seed, col_offset, Y, normsq);
 }
 
 void omega_rows(Ctx &c, DT out, uint64_t seed, int mode, const int64_t *cols, int64_t n, int ell,

@@ -112,3 +112,18 @@ def test_sparse_invalid(ctx):
         with pytest.raises(RTuckerError) as e:
             _run(ctx, idx, vals, (3, 3, 3), a["ranks"], a["p"], eta=a["eta"], device=False)
         assert e.value.name == "EINVAL", kw
+
+
+@pytest.mark.slow
+def test_zipf_full_scale_c5(ctx):
+    """BASELINE configs[4] at full scale (50M draws -> ~40.7M nnz), against the oracle."""
+    import time
+    idx, vals = sparse_zipf()
+    dims = (8000, 8000, 200000, 1200)
+    t0 = time.perf_counter()
+    g = _run(ctx, idx, vals, dims, (10, 10, 10, 10), 5, seed=0)
+    t1 = time.perf_counter()
+    o = O.sp_sthosvd(idx, vals, dims, (10, 10, 10, 10), 5, seed=0)
+    t2 = time.perf_counter()
+    print(f"C5 nnz={idx.shape[1]} gpu {t1 - t0:.3f}s (incl. H2D) oracle {t2 - t1:.1f}s nnz chain {g.nnz_history}")
+    _check(g, o, 2.0, 1e-4)
