@@ -174,13 +174,58 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def bench_sparse(args):
+    """SP-STHOSVD (Alg 6) of BASELINE configs[4] (C5: 4-mode Zipf(1.1) counts, 50M draws ->
+    ~40.7M nnz, r = 10, p = 5), COO resident in HBM; metric = input nnz / step time.  Single GPU
+    (the nnz-partitioned multi-GPU path is not built yet: DESIGN §12)."""
+    import numpy as np
+    import torch
+    from paper_1905_07311_b200.rtucker import Context
+    from workloads import sparse_zipf
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    dims = (8000, 8000, 200000, 1200)
+    idx, vals = sparse_zipf()
+    it = torch.as_tensor(idx, device="cuda")
+    vt = torch.as_tensor(vals, device="cuda")
+    stream = torch.cuda.Stream()
+    ctx = Context(0, stream=stream)
+    step = lambda: ctx.sparse_sthosvd(it, vt, dims, (10, 10, 10, 10), 5, SEED, None, 2.0)
+    for _ in range(args.warmup):
+        step().free()
+    torch.cuda.synchronize()
+    ctx.set_profiling(True)
+    ctx.phase_times(reset=True)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ctx.launches
+    e0.record(stream)
+    hist = None
+    for _ in range(args.steps):
+        r = step()
+        hist = [int(r.s.nnz_history[k]) for k in range(5)]
+        r.free()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    phases = {f"{k[0]}{k[1] + 1}": round(v[0] / max(v[1], 1), 4) for k, v in sorted(ctx.phase_times().items())}
+    nnz = idx.shape[1]
+    line = {"metric": "SP-STHOSVD Gnnz/s (C5 8000x8000x200000x1200, 50M Zipf(1.1) draws, r=10, p=5)",
+            "value": nnz / (ms * 1e-3) / 1e9, "unit": "Gnnz/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 values, fp64 sketch sums", "data": "synthetic",
+            "config": {"workload": "C5 sparse_zipf data seed 5, SP-STHOSVD rho=auto [3,1,2,4], eta=2",
+                       "nnz": nnz, "nnz_chain": hist},
+            "phase_ms": phases, "gpu_launches": (ctx.launches - l0) // args.steps}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--algo", default="sthosvd", choices=["sthosvd", "hosvd"])
+    ap.add_argument("--algo", default="sthosvd", choices=["sthosvd", "hosvd", "sparse"])
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -189,6 +234,8 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
+    if args.algo == "sparse":
+        return bench_sparse(args)
     import numpy as np
     import torch
     import torch.distributed as dist

@@ -194,6 +194,12 @@ rtucker_status rtucker_phase_times(rtucker_ctx *ctx, double *ms, int64_t *counts
 
 /* ---- measurement / debug exports (not part of the method) ---------------------- */
 
+/* Single-rank loopback of the sharded dense path: with enabled != 0, a descriptor whose
+ * shard covers the whole last mode (shard_offset 0, shard_extent = dims[d-1]) runs the
+ * multi-rank code path (global column offsets, row-block gather of the last mode, B_d
+ * reduction) with the collectives degenerating to local copies.  nranks must be 1. */
+rtucker_status rtucker_debug_loopback_sharding(rtucker_ctx *ctx, int enabled);
+
 /* ||X - X_hat||_F / ||X||_F for a dense result, computed on the device. */
 rtucker_status rtucker_rel_error(rtucker_ctx *ctx, const rtucker_dense_desc *X,
                                  const rtucker_result *res, double *out);

@@ -59,6 +59,7 @@ struct Ctx {
   int num_sms = 148;
   std::string last_error;
   bool profiling = false;
+  bool loopback_sharding = false;  // debug: run the sharded path on one rank (full slab)
   std::vector<PhaseEvent> events;
   double phase_ms[PH_COUNT * kMaxModes] = {0};
   int64_t phase_n[PH_COUNT * kMaxModes] = {0};

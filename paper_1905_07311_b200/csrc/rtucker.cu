@@ -39,7 +39,7 @@ void prepare_dense(Ctx &c, const rtucker_dense_desc *X, DenseIn &in) {
     in.gdims[k] = X->dims[k];
     in.ldims[k] = X->dims[k];
   }
-  in.sharded = X->shard_extent > 0 && (X->shard_extent != X->dims[in.d - 1] || c.nranks > 1);
+  in.sharded = X->shard_extent > 0 && (X->shard_extent != X->dims[in.d - 1] || c.nranks > 1 || c.loopback_sharding);
   in.offset = 0;
   if (X->shard_extent > 0) {
     RT_REQUIRE(X->shard_offset >= 0 && X->shard_offset + X->shard_extent <= X->dims[in.d - 1],
@@ -47,7 +47,8 @@ void prepare_dense(Ctx &c, const rtucker_dense_desc *X, DenseIn &in) {
     in.ldims[in.d - 1] = X->shard_extent;
     in.offset = X->shard_offset;
   }
-  RT_REQUIRE(!in.sharded || c.nranks > 1, "a partial shard needs a multi-rank context");
+  RT_REQUIRE(!in.sharded || c.nranks > 1 || (c.loopback_sharding && X->shard_extent == X->dims[in.d - 1]),
+             "a partial shard needs a multi-rank context");
   const int64_t n = prod(in.ldims, in.d);
   if (X->memory == RTUCKER_HOST) {
     in.owned.alloc(c, n * dt_size(in.dt));
@@ -177,6 +178,12 @@ rtucker_status rtucker_memcpy(rtucker_ctx *ctx, void *dst, const void *src, size
 rtucker_status rtucker_sync(rtucker_ctx *ctx) {
   if (!ctx) return RTUCKER_EINVAL;
   return guard(ctx, [&] { RT_CUDA(cudaStreamSynchronize(ctx->c.stream)); });
+}
+
+rtucker_status rtucker_debug_loopback_sharding(rtucker_ctx *ctx, int enabled) {
+  if (!ctx || ctx->c.nranks != 1) return RTUCKER_EINVAL;
+  ctx->c.loopback_sharding = enabled != 0;
+  return RTUCKER_OK;
 }
 
 rtucker_status rtucker_set_profiling(rtucker_ctx *ctx, int enabled) {

@@ -20,20 +20,29 @@ namespace rt {
 
 namespace {
 
-constexpr int kCacheRows = 1024;  // rows of Y accumulated per CTA in shared memory
+constexpr int kHot = 32;      // hottest rows (smallest indices) kept warp-private per CTA
+constexpr int kCooT = 256;
+constexpr int kMaxEll = 64;
 
 // ---------------------------------------------------------------- COO sketch (a8) --
 // Y[i_j, k] += v * Omega_j[c, k0 + k], c = sum_{m != j} i_m prod_{m' < m, m' != j} I_m'.
-// Products and sums in fp64.  Rows < kCacheRows (the heavy rows of the Zipf-skewed count
-// tensors of BASELINE configs[4], whose mass sits at small indices) are pre-aggregated per
-// CTA in shared memory and flushed once; other rows use global fp64 atomics.
+// Products and sums in fp64.  Count tensors are heavy-tailed (BASELINE configs[4]: Zipf(1.1)
+// indices, the heaviest mode-3 row holds ~9 % of the nonzeros), so naive atomics serialise
+// on a few addresses.  Per warp instruction, lanes holding the same row are first combined
+// with __match_any_sync + a leader reduction (one update per distinct row and warp); rows
+// < kHot (the heavy rows of these tensors) then go to a warp-private shared-memory
+// accumulator (no atomics: one writer lane per row per instruction), flushed once per CTA;
+// other rows use one fp64 global atomic per distinct row and warp.  Global fp64 atomics make
+// the sum order run-dependent (rounding-level differences only).
 template <typename TV, typename TN>
-__global__ void __launch_bounds__(256) sketch_coo_kernel(CooDev g, int mode, int ell, uint64_t seed,
-                                                         int64_t nper, double *__restrict__ Y) {
-  extern __shared__ double cache[];  // [crows][ell]
+__global__ void __launch_bounds__(kCooT) sketch_coo_kernel(CooDev g, int mode, int ell, uint64_t seed,
+                                                           int64_t nper, double *__restrict__ Y) {
+  extern __shared__ double hot[];  // [warps][kHot][ell]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t I = g.dims[mode];
-  const int crows = (int)(I < kCacheRows ? I : kCacheRows);
-  for (int e = threadIdx.x; e < crows * ell; e += blockDim.x) cache[e] = 0.0;
+  const int hrows = (int)(I < kHot ? I : kHot);
+  double *myhot = hot + (size_t)warp * kHot * ell;
+  for (int e = threadIdx.x; e < (kCooT / 32) * kHot * ell; e += kCooT) hot[e] = 0.0;
   __syncthreads();
   int64_t stride[kMaxModes];
   int64_t s = 1;
@@ -44,29 +53,59 @@ __global__ void __launch_bounds__(256) sketch_coo_kernel(CooDev g, int mode, int
   const TV *vals = (const TV *)g.vals;
   const int nb = (ell + 3) >> 2;
   const int64_t e0 = (int64_t)blockIdx.x * nper, e1 = min(g.nnz, e0 + nper);
-  for (int64_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+  // warp-strided loop with uniform trip count (inactive lanes carry row = -1)
+  for (int64_t base = e0 + (int64_t)warp * 32; base < e1; base += kCooT) {
+    const int64_t e = base + lane;
+    const bool act = e < e1;
     int64_t c = 0;
-    for (int k = 0; k < g.d; ++k) c += (int64_t)g.idx[k][e] * stride[k];
-    const int64_t row = g.idx[mode][e];
-    const double v = (double)vals[e];
+    int row = -1;
+    double v = 0.0;
+    if (act) {
+      for (int k = 0; k < g.d; ++k) c += (int64_t)g.idx[k][e] * stride[k];
+      row = g.idx[mode][e];
+      v = (double)vals[e];
+    }
+    const unsigned grp = __match_any_sync(0xffffffffu, row);
+    const int leader = __ffs(grp) - 1;
     for (int jb = 0; jb < nb; ++jb) {
-      const uint4 w = omega_words(seed, mode, 0, (uint64_t)c, (uint32_t)jb);
-      Normal4<TN> z(w);
+      float4 dummy;
+      (void)dummy;
+      double pr[4] = {0.0, 0.0, 0.0, 0.0};
+      if (act) {
+        const uint4 w = omega_words(seed, mode, 0, (uint64_t)c, (uint32_t)jb);
+        Normal4<TN> z(w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pr[q] = v * (double)z.v[q];
+      }
+      // sum over the lanes of this row group (fixed order: by lane index)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int k = 4 * jb + q;
-        if (k < ell) {
-          const double pr = v * (double)z.v[q];
-          if (row < crows) atomicAdd(&cache[row * ell + k], pr);
-          else atomicAdd(&Y[row + I * k], pr);
+        double t = 0.0;
+        unsigned m = grp;
+        while (m) {
+          const int src = __ffs(m) - 1;
+          t += __shfl_sync(grp, pr[q], src);
+          m &= m - 1;
+        }
+        pr[q] = t;
+      }
+      if (act && lane == leader) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int k = 4 * jb + q;
+          if (k < ell) {
+            if (row < hrows) myhot[row * ell + k] += pr[q];
+            else atomicAdd(&Y[row + I * k], pr[q]);
+          }
         }
       }
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < crows * ell; e += blockDim.x) {
-    const double v = cache[e];
-    if (v != 0.0) atomicAdd(&Y[(e / ell) + I * (e % ell)], v);
+  for (int e = threadIdx.x; e < hrows * ell; e += kCooT) {
+    double t = 0.0;
+    for (int w = 0; w < kCooT / 32; ++w) t += hot[(size_t)w * kHot * ell + e];
+    if (t != 0.0) atomicAdd(&Y[(e / ell) + I * (e % ell)], t);
   }
 }
 
@@ -354,17 +393,17 @@ int grid_for(Ctx &c, int64_t n, int threads = 256) {
 
 void sketch_coo(Ctx &c, const CooDev &g, int mode, int ell, uint64_t seed, bool normals_f64, double *Y) {
   const int64_t I = g.dims[mode];
+  RT_REQUIRE(ell <= kMaxEll, "sparse sketch: l > 64 is not supported");
   RT_CUDA(cudaMemsetAsync(Y, 0, sizeof(double) * I * ell, c.stream));
   if (g.nnz == 0) return;
-  const int crows = (int)std::min<int64_t>(I, kCacheRows);
-  const size_t smem = sizeof(double) * crows * ell;
+  const size_t smem = sizeof(double) * (kCooT / 32) * kHot * ell;
   const int64_t blocks = std::min<int64_t>((int64_t)c.num_sms * 4, (g.nnz + 1023) / 1024);
   const int64_t nper = (g.nnz + blocks - 1) / blocks;
-#define RT_COO(TV, TN)                                                                                    \
-  do {                                                                                                    \
-    RT_CUDA(cudaFuncSetAttribute(sketch_coo_kernel<TV, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                 (int)smem));                                                             \
-    RT_LAUNCH(c, (sketch_coo_kernel<TV, TN>), (int)blocks, 256, smem, g, mode, ell, seed, nper, Y);       \
+#define RT_COO(TV, TN)                                                                                     \
+  do {                                                                                                     \
+    RT_CUDA(cudaFuncSetAttribute(sketch_coo_kernel<TV, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                                 (int)smem));                                                              \
+    RT_LAUNCH(c, (sketch_coo_kernel<TV, TN>), (int)blocks, kCooT, smem, g, mode, ell, seed, nper, Y);      \
   } while (0)
   if (g.vt == DT::F64) {
     RT_COO(double, double);

@@ -38,7 +38,7 @@ EXPORTED = [
     "rtucker_adaptive", "rtucker_sparse_sthosvd", "rtucker_result_free", "rtucker_memcpy", "rtucker_sync",
     "rtucker_rel_error", "rtucker_debug_sketch", "rtucker_debug_omega", "rtucker_debug_philox",
     "rtucker_debug_qr", "rtucker_debug_eig", "rtucker_debug_srrqr", "rtucker_set_profiling",
-    "rtucker_phase_times", "rtucker_debug_gram_eig", "rtucker_debug_ttm",
+    "rtucker_phase_times", "rtucker_debug_gram_eig", "rtucker_debug_ttm", "rtucker_debug_loopback_sharding",
 ]
 PHASES = ("sketch", "qr", "bpass", "eig", "shrink", "other")
 
@@ -110,6 +110,7 @@ def load_library(path: str = LIB_PATH):
         "rtucker_debug_srrqr": (C.c_int, [P, I64, I32, P, D, P, P, C.POINTER(I32)]),
         "rtucker_debug_gram_eig": (C.c_int, [P, I32, P, P, P, C.POINTER(I32)]),
         "rtucker_debug_ttm": (C.c_int, [P, C.POINTER(DenseDesc), I32, P, I32, U32, P, P]),
+        "rtucker_debug_loopback_sharding": (C.c_int, [P, C.c_int]),
         "rtucker_set_profiling": (C.c_int, [P, C.c_int]),
         "rtucker_phase_times": (C.c_int, [P, P, P, C.c_int]),
     }
@@ -295,6 +296,9 @@ class Context:
 
     def sync(self):
         self._check(self.lib.rtucker_sync(self.h))
+
+    def loopback_sharding(self, on: bool = True):
+        self._check(self.lib.rtucker_debug_loopback_sharding(self.h, 1 if on else 0))
 
     def set_profiling(self, on: bool = True):
         self._check(self.lib.rtucker_set_profiling(self.h, 1 if on else 0))

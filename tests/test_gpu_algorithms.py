@@ -209,3 +209,29 @@ def test_c4_full_size_rsthosvd(ctx):
         t = O.mode_product(t, g.factors[j].T @ o.factors[j], j)
     d2 = np.sum(g.core ** 2) + np.sum(o.core ** 2) - 2 * np.sum(g.core * t)
     assert np.sqrt(max(d2, 0.0) / nx2) <= 1e-5
+
+
+@pytest.mark.parametrize("algo", ["sthosvd", "hosvd"])
+@pytest.mark.parametrize("name,make,ranks,p", [
+    ("c1", lambda: hilbert((50, 50, 50), "shifted"), (5, 5, 5), 5),
+    ("ragged4", lambda: np.asfortranarray(np.random.default_rng(8).standard_normal((9, 7, 11, 13))), (3, 2, 4, 5), 2),
+    ("odeco96_f32", lambda: odeco(96, seed=4, dtype=np.float32), (12, 12, 12), 10),
+])
+def test_sharded_path_loopback(ctx, algo, name, make, ranks, p):
+    """The multi-rank dense path (last-mode slab, global Omega columns, row-block gather of the
+    last mode, B_d reduction) run on one rank must reproduce the oracle."""
+    import torch
+    from paper_1905_07311_b200.rtucker import RESULT_HOST
+    x = make()
+    d = x.ndim
+    xd = torch.as_tensor(to_first_mode_fastest(x), device="cuda")
+    ctx.loopback_sharding(True)
+    try:
+        if algo == "sthosvd":
+            g = ctx.sthosvd(xd, x.shape, ranks, p, 1, tuple(range(d)), RESULT_HOST, shard=(0, x.shape[-1])).numpy()
+        else:
+            g = ctx.hosvd(xd, x.shape, ranks, p, 1, RESULT_HOST, shard=(0, x.shape[-1])).numpy()
+    finally:
+        ctx.loopback_sharding(False)
+    o = _oracle(algo, x, ranks, p, 1, tuple(range(d)))
+    _check(x, g, o, x.dtype == np.float64)
