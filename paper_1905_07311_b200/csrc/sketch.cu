@@ -223,34 +223,42 @@ __global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict_
     for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
   double nsq = 0.0;
   for (int e = tid; e < kSP * 64; e += 256) Os[e >> 6][e & 63] = 0.0;
-  for (int64_t p0 = pbeg; p0 < pend; p0 += kSP) {
-    __syncthreads();
-    // X chunk: rows i0.., columns p0.. (fp64)
-    if (L == 1) {  // X[i + I p]: coalesced along i
-      for (int e = tid; e < kSP * 128; e += 256) {
-        const int ii = e & 127, pp = e >> 7;
-        const int64_t i = i0 + ii, p = p0 + pp;
-        double v = 0.0;
-        if (i < I && p < pend) {
-          v = (double)X[i + I * p];
-          nsq = fma(v, v, nsq);
-        }
-        Xs[pp][ii] = v;
-      }
-    } else {  // coalesced along p (= l)
-      const int64_t pl0 = p0 % L, pr0 = p0 / L;
-      for (int e = tid; e < kSP * 128; e += 256) {
-        const int pp = e % kSP, ii = e / kSP;
-        const int64_t i = i0 + ii, p = p0 + pp;
-        double v = 0.0;
-        if (i < I && p < pend) {
+  // X staging with a register prefetch of the next chunk (8 values per thread and chunk)
+  //   L == 1: element e = tid + 256 q: row ii = e & 127, column pp = e >> 7 (coalesced along i)
+  //   L > 1 : element e: column pp = e % 16, row ii = e / 16 (coalesced along p = l)
+  Tin pre[kSP * 128 / 256];
+  auto load_x = [&](int64_t p0) {
+    const int64_t pl0 = p0 % L, pr0 = p0 / L;
+#pragma unroll
+    for (int q = 0; q < kSP * 128 / 256; ++q) {
+      const int e = tid + 256 * q;
+      int ii, pp;
+      if (L == 1) { ii = e & 127; pp = e >> 7; } else { pp = e % kSP; ii = e / kSP; }
+      const int64_t i = i0 + ii, p = p0 + pp;
+      Tin v = Tin(0);
+      if (i < I && p < pend) {
+        if (L == 1) {
+          v = X[i + I * p];
+        } else {
           int64_t l = pl0 + pp, r = pr0;
           while (l >= L) { l -= L; ++r; }
-          v = (double)X[l + L * (i + I * r)];
-          nsq = fma(v, v, nsq);
+          v = X[l + L * (i + I * r)];
         }
-        Xs[pp][ii] = v;
       }
+      pre[q] = v;
+    }
+  };
+  if (pbeg < pend) load_x(pbeg);
+  for (int64_t p0 = pbeg; p0 < pend; p0 += kSP) {
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kSP * 128 / 256; ++q) {
+      const int e = tid + 256 * q;
+      int ii, pp;
+      if (L == 1) { ii = e & 127; pp = e >> 7; } else { pp = e % kSP; ii = e / kSP; }
+      const double v = (double)pre[q];
+      nsq = fma(v, v, nsq);
+      Xs[pp][ii] = v;
     }
     // Omega chunk: rows p0.., columns k0.. (Philox block granularity)
     for (int e = tid; e < kSP * nb; e += 256) {
@@ -266,6 +274,7 @@ __global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict_
       }
     }
     __syncthreads();
+    if (p0 + kSP < pend) load_x(p0 + kSP);  // in flight during the DFMA block
 #pragma unroll 4
     for (int pp = 0; pp < kSP; ++pp) {
       double a[8];

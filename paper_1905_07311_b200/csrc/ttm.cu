@@ -464,7 +464,36 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dfma_kernel(const Tin *__restrict_
       }
     }
     // ---- epilogue: thread holds out(j = 8 warp + u, p = p0 + 2 lane + 64 (v / 2) + v % 2)
-    if (STORE) {
+    if (STORE && L == 1) {
+      // out[j + J p]: the tile is ONE contiguous range of J * 256 doubles; stage it [p][J] in
+      // shared memory (two halves of 128 columns) and write it with coalesced 16-B stores
+      for (int h = 0; h < 2; ++h) {
+        __syncthreads();
+        double *T = dsm;  // [128][J]
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const int pp = 2 * lane + 64 * (v >> 1) + (v & 1);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int j = 8 * warp + u;
+            if (j < J) T[pp * J + j] = acc[u][4 * h + v];
+          }
+        }
+        __syncthreads();
+        const int64_t pb = p0 + 128 * h;
+        const int64_t ncol = P - pb < 128 ? (P - pb) : 128;
+        if (ncol > 0) {
+          const int64_t n = ncol * J;
+          double *dst = out + pb * J;
+          if (((J & 1) == 0)) {
+            for (int64_t e = 2 * tid; e < n; e += 2 * kDT)
+              *reinterpret_cast<double2 *>(dst + e) = *reinterpret_cast<const double2 *>(T + e);
+          } else {
+            for (int64_t e = tid; e < n; e += kDT) dst[e] = T[e];
+          }
+        }
+      }
+    } else if (STORE) {
 #pragma unroll
       for (int v = 0; v < 8; ++v) {
         const int pp = 2 * lane + 64 * (v >> 1) + (v & 1);
