@@ -540,24 +540,355 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dfma_kernel(const Tin *__restrict_
   }
 }
 
+// ------------------------------------------------------ fp64 tensor-core (DMMA) TTM ----
+// Same contraction and tiling contract as ttm_dfma_kernel, on the fp64 tensor cores
+// (mma.sync.m8n8k4.f64: 256 FMA per warp instruction; the measured B200 peak equals DFMA's
+// 37 TF/s, scripts/dbg/dmma_probe.cu, but the 8x lower instruction count leaves issue slots
+// for the operand loads).  CTA tile 64 (j) x 256 (p); warp (wj = w & 1, wp = w >> 1) owns
+// 32 j x 64 p = 4 x 8 MMA tiles (64 fp64 accumulators per thread).  Per chunk of 16 values of
+// i: A staged [i][68] (A_mma[m][k] = A[i0 + k][j0 + m]), X staged [p][20] (B_mma[k][n] =
+// X(i0 + k, p0 + n)); the paddings make both fragment loads bank-conflict-free per half warp.
+// Fragment layouts (PTX m8n8k4 .f64): A row-major, lane -> (m = lane >> 2, k = lane & 3);
+// B col-major, lane -> (k = lane & 3, n = lane >> 2); C lane -> (m = lane >> 2, n = 2 (lane & 3) + {0, 1}).
+constexpr int kMA = 68;  // As row stride (doubles)
+constexpr int kMX = 20;  // Xs row stride (doubles), rows = p
+template <typename Tin, bool STORE, bool GRAM>
+__global__ void __launch_bounds__(kDT, 1) ttm_dmma_kernel(const Tin *__restrict__ X, int64_t L, int64_t I, int64_t R,
+                                                          const double *__restrict__ A, int64_t lda, int J,
+                                                          double *__restrict__ out, double *__restrict__ gram_partial) {
+  extern __shared__ __align__(16) double dsm[];
+  double *Xs = dsm;                        // [kDP][kMX]
+  double *As = Xs + kDP * kMX;             // [kDK][kMA]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wj = warp & 1, wp = warp >> 1;
+  const int fr = lane >> 2, fc = lane & 3;  // fragment row / column
+  const int64_t P = L * R;
+  const int64_t ntiles = (P + kDP - 1) / kDP;
+  const int nchunk = (int)((I + kDK - 1) / kDK);
+  double g[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) g[e] = 0.0;
+  const int gj1 = (tid >> 4) * 4, gj2 = (tid & 15) * 4;
+  Tin pre[16];
+  double apre[4];
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t p0 = tile * kDP;
+    const int64_t pl0 = p0 % L, pr0 = p0 / L;
+    int64_t mycol = -1;
+    if (L > 1) {
+      const int64_t p = p0 + tid;
+      if (p < P) {
+        int64_t l = pl0 + tid, r = pr0;
+        while (l >= L) { l -= L; ++r; }
+        mycol = l + L * I * r;
+      }
+    }
+    auto load_chunk = [&](int ch) {
+      const int64_t i0 = (int64_t)ch * kDK;
+      if (L == 1) {  // unit k = tid + 256 q: column pp = k / 4, rows 4 (k % 4) .. +3
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int k = tid + kDT * q, pp = k >> 2, iq = k & 3;
+          const int64_t p = p0 + pp, i = i0 + 4 * iq;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) pre[4 * q + u] = (p < P && i + u < I) ? X[(i + u) + I * p] : Tin(0);
+        }
+      } else {  // column pp = tid, rows q
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+          const int64_t i = i0 + q;
+          pre[q] = (mycol >= 0 && i < I) ? X[mycol + L * i] : Tin(0);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = tid + kDT * q, ii = e >> 6, j = e & 63;
+        const int64_t i = i0 + ii;
+        apre[q] = (i < I && j < J) ? A[i + lda * j] : 0.0;
+      }
+    };
+    auto store_chunk = [&]() {
+      if (L == 1) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int k = tid + kDT * q, pp = k >> 2, iq = k & 3;
+          double2 *d = reinterpret_cast<double2 *>(Xs + pp * kMX + 4 * iq);
+          d[0] = make_double2((double)pre[4 * q], (double)pre[4 * q + 1]);
+          d[1] = make_double2((double)pre[4 * q + 2], (double)pre[4 * q + 3]);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) Xs[tid * kMX + q] = (double)pre[q];
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = tid + kDT * q, ii = e >> 6, j = e & 63;
+        As[ii * kMA + j] = apre[q];
+      }
+    };
+    double acc[4][8][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
+    load_chunk(0);
+    for (int ch = 0; ch < nchunk; ++ch) {
+      __syncthreads();
+      store_chunk();
+      __syncthreads();
+      if (ch + 1 < nchunk) load_chunk(ch + 1);
+#pragma unroll
+      for (int ks = 0; ks < kDK / 4; ++ks) {
+        double af[4], bf[8];
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt) af[jt] = As[(4 * ks + fc) * kMA + 32 * wj + 8 * jt + fr];
+#pragma unroll
+        for (int pt = 0; pt < 8; ++pt) bf[pt] = Xs[(64 * wp + 8 * pt + fr) * kMX + 4 * ks + fc];
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+          for (int pt = 0; pt < 8; ++pt)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(acc[jt][pt][0]), "+d"(acc[jt][pt][1])
+                         : "d"(af[jt]), "d"(bf[pt]));
+      }
+    }
+    // ---- epilogue: acc[jt][pt][h] = out(j = 32 wj + 8 jt + fr, p = 64 wp + 8 pt + 2 fc + h)
+    if (STORE || GRAM) {
+      for (int half = 0; half < 2; ++half) {  // stage 128 columns at a time: T[p][65]
+        __syncthreads();
+        double *T = dsm;
+        if ((wp >> 1) == half) {
+#pragma unroll
+          for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+            for (int pt = 0; pt < 8; ++pt)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int pp = 64 * (wp & 1) + 8 * pt + 2 * fc + h;
+                T[pp * 65 + 32 * wj + 8 * jt + fr] = acc[jt][pt][h];
+              }
+        }
+        __syncthreads();
+        const int64_t pb = p0 + 128 * half;
+        const int64_t ncol = P - pb < 128 ? (P - pb) : 128;
+        if (STORE && ncol > 0) {
+          if (L == 1) {  // contiguous J x ncol range out[pb J ..]
+            double *dst = out + pb * J;
+            for (int64_t e = tid; e < ncol * J; e += kDT) {
+              const int pp = (int)(e / J), j = (int)(e - (int64_t)pp * J);
+              dst[e] = T[pp * 65 + j];
+            }
+          } else {
+            for (int e = tid; e < 128 * 64; e += kDT) {
+              const int pp = e & 127, j = e >> 7;
+              if (pp < ncol && j < J) {
+                int64_t l = pl0 + 128 * half + pp, r = pr0;
+                while (l >= L) { l -= L; ++r; }
+                out[l + L * (j + (int64_t)J * r)] = T[pp * 65 + j];
+              }
+            }
+          }
+        }
+        if (GRAM) {
+          for (int pp = 0; pp < (int)(ncol > 0 ? ncol : 0); ++pp) {
+            double a4[4], b4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) { a4[q] = T[pp * 65 + gj1 + q]; b4[q] = T[pp * 65 + gj2 + q]; }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+              for (int s = 0; s < 4; ++s) g[q * 4 + s] = fma(a4[q], b4[s], g[q * 4 + s]);
+          }
+        }
+      }
+    }
+  }
+  if (GRAM) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int s = 0; s < 4; ++s) gram_partial[(int64_t)blockIdx.x * 4096 + (gj1 + q) * 64 + gj2 + s] = g[q * 4 + s];
+  }
+}
+
+// L == 1 variant of ttm_dmma_kernel with a 3-stage cp.async pipeline: X(i, p) = X[i + I p]
+// (i contiguous) and A[i + lda j] are copied raw (16-byte units, zero-filled out of range)
+// into [p][20] / [j][20] stage buffers, so no register staging pass and two chunks in
+// flight while the tensor cores work on the third; X is converted to fp64 at fragment load.
+constexpr int kNST = 3;
+constexpr int kS = 20;  // row stride (elements) of the X and A stage tiles
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <typename Tin, bool STORE, bool GRAM>
+__global__ void __launch_bounds__(kDT, 1) ttm_dmma_l1_kernel(const Tin *__restrict__ X, int64_t I, int64_t P,
+                                                             const double *__restrict__ A, int64_t lda, int J,
+                                                             double *__restrict__ out, double *__restrict__ gram_partial) {
+  extern __shared__ __align__(16) double dsm[];
+  constexpr int kVX = 16 / sizeof(Tin);          // elements of X per 16-byte unit
+  constexpr int kXStage = kDP * kS * (int)sizeof(Tin);  // bytes
+  constexpr int kAStage = 64 * kS * 8;
+  unsigned char *sbase = reinterpret_cast<unsigned char *>(dsm);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int wj = warp & 1, wp = warp >> 1;
+  const int fr = lane >> 2, fc = lane & 3;
+  const int64_t ntiles = (P + kDP - 1) / kDP;
+  const int nchunk = (int)((I + kDK - 1) / kDK);
+  double g[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) g[e] = 0.0;
+  const int gj1 = (tid >> 4) * 4, gj2 = (tid & 15) * 4;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t p0 = tile * kDP;
+    auto issue = [&](int ch) {
+      const int st = ch % kNST;
+      Tin *xs = reinterpret_cast<Tin *>(sbase + st * (kXStage + kAStage));
+      double *as = reinterpret_cast<double *>(sbase + st * (kXStage + kAStage) + kXStage);
+      const int64_t i0 = (int64_t)ch * kDK;
+      constexpr int kUX = kDP * (kDK / kVX);     // X units per chunk
+      for (int u = tid; u < kUX; u += kDT) {
+        const int pp = u / (kDK / kVX), iq = u % (kDK / kVX);
+        const int64_t p = p0 + pp, i = i0 + kVX * iq;
+        const bool ok = p < P && i < I;
+        cp_async16(xs + pp * kS + kVX * iq, ok ? (const void *)(X + i + I * p) : (const void *)X, ok);
+      }
+      for (int u = tid; u < 64 * (kDK / 2); u += kDT) {  // A: 2 doubles per unit
+        const int j = u / (kDK / 2), iq = u % (kDK / 2);
+        const int64_t i = i0 + 2 * iq;
+        const bool ok = j < J && i < I;
+        cp_async16(as + j * kS + 2 * iq, ok ? (const void *)(A + i + lda * j) : (const void *)A, ok);
+      }
+    };
+    double acc[4][8][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
+    __syncthreads();  // previous tile's epilogue is done with the stage buffers
+#pragma unroll
+    for (int s = 0; s < kNST - 1; ++s) {
+      if (s < nchunk) issue(s);
+      cp_async_commit();
+    }
+    for (int ch = 0; ch < nchunk; ++ch) {
+      cp_async_wait<kNST - 2>();
+      __syncthreads();
+      if (ch + kNST - 1 < nchunk) issue(ch + kNST - 1);
+      cp_async_commit();
+      const int st = ch % kNST;
+      const Tin *xs = reinterpret_cast<const Tin *>(sbase + st * (kXStage + kAStage));
+      const double *as = reinterpret_cast<const double *>(sbase + st * (kXStage + kAStage) + kXStage);
+#pragma unroll
+      for (int ks = 0; ks < kDK / 4; ++ks) {
+        double af[4], bf[8];
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt) af[jt] = as[(32 * wj + 8 * jt + fr) * kS + 4 * ks + fc];
+#pragma unroll
+        for (int pt = 0; pt < 8; ++pt) bf[pt] = (double)xs[(64 * wp + 8 * pt + fr) * kS + 4 * ks + fc];
+#pragma unroll
+        for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+          for (int pt = 0; pt < 8; ++pt)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(acc[jt][pt][0]), "+d"(acc[jt][pt][1])
+                         : "d"(af[jt]), "d"(bf[pt]));
+      }
+    }
+    cp_async_wait<0>();
+    // ---- epilogue (as ttm_dmma_kernel, L == 1: the tile is one contiguous range out[p0 J ..])
+    if (STORE || GRAM) {
+      for (int half = 0; half < 2; ++half) {
+        __syncthreads();
+        double *T = dsm;
+        if ((wp >> 1) == half) {
+#pragma unroll
+          for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+            for (int pt = 0; pt < 8; ++pt)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                const int pp = 64 * (wp & 1) + 8 * pt + 2 * fc + h;
+                T[pp * 65 + 32 * wj + 8 * jt + fr] = acc[jt][pt][h];
+              }
+        }
+        __syncthreads();
+        const int64_t pb = p0 + 128 * half;
+        const int64_t ncol = P - pb < 128 ? (P - pb) : 128;
+        if (STORE && ncol > 0) {
+          double *dst = out + pb * J;
+          for (int e = tid; e < (int)ncol * J; e += kDT) {
+            const int pp = e / J, j = e - pp * J;
+            dst[e] = T[pp * 65 + j];
+          }
+        }
+        if (GRAM) {
+          for (int pp = 0; pp < (int)(ncol > 0 ? ncol : 0); ++pp) {
+            double a4[4], b4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) { a4[q] = T[pp * 65 + gj1 + q]; b4[q] = T[pp * 65 + gj2 + q]; }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+              for (int s = 0; s < 4; ++s) g[q * 4 + s] = fma(a4[q], b4[s], g[q * 4 + s]);
+          }
+        }
+      }
+    }
+  }
+  if (GRAM) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int s = 0; s < 4; ++s) gram_partial[(int64_t)blockIdx.x * 4096 + (gj1 + q) * 64 + gj2 + s] = g[q * 4 + s];
+  }
+}
+
 template <typename Tin>
 void launch_ttm_dfma(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t lda, int J, double *out, double *gram) {
   const int64_t P = v.L * v.R;
   const int64_t ntiles = (P + kDP - 1) / kDP;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, c.num_sms));
-  const size_t smem = std::max(sizeof(double) * (kDK * kDS + kDK * 64), sizeof(double) * 128 * 65);
+  static const bool use_dfma = getenv("RTUCKER_NO_DMMA") != nullptr;
   DevBuf<double> part;
   if (gram) part.alloc(c, (size_t)grid * 4096);
+  // cp.async pipeline for L == 1 with 16-byte aligned rows of X and A
+  const bool l1 = !use_dfma && v.L == 1 && (v.I % (16 / sizeof(Tin))) == 0 && (lda % 2) == 0 &&
+                  (((uintptr_t)X) & 15) == 0 && (((uintptr_t)A) & 15) == 0;
+  if (l1) {
+    const size_t stage = (size_t)kDP * kS * sizeof(Tin) + 64 * kS * 8;
+    const size_t smem = std::max(kNST * stage, sizeof(double) * 128 * 65);
+#define RT_DL(ST, GR)                                                                                 \
+  do {                                                                                                \
+    auto k = ttm_dmma_l1_kernel<Tin, ST, GR>;                                                         \
+    RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));         \
+    RT_LAUNCH(c, k, grid, kDT, smem, X, v.I, P, A, lda, J, out, part.p);                              \
+  } while (0)
+    if (out && gram) RT_DL(true, true);
+    else if (out) RT_DL(true, false);
+    else RT_DL(false, true);
+#undef RT_DL
+  } else {
+    const size_t smem = use_dfma ? std::max(sizeof(double) * (kDK * kDS + kDK * 64), sizeof(double) * 128 * 65)
+                                 : std::max(sizeof(double) * (kDP * kMX + kDK * kMA), sizeof(double) * 128 * 65);
 #define RT_DF(ST, GR)                                                                                 \
   do {                                                                                                \
-    auto k = ttm_dfma_kernel<Tin, ST, GR>;                                                            \
+    auto k = use_dfma ? ttm_dfma_kernel<Tin, ST, GR> : ttm_dmma_kernel<Tin, ST, GR>;                  \
     RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));         \
     RT_LAUNCH(c, k, grid, kDT, smem, X, v.L, v.I, v.R, A, lda, J, out, part.p);                       \
   } while (0)
-  if (out && gram) RT_DF(true, true);
-  else if (out) RT_DF(true, false);
-  else RT_DF(false, true);
+    if (out && gram) RT_DF(true, true);
+    else if (out) RT_DF(true, false);
+    else RT_DF(false, true);
 #undef RT_DF
+  }
   if (gram) RT_LAUNCH(c, gram_reduce2_kernel, J * J, 128, 0, part.p, grid, J, gram);
 }
 
