@@ -666,6 +666,173 @@ __global__ void __launch_bounds__(128) trsm_rows_kernel(const double *__restrict
   }
 }
 
+// ------------------------------------------------- cluster CholeskyQR2 (dense) --------
+// Thin QR of a sketch with m <= 8 * 256 rows and n <= 64 columns in ONE cluster kernel.
+// Each CTA keeps its row slab in shared memory (column-major, ld = ldY).  Per pass:
+//  1. partial Gram Y_slab^T Y_slab on the fp64 tensor cores (mma.m8n8k4, upper 8x8 tiles);
+//  2. cluster-wide sum through DSMEM in a fixed CTA order, straight into registers: thread t
+//     owns row i = t / 8 of G and the columns j = t % 8 + 8u, u < 8 (every CTA derives the
+//     bitwise identical Gram);
+//  3. elimination of [G | I] (right-looking Cholesky as Gaussian elimination: step k scales
+//     row k by d_k^{-1/2}, publishes it, every row i > k subtracts G_ik d_k^{-1/2} times it)
+//     -> the published rows are R (upper, G = R^T R) and E = R^{-T}; one barrier per step;
+//  4. slab <- slab R^{-1} = slab E^T on the tensor cores (warp per 8-row block, in place).
+// Two passes (CholeskyQR2).  A pivot d_k <= 1e-13 of its original diagonal (or NaN) marks
+// the sketch as too ill-conditioned: the kernel flags it and Householder recomputes Q.
+constexpr int kCQT = 512;
+constexpr int kCQN = 64;                // max columns
+constexpr size_t kCQSmem = 225 * 1024;  // dynamic shared memory budget of one CTA
+
+__device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kCQT, 1) cholqr2_cluster_kernel(const double *__restrict__ Y, int64_t m, int n,
+                                                                  int rows, int ldY, int ldG, int ldE,
+                                                                  double *__restrict__ Q, int *__restrict__ bad) {
+  extern __shared__ __align__(16) double cq[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int ncta = (int)cl.num_blocks();
+  const int me = (int)cl.block_rank();
+  const int64_t r0 = (int64_t)me * rows;
+  const int64_t left_ = m - r0;
+  const int nloc = left_ <= 0 ? 0 : (left_ < rows ? (int)left_ : rows);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n8 = (n + 7) & ~7, nbk = n8 >> 3;
+  double *Yl = cq;                 // ldY x n8 slab (column-major), zero padded
+  double *Gp = Yl + ldY * n8;      // n8 x ldG partial Gram (row-major)
+  double *E = Gp + n8 * ldG;       // n8 x ldE, row k = row k of R^{-T} (column k of R^{-1})
+  double *pv = E + n8 * ldE;       // [2 buffers][R row | E row][kCQN]
+  double *d0 = pv + 4 * kCQN;      // original diagonal of the pass's Gram
+  __shared__ int sbad;
+  for (int e = tid; e < ldY * n8; e += kCQT) {
+    const int i = e % ldY, c = e / ldY;
+    Yl[e] = (i < nloc && c < n) ? Y[r0 + i + m * c] : 0.0;
+  }
+  if (tid == 0) sbad = 0;
+  const int ri = tid >> 3, g = tid & 7;  // elimination ownership: row ri, columns g + 8u
+  const unsigned gmask = 0xFFu << (8 * (ri & 3));
+  const int kend = (nloc + 3) & ~3;      // slab rows past nloc are zero
+  const int ntiles = nbk * (nbk + 1) / 2;
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) cluster_wait();  // every CTA has read the pass-0 partial Grams
+    // ---- 1. partial Gram, upper tiles (a <= b), mirrored
+    for (int tile = warp; tile < ntiles; tile += kCQT / 32) {
+      int a = 0, rem = tile;
+      while (rem >= nbk - a) { rem -= nbk - a; ++a; }
+      const int b = a + rem;
+      const double *pa = Yl + (size_t)ldY * (8 * a + (lane >> 2)) + (lane & 3);
+      const double *pb = Yl + (size_t)ldY * (8 * b + (lane >> 2)) + (lane & 3);
+      double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+      int k0 = 0;
+      for (; k0 + 8 <= kend; k0 += 8) {  // two independent accumulator chains
+        dmma884(c0, c1, pa[k0], pb[k0]);
+        dmma884(e0, e1, pa[k0 + 4], pb[k0 + 4]);
+      }
+      if (k0 < kend) dmma884(c0, c1, pa[k0], pb[k0]);
+      c0 += e0; c1 += e1;
+      const int gi = 8 * a + (lane >> 2), gj = 8 * b + 2 * (lane & 3);
+      Gp[gi * ldG + gj] = c0; Gp[gi * ldG + gj + 1] = c1;
+      if (a != b) { Gp[gj * ldG + gi] = c0; Gp[(gj + 1) * ldG + gi] = c1; }
+    }
+    cluster_arrive();
+    cluster_wait();
+    // ---- 2. cluster sum into registers (fixed CTA order)
+    double gr[8], er[8], diag = 0.0;  // diag: running G[ri][ri], kept by its owner (g == ri % 8)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = g + 8 * u;
+      double s = 0.0;
+      if (ri < n && j < n)
+        for (int q = 0; q < ncta; ++q) s += cl.map_shared_rank(Gp, q)[ri * ldG + j];
+      gr[u] = s;
+      er[u] = (j == ri) ? 1.0 : 0.0;
+      if (j == ri && ri < n) { d0[ri] = s; diag = s; }
+    }
+    cluster_arrive();  // matched by the wait before the next Gram (or before exit)
+    __syncthreads();
+    // ---- 3. elimination of [G | I]
+    for (int k = 0; k < n; ++k) {
+      double *pR = pv + (k & 1) * 2 * kCQN, *pE = pR + kCQN;
+      if (ri == k) {  // the 8 owners of row k (one lane group of warp k / 4)
+        const double dk = __shfl_sync(gmask, diag, k & 7, 8);
+        if (g == 0 && !(dk > 1e-13 * d0[k])) sbad = 1;
+        const double inv = rsqrt(dk);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int j = g + 8 * u;
+          pR[j] = (j >= k) ? gr[u] * inv : 0.0;
+          const double ev = er[u] * inv;
+          pE[j] = ev;
+          if (j < n8) E[k * ldE + j] = ev;
+        }
+      }
+      __syncthreads();
+      if (ri > k && ri < n) {
+        const double f = pR[ri];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int j = g + 8 * u;
+          gr[u] = fma(-f, pR[j], gr[u]);
+          er[u] = fma(-f, pE[j], er[u]);
+        }
+        diag = fma(-f, f, diag);  // == gr[ri >> 3] in the owner of G[ri][ri] (same operands)
+      }
+    }
+    // rows n..n8-1 of E (padding) stay as written by a previous pass or zero them once
+    for (int e = n * ldE + tid; e < n8 * ldE; e += kCQT) E[e] = 0.0;
+    __syncthreads();
+    // ---- 4. slab <- slab E^T (W = R^{-1} upper: W[t][j] = E[j][t], only t <= j contributes)
+    for (int rb = warp; 8 * rb < nloc; rb += kCQT / 32) {
+      double acc[8][2];
+#pragma unroll
+      for (int cb = 0; cb < 8; ++cb) acc[cb][0] = acc[cb][1] = 0.0;
+      const double *pa = Yl + 8 * rb + (lane >> 2) + (size_t)ldY * (lane & 3);
+#pragma unroll
+      for (int tb = 0; tb < 8; ++tb) {
+        if (tb < nbk) {
+#pragma unroll
+          for (int kh = 0; kh < 2; ++kh) {
+            const int t0 = 8 * tb + 4 * kh;
+            const double av = pa[(size_t)ldY * t0];
+#pragma unroll
+            for (int cb = tb; cb < 8; ++cb)
+              if (cb < nbk) dmma884(acc[cb][0], acc[cb][1], av, E[(8 * cb + (lane >> 2)) * ldE + t0 + (lane & 3)]);
+          }
+        }
+      }
+      __syncwarp();
+      const int row = 8 * rb + (lane >> 2);
+#pragma unroll
+      for (int cb = 0; cb < 8; ++cb)
+        if (cb < nbk) {
+          const int col = 8 * cb + 2 * (lane & 3);
+          Yl[row + (size_t)ldY * col] = acc[cb][0];
+          Yl[row + (size_t)ldY * (col + 1)] = acc[cb][1];
+        }
+    }
+    __syncthreads();
+  }
+  cluster_wait();  // no CTA leaves while others may still read its partial Gram
+  if (sbad) {
+    if (me == 0 && tid == 0) *bad = 1;
+    return;
+  }
+  for (int e = tid; e < nloc * n; e += kCQT) {
+    const int i = e % nloc, c = e / nloc;
+    Q[r0 + i + m * c] = Yl[i + (size_t)ldY * c];
+  }
+}
+
 // One CTA per column k: argmax |A[:, k]| (first index on ties); flip A[:, k] and U[:, k]
 // when that entry is negative (DESIGN reading R4b).
 __global__ void canonical_signs_kernel(double *__restrict__ A, int64_t m, double *__restrict__ U, int64_t ldu,
@@ -765,22 +932,50 @@ void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps,
 
 void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
   RT_REQUIRE(m >= n && n >= 1, "qr: need m >= n >= 1");
-  // sketches whose rows fit a 16-CTA cluster: Householder directly (latency-bound either way);
-  // tall sketches (sparse modes, I_n ~ 1e5): CholeskyQR2 with the Householder fallback
-  if (n > 64 || m <= 16 * 256) return householder_qr(c, Y, m, n, Q, nullptr);
-  DevBuf<double> G(c, (size_t)n * n), Ri(c, (size_t)n * n), Q1(c, (size_t)m * n);
+  if (n > 64) return householder_qr(c, Y, m, n, Q, nullptr);
+  static const bool no_chol = getenv("RTUCKER_QR_HOUSEHOLDER") != nullptr;
+  if (no_chol) return householder_qr(c, Y, m, n, Q, nullptr);
   DevBuf<int> bad(c, 1);
   bad.zero();
-  const size_t csm = sizeof(double) * ((size_t)n * n + n);
-  RT_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
-  const double *src = Y;
-  for (int pass = 0; pass < 2; ++pass) {
-    double *dst = pass == 0 ? Q1.p : Q;
-    mode_gram(c, src, DT::F64, ModeView{m, n, 1}, G.p);
-    RT_LAUNCH(c, chol_inv_kernel, 1, 256, csm, G.p, n, Ri.p, bad.p);
-    RT_LAUNCH(c, trsm_rows_kernel, std::max(1, std::min(c.num_sms * 8, ceil_div(m, 128))), 128,
-              sizeof(double) * n * n, src, m, n, Ri.p, dst, bad.p);
-    src = dst;
+  if (m <= 8 * 256) {
+    // one portable cluster: CholeskyQR2 in shared memory (row slabs of <= 256 rows per CTA)
+    int ncta = 1;
+    while (ncta < 8 && (m + ncta - 1) / ncta > 256) ncta *= 2;
+    const int rows = (int)((m + ncta - 1) / ncta);
+    const int n8 = (n + 7) & ~7;
+    const int ldY = ((rows + 7) / 8 * 8 + 11) / 16 * 16 + 4;  // >= rows rounded to 8, = 4 mod 16
+    const int ldG = (n8 + 15) / 16 * 16 + 8, ldE = (n8 + 15) / 16 * 16 + 4;
+    const size_t smem = sizeof(double) * ((size_t)ldY * n8 + (size_t)n8 * ldG + (size_t)n8 * ldE + 4 * kCQN + kCQN);
+    RT_REQUIRE(smem <= kCQSmem, "qr: CholeskyQR2 slab does not fit shared memory");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ncta);
+    cfg.blockDim = dim3(kCQT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = ncta;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    RT_CUDA(cudaFuncSetAttribute(cholqr2_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    RT_CUDA(cudaLaunchKernelEx(&cfg, cholqr2_cluster_kernel, Y, m, n, rows, ldY, ldG, ldE, Q, bad.p));
+    c.launches++;
+  } else {
+    // tall sketches (sparse modes, I_n ~ 1e5): CholeskyQR2 over the whole grid
+    DevBuf<double> G(c, (size_t)n * n), Ri(c, (size_t)n * n), Q1(c, (size_t)m * n);
+    const size_t csm = sizeof(double) * ((size_t)n * n + n);
+    RT_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+    const double *src = Y;
+    for (int pass = 0; pass < 2; ++pass) {
+      double *dst = pass == 0 ? Q1.p : Q;
+      mode_gram(c, src, DT::F64, ModeView{m, n, 1}, G.p);
+      RT_LAUNCH(c, chol_inv_kernel, 1, 256, csm, G.p, n, Ri.p, bad.p);
+      RT_LAUNCH(c, trsm_rows_kernel, std::max(1, std::min(c.num_sms * 8, ceil_div(m, 128))), 128,
+                sizeof(double) * n * n, src, m, n, Ri.p, dst, bad.p);
+      src = dst;
+    }
   }
   householder_qr(c, Y, m, n, Q, bad.p);  // runs only when a Cholesky pass flagged
 }
