@@ -727,44 +727,67 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Epilogue tile T[p][kTS] (kTS = 4 mod 16 doubles): conflict-free for the accumulator stores
+// and for the Gram's DMMA fragment loads.  The Gram partial G += T^T T runs on the fp64 tensor
+// cores too: the 36 upper 8x8 tiles of the 64 x 64 Gram are spread over the 8 warps.
+constexpr int kTS = 68;
+__device__ __forceinline__ void gram_tile_ab(int t, int &a, int &b) {
+  a = 0;
+  while (t >= 8 - a) { t -= 8 - a; ++a; }
+  b = a + t;
+}
+
 template <typename Tin, bool STORE, bool GRAM>
 __global__ void __launch_bounds__(kDT, 1) ttm_dmma_l1_kernel(const Tin *__restrict__ X, int64_t I, int64_t P,
                                                              const double *__restrict__ A, int64_t lda, int J,
                                                              double *__restrict__ out, double *__restrict__ gram_partial) {
   extern __shared__ __align__(16) double dsm[];
-  constexpr int kVX = 16 / sizeof(Tin);          // elements of X per 16-byte unit
+  constexpr int kVX = 16 / sizeof(Tin);                 // elements of X per 16-byte unit
   constexpr int kXStage = kDP * kS * (int)sizeof(Tin);  // bytes
   constexpr int kAStage = 64 * kS * 8;
+  constexpr int kQX = kDK / kVX;                        // 16-byte units per X row of a chunk
+  constexpr int kUXT = kDP * kQX / kDT;                 // X units per thread per chunk
+  constexpr int kUAT = 64 * (kDK / 2) / kDT;            // A units per thread per chunk
+  static_assert(kDP * kQX % kDT == 0 && 64 * (kDK / 2) % kDT == 0, "unit split");
   unsigned char *sbase = reinterpret_cast<unsigned char *>(dsm);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wj = warp & 1, wp = warp >> 1;
   const int fr = lane >> 2, fc = lane & 3;
   const int64_t ntiles = (P + kDP - 1) / kDP;
   const int nchunk = (int)((I + kDK - 1) / kDK);
-  double g[16];
+  // Gram tiles of this warp: t = warp + 8 s (s < 5, t < 36)
+  double gacc[5][2];
 #pragma unroll
-  for (int e = 0; e < 16; ++e) g[e] = 0.0;
-  const int gj1 = (tid >> 4) * 4, gj2 = (tid & 15) * 4;
+  for (int s5 = 0; s5 < 5; ++s5) gacc[s5][0] = gacc[s5][1] = 0.0;
+  // per-thread copy assignment (fixed for every chunk): X unit k -> row pp = xr + (kDT / kQX) k,
+  // column iq = xq; A unit k -> row j = ar + (kDT / (kDK / 2)) k, column aq
+  const int xr = tid / kQX, xq = tid % kQX;
+  const int ar = tid / (kDK / 2), aq = tid % (kDK / 2);
+  const double *abase = A + 2 * aq + lda * ar;
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t p0 = tile * kDP;
+    const Tin *xbase = X + kVX * xq + I * (p0 + xr);
     auto issue = [&](int ch) {
       const int st = ch % kNST;
       Tin *xs = reinterpret_cast<Tin *>(sbase + st * (kXStage + kAStage));
       double *as = reinterpret_cast<double *>(sbase + st * (kXStage + kAStage) + kXStage);
       const int64_t i0 = (int64_t)ch * kDK;
-      constexpr int kUX = kDP * (kDK / kVX);     // X units per chunk
-      for (int u = tid; u < kUX; u += kDT) {
-        const int pp = u / (kDK / kVX), iq = u % (kDK / kVX);
-        const int64_t p = p0 + pp, i = i0 + kVX * iq;
-        const bool ok = p < P && i < I;
-        cp_async16(xs + pp * kS + kVX * iq, ok ? (const void *)(X + i + I * p) : (const void *)X, ok);
+      const bool iok = i0 + kVX * xq < I;
+#pragma unroll
+      for (int k = 0; k < kUXT; ++k) {
+        const int pp = xr + (kDT / kQX) * k;
+        const bool ok = iok && p0 + pp < P;
+        cp_async16(xs + pp * kS + kVX * xq, ok ? (const void *)(xbase + i0 + I * (int64_t)((kDT / kQX) * k)) : (const void *)X,
+                   ok);
       }
-      for (int u = tid; u < 64 * (kDK / 2); u += kDT) {  // A: 2 doubles per unit
-        const int j = u / (kDK / 2), iq = u % (kDK / 2);
-        const int64_t i = i0 + 2 * iq;
-        const bool ok = j < J && i < I;
-        cp_async16(as + j * kS + 2 * iq, ok ? (const void *)(A + i + lda * j) : (const void *)A, ok);
+      const bool aiok = i0 + 2 * aq < I;
+#pragma unroll
+      for (int k = 0; k < kUAT; ++k) {
+        const int j = ar + (kDT / (kDK / 2)) * k;
+        const bool ok = aiok && j < J;
+        cp_async16(as + j * kS + 2 * aq, ok ? (const void *)(abase + i0 + lda * (int64_t)((kDT / (kDK / 2)) * k)) : (const void *)A,
+                   ok);
       }
     };
     double acc[4][8][2];
@@ -803,7 +826,8 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_l1_kernel(const Tin *__restri
       }
     }
     cp_async_wait<0>();
-    // ---- epilogue (as ttm_dmma_kernel, L == 1: the tile is one contiguous range out[p0 J ..])
+    // ---- epilogue (L == 1: the tile is one contiguous range out[p0 J ..]); columns p >= P
+    // and rows j >= J of the tile are exact zeros (zero-filled copies)
     if (STORE || GRAM) {
       for (int half = 0; half < 2; ++half) {
         __syncthreads();
@@ -816,7 +840,7 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_l1_kernel(const Tin *__restri
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int pp = 64 * (wp & 1) + 8 * pt + 2 * fc + h;
-                T[pp * 65 + 32 * wj + 8 * jt + fr] = acc[jt][pt][h];
+                T[pp * kTS + 32 * wj + 8 * jt + fr] = acc[jt][pt][h];
               }
         }
         __syncthreads();
@@ -826,28 +850,46 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_l1_kernel(const Tin *__restri
           double *dst = out + pb * J;
           for (int e = tid; e < (int)ncol * J; e += kDT) {
             const int pp = e / J, j = e - pp * J;
-            dst[e] = T[pp * 65 + j];
+            dst[e] = T[pp * kTS + j];
           }
         }
         if (GRAM) {
-          for (int pp = 0; pp < (int)(ncol > 0 ? ncol : 0); ++pp) {
-            double a4[4], b4[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) { a4[q] = T[pp * 65 + gj1 + q]; b4[q] = T[pp * 65 + gj2 + q]; }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-              for (int s = 0; s < 4; ++s) g[q * 4 + s] = fma(a4[q], b4[s], g[q * 4 + s]);
+          for (int s5 = 0; s5 < 5; ++s5) {
+            const int t = warp + 8 * s5;
+            if (t < 36) {
+              int a, b;
+              gram_tile_ab(t, a, b);
+              const double *ta = T + fc * kTS + 8 * a + fr;
+              const double *tb = T + fc * kTS + 8 * b + fr;
+#pragma unroll 8
+              for (int k0 = 0; k0 < 128; k0 += 4)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                             : "+d"(gacc[s5][0]), "+d"(gacc[s5][1])
+                             : "d"(ta[k0 * kTS]), "d"(tb[k0 * kTS]));
+            }
           }
         }
       }
     }
   }
   if (GRAM) {
+    double *gp = gram_partial + (int64_t)blockIdx.x * 4096;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int s = 0; s < 4; ++s) gram_partial[(int64_t)blockIdx.x * 4096 + (gj1 + q) * 64 + gj2 + s] = g[q * 4 + s];
+    for (int s5 = 0; s5 < 5; ++s5) {
+      const int t = warp + 8 * s5;
+      if (t < 36) {
+        int a, b;
+        gram_tile_ab(t, a, b);
+        const int gi = 8 * a + fr, gj = 8 * b + 2 * fc;
+        gp[gi * 64 + gj] = gacc[s5][0];
+        gp[gi * 64 + gj + 1] = gacc[s5][1];
+        if (a != b) {
+          gp[gj * 64 + gi] = gacc[s5][0];
+          gp[(gj + 1) * 64 + gi] = gacc[s5][1];
+        }
+      }
+    }
   }
 }
 
@@ -864,7 +906,7 @@ void launch_ttm_dfma(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t 
                   (((uintptr_t)X) & 15) == 0 && (((uintptr_t)A) & 15) == 0;
   if (l1) {
     const size_t stage = (size_t)kDP * kS * sizeof(Tin) + 64 * kS * 8;
-    const size_t smem = std::max(kNST * stage, sizeof(double) * 128 * 65);
+    const size_t smem = std::max(kNST * stage, sizeof(double) * 128 * kTS);
 #define RT_DL(ST, GR)                                                                                 \
   do {                                                                                                \
     auto k = ttm_dmma_l1_kernel<Tin, ST, GR>;                                                         \

@@ -15,7 +15,11 @@ for r in data:
     if len(r) < len(h) or not r[0].isdigit():
         continue  # SASS rows; line rows carry the per-line aggregates
     key = (int(r[0]), r[1].strip()[:70])
-    num = lambda x: int(x) if x not in ("", "-") else 0
+    def num(x):
+        try:
+            return int(x)
+        except ValueError:
+            return 0
     e = per.setdefault(key, [0, 0, {}])
     e[0] += num(r[iS]); e[1] += num(r[iI])
     for i, k in stalls:
