@@ -718,7 +718,8 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_kernel(const Tin *__restrict_
 // into [p][20] / [j][20] stage buffers, so no register staging pass and two chunks in
 // flight while the tensor cores work on the third; X is converted to fp64 at fragment load.
 constexpr int kNST = 3;
-constexpr int kS = 20;  // row stride (elements) of the X and A stage tiles
+template <typename Tin>
+__host__ __device__ constexpr int l1_chunk() { return sizeof(Tin) == 4 ? 32 : 16; }
 __device__ __forceinline__ void cp_async16(void *dst, const void *src, bool valid) {
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
@@ -742,27 +743,28 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_l1_kernel(const Tin *__restri
                                                              const double *__restrict__ A, int64_t lda, int J,
                                                              double *__restrict__ out, double *__restrict__ gram_partial) {
   extern __shared__ __align__(16) double dsm[];
+  constexpr int kDKt = l1_chunk<Tin>(), kSt = kDKt + 4;  // i per chunk; stage row stride (= 4 mod 16)
   constexpr int kVX = 16 / sizeof(Tin);                 // elements of X per 16-byte unit
-  constexpr int kXStage = kDP * kS * (int)sizeof(Tin);  // bytes
-  constexpr int kAStage = 64 * kS * 8;
-  constexpr int kQX = kDK / kVX;                        // 16-byte units per X row of a chunk
+  constexpr int kXStage = kDP * kSt * (int)sizeof(Tin);  // bytes
+  constexpr int kAStage = 64 * kSt * 8;
+  constexpr int kQX = kDKt / kVX;                        // 16-byte units per X row of a chunk
   constexpr int kUXT = kDP * kQX / kDT;                 // X units per thread per chunk
-  constexpr int kUAT = 64 * (kDK / 2) / kDT;            // A units per thread per chunk
-  static_assert(kDP * kQX % kDT == 0 && 64 * (kDK / 2) % kDT == 0, "unit split");
+  constexpr int kUAT = 64 * (kDKt / 2) / kDT;            // A units per thread per chunk
+  static_assert(kDP * kQX % kDT == 0 && 64 * (kDKt / 2) % kDT == 0, "unit split");
   unsigned char *sbase = reinterpret_cast<unsigned char *>(dsm);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wj = warp & 1, wp = warp >> 1;
   const int fr = lane >> 2, fc = lane & 3;
   const int64_t ntiles = (P + kDP - 1) / kDP;
-  const int nchunk = (int)((I + kDK - 1) / kDK);
+  const int nchunk = (int)((I + kDKt - 1) / kDKt);
   // Gram tiles of this warp: t = warp + 8 s (s < 5, t < 36)
   double gacc[5][2];
 #pragma unroll
   for (int s5 = 0; s5 < 5; ++s5) gacc[s5][0] = gacc[s5][1] = 0.0;
   // per-thread copy assignment (fixed for every chunk): X unit k -> row pp = xr + (kDT / kQX) k,
-  // column iq = xq; A unit k -> row j = ar + (kDT / (kDK / 2)) k, column aq
+  // column iq = xq; A unit k -> row j = ar + (kDT / (kDKt / 2)) k, column aq
   const int xr = tid / kQX, xq = tid % kQX;
-  const int ar = tid / (kDK / 2), aq = tid % (kDK / 2);
+  const int ar = tid / (kDKt / 2), aq = tid % (kDKt / 2);
   const double *abase = A + 2 * aq + lda * ar;
 
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -772,21 +774,21 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_l1_kernel(const Tin *__restri
       const int st = ch % kNST;
       Tin *xs = reinterpret_cast<Tin *>(sbase + st * (kXStage + kAStage));
       double *as = reinterpret_cast<double *>(sbase + st * (kXStage + kAStage) + kXStage);
-      const int64_t i0 = (int64_t)ch * kDK;
+      const int64_t i0 = (int64_t)ch * kDKt;
       const bool iok = i0 + kVX * xq < I;
 #pragma unroll
       for (int k = 0; k < kUXT; ++k) {
         const int pp = xr + (kDT / kQX) * k;
         const bool ok = iok && p0 + pp < P;
-        cp_async16(xs + pp * kS + kVX * xq, ok ? (const void *)(xbase + i0 + I * (int64_t)((kDT / kQX) * k)) : (const void *)X,
+        cp_async16(xs + pp * kSt + kVX * xq, ok ? (const void *)(xbase + i0 + I * (int64_t)((kDT / kQX) * k)) : (const void *)X,
                    ok);
       }
       const bool aiok = i0 + 2 * aq < I;
 #pragma unroll
       for (int k = 0; k < kUAT; ++k) {
-        const int j = ar + (kDT / (kDK / 2)) * k;
+        const int j = ar + (kDT / (kDKt / 2)) * k;
         const bool ok = aiok && j < J;
-        cp_async16(as + j * kS + 2 * aq, ok ? (const void *)(abase + i0 + lda * (int64_t)((kDT / (kDK / 2)) * k)) : (const void *)A,
+        cp_async16(as + j * kSt + 2 * aq, ok ? (const void *)(abase + i0 + lda * (int64_t)((kDT / (kDKt / 2)) * k)) : (const void *)A,
                    ok);
       }
     };
@@ -810,12 +812,12 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_l1_kernel(const Tin *__restri
       const Tin *xs = reinterpret_cast<const Tin *>(sbase + st * (kXStage + kAStage));
       const double *as = reinterpret_cast<const double *>(sbase + st * (kXStage + kAStage) + kXStage);
 #pragma unroll
-      for (int ks = 0; ks < kDK / 4; ++ks) {
+      for (int ks = 0; ks < kDKt / 4; ++ks) {
         double af[4], bf[8];
 #pragma unroll
-        for (int jt = 0; jt < 4; ++jt) af[jt] = as[(32 * wj + 8 * jt + fr) * kS + 4 * ks + fc];
+        for (int jt = 0; jt < 4; ++jt) af[jt] = as[(32 * wj + 8 * jt + fr) * kSt + 4 * ks + fc];
 #pragma unroll
-        for (int pt = 0; pt < 8; ++pt) bf[pt] = (double)xs[(64 * wp + 8 * pt + fr) * kS + 4 * ks + fc];
+        for (int pt = 0; pt < 8; ++pt) bf[pt] = (double)xs[(64 * wp + 8 * pt + fr) * kSt + 4 * ks + fc];
 #pragma unroll
         for (int jt = 0; jt < 4; ++jt)
 #pragma unroll
@@ -905,7 +907,8 @@ void launch_ttm_dfma(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t 
   const bool l1 = !use_dfma && v.L == 1 && (v.I % (16 / sizeof(Tin))) == 0 && (lda % 2) == 0 &&
                   (((uintptr_t)X) & 15) == 0 && (((uintptr_t)A) & 15) == 0;
   if (l1) {
-    const size_t stage = (size_t)kDP * kS * sizeof(Tin) + 64 * kS * 8;
+    constexpr int kSt = l1_chunk<Tin>() + 4;
+    const size_t stage = (size_t)kDP * kSt * sizeof(Tin) + 64 * kSt * 8;
     const size_t smem = std::max(kNST * stage, sizeof(double) * 128 * kTS);
 #define RT_DL(ST, GR)                                                                                 \
   do {                                                                                                \
