@@ -419,163 +419,261 @@ __global__ void __launch_bounds__(kL == 8 ? 256 : (kL == 16 ? 512 : kEigT)) jaco
 }
 
 // Eigenpairs of a PSD Gram G (n <= 64), preconditioned one-sided Jacobi (Drmac-Veselic
-// style): pivoted Cholesky P^T G P = L L^T (diagonal pivoting, ties to the smallest index,
-// stops at rank when the largest remaining diagonal is <= n eps max diag(G)), then one-sided
-// Jacobi orthogonalises the columns of M = L (M J = U Sigma), so P^T G P = U Sigma^2 U^T:
-// lambda_k = |m_k|^2 and v_k = P m_k / |m_k|.  The pivoted factor is already close to
-// column-orthogonal, so the Jacobi needs a handful of sweeps instead of the 13-25 sweeps of
-// Jacobi on G itself; no rotation matrix is accumulated.  Eigenvectors are accurate to
-// ~eps sigma_1 / sigma_k, i.e. for the leading part of the spectrum that the truncation keeps.
+// style): pivoted Cholesky G = M M^T with M = P L (diagonal pivoting, ties to the smallest
+// index, stops at rank when the largest remaining diagonal is <= n eps max diag(G); rows are
+// not exchanged, so M keeps G's index order), then one-sided Jacobi orthogonalises the
+// columns of M (M J = U Sigma), so G = U Sigma^2 U^T: lambda_k = |m_k|^2, v_k = m_k / |m_k|.
+// The pivoted factor is already close to column-orthogonal, so the Jacobi needs a handful of
+// sweeps instead of the 13-25 sweeps of Jacobi on G itself; no rotation matrix is
+// accumulated.  Eigenvectors are accurate to ~eps sigma_1 / sigma_k, i.e. for the leading part
+// of the spectrum that the truncation keeps.
+//
+// Jacobi schedule (register resident, block ordered): the columns of M form nb (even) blocks
+// of 8.  A sweep visits every column pair once: first the pairs inside each block (warp w
+// holds blocks 2w, 2w+1, one column of each per 4-lane slot; round m = 1..7 pairs slot k with
+// slot k ^ m, both slots evaluate the pair on shuffled copies and each updates its own column),
+// then the pairs between blocks (nb - 1 outer rounds; in round t warp w takes the block pair
+// rr(w, t) and its 64 column pairs in 8 rounds, the B columns shifting one slot per round).
+// Lane (slot k = lane / 4, quarter q = lane % 4) keeps rows q + 4v of its columns in
+// registers; g = m_p^T m_q and the two squared norms are reduced over the slot's 4 lanes
+// (exact every round, nothing carried); one CTA barrier per outer round.
 constexpr int kGramT = 256;
+
+__device__ __forceinline__ double rcp_approx_f64(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return r;
+}
+
+// Rotation (c, s) annihilating g for squared norms a (column p), b (column q).  t is evaluated
+// with fp32 approximations (a rotation that leaves ~1e-7 g behind still converges
+// quadratically); c = (1 + t^2)^{-1/2} to working precision, so the rotation is orthogonal.
+__device__ __forceinline__ void jac_angle(double a, double b, double g, double &c, double &s) {
+  const double zeta = (b - a) * rcp_approx_f64(2.0 * g);
+  double t;
+  if (fabs(zeta) > 1e7) {
+    t = 0.5 * rcp_approx_f64(zeta);
+  } else {  // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), fp32 approximations
+    const float zf = (float)zeta;
+    const float s1 = fmaf(zf, zf, 1.0f);
+    float r1, r2;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r1) : "f"(s1));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r2) : "f"(fabsf(zf) + s1 * r1));
+    t = (double)copysignf(r2, zf);
+  }
+  // c = (1 + t^2)^{-1/2} to working precision: approximate rsqrt + two Newton steps
+  const double u = fma(t, t, 1.0), hu = 0.5 * u;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(c) : "d"(u));
+  c = c * fma(-hu * c, c, 1.5);
+  c = c * fma(-hu * c, c, 1.5);
+  s = t * c;
+}
+
+template <int kV>
+__device__ __forceinline__ void jac_pair(double (&x)[kV], double (&y)[kV], double tol2, int &rot) {
+  double g0 = 0.0, g1 = 0.0, a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll
+  for (int v = 0; v < kV; v += 2) {  // six independent chains
+    g0 = fma(x[v], y[v], g0);
+    g1 = fma(x[v + 1], y[v + 1], g1);
+    a0 = fma(x[v], x[v], a0);
+    a1 = fma(x[v + 1], x[v + 1], a1);
+    b0 = fma(y[v], y[v], b0);
+    b1 = fma(y[v + 1], y[v + 1], b1);
+  }
+  double g = g0 + g1, a = a0 + a1, b = b0 + b1;
+#pragma unroll
+  for (int o = 1; o <= 2; o <<= 1) {  // the slot's 4 lanes; identical sums in all of them
+    g += __shfl_xor_sync(0xffffffffu, g, o);
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if (g != 0.0 && g * g > tol2 * a * b) {
+    rot = 1;
+    double c, s;
+    jac_angle(a, b, g, c, s);
+#pragma unroll
+    for (int v = 0; v < kV; ++v) {
+      const double xv = x[v], yv = y[v];
+      x[v] = fma(c, xv, -s * yv);
+      y[v] = fma(s, xv, c * yv);
+    }
+  }
+}
+
+// Pair (p, q) evaluated on BOTH slots that hold copies of the two columns (XOR schedule): the
+// slot owning column p passes (own = m_p, oth = m_q, own_is_p = true), the slot owning q the
+// mirror; the sums are formed in the same order on both (x*y == y*x exactly), so both take
+// the identical rotation and each updates its own column only.
+template <int kV>
+__device__ __forceinline__ void jac_half(double (&own)[kV], const double (&oth)[kV], bool own_is_p, double tol2,
+                                         int &rot) {
+  double g0 = 0.0, g1 = 0.0, o0 = 0.0, o1 = 0.0, t0 = 0.0, t1 = 0.0;
+#pragma unroll
+  for (int v = 0; v < kV; v += 2) {
+    g0 = fma(own[v], oth[v], g0);
+    g1 = fma(own[v + 1], oth[v + 1], g1);
+    o0 = fma(own[v], own[v], o0);
+    o1 = fma(own[v + 1], own[v + 1], o1);
+    t0 = fma(oth[v], oth[v], t0);
+    t1 = fma(oth[v + 1], oth[v + 1], t1);
+  }
+  double g = g0 + g1, so = o0 + o1, st = t0 + t1;
+#pragma unroll
+  for (int o = 1; o <= 2; o <<= 1) {
+    g += __shfl_xor_sync(0xffffffffu, g, o);
+    so += __shfl_xor_sync(0xffffffffu, so, o);
+    st += __shfl_xor_sync(0xffffffffu, st, o);
+  }
+  const double a = own_is_p ? so : st, b = own_is_p ? st : so;
+  if (g != 0.0 && g * g > tol2 * a * b) {
+    rot = 1;
+    double c, s;
+    jac_angle(a, b, g, c, s);
+    if (own_is_p) {
+#pragma unroll
+      for (int v = 0; v < kV; ++v) own[v] = fma(c, own[v], -s * oth[v]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < kV; ++v) own[v] = fma(s, oth[v], c * own[v]);
+    }
+  }
+}
+
+template <int kV>
 __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restrict__ Ain, int n, double *__restrict__ w,
                                                           double *__restrict__ Vout, double tol, int max_sweeps,
                                                           int *__restrict__ info, int r_need, int *__restrict__ refine) {
   extern __shared__ double gsm2[];
   const int np = n + (n & 1);
-  double *G = gsm2;                     // np x np working copy (column-major)
-  double *M = G + np * np;              // L, then M J
-  double *lam = M + np * np;            // np
-  int *perm = reinterpret_cast<int *>(lam + np);
-  short2 *ptab = reinterpret_cast<short2 *>(perm + np + (np & 1));
-  __shared__ int sconv, spiv, srank;
+  const int nb = ((n + 15) / 16) * 2;  // column blocks of 8 (even count)
+  const int ncol = 8 * nb;
+  constexpr int ldm = 4 * kV + 4;      // = 4 mod 16 (kV in {4, 8, 16}): conflict-free slot loads
+  double *G = gsm2;                    // np x np working copy (column-major)
+  double *M = G + np * np;             // ldm x ncol: P L, then M J
+  double *lam = M + ldm * ncol;        // ncol
+  double *lc = lam + ncol;             // np: current column of L
+  int *dn = reinterpret_cast<int *>(lc + np);  // np: row already pivoted
+  __shared__ int spiv, sflag;
   __shared__ double sdmax;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  constexpr int nw = kGramT / 32;
-  constexpr int kL = 8, kGroups = 4, kR = 8;
-  const int sub = lane / kL, gl = lane % kL;
-  const unsigned gmask = 0xFFu << (sub * kL);
-  const int npairs = np / 2;
   for (int e = tid; e < np * np; e += kGramT) {
     const int i = e % np, j = e / np;
     G[e] = (i < n && j < n) ? 0.5 * (Ain[i + (size_t)n * j] + Ain[j + (size_t)n * i]) : 0.0;
-    M[e] = 0.0;
   }
-  for (int i = tid; i < np; i += kGramT) perm[i] = i;
-  for (int e = tid; e < (np - 1) * npairs; e += kGramT) {
-    int p, q;
-    rr_pair(e % npairs, e / npairs, np, p, q);
-    ptab[e] = make_short2((short)p, (short)q);
-  }
+  for (int e = tid; e < ldm * ncol; e += kGramT) M[e] = 0.0;
+  for (int i = tid; i < np; i += kGramT) dn[i] = i < n ? 0 : 1;
   __syncthreads();
+  // pivot = largest remaining diagonal (first index on ties); -1 once it is <= n eps max diag(G)
+  auto pick_pivot = [&](double thresh) {
+    double bv = -1.0;
+    int bi = n;
+    for (int i = lane; i < n; i += 32) {
+      const double v = dn[i] ? -1.0 : G[i + np * i];
+      if (v > bv) { bv = v; bi = i; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (lane == 0) spiv = (bv > thresh) ? bi : -1;
+  };
   if (warp == 0) {
     double m = 0.0;
     for (int i = lane; i < n; i += 32) m = fmax(m, G[i + np * i]);
     for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) { sdmax = m; srank = n; }
+    if (lane == 0) sdmax = m;
+    pick_pivot(n * 2.2e-16 * m);
   }
   __syncthreads();
   const double thresh = n * 2.2e-16 * sdmax;
-  // ---- pivoted Cholesky (right-looking), L stored in M (column-major, lower)
+  // ---- pivoted Cholesky without row exchanges: M[:, k] = G[:, p] / sqrt(G[p][p]) on the rows
+  // not yet pivoted, G <- G - M[:, k] M[:, k]^T.  M = P L (P the pivot permutation): its
+  // columns have the preconditioning of L, and M M^T = G in the original index order.
+  const int ui = tid & 63, uj = tid >> 6;  // update ownership: G[ui][uj + 4 u]
   for (int k = 0; k < n; ++k) {
-    if (warp == 0) {  // pivot: largest remaining diagonal, first index on ties
-      double bv = -1.0;
-      int bi = n;
-      for (int i = k + lane; i < n; i += 32) {
-        const double v = G[i + np * i];
-        if (v > bv) { bv = v; bi = i; }
-      }
-      for (int o = 16; o; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-      }
-      if (lane == 0) {
-        spiv = bi;
-        if (!(bv > thresh)) srank = k;
-      }
-    }
-    __syncthreads();
-    if (srank <= k) break;  // rank reached: the remaining columns of L are zero
     const int p = spiv;
-    if (p != k) {  // symmetric swap of G rows/cols k <-> p, rows of L computed so far, perm
-      for (int j = tid; j < n; j += kGramT) {
-        double t = G[k + np * j]; G[k + np * j] = G[p + np * j]; G[p + np * j] = t;
-      }
-      __syncthreads();
-      for (int i = tid; i < n; i += kGramT) {
-        double t = G[i + np * k]; G[i + np * k] = G[i + np * p]; G[i + np * p] = t;
-      }
-      for (int j = tid; j < k; j += kGramT) {
-        double t = M[k + np * j]; M[k + np * j] = M[p + np * j]; M[p + np * j] = t;
-      }
-      if (tid == 0) { int t = perm[k]; perm[k] = perm[p]; perm[p] = t; }
-      __syncthreads();
+    if (p < 0) break;  // rank reached: the remaining columns of M are zero
+    const double inv = rsqrt(G[p + np * p]);
+    for (int i = tid; i < np; i += kGramT) {
+      const double l = dn[i] ? 0.0 : G[i + np * p] * inv;
+      lc[i] = l;
+      M[i + ldm * k] = l;
     }
-    const double lkk = sqrt(G[k + np * k]);
-    for (int i = k + tid; i < n; i += kGramT) M[i + np * k] = (i == k) ? lkk : G[i + np * k] / lkk;
     __syncthreads();
-    for (int e = tid; e < (n - k - 1) * (n - k - 1); e += kGramT) {
-      const int i = k + 1 + e % (n - k - 1), j = k + 1 + e / (n - k - 1);
-      G[i + np * j] -= M[i + np * k] * M[j + np * k];
+    if (tid == 0) dn[p] = 1;
+    if (ui < np) {
+      const double li = lc[ui];
+#pragma unroll 4
+      for (int j = uj; j < np; j += kGramT / 64) G[ui + np * j] = fma(-li, lc[j], G[ui + np * j]);
     }
+    __syncthreads();
+    if (warp == 0) pick_pivot(thresh);
     __syncthreads();
   }
-  // ---- one-sided Jacobi on the columns of M
+  // ---- block-ordered one-sided Jacobi on the columns of M
   const double tol2 = tol * tol;
+  const int slot = lane >> 2, q = lane & 3;
+  const int nwk = nb / 2;  // working warps
   int sweeps = 0;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
-    for (int k = warp; k < np; k += nw) {
-      double d = 0.0;
-      for (int r = lane; r < np; r += 32) { const double x = M[r + np * k]; d = fma(x, x, d); }
-      d = warp_sum(d);
-      if (lane == 0) lam[k] = d;
-    }
-    if (tid == 0) sconv = 1;
+    if (tid == 0) sflag = 0;
     __syncthreads();
-    for (int t = 0; t < np - 1; ++t) {
-      const short2 *row = ptab + t * npairs;
-      for (int k0 = warp * kGroups; k0 < npairs; k0 += kGroups * nw) {
-        const int k = k0 + sub;
-        const bool act = k < npairs;
-        const short2 pq = row[act ? k : 0];
-        double *__restrict__ mp = M + np * pq.x;
-        double *__restrict__ mq = M + np * pq.y;
-        double xp[kR], xq[kR], pr[kR];
+    int rot = 0;
+    if (warp < nwk) {  // pairs inside blocks 2w (x) and 2w + 1 (y): round m pairs slot k with k ^ m
+      double *c1 = M + ldm * (16 * warp + slot), *c2 = c1 + 8 * ldm;
+      double x[kV], y[kV];
 #pragma unroll
-        for (int u = 0; u < kR; ++u) {
-          const int r = gl + kL * u;
-          xp[u] = r < np ? mp[r] : 0.0;
-          xq[u] = r < np ? mq[r] : 0.0;
-          pr[u] = xp[u] * xq[u];
+      for (int v = 0; v < kV; ++v) { x[v] = c1[q + 4 * v]; y[v] = c2[q + 4 * v]; }
+#pragma unroll 1
+      for (int m = 1; m < 8; ++m) {
+        const int src = ((slot ^ m) << 2) + q;
+        const bool own_p = slot < (slot ^ m);
+        double px[kV], py[kV];
+#pragma unroll
+        for (int v = 0; v < kV; ++v) {
+          px[v] = __shfl_sync(0xffffffffu, x[v], src);
+          py[v] = __shfl_sync(0xffffffffu, y[v], src);
+        }
+        jac_half<kV>(x, px, own_p, tol2, rot);
+        jac_half<kV>(y, py, own_p, tol2, rot);
+      }
+#pragma unroll
+      for (int v = 0; v < kV; ++v) { c1[q + 4 * v] = x[v]; c2[q + 4 * v] = y[v]; }
+    }
+    __syncthreads();
+    for (int t = 0; t < nb - 1; ++t) {  // pairs between blocks
+      if (warp < nwk) {
+        int bA, bB;
+        rr_pair(warp, t, nb, bA, bB);
+        double *c1 = M + ldm * (8 * bA + slot), *c2 = M + ldm * (8 * bB + slot);
+        double x[kV], y[kV];
+#pragma unroll
+        for (int v = 0; v < kV; ++v) { x[v] = c1[q + 4 * v]; y[v] = c2[q + 4 * v]; }
+        const int nxt = ((slot + 1) & 7) * 4 + q;
+#pragma unroll 1
+        for (int r = 0; r < 8; ++r) {
+          jac_pair<kV>(x, y, tol2, rot);
+#pragma unroll
+          for (int v = 0; v < kV; ++v) y[v] = __shfl_sync(0xffffffffu, y[v], nxt);
         }
 #pragma unroll
-        for (int h = kR / 2; h; h >>= 1)
-#pragma unroll
-          for (int u = 0; u < h; ++u) pr[u] += pr[u + h];
-        double g = pr[0];
-#pragma unroll
-        for (int o = kL / 2; o; o >>= 1) g += __shfl_xor_sync(gmask, g, o, kL);
-        const double a = lam[pq.x], b = lam[pq.y];
-        if (act && g != 0.0 && g * g > tol2 * a * b) {  // group-uniform
-          if (gl == 0) sconv = 0;
-          const double zeta = (b - a) / (2.0 * g);
-          const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-          const double c = rsqrt(fma(tt, tt, 1.0)), s = tt * c;
-#pragma unroll
-          for (int u = 0; u < kR; ++u) {
-            const int r = gl + kL * u;
-            if (r < np) {
-              mp[r] = c * xp[u] - s * xq[u];
-              mq[r] = s * xp[u] + c * xq[u];
-            }
-          }
-          if (gl == 0) {
-            lam[pq.x] = a - tt * g;
-            lam[pq.y] = b + tt * g;
-          }
-        }
+        for (int v = 0; v < kV; ++v) { c1[q + 4 * v] = x[v]; c2[q + 4 * v] = y[v]; }
       }
       __syncthreads();
     }
-    sweeps = sweep + 1;
-    const int done = sconv;
+    if (rot) sflag = 1;
     __syncthreads();
-    if (done) break;
+    sweeps = sweep + 1;
+    const int more = sflag;
+    __syncthreads();
+    if (!more) break;
   }
   if (tid == 0 && info) *info = sweeps;
-  for (int k = warp; k < np; k += nw) {  // exact column norms
+  for (int k = warp; k < np; k += kGramT / 32) {  // exact column norms
     double d = 0.0;
-    for (int r = lane; r < np; r += 32) { const double x = M[r + np * k]; d = fma(x, x, d); }
+    for (int r = lane; r < np; r += 32) { const double x = M[r + ldm * k]; d = fma(x, x, d); }
     d = warp_sum(d);
     if (lane == 0) lam[k] = d;
   }
@@ -591,7 +689,7 @@ __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restri
     if (rank >= n) continue;
     w[rank] = di;
     const double inv = di > 0.0 ? 1.0 / sqrt(di) : 0.0;
-    for (int r = 0; r < n; ++r) Vout[perm[r] + (int64_t)n * rank] = M[r + np * i] * inv;
+    for (int r = 0; r < n; ++r) Vout[r + (int64_t)n * rank] = M[r + ldm * i] * inv;
   }
   // v_k from a normalised column is accurate to ~eps sqrt(lambda_0 / lambda_k): request the
   // unpreconditioned solver when the wanted rank reaches lambda_k < 1e-8 lambda_0
@@ -921,12 +1019,18 @@ void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q, const 
 void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps, int r_need) {
   const int np = n + (n & 1);
   if (np > 64) return sym_eig(c, A, n, w, V, sweeps);
-  const size_t need = sizeof(double) * (2 * (size_t)np * np + np) + sizeof(int) * (np + 1) +
-                      sizeof(short2) * (size_t)(np - 1) * (np / 2) + 64;
+  const int nb = ((n + 15) / 16) * 2, ncol = 8 * nb;
+  const int kv = np <= 16 ? 4 : (np <= 32 ? 8 : 16);
+  const int ldm = 4 * kv + 4;
+  const size_t need = sizeof(double) * ((size_t)np * np + (size_t)ldm * ncol + ncol + np) + sizeof(int) * np + 64;
   DevBuf<int> refine(c, 1);
-  RT_CUDA(cudaFuncSetAttribute(gram_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
-  RT_LAUNCH(c, gram_eig_kernel, 1, kGramT, need, A, n, w, V, 3e-15 * std::sqrt((double)n), 40, sweeps,
-            std::max(1, std::min(r_need, n)), refine.p);
+  const double tol = 3e-15 * std::sqrt((double)n);
+  const int rn = std::max(1, std::min(r_need, n));
+#define RT_GE(KV)                                                                                      \
+  RT_CUDA(cudaFuncSetAttribute(gram_eig_kernel<KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need)); \
+  RT_LAUNCH(c, gram_eig_kernel<KV>, 1, kGramT, need, A, n, w, V, tol, 40, sweeps, rn, refine.p)
+  if (kv == 4) { RT_GE(4); } else if (kv == 8) { RT_GE(8); } else { RT_GE(16); }
+#undef RT_GE
   sym_eig(c, A, n, w, V, nullptr, refine.p);  // no-op unless the gate asks for it
 }
 
