@@ -22,6 +22,7 @@ SOURCES = ["rtucker.cu", "dense.cu", "adaptive.cu", "sparse.cu", "sketch.cu", "s
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                      "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
+NVCC_FLAGS += os.environ.get("RTUCKER_NVCC_EXTRA", "").split()  # experiments only (e.g. -DRT_EXP_...)
 
 
 def nvcc() -> str:

@@ -191,44 +191,55 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------- X workers
     const int wt = threadIdx.x - 32 * (2 + kGen);  // 0 .. 32*kWorkers-1
     const int rows_st = min(NT * 128, p.nbox * p.BR);  // operand rows filled from staging
+    // rows i = wt + 32 kWorkers j of every stage: staging offsets (floats) and operand offsets
+    // (bytes) are fixed, computed once
+    constexpr int kRJ = (8 * 128 + 32 * kWorkers - 1) / (32 * kWorkers);  // NT <= 8
+    int soff[kRJ], ooff[kRJ];
+#pragma unroll
+    for (int j = 0; j < kRJ; ++j) {
+      const int i = wt + 32 * kWorkers * j;
+      soff[j] = (i / p.BR) * (p.BR * kBK) + i % p.BR;
+      ooff[j] = (i >> 3) * 256 + (i & 7) * 16;
+    }
     double nsq = 0.0;
+    int so = 0, ss = 0;
+    uint32_t po = 0, ps = 0;  // phase parities of the current operand / staging slot
     for (int it = 0; it < nst; ++it) {
-      const int so = it % NSO, ss = it % NSS;
       // the MMAs of this operand slot's previous use must have finished reading it
-      if (it >= NSO) tc::mbar_wait(&xempty[so], ((it / NSO) & 1) ^ 1);
+      if (it >= NSO) tc::mbar_wait(&xempty[so], po ^ 1);
       // X staging [box][c][BR rows] -> hi / lo K-major tiles (rows i, K = c); rows >= I are
       // zero-filled by the TMA, rows beyond the staging extent are never read by a valid D row
-      tc::mbar_wait(&full[ss], (it / NSS) & 1);
+      tc::mbar_wait(&full[ss], ps);
       const float *st = (const float *)(sb + (size_t)ss * sbytes);
       unsigned char *hs = hb + (size_t)so * abytes, *ls = lb + (size_t)so * abytes;
       float acc = 0.f;
-      int box = 0, r = wt;
-      while (r >= p.BR) { r -= p.BR; ++box; }
-      for (int i = wt; i < rows_st; i += 32 * kWorkers) {
-        const float *src = st + box * (p.BR * kBK) + r;
-        float x[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) x[u] = src[u * p.BR];
+      for (int j = 0; j < kRJ; ++j) {
+        if (wt + 32 * kWorkers * j < rows_st) {
+          const float *src = st + soff[j];
+          float x[8];
 #pragma unroll
-        for (int cq = 0; cq < 2; ++cq) {
-          float4 h, l;
-          h.x = tc::tf32_hi(x[4 * cq]); h.y = tc::tf32_hi(x[4 * cq + 1]);
-          h.z = tc::tf32_hi(x[4 * cq + 2]); h.w = tc::tf32_hi(x[4 * cq + 3]);
-          l.x = tc::tf32_lo(x[4 * cq], h.x); l.y = tc::tf32_lo(x[4 * cq + 1], h.y);
-          l.z = tc::tf32_lo(x[4 * cq + 2], h.z); l.w = tc::tf32_lo(x[4 * cq + 3], h.w);
-          const int off = (i >> 3) * 256 + cq * 128 + (i & 7) * 16;
-          *(float4 *)(hs + off) = h;
-          *(float4 *)(ls + off) = l;
+          for (int u = 0; u < 8; ++u) x[u] = src[u * p.BR];
+#pragma unroll
+          for (int cq = 0; cq < 2; ++cq) {
+            float4 h, l;
+            h.x = tc::tf32_hi(x[4 * cq]); h.y = tc::tf32_hi(x[4 * cq + 1]);
+            h.z = tc::tf32_hi(x[4 * cq + 2]); h.w = tc::tf32_hi(x[4 * cq + 3]);
+            l.x = tc::tf32_lo(x[4 * cq], h.x); l.y = tc::tf32_lo(x[4 * cq + 1], h.y);
+            l.z = tc::tf32_lo(x[4 * cq + 2], h.z); l.w = tc::tf32_lo(x[4 * cq + 3], h.w);
+            *(float4 *)(hs + ooff[j] + cq * 128) = h;
+            *(float4 *)(ls + ooff[j] + cq * 128) = l;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc = fmaf(x[u], x[u], acc);
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u) acc = fmaf(x[u], x[u], acc);
-        r += 32 * kWorkers;
-        while (r >= p.BR) { r -= p.BR; ++box; }
       }
       nsq += (double)acc;
       tc::mbar_arrive(&sfree[ss]);       // staging slot may be refilled
       tc::fence_proxy_async_smem();
       tc::mbar_arrive(&xready[so]);
+      if (++so == NSO) { so = 0; po ^= 1; }
+      if (++ss == NSS) { ss = 0; ps ^= 1; }
     }
     // ---- epilogue: TMEM -> fp64 partial[blockIdx.x][k * I + i]
     const int q4 = warp & 3;                       // TMEM lane quadrant of this warp
