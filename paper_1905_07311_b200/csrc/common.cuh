@@ -63,6 +63,11 @@ struct Ctx {
   std::vector<PhaseEvent> events;
   double phase_ms[PH_COUNT * kMaxModes] = {0};
   int64_t phase_n[PH_COUNT * kMaxModes] = {0};
+  // stream-K hand-off flags (one per CTA of a persistent grid); a launch signals with its own
+  // epoch value, so the flags never need resetting
+  unsigned *sk_flags = nullptr;
+  int sk_n = 0;
+  unsigned sk_epoch = 0;
 };
 
 // RAII scope that records a start/stop event pair when profiling is on.

@@ -253,6 +253,7 @@ rtucker_status rtucker_ctx_create(int device, void *cuda_stream, const void *ncc
 void rtucker_ctx_destroy(rtucker_ctx *ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->c.stream);
+  if (ctx->c.sk_flags) cudaFree(ctx->c.sk_flags);
   comm_destroy(ctx->c.comm);
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
   delete ctx;

@@ -552,10 +552,40 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dfma_kernel(const Tin *__restrict_
 // B col-major, lane -> (k = lane & 3, n = lane >> 2); C lane -> (m = lane >> 2, n = 2 (lane & 3) + {0, 1}).
 constexpr int kMA = 68;  // As row stride (doubles)
 constexpr int kMX = 20;  // Xs row stride (doubles), rows = p
+// Epilogue tile T[p][kTS] (kTS = 4 mod 16 doubles): conflict-free for the accumulator stores
+// and for the Gram's DMMA fragment loads.  The Gram partial G += T^T T runs on the fp64 tensor
+// cores too: the 36 upper 8x8 tiles of the 64 x 64 Gram are spread over the 8 warps.
+constexpr int kTS = 68;
+__device__ __forceinline__ void gram_tile_ab(int t, int &a, int &b) {
+  a = 0;
+  while (t >= 8 - a) { t -= 8 - a; ++a; }
+  b = a + t;
+}
+
+// Stream-K work split (Osama et al. style): the ntiles x nchunk MAC iterations are divided
+// evenly over the persistent grid, so a short tile list (P = L R of a few hundred columns)
+// still fills every SM.  CTA b owns iterations [b T / G, (b+1) T / G).  A segment that starts
+// mid-tile can only be the CTA's FIRST segment: it runs first, its accumulators go to fix[b]
+// and flags[b] is set to this launch's epoch.  The CTA that runs a tile's chunk 0 (late in
+// its own range) adds the partials of the CTAs b+1, b+2, .. that cover the rest of the tile
+// (fixed order, deterministic), then runs the epilogue.  Partials are produced before any
+// CTA waits, all CTAs are co-resident (grid = #SMs, one CTA per SM), so the hand-off
+// neither serialises nor deadlocks.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 template <typename Tin, bool STORE, bool GRAM>
 __global__ void __launch_bounds__(kDT, 1) ttm_dmma_kernel(const Tin *__restrict__ X, int64_t L, int64_t I, int64_t R,
                                                           const double *__restrict__ A, int64_t lda, int J,
-                                                          double *__restrict__ out, double *__restrict__ gram_partial) {
+                                                          double *__restrict__ out, double *__restrict__ gram_partial,
+                                                          double *__restrict__ fix, unsigned *__restrict__ flags,
+                                                          unsigned epoch) {
   extern __shared__ __align__(16) double dsm[];
   double *Xs = dsm;                        // [kDP][kMX]
   double *As = Xs + kDP * kMX;             // [kDK][kMA]
@@ -565,14 +595,22 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_kernel(const Tin *__restrict_
   const int64_t P = L * R;
   const int64_t ntiles = (P + kDP - 1) / kDP;
   const int nchunk = (int)((I + kDK - 1) / kDK);
-  double g[16];
+  const int64_t total = ntiles * nchunk, G = gridDim.x, b = blockIdx.x;
+  auto seg_start = [&](int64_t cta) { return cta * total / G; };
+  double gacc[5][2];
 #pragma unroll
-  for (int e = 0; e < 16; ++e) g[e] = 0.0;
-  const int gj1 = (tid >> 4) * 4, gj2 = (tid & 15) * 4;
+  for (int s5 = 0; s5 < 5; ++s5) gacc[s5][0] = gacc[s5][1] = 0.0;
   Tin pre[16];
   double apre[4];
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+  int64_t it = seg_start(b);
+  const int64_t it_end = seg_start(b + 1);
+  while (it < it_end) {
+    const int64_t tile = it / nchunk;
+    const int c0 = (int)(it - tile * nchunk);
+    const int64_t rem = it_end - it;
+    const int c1 = (c0 + rem < nchunk) ? (int)(c0 + rem) : nchunk;
+    it += c1 - c0;
     const int64_t p0 = tile * kDP;
     const int64_t pl0 = p0 % L, pr0 = p0 / L;
     int64_t mycol = -1;
@@ -631,13 +669,13 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_kernel(const Tin *__restrict_
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 8; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
-    load_chunk(0);
-    for (int ch = 0; ch < nchunk; ++ch) {
+      for (int bb = 0; bb < 8; ++bb) { acc[a][bb][0] = 0.0; acc[a][bb][1] = 0.0; }
+    load_chunk(c0);
+    for (int ch = c0; ch < c1; ++ch) {
       __syncthreads();
       store_chunk();
       __syncthreads();
-      if (ch + 1 < nchunk) load_chunk(ch + 1);
+      if (ch + 1 < c1) load_chunk(ch + 1);
 #pragma unroll
       for (int ks = 0; ks < kDK / 4; ++ks) {
         double af[4], bf[8];
@@ -654,9 +692,45 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_kernel(const Tin *__restrict_
                          : "d"(af[jt]), "d"(bf[pt]));
       }
     }
+    if (c0 > 0) {  // tile begun by a lower CTA (this CTA's first segment): hand the partial over
+      double *f = fix + b * (int64_t)(64 * kDT);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 8; ++bb)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) f[((a * 8 + bb) * 2 + h) * kDT + tid] = acc[a][bb][h];
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_release_u32(flags + b, epoch);
+      continue;
+    }
+    if (c1 < nchunk) {  // add the partials of the CTAs that run the rest of this tile
+      const int64_t tend = (tile + 1) * nchunk;
+      for (int64_t bn = b + 1; bn < G; ++bn) {
+        const int64_t se = seg_start(bn + 1);
+        if (seg_start(bn) == se) continue;  // empty range (more CTAs than iterations)
+        if (tid == 0) {
+          const long long t0 = clock64();
+          while (ld_acquire_u32(flags + bn) != epoch) {  // a lost hand-off traps instead of hanging
+            __nanosleep(32);
+            if (clock64() - t0 > 8000000000LL) __trap();
+          }
+        }
+        __syncthreads();
+        const double *f = fix + bn * (int64_t)(64 * kDT);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int bb = 0; bb < 8; ++bb)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) acc[a][bb][h] += __ldcg(f + ((a * 8 + bb) * 2 + h) * kDT + tid);
+        if (se >= tend) break;
+      }
+    }
     // ---- epilogue: acc[jt][pt][h] = out(j = 32 wj + 8 jt + fr, p = 64 wp + 8 pt + 2 fc + h)
     if (STORE || GRAM) {
-      for (int half = 0; half < 2; ++half) {  // stage 128 columns at a time: T[p][65]
+      for (int half = 0; half < 2; ++half) {  // stage 128 columns at a time: T[p][kTS]
         __syncthreads();
         double *T = dsm;
         if ((wp >> 1) == half) {
@@ -667,7 +741,7 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_kernel(const Tin *__restrict_
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
                 const int pp = 64 * (wp & 1) + 8 * pt + 2 * fc + h;
-                T[pp * 65 + 32 * wj + 8 * jt + fr] = acc[jt][pt][h];
+                T[pp * kTS + 32 * wj + 8 * jt + fr] = acc[jt][pt][h];
               }
         }
         __syncthreads();
@@ -678,7 +752,7 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_kernel(const Tin *__restrict_
             double *dst = out + pb * J;
             for (int64_t e = tid; e < ncol * J; e += kDT) {
               const int pp = (int)(e / J), j = (int)(e - (int64_t)pp * J);
-              dst[e] = T[pp * 65 + j];
+              dst[e] = T[pp * kTS + j];
             }
           } else {
             for (int e = tid; e < 128 * 64; e += kDT) {
@@ -686,30 +760,48 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_kernel(const Tin *__restrict_
               if (pp < ncol && j < J) {
                 int64_t l = pl0 + 128 * half + pp, r = pr0;
                 while (l >= L) { l -= L; ++r; }
-                out[l + L * (j + (int64_t)J * r)] = T[pp * 65 + j];
+                out[l + L * (j + (int64_t)J * r)] = T[pp * kTS + j];
               }
             }
           }
         }
-        if (GRAM) {
-          for (int pp = 0; pp < (int)(ncol > 0 ? ncol : 0); ++pp) {
-            double a4[4], b4[4];
+        if (GRAM) {  // G += T^T T on the tensor cores (columns p >= P of T are zero)
 #pragma unroll
-            for (int q = 0; q < 4; ++q) { a4[q] = T[pp * 65 + gj1 + q]; b4[q] = T[pp * 65 + gj2 + q]; }
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-#pragma unroll
-              for (int s = 0; s < 4; ++s) g[q * 4 + s] = fma(a4[q], b4[s], g[q * 4 + s]);
+          for (int s5 = 0; s5 < 5; ++s5) {
+            const int t = warp + 8 * s5;
+            if (t < 36) {
+              int ga, gb;
+              gram_tile_ab(t, ga, gb);
+              const double *ta = T + fc * kTS + 8 * ga + fr;
+              const double *tb = T + fc * kTS + 8 * gb + fr;
+#pragma unroll 8
+              for (int k0 = 0; k0 < 128; k0 += 4)
+                asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                             : "+d"(gacc[s5][0]), "+d"(gacc[s5][1])
+                             : "d"(ta[k0 * kTS]), "d"(tb[k0 * kTS]));
+            }
           }
         }
       }
     }
   }
   if (GRAM) {
+    double *gp = gram_partial + b * 4096;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-      for (int s = 0; s < 4; ++s) gram_partial[(int64_t)blockIdx.x * 4096 + (gj1 + q) * 64 + gj2 + s] = g[q * 4 + s];
+    for (int s5 = 0; s5 < 5; ++s5) {
+      const int t = warp + 8 * s5;
+      if (t < 36) {
+        int ga, gb;
+        gram_tile_ab(t, ga, gb);
+        const int gi = 8 * ga + fr, gj = 8 * gb + 2 * fc;
+        gp[gi * 64 + gj] = gacc[s5][0];
+        gp[gi * 64 + gj + 1] = gacc[s5][1];
+        if (ga != gb) {
+          gp[gj * 64 + gi] = gacc[s5][0];
+          gp[(gj + 1) * 64 + gi] = gacc[s5][1];
+        }
+      }
+    }
   }
 }
 
@@ -727,16 +819,6 @@ __device__ __forceinline__ void cp_async16(void *dst, const void *src, bool vali
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// Epilogue tile T[p][kTS] (kTS = 4 mod 16 doubles): conflict-free for the accumulator stores
-// and for the Gram's DMMA fragment loads.  The Gram partial G += T^T T runs on the fp64 tensor
-// cores too: the 36 upper 8x8 tiles of the 64 x 64 Gram are spread over the 8 warps.
-constexpr int kTS = 68;
-__device__ __forceinline__ void gram_tile_ab(int t, int &a, int &b) {
-  a = 0;
-  while (t >= 8 - a) { t -= 8 - a; ++a; }
-  b = a + t;
-}
 
 template <typename Tin, bool STORE, bool GRAM>
 __global__ void __launch_bounds__(kDT, 1) ttm_dmma_l1_kernel(const Tin *__restrict__ X, int64_t I, int64_t P,
@@ -920,12 +1002,11 @@ void launch_ttm_dfma(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t 
     else if (out) RT_DL(true, false);
     else RT_DL(false, true);
 #undef RT_DL
-  } else {
-    const size_t smem = use_dfma ? std::max(sizeof(double) * (kDK * kDS + kDK * 64), sizeof(double) * 128 * 65)
-                                 : std::max(sizeof(double) * (kDP * kMX + kDK * kMA), sizeof(double) * 128 * 65);
+  } else if (use_dfma) {
+    const size_t smem = std::max(sizeof(double) * (kDK * kDS + kDK * 64), sizeof(double) * 128 * 65);
 #define RT_DF(ST, GR)                                                                                 \
   do {                                                                                                \
-    auto k = use_dfma ? ttm_dfma_kernel<Tin, ST, GR> : ttm_dmma_kernel<Tin, ST, GR>;                  \
+    auto k = ttm_dfma_kernel<Tin, ST, GR>;                                                            \
     RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));         \
     RT_LAUNCH(c, k, grid, kDT, smem, X, v.L, v.I, v.R, A, lda, J, out, part.p);                       \
   } while (0)
@@ -933,6 +1014,31 @@ void launch_ttm_dfma(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t 
     else if (out) RT_DF(true, false);
     else RT_DF(false, true);
 #undef RT_DF
+  } else {
+    // stream-K over all SMs (the tile list alone is often shorter than the SM count)
+    const int sk_grid = c.num_sms;
+    if (c.sk_n < sk_grid) {
+      if (c.sk_flags) RT_CUDA(cudaFree(c.sk_flags));
+      RT_CUDA(cudaMalloc((void **)&c.sk_flags, sizeof(unsigned) * sk_grid));
+      RT_CUDA(cudaMemsetAsync(c.sk_flags, 0, sizeof(unsigned) * sk_grid, c.stream));
+      c.sk_n = sk_grid;
+    }
+    if (++c.sk_epoch == 0) ++c.sk_epoch;  // 0 is the initial flag value
+    DevBuf<double> fix(c, (size_t)sk_grid * 64 * kDT);
+    if (gram) part.alloc(c, (size_t)sk_grid * 4096);
+    const size_t smem = std::max(sizeof(double) * (kDP * kMX + kDK * kMA), sizeof(double) * 128 * kTS);
+#define RT_DM(ST, GR)                                                                                 \
+  do {                                                                                                \
+    auto k = ttm_dmma_kernel<Tin, ST, GR>;                                                            \
+    RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));         \
+    RT_LAUNCH(c, k, sk_grid, kDT, smem, X, v.L, v.I, v.R, A, lda, J, out, part.p, fix.p, c.sk_flags, c.sk_epoch); \
+  } while (0)
+    if (out && gram) RT_DM(true, true);
+    else if (out) RT_DM(true, false);
+    else RT_DM(false, true);
+#undef RT_DM
+    if (gram) RT_LAUNCH(c, gram_reduce2_kernel, J * J, 128, 0, part.p, sk_grid, J, gram);
+    return;
   }
   if (gram) RT_LAUNCH(c, gram_reduce2_kernel, J * J, 128, 0, part.p, grid, J, gram);
 }
