@@ -196,56 +196,60 @@ void launch_sketch(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int64_t 
 
 // ------------------------------------------------------------ fp64-product sketch ----
 // Y[i, k] = sum_p X(l, i, r) Omega(p, k), p = l + L r, with fp64 products and sums (X fp32
-// or fp64; normals fp32 or fp64 per reading R3).  A CTA owns 128 rows x 64 sketch columns
-// and a contiguous range of p (split-K); thread (ti, tk) the rows ti + 16 u (u < 8) and the
-// columns 4 tk .. 4 tk + 3.  X and Omega are staged 16 values of p at a time (Omega
-// generated into shared memory: ceil(I/128) row tiles regenerate it, 0.5 normals per element
-// at most); partials per split are summed in a fixed order (deterministic).
-constexpr int kSP = 16;  // p per chunk
+// or fp64; normals fp32 or fp64 per reading R3), on the fp64 tensor cores (mma.m8n8k4).
+// A CTA owns 128 rows x 64 sketch columns and a contiguous range of p (split-K); warp
+// (wm = w & 3, wn = w >> 2) the 32 x 32 block rows 32 wm.., columns 32 wn.. (4 x 4 MMA
+// tiles).  X and Omega are staged 16 values of p at a time (Omega generated into shared
+// memory: ceil(I/128) row tiles regenerate it); partials per split are summed in a fixed
+// order (deterministic).
+constexpr int kSP = 16;   // p per chunk
+constexpr int kSX = 136;  // Xs row stride (doubles, = 8 mod 16): conflict-free A fragments
+constexpr int kSO = 72;   // Os row stride
 template <typename Tin, typename TN>
 __global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict__ X, int64_t L, int64_t I, int64_t R,
                                                           int64_t cols_per_split, uint64_t seed, int mode, int ell,
                                                           int64_t k0, int64_t col_offset, double *__restrict__ partial,
                                                           double *__restrict__ norm_partial) {
-  __shared__ double Xs[kSP][128 + 1];
-  __shared__ __align__(16) double Os[kSP][64];
+  __shared__ __align__(16) double Xs[kSP * kSX];
+  __shared__ __align__(16) double Os[kSP * kSO];
   __shared__ double sred[8];
-  const int tid = threadIdx.x, ti = tid & 15, tk = tid >> 4;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 3, wn = warp >> 2, fr = lane >> 2, fc = lane & 3;
   const int64_t i0 = (int64_t)blockIdx.x * 128;
   const int64_t P = L * R;
   const int64_t pbeg = (int64_t)blockIdx.y * cols_per_split, pend = min(P, pbeg + cols_per_split);
   const int64_t jb0 = k0 >> 2;
   const int nb = (int)(((k0 + ell - 1) >> 2) - jb0 + 1);
-  double acc[8][4];
+  double acc[4][4][2];
 #pragma unroll
-  for (int u = 0; u < 8; ++u)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) acc[u][q] = 0.0;
+    for (int q = 0; q < 4; ++q) acc[a][q][0] = acc[a][q][1] = 0.0;
   double nsq = 0.0;
-  for (int e = tid; e < kSP * 64; e += 256) Os[e >> 6][e & 63] = 0.0;
+  for (int e = tid; e < kSP * kSO; e += 256) Os[e] = 0.0;
   // X staging with a register prefetch of the next chunk (8 values per thread and chunk)
   //   L == 1: element e = tid + 256 q: row ii = e & 127, column pp = e >> 7 (coalesced along i)
   //   L > 1 : element e: column pp = e % 16, row ii = e / 16 (coalesced along p = l)
   Tin pre[kSP * 128 / 256];
   auto load_x = [&](int64_t p0) {
-    const int64_t pl0 = p0 % L, pr0 = p0 / L;
+    if (L == 1) {
 #pragma unroll
-    for (int q = 0; q < kSP * 128 / 256; ++q) {
-      const int e = tid + 256 * q;
-      int ii, pp;
-      if (L == 1) { ii = e & 127; pp = e >> 7; } else { pp = e % kSP; ii = e / kSP; }
-      const int64_t i = i0 + ii, p = p0 + pp;
-      Tin v = Tin(0);
-      if (i < I && p < pend) {
-        if (L == 1) {
-          v = X[i + I * p];
-        } else {
-          int64_t l = pl0 + pp, r = pr0;
-          while (l >= L) { l -= L; ++r; }
-          v = X[l + L * (i + I * r)];
-        }
+      for (int q = 0; q < kSP * 128 / 256; ++q) {
+        const int e = tid + 256 * q, ii = e & 127, pp = e >> 7;
+        const int64_t i = i0 + ii, p = p0 + pp;
+        pre[q] = (i < I && p < pend) ? X[i + I * p] : Tin(0);
       }
-      pre[q] = v;
+    } else {  // this thread's column pp = tid % 16 is the same for every q: one div per chunk
+      const int pp = tid % kSP;
+      const int64_t p = p0 + pp;
+      const bool pok = p < pend;
+      const int64_t r = p / L, l = p - r * L;
+      const Tin *base = X + l + L * I * r;
+#pragma unroll
+      for (int q = 0; q < kSP * 128 / 256; ++q) {
+        const int64_t i = i0 + tid / kSP + 16 * q;
+        pre[q] = (pok && i < I) ? base[L * i] : Tin(0);
+      }
     }
   };
   if (pbeg < pend) load_x(pbeg);
@@ -258,47 +262,51 @@ __global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict_
       if (L == 1) { ii = e & 127; pp = e >> 7; } else { pp = e % kSP; ii = e / kSP; }
       const double v = (double)pre[q];
       nsq = fma(v, v, nsq);
-      Xs[pp][ii] = v;
+      Xs[pp * kSX + ii] = v;
     }
-    // Omega chunk: rows p0.., columns k0.. (Philox block granularity)
+    // Omega chunk: rows p0.., columns k0.. (Philox block granularity); rows past pend are 0
     for (int e = tid; e < kSP * nb; e += 256) {
       const int pp = e / nb, jb = e % nb;
       const int64_t p = p0 + pp;
-      if (p >= pend) continue;
       const uint4 w = omega_words(seed, mode, 0, (uint64_t)(p + col_offset), (uint32_t)(jb0 + jb));
       Normal4<TN> z(w);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t kk = 4 * (jb0 + jb) + q - k0;
-        if (kk >= 0 && kk < ell) Os[pp][kk] = (double)z.v[q];
+        if (kk >= 0 && kk < ell) Os[pp * kSO + kk] = p < pend ? (double)z.v[q] : 0.0;
       }
     }
     __syncthreads();
-    if (p0 + kSP < pend) load_x(p0 + kSP);  // in flight during the DFMA block
-#pragma unroll 4
-    for (int pp = 0; pp < kSP; ++pp) {
-      double a[8];
+    if (p0 + kSP < pend) load_x(p0 + kSP);  // in flight during the MMA block
 #pragma unroll
-      for (int u = 0; u < 8; ++u) a[u] = Xs[pp][ti + 16 * u];
-      const double2 b01 = *reinterpret_cast<const double2 *>(&Os[pp][4 * tk]);
-      const double2 b23 = *reinterpret_cast<const double2 *>(&Os[pp][4 * tk + 2]);
-      const double b[4] = {b01.x, b01.y, b23.x, b23.y};
+    for (int ks = 0; ks < kSP / 4; ++ks) {
+      double af[4], bf[4];
 #pragma unroll
-      for (int u = 0; u < 8; ++u)
+      for (int mt = 0; mt < 4; ++mt) af[mt] = Xs[(4 * ks + fc) * kSX + 32 * wm + 8 * mt + fr];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc[u][q] = fma(a[u], b[q], acc[u][q]);
+      for (int nt = 0; nt < 4; ++nt) bf[nt] = Os[(4 * ks + fc) * kSO + 32 * wn + 8 * nt + fr];
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1])
+                       : "d"(af[mt]), "d"(bf[nt]));
     }
   }
+  // C fragment: acc[mt][nt][h] = Y(i = 32 wm + 8 mt + fr, k = 32 wn + 8 nt + 2 fc + h)
   double *dst = partial + (int64_t)blockIdx.y * I * ell;
 #pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int64_t i = i0 + ti + 16 * u;
+  for (int mt = 0; mt < 4; ++mt) {
+    const int64_t i = i0 + 32 * wm + 8 * mt + fr;
     if (i >= I) continue;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int k = 4 * tk + q;
-      if (k < ell) dst[(int64_t)k * I + i] = acc[u][q];
-    }
+    for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = 32 * wn + 8 * nt + 2 * fc + h;
+        if (k < ell) dst[(int64_t)k * I + i] = acc[mt][nt][h];
+      }
   }
   if (norm_partial) {
     for (int o = 16; o; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
@@ -317,7 +325,8 @@ void launch_sketch_dfma(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int
                         int64_t col_offset, double *Y, double *normsq) {
   const int gx = ceil_div(v.I, 128);
   const int64_t P = v.L * v.R;
-  int64_t target = std::max<int64_t>(1, (int64_t)c.num_sms * 3 / gx);
+  // one full wave: 2 CTAs of 256 threads per SM (126 registers per thread)
+  int64_t target = std::max<int64_t>(1, (int64_t)c.num_sms * 2 / gx);
   int64_t maxsplit = std::max<int64_t>(1, P / (4 * kSP));
   int64_t nsplit = std::min<int64_t>(target, maxsplit);
   int64_t cps = ((P + nsplit - 1) / nsplit + kSP - 1) / kSP * kSP;
