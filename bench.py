@@ -229,6 +229,7 @@ def main():
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-phases", action="store_true", help="time without the per-phase events")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -269,7 +270,7 @@ def main():
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, barrier + sync on both sides, CUDA events on the ctx stream
-    ctx.set_profiling(True)
+    ctx.set_profiling(not args.no_phases)
     ctx.phase_times(reset=True)
     clocks = Clocks(local)
     clocks.start()
@@ -281,14 +282,17 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     results = []
+    th0 = time.perf_counter()
     for _ in range(args.steps):
         results.append(step(x))
+    host_ms = (time.perf_counter() - th0) * 1e3 / args.steps
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     launches = ctx.launches - l0
     ms_local = e0.elapsed_time(e1) / args.steps
+    print(f"[bench] host enqueue {host_ms:.3f} ms/step, device {ms_local:.3f} ms/step", file=sys.stderr)
     clk = clocks.stop()
     phases = ctx.phase_times(reset=True)
     ctx.set_profiling(False)

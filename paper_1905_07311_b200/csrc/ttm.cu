@@ -820,6 +820,16 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// Epilogue staging of the L == 1 kernel: kTP columns of the tile at a time in its own buffer
+// (after the stage ring), so the copies of the next tile's first chunks run during the
+// epilogue of this one (the chunk sequence is flat across the CTA's tiles).
+template <typename Tin>
+__host__ __device__ constexpr int l1_tp() { return sizeof(Tin) == 4 ? 64 : 128; }
+template <typename Tin>
+__host__ __device__ constexpr size_t l1_stage_bytes() {
+  return (size_t)kDP * (l1_chunk<Tin>() + 4) * sizeof(Tin) + 64 * (l1_chunk<Tin>() + 4) * 8;
+}
+
 template <typename Tin, bool STORE, bool GRAM>
 __global__ void __launch_bounds__(kDT, 1) ttm_dmma_l1_kernel(const Tin *__restrict__ X, int64_t I, int64_t P,
                                                              const double *__restrict__ A, int64_t lda, int J,
@@ -832,13 +842,17 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_l1_kernel(const Tin *__restri
   constexpr int kQX = kDKt / kVX;                        // 16-byte units per X row of a chunk
   constexpr int kUXT = kDP * kQX / kDT;                 // X units per thread per chunk
   constexpr int kUAT = 64 * (kDKt / 2) / kDT;            // A units per thread per chunk
+  constexpr int kTP = l1_tp<Tin>();                     // epilogue columns per pass
   static_assert(kDP * kQX % kDT == 0 && 64 * (kDKt / 2) % kDT == 0, "unit split");
   unsigned char *sbase = reinterpret_cast<unsigned char *>(dsm);
+  double *T = reinterpret_cast<double *>(sbase + kNST * (kXStage + kAStage));  // [kTP][kTS]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int wj = warp & 1, wp = warp >> 1;
   const int fr = lane >> 2, fc = lane & 3;
   const int64_t ntiles = (P + kDP - 1) / kDP;
   const int nchunk = (int)((I + kDKt - 1) / kDKt);
+  const int64_t mytiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t total = mytiles * nchunk;
   // Gram tiles of this warp: t = warp + 8 s (s < 5, t < 36)
   double gacc[5][2];
 #pragma unroll
@@ -849,87 +863,94 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_l1_kernel(const Tin *__restri
   const int ar = tid / (kDKt / 2), aq = tid % (kDKt / 2);
   const double *abase = A + 2 * aq + lda * ar;
 
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int64_t p0 = tile * kDP;
+  auto issue = [&](int64_t g) {  // flat chunk g of this CTA: tile g / nchunk, chunk g % nchunk
+    const int64_t tk = g / nchunk;
+    const int ch = (int)(g - tk * nchunk);
+    const int64_t p0 = (blockIdx.x + tk * gridDim.x) * kDP;
     const Tin *xbase = X + kVX * xq + I * (p0 + xr);
-    auto issue = [&](int ch) {
-      const int st = ch % kNST;
-      Tin *xs = reinterpret_cast<Tin *>(sbase + st * (kXStage + kAStage));
-      double *as = reinterpret_cast<double *>(sbase + st * (kXStage + kAStage) + kXStage);
-      const int64_t i0 = (int64_t)ch * kDKt;
-      const bool iok = i0 + kVX * xq < I;
+    const int st = (int)(g % kNST);
+    Tin *xs = reinterpret_cast<Tin *>(sbase + st * (kXStage + kAStage));
+    double *as = reinterpret_cast<double *>(sbase + st * (kXStage + kAStage) + kXStage);
+    const int64_t i0 = (int64_t)ch * kDKt;
+    const bool iok = i0 + kVX * xq < I;
 #pragma unroll
-      for (int k = 0; k < kUXT; ++k) {
-        const int pp = xr + (kDT / kQX) * k;
-        const bool ok = iok && p0 + pp < P;
-        cp_async16(xs + pp * kSt + kVX * xq, ok ? (const void *)(xbase + i0 + I * (int64_t)((kDT / kQX) * k)) : (const void *)X,
-                   ok);
-      }
-      const bool aiok = i0 + 2 * aq < I;
-#pragma unroll
-      for (int k = 0; k < kUAT; ++k) {
-        const int j = ar + (kDT / (kDKt / 2)) * k;
-        const bool ok = aiok && j < J;
-        cp_async16(as + j * kSt + 2 * aq, ok ? (const void *)(abase + i0 + lda * (int64_t)((kDT / (kDKt / 2)) * k)) : (const void *)A,
-                   ok);
-      }
-    };
-    double acc[4][8][2];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < 8; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
-    __syncthreads();  // previous tile's epilogue is done with the stage buffers
-#pragma unroll
-    for (int s = 0; s < kNST - 1; ++s) {
-      if (s < nchunk) issue(s);
-      cp_async_commit();
+    for (int k = 0; k < kUXT; ++k) {
+      const int pp = xr + (kDT / kQX) * k;
+      const bool ok = iok && p0 + pp < P;
+      cp_async16(xs + pp * kSt + kVX * xq, ok ? (const void *)(xbase + i0 + I * (int64_t)((kDT / kQX) * k)) : (const void *)X,
+                 ok);
     }
-    for (int ch = 0; ch < nchunk; ++ch) {
-      cp_async_wait<kNST - 2>();
-      __syncthreads();
-      if (ch + kNST - 1 < nchunk) issue(ch + kNST - 1);
-      cp_async_commit();
-      const int st = ch % kNST;
-      const Tin *xs = reinterpret_cast<const Tin *>(sbase + st * (kXStage + kAStage));
-      const double *as = reinterpret_cast<const double *>(sbase + st * (kXStage + kAStage) + kXStage);
+    const bool aiok = i0 + 2 * aq < I;
 #pragma unroll
-      for (int ks = 0; ks < kDKt / 4; ++ks) {
-        double af[4], bf[8];
-#pragma unroll
-        for (int jt = 0; jt < 4; ++jt) af[jt] = as[(32 * wj + 8 * jt + fr) * kSt + 4 * ks + fc];
-#pragma unroll
-        for (int pt = 0; pt < 8; ++pt) bf[pt] = (double)xs[(64 * wp + 8 * pt + fr) * kSt + 4 * ks + fc];
-#pragma unroll
-        for (int jt = 0; jt < 4; ++jt)
-#pragma unroll
-          for (int pt = 0; pt < 8; ++pt)
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                         : "+d"(acc[jt][pt][0]), "+d"(acc[jt][pt][1])
-                         : "d"(af[jt]), "d"(bf[pt]));
-      }
+    for (int k = 0; k < kUAT; ++k) {
+      const int j = ar + (kDT / (kDKt / 2)) * k;
+      const bool ok = aiok && j < J;
+      cp_async16(as + j * kSt + 2 * aq, ok ? (const void *)(abase + i0 + lda * (int64_t)((kDT / (kDKt / 2)) * k)) : (const void *)A,
+                 ok);
     }
-    cp_async_wait<0>();
-    // ---- epilogue (L == 1: the tile is one contiguous range out[p0 J ..]); columns p >= P
-    // and rows j >= J of the tile are exact zeros (zero-filled copies)
+  };
+
+#pragma unroll
+  for (int s = 0; s < kNST - 1; ++s) {
+    if (s < total) issue(s);
+    cp_async_commit();
+  }
+  double acc[4][8][2];
+  int ch = 0;
+  int64_t tk = 0;
+  for (int64_t g = 0; g < total; ++g) {
+    if (ch == 0) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b) { acc[a][b][0] = 0.0; acc[a][b][1] = 0.0; }
+    }
+    cp_async_wait<kNST - 2>();
+    __syncthreads();
+    if (g + kNST - 1 < total) issue(g + kNST - 1);
+    cp_async_commit();
+    const int st = (int)(g % kNST);
+    const Tin *xs = reinterpret_cast<const Tin *>(sbase + st * (kXStage + kAStage));
+    const double *as = reinterpret_cast<const double *>(sbase + st * (kXStage + kAStage) + kXStage);
+#pragma unroll
+    for (int ks = 0; ks < kDKt / 4; ++ks) {
+      double af[4], bf[8];
+#pragma unroll
+      for (int jt = 0; jt < 4; ++jt) af[jt] = as[(32 * wj + 8 * jt + fr) * kSt + 4 * ks + fc];
+#pragma unroll
+      for (int pt = 0; pt < 8; ++pt) bf[pt] = (double)xs[(64 * wp + 8 * pt + fr) * kSt + 4 * ks + fc];
+#pragma unroll
+      for (int jt = 0; jt < 4; ++jt)
+#pragma unroll
+        for (int pt = 0; pt < 8; ++pt)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[jt][pt][0]), "+d"(acc[jt][pt][1])
+                       : "d"(af[jt]), "d"(bf[pt]));
+    }
+    if (++ch < nchunk) continue;
+    // ---- tile done: epilogue (L == 1: the tile is one contiguous range out[p0 J ..]); columns
+    // p >= P and rows j >= J of the tile are exact zeros (zero-filled copies)
+    ch = 0;
+    const int64_t p0 = (blockIdx.x + tk * gridDim.x) * kDP;
+    ++tk;
     if (STORE || GRAM) {
-      for (int half = 0; half < 2; ++half) {
-        __syncthreads();
-        double *T = dsm;
-        if ((wp >> 1) == half) {
+#pragma unroll 1
+      for (int part = 0; part < kDP / kTP; ++part) {
+        __syncthreads();  // T free (previous pass / tile done reading it)
+        if ((64 * wp) / kTP == part) {
 #pragma unroll
           for (int jt = 0; jt < 4; ++jt)
 #pragma unroll
             for (int pt = 0; pt < 8; ++pt)
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
-                const int pp = 64 * (wp & 1) + 8 * pt + 2 * fc + h;
+                const int pp = (64 * wp) % kTP + 8 * pt + 2 * fc + h;
                 T[pp * kTS + 32 * wj + 8 * jt + fr] = acc[jt][pt][h];
               }
         }
         __syncthreads();
-        const int64_t pb = p0 + 128 * half;
-        const int64_t ncol = P - pb < 128 ? (P - pb) : 128;
+        const int64_t pb = p0 + kTP * part;
+        const int64_t ncol = P - pb < kTP ? (P - pb) : kTP;
         if (STORE && ncol > 0) {
           double *dst = out + pb * J;
           for (int e = tid; e < (int)ncol * J; e += kDT) {
@@ -947,7 +968,7 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_l1_kernel(const Tin *__restri
               const double *ta = T + fc * kTS + 8 * a + fr;
               const double *tb = T + fc * kTS + 8 * b + fr;
 #pragma unroll 8
-              for (int k0 = 0; k0 < 128; k0 += 4)
+              for (int k0 = 0; k0 < kTP; k0 += 4)
                 asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                              : "+d"(gacc[s5][0]), "+d"(gacc[s5][1])
                              : "d"(ta[k0 * kTS]), "d"(tb[k0 * kTS]));
@@ -957,6 +978,7 @@ __global__ void __launch_bounds__(kDT, 1) ttm_dmma_l1_kernel(const Tin *__restri
       }
     }
   }
+  cp_async_wait<0>();
   if (GRAM) {
     double *gp = gram_partial + (int64_t)blockIdx.x * 4096;
 #pragma unroll
@@ -989,9 +1011,7 @@ void launch_ttm_dfma(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t 
   const bool l1 = !use_dfma && v.L == 1 && (v.I % (16 / sizeof(Tin))) == 0 && (lda % 2) == 0 &&
                   (((uintptr_t)X) & 15) == 0 && (((uintptr_t)A) & 15) == 0;
   if (l1) {
-    constexpr int kSt = l1_chunk<Tin>() + 4;
-    const size_t stage = (size_t)kDP * kSt * sizeof(Tin) + 64 * kSt * 8;
-    const size_t smem = std::max(kNST * stage, sizeof(double) * 128 * kTS);
+    const size_t smem = kNST * l1_stage_bytes<Tin>() + sizeof(double) * l1_tp<Tin>() * kTS;
 #define RT_DL(ST, GR)                                                                                 \
   do {                                                                                                \
     auto k = ttm_dmma_l1_kernel<Tin, ST, GR>;                                                         \
