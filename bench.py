@@ -55,8 +55,10 @@ def peaks():
 
 
 def fp64_peak_tflops():
-    """fp64 FMA peak derived from the measured DFMA issue rate (64 DFMA/clk/SM,
-    scripts/dbg/lat_probe2.cu on this pool's B200) x SMs x 2 flop x max SM clock."""
+    """fp64 FMA peak derived from the measured fp64 rate (64 FMA/clk/SM: DFMA and the fp64
+    tensor-core mma.m8n8k4 measure the same 37 TF/s and share one datapath, mixing them does
+    not add up - scripts/dbg/lat_probe2.cu, scripts/dbg/dmma_probe.cu on this pool's B200)
+    x SMs x 2 flop x max SM clock."""
     try:
         import torch
         sms = torch.cuda.get_device_properties(0).multi_processor_count
@@ -68,7 +70,7 @@ def fp64_peak_tflops():
             mhz = float(json.load(f).get("sm_max_mhz", mhz))
     except Exception:
         pass
-    return sms * 64 * 2 * mhz * 1e6 / 1e12, f"derived: {sms} SMs x 64 DFMA/clk (measured) x 2 x {mhz:.0f} MHz"
+    return sms * 64 * 2 * mhz * 1e6 / 1e12, f"derived: {sms} SMs x 64 fp64 FMA/clk (DFMA = DMMA, measured) x 2 x {mhz:.0f} MHz"
 
 
 def load_traffic():
@@ -325,9 +327,10 @@ def main():
         t_k = bp_ms / bp_n
         flops = 2.0 * (RANKS[0] + P) * N_ELEM / world  # B = Q^T X_(1): 2 l flop per element (fp64 products)
         ach = flops / (t_k * 1e-3) / 1e12
-        kernels.append({"kernel": "ttm_dfma_kernel (mode-1 B-pass + fp64 Gram, HYBRID policy)", "bound": "alu",
+        kernels.append({"kernel": "ttm_dmma_l1_kernel (mode-1 B-pass on the fp64 tensor cores + fp64 Gram, "
+                                  "HYBRID policy)", "bound": "alu",
                         "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
-                        "traffic": traffic.get("ttm_dfma_kernel<float, 1, 1>"), "ms": t_k,
+                        "traffic": traffic.get("ttm_dmma_l1_kernel<float, 1, 1>"), "ms": t_k,
                         "algorithmic": f"{flops:.4g} fp64 flop per launch (2 l N, l = 60)",
                         "peak_source": fp64_src})
     dom = max(kernels, key=lambda k: k["ms"]) if kernels else None

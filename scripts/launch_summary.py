@@ -26,6 +26,14 @@ def main(path, steps=1):
     print(f"{'total_us':>10} {'count':>6} {'avg_us':>9} {'share':>6}  kernel")
     for k, v in sorted(agg.items(), key=lambda t: -t[1][1]):
         print(f"{v[1]:10.1f} {v[0]:6d} {v[1] / v[0]:9.1f} {100 * v[1] / tot:5.1f}%  {k}")
+    # the library's own kernels (rt::), per step: the shares to compare with bench.py's phases
+    # (torch kernels above are the benchmark's data generation / e2e copies, outside the step)
+    ours = {k: v for k, v in agg.items() if "rt::" in k}
+    tot_ours = sum(v[1] for v in ours.values())
+    print(f"\n# library kernels only, per step ({steps} steps in the capture): {tot_ours / steps:.1f} us/step")
+    print(f"{'us/step':>10} {'n/step':>6} {'avg_us':>9} {'share':>6}  kernel")
+    for k, v in sorted(ours.items(), key=lambda t: -t[1][1]):
+        print(f"{v[1] / steps:10.1f} {v[0] / steps:6.1f} {v[1] / v[0]:9.1f} {100 * v[1] / tot_ours:5.1f}%  {k}")
 
 
 if __name__ == "__main__":
