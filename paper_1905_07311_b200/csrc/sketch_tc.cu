@@ -22,6 +22,12 @@
 //   accumulation in TMEM (BASELINE "3xTF32"; the dropped Xlo*Olo term is 2^-22 relative).
 //   K-major no-swizzle operand tile (rows r, 8 K): byte (r/8)*256 + (k/4)*128 + (r%8)*16 + (k%4)*4.
 // Per-CTA partial sketches are reduced in a fixed order by the caller (deterministic).
+//
+// KM variant (L > 1: every mode but the first, e.g. R-HOSVD's modes 2..d on the input): the
+// contraction index p = l + L r has l contiguous, so X_(n) is already K-major for the MMA.
+// One 5-D TMA box per stage, dims (l%4, i%8, l/4, i/8, r), lands the tile of 8 consecutive l
+// (fixed r) x all rows i directly in the K-major core-matrix layout; the X workers only split
+// it into hi / lo planes (elementwise, no transposition).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -41,6 +47,7 @@ constexpr int kNSG = 4;              // Omega stages
 
 struct SketchTcParams {
   int64_t I, C;          // rows, unfolding columns
+  int64_t L;             // KM variant: extent of the contiguous lower index (C = L R)
   int64_t cps;           // columns per CTA (multiple of kBK)
   int NT;                // M-tiles of 128 rows
   int nbox, BR;          // TMA boxes per stage and rows per box (nbox * BR >= I, BR <= 256)
@@ -58,7 +65,7 @@ __device__ __forceinline__ int kmaj_off(int r, int k) {  // byte offset in a K-m
   return (r >> 3) * 256 + (k >> 2) * 128 + (r & 7) * 16 + (k & 3) * 4;
 }
 
-template <int N>
+template <int N, bool KM>
 __global__ void __launch_bounds__(kThreads, 1)
     sketch_tc_mn_kernel(const __grid_constant__ CUtensorMap tmap, const SketchTcParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -127,7 +134,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc::mbar_arrive_expect_tx(&full[s], bytes);
         const int c0 = (int)(cbeg + (int64_t)it * kBK);
         unsigned char *dst = sb + (size_t)s * sbytes;
-        for (int b = 0; b < p.nbox; ++b) tc::tma_load_2d(dst + b * boxb, &tmap, &full[s], p.BR * b, c0);
+        if (KM) {  // 8 consecutive l of one r (L % 8 == 0): tile already K-major
+          const int r = c0 / (int)p.L, l0 = c0 - r * (int)p.L;
+          tc::tma_load_5d(dst, &tmap, &full[s], 0, 0, l0 >> 2, 0, r);
+        } else {
+          for (int b = 0; b < p.nbox; ++b) tc::tma_load_2d(dst + b * boxb, &tmap, &full[s], p.BR * b, c0);
+        }
       }
     }
   } else if (warp == 1) {
@@ -213,9 +225,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float *st = (const float *)(sb + (size_t)ss * sbytes);
       unsigned char *hs = hb + (size_t)so * abytes, *ls = lb + (size_t)so * abytes;
       float acc = 0.f;
+      if (KM) {  // staging and operand planes share the K-major layout: elementwise split
+        const int nun = p.nbox * p.BR * kBK / 4;  // float4 units
+        for (int u = wt; u < nun; u += 32 * kWorkers) {
+          const float4 x = *(const float4 *)(st + 4 * u);
+          float4 h, l;
+          h.x = tc::tf32_hi(x.x); h.y = tc::tf32_hi(x.y); h.z = tc::tf32_hi(x.z); h.w = tc::tf32_hi(x.w);
+          l.x = tc::tf32_lo(x.x, h.x); l.y = tc::tf32_lo(x.y, h.y); l.z = tc::tf32_lo(x.z, h.z); l.w = tc::tf32_lo(x.w, h.w);
+          *(float4 *)(hs + 16 * u) = h;
+          *(float4 *)(ls + 16 * u) = l;
+          acc = fmaf(x.x, x.x, acc); acc = fmaf(x.y, x.y, acc); acc = fmaf(x.z, x.z, acc); acc = fmaf(x.w, x.w, acc);
+        }
+      }
 #pragma unroll
       for (int j = 0; j < kRJ; ++j) {
-        if (wt + 32 * kWorkers * j < rows_st) {
+        if (!KM && wt + 32 * kWorkers * j < rows_st) {
           const float *src = st + soff[j];
           float x[8];
 #pragma unroll
@@ -302,9 +326,9 @@ __global__ void reduce_partials_kernel(const double *__restrict__ partial, int n
   }
 }
 
-template <int N>
+template <int N, bool KM>
 void launch(Ctx &c, const CUtensorMap &tm, SketchTcParams &p, int grid, size_t smem) {
-  auto k = sketch_tc_mn_kernel<N>;
+  auto k = sketch_tc_mn_kernel<N, KM>;
   RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   RT_LAUNCH(c, k, grid, kThreads, smem, tm, p);
 }
@@ -318,23 +342,28 @@ bool sketch_tc_enabled() {
   return !off;
 }
 
-// Y (I x ell fp64, column-major) = X_(n) Omega(:, k0:k0+ell) for fp32 X with L == 1.
+// Y (I x ell fp64, column-major) = X_(n) Omega(:, k0:k0+ell) for fp32 X (L == 1, or L > 1 with
+// L and I multiples of 8: the K-major variant).
 // Returns false when the shape is outside this kernel's envelope (caller falls back).
 bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0, uint64_t seed,
                   int64_t col_offset, double *Y, double *normsq) {
   static const bool off = getenv("RTUCKER_NO_TC_SKETCH") != nullptr;
-  if (off || !sketch_tc_enabled() || v.L != 1 || (v.I % 4) != 0 || ell > 64 || ell < 1) return false;
+  if (off || !sketch_tc_enabled() || ell > 64 || ell < 1) return false;
+  const bool km = v.L > 1;  // K-major variant: l contiguous (5-D TMA box, no transposition)
+  if (!km && (v.I % 4) != 0) return false;
+  if (km && ((v.L % 8) != 0 || (v.I % 8) != 0 || v.I / 8 > 256)) return false;
   const int N = ell <= 32 ? 32 : 64;
   const int NT = (int)((v.I + 127) / 128);
   if (NT * N > 512 || (((uintptr_t)X) & 15) != 0) return false;
-  const int64_t C = v.R;
+  const int64_t C = v.L * v.R;
   if (C > (int64_t)INT32_MAX - 64) return false;
   SketchTcParams p{};
   p.I = v.I;
   p.C = C;
+  p.L = v.L;
   p.NT = NT;
-  p.nbox = (int)((v.I + 255) / 256);
-  p.BR = (int)(((v.I + p.nbox - 1) / p.nbox + 7) / 8 * 8);
+  p.nbox = km ? 1 : (int)((v.I + 255) / 256);
+  p.BR = km ? (int)v.I : (int)(((v.I + p.nbox - 1) / p.nbox + 7) / 8 * 8);
   const size_t sbytes = (size_t)p.nbox * p.BR * kBK * 4, abytes = (size_t)NT * 128 * kBK * 4,
                obytes = (size_t)N * kBK * 4;
   const size_t budget = 220 * 1024;
@@ -359,16 +388,33 @@ bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t
   p.norm_partial = normsq ? npart.p : nullptr;
 
   CUtensorMap tm;
-  cuuint64_t dims[2] = {(cuuint64_t)v.I, (cuuint64_t)C};
-  cuuint64_t strides[1] = {(cuuint64_t)v.I * 4};
-  cuuint32_t box[2] = {(cuuint32_t)p.BR, kBK};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)X, dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r;
+  if (!km) {
+    cuuint64_t dims[2] = {(cuuint64_t)v.I, (cuuint64_t)C};
+    cuuint64_t strides[1] = {(cuuint64_t)v.I * 4};
+    cuuint32_t box[2] = {(cuuint32_t)p.BR, kBK};
+    cuuint32_t es[2] = {1, 1};
+    r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)X, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    // (l % 4, i % 8, l / 4, i / 8, r): the box lands as K-major core matrices of 8 rows x 16 B
+    cuuint64_t dims[5] = {4, 8, (cuuint64_t)v.L / 4, (cuuint64_t)v.I / 8, (cuuint64_t)v.R};
+    cuuint64_t strides[4] = {(cuuint64_t)v.L * 4, 16, (cuuint64_t)v.L * 32, (cuuint64_t)v.L * v.I * 4};
+    cuuint32_t box[5] = {4, 8, 2, (cuuint32_t)(v.I / 8), 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, (void *)X, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   if (r != CUDA_SUCCESS) throw Error(RTUCKER_ECUDA, "cuTensorMapEncodeTiled failed for the sketch operand");
-  if (N == 32) launch<32>(c, tm, p, g, smem);
-  else launch<64>(c, tm, p, g, smem);
+  if (km) {
+    if (N == 32) launch<32, true>(c, tm, p, g, smem);
+    else launch<64, true>(c, tm, p, g, smem);
+  } else {
+    if (N == 32) launch<32, false>(c, tm, p, g, smem);
+    else launch<64, false>(c, tm, p, g, smem);
+  }
   const int64_t n = v.I * ell;
   RT_LAUNCH(c, reduce_partials_kernel, (int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, part.p, g, n, Y);
   if (normsq) sum_vec(c, npart.p, g, normsq);

@@ -141,6 +141,21 @@ def test_sketch_tc_mode1(ctx, shape, ell, k0):
     assert err <= 1e-5 and colerr <= 2e-5, (err, colerr)
 
 
+@pytest.mark.parametrize("shape,mode,ell,k0", [((80, 800, 30), 1, 60, 0), ((16, 96, 9), 1, 33, 4), ((40, 24, 200), 2, 20, 0),
+                                               ((8, 8, 8, 296), 3, 64, 0), ((24, 56, 17), 1, 17, 10)])
+def test_sketch_tc_kmajor(ctx, shape, mode, ell, k0):
+    """fp32 sketch of a mode with L > 1 (tcgen05 3xTF32, K-major 5-D TMA tiles: L % 8 == 0,
+    I % 8 == 0) against the fp64 oracle product on the same fp32 bits; same tolerance as the
+    mode-1 kernel (fp32 accumulation over a CTA's column range)."""
+    rng = np.random.default_rng(sum(shape) + ell + mode)
+    x = np.asfortranarray(rng.standard_normal(shape).astype(np.float32))
+    got = ctx.debug_sketch(x, x.shape, mode, ell, seed=7, k0=k0)
+    ref = _sketch_ref(x, mode, ell, 7, k0=k0)
+    err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    colerr = np.max(np.linalg.norm(got - ref, axis=0) / np.linalg.norm(ref, axis=0))
+    assert err <= 1e-5 and colerr <= 2e-5, (err, colerr)
+
+
 @pytest.mark.parametrize("kind,n,k", [("c4like", 60, 50), ("hilbert", 60, 5), ("rankdef", 40, 7), ("small", 10, 5),
                                       ("odd", 33, 20), ("one", 1, 1)])
 def test_gram_eig(ctx, kind, n, k):
