@@ -1,0 +1,453 @@
+// Mode-1 B-pass B = Q^T X_(1) (+ its Gram) for fp32 X under the HYBRID policy, with fp64-level
+// products from EXACT int8 tensor-core products (Ozaki-style splitting, tcgen05 kind::i8).
+//
+// Why: R16 needs B to ~1e-9 relative, which fp32/TF32 accumulation cannot give; the
+// fp64 tensor cores give it at 37 TF/s (the previous kernel, 71 % of that peak).  Here every
+// column p of X_(1) is scaled by 2^-e_p (e_p: exponent of max_i |X_ip|, computed beforehand) and
+// every column j of Q by 2^-f_j; the scaled values (|.| < 1) are cut into S = 5 signed slices
+// by rounding to nearest:  x = sum_{s=1..5} x_s 2^{1-7s} + O(2^-35),  x_s in [-64, 64]
+// (first slice of x 2^6, then 7 more bits per slice; the rounding is done with the fp32 magic
+// constant 1.5 2^23, whose sum's low byte IS the int8 slice: FMA-pipe work only, no F2I).
+// Then  B_jp = 2^{e_p + f_j} sum_{L=2..6} 2^{2-7L} acc_L,  acc_L = sum_{s+t=L} sum_i q_t[i,j] x_s[i,p],
+// each acc_L an exact int32 sum of int8 products (|acc_L| <= 5 * I * 64^2 < 2^31 for I <= 100000)
+// accumulated in TMEM; levels L >= 7 (and the slice residuals) are dropped: |error| ~
+// 2^-35 relative to the scaled magnitudes, i.e. ~1e-10 relative to |B_jp| for
+// random-sign sums (measured against fp64 products in tests/test_gpu_kernels.py).
+//
+// Layout of one CTA (persistent, one per SM; tile = 128 columns p, all I rows i):
+//   warp 0       TMA producer: per chunk (32 values of i) an X box {32 i, 128 p} (fp32) into a
+//                staging ring, and the chunk's pre-sliced Q (5 slices, K-major int8, 10 KB) by
+//                a bulk copy from the qslice buffer
+//   warp 1       TMEM owner + MMA issuer: 15 kind::i8 MMAs per chunk (M = 128 p, N = 64 j,
+//                K = 32), pair (s, t) into the level-(s+t) accumulator (5 x 64 TMEM columns)
+//   warps 2-9    slicers: X staging -> 5 int8 K-major slices (4 consecutive i per item)
+//   warps 10-13  epilogue (one per TMEM lane quadrant): levels -> fp64 B tile (scales
+//                applied) -> shared T -> coalesced store of B and the tile's Gram on the fp64
+//                tensor cores (36 upper 8 x 8 tiles, mma.m8n8k4)
+// Everything else (scales, Q slices) is computed by two small kernels below.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "kernels.h"
+#include "tc.cuh"
+
+namespace rt {
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder();  // sketch_tc.cu
+
+namespace {
+
+constexpr int kOP = 128;       // columns p per tile (MMA M)
+constexpr int kOK = 32;        // values of i per chunk (MMA K for int8)
+constexpr int kOS = 5;         // slices per operand
+constexpr int kOLv = 5;        // levels L = 2 .. 6
+constexpr int kON = 64;        // MMA N (j, ell <= 64)
+constexpr int kONSS = 3;       // staging / Q ring depth
+constexpr int kONXS = 3;       // slice buffers
+constexpr int kOSlicers = 8;   // slicer warps
+constexpr int kOEpi = 4;       // epilogue warps
+constexpr int kOThreads = 32 * (2 + kOSlicers + kOEpi);
+constexpr int kOTS = 65;       // epilogue tile stride (doubles): row-per-lane stores conflict-free
+constexpr int kXStB = kOP * kOK * 4;         // staging bytes per chunk (16 KB)
+constexpr int kQChB = kOS * kON * kOK;       // pre-sliced Q bytes per chunk (10 KB)
+constexpr int kXSlB = kOP * kOK;             // one X slice (4 KB)
+constexpr int kXsB = kOS * kXSlB;            // all slices of a chunk (20 KB)
+
+__device__ __forceinline__ int kmaj8(int r, int k) {  // byte offset, K-major int8 core matrices
+  return (r >> 3) * 256 + (k >> 4) * 128 + (r & 7) * 16 + (k & 15);
+}
+__host__ __device__ constexpr uint32_t idesc_s8(int M, int N) {  // s32 <- s8 x s8, K-major
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   tc::smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// Cut a scaled value r (|r| < 1) into 5 slices rounded to nearest (exact fp32 arithmetic):
+// u = r 2^k + 1.5 2^23 holds round(r 2^k) in its low bits (two's complement byte), t = u -
+// 1.5 2^23 is that integer as a float, r <- r 2^k - t stays exact.  Returns the raw bits of u.
+__device__ __forceinline__ void slice5(float r, uint32_t (&q)[kOS]) {
+  constexpr float M = 12582912.0f;  // 1.5 * 2^23
+#pragma unroll
+  for (int s = 0; s < kOS; ++s) {
+    const float k = s == 0 ? 64.0f : 128.0f;
+    const float u = fmaf(r, k, M);
+    const float t = u - M;
+    r = fmaf(r, k, -t);
+    q[s] = __float_as_uint(u);
+  }
+}
+
+// e_p = exponent of max_i |X(i, p)| (frexp convention: max < 2^e), one warp per column.
+__global__ void colexp_kernel(const float *__restrict__ X, int64_t I, int64_t P, int *__restrict__ e) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P;
+       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const float *col = X + I * p;
+    float m = 0.f;
+    if (((I & 3) == 0)) {
+      for (int64_t i = 4 * lane; i < I; i += 128) {
+        const float4 v = *(const float4 *)(col + i);
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+      }
+    } else {
+      for (int64_t i = lane; i < I; i += 32) m = fmaxf(m, fabsf(col[i]));
+    }
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) {
+      int ex = 0;
+      if (m > 0.f) frexpf(m, &ex);
+      e[p] = ex;
+    }
+  }
+}
+
+// Q (I x J fp64, column-major) -> per chunk c: 5 slices, each [64 j][32 i] K-major int8 (rows
+// j >= J and i >= I zero); f_j = exponent of max_i |Q(i, j)|.  One CTA per column j.
+__global__ void qslice_kernel(const double *__restrict__ Q, int64_t I, int64_t lda, int J, int nchunk,
+                              int8_t *__restrict__ qs, int *__restrict__ f) {
+  const int j = blockIdx.x;  // 0 .. 63
+  __shared__ double red[32];
+  double m = 0.0;
+  if (j < J)
+    for (int64_t i = threadIdx.x; i < I; i += blockDim.x) m = fmax(m, fabs(Q[i + lda * j]));
+  for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) red[0] = m;
+  }
+  __syncthreads();
+  int ex = 0;
+  if (red[0] > 0.0) frexp(red[0], &ex);
+  if (threadIdx.x == 0) f[j] = ex;
+  for (int64_t i = threadIdx.x; i < (int64_t)nchunk * kOK; i += blockDim.x) {
+    double r = (j < J && i < I) ? ldexp(Q[i + lda * j], -ex) : 0.0;
+    const int c = (int)(i / kOK), k = (int)(i % kOK);
+    int8_t *dst = qs + (size_t)c * kQChB;
+#pragma unroll
+    for (int s = 0; s < kOS; ++s) {  // same convention as slice5: x 2^6, then x 2^7, nearest
+      r *= (s == 0) ? 64.0 : 128.0;
+      const double t = rint(r);
+      r -= t;
+      dst[s * (kON * kOK) + kmaj8(j, k)] = (int8_t)(int)t;
+    }
+  }
+}
+
+struct OzParams {
+  int64_t I, P;
+  int J, nchunk;
+  const int8_t *qs;     // [nchunk][5][64 x 32]
+  const int *e;         // [P]
+  const int *f;         // [64]
+  double *out;          // B: (J x P) column-major, or null
+  double *gram_partial; // [grid][64 x 64] or null
+};
+
+__global__ void __launch_bounds__(kOThreads, 1)
+    bpass_ozaki_kernel(const __grid_constant__ CUtensorMap tmap, const OzParams p) {
+  extern __shared__ __align__(1024) unsigned char ozs[];
+  const uint32_t pad = (1024u - (tc::smem_u32(ozs) & 1023u)) & 1023u;
+  unsigned char *base = ozs + pad;
+  unsigned char *stg = base;                             // [kONSS][16 KB] fp32 X boxes
+  unsigned char *qb = stg + kONSS * kXStB;               // [kONSS][10 KB] Q slices
+  unsigned char *xsb = qb + kONSS * kQChB;               // [kONXS][20 KB] X slices
+  double *T = reinterpret_cast<double *>(xsb + kONXS * kXsB);  // [128][kOTS]
+  uint64_t *full = reinterpret_cast<uint64_t *>(T + kOP * kOTS);
+  uint64_t *sfree = full + kONSS, *qfree = sfree + kONSS;
+  uint64_t *xready = qfree + kONSS, *xempty = xready + kONXS;
+  uint64_t *accfull = xempty + kONXS, *accempty = accfull + 1;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(accempty + 1);
+  int *fsh = reinterpret_cast<int *>(tslot + 2);        // [64] Q exponents
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t ntiles = (p.P + kOP - 1) / kOP;
+  const int64_t mytiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int nchunk = p.nchunk;
+  const int64_t total = mytiles * nchunk;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kONSS; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&sfree[s], 32 * kOSlicers);
+      tc::mbar_init(&qfree[s], 1);
+    }
+    for (int s = 0; s < kONXS; ++s) {
+      tc::mbar_init(&xready[s], 32 * kOSlicers);
+      tc::mbar_init(&xempty[s], 1);
+    }
+    tc::mbar_init(accfull, 1);
+    tc::mbar_init(accempty, 32 * kOEpi);
+    tc::fence_barrier_init();
+  }
+  for (int j = threadIdx.x; j < kON; j += kOThreads) fsh[j] = p.f[j];
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      tc::tma_prefetch_desc(&tmap);
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t g = 0; g < total; ++g) {
+        const int64_t tk = g / nchunk;
+        const int ch = (int)(g - tk * nchunk);
+        const int64_t p0 = (blockIdx.x + tk * gridDim.x) * kOP;
+        if (g >= kONSS) {
+          tc::mbar_wait(&sfree[s], ph ^ 1);
+          tc::mbar_wait(&qfree[s], ph ^ 1);
+        }
+        tc::mbar_arrive_expect_tx(&full[s], kXStB + kQChB);
+        tc::tma_load_2d(stg + s * kXStB, &tmap, &full[s], ch * kOK, (int)p0);
+        bulk_g2s(qb + s * kQChB, p.qs + (size_t)ch * kQChB, kQChB, &full[s]);
+        if (++s == kONSS) { s = 0; ph ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_s8(kOP, kON);
+      int s = 0, x = 0;
+      uint32_t ph = 0, phx = 0;
+      int ch = 0;
+      int64_t tt = 0;
+      for (int64_t g = 0; g < total; ++g) {
+        if (ch == 0 && tt > 0) tc::mbar_wait(accempty, (uint32_t)((tt - 1) & 1));  // TMEM drained
+        tc::mbar_wait(&full[s], ph);
+        tc::mbar_wait(&xready[x], phx);
+        tc::tc_fence_after();
+        const uint32_t xa = tc::smem_u32(xsb + x * kXsB), qa = tc::smem_u32(qb + s * kQChB);
+#pragma unroll
+        for (int sx = 0; sx < kOS; ++sx)
+#pragma unroll
+          for (int sq = 0; sq < kOS; ++sq) {
+            const int L = sx + sq;  // level - 2 (slices are 1-based in the derivation)
+            if (L >= kOLv) continue;
+            const uint64_t ad = tc::smem_desc(xa + sx * kXSlB, 128, 256, tc::kSwNone);
+            const uint64_t bd = tc::smem_desc(qa + sq * (kON * kOK), 128, 256, tc::kSwNone);
+            // first product of a level in a tile overwrites the accumulator
+            const bool first = (ch == 0) && (sx == 0 || sq == L);
+            mma_i8(tmem + L * kON, ad, bd, idesc, first ? 0u : 1u);
+          }
+        tc::mma_commit(&xempty[x]);
+        tc::mma_commit(&qfree[s]);
+        if (++ch == nchunk) {
+          ch = 0;
+          tc::mma_commit(accfull);
+          ++tt;
+        }
+        if (++s == kONSS) { s = 0; ph ^= 1; }
+        if (++x == kONXS) { x = 0; phx ^= 1; }
+      }
+    }
+  } else if (warp < 2 + kOSlicers) {
+    // ------------------------------------------------------------------- slicers
+    const int wt = threadIdx.x - 64;  // 0 .. 255
+    int s = 0, x = 0;
+    uint32_t ph = 0, phx = 0;
+    int ch = 0;
+    int64_t tk = 0;
+    float sc[4];  // 2^-e_p of this thread's 4 columns (items wt + 256 k: column (wt >> 3) + 32 k)
+    for (int64_t g = 0; g < total; ++g) {
+      if (ch == 0) {
+        const int64_t p0 = (blockIdx.x + tk * gridDim.x) * kOP;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int64_t pp = p0 + (wt >> 3) + 32 * k;
+          sc[k] = pp < p.P ? ldexpf(1.0f, -p.e[pp]) : 0.f;
+        }
+      }
+      tc::mbar_wait(&full[s], ph);
+      if (g >= kONXS) tc::mbar_wait(&xempty[x], phx ^ 1);
+      const float *st = reinterpret_cast<const float *>(stg + s * kXStB);  // [128 p][32 i]
+      unsigned char *xs = xsb + x * kXsB;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int item = wt + 256 * k, pr = item >> 3, i4 = item & 7;
+        const float4 v = *reinterpret_cast<const float4 *>(st + pr * kOK + 4 * i4);
+        uint32_t a[kOS], b[kOS], c[kOS], d[kOS];
+        slice5(v.x * sc[k], a);
+        slice5(v.y * sc[k], b);
+        slice5(v.z * sc[k], c);
+        slice5(v.w * sc[k], d);
+        const int off = kmaj8(pr, 4 * i4);
+#pragma unroll
+        for (int q = 0; q < kOS; ++q) {  // low bytes of a, b, c, d -> one word
+          const uint32_t w = __byte_perm(__byte_perm(a[q], b[q], 0x0040), __byte_perm(c[q], d[q], 0x0040), 0x5410);
+          *reinterpret_cast<uint32_t *>(xs + q * kXSlB + off) = w;
+        }
+      }
+      tc::mbar_arrive(&sfree[s]);
+      tc::fence_proxy_async_smem();
+      tc::mbar_arrive(&xready[x]);
+      if (++ch == nchunk) { ch = 0; ++tk; }
+      if (++s == kONSS) { s = 0; ph ^= 1; }
+      if (++x == kONXS) { x = 0; phx ^= 1; }
+    }
+  } else {
+    // ------------------------------------------------------------------- epilogue
+    const int q4 = warp & 3;            // TMEM lane quadrant
+    const int et = threadIdx.x - 32 * (2 + kOSlicers);  // 0 .. 127
+    const int row = 32 * q4 + lane;     // tile row (column p)
+    double gacc[9][2];
+#pragma unroll
+    for (int u = 0; u < 9; ++u) gacc[u][0] = gacc[u][1] = 0.0;
+    const int ew = warp - (2 + kOSlicers);  // 0 .. 3
+    for (int64_t tt = 0; tt < mytiles; ++tt) {
+      const int64_t p0 = (blockIdx.x + tt * gridDim.x) * kOP;
+      tc::mbar_wait(accfull, (uint32_t)(tt & 1));
+      tc::tc_fence_after();
+      const int64_t pp = p0 + row;
+      const int ep = pp < p.P ? p.e[pp] : 0;
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {  // two halves of 32 columns: 5 levels each, smallest first
+        double bv[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) bv[j] = 0.0;
+#pragma unroll
+        for (int L = kOLv - 1; L >= 0; --L) {
+          uint32_t r[32];
+          tc::tmem_ld32(tmem + ((uint32_t)(32 * q4) << 16) + L * kON + 32 * h, r);
+          const double w = ldexp(1.0, 2 - 7 * (L + 2));
+#pragma unroll
+          for (int j = 0; j < 32; ++j) bv[j] = fma((double)(int)r[j], w, bv[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int jj = 32 * h + j;
+          T[row * kOTS + jj] = (pp < p.P && jj < p.J) ? ldexp(bv[j], ep + fsh[jj]) : 0.0;
+        }
+      }
+      tc::tc_fence_before();
+      tc::mbar_arrive(accempty);  // the MMA warp may overwrite the accumulators
+      named_bar(1, 32 * kOEpi);
+      const int64_t ncol = p.P - p0 < kOP ? p.P - p0 : kOP;
+      if (p.out && ncol > 0) {  // B tile (J x ncol) is one contiguous range out[p0 J ..]
+        double *dst = p.out + p0 * p.J;
+        for (int e = et; e < (int)ncol * p.J; e += 32 * kOEpi) {
+          const int pr = e / p.J, j = e - pr * p.J;
+          dst[e] = T[pr * kOTS + j];
+        }
+      }
+      if (p.gram_partial) {  // G += T^T T, 36 upper 8x8 tiles over the 4 epilogue warps
+        const int fr = lane >> 2, fc = lane & 3;
+#pragma unroll
+        for (int u = 0; u < 9; ++u) {
+          const int t = ew + 4 * u;
+          int a = 0, rem = t;
+          while (rem >= 8 - a) { rem -= 8 - a; ++a; }
+          const int b = a + rem;
+          const double *ta = T + fc * kOTS + 8 * a + fr;
+          const double *tb = T + fc * kOTS + 8 * b + fr;
+#pragma unroll 8
+          for (int k0 = 0; k0 < kOP; k0 += 4)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                         : "+d"(gacc[u][0]), "+d"(gacc[u][1])
+                         : "d"(ta[k0 * kOTS]), "d"(tb[k0 * kOTS]));
+        }
+      }
+      named_bar(1, 32 * kOEpi);  // T free for the next tile
+    }
+    if (p.gram_partial) {
+      const int fr = lane >> 2, fc = lane & 3;
+      double *gp = p.gram_partial + (int64_t)blockIdx.x * 4096;
+#pragma unroll
+      for (int u = 0; u < 9; ++u) {
+        const int t = ew + 4 * u;
+        int a = 0, rem = t;
+        while (rem >= 8 - a) { rem -= 8 - a; ++a; }
+        const int b = a + rem;
+        const int gi = 8 * a + fr, gj = 8 * b + 2 * fc;
+        gp[gi * 64 + gj] = gacc[u][0];
+        gp[gi * 64 + gj + 1] = gacc[u][1];
+        if (a != b) {
+          gp[gj * 64 + gi] = gacc[u][0];
+          gp[(gj + 1) * 64 + gi] = gacc[u][1];
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+}
+
+__global__ void oz_gram_reduce_kernel(const double *__restrict__ part, int nblk, int J, double *__restrict__ gram) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= J * J) return;
+  const int i = e % J, j = e / J;
+  double s = 0.0;
+  for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * 4096 + i * 64 + j];
+  gram[i + (int64_t)J * j] = s;
+}
+
+}  // namespace
+
+bool ozaki_bpass_enabled() {
+  static const bool off = getenv("RTUCKER_NO_OZAKI") != nullptr;
+  return !off;
+}
+
+// B = A^T X_(1) (J x P fp64, column-major) and/or its Gram for fp32 X with L == 1.
+// Returns false outside the kernel's envelope (caller falls back to the fp64 tensor cores).
+bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda, int J, double *out, double *gram) {
+  if (!ozaki_bpass_enabled() || v.L != 1 || J < 1 || J > kON || (v.I % 4) != 0 || v.I > 26000 ||
+      (((uintptr_t)X) & 15) != 0 || v.R > (int64_t)INT32_MAX - kOP)
+    return false;
+  const int64_t I = v.I, P = v.R;
+  const int nchunk = (int)((I + kOK - 1) / kOK);
+  DevBuf<int8_t> qs(c, (size_t)nchunk * kQChB);
+  DevBuf<int> fexp(c, kON), eexp(c, (size_t)P);
+  RT_LAUNCH(c, qslice_kernel, kON, 256, 0, A, I, lda, J, nchunk, qs.p, fexp.p);
+  RT_LAUNCH(c, colexp_kernel, std::max(1, std::min(c.num_sms * 16, (int)((P + 7) / 8))), 256, 0, X, I, P, eexp.p);
+  const int64_t ntiles = (P + kOP - 1) / kOP;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, c.num_sms));
+  DevBuf<double> part;
+  if (gram) part.alloc(c, (size_t)grid * 4096);
+  OzParams prm{};
+  prm.I = I;
+  prm.P = P;
+  prm.J = J;
+  prm.nchunk = nchunk;
+  prm.qs = qs.p;
+  prm.e = eexp.p;
+  prm.f = fexp.p;
+  prm.out = out;
+  prm.gram_partial = gram ? part.p : nullptr;
+  CUtensorMap tm;
+  cuuint64_t dims[2] = {(cuuint64_t)I, (cuuint64_t)P};
+  cuuint64_t strides[1] = {(cuuint64_t)I * 4};
+  cuuint32_t box[2] = {kOK, kOP};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = tensor_map_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)X, dims, strides, box, es,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(RTUCKER_ECUDA, "cuTensorMapEncodeTiled failed for the Ozaki B-pass");
+  const size_t smem = 1024 + (size_t)kONSS * (kXStB + kQChB) + (size_t)kONXS * kXsB + sizeof(double) * kOP * kOTS +
+                      8 * (3 * kONSS + 2 * kONXS + 2) + 16 + 4 * kON;
+  RT_CUDA(cudaFuncSetAttribute(bpass_ozaki_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  RT_LAUNCH(c, bpass_ozaki_kernel, grid, kOThreads, smem, tm, prm);
+  if (gram) RT_LAUNCH(c, oz_gram_reduce_kernel, (J * J + 127) / 128, 128, 0, part.p, grid, J, gram);
+  return true;
+}
+
+}  // namespace rt

@@ -47,6 +47,9 @@ void philox_raw(Ctx &c, const uint32_t *ctr, int64_t n, uint32_t k0, uint32_t k1
 // out = X x_n A^T with A (I x J, fp64 col-major, leading dim lda): out(l, j, r) = sum_i A[i,j] X(l,i,r).
 // out may be null (Gram-only pass).  gram (optional, J x J fp64) <- B_(n) B_(n)^T of the
 // (stored-precision) output.
+// Ozaki-style mode-1 B-pass on the int8 tensor cores (bpass_ozaki.cu); false if not applicable.
+bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda, int J, double *out, double *gram);
+bool ozaki_bpass_enabled();
 void ttm_dense(Ctx &c, const void *X, DT in, ModeView v, const double *A, int64_t lda, int J,
                void *out, DT outT, bool mul_f64, double *gram);
 

@@ -156,6 +156,32 @@ def test_sketch_tc_kmajor(ctx, shape, mode, ell, k0):
     assert err <= 1e-5 and colerr <= 2e-5, (err, colerr)
 
 
+@pytest.mark.parametrize("shape,J,graded", [((800, 300, 5), 60, False), ((96, 1001, 3), 17, True), ((64, 50, 7), 64, True),
+                                          ((800, 129, 1), 60, False), ((4, 300, 2), 1, False)])
+def test_ozaki_bpass(ctx, shape, J, graded):
+    """Mode-1 HYBRID B-pass on the int8 tensor cores (Ozaki-style exact slice products, DESIGN
+    R18) against the fp64 product on the same fp32 bits: B and its Gram to 2e-9 relative
+    (slices keep 35 bits of every column-scaled operand).  `graded` scales the columns of X
+    over 12 decades and zeroes one, exercising the per-column exponents."""
+    rng = np.random.default_rng(sum(shape) + J)
+    x = rng.standard_normal(shape)
+    if graded:
+        x *= np.logspace(0, -12, shape[1])[None, :, None]
+        x[:, 1, 0] = 0.0
+    x = np.asfortranarray(x.astype(np.float32))
+    q, _ = np.linalg.qr(rng.standard_normal((shape[0], J)))
+    b, g = ctx.debug_ttm(x, x.shape, 0, q)
+    x1 = O.unfold(np.asarray(x, dtype=np.float64), 0)
+    bref = q.T @ x1
+    bgot = b.cpu().numpy().reshape((J, -1), order="F")
+    assert np.linalg.norm(bgot - bref) <= 2e-9 * np.linalg.norm(bref)
+    # per column, against the column's natural scale ||q_j|| ||x_p|| (the slices are scaled per column)
+    scale = np.linalg.norm(q, axis=0)[:, None] * np.linalg.norm(x1, axis=0)[None, :]
+    assert np.all(np.abs(bgot - bref) <= 2e-9 * scale + 1e-300)
+    gref = bref @ bref.T
+    assert np.linalg.norm(g - gref) <= 2e-9 * np.linalg.norm(gref)
+
+
 @pytest.mark.parametrize("kind,n,k", [("c4like", 60, 50), ("hilbert", 60, 5), ("rankdef", 40, 7), ("small", 10, 5),
                                       ("odd", 33, 20), ("one", 1, 1)])
 def test_gram_eig(ctx, kind, n, k):
