@@ -87,8 +87,9 @@ __device__ __forceinline__ void slice5(float r, uint32_t (&q)[kOS]) {
   }
 }
 
-// e_p = exponent of max_i |X(i, p)| (frexp convention: max < 2^e), one warp per column.
-__global__ void colexp_kernel(const float *__restrict__ X, int64_t I, int64_t P, int *__restrict__ e) {
+// m_p = max_i |X(i, p)| as fp32 bits (the scale exponent is taken from it), one warp per column.
+// The R-STHOSVD path gets these from the mode-1 sketch instead (sketch_tc.cu, colmax).
+__global__ void colmax_kernel(const float *__restrict__ X, int64_t I, int64_t P, uint32_t *__restrict__ cm) {
   const int lane = threadIdx.x & 31;
   for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < P;
        p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
@@ -102,13 +103,16 @@ __global__ void colexp_kernel(const float *__restrict__ X, int64_t I, int64_t P,
     } else {
       for (int64_t i = lane; i < I; i += 32) m = fmaxf(m, fabsf(col[i]));
     }
-    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) {
-      int ex = 0;
-      if (m > 0.f) frexpf(m, &ex);
-      e[p] = ex;
-    }
+    const uint32_t r = __reduce_max_sync(0xffffffffu, __float_as_uint(m));
+    if (lane == 0) cm[p] = r;
   }
+}
+// exponent e with m < 2^e (frexp convention), 0 for m == 0
+__device__ __forceinline__ int exp_of(uint32_t mbits) {
+  if (mbits == 0) return 0;
+  int e;
+  frexpf(__uint_as_float(mbits), &e);
+  return e;
 }
 
 // Q (I x J fp64, column-major) -> per chunk c: 5 slices, each [64 j][32 i] K-major int8 (rows
@@ -150,7 +154,7 @@ struct OzParams {
   int64_t I, P;
   int J, nchunk;
   const int8_t *qs;     // [nchunk][5][64 x 32]
-  const int *e;         // [P]
+  const uint32_t *cm;   // [P] fp32 bits of the column maxima of X
   const int *f;         // [64]
   double *out;          // B: (J x P) column-major, or null
   double *gram_partial; // [grid][64 x 64] or null
@@ -270,7 +274,7 @@ __global__ void __launch_bounds__(kOThreads, 1)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int64_t pp = p0 + (wt >> 3) + 32 * k;
-          sc[k] = pp < p.P ? ldexpf(1.0f, -p.e[pp]) : 0.f;
+          sc[k] = pp < p.P ? ldexpf(1.0f, -exp_of(p.cm[pp])) : 0.f;
         }
       }
       tc::mbar_wait(&full[s], ph);
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(kOThreads, 1)
       tc::mbar_wait(accfull, (uint32_t)(tt & 1));
       tc::tc_fence_after();
       const int64_t pp = p0 + row;
-      const int ep = pp < p.P ? p.e[pp] : 0;
+      const int ep = pp < p.P ? exp_of(p.cm[pp]) : 0;
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {  // two halves of 32 columns: 5 levels each, smallest first
         double bv[32];
@@ -409,16 +413,22 @@ bool ozaki_bpass_enabled() {
 
 // B = A^T X_(1) (J x P fp64, column-major) and/or its Gram for fp32 X with L == 1.
 // Returns false outside the kernel's envelope (caller falls back to the fp64 tensor cores).
-bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda, int J, double *out, double *gram) {
+bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda, int J, double *out, double *gram,
+               const uint32_t *colmax) {
   if (!ozaki_bpass_enabled() || v.L != 1 || J < 1 || J > kON || (v.I % 4) != 0 || v.I > 26000 ||
       (((uintptr_t)X) & 15) != 0 || v.R > (int64_t)INT32_MAX - kOP)
     return false;
   const int64_t I = v.I, P = v.R;
   const int nchunk = (int)((I + kOK - 1) / kOK);
   DevBuf<int8_t> qs(c, (size_t)nchunk * kQChB);
-  DevBuf<int> fexp(c, kON), eexp(c, (size_t)P);
+  DevBuf<int> fexp(c, kON);
+  DevBuf<uint32_t> cmown;
   RT_LAUNCH(c, qslice_kernel, kON, 256, 0, A, I, lda, J, nchunk, qs.p, fexp.p);
-  RT_LAUNCH(c, colexp_kernel, std::max(1, std::min(c.num_sms * 16, (int)((P + 7) / 8))), 256, 0, X, I, P, eexp.p);
+  if (!colmax) {
+    cmown.alloc(c, (size_t)P);
+    RT_LAUNCH(c, colmax_kernel, std::max(1, std::min(c.num_sms * 16, (int)((P + 7) / 8))), 256, 0, X, I, P, cmown.p);
+    colmax = cmown.p;
+  }
   const int64_t ntiles = (P + kOP - 1) / kOP;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, c.num_sms));
   DevBuf<double> part;
@@ -429,7 +439,7 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
   prm.J = J;
   prm.nchunk = nchunk;
   prm.qs = qs.p;
-  prm.e = eexp.p;
+  prm.cm = colmax;
   prm.f = fexp.p;
   prm.out = out;
   prm.gram_partial = gram ? part.p : nullptr;

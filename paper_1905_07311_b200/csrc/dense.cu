@@ -137,11 +137,18 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
 
     // ---- line 2 of Alg 3 / line 1 of Alg 1: Y = G_(n) Omega_n   (+ ||G||^2)
     DevBuf<double> Y(c, (size_t)Ig * ell + 1);
+    // fp32 input, HYBRID, L == 1: the sketch also records the column maxima that scale the
+    // Ozaki B-pass of the same pass over X (bpass_ozaki.cu)
+    DevBuf<uint32_t> colmax;
+    if (gt == DT::F32 && !pol.mul_f64 && v.L == 1 && !last_sharded && ozaki_bpass_enabled()) {
+      colmax.alloc(c, (size_t)v.R);
+      colmax.zero();
+    }
     {
       PhaseScope ps(c, PH_SKETCH, jj);
       if (!last_sharded) {
         sketch_dense(c, G, gt, v, n, ell, 0, seed, col_offset_for(in, cur, n), pol.mul_f64, Y.p, Y.p + Ig * ell,
-                     in.dt == DT::F32 && !pol.mul_f64);
+                     in.dt == DT::F32 && !pol.mul_f64, colmax.p);
         allreduce_sum_f64(c, Y.p, (size_t)Ig * ell + 1);
         RT_CUDA(cudaMemcpyAsync(scal.p + 2 * n, Y.p + Ig * ell, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
       } else {
@@ -161,7 +168,7 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
     DevBuf<double> gram(c, (size_t)ell * ell);
     PhaseScope ps_b(c, PH_BPASS, jj);
     if (!last_sharded) {
-      ttm_dense(c, G, gt, v, Q.p, Ig, ell, B.p, pol.store, pol.mul_f64, gram.p);
+      ttm_dense(c, G, gt, v, Q.p, Ig, ell, B.p, pol.store, pol.mul_f64, gram.p, colmax.p);
       allreduce_sum_f64(c, gram.p, (size_t)ell * ell);
     } else {
       ttm_dense(c, G, gt, v, Q.p + in.offset, Ig, ell, B.p, pol.store, pol.mul_f64, nullptr);
@@ -236,10 +243,15 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
     const bool last_sharded = in.sharded && n == d - 1;
     const int64_t Ig = in.gdims[n];
     DevBuf<double> Y(c, (size_t)Ig * ell + 1);
+    DevBuf<uint32_t> colmax;  // column maxima for the Ozaki B-pass (mode 1, fp32, HYBRID)
+    if (in.dt == DT::F32 && !pol.mul_f64 && v.L == 1 && !last_sharded && ozaki_bpass_enabled()) {
+      colmax.alloc(c, (size_t)v.R);
+      colmax.zero();
+    }
     PhaseScope ps(c, PH_SKETCH, n);
     if (!last_sharded) {
       sketch_dense(c, in.ptr, in.dt, v, n, ell, 0, seed, col_offset_for(in, in.ldims, n), pol.mul_f64, Y.p,
-                   Y.p + Ig * ell, in.dt == DT::F32 && !pol.mul_f64);
+                   Y.p + Ig * ell, in.dt == DT::F32 && !pol.mul_f64, colmax.p);
       allreduce_sum_f64(c, Y.p, (size_t)Ig * ell + 1);
       RT_CUDA(cudaMemcpyAsync(scal.p + 2 * n, Y.p + Ig * ell, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
     } else {
@@ -254,9 +266,9 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
     if (!last_sharded) {
       if (n == 0 && keep_b1) {
         B1.alloc(c, (size_t)v.L * ell * v.R * dt_size(pol.store));
-        ttm_dense(c, in.ptr, in.dt, v, Q.p, Ig, ell, B1.p, pol.store, pol.mul_f64, gram.p);
+        ttm_dense(c, in.ptr, in.dt, v, Q.p, Ig, ell, B1.p, pol.store, pol.mul_f64, gram.p, colmax.p);
       } else {
-        ttm_dense(c, in.ptr, in.dt, v, Q.p, Ig, ell, nullptr, pol.store, pol.mul_f64, gram.p);  // Gram only
+        ttm_dense(c, in.ptr, in.dt, v, Q.p, Ig, ell, nullptr, pol.store, pol.mul_f64, gram.p, colmax.p);  // Gram only
       }
       allreduce_sum_f64(c, gram.p, (size_t)ell * ell);
     } else {

@@ -26,14 +26,16 @@ inline ModeView mode_view(const int64_t *dims, int d, int n) {
 // Normals (reading R3): products in fp32 (FAST) draw fp32 normals; products in fp64 draw fp64
 // normals unless normals_f32 (fp32 input under the HYBRID policy, whose later passes run in
 // fp64 on fp64 intermediates but keep the fp32 data's Omega).
+// colmax (optional, mode-1 fp32 tcgen05 path only): gets max_i |X(i, c)| (fp32 bits, atomic
+// max into a zeroed buffer) for every unfolding column c - the Ozaki B-pass's column scales.
 void sketch_dense(Ctx &c, const void *X, DT in, ModeView v, int mode, int ell, int64_t k0,
                   uint64_t seed, int64_t col_offset, bool mul_f64, double *Y, double *normsq,
-                  bool normals_f32 = false);
+                  bool normals_f32 = false, uint32_t *colmax = nullptr);
 
 // sketch_tc.cu: tcgen05 3xTF32 variant for fp32 data with L == 1 (MN-major rows); returns
 // false when the shape is outside its envelope.
 bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0, uint64_t seed,
-                  int64_t col_offset, double *Y, double *normsq);
+                  int64_t col_offset, double *Y, double *normsq, uint32_t *colmax = nullptr);
 bool sketch_tc_enabled();
 // bpass_tc.cu: B = Q^T X_(n) (B[k + ell c]) for fp32 X with L == 1 on tcgen05 (3xTF32).
 bool bpass_tc_mn(Ctx &c, const float *X, ModeView v, const double *Q, int64_t ldq, int ell, void *B, bool out_f64);
@@ -48,10 +50,12 @@ void philox_raw(Ctx &c, const uint32_t *ctr, int64_t n, uint32_t k0, uint32_t k1
 // out may be null (Gram-only pass).  gram (optional, J x J fp64) <- B_(n) B_(n)^T of the
 // (stored-precision) output.
 // Ozaki-style mode-1 B-pass on the int8 tensor cores (bpass_ozaki.cu); false if not applicable.
-bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda, int J, double *out, double *gram);
+// colmax: column maxima from the mode-1 sketch (sketch_dense), or null (computed here).
+bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda, int J, double *out, double *gram,
+               const uint32_t *colmax = nullptr);
 bool ozaki_bpass_enabled();
 void ttm_dense(Ctx &c, const void *X, DT in, ModeView v, const double *A, int64_t lda, int J,
-               void *out, DT outT, bool mul_f64, double *gram);
+               void *out, DT outT, bool mul_f64, double *gram, const uint32_t *colmax = nullptr);
 
 // Gram of the mode-n unfolding of B (mode size v.I): gram (v.I x v.I, fp64).
 void mode_gram(Ctx &c, const void *B, DT t, ModeView v, double *gram);

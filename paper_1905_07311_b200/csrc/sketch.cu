@@ -345,14 +345,14 @@ void launch_sketch_dfma(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int
 
 template <typename Tin, typename Tmul>
 void sketch_dispatch(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int64_t k0,
-                     uint64_t seed, int64_t col_offset, double *Y, double *normsq) {
+                     uint64_t seed, int64_t col_offset, double *Y, double *normsq, uint32_t *colmax = nullptr) {
   // Column blocks of <= 64 sketch columns; the norm is fused into the first block only.
   for (int kb = 0; kb < ell; kb += 64) {
     const int e = std::min(64, ell - kb);
     double *Yb = Y + (int64_t)kb * v.I;
     double *ns = kb == 0 ? normsq : nullptr;
     if constexpr (std::is_same<Tin, float>::value && std::is_same<Tmul, float>::value) {
-      if (sketch_tc_mn(c, X, v, mode, e, k0 + kb, seed, col_offset, Yb, ns)) continue;
+      if (sketch_tc_mn(c, X, v, mode, e, k0 + kb, seed, col_offset, Yb, ns, kb == 0 ? colmax : nullptr)) continue;
     }
     if (e <= 16)
       launch_sketch<Tin, Tmul, 16>(c, X, v, mode, e, k0 + kb, seed, col_offset, Yb, ns);
@@ -366,7 +366,8 @@ void sketch_dispatch(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int64_
 }  // namespace
 
 void sketch_dense(Ctx &c, const void *X, DT in, ModeView v, int mode, int ell, int64_t k0,
-                  uint64_t seed, int64_t col_offset, bool mul_f64, double *Y, double *normsq, bool normals_f32) {
+                  uint64_t seed, int64_t col_offset, bool mul_f64, double *Y, double *normsq, bool normals_f32,
+                  uint32_t *colmax) {
   if (in == DT::F64 || mul_f64) {
     // fp64 products: DFMA kernel in column blocks of <= 64 (norm fused into the first block)
     for (int kb = 0; kb < ell; kb += 64) {
@@ -383,7 +384,7 @@ void sketch_dense(Ctx &c, const void *X, DT in, ModeView v, int mode, int ell, i
     }
     return;
   }
-  sketch_dispatch<float, float>(c, (const float *)X, v, mode, ell, k0, seed, col_offset, Y, normsq);
+  sketch_dispatch<float, float>(c, (const float *)X, v, mode, ell, k0, seed, col_offset, Y, normsq, colmax);
 }
 
 void omega_rows(Ctx &c, DT out, uint64_t seed, int mode, const int64_t *cols, int64_t n, int ell,

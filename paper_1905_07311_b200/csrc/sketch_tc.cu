@@ -59,6 +59,7 @@ struct SketchTcParams {
   int64_t col_offset;    // global unfolding-column offset of this shard
   double *partial;       // [grid][ell][I]
   double *norm_partial;  // [grid] or null
+  uint32_t *colmax;      // [C] fp32 bits of max_i |X(i, c)| (atomic max), or null (L == 1 only)
 };
 
 __device__ __forceinline__ int kmaj_off(int r, int k) {  // byte offset in a K-major tile
@@ -237,6 +238,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           acc = fmaf(x.x, x.x, acc); acc = fmaf(x.y, x.y, acc); acc = fmaf(x.z, x.z, acc); acc = fmaf(x.w, x.w, acc);
         }
       }
+      float cm[8];  // this thread's column maxima of the stage (L == 1: 8 columns c0 .. c0+7)
+#pragma unroll
+      for (int u = 0; u < 8; ++u) cm[u] = 0.f;
 #pragma unroll
       for (int j = 0; j < kRJ; ++j) {
         if (!KM && wt + 32 * kWorkers * j < rows_st) {
@@ -255,7 +259,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             *(float4 *)(ls + ooff[j] + cq * 128) = l;
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) acc = fmaf(x[u], x[u], acc);
+          for (int u = 0; u < 8; ++u) {
+            acc = fmaf(x[u], x[u], acc);
+            cm[u] = fmaxf(cm[u], fabsf(x[u]));
+          }
+        }
+      }
+      if (!KM && p.colmax) {  // warp max per column, one atomic per warp and column
+        const int64_t c0 = cbeg + (int64_t)it * kBK;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const uint32_t m = __reduce_max_sync(0xffffffffu, __float_as_uint(cm[u]));
+          if (lane == 0 && c0 + u < cend) atomicMax(p.colmax + c0 + u, m);
         }
       }
       nsq += (double)acc;
@@ -346,7 +361,7 @@ bool sketch_tc_enabled() {
 // L and I multiples of 8: the K-major variant).
 // Returns false when the shape is outside this kernel's envelope (caller falls back).
 bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0, uint64_t seed,
-                  int64_t col_offset, double *Y, double *normsq) {
+                  int64_t col_offset, double *Y, double *normsq, uint32_t *colmax) {
   static const bool off = getenv("RTUCKER_NO_TC_SKETCH") != nullptr;
   if (off || !sketch_tc_enabled() || ell > 64 || ell < 1) return false;
   const bool km = v.L > 1;  // K-major variant: l contiguous (5-D TMA box, no transposition)
@@ -386,6 +401,7 @@ bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t
   if (normsq) npart.alloc(c, g);
   p.partial = part.p;
   p.norm_partial = normsq ? npart.p : nullptr;
+  p.colmax = km ? nullptr : colmax;
 
   CUtensorMap tm;
   CUresult r;

@@ -1092,12 +1092,12 @@ bool ttm_dense_tc(Ctx &c, const void *X, DT in, ModeView v, const double *A, int
                   bool mul_f64, double *gram);
 
 void ttm_dense(Ctx &c, const void *X, DT in, ModeView v, const double *A, int64_t lda, int J,
-               void *out, DT outT, bool mul_f64, double *gram) {
+               void *out, DT outT, bool mul_f64, double *gram, const uint32_t *colmax) {
   RT_REQUIRE(out || gram, "ttm: nothing to compute");
   if (ttm_dense_tc(c, X, in, v, A, lda, J, out, outT, mul_f64, gram)) return;
   // HYBRID mode-1 B-pass on fp32 data: fp64-level products from exact int8 tensor-core slices
   if (in == DT::F32 && !mul_f64 && (!out || outT == DT::F64) &&
-      ttm_ozaki(c, (const float *)X, v, A, lda, J, (double *)out, gram))
+      ttm_ozaki(c, (const float *)X, v, A, lda, J, (double *)out, gram, colmax))
     return;
   // fp64 output (HYBRID / FP64 policies, fp64 data): DFMA kernel
   if (J <= 64 && (!out || outT == DT::F64) && (in == DT::F64 || mul_f64 || outT == DT::F64)) {
