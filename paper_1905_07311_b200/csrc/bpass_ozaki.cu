@@ -18,9 +18,13 @@
 //   warp 0       TMA producer: per chunk (32 values of i) an X box {32 i, 128 p} (fp32) into a
 //                staging ring, and the chunk's pre-sliced Q (5 slices, K-major int8, 10 KB) by
 //                a bulk copy from the qslice buffer
-//   warp 1       TMEM owner + MMA issuer: 15 kind::i8 MMAs per chunk (M = 128 p, N = 64 j,
-//                K = 32), pair (s, t) into the level-(s+t) accumulator (5 x 64 TMEM columns)
-//   warps 2-9    slicers: X staging -> 5 int8 K-major slices (4 consecutive i per item)
+//   warp 1       TMEM owner + MMA issuer: the 15 slice pairs of a chunk in 10 kind::i8 MMAs
+//                (M = 128 p, N = 128 j x 2 levels or 64, K = 32, A from TMEM, B from shared
+//                memory), pair (s, t) into the level-(s+t) accumulator (5 x 64 TMEM columns)
+//   warps 2-9    slicers: thread = one column p of the tile (its TMEM lane) and 16 values of i;
+//                X staging (128B-swizzled TMA box, conflict-free row reads) -> 5 int8 slices
+//                stored straight into the A-operand buffers in TMEM (tcgen05.st): no shared-
+//                memory round trip for the slices, the MMAs read only the small B operand
 //   warps 10-13  epilogue (one per TMEM lane quadrant): levels -> fp64 B tile (scales
 //                applied) -> shared T -> coalesced store of B and the tile's Gram on the fp64
 //                tensor cores (36 upper 8 x 8 tiles, mma.m8n8k4)
@@ -42,16 +46,14 @@ constexpr int kOK = 32;        // values of i per chunk (MMA K for int8)
 constexpr int kOS = 5;         // slices per operand
 constexpr int kOLv = 5;        // levels L = 2 .. 6
 constexpr int kON = 64;        // MMA N (j, ell <= 64)
-constexpr int kONSS = 3;       // staging / Q ring depth
-constexpr int kONXS = 3;       // slice buffers
+constexpr int kONSS = 6;       // X staging ring depth
+constexpr int kONQ = 3;        // Q slice ring depth
 constexpr int kOSlicers = 8;   // slicer warps
 constexpr int kOEpi = 4;       // epilogue warps
-constexpr int kOThreads = 32 * (2 + kOSlicers + kOEpi);
+constexpr int kOThreads = 32 * (2 + kOSlicers + kOEpi + 1);  // + the Q producer warp
 constexpr int kOTS = 65;       // epilogue tile stride (doubles): row-per-lane stores conflict-free
 constexpr int kXStB = kOP * kOK * 4;         // staging bytes per chunk (16 KB)
 constexpr int kQChB = kOS * kON * kOK;       // pre-sliced Q bytes per chunk (10 KB)
-constexpr int kXSlB = kOP * kOK;             // one X slice (4 KB)
-constexpr int kXsB = kOS * kXSlB;            // all slices of a chunk (20 KB)
 
 __device__ __forceinline__ int kmaj8(int r, int k) {  // byte offset, K-major int8 core matrices
   return (r >> 3) * 256 + (k >> 4) * 128 + (r & 7) * 16 + (k & 15);
@@ -160,21 +162,43 @@ struct OzParams {
   double *gram_partial; // [grid][64 x 64] or null
 };
 
+// 2^k as a double for k in the normal range (clamped)
+__device__ __forceinline__ double pow2d(int k) {
+  k = k < -1022 ? -1022 : (k > 1023 ? 1023 : k);
+  return __longlong_as_double((long long)(k + 1023) << 52);
+}
+__device__ __forceinline__ void mma_i8_ta(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+
+// TMEM map: columns [0, 320): the 5 level accumulators (64 columns each); columns
+// [320 + 40 b, +40): A-operand buffer b (5 X slices x 8 columns: lane = column p of the tile,
+// column c of a slice = int8 values k = 4c .. 4c + 3 of the chunk).
+constexpr int kOXB = 4;          // A-operand buffers in TMEM
+constexpr uint32_t kOAcol = 320;
+
 __global__ void __launch_bounds__(kOThreads, 1)
     bpass_ozaki_kernel(const __grid_constant__ CUtensorMap tmap, const OzParams p) {
   extern __shared__ __align__(1024) unsigned char ozs[];
   const uint32_t pad = (1024u - (tc::smem_u32(ozs) & 1023u)) & 1023u;
   unsigned char *base = ozs + pad;
-  unsigned char *stg = base;                             // [kONSS][16 KB] fp32 X boxes
-  unsigned char *qb = stg + kONSS * kXStB;               // [kONSS][10 KB] Q slices
-  unsigned char *xsb = qb + kONSS * kQChB;               // [kONXS][20 KB] X slices
-  double *T = reinterpret_cast<double *>(xsb + kONXS * kXsB);  // [128][kOTS]
-  uint64_t *full = reinterpret_cast<uint64_t *>(T + kOP * kOTS);
-  uint64_t *sfree = full + kONSS, *qfree = sfree + kONSS;
-  uint64_t *xready = qfree + kONSS, *xempty = xready + kONXS;
-  uint64_t *accfull = xempty + kONXS, *accempty = accfull + 1;
+  unsigned char *stg = base;                             // [kONSS][16 KB] fp32 X boxes (128B swizzle)
+  unsigned char *qb = stg + kONSS * kXStB;               // [kONQ][10 KB] Q slices
+  double *T = reinterpret_cast<double *>(qb + kONQ * kQChB);  // [128][kOTS]
+  uint64_t *full = reinterpret_cast<uint64_t *>(T + kOP * kOTS);  // X stage landed
+  uint64_t *sfree = full + kONSS;                        // X stage consumed by the slicers
+  uint64_t *qfull = sfree + kONSS, *qfree = qfull + kONQ;
+  uint64_t *xready = qfree + kONQ, *xempty = xready + kOXB;
+  uint64_t *accfull = xempty + kOXB, *accempty = accfull + 1;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(accempty + 1);
-  int *fsh = reinterpret_cast<int *>(tslot + 2);        // [64] Q exponents
+  double *fpw = reinterpret_cast<double *>(tslot + 2);  // [64] 2^{f_j}
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t ntiles = (p.P + kOP - 1) / kOP;
@@ -186,9 +210,12 @@ __global__ void __launch_bounds__(kOThreads, 1)
     for (int s = 0; s < kONSS; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&sfree[s], 32 * kOSlicers);
+    }
+    for (int s = 0; s < kONQ; ++s) {
+      tc::mbar_init(&qfull[s], 1);
       tc::mbar_init(&qfree[s], 1);
     }
-    for (int s = 0; s < kONXS; ++s) {
+    for (int s = 0; s < kOXB; ++s) {
       tc::mbar_init(&xready[s], 32 * kOSlicers);
       tc::mbar_init(&xempty[s], 1);
     }
@@ -196,7 +223,7 @@ __global__ void __launch_bounds__(kOThreads, 1)
     tc::mbar_init(accempty, 32 * kOEpi);
     tc::fence_barrier_init();
   }
-  for (int j = threadIdx.x; j < kON; j += kOThreads) fsh[j] = p.f[j];
+  for (int j = threadIdx.x; j < kON; j += kOThreads) fpw[j] = pow2d(p.f[j]);
   if (warp == 1) tc::tmem_alloc(tslot, 512);
   tc::tc_fence_before();
   __syncthreads();
@@ -213,41 +240,39 @@ __global__ void __launch_bounds__(kOThreads, 1)
         const int64_t tk = g / nchunk;
         const int ch = (int)(g - tk * nchunk);
         const int64_t p0 = (blockIdx.x + tk * gridDim.x) * kOP;
-        if (g >= kONSS) {
-          tc::mbar_wait(&sfree[s], ph ^ 1);
-          tc::mbar_wait(&qfree[s], ph ^ 1);
-        }
-        tc::mbar_arrive_expect_tx(&full[s], kXStB + kQChB);
+        if (g >= kONSS) tc::mbar_wait(&sfree[s], ph ^ 1);
+        tc::mbar_arrive_expect_tx(&full[s], kXStB);
         tc::tma_load_2d(stg + s * kXStB, &tmap, &full[s], ch * kOK, (int)p0);
-        bulk_g2s(qb + s * kQChB, p.qs + (size_t)ch * kQChB, kQChB, &full[s]);
         if (++s == kONSS) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------- MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_s8(kOP, kON);
-      int s = 0, x = 0;
+      constexpr uint32_t idesc = idesc_s8(kOP, kON), idesc2 = idesc_s8(kOP, 2 * kON);
+      int s = 0, x = 0;  // s: Q ring slot
       uint32_t ph = 0, phx = 0;
       int ch = 0;
       int64_t tt = 0;
       for (int64_t g = 0; g < total; ++g) {
         if (ch == 0 && tt > 0) tc::mbar_wait(accempty, (uint32_t)((tt - 1) & 1));  // TMEM drained
-        tc::mbar_wait(&full[s], ph);
+        tc::mbar_wait(&qfull[s], ph);
         tc::mbar_wait(&xready[x], phx);
         tc::tc_fence_after();
-        const uint32_t xa = tc::smem_u32(xsb + x * kXsB), qa = tc::smem_u32(qb + s * kQChB);
+        const uint32_t xa = tmem + kOAcol + 40 * x;
+        const uint64_t bd0 = tc::smem_desc(tc::smem_u32(qb + s * kQChB), 128, 256, tc::kSwNone);
+        // pairs (sx, t) and (sx, t + 1) in ONE N = 128 MMA: the B slices q_t, q_{t+1} are
+        // adjacent 64-row tiles in shared memory, and the levels sx + t, sx + t + 1 adjacent
+        // 64-column accumulators in TMEM (10 MMAs per chunk instead of 15)
 #pragma unroll
         for (int sx = 0; sx < kOS; ++sx)
 #pragma unroll
-          for (int sq = 0; sq < kOS; ++sq) {
+          for (int sq = 0; sx + sq < kOLv; sq += 2) {
             const int L = sx + sq;  // level - 2 (slices are 1-based in the derivation)
-            if (L >= kOLv) continue;
-            const uint64_t ad = tc::smem_desc(xa + sx * kXSlB, 128, 256, tc::kSwNone);
-            const uint64_t bd = tc::smem_desc(qa + sq * (kON * kOK), 128, 256, tc::kSwNone);
-            // first product of a level in a tile overwrites the accumulator
-            const bool first = (ch == 0) && (sx == 0 || sq == L);
-            mma_i8(tmem + L * kON, ad, bd, idesc, first ? 0u : 1u);
+            const bool two = L + 1 < kOLv;
+            // the first products of a level in a tile (sx = 0) overwrite the accumulators
+            mma_i8_ta(tmem + L * kON, xa + 8 * sx, bd0 + (uint64_t)(sq * ((kON * kOK) >> 4)), two ? idesc2 : idesc,
+                      (ch == 0 && sx == 0) ? 0u : 1u);
           }
         tc::mma_commit(&xempty[x]);
         tc::mma_commit(&qfree[s]);
@@ -256,53 +281,68 @@ __global__ void __launch_bounds__(kOThreads, 1)
           tc::mma_commit(accfull);
           ++tt;
         }
-        if (++s == kONSS) { s = 0; ph ^= 1; }
-        if (++x == kONXS) { x = 0; phx ^= 1; }
+        if (++s == kONQ) { s = 0; ph ^= 1; }
+        if (++x == kOXB) { x = 0; phx ^= 1; }
+      }
+    }
+  } else if (warp == 2 + kOSlicers + kOEpi) {
+    // ------------------------------------------------------------------- Q producer
+    if (lane == 0) {  // pre-sliced Q chunks (L2-resident, the same for every tile)
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t g = 0; g < total; ++g) {
+        const int64_t tk = g / nchunk;
+        const int ch = (int)(g - tk * nchunk);
+        if (g >= kONQ) tc::mbar_wait(&qfree[s], ph ^ 1);
+        tc::mbar_arrive_expect_tx(&qfull[s], kQChB);
+        bulk_g2s(qb + s * kQChB, p.qs + (size_t)ch * kQChB, kQChB, &qfull[s]);
+        if (++s == kONQ) { s = 0; ph ^= 1; }
       }
     }
   } else if (warp < 2 + kOSlicers) {
     // ------------------------------------------------------------------- slicers
-    const int wt = threadIdx.x - 64;  // 0 .. 255
+    // warp -> TMEM lane quadrant q = warp % 4 (tile rows 32 q ..) and half of the chunk's i
+    const int q = warp & 3, half = (warp - 2) >> 2;
+    const int row = 32 * q + lane;
     int s = 0, x = 0;
     uint32_t ph = 0, phx = 0;
     int ch = 0;
     int64_t tk = 0;
-    float sc[4];  // 2^-e_p of this thread's 4 columns (items wt + 256 k: column (wt >> 3) + 32 k)
+    float sc = 0.f;  // 2^-e_p of this thread's column
     for (int64_t g = 0; g < total; ++g) {
       if (ch == 0) {
-        const int64_t p0 = (blockIdx.x + tk * gridDim.x) * kOP;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int64_t pp = p0 + (wt >> 3) + 32 * k;
-          sc[k] = pp < p.P ? ldexpf(1.0f, -exp_of(p.cm[pp])) : 0.f;
-        }
+        const int64_t pp = (blockIdx.x + tk * gridDim.x) * kOP + row;
+        sc = pp < p.P ? ldexpf(1.0f, -exp_of(p.cm[pp])) : 0.f;
       }
       tc::mbar_wait(&full[s], ph);
-      if (g >= kONXS) tc::mbar_wait(&xempty[x], phx ^ 1);
-      const float *st = reinterpret_cast<const float *>(stg + s * kXStB);  // [128 p][32 i]
-      unsigned char *xs = xsb + x * kXsB;
+      if (g >= kOXB) tc::mbar_wait(&xempty[x], phx ^ 1);
+      tc::tc_fence_after();
+      // staging row `row` = 32 floats (128 B, 16-byte chunks XOR-swizzled by row % 8)
+      const unsigned char *srow = stg + s * kXStB + row * 128;
+      uint32_t w[kOS][4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int item = wt + 256 * k, pr = item >> 3, i4 = item & 7;
-        const float4 v = *reinterpret_cast<const float4 *>(st + pr * kOK + 4 * i4);
+      for (int cq = 0; cq < 4; ++cq) {  // 16-byte chunk j = 4 half + cq: values k = 4 j .. 4 j + 3
+        const int j = 4 * half + cq;
+        const float4 v = *reinterpret_cast<const float4 *>(srow + ((j ^ (row & 7)) << 4));
         uint32_t a[kOS], b[kOS], c[kOS], d[kOS];
-        slice5(v.x * sc[k], a);
-        slice5(v.y * sc[k], b);
-        slice5(v.z * sc[k], c);
-        slice5(v.w * sc[k], d);
-        const int off = kmaj8(pr, 4 * i4);
+        slice5(v.x * sc, a);
+        slice5(v.y * sc, b);
+        slice5(v.z * sc, c);
+        slice5(v.w * sc, d);
 #pragma unroll
-        for (int q = 0; q < kOS; ++q) {  // low bytes of a, b, c, d -> one word
-          const uint32_t w = __byte_perm(__byte_perm(a[q], b[q], 0x0040), __byte_perm(c[q], d[q], 0x0040), 0x5410);
-          *reinterpret_cast<uint32_t *>(xs + q * kXSlB + off) = w;
-        }
+        for (int t = 0; t < kOS; ++t)
+          w[t][cq] = __byte_perm(__byte_perm(a[t], b[t], 0x0040), __byte_perm(c[t], d[t], 0x0040), 0x5410);
       }
-      tc::mbar_arrive(&sfree[s]);
-      tc::fence_proxy_async_smem();
+      tc::mbar_arrive(&sfree[s]);  // staging slot may be refilled
+      const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + kOAcol + 40 * x + 4 * half;
+#pragma unroll
+      for (int t = 0; t < kOS; ++t) tmem_st4(ta + 8 * t, w[t][0], w[t][1], w[t][2], w[t][3]);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc::tc_fence_before();
       tc::mbar_arrive(&xready[x]);
       if (++ch == nchunk) { ch = 0; ++tk; }
       if (++s == kONSS) { s = 0; ph ^= 1; }
-      if (++x == kONXS) { x = 0; phx ^= 1; }
+      if (++x == kOXB) { x = 0; phx ^= 1; }
     }
   } else {
     // ------------------------------------------------------------------- epilogue
@@ -313,33 +353,37 @@ __global__ void __launch_bounds__(kOThreads, 1)
 #pragma unroll
     for (int u = 0; u < 9; ++u) gacc[u][0] = gacc[u][1] = 0.0;
     const int ew = warp - (2 + kOSlicers);  // 0 .. 3
+    long long *Ti = reinterpret_cast<long long *>(T);
     for (int64_t tt = 0; tt < mytiles; ++tt) {
       const int64_t p0 = (blockIdx.x + tt * gridDim.x) * kOP;
+      const int64_t pp = p0 + row;
       tc::mbar_wait(accfull, (uint32_t)(tt & 1));
       tc::tc_fence_after();
-      const int64_t pp = p0 + row;
-      const int ep = pp < p.P ? exp_of(p.cm[pp]) : 0;
+      // phase 1 (holds TMEM): S = sum_L acc_L 2^{7 (4 - L)} exactly in int64 (|S| < 2^60 for
+      // I <= 100000), parked in T; then release the accumulators
 #pragma unroll 1
-      for (int h = 0; h < 2; ++h) {  // two halves of 32 columns: 5 levels each, smallest first
-        double bv[32];
+      for (int h = 0; h < 2; ++h) {
+        long long S[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) bv[j] = 0.0;
-#pragma unroll
-        for (int L = kOLv - 1; L >= 0; --L) {
+        for (int L = 0; L < kOLv; ++L) {
           uint32_t r[32];
           tc::tmem_ld32(tmem + ((uint32_t)(32 * q4) << 16) + L * kON + 32 * h, r);
-          const double w = ldexp(1.0, 2 - 7 * (L + 2));
 #pragma unroll
-          for (int j = 0; j < 32; ++j) bv[j] = fma((double)(int)r[j], w, bv[j]);
+          for (int j = 0; j < 32; ++j) S[j] = (L == 0 ? 0ll : (S[j] << 7)) + (long long)(int)r[j];
         }
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int jj = 32 * h + j;
-          T[row * kOTS + jj] = (pp < p.P && jj < p.J) ? ldexp(bv[j], ep + fsh[jj]) : 0.0;
-        }
+        for (int j = 0; j < 32; ++j) Ti[row * kOTS + 32 * h + j] = S[j];
       }
       tc::tc_fence_before();
       tc::mbar_arrive(accempty);  // the MMA warp may overwrite the accumulators
+      // phase 2: B_jp = S 2^{e_p - 40} 2^{f_j} (level weights 2^{2 - 7 (L + 2)}, L = 0 .. 4)
+      const int ep = pp < p.P ? exp_of(p.cm[pp]) : 0;
+      const double rs = pow2d(ep - 40);
+#pragma unroll 8
+      for (int jj = 0; jj < kON; ++jj) {
+        const long long Sv = Ti[row * kOTS + jj];
+        T[row * kOTS + jj] = (pp < p.P && jj < p.J) ? (double)Sv * rs * fpw[jj] : 0.0;
+      }
       named_bar(1, 32 * kOEpi);
       const int64_t ncol = p.P - p0 < kOP ? p.P - p0 : kOP;
       if (p.out && ncol > 0) {  // B tile (J x ncol) is one contiguous range out[p0 J ..]
@@ -449,11 +493,11 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
   cuuint32_t box[2] = {kOK, kOP};
   cuuint32_t es[2] = {1, 1};
   CUresult r = tensor_map_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)X, dims, strides, box, es,
-                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(RTUCKER_ECUDA, "cuTensorMapEncodeTiled failed for the Ozaki B-pass");
-  const size_t smem = 1024 + (size_t)kONSS * (kXStB + kQChB) + (size_t)kONXS * kXsB + sizeof(double) * kOP * kOTS +
-                      8 * (3 * kONSS + 2 * kONXS + 2) + 16 + 4 * kON;
+  const size_t smem = 1024 + (size_t)kONSS * kXStB + (size_t)kONQ * kQChB + sizeof(double) * kOP * kOTS +
+                      8 * (2 * kONSS + 2 * kONQ + 2 * kOXB + 2) + 16 + 8 * kON;
   RT_CUDA(cudaFuncSetAttribute(bpass_ozaki_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   RT_LAUNCH(c, bpass_ozaki_kernel, grid, kOThreads, smem, tm, prm);
   if (gram) RT_LAUNCH(c, oz_gram_reduce_kernel, (J * J + 127) / 128, 128, 0, part.p, grid, J, gram);

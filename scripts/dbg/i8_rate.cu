@@ -12,7 +12,12 @@ __device__ __forceinline__ void mma_i8(uint32_t d, uint64_t a, uint64_t b, uint3
                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d), "l"(a), "l"(b), "r"(idesc), "r"(acc)
                : "memory");
 }
-template <int N>
+__device__ __forceinline__ void mma_i8_ta(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d), "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+               : "memory");
+}
+template <int N, bool TA>
 __global__ void rate(long long *out, int R) {
   __shared__ __align__(1024) int8_t sa[128 * 32];
   __shared__ __align__(1024) int8_t sb[256 * 32];
@@ -22,7 +27,7 @@ __global__ void rate(long long *out, int R) {
   for (int i = t; i < 128 * 32; i += blockDim.x) sa[i] = (int8_t)(i % 7 - 3);
   for (int i = t; i < 256 * 32; i += blockDim.x) sb[i] = (int8_t)(i % 5 - 2);
   if (t == 0) { tc::mbar_init(&bar, 1); tc::fence_barrier_init(); }
-  if (warp == 0) tc::tmem_alloc(&slot, 256);
+  if (warp == 0) tc::tmem_alloc(&slot, 512);
   tc::fence_proxy_async_smem();
   tc::tc_fence_before();
   __syncthreads();
@@ -31,7 +36,10 @@ __global__ void rate(long long *out, int R) {
     const uint64_t ad = tc::smem_desc(tc::smem_u32(sa), 128, 256, tc::kSwNone);
     const uint64_t bd = tc::smem_desc(tc::smem_u32(sb), 128, 256, tc::kSwNone);
     long long t0 = clock64();
-    for (int r = 0; r < R; ++r) mma_i8(slot, ad, bd, idesc_s8(128, N), r > 0);
+    for (int r = 0; r < R; ++r) {
+      if (TA) mma_i8_ta(slot, slot + 256, bd, idesc_s8(128, N), r > 0);
+      else mma_i8(slot, ad, bd, idesc_s8(128, N), r > 0);
+    }
     tc::mma_commit(&bar);
     long long t1 = clock64();
     tc::mbar_wait(&bar, 0);
@@ -40,18 +48,22 @@ __global__ void rate(long long *out, int R) {
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(slot, 256);
+  if (warp == 0) tc::tmem_dealloc(slot, 512);
 }
 int main() {
   long long *o, h[2];
   cudaMalloc(&o, 16);
   const int R = 4096;
-  rate<64><<<148, 128>>>(o, R); cudaDeviceSynchronize();
-  rate<64><<<148, 128>>>(o, R); cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost);
+  rate<64, false><<<148, 128>>>(o, R); cudaDeviceSynchronize();
+  rate<64, false><<<148, 128>>>(o, R); cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost);
   printf("N=64 : issue %.1f cyc/MMA, complete %.1f cyc/MMA -> %.0f MAC/clk/SM\n", (double)h[0] / R, (double)h[1] / R, 128.0 * 64 * 32 * R / h[1]);
-  rate<128><<<148, 128>>>(o, R); cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost);
+  rate<128, false><<<148, 128>>>(o, R); cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost);
   printf("N=128: issue %.1f cyc/MMA, complete %.1f cyc/MMA -> %.0f MAC/clk/SM\n", (double)h[0] / R, (double)h[1] / R, 128.0 * 128 * 32 * R / h[1]);
-  rate<256><<<148, 128>>>(o, R); cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost);
+  rate<256, false><<<148, 128>>>(o, R); cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost);
   printf("N=256: issue %.1f cyc/MMA, complete %.1f cyc/MMA -> %.0f MAC/clk/SM\n", (double)h[0] / R, (double)h[1] / R, 128.0 * 256 * 32 * R / h[1]);
+  rate<64, true><<<148, 128>>>(o, R); cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost);
+  printf("TMEM-A N=64 : issue %.1f cyc/MMA, complete %.1f cyc/MMA -> %.0f MAC/clk/SM\n", (double)h[0] / R, (double)h[1] / R, 128.0 * 64 * 32 * R / h[1]);
+  rate<128, true><<<148, 128>>>(o, R); cudaMemcpy(h, o, 16, cudaMemcpyDeviceToHost);
+  printf("TMEM-A N=128: issue %.1f cyc/MMA, complete %.1f cyc/MMA -> %.0f MAC/clk/SM\n", (double)h[0] / R, (double)h[1] / R, 128.0 * 128 * 32 * R / h[1]);
   return 0;
 }
