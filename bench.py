@@ -73,6 +73,23 @@ def fp64_peak_tflops():
     return sms * 64 * 2 * mhz * 1e6 / 1e12, f"derived: {sms} SMs x 64 fp64 FMA/clk (DFMA = DMMA, measured) x 2 x {mhz:.0f} MHz"
 
 
+def int8_peak_tops():
+    """Dense int8 tensor-core peak from the measured tcgen05 kind::i8 rate (8186 MAC/clk/SM
+    at N >= 128, scripts/dbg/i8_rate.cu on this pool's B200) x SMs x 2 x max SM clock."""
+    try:
+        import torch
+        sms = torch.cuda.get_device_properties(0).multi_processor_count
+    except Exception:
+        sms = 148
+    mhz = 1965.0
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mhz = float(json.load(f).get("sm_max_mhz", mhz))
+    except Exception:
+        pass
+    return sms * 8186 * 2 * mhz * 1e6 / 1e12, f"derived: {sms} SMs x 8186 int8 MAC/clk (measured) x 2 x {mhz:.0f} MHz"
+
+
 def load_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
     captures (profiles/traffic.json, written by scripts/ncu_traffic.py); {} if absent."""
@@ -310,6 +327,7 @@ def main():
     # ---- rooflines: per-kernel algorithmic work / event-timed duration
     hbm, peak_src = peaks()
     fp64_peak, fp64_src = fp64_peak_tflops()
+    i8_peak, i8_src = int8_peak_tops()
     step_phase_ms = {f"{k[0]}{k[1] + 1}": round(v[0] / max(v[1], 1), 4) for k, v in sorted(phases.items())}
     traffic = load_traffic()
     kernels = []
@@ -324,15 +342,25 @@ def main():
                         "algorithmic": f"{algo} B per launch (800^3 fp32 read once)"})
     bp_ms, bp_n = phases.get(("bpass", 0), (0.0, 0))
     if bp_n and args.algo == "sthosvd":
+        # mode-1 B-pass: Ozaki-style fp64-accurate products on the int8 tensor cores
+        # (bpass_ozaki.cu). Roofline model: HBM (X read + B written, 0.36 ms at the measured
+        # copy bandwidth) bounds it before the int8 tensor work (15 slice products, ~0.2 ms).
         t_k = bp_ms / bp_n
-        flops = 2.0 * (RANKS[0] + P) * N_ELEM / world  # B = Q^T X_(1): 2 l flop per element (fp64 products)
-        ach = flops / (t_k * 1e-3) / 1e12
-        kernels.append({"kernel": "ttm_dmma_l1_kernel (mode-1 B-pass on the fp64 tensor cores + fp64 Gram, "
-                                  "HYBRID policy)", "bound": "alu",
-                        "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s", "frac": ach / fp64_peak,
-                        "traffic": traffic.get("ttm_dmma_l1_kernel<float, 1, 1>"), "ms": t_k,
-                        "algorithmic": f"{flops:.4g} fp64 flop per launch (2 l N, l = 60)",
-                        "peak_source": fp64_src})
+        ell = RANKS[0] + P
+        algo_b = BYTES_X // world + 8 * ell * (N_ELEM // I) // world  # X once + B (fp64) once
+        ach = algo_b / (t_k * 1e-3) / 1e9
+        flops = 2.0 * ell * N_ELEM / world
+        i8_ops = 15 * 2.0 * 64 * N_ELEM / world  # 15 slice pairs, N padded to 64
+        kernels.append({"kernel": "bpass_ozaki_kernel (mode-1 B-pass + fp64 Gram: fp64-accurate products from "
+                                  "exact int8 tensor-core slice products, tcgen05 kind::i8)",
+                        "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                        "traffic": traffic.get("bpass_ozaki_kernel"), "ms": t_k,
+                        "algorithmic": f"{algo_b} B per launch (800^3 fp32 read once + B 60 x 640000 fp64 written)",
+                        "fp64_equiv_tflops": flops / (t_k * 1e-3) / 1e12,
+                        "fp64_peak_tflops": fp64_peak,
+                        "int8_tops": i8_ops / (t_k * 1e-3) / 1e12,
+                        "int8_peak_tops": i8_peak,
+                        "int8_peak_source": i8_src})
     dom = max(kernels, key=lambda k: k["ms"]) if kernels else None
     roofline = None
     if dom:
