@@ -67,6 +67,16 @@ __global__ void __launch_bounds__(kCooT) sketch_coo_kernel(CooDev g, int mode, i
     }
     const unsigned grp = __match_any_sync(0xffffffffu, row);
     const int leader = __ffs(grp) - 1;
+    // rows shared by more than two lanes (the heavy rows of Zipf-like data): tree reduction over
+    // the group in 5 shuffle steps (partner = the member 2^k ranks further, __fns) instead of
+    // a serial loop over up to 32 members
+    const bool big = __any_sync(0xffffffffu, __popc(grp) > 2);
+    unsigned src[5];
+    const int rank = __popc(grp & ((1u << lane) - 1u));
+    if (big) {
+#pragma unroll
+      for (int k = 0; k < 5; ++k) src[k] = __fns(grp, lane, 1 + (1 << k));
+    }
     for (int jb = 0; jb < nb; ++jb) {
       float4 dummy;
       (void)dummy;
@@ -77,17 +87,30 @@ __global__ void __launch_bounds__(kCooT) sketch_coo_kernel(CooDev g, int mode, i
 #pragma unroll
         for (int q = 0; q < 4; ++q) pr[q] = v * (double)z.v[q];
       }
-      // sum over the lanes of this row group (fixed order: by lane index)
+      // sum over the lanes of this row group (into the group's first lane)
+      if (!big) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        double t = 0.0;
-        unsigned m = grp;
-        while (m) {
-          const int src = __ffs(m) - 1;
-          t += __shfl_sync(grp, pr[q], src);
-          m &= m - 1;
+        for (int q = 0; q < 4; ++q) {
+          double t = 0.0;
+          unsigned m = grp;
+          while (m) {
+            const int sl = __ffs(m) - 1;
+            t += __shfl_sync(grp, pr[q], sl);
+            m &= m - 1;
+          }
+          pr[q] = t;
         }
-        pr[q] = t;
+      } else {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+          const bool take = src[k] != 0xffffffffu && (rank & ((2 << k) - 1)) == 0;
+          const int sl = (src[k] != 0xffffffffu) ? (int)src[k] : lane;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const double o = __shfl_sync(0xffffffffu, pr[q], sl);
+            if (take) pr[q] += o;
+          }
+        }
       }
       if (act && lane == leader) {
 #pragma unroll
