@@ -450,6 +450,10 @@ __global__ void oz_gram_reduce_kernel(const double *__restrict__ part, int nblk,
 
 }  // namespace
 
+void column_maxima(Ctx &c, const float *X, int64_t I, int64_t P, uint32_t *cm) {
+  RT_LAUNCH(c, colmax_kernel, std::max(1, std::min(c.num_sms * 16, (int)((P + 7) / 8))), 256, 0, X, I, P, cm);
+}
+
 bool ozaki_bpass_enabled() {
   static const bool off = getenv("RTUCKER_NO_OZAKI") != nullptr;
   return !off;

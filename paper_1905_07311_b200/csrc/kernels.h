@@ -54,6 +54,8 @@ void philox_raw(Ctx &c, const uint32_t *ctr, int64_t n, uint32_t k0, uint32_t k1
 bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda, int J, double *out, double *gram,
                const uint32_t *colmax = nullptr);
 bool ozaki_bpass_enabled();
+// cm[p] = fp32 bits of max_i |X(i, p)| for X (I x P, column-major) - the Ozaki column scales.
+void column_maxima(Ctx &c, const float *X, int64_t I, int64_t P, uint32_t *cm);
 void ttm_dense(Ctx &c, const void *X, DT in, ModeView v, const double *A, int64_t lda, int J,
                void *out, DT outT, bool mul_f64, double *gram, const uint32_t *colmax = nullptr);
 

@@ -85,6 +85,10 @@ FP32_CASES = [
     ("C3_f32", lambda: hilbert((25,) * 5, "shifted", dtype=np.float32), (5,) * 5, 5, (0, 1, 2, 3, 4)),
     ("C1_f32", lambda: hilbert((50, 50, 50), "shifted", dtype=np.float32), (5, 5, 5), 5, (0, 1, 2)),
     ("odeco96", lambda: odeco(96, seed=4, dtype=np.float32), (12, 12, 12), 10, (0, 1, 2)),
+    # mode 1 with I_1 = 1100 > 1024: the tcgen05 sketch declines (TMEM), so the Ozaki B-pass
+    # gets its column maxima from the separate column_maxima pass
+    ("tall_mode1", lambda: np.asfortranarray(np.random.default_rng(11).standard_normal((1100, 24, 20))
+                                             .astype(np.float32)), (10, 8, 8), 6, (0, 1, 2)),
 ]
 
 
