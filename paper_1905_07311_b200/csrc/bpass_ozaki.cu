@@ -32,6 +32,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdio>
+
 #include "kernels.h"
 #include "tc.cuh"
 
@@ -160,7 +162,14 @@ struct OzParams {
   const int *f;         // [64]
   double *out;          // B: (J x P) column-major, or null
   double *gram_partial; // [grid][64 x 64] or null
+  long long *prof;      // CTA 0 wait-cycle counters (builds with -DRTUCKER_OZ_PROF_BUILD only)
 };
+
+#ifdef RTUCKER_OZ_PROF_BUILD
+#define OZP(...) __VA_ARGS__
+#else
+#define OZP(...)
+#endif
 
 // 2^k as a double for k in the normal range (clamped)
 __device__ __forceinline__ double pow2d(int k) {
@@ -247,20 +256,28 @@ __global__ void __launch_bounds__(kOThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------------- MMA issuer (warp-wide,
+    // elect.sync inside the MMA asm: uniform operands, see tc::mma_tf32_w)
+    {
       constexpr uint32_t idesc = idesc_s8(kOP, kON), idesc2 = idesc_s8(kOP, 2 * kON);
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint32_t qb0 = __shfl_sync(0xffffffffu, tc::smem_u32(qb), 0);
       int s = 0, x = 0;  // s: Q ring slot
       uint32_t ph = 0, phx = 0;
       int ch = 0;
       int64_t tt = 0;
+      OZP(long long w0 = 0, w1 = 0, w2 = 0, t0 = clock64();)
       for (int64_t g = 0; g < total; ++g) {
+        OZP(const long long c0 = clock64();)
         if (ch == 0 && tt > 0) tc::mbar_wait(accempty, (uint32_t)((tt - 1) & 1));  // TMEM drained
+        OZP(const long long c1 = clock64();)
         tc::mbar_wait(&qfull[s], ph);
+        OZP(const long long c2 = clock64();)
         tc::mbar_wait(&xready[x], phx);
+        OZP(w0 += c1 - c0; w1 += c2 - c1; w2 += clock64() - c2;)
         tc::tc_fence_after();
-        const uint32_t xa = tmem + kOAcol + 40 * x;
-        const uint64_t bd0 = tc::smem_desc(tc::smem_u32(qb + s * kQChB), 128, 256, tc::kSwNone);
+        const uint32_t xa = tm + kOAcol + 40 * x;
+        const uint64_t bd0 = tc::smem_desc(qb0 + s * kQChB, 128, 256, tc::kSwNone);
         // pairs (sx, t) and (sx, t + 1) in ONE N = 128 MMA: the B slices q_t, q_{t+1} are
         // adjacent 64-row tiles in shared memory, and the levels sx + t, sx + t + 1 adjacent
         // 64-column accumulators in TMEM (10 MMAs per chunk instead of 15)
@@ -271,19 +288,22 @@ __global__ void __launch_bounds__(kOThreads, 1)
             const int L = sx + sq;  // level - 2 (slices are 1-based in the derivation)
             const bool two = L + 1 < kOLv;
             // the first products of a level in a tile (sx = 0) overwrite the accumulators
-            mma_i8_ta(tmem + L * kON, xa + 8 * sx, bd0 + (uint64_t)(sq * ((kON * kOK) >> 4)), two ? idesc2 : idesc,
+            tc::mma_i8_ta_w(tm + L * kON, xa + 8 * sx, bd0 + (uint64_t)(sq * ((kON * kOK) >> 4)), two ? idesc2 : idesc,
                       (ch == 0 && sx == 0) ? 0u : 1u);
           }
-        tc::mma_commit(&xempty[x]);
-        tc::mma_commit(&qfree[s]);
+        tc::mma_commit_w(&xempty[x]);
+        tc::mma_commit_w(&qfree[s]);
         if (++ch == nchunk) {
           ch = 0;
-          tc::mma_commit(accfull);
+          tc::mma_commit_w(accfull);
           ++tt;
         }
         if (++s == kONQ) { s = 0; ph ^= 1; }
         if (++x == kOXB) { x = 0; phx ^= 1; }
       }
+      OZP(if (p.prof && blockIdx.x == 0 && lane == 0) {
+        p.prof[0] = w0; p.prof[1] = w1; p.prof[2] = w2; p.prof[3] = clock64() - t0; p.prof[15] = total;
+      })
     }
   } else if (warp == 2 + kOSlicers + kOEpi) {
     // ------------------------------------------------------------------- Q producer
@@ -309,13 +329,17 @@ __global__ void __launch_bounds__(kOThreads, 1)
     int ch = 0;
     int64_t tk = 0;
     float sc = 0.f;  // 2^-e_p of this thread's column
+    OZP(long long w4 = 0, w5 = 0, t0 = clock64();)
     for (int64_t g = 0; g < total; ++g) {
       if (ch == 0) {
         const int64_t pp = (blockIdx.x + tk * gridDim.x) * kOP + row;
         sc = pp < p.P ? ldexpf(1.0f, -exp_of(p.cm[pp])) : 0.f;
       }
+      OZP(const long long c0 = clock64();)
       tc::mbar_wait(&full[s], ph);
+      OZP(const long long c1 = clock64();)
       if (g >= kOXB) tc::mbar_wait(&xempty[x], phx ^ 1);
+      OZP(w4 += c1 - c0; w5 += clock64() - c1;)
       tc::tc_fence_after();
       // staging row `row` = 32 floats (128 B, 16-byte chunks XOR-swizzled by row % 8)
       const unsigned char *srow = stg + s * kXStB + row * 128;
@@ -344,6 +368,7 @@ __global__ void __launch_bounds__(kOThreads, 1)
       if (++s == kONSS) { s = 0; ph ^= 1; }
       if (++x == kOXB) { x = 0; phx ^= 1; }
     }
+    OZP(if (p.prof && blockIdx.x == 0 && threadIdx.x == 64) { p.prof[4] = w4; p.prof[5] = w5; p.prof[6] = clock64() - t0; })
   } else {
     // ------------------------------------------------------------------- epilogue
     const int q4 = warp & 3;            // TMEM lane quadrant
@@ -354,10 +379,13 @@ __global__ void __launch_bounds__(kOThreads, 1)
     for (int u = 0; u < 9; ++u) gacc[u][0] = gacc[u][1] = 0.0;
     const int ew = warp - (2 + kOSlicers);  // 0 .. 3
     long long *Ti = reinterpret_cast<long long *>(T);
+    OZP(long long e0 = 0, e1 = 0, e2 = 0, e3 = 0, e4 = 0, et0 = clock64();)
     for (int64_t tt = 0; tt < mytiles; ++tt) {
       const int64_t p0 = (blockIdx.x + tt * gridDim.x) * kOP;
       const int64_t pp = p0 + row;
+      OZP(const long long c0 = clock64();)
       tc::mbar_wait(accfull, (uint32_t)(tt & 1));
+      OZP(const long long c1 = clock64(); e0 += c1 - c0;)
       tc::tc_fence_after();
       // phase 1 (holds TMEM): S = sum_L acc_L 2^{7 (4 - L)} exactly in int64 (|S| < 2^60 for
       // I <= 100000), parked in T; then release the accumulators
@@ -376,6 +404,7 @@ __global__ void __launch_bounds__(kOThreads, 1)
       }
       tc::tc_fence_before();
       tc::mbar_arrive(accempty);  // the MMA warp may overwrite the accumulators
+      OZP(const long long c2 = clock64(); e1 += c2 - c1;)
       // phase 2: B_jp = S 2^{e_p - 40} 2^{f_j} (level weights 2^{2 - 7 (L + 2)}, L = 0 .. 4)
       const int ep = pp < p.P ? exp_of(p.cm[pp]) : 0;
       const double rs = pow2d(ep - 40);
@@ -385,33 +414,64 @@ __global__ void __launch_bounds__(kOThreads, 1)
         T[row * kOTS + jj] = (pp < p.P && jj < p.J) ? (double)Sv * rs * fpw[jj] : 0.0;
       }
       named_bar(1, 32 * kOEpi);
+      OZP(const long long c3 = clock64(); e2 += c3 - c2;)
       const int64_t ncol = p.P - p0 < kOP ? p.P - p0 : kOP;
       if (p.out && ncol > 0) {  // B tile (J x ncol) is one contiguous range out[p0 J ..]
         double *dst = p.out + p0 * p.J;
-        for (int e = et; e < (int)ncol * p.J; e += 32 * kOEpi) {
-          const int pr = e / p.J, j = e - pr * p.J;
-          dst[e] = T[pr * kOTS + j];
+        const int ne = (int)ncol * p.J;
+        if ((p.J & 1) == 0) {  // pairs (j, j + 1) of one column: 16-byte stores, no division
+          const int st = 2 * 32 * kOEpi, sp = st / p.J, sj = st - sp * p.J;
+          int pr = (2 * et) / p.J, j = 2 * et - pr * p.J;
+          for (int e = 2 * et; e < ne; e += st) {
+            *reinterpret_cast<double2 *>(dst + e) = make_double2(T[pr * kOTS + j], T[pr * kOTS + j + 1]);
+            pr += sp;
+            j += sj;
+            if (j >= p.J) { j -= p.J; ++pr; }
+          }
+        } else {
+          const int st = 32 * kOEpi, sp = st / p.J, sj = st - sp * p.J;
+          int pr = et / p.J, j = et - pr * p.J;
+          for (int e = et; e < ne; e += st) {
+            dst[e] = T[pr * kOTS + j];
+            pr += sp;
+            j += sj;
+            if (j >= p.J) { j -= p.J; ++pr; }
+          }
         }
       }
+      OZP(const long long c4 = clock64(); e3 += c4 - c3;)
       if (p.gram_partial) {  // G += T^T T, 36 upper 8x8 tiles over the 4 epilogue warps
         const int fr = lane >> 2, fc = lane & 3;
+        // three tiles at a time, k inner: three independent DMMA accumulation chains in flight
+        // (one tile at a time left a dependent chain of 32 DMMAs: 22k cycles per tile; all
+        // nine at once spills)
 #pragma unroll
-        for (int u = 0; u < 9; ++u) {
-          const int t = ew + 4 * u;
-          int a = 0, rem = t;
-          while (rem >= 8 - a) { rem -= 8 - a; ++a; }
-          const int b = a + rem;
-          const double *ta = T + fc * kOTS + 8 * a + fr;
-          const double *tb = T + fc * kOTS + 8 * b + fr;
-#pragma unroll 8
-          for (int k0 = 0; k0 < kOP; k0 += 4)
-            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-                         : "+d"(gacc[u][0]), "+d"(gacc[u][1])
-                         : "d"(ta[k0 * kOTS]), "d"(tb[k0 * kOTS]));
+        for (int u0 = 0; u0 < 9; u0 += 3) {
+          int oa[3], ob[3];
+#pragma unroll
+          for (int v = 0; v < 3; ++v) {
+            const int t = ew + 4 * (u0 + v);
+            int a = 0, rem = t;
+            while (rem >= 8 - a) { rem -= 8 - a; ++a; }
+            oa[v] = fc * kOTS + 8 * a + fr;
+            ob[v] = fc * kOTS + 8 * (a + rem) + fr;
+          }
+#pragma unroll 4
+          for (int k0 = 0; k0 < kOP; k0 += 4) {
+#pragma unroll
+            for (int v = 0; v < 3; ++v)
+              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                           : "+d"(gacc[u0 + v][0]), "+d"(gacc[u0 + v][1])
+                           : "d"(T[oa[v] + k0 * kOTS]), "d"(T[ob[v] + k0 * kOTS]));
+          }
         }
       }
+      OZP(e4 += clock64() - c4;)
       named_bar(1, 32 * kOEpi);  // T free for the next tile
     }
+    OZP(if (p.prof && blockIdx.x == 0 && et == 0) {
+      p.prof[7] = e0; p.prof[8] = e1; p.prof[9] = e2; p.prof[10] = e3; p.prof[11] = e4; p.prof[12] = clock64() - et0;
+    })
     if (p.gram_partial) {
       const int fr = lane >> 2, fc = lane & 3;
       double *gp = p.gram_partial + (int64_t)blockIdx.x * 4096;
@@ -503,7 +563,23 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
   const size_t smem = 1024 + (size_t)kONSS * kXStB + (size_t)kONQ * kQChB + sizeof(double) * kOP * kOTS +
                       8 * (2 * kONSS + 2 * kONQ + 2 * kOXB + 2) + 16 + 8 * kON;
   RT_CUDA(cudaFuncSetAttribute(bpass_ozaki_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static const bool prof = getenv("RTUCKER_OZ_PROF") != nullptr;
+  DevBuf<long long> pbuf;
+  if (prof) {
+    pbuf.alloc(c, 16);
+    RT_CUDA(cudaMemsetAsync(pbuf.p, 0, 128, c.stream));
+    prm.prof = pbuf.p;
+  }
   RT_LAUNCH(c, bpass_ozaki_kernel, grid, kOThreads, smem, tm, prm);
+  if (prof) {
+    long long h[16];
+    RT_CUDA(cudaMemcpyAsync(h, pbuf.p, 128, cudaMemcpyDeviceToHost, c.stream));
+    RT_CUDA(cudaStreamSynchronize(c.stream));
+    fprintf(stderr,
+            "[oz prof] chunks %lld | mma: wait accempty %lld qfull %lld xready %lld total %lld | slicer: wait full %lld "
+            "xempty %lld total %lld | epi: wait accfull %lld ph1 %lld ph2 %lld store %lld gram %lld total %lld\n",
+            h[15], h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[10], h[11], h[12]);
+  }
   if (gram) RT_LAUNCH(c, oz_gram_reduce_kernel, (J * J + 127) / 128, 128, 0, part.p, grid, J, gram);
   return true;
 }

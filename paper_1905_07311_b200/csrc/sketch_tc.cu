@@ -30,6 +30,7 @@
 // it into hi / lo planes (elementwise, no transposition).
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cstdio>
 
 #include "kernels.h"
 #include "philox.cuh"
@@ -144,30 +145,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------- MMA issuer
-    if (lane == 0 && nst > 0) {
+    // ------------------------------------------------------------- MMA issuer (warp-wide)
+    if (nst > 0) {
       constexpr uint32_t idesc = tc::idesc_tf32(128, N, false, false);
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint32_t hb0 = __shfl_sync(0xffffffffu, tc::smem_u32(hb), 0);
+      const uint32_t lb0 = __shfl_sync(0xffffffffu, tc::smem_u32(lb), 0);
+      const uint32_t obh = __shfl_sync(0xffffffffu, tc::smem_u32(ohb), 0);
+      const uint32_t obl = __shfl_sync(0xffffffffu, tc::smem_u32(olb), 0);
       for (int it = 0; it < nst; ++it) {
         const int s = it % NSO, g = it % kNSG;
         tc::mbar_wait(&oready[g], (it / kNSG) & 1);
         tc::mbar_wait(&xready[s], (it / NSO) & 1);
         tc::tc_fence_after();
-        const uint32_t ha = tc::smem_u32(hb + (size_t)s * abytes);
-        const uint32_t la = tc::smem_u32(lb + (size_t)s * abytes);
-        const uint64_t bh = tc::smem_desc(tc::smem_u32(ohb + (size_t)g * obytes), 128, 256, tc::kSwNone);
-        const uint64_t bl = tc::smem_desc(tc::smem_u32(olb + (size_t)g * obytes), 128, 256, tc::kSwNone);
+        const uint32_t ha = hb0 + s * abytes, la = lb0 + s * abytes;
+        const uint64_t bh = tc::smem_desc(obh + g * obytes, 128, 256, tc::kSwNone);
+        const uint64_t bl = tc::smem_desc(obl + g * obytes, 128, 256, tc::kSwNone);
         for (int mt = 0; mt < NT; ++mt) {
           const uint64_t ah = tc::smem_desc(ha + mt * 128 * kBK * 4, 128, 256, tc::kSwNone);
           const uint64_t al = tc::smem_desc(la + mt * 128 * kBK * 4, 128, 256, tc::kSwNone);
-          const uint32_t d = tmem + mt * N;
-          tc::mma_tf32(d, ah, bh, idesc, it > 0 ? 1u : 0u);
-          tc::mma_tf32(d, ah, bl, idesc, 1u);
-          tc::mma_tf32(d, al, bh, idesc, 1u);
+          const uint32_t d = tm + mt * N;
+          tc::mma_tf32_w(d, ah, bh, idesc, it > 0 ? 1u : 0u);
+          tc::mma_tf32_w(d, ah, bl, idesc, 1u);
+          tc::mma_tf32_w(d, al, bh, idesc, 1u);
         }
-        tc::mma_commit(&xempty[s]);
-        tc::mma_commit(&oempty[g]);
+        tc::mma_commit_w(&xempty[s]);
+        tc::mma_commit_w(&oempty[g]);
       }
-      tc::mma_commit(done);
+      tc::mma_commit_w(done);
     }
   } else if (warp < 2 + kGen) {
     // ------------------------------------------------------------- Omega generators
@@ -265,13 +270,31 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (!KM && p.colmax) {  // warp max per column, one atomic per warp and column
-        const int64_t c0 = cbeg + (int64_t)it * kBK;
+      if (!KM && p.colmax) {
+        // warp max per column by a transposing butterfly: at distance 16, 8, 4 each lane keeps
+        // half of its columns and takes the partner's maxima of them (4 + 2 + 1 shuffles), so
+        // lane l ends with column l / 4 over 8 lanes; distances 2, 1 finish the warp.  Then
+        // lanes 4u issue the 8 atomics in one instruction.  Values are |x| >= 0, so the fp32
+        // maximum equals the maximum of the bit patterns the B-pass reads.
+        const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const uint32_t m = __reduce_max_sync(0xffffffffu, __float_as_uint(cm[u]));
-          if (lane == 0 && c0 + u < cend) atomicMax(p.colmax + c0 + u, m);
+        for (int k = 0; k < 4; ++k) {
+          const float keep = u16 ? cm[k + 4] : cm[k], send = u16 ? cm[k] : cm[k + 4];
+          cm[k] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 16));
         }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const float keep = u8 ? cm[k + 2] : cm[k], send = u8 ? cm[k] : cm[k + 2];
+          cm[k] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+        }
+        {
+          const float keep = u4 ? cm[1] : cm[0], send = u4 ? cm[0] : cm[1];
+          cm[0] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+        }
+        cm[0] = fmaxf(cm[0], __shfl_xor_sync(0xffffffffu, cm[0], 2));
+        cm[0] = fmaxf(cm[0], __shfl_xor_sync(0xffffffffu, cm[0], 1));
+        const int64_t c = cbeg + (int64_t)it * kBK + (lane >> 2);
+        if ((lane & 3) == 0 && c < cend) atomicMax(p.colmax + c, __float_as_uint(cm[0]));
       }
       nsq += (double)acc;
       tc::mbar_arrive(&sfree[ss]);       // staging slot may be refilled
@@ -320,6 +343,316 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// L == 1 variant with the A operand in TMEM (sketch_tc_ta_kernel).  The smem-operand kernel
+// above spends ~70 % of the shared-memory bandwidth on the X operand (hi / lo planes written
+// by the workers, read 3x by the MMAs: ~1900 wavefronts per 8-column stage, measured).  Here
+// the workers split the staged X rows and store hi / lo straight into TMEM (tcgen05.st, lane =
+// row i, one tf32 value per 32-bit column, K = 8 columns per MMA), so shared memory carries
+// only the TMA staging, its one read and the small Omega tiles.  TMEM then holds the
+// accumulators (<= 4 M-tiles x N columns, [0, 256)) and a ring of A stages ([256, 512):
+// tile t of stage s at 256 + 16 (s NTg + t), hi in its first 8 columns, lo in the next 8), so
+// a CTA covers at most 512 rows: the rows are split into ng = ceil(NT / 4) groups and CTA b
+// takes row group b % ng of column range b / ng (X is still read once; Omega is generated
+// by both CTAs of a column range).
+//   warp 0 TMA (boxes of BR rows x 8 columns of the CTA's row group), warp 1 MMA issuer,
+//   warps 2-5 Omega generators (as above), warps 6-13 workers: warp w owns TMEM lane quadrant
+//   q = w % 4 and the tiles t = (w - 6) / 4 + 2 u, i.e. rows r = 128 t + 32 q + lane.
+// D rows of rows outside the group (r >= rvalid) are never read, so their A lanes may hold
+// anything.
+constexpr int kTaCol = 256;  // first TMEM column of the A ring
+constexpr int kTaGen = 8;    // Omega generator warps (groups of 4 warps share the stages)
+constexpr int kTaWork = 8;   // X worker warps (kTaWq per TMEM lane quadrant)
+constexpr int kTaWq = kTaWork / 4;
+constexpr int kTaTpw = 4 / kTaWq;  // M-tiles per worker warp
+constexpr int kTaNSG = 8;    // Omega stages
+constexpr int kTaThreads = 32 * (2 + kTaGen + kTaWork);
+static_assert(kTaGen % 4 == 0 && kTaWork % 4 == 0, "TA warp roles");
+
+struct SketchTaParams {
+  int64_t I, C, cps;
+  int ng, RG, NTg, nbox, BR, NSS, NSA;
+  int gsplit;            // Omega generator groups (stages round-robin over the groups)
+  int ell;
+  int64_t k0;
+  uint64_t seed;
+  int mode;
+  int64_t col_offset;
+  double *partial;       // [C ranges][ell][I]
+  double *norm_partial;  // [grid] or null
+  uint32_t *colmax;      // [C] or null
+  long long *prof;       // optional: CTA 0 wait-cycle counters (RTUCKER_TA_PROF)
+};
+
+__device__ __forceinline__ void mma_tf32_ta(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+               "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d), "r"(a_tmem), "l"(b),
+               "r"(idesc), "r"(acc)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
+template <int N>
+__global__ void __launch_bounds__(kTaThreads, 1)
+    sketch_tc_ta_kernel(const __grid_constant__ CUtensorMap tmap, const SketchTaParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
+  unsigned char *base = smem_raw + pad;
+  const int NSS = p.NSS, NSA = p.NSA, NTg = p.NTg, BR = p.BR;
+  const int sbytes = p.nbox * BR * kBK * 4;
+  constexpr int obytes = N * kBK * 4;
+  unsigned char *ohb = base;                          // [kTaNSG][obytes]
+  unsigned char *olb = ohb + (size_t)kTaNSG * obytes; // [kTaNSG][obytes]
+  unsigned char *sb = olb + (size_t)kTaNSG * obytes;  // [NSS][sbytes]
+  uint64_t *full = (uint64_t *)(sb + (size_t)NSS * sbytes);
+  uint64_t *sfree = full + NSS;
+  uint64_t *aready = sfree + NSS;
+  uint64_t *aempty = aready + NSA;
+  uint64_t *oready = aempty + NSA;
+  uint64_t *oempty = oready + kTaNSG;
+  uint64_t *done = oempty + kTaNSG;
+  uint32_t *tslot = (uint32_t *)(done + 1);
+  double *wsum = (double *)(tslot + 2);  // [kTaWork]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int grp = blockIdx.x % p.ng, cr = blockIdx.x / p.ng;
+  const int64_t row0 = (int64_t)grp * p.RG;
+  const int rvalid = (int)min((int64_t)p.RG, p.I - row0);
+  const int64_t cbeg = (int64_t)cr * p.cps;
+  const int64_t cend = min(p.C, cbeg + p.cps);
+  const int nst = cend > cbeg ? (int)((cend - cbeg + kBK - 1) / kBK) : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSS; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&sfree[s], 32 * kTaWork);
+    }
+    for (int s = 0; s < NSA; ++s) {
+      tc::mbar_init(&aready[s], 32 * kTaWork);
+      tc::mbar_init(&aempty[s], 1);
+    }
+    for (int s = 0; s < kTaNSG; ++s) {
+      tc::mbar_init(&oready[s], 32 * kTaGen / p.gsplit);
+      tc::mbar_init(&oempty[s], 1);
+    }
+    tc::mbar_init(done, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, 512);
+  for (int e = threadIdx.x; e < 2 * kTaNSG * obytes / 4; e += kTaThreads) ((float *)ohb)[e] = 0.f;
+  tc::fence_proxy_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------- TMA producer
+    if (lane == 0 && nst > 0) {
+      tc::tma_prefetch_desc(&tmap);
+      const int boxb = BR * kBK * 4;
+      for (int it = 0; it < nst; ++it) {
+        const int s = it % NSS;
+        if (it >= NSS) tc::mbar_wait(&sfree[s], ((it / NSS) & 1) ^ 1);
+        tc::mbar_arrive_expect_tx(&full[s], (uint32_t)sbytes);
+        const int c0 = (int)(cbeg + (int64_t)it * kBK);
+        unsigned char *dst = sb + (size_t)s * sbytes;
+        for (int b = 0; b < p.nbox; ++b) tc::tma_load_2d(dst + b * boxb, &tmap, &full[s], (int)row0 + BR * b, c0);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------- MMA issuer (warp-wide)
+    if (nst > 0) {
+      constexpr uint32_t idesc = tc::idesc_tf32(128, N, false, false);
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint32_t obh = __shfl_sync(0xffffffffu, tc::smem_u32(ohb), 0);
+      const uint32_t obl = __shfl_sync(0xffffffffu, tc::smem_u32(olb), 0);
+      long long w0 = 0, w1 = 0, w2 = 0;
+      for (int it = 0; it < nst; ++it) {
+        const int s = it % NSA, g = it % kTaNSG;
+        const long long c0 = clock64();
+        tc::mbar_wait(&oready[g], (it / kTaNSG) & 1);
+        const long long c1 = clock64();
+        tc::mbar_wait(&aready[s], (it / NSA) & 1);
+        const long long c2 = clock64();
+        w0 += c1 - c0; w1 += c2 - c1;
+        tc::tc_fence_after();
+        const uint64_t bh = tc::smem_desc(obh + g * obytes, 128, 256, tc::kSwNone);
+        const uint64_t bl = tc::smem_desc(obl + g * obytes, 128, 256, tc::kSwNone);
+        const uint32_t a0 = tm + kTaCol + 16 * s * NTg;
+        for (int t = 0; t < NTg; ++t) {
+          const uint32_t d = tm + t * N, ah = a0 + 16 * t;
+          tc::mma_tf32_ta_w(d, ah, bh, idesc, it > 0 ? 1u : 0u);
+          tc::mma_tf32_ta_w(d, ah, bl, idesc, 1u);
+          tc::mma_tf32_ta_w(d, ah + 8, bh, idesc, 1u);
+        }
+        tc::mma_commit_w(&aempty[s]);
+        tc::mma_commit_w(&oempty[g]);
+        w2 += clock64() - c2;
+      }
+      tc::mma_commit_w(done);
+      if (p.prof && blockIdx.x == 0 && lane == 0) { p.prof[0] = w0; p.prof[1] = w1; p.prof[2] = w2; p.prof[3] = nst; }
+    }
+  } else if (warp < 2 + kTaGen) {
+    // ------------------------------------------------------------- Omega generators
+    // group gg = 0 / 1 of 4 warps fills the even / odd stages
+    const int gsz = 32 * kTaGen / p.gsplit;
+    const int gg = (threadIdx.x - 64) / gsz, gt = threadIdx.x - 64 - gsz * gg;
+    const int64_t jb0 = p.k0 >> 2;
+    const int nb = (int)(((p.k0 + p.ell - 1) >> 2) - jb0 + 1);
+    for (int it = gg; it < nst; it += p.gsplit) {
+      const int g = it % kTaNSG;
+      const int64_t c0 = cbeg + (int64_t)it * kBK;
+      if (it >= kTaNSG) tc::mbar_wait(&oempty[g], ((it / kTaNSG) & 1) ^ 1);
+      float *oh = (float *)(ohb + (size_t)g * obytes), *ol = (float *)(olb + (size_t)g * obytes);
+      for (int t = gt; t < kBK * nb; t += gsz) {
+        const int kk = t & (kBK - 1), jb = t >> 3;
+        const int64_t c = c0 + kk;
+        const bool valid = c < cend;
+        const uint4 w = omega_words(p.seed, p.mode, 0, (uint64_t)(c + p.col_offset), (uint32_t)(jb0 + jb));
+        Normal4<float> z(w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t n = 4 * (jb0 + jb) + q - p.k0;
+          if (n >= 0 && n < p.ell) {
+            const float v = valid ? z.v[q] : 0.f;
+            const float hi = tc::tf32_hi(v);
+            const int off = kmaj_off((int)n, kk) >> 2;
+            oh[off] = hi;
+            ol[off] = tc::tf32_lo(v, hi);
+          }
+        }
+      }
+      tc::fence_proxy_async_smem();
+      tc::mbar_arrive(&oready[g]);
+    }
+  } else {
+    // ------------------------------------------------------------- X workers
+    const int q = warp & 3, hw = (warp - 2 - kTaGen) >> 2;
+    const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+    int soff[kTaTpw];
+    bool rok[kTaTpw];
+#pragma unroll
+    for (int u = 0; u < kTaTpw; ++u) {
+      const int t = hw + kTaWq * u;
+      const int r = 128 * t + 32 * q + lane;
+      rok[u] = t < NTg && r < rvalid;
+      soff[u] = (r / BR) * (BR * kBK) + r % BR;
+    }
+    float acc = 0.f;
+    double nsq = 0.0;
+    int ss = 0, sa = 0;
+    uint32_t ps = 0, pa = 0;
+    long long w3 = 0, w4 = 0, tw0 = clock64();
+    for (int it = 0; it < nst; ++it) {
+      const long long c0 = clock64();
+      if (it >= NSA) tc::mbar_wait(&aempty[sa], pa ^ 1);
+      const long long c1 = clock64();
+      tc::mbar_wait(&full[ss], ps);
+      w3 += c1 - c0; w4 += clock64() - c1;
+      tc::tc_fence_after();
+      const float *st = (const float *)(sb + (size_t)ss * sbytes);
+      float cm[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) cm[u] = 0.f;
+#pragma unroll
+      for (int u = 0; u < kTaTpw; ++u) {
+        const int t = hw + kTaWq * u;
+        if (t < NTg) {  // warp-uniform
+          float x[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) x[k] = rok[u] ? st[soff[u] + k * BR] : 0.f;
+          uint32_t v[16];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const float h = tc::tf32_hi(x[k]);
+            v[k] = __float_as_uint(h);
+            v[8 + k] = __float_as_uint(tc::tf32_lo(x[k], h));
+            acc = fmaf(x[k], x[k], acc);
+            cm[k] = fmaxf(cm[k], fabsf(x[k]));
+          }
+          tmem_st16(tmem + lane_base + kTaCol + 16 * (sa * NTg + t), v);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      tc::mbar_arrive(&sfree[ss]);
+      tc::tc_fence_before();
+      tc::mbar_arrive(&aready[sa]);
+      if (p.colmax) {  // transposing butterfly (see sketch_tc_mn_kernel)
+        const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float keep = u16 ? cm[k + 4] : cm[k], send = u16 ? cm[k] : cm[k + 4];
+          cm[k] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const float keep = u8 ? cm[k + 2] : cm[k], send = u8 ? cm[k] : cm[k + 2];
+          cm[k] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+        }
+        {
+          const float keep = u4 ? cm[1] : cm[0], send = u4 ? cm[0] : cm[1];
+          cm[0] = fmaxf(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+        }
+        cm[0] = fmaxf(cm[0], __shfl_xor_sync(0xffffffffu, cm[0], 2));
+        cm[0] = fmaxf(cm[0], __shfl_xor_sync(0xffffffffu, cm[0], 1));
+        const int64_t c = cbeg + (int64_t)it * kBK + (lane >> 2);
+        if ((lane & 3) == 0 && c < cend) atomicMax(p.colmax + c, __float_as_uint(cm[0]));
+      }
+      nsq += (double)acc;
+      acc = 0.f;
+      if (++sa == NSA) { sa = 0; pa ^= 1; }
+      if (++ss == NSS) { ss = 0; ps ^= 1; }
+    }
+    if (p.prof && blockIdx.x == 0 && threadIdx.x == 32 * (2 + kTaGen)) {
+      p.prof[4] = w3; p.prof[5] = w4; p.prof[6] = clock64() - tw0;
+    }
+    // ---- epilogue: TMEM -> fp64 partial[cr][k * I + i]
+    if (nst > 0) {
+      tc::mbar_wait(done, 0);
+      tc::tc_fence_after();
+    }
+    double *dst = p.partial + (int64_t)cr * p.ell * p.I;
+    for (int t = hw; t < NTg; t += kTaWq) {
+      for (int h = 0; h * 32 < N; ++h) {
+        uint32_t rr[32];
+        if (nst > 0) tc::tmem_ld32(tmem + lane_base + t * N + h * 32, rr);
+        const int r = 128 * t + 32 * q + lane;
+        if (r < rvalid) {
+          const int64_t i = row0 + r;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int k = h * 32 + j;
+            if (k < p.ell) dst[(int64_t)k * p.I + i] = nst > 0 ? (double)__uint_as_float(rr[j]) : 0.0;
+          }
+        }
+      }
+    }
+    if (p.norm_partial) {
+      for (int o = 16; o; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
+      if (lane == 0) wsum[warp - 2 - kTaGen] = nsq;
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (p.norm_partial && threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kTaWork; ++w) s += wsum[w];
+    p.norm_partial[blockIdx.x] = s;
+  }
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, 512);
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -339,6 +672,80 @@ __global__ void reduce_partials_kernel(const double *__restrict__ partial, int n
     for (int k = 0; k < nsplit; ++k) s += partial[(int64_t)k * n + e];
     Y[e] = s;
   }
+}
+
+template <int N>
+void launch_ta(Ctx &c, const CUtensorMap &tm, SketchTaParams &p, int grid, size_t smem) {
+  auto k = sketch_tc_ta_kernel<N>;
+  RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  RT_LAUNCH(c, k, grid, kTaThreads, smem, tm, p);
+}
+
+// L == 1 sketch with the A operand in TMEM (sketch_tc_ta_kernel).
+bool sketch_ta(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0, uint64_t seed, int64_t col_offset,
+               double *Y, double *normsq, uint32_t *colmax) {
+  const int N = ell <= 32 ? 32 : 64;
+  const int NT = (int)((v.I + 127) / 128);
+  SketchTaParams p{};
+  p.I = v.I;
+  p.C = v.R;
+  p.ng = (NT + 3) / 4;
+  p.RG = (int)(((v.I + p.ng - 1) / p.ng + 7) / 8 * 8);
+  p.NTg = (p.RG + 127) / 128;
+  p.nbox = (p.RG + 255) / 256;
+  p.BR = ((p.RG + p.nbox - 1) / p.nbox + 7) / 8 * 8;
+  p.NSA = std::min(4, (512 - kTaCol) / (16 * p.NTg));
+  p.gsplit = kTaGen / 4;
+  static const bool prof = getenv("RTUCKER_TA_PROF") != nullptr;
+  DevBuf<long long> pbuf;
+  if (prof) {
+    pbuf.alloc(c, 8);
+    RT_CUDA(cudaMemsetAsync(pbuf.p, 0, 64, c.stream));
+    p.prof = pbuf.p;
+  }
+  const size_t sbytes = (size_t)p.nbox * p.BR * kBK * 4, obytes = (size_t)N * kBK * 4;
+  const size_t budget = 200 * 1024, fixed = 1024 + 2 * kTaNSG * obytes + 512;
+  p.NSS = (int)std::min<size_t>(8, (budget - fixed) / sbytes);
+  if (p.NSS < 2) return false;
+  const size_t smem = fixed + p.NSS * sbytes;
+  const int64_t nchunks = (p.C + kBK - 1) / kBK;
+  const int ncr = (int)std::max<int64_t>(1, std::min<int64_t>(c.num_sms / p.ng, nchunks / 4));
+  p.cps = ((nchunks + ncr - 1) / ncr) * kBK;
+  const int ncr_used = (int)((p.C + p.cps - 1) / p.cps);
+  const int grid = ncr_used * p.ng;
+  p.ell = ell;
+  p.k0 = k0;
+  p.seed = seed;
+  p.mode = mode;
+  p.col_offset = col_offset;
+  DevBuf<double> part(c, (size_t)ncr_used * ell * v.I);
+  DevBuf<double> npart;
+  if (normsq) npart.alloc(c, grid);
+  p.partial = part.p;
+  p.norm_partial = normsq ? npart.p : nullptr;
+  p.colmax = colmax;
+  CUtensorMap tm;
+  cuuint64_t dims[2] = {(cuuint64_t)v.I, (cuuint64_t)p.C};
+  cuuint64_t strides[1] = {(cuuint64_t)v.I * 4};
+  cuuint32_t box[2] = {(cuuint32_t)p.BR, kBK};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)X, dims, strides, box, es,
+                                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Error(RTUCKER_ECUDA, "cuTensorMapEncodeTiled failed for the sketch operand");
+  if (N == 32) launch_ta<32>(c, tm, p, grid, smem);
+  else launch_ta<64>(c, tm, p, grid, smem);
+  if (prof) {
+    long long h[8];
+    RT_CUDA(cudaMemcpyAsync(h, pbuf.p, 64, cudaMemcpyDeviceToHost, c.stream));
+    RT_CUDA(cudaStreamSynchronize(c.stream));
+    fprintf(stderr, "[ta prof] nst %lld  mma: wait oready %lld aready %lld issue %lld | worker: wait aempty %lld full %lld total %lld\n",
+            h[3], h[0], h[1], h[2], h[4], h[5], h[6]);
+  }
+  const int64_t n = v.I * ell;
+  RT_LAUNCH(c, reduce_partials_kernel, (int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, part.p, ncr_used, n, Y);
+  if (normsq) sum_vec(c, npart.p, grid, normsq);
+  return true;
 }
 
 template <int N, bool KM>
@@ -367,6 +774,9 @@ bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t
   const bool km = v.L > 1;  // K-major variant: l contiguous (5-D TMA box, no transposition)
   if (!km && (v.I % 4) != 0) return false;
   if (km && ((v.L % 8) != 0 || (v.I % 8) != 0 || v.I / 8 > 256)) return false;
+  static const bool ta = getenv("RTUCKER_SKETCH_TA") != nullptr;  // TMEM-A variant (experimental)
+  if (!km && ta && (((uintptr_t)X) & 15) == 0 && v.I <= 2048 && v.L * v.R <= (int64_t)INT32_MAX - 64)
+    return sketch_ta(c, X, v, mode, ell, k0, seed, col_offset, Y, normsq, colmax);
   const int N = ell <= 32 ? 32 : 64;
   const int NT = (int)((v.I + 127) / 128);
   if (NT * N > 512 || (((uintptr_t)X) & 15) != 0) return false;

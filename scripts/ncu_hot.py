@@ -1,9 +1,10 @@
 """Summarise an ncu --set full capture's source page: samples per 1 KB SASS region and the
-hottest instructions with their top stall reasons.  usage: ncu_hot.py report.ncu-rep [N]"""
+hottest instructions with their top stall reasons.  usage: ncu_hot.py report.ncu-rep [N] [kernel-regex]"""
 import csv, io, subprocess, sys
 rep = sys.argv[1]
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+kf = sys.argv[3:] and ["--kernel-name", "regex:" + sys.argv[3]] or []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"] + kf, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))[1:]
 h = rows[0]; ci = {k: i for i, k in enumerate(h)}; data = rows[1:]
 stalls = [k for k in h if k.startswith("stall_") and "Not Issued" not in k]
