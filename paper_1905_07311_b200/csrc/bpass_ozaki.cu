@@ -53,7 +53,8 @@ constexpr int kONQ = 3;        // Q slice ring depth
 constexpr int kOSlicers = 8;   // slicer warps
 constexpr int kOEpi = 4;       // epilogue warps
 constexpr int kOThreads = 32 * (2 + kOSlicers + kOEpi + 1);  // + the Q producer warp
-constexpr int kOTS = 65;       // epilogue tile stride (doubles): row-per-lane stores conflict-free
+constexpr int kOTP = 132;      // epilogue tile T[j][p] stride (doubles, = 4 mod 16): lane-per-p
+                               // rows and the DMMA Gram fragments both conflict-free
 constexpr int kXStB = kOP * kOK * 4;         // staging bytes per chunk (16 KB)
 constexpr int kQChB = kOS * kON * kOK;       // pre-sliced Q bytes per chunk (10 KB)
 
@@ -200,8 +201,8 @@ __global__ void __launch_bounds__(kOThreads, 1)
   unsigned char *base = ozs + pad;
   unsigned char *stg = base;                             // [kONSS][16 KB] fp32 X boxes (128B swizzle)
   unsigned char *qb = stg + kONSS * kXStB;               // [kONQ][10 KB] Q slices
-  double *T = reinterpret_cast<double *>(qb + kONQ * kQChB);  // [128][kOTS]
-  uint64_t *full = reinterpret_cast<uint64_t *>(T + kOP * kOTS);  // X stage landed
+  double *T = reinterpret_cast<double *>(qb + kONQ * kQChB);  // [64 j][kOTP] (p = 0 .. 127)
+  uint64_t *full = reinterpret_cast<uint64_t *>(T + kON * kOTP);  // X stage landed
   uint64_t *sfree = full + kONSS;                        // X stage consumed by the slicers
   uint64_t *qfull = sfree + kONSS, *qfree = qfull + kONQ;
   uint64_t *xready = qfree + kONQ, *xempty = xready + kOXB;
@@ -400,45 +401,36 @@ __global__ void __launch_bounds__(kOThreads, 1)
           for (int j = 0; j < 32; ++j) S[j] = (L == 0 ? 0ll : (S[j] << 7)) + (long long)(int)r[j];
         }
 #pragma unroll
-        for (int j = 0; j < 32; ++j) Ti[row * kOTS + 32 * h + j] = S[j];
+        for (int j = 0; j < 32; ++j) Ti[(32 * h + j) * kOTP + row] = S[j];
       }
       tc::tc_fence_before();
       tc::mbar_arrive(accempty);  // the MMA warp may overwrite the accumulators
       OZP(const long long c2 = clock64(); e1 += c2 - c1;)
-      // phase 2: B_jp = S 2^{e_p - 40} 2^{f_j} (level weights 2^{2 - 7 (L + 2)}, L = 0 .. 4)
+      // phase 2: B_jp = S 2^{e_p - 40} 2^{f_j} (level weights 2^{2 - 7 (L + 2)}, L = 0 .. 4),
+      // kept in T (fp64, in place) for the Gram and stored straight to B = out[p J + j]: a row
+      // of B is one thread's 60 contiguous doubles (16-byte stores; L2 merges the sectors)
       const int ep = pp < p.P ? exp_of(p.cm[pp]) : 0;
       const double rs = pow2d(ep - 40);
-#pragma unroll 8
-      for (int jj = 0; jj < kON; ++jj) {
-        const long long Sv = Ti[row * kOTS + jj];
-        T[row * kOTS + jj] = (pp < p.P && jj < p.J) ? (double)Sv * rs * fpw[jj] : 0.0;
-      }
-      named_bar(1, 32 * kOEpi);
-      OZP(const long long c3 = clock64(); e2 += c3 - c2;)
-      const int64_t ncol = p.P - p0 < kOP ? p.P - p0 : kOP;
-      if (p.out && ncol > 0) {  // B tile (J x ncol) is one contiguous range out[p0 J ..]
-        double *dst = p.out + p0 * p.J;
-        const int ne = (int)ncol * p.J;
-        if ((p.J & 1) == 0) {  // pairs (j, j + 1) of one column: 16-byte stores, no division
-          const int st = 2 * 32 * kOEpi, sp = st / p.J, sj = st - sp * p.J;
-          int pr = (2 * et) / p.J, j = 2 * et - pr * p.J;
-          for (int e = 2 * et; e < ne; e += st) {
-            *reinterpret_cast<double2 *>(dst + e) = make_double2(T[pr * kOTS + j], T[pr * kOTS + j + 1]);
-            pr += sp;
-            j += sj;
-            if (j >= p.J) { j -= p.J; ++pr; }
-          }
-        } else {
-          const int st = 32 * kOEpi, sp = st / p.J, sj = st - sp * p.J;
-          int pr = et / p.J, j = et - pr * p.J;
-          for (int e = et; e < ne; e += st) {
-            dst[e] = T[pr * kOTS + j];
-            pr += sp;
-            j += sj;
-            if (j >= p.J) { j -= p.J; ++pr; }
+      const bool pok = pp < p.P;
+      double *orow = p.out ? p.out + pp * p.J : nullptr;
+      const bool vec = (p.J & 1) == 0;
+#pragma unroll 4
+      for (int jj = 0; jj < kON; jj += 2) {
+        const double v0 = (pok && jj < p.J) ? (double)Ti[jj * kOTP + row] * rs * fpw[jj] : 0.0;
+        const double v1 = (pok && jj + 1 < p.J) ? (double)Ti[(jj + 1) * kOTP + row] * rs * fpw[jj + 1] : 0.0;
+        T[jj * kOTP + row] = v0;
+        T[(jj + 1) * kOTP + row] = v1;
+        if (orow && pok) {
+          if (vec) {
+            if (jj < p.J) *reinterpret_cast<double2 *>(orow + jj) = make_double2(v0, v1);
+          } else {
+            if (jj < p.J) orow[jj] = v0;
+            if (jj + 1 < p.J) orow[jj + 1] = v1;
           }
         }
       }
+      named_bar(1, 32 * kOEpi);
+      OZP(const long long c3 = clock64(); e2 += c3 - c2;)
       OZP(const long long c4 = clock64(); e3 += c4 - c3;)
       if (p.gram_partial) {  // G += T^T T, 36 upper 8x8 tiles over the 4 epilogue warps
         const int fr = lane >> 2, fc = lane & 3;
@@ -453,16 +445,16 @@ __global__ void __launch_bounds__(kOThreads, 1)
             const int t = ew + 4 * (u0 + v);
             int a = 0, rem = t;
             while (rem >= 8 - a) { rem -= 8 - a; ++a; }
-            oa[v] = fc * kOTS + 8 * a + fr;
-            ob[v] = fc * kOTS + 8 * (a + rem) + fr;
+            oa[v] = (8 * a + fr) * kOTP + fc;
+            ob[v] = (8 * (a + rem) + fr) * kOTP + fc;
           }
 #pragma unroll 4
           for (int k0 = 0; k0 < kOP; k0 += 4) {
 #pragma unroll
-            for (int v = 0; v < 3; ++v)
-              asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+            for (int v = 0; v < 3; ++v)  // non-volatile: pure register op, freely scheduled
+              asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                            : "+d"(gacc[u0 + v][0]), "+d"(gacc[u0 + v][1])
-                           : "d"(T[oa[v] + k0 * kOTS]), "d"(T[ob[v] + k0 * kOTS]));
+                           : "d"(T[oa[v] + k0]), "d"(T[ob[v] + k0]));
           }
         }
       }
@@ -540,7 +532,6 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
   const int64_t ntiles = (P + kOP - 1) / kOP;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, c.num_sms));
   DevBuf<double> part;
-  if (gram) part.alloc(c, (size_t)grid * 4096);
   OzParams prm{};
   prm.I = I;
   prm.P = P;
@@ -550,7 +541,13 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
   prm.cm = colmax;
   prm.f = fexp.p;
   prm.out = out;
-  prm.gram_partial = gram ? part.p : nullptr;
+  // Gram of B in the epilogue (DMMA, 36 upper 8x8 tiles per 128-column tile).  The alternative,
+  // a separate pass over B (gram64_kernel, RTUCKER_OZ_GRAM_SEPARATE), measured slower at C4
+  // (B-pass + Gram 1.37 vs 0.82 ms).
+  static const bool gsep_env = getenv("RTUCKER_OZ_GRAM_SEPARATE") != nullptr;
+  const bool gsep = gram && out && gsep_env;
+  if (gram && !gsep) part.alloc(c, (size_t)grid * 4096);
+  prm.gram_partial = (gram && !gsep) ? part.p : nullptr;
   CUtensorMap tm;
   cuuint64_t dims[2] = {(cuuint64_t)I, (cuuint64_t)P};
   cuuint64_t strides[1] = {(cuuint64_t)I * 4};
@@ -560,7 +557,7 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
                                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Error(RTUCKER_ECUDA, "cuTensorMapEncodeTiled failed for the Ozaki B-pass");
-  const size_t smem = 1024 + (size_t)kONSS * kXStB + (size_t)kONQ * kQChB + sizeof(double) * kOP * kOTS +
+  const size_t smem = 1024 + (size_t)kONSS * kXStB + (size_t)kONQ * kQChB + sizeof(double) * kON * kOTP +
                       8 * (2 * kONSS + 2 * kONQ + 2 * kOXB + 2) + 16 + 8 * kON;
   RT_CUDA(cudaFuncSetAttribute(bpass_ozaki_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   static const bool prof = getenv("RTUCKER_OZ_PROF") != nullptr;
@@ -580,7 +577,8 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
             "xempty %lld total %lld | epi: wait accfull %lld ph1 %lld ph2 %lld store %lld gram %lld total %lld\n",
             h[15], h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[10], h[11], h[12]);
   }
-  if (gram) RT_LAUNCH(c, oz_gram_reduce_kernel, (J * J + 127) / 128, 128, 0, part.p, grid, J, gram);
+  if (gsep) mode_gram(c, out, DT::F64, ModeView{1, J, P}, gram);
+  else if (gram) RT_LAUNCH(c, oz_gram_reduce_kernel, (J * J + 127) / 128, 128, 0, part.p, grid, J, gram);
   return true;
 }
 

@@ -111,29 +111,33 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------- MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------- MMA issuer (warp-wide)
+    {
       constexpr uint32_t idesc = tc::idesc_tf32(128, 64, false, false);
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint32_t xb0 = __shfl_sync(0xffffffffu, tc::smem_u32(xb), 0);
+      const uint32_t lb0 = __shfl_sync(0xffffffffu, tc::smem_u32(lb), 0);
+      const uint32_t qb0 = __shfl_sync(0xffffffffu, tc::smem_u32(qb), 0);
       for (int64_t it = 0; it < nst; ++it) {
         const int s = (int)(it % kNS);
         const int ab = (int)(it & 1);          // accumulator buffer
         if (it >= 2) tc::mbar_wait(&accempty[ab], (uint32_t)(((it / 2) & 1) ^ 1));
         tc::mbar_wait(&ready[s], (uint32_t)((it / kNS) & 1));
         tc::tc_fence_after();
-        const uint32_t xa = tc::smem_u32(xb + s * kXBytes), la = tc::smem_u32(lb + s * kXBytes);
-        const uint32_t qh = tc::smem_u32(qb + s * 2 * kQBytes), ql = qh + kQBytes;
-        const uint32_t d = tmem + ab * 64;
+        const uint32_t xa = xb0 + s * kXBytes, la = lb0 + s * kXBytes;
+        const uint32_t qh = qb0 + s * 2 * kQBytes, ql = qh + kQBytes;
+        const uint32_t d = tm + ab * 64;
         for (int ks = 0; ks < kKC / 8; ++ks) {
           const uint64_t ah = tc::smem_desc(xa + ks * 256, 128, 1024, tc::kSwNone);
           const uint64_t al = tc::smem_desc(la + ks * 256, 128, 1024, tc::kSwNone);
           const uint64_t bh = tc::smem_desc(qh + ks * 256, 128, 1024, tc::kSwNone);
           const uint64_t bl = tc::smem_desc(ql + ks * 256, 128, 1024, tc::kSwNone);
-          tc::mma_tf32(d, ah, bh, idesc, ks ? 1u : 0u);
-          tc::mma_tf32(d, ah, bl, idesc, 1u);
-          tc::mma_tf32(d, al, bh, idesc, 1u);
+          tc::mma_tf32_w(d, ah, bh, idesc, ks ? 1u : 0u);
+          tc::mma_tf32_w(d, ah, bl, idesc, 1u);
+          tc::mma_tf32_w(d, al, bh, idesc, 1u);
         }
-        tc::mma_commit(&empty[s]);
-        tc::mma_commit(&accfull[ab]);
+        tc::mma_commit_w(&empty[s]);
+        tc::mma_commit_w(&accfull[ab]);
       }
     }
   } else if (warp < 2 + kEpi) {
