@@ -373,6 +373,7 @@ struct SketchTaParams {
   int64_t I, C, cps;
   int ng, RG, NTg, nbox, BR, NSS, NSA;
   int gsplit;            // Omega generator groups (stages round-robin over the groups)
+  int acol;              // first TMEM column of the A ring (= NTg N)
   int ell;
   int64_t k0;
   uint64_t seed;
@@ -486,7 +487,7 @@ __global__ void __launch_bounds__(kTaThreads, 1)
         tc::tc_fence_after();
         const uint64_t bh = tc::smem_desc(obh + g * obytes, 128, 256, tc::kSwNone);
         const uint64_t bl = tc::smem_desc(obl + g * obytes, 128, 256, tc::kSwNone);
-        const uint32_t a0 = tm + kTaCol + 16 * s * NTg;
+        const uint32_t a0 = tm + p.acol + 16 * s * NTg;
         for (int t = 0; t < NTg; ++t) {
           const uint32_t d = tm + t * N, ah = a0 + 16 * t;
           tc::mma_tf32_ta_w(d, ah, bh, idesc, it > 0 ? 1u : 0u);
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(kTaThreads, 1)
             acc = fmaf(x[k], x[k], acc);
             cm[k] = fmaxf(cm[k], fabsf(x[k]));
           }
-          tmem_st16(tmem + lane_base + kTaCol + 16 * (sa * NTg + t), v);
+          tmem_st16(tmem + lane_base + p.acol + 16 * (sa * NTg + t), v);
         }
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -690,11 +691,13 @@ bool sketch_ta(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0
   p.I = v.I;
   p.C = v.R;
   p.ng = (NT + 3) / 4;
+  if (const char *e = getenv("RTUCKER_TA_NG")) p.ng = std::max(p.ng, atoi(e));  // experiments
   p.RG = (int)(((v.I + p.ng - 1) / p.ng + 7) / 8 * 8);
   p.NTg = (p.RG + 127) / 128;
   p.nbox = (p.RG + 255) / 256;
   p.BR = ((p.RG + p.nbox - 1) / p.nbox + 7) / 8 * 8;
-  p.NSA = std::min(4, (512 - kTaCol) / (16 * p.NTg));
+  p.acol = p.NTg * N;
+  p.NSA = std::min(8, (512 - p.acol) / (16 * p.NTg));
   p.gsplit = kTaGen / 4;
   static const bool prof = getenv("RTUCKER_TA_PROF") != nullptr;
   DevBuf<long long> pbuf;
