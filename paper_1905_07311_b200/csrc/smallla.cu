@@ -469,7 +469,7 @@ __device__ __forceinline__ void jac_angle(double a, double b, double g, double &
   s = t * c;
 }
 
-template <int kV>
+template <int kV, int LPS>
 __device__ __forceinline__ void jac_pair(double (&x)[kV], double (&y)[kV], double tol2, int &rot) {
   double g0 = 0.0, g1 = 0.0, a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
 #pragma unroll
@@ -483,7 +483,7 @@ __device__ __forceinline__ void jac_pair(double (&x)[kV], double (&y)[kV], doubl
   }
   double g = g0 + g1, a = a0 + a1, b = b0 + b1;
 #pragma unroll
-  for (int o = 1; o <= 2; o <<= 1) {  // the slot's 4 lanes; identical sums in all of them
+  for (int o = 1; o < LPS; o <<= 1) {  // the slot's LPS lanes; identical sums in all of them
     g += __shfl_xor_sync(0xffffffffu, g, o);
     a += __shfl_xor_sync(0xffffffffu, a, o);
     b += __shfl_xor_sync(0xffffffffu, b, o);
@@ -505,7 +505,7 @@ __device__ __forceinline__ void jac_pair(double (&x)[kV], double (&y)[kV], doubl
 // slot owning column p passes (own = m_p, oth = m_q, own_is_p = true), the slot owning q the
 // mirror; the sums are formed in the same order on both (x*y == y*x exactly), so both take
 // the identical rotation and each updates its own column only.
-template <int kV>
+template <int kV, int LPS>
 __device__ __forceinline__ void jac_half(double (&own)[kV], const double (&oth)[kV], bool own_is_p, double tol2,
                                          int &rot) {
   double g0 = 0.0, g1 = 0.0, o0 = 0.0, o1 = 0.0, t0 = 0.0, t1 = 0.0;
@@ -520,7 +520,7 @@ __device__ __forceinline__ void jac_half(double (&own)[kV], const double (&oth)[
   }
   double g = g0 + g1, so = o0 + o1, st = t0 + t1;
 #pragma unroll
-  for (int o = 1; o <= 2; o <<= 1) {
+  for (int o = 1; o < LPS; o <<= 1) {
     g += __shfl_xor_sync(0xffffffffu, g, o);
     so += __shfl_xor_sync(0xffffffffu, so, o);
     st += __shfl_xor_sync(0xffffffffu, st, o);
@@ -540,15 +540,16 @@ __device__ __forceinline__ void jac_half(double (&own)[kV], const double (&oth)[
   }
 }
 
-template <int kV>
+template <int kV, int LPS>
 __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restrict__ Ain, int n, double *__restrict__ w,
                                                           double *__restrict__ Vout, double tol, int max_sweeps,
                                                           int *__restrict__ info, int r_need, int *__restrict__ refine) {
   extern __shared__ double gsm2[];
+  constexpr int SPW = 32 / LPS;        // column slots per warp = block size
   const int np = n + (n & 1);
-  const int nb = ((n + 15) / 16) * 2;  // column blocks of 8 (even count)
-  const int ncol = 8 * nb;
-  constexpr int ldm = 4 * kV + 4;      // = 4 mod 16 (kV in {4, 8, 16}): conflict-free slot loads
+  const int nb = ((n + 2 * SPW - 1) / (2 * SPW)) * 2;  // column blocks of SPW (even count)
+  const int ncol = SPW * nb;
+  constexpr int ldm = LPS * kV + LPS;  // = LPS mod 16: conflict-free slot loads
   double *G = gsm2;                    // np x np working copy (column-major)
   double *M = G + np * np;             // ldm x ncol: P L, then M J
   double *lam = M + ldm * ncol;        // ncol
@@ -614,7 +615,7 @@ __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restri
   }
   // ---- block-ordered one-sided Jacobi on the columns of M
   const double tol2 = tol * tol;
-  const int slot = lane >> 2, q = lane & 3;
+  const int slot = lane / LPS, q = lane % LPS;
   const int nwk = nb / 2;  // working warps
   int sweeps = 0;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
@@ -622,13 +623,13 @@ __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restri
     __syncthreads();
     int rot = 0;
     if (warp < nwk) {  // pairs inside blocks 2w (x) and 2w + 1 (y): round m pairs slot k with k ^ m
-      double *c1 = M + ldm * (16 * warp + slot), *c2 = c1 + 8 * ldm;
+      double *c1 = M + ldm * (2 * SPW * warp + slot), *c2 = c1 + SPW * ldm;
       double x[kV], y[kV];
 #pragma unroll
-      for (int v = 0; v < kV; ++v) { x[v] = c1[q + 4 * v]; y[v] = c2[q + 4 * v]; }
+      for (int v = 0; v < kV; ++v) { x[v] = c1[q + LPS * v]; y[v] = c2[q + LPS * v]; }
 #pragma unroll 1
-      for (int m = 1; m < 8; ++m) {
-        const int src = ((slot ^ m) << 2) + q;
+      for (int m = 1; m < SPW; ++m) {
+        const int src = (slot ^ m) * LPS + q;
         const bool own_p = slot < (slot ^ m);
         double px[kV], py[kV];
 #pragma unroll
@@ -636,30 +637,30 @@ __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restri
           px[v] = __shfl_sync(0xffffffffu, x[v], src);
           py[v] = __shfl_sync(0xffffffffu, y[v], src);
         }
-        jac_half<kV>(x, px, own_p, tol2, rot);
-        jac_half<kV>(y, py, own_p, tol2, rot);
+        jac_half<kV, LPS>(x, px, own_p, tol2, rot);
+        jac_half<kV, LPS>(y, py, own_p, tol2, rot);
       }
 #pragma unroll
-      for (int v = 0; v < kV; ++v) { c1[q + 4 * v] = x[v]; c2[q + 4 * v] = y[v]; }
+      for (int v = 0; v < kV; ++v) { c1[q + LPS * v] = x[v]; c2[q + LPS * v] = y[v]; }
     }
     __syncthreads();
     for (int t = 0; t < nb - 1; ++t) {  // pairs between blocks
       if (warp < nwk) {
         int bA, bB;
         rr_pair(warp, t, nb, bA, bB);
-        double *c1 = M + ldm * (8 * bA + slot), *c2 = M + ldm * (8 * bB + slot);
+        double *c1 = M + ldm * (SPW * bA + slot), *c2 = M + ldm * (SPW * bB + slot);
         double x[kV], y[kV];
 #pragma unroll
-        for (int v = 0; v < kV; ++v) { x[v] = c1[q + 4 * v]; y[v] = c2[q + 4 * v]; }
-        const int nxt = ((slot + 1) & 7) * 4 + q;
+        for (int v = 0; v < kV; ++v) { x[v] = c1[q + LPS * v]; y[v] = c2[q + LPS * v]; }
+        const int nxt = ((slot + 1) % SPW) * LPS + q;
 #pragma unroll 1
-        for (int r = 0; r < 8; ++r) {
-          jac_pair<kV>(x, y, tol2, rot);
+        for (int r = 0; r < SPW; ++r) {
+          jac_pair<kV, LPS>(x, y, tol2, rot);
 #pragma unroll
           for (int v = 0; v < kV; ++v) y[v] = __shfl_sync(0xffffffffu, y[v], nxt);
         }
 #pragma unroll
-        for (int v = 0; v < kV; ++v) { c1[q + 4 * v] = x[v]; c2[q + 4 * v] = y[v]; }
+        for (int v = 0; v < kV; ++v) { c1[q + LPS * v] = x[v]; c2[q + LPS * v] = y[v]; }
       }
       __syncthreads();
     }
@@ -1019,17 +1020,31 @@ void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q, const 
 void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps, int r_need) {
   const int np = n + (n & 1);
   if (np > 64) return sym_eig(c, A, n, w, V, sweeps);
-  const int nb = ((n + 15) / 16) * 2, ncol = 8 * nb;
-  const int kv = np <= 16 ? 4 : (np <= 32 ? 8 : 16);
-  const int ldm = 4 * kv + 4;
+  // 4 lanes per column slot (blocks of 8 columns, nb / 2 busy warps).  RTUCKER_EIG_LPS8 (n > 32):
+  // 8 lanes (blocks of 4, all 8 warps busy, 8 rows per lane) measured no faster at n = 60
+  // (405 vs 412 us): a round is bound by its dependent latency chain (reductions, angle),
+  // not by the per-lane work.
+  static const bool lps8 = getenv("RTUCKER_EIG_LPS8") != nullptr;
+  const int lps = (np > 32 && lps8) ? 8 : 4, spw = 32 / lps;
+  const int nb = ((n + 2 * spw - 1) / (2 * spw)) * 2, ncol = spw * nb;
+  const int kv = (np + lps - 1) / lps <= 4 ? 4 : ((np + lps - 1) / lps <= 8 ? 8 : 16);
+  const int ldm = lps * kv + lps;
   const size_t need = sizeof(double) * ((size_t)np * np + (size_t)ldm * ncol + ncol + np) + sizeof(int) * np + 64;
   DevBuf<int> refine(c, 1);
   const double tol = 3e-15 * std::sqrt((double)n);
   const int rn = std::max(1, std::min(r_need, n));
-#define RT_GE(KV)                                                                                      \
-  RT_CUDA(cudaFuncSetAttribute(gram_eig_kernel<KV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need)); \
-  RT_LAUNCH(c, gram_eig_kernel<KV>, 1, kGramT, need, A, n, w, V, tol, 40, sweeps, rn, refine.p)
-  if (kv == 4) { RT_GE(4); } else if (kv == 8) { RT_GE(8); } else { RT_GE(16); }
+#define RT_GE(KV, L)                                                                                      \
+  RT_CUDA(cudaFuncSetAttribute(gram_eig_kernel<KV, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need)); \
+  RT_LAUNCH(c, (gram_eig_kernel<KV, L>), 1, kGramT, need, A, n, w, V, tol, 40, sweeps, rn, refine.p)
+  if (lps == 8) {
+    RT_GE(8, 8);
+  } else if (kv == 4) {
+    RT_GE(4, 4);
+  } else if (kv == 8) {
+    RT_GE(8, 4);
+  } else {
+    RT_GE(16, 4);
+  }
 #undef RT_GE
   sym_eig(c, A, n, w, V, nullptr, refine.p);  // no-op unless the gate asks for it
 }

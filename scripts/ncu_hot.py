@@ -5,8 +5,9 @@ rep = sys.argv[1]
 N = int(sys.argv[2]) if len(sys.argv) > 2 else 25
 kf = sys.argv[3:] and ["--kernel-name", "regex:" + sys.argv[3]] or []
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"] + kf, capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(out)))[1:]
-h = rows[0]; ci = {k: i for i, k in enumerate(h)}; data = rows[1:]
+rows = list(csv.reader(io.StringIO(out)))
+hi = next(i for i, r in enumerate(rows) if "# Samples" in r)
+h = rows[hi]; ci = {k: i for i, k in enumerate(h)}; data = [r for r in rows[hi + 1:] if len(r) == len(h) and r[0].startswith("0x")]
 stalls = [k for k in h if k.startswith("stall_") and "Not Issued" not in k]
 tot = sum(int(r[ci["# Samples"]]) for r in data)
 print("total samples", tot, "warp insts", sum(int(r[ci["Instructions Executed"]]) for r in data))
