@@ -13,6 +13,7 @@
 //                   column pair of the round-robin ordering, so a round needs a single CTA
 //                   barrier.
 //  canonical_signs  the sign convention of DESIGN reading R4b.
+#include <cstdio>
 #include <cooperative_groups.h>
 
 #include "kernels.h"
@@ -798,6 +799,14 @@ __global__ void __launch_bounds__(kCQT, 1) cholqr2_cluster_kernel(const double *
                                                                   int rows, int ldY, int ldG, int ldE,
                                                                   double *__restrict__ Q, int *__restrict__ bad) {
   extern __shared__ __align__(16) double cq[];
+#ifdef RTUCKER_CQ_PROF_BUILD
+  long long pt[12];
+  int np_ = 0;
+#define CQP() if (threadIdx.x == 0 && np_ < 12) pt[np_++] = clock64()
+#else
+#define CQP()
+#endif
+  CQP();
   cg::cluster_group cl = cg::this_cluster();
   const int ncta = (int)cl.num_blocks();
   const int me = (int)cl.block_rank();
@@ -817,6 +826,7 @@ __global__ void __launch_bounds__(kCQT, 1) cholqr2_cluster_kernel(const double *
     Yl[e] = (i < nloc && c < n) ? Y[r0 + i + m * c] : 0.0;
   }
   if (tid == 0) sbad = 0;
+  CQP();
   const int ri = tid >> 3, g = tid & 7;  // elimination ownership: row ri, columns g + 8u
   const unsigned gmask = 0xFFu << (8 * (ri & 3));
   const int kend = (nloc + 3) & ~3;      // slab rows past nloc are zero
@@ -843,22 +853,36 @@ __global__ void __launch_bounds__(kCQT, 1) cholqr2_cluster_kernel(const double *
       Gp[gi * ldG + gj] = c0; Gp[gi * ldG + gj + 1] = c1;
       if (a != b) { Gp[gj * ldG + gi] = c0; Gp[(gj + 1) * ldG + gi] = c1; }
     }
+    CQP();
     cluster_arrive();
     cluster_wait();
+    CQP();
     // ---- 2. cluster sum into registers (fixed CTA order)
     double gr[8], er[8], diag = 0.0;  // diag: running G[ri][ri], kept by its owner (g == ri % 8)
+    // all remote loads issued before the (fixed-order) sums: one DSMEM round trip, not 8 x 8
+    double rv[8][8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double *gq = cl.map_shared_rank(Gp, q < ncta ? q : 0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int j = g + 8 * u;
+        rv[q][u] = (q < ncta && ri < n && j < n) ? gq[ri * ldG + j] : 0.0;
+      }
+    }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int j = g + 8 * u;
       double s = 0.0;
-      if (ri < n && j < n)
-        for (int q = 0; q < ncta; ++q) s += cl.map_shared_rank(Gp, q)[ri * ldG + j];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += rv[q][u];
       gr[u] = s;
       er[u] = (j == ri) ? 1.0 : 0.0;
       if (j == ri && ri < n) { d0[ri] = s; diag = s; }
     }
     cluster_arrive();  // matched by the wait before the next Gram (or before exit)
     __syncthreads();
+    CQP();
     // ---- 3. elimination of [G | I]
     for (int k = 0; k < n; ++k) {
       double *pR = pv + (k & 1) * 2 * kCQN, *pE = pR + kCQN;
@@ -890,6 +914,7 @@ __global__ void __launch_bounds__(kCQT, 1) cholqr2_cluster_kernel(const double *
     // rows n..n8-1 of E (padding) stay as written by a previous pass or zero them once
     for (int e = n * ldE + tid; e < n8 * ldE; e += kCQT) E[e] = 0.0;
     __syncthreads();
+    CQP();
     // ---- 4. slab <- slab E^T (W = R^{-1} upper: W[t][j] = E[j][t], only t <= j contributes)
     for (int rb = warp; 8 * rb < nloc; rb += kCQT / 32) {
       double acc[8][2];
@@ -922,6 +947,14 @@ __global__ void __launch_bounds__(kCQT, 1) cholqr2_cluster_kernel(const double *
     __syncthreads();
   }
   cluster_wait();  // no CTA leaves while others may still read its partial Gram
+  CQP();
+#ifdef RTUCKER_CQ_PROF_BUILD
+  if (threadIdx.x == 0 && me == 0) {
+    printf("[cq prof] m %lld n %d:", (long long)m, n);
+    for (int i = 1; i < np_; ++i) printf(" %lld", pt[i] - pt[i - 1]);
+    printf("\n");
+  }
+#endif
   if (sbad) {
     if (me == 0 && tid == 0) *bad = 1;
     return;
