@@ -859,23 +859,12 @@ __global__ void __launch_bounds__(kCQT, 1) cholqr2_cluster_kernel(const double *
     CQP();
     // ---- 2. cluster sum into registers (fixed CTA order)
     double gr[8], er[8], diag = 0.0;  // diag: running G[ri][ri], kept by its owner (g == ri % 8)
-    // all remote loads issued before the (fixed-order) sums: one DSMEM round trip, not 8 x 8
-    double rv[8][8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const double *gq = cl.map_shared_rank(Gp, q < ncta ? q : 0);
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int j = g + 8 * u;
-        rv[q][u] = (q < ncta && ri < n && j < n) ? gq[ri * ldG + j] : 0.0;
-      }
-    }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int j = g + 8 * u;
       double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) s += rv[q][u];
+      if (ri < n && j < n)
+        for (int q = 0; q < ncta; ++q) s += cl.map_shared_rank(Gp, q)[ri * ldG + j];
       gr[u] = s;
       er[u] = (j == ri) ? 1.0 : 0.0;
       if (j == ri && ri < n) { d0[ri] = s; diag = s; }
