@@ -546,6 +546,14 @@ __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restri
                                                           double *__restrict__ Vout, double tol, int max_sweeps,
                                                           int *__restrict__ info, int r_need, int *__restrict__ refine) {
   extern __shared__ double gsm2[];
+#ifdef RTUCKER_EIG_PROF_BUILD
+  long long et_[6];
+  int en_ = 0;
+#define EGP() if (threadIdx.x == 0 && en_ < 6) et_[en_++] = clock64()
+#else
+#define EGP()
+#endif
+  EGP();
   constexpr int SPW = 32 / LPS;        // column slots per warp = block size
   const int np = n + (n & 1);
   const int nb = ((n + 2 * SPW - 1) / (2 * SPW)) * 2;  // column blocks of SPW (even count)
@@ -566,54 +574,93 @@ __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restri
   for (int e = tid; e < ldm * ncol; e += kGramT) M[e] = 0.0;
   for (int i = tid; i < np; i += kGramT) dn[i] = i < n ? 0 : 1;
   __syncthreads();
-  // pivot = largest remaining diagonal (first index on ties); -1 once it is <= n eps max diag(G)
-  auto pick_pivot = [&](double thresh) {
-    double bv = -1.0;
-    int bi = n;
-    for (int i = lane; i < n; i += 32) {
-      const double v = dn[i] ? -1.0 : G[i + np * i];
-      if (v > bv) { bv = v; bi = i; }
-    }
-    for (int o = 16; o; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-    }
-    if (lane == 0) spiv = (bv > thresh) ? bi : -1;
-  };
-  if (warp == 0) {
-    double m = 0.0;
-    for (int i = lane; i < n; i += 32) m = fmax(m, G[i + np * i]);
-    for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0) sdmax = m;
-    pick_pivot(n * 2.2e-16 * m);
-  }
+  // ---- pivoted Cholesky without row exchanges, left-looking, one CTA barrier per step:
+  //   p = argmax of the remaining diagonal d (first index on ties; every warp evaluates it
+  //   redundantly from d in shared memory, so no barrier publishes it), stop once d_p <= n eps
+  //   max diag(G);  M[i, k] = (G[i, p] - sum_{k' < k} M[i, k'] M[p, k']) / sqrt(d_p) on the rows
+  //   not yet pivoted (4 threads per row split the dot product), d_i -= M[i, k]^2.
+  //   M = P L (P the pivot permutation): its columns have the preconditioning of L, and
+  //   M M^T = G in the original index order.  (Right-looking with a rank-1 update of G and a
+  //   separate pivot pass cost 3 barriers and ~2100 cycles per step: 125k cycles at n = 60.)
+  // remaining diagonal, double-buffered (step k reads dq[k & 1], writes dq[(k + 1) & 1]); -inf
+  // marks a pivoted (or padding) row; a remaining diagonal that rounds below zero stays live
+  double *dq[2] = {lc, lam};
+  for (int i = tid; i < np; i += kGramT) lc[i] = i < n ? G[i + np * i] : -INFINITY;
+  double dmax = 0.0;
+  for (int i = lane; i < n; i += 32) dmax = fmax(dmax, G[i + np * i]);
+  for (int o = 16; o; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  const double thresh = n * 2.2e-16 * dmax;
   __syncthreads();
-  const double thresh = n * 2.2e-16 * sdmax;
-  // ---- pivoted Cholesky without row exchanges: M[:, k] = G[:, p] / sqrt(G[p][p]) on the rows
-  // not yet pivoted, G <- G - M[:, k] M[:, k]^T.  M = P L (P the pivot permutation): its
-  // columns have the preconditioning of L, and M M^T = G in the original index order.
-  const int ui = tid & 63, uj = tid >> 6;  // update ownership: G[ui][uj + 4 u]
+  EGP();
+  const int ci = tid >> 2, cs = tid & 3;  // row ci, dot-product quarter cs
+#ifdef RTUCKER_EIG_PROF_BUILD
+  long long ca = 0, cb = 0, cc = 0, cd = 0;
+#endif
   for (int k = 0; k < n; ++k) {
-    const int p = spiv;
-    if (p < 0) break;  // rank reached: the remaining columns of M are zero
-    const double inv = rsqrt(G[p + np * p]);
-    for (int i = tid; i < np; i += kGramT) {
-      const double l = dn[i] ? 0.0 : G[i + np * p] * inv;
-      lc[i] = l;
-      M[i + ldm * k] = l;
+#ifdef RTUCKER_EIG_PROF_BUILD
+    const long long q0 = clock64();
+#endif
+    const double *dc = dq[k & 1];
+    double *dnx = dq[(k + 1) & 1];
+    // argmax by three single-instruction warp reductions (redux.sync) instead of a 5-round
+    // shuffle tree (~700 cycles measured): a double >= 0 orders like its bit pattern, so the
+    // maximum is (max of the high words, then max of the low words among those), and ties go to
+    // the smallest index; negative entries (pivoted rows, diagonals rounded below 0) count as 0.
+    uint32_t khi = 0, klo = 0;
+    int kid = n;
+    for (int i = lane; i < n; i += 32) {
+      const double v = dc[i];
+      const uint32_t h = v > 0.0 ? (uint32_t)__double2hiint(v) : 0u, l = v > 0.0 ? (uint32_t)__double2loint(v) : 0u;
+      if (h > khi || (h == khi && l > klo)) { khi = h; klo = l; kid = i; }
     }
-    __syncthreads();
-    if (tid == 0) dn[p] = 1;
-    if (ui < np) {
-      const double li = lc[ui];
-#pragma unroll 4
-      for (int j = uj; j < np; j += kGramT / 64) G[ui + np * j] = fma(-li, lc[j], G[ui + np * j]);
+    const uint32_t mhi = __reduce_max_sync(0xffffffffu, khi);
+    const uint32_t mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
+    const int bi = (int)__reduce_min_sync(0xffffffffu, (khi == mhi && klo == mlo) ? (uint32_t)kid : 0xffffffffu);
+    const double bv = __hiloint2double((int)mhi, (int)mlo);
+    if (!(bv > thresh)) break;  // rank reached (same decision in every warp): the rest of M is zero
+#ifdef RTUCKER_EIG_PROF_BUILD
+    const long long q1 = clock64();
+#endif
+    const int p = bi;
+    const double inv = rsqrt(bv);
+    double dot = 0.0;
+    if (ci < np) {  // four independent chains (loads of 4 steps in flight)
+      double d1 = 0.0, d2 = 0.0, d3 = 0.0;
+      int kk = cs;
+      for (; kk + 12 < k; kk += 16) {
+        dot = fma(M[ci + ldm * kk], M[p + ldm * kk], dot);
+        d1 = fma(M[ci + ldm * (kk + 4)], M[p + ldm * (kk + 4)], d1);
+        d2 = fma(M[ci + ldm * (kk + 8)], M[p + ldm * (kk + 8)], d2);
+        d3 = fma(M[ci + ldm * (kk + 12)], M[p + ldm * (kk + 12)], d3);
+      }
+      for (; kk < k; kk += 4) dot = fma(M[ci + ldm * kk], M[p + ldm * kk], dot);
+      dot = (dot + d1) + (d2 + d3);
     }
+    dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+    dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+#ifdef RTUCKER_EIG_PROF_BUILD
+    const long long q2 = clock64();
+#endif
+    if (cs == 0 && ci < np) {
+      const double dci = dc[ci];
+      const bool done = dci == -INFINITY;
+      const double l = done ? 0.0 : (G[ci + np * p] - dot) * inv;
+      M[ci + ldm * k] = l;
+      dnx[ci] = (done || ci == p) ? -INFINITY : dci - l * l;
+    }
+#ifdef RTUCKER_EIG_PROF_BUILD
+    const long long q3 = clock64();
+#endif
     __syncthreads();
-    if (warp == 0) pick_pivot(thresh);
-    __syncthreads();
+#ifdef RTUCKER_EIG_PROF_BUILD
+    const long long q4 = clock64();
+    ca += q1 - q0; cb += q2 - q1; cc += q3 - q2; cd += q4 - q3;
+#endif
   }
+#ifdef RTUCKER_EIG_PROF_BUILD
+  if (tid == 0 || tid == 255) printf("[chol prof] tid %d argmax %lld dot %lld write %lld barrier %lld\n", tid, ca, cb, cc, cd);
+#endif
+  EGP();
   // ---- block-ordered one-sided Jacobi on the columns of M
   const double tol2 = tol * tol;
   const int slot = lane / LPS, q = lane % LPS;
@@ -672,6 +719,7 @@ __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restri
     __syncthreads();
     if (!more) break;
   }
+  EGP();
   if (tid == 0 && info) *info = sweeps;
   for (int k = warp; k < np; k += kGramT / 32) {  // exact column norms
     double d = 0.0;
@@ -693,6 +741,11 @@ __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restri
     const double inv = di > 0.0 ? 1.0 / sqrt(di) : 0.0;
     for (int r = 0; r < n; ++r) Vout[r + (int64_t)n * rank] = M[r + ldm * i] * inv;
   }
+  EGP();
+#ifdef RTUCKER_EIG_PROF_BUILD
+  if (threadIdx.x == 0) printf("[eig prof] n %d sweeps %d: init %lld chol %lld jacobi %lld final %lld\n", n, sweeps,
+                               et_[1] - et_[0], et_[2] - et_[1], et_[3] - et_[2], et_[4] - et_[3]);
+#endif
   // v_k from a normalised column is accurate to ~eps sqrt(lambda_0 / lambda_k): request the
   // unpreconditioned solver when the wanted rank reaches lambda_k < 1e-8 lambda_0
   if (refine) {
