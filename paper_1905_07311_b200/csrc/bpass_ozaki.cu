@@ -120,6 +120,18 @@ __device__ __forceinline__ int exp_of(uint32_t mbits) {
   return e;
 }
 
+// m_p = max_i |X(l, i, r)| for p = l + L r (strided contraction index): thread per column,
+// consecutive threads consecutive l (coalesced rows).
+__global__ void colmax_l_kernel(const float *__restrict__ X, int64_t L, int64_t I, int64_t P, uint32_t *__restrict__ cm) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < P; p += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = p / L, l = p - r * L;
+    const float *col = X + l + L * I * r;
+    float m = 0.f;
+    for (int64_t i = 0; i < I; ++i) m = fmaxf(m, fabsf(col[L * i]));
+    cm[p] = __float_as_uint(m);
+  }
+}
+
 // Q (I x J fp64, column-major) -> per chunk c: 5 slices, each [64 j][32 i] K-major int8 (rows
 // j >= J and i >= I zero); f_j = exponent of max_i |Q(i, j)|.  One CTA per column j.
 __global__ void qslice_kernel(const double *__restrict__ Q, int64_t I, int64_t lda, int J, int nchunk,
@@ -157,6 +169,7 @@ __global__ void qslice_kernel(const double *__restrict__ Q, int64_t I, int64_t l
 
 struct OzParams {
   int64_t I, P;
+  int64_t L, tpr;       // LG layout: extent of the contiguous index l and 128-column tiles per r
   int J, nchunk;
   const int8_t *qs;     // [nchunk][5][64 x 32]
   const uint32_t *cm;   // [P] fp32 bits of the column maxima of X
@@ -171,6 +184,26 @@ struct OzParams {
 #else
 #define OZP(...)
 #endif
+
+// Tile -> column p of tile row `row` (-1 past the end).  Mode 1 (L == 1): tiles of 128
+// consecutive p.  LG (L > 1, Gram only): tile (r, l0) = 128 consecutive l of one r, p = l + L r.
+__device__ __forceinline__ void tma_load_3d(void *dst, const void *tmap, uint64_t *bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(tc::smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(tc::smem_u32(bar))
+      : "memory");
+}
+
+template <bool LG>
+__device__ __forceinline__ int64_t oz_col(const OzParams &p, int64_t tile, int row) {
+  if (!LG) {
+    const int64_t pp = tile * kOP + row;
+    return pp < p.P ? pp : -1;
+  }
+  const int64_t r = tile / p.tpr, l = (tile - r * p.tpr) * kOP + row;
+  return l < p.L ? l + p.L * r : -1;
+}
 
 // 2^k as a double for k in the normal range (clamped)
 __device__ __forceinline__ double pow2d(int k) {
@@ -194,6 +227,9 @@ __device__ __forceinline__ void tmem_st4(uint32_t taddr, uint32_t a, uint32_t b,
 constexpr int kOXB = 4;          // A-operand buffers in TMEM
 constexpr uint32_t kOAcol = 320;
 
+// LG: the contraction index i is strided (mode n > 1 with L > 1: X(l, i, r)); 3-D TMA boxes of
+// 128 l x 32 i (plain layout [i][l]) and a Gram-only epilogue.
+template <bool LG>
 __global__ void __launch_bounds__(kOThreads, 1)
     bpass_ozaki_kernel(const __grid_constant__ CUtensorMap tmap, const OzParams p) {
   extern __shared__ __align__(1024) unsigned char ozs[];
@@ -211,7 +247,7 @@ __global__ void __launch_bounds__(kOThreads, 1)
   double *fpw = reinterpret_cast<double *>(tslot + 2);  // [64] 2^{f_j}
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t ntiles = (p.P + kOP - 1) / kOP;
+  const int64_t ntiles = LG ? p.tpr * (p.P / p.L) : (p.P + kOP - 1) / kOP;
   const int64_t mytiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int nchunk = p.nchunk;
   const int64_t total = mytiles * nchunk;
@@ -249,10 +285,15 @@ __global__ void __launch_bounds__(kOThreads, 1)
       for (int64_t g = 0; g < total; ++g) {
         const int64_t tk = g / nchunk;
         const int ch = (int)(g - tk * nchunk);
-        const int64_t p0 = (blockIdx.x + tk * gridDim.x) * kOP;
+        const int64_t tile = blockIdx.x + tk * gridDim.x;
         if (g >= kONSS) tc::mbar_wait(&sfree[s], ph ^ 1);
         tc::mbar_arrive_expect_tx(&full[s], kXStB);
-        tc::tma_load_2d(stg + s * kXStB, &tmap, &full[s], ch * kOK, (int)p0);
+        if (LG) {
+          const int64_t r = tile / p.tpr;
+          tma_load_3d(stg + s * kXStB, &tmap, &full[s], (int)((tile - r * p.tpr) * kOP), ch * kOK, (int)r);
+        } else {
+          tc::tma_load_2d(stg + s * kXStB, &tmap, &full[s], ch * kOK, (int)(tile * kOP));
+        }
         if (++s == kONSS) { s = 0; ph ^= 1; }
       }
     }
@@ -333,8 +374,8 @@ __global__ void __launch_bounds__(kOThreads, 1)
     OZP(long long w4 = 0, w5 = 0, t0 = clock64();)
     for (int64_t g = 0; g < total; ++g) {
       if (ch == 0) {
-        const int64_t pp = (blockIdx.x + tk * gridDim.x) * kOP + row;
-        sc = pp < p.P ? ldexpf(1.0f, -exp_of(p.cm[pp])) : 0.f;
+        const int64_t pp = oz_col<LG>(p, blockIdx.x + tk * gridDim.x, row);
+        sc = pp >= 0 ? ldexpf(1.0f, -exp_of(p.cm[pp])) : 0.f;
       }
       OZP(const long long c0 = clock64();)
       tc::mbar_wait(&full[s], ph);
@@ -342,13 +383,20 @@ __global__ void __launch_bounds__(kOThreads, 1)
       if (g >= kOXB) tc::mbar_wait(&xempty[x], phx ^ 1);
       OZP(w4 += c1 - c0; w5 += clock64() - c1;)
       tc::tc_fence_after();
-      // staging row `row` = 32 floats (128 B, 16-byte chunks XOR-swizzled by row % 8)
+      // mode 1: staging row `row` = 32 floats (128 B, 16-byte chunks XOR-swizzled by row % 8);
+      // LG: staging [32 i][128 l], this thread's values at stride 128 floats (conflict-free)
       const unsigned char *srow = stg + s * kXStB + row * 128;
+      const float *scol = reinterpret_cast<const float *>(stg + s * kXStB) + row;
       uint32_t w[kOS][4];
 #pragma unroll
       for (int cq = 0; cq < 4; ++cq) {  // 16-byte chunk j = 4 half + cq: values k = 4 j .. 4 j + 3
         const int j = 4 * half + cq;
-        const float4 v = *reinterpret_cast<const float4 *>(srow + ((j ^ (row & 7)) << 4));
+        float4 v;
+        if (LG) {
+          v = make_float4(scol[(4 * j) * kOP], scol[(4 * j + 1) * kOP], scol[(4 * j + 2) * kOP], scol[(4 * j + 3) * kOP]);
+        } else {
+          v = *reinterpret_cast<const float4 *>(srow + ((j ^ (row & 7)) << 4));
+        }
         uint32_t a[kOS], b[kOS], c[kOS], d[kOS];
         slice5(v.x * sc, a);
         slice5(v.y * sc, b);
@@ -382,8 +430,7 @@ __global__ void __launch_bounds__(kOThreads, 1)
     long long *Ti = reinterpret_cast<long long *>(T);
     OZP(long long e0 = 0, e1 = 0, e2 = 0, e3 = 0, e4 = 0, et0 = clock64();)
     for (int64_t tt = 0; tt < mytiles; ++tt) {
-      const int64_t p0 = (blockIdx.x + tt * gridDim.x) * kOP;
-      const int64_t pp = p0 + row;
+      const int64_t pp = oz_col<LG>(p, blockIdx.x + tt * gridDim.x, row);
       OZP(const long long c0 = clock64();)
       tc::mbar_wait(accfull, (uint32_t)(tt & 1));
       OZP(const long long c1 = clock64(); e0 += c1 - c0;)
@@ -409,10 +456,10 @@ __global__ void __launch_bounds__(kOThreads, 1)
       // phase 2: B_jp = S 2^{e_p - 40} 2^{f_j} (level weights 2^{2 - 7 (L + 2)}, L = 0 .. 4),
       // kept in T (fp64, in place) for the Gram and stored straight to B = out[p J + j]: a row
       // of B is one thread's 60 contiguous doubles (16-byte stores; L2 merges the sectors)
-      const int ep = pp < p.P ? exp_of(p.cm[pp]) : 0;
+      const bool pok = pp >= 0;
+      const int ep = pok ? exp_of(p.cm[pp]) : 0;
       const double rs = pow2d(ep - 40);
-      const bool pok = pp < p.P;
-      double *orow = p.out ? p.out + pp * p.J : nullptr;
+      double *orow = (!LG && p.out) ? p.out + pp * p.J : nullptr;
       const bool vec = (p.J & 1) == 0;
 #pragma unroll 4
       for (int jj = 0; jj < kON; jj += 2) {
@@ -515,10 +562,13 @@ bool ozaki_bpass_enabled() {
 // Returns false outside the kernel's envelope (caller falls back to the fp64 tensor cores).
 bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda, int J, double *out, double *gram,
                const uint32_t *colmax) {
-  if (!ozaki_bpass_enabled() || v.L != 1 || J < 1 || J > kON || (v.I % 4) != 0 || v.I > 26000 ||
+  const bool lg = v.L > 1;  // strided contraction index: Gram-only variant (R-HOSVD modes n > 1)
+  if (!ozaki_bpass_enabled() || J < 1 || J > kON || (v.I % 4) != 0 || v.I > 26000 ||
       (((uintptr_t)X) & 15) != 0 || v.R > (int64_t)INT32_MAX - kOP)
     return false;
-  const int64_t I = v.I, P = v.R;
+  if (lg && (out || !gram || (v.L % 4) != 0 || v.L > (int64_t)INT32_MAX - kOP || getenv("RTUCKER_NO_OZAKI_LG")))
+    return false;
+  const int64_t I = v.I, P = v.L * v.R;
   const int nchunk = (int)((I + kOK - 1) / kOK);
   DevBuf<int8_t> qs(c, (size_t)nchunk * kQChB);
   DevBuf<int> fexp(c, kON);
@@ -526,15 +576,23 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
   RT_LAUNCH(c, qslice_kernel, kON, 256, 0, A, I, lda, J, nchunk, qs.p, fexp.p);
   if (!colmax) {
     cmown.alloc(c, (size_t)P);
-    RT_LAUNCH(c, colmax_kernel, std::max(1, std::min(c.num_sms * 16, (int)((P + 7) / 8))), 256, 0, X, I, P, cmown.p);
+    if (lg) {
+      RT_LAUNCH(c, colmax_l_kernel, (int)std::min<int64_t>((P + 255) / 256, (int64_t)c.num_sms * 32), 256, 0, X, v.L,
+                I, P, cmown.p);
+    } else {
+      RT_LAUNCH(c, colmax_kernel, std::max(1, std::min(c.num_sms * 16, (int)((P + 7) / 8))), 256, 0, X, I, P, cmown.p);
+    }
     colmax = cmown.p;
   }
-  const int64_t ntiles = (P + kOP - 1) / kOP;
+  const int64_t tpr = (v.L + kOP - 1) / kOP;
+  const int64_t ntiles = lg ? tpr * v.R : (P + kOP - 1) / kOP;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, c.num_sms));
   DevBuf<double> part;
   OzParams prm{};
   prm.I = I;
   prm.P = P;
+  prm.L = v.L;
+  prm.tpr = tpr;
   prm.J = J;
   prm.nchunk = nchunk;
   prm.qs = qs.p;
@@ -549,17 +607,29 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
   if (gram && !gsep) part.alloc(c, (size_t)grid * 4096);
   prm.gram_partial = (gram && !gsep) ? part.p : nullptr;
   CUtensorMap tm;
-  cuuint64_t dims[2] = {(cuuint64_t)I, (cuuint64_t)P};
-  cuuint64_t strides[1] = {(cuuint64_t)I * 4};
-  cuuint32_t box[2] = {kOK, kOP};
-  cuuint32_t es[2] = {1, 1};
-  CUresult r = tensor_map_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)X, dims, strides, box, es,
-                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r;
+  if (lg) {  // (l, i, r), box 128 l x 32 i x 1 r, plain [i][l] staging
+    cuuint64_t dims[3] = {(cuuint64_t)v.L, (cuuint64_t)I, (cuuint64_t)v.R};
+    cuuint64_t strides[2] = {(cuuint64_t)v.L * 4, (cuuint64_t)v.L * I * 4};
+    cuuint32_t box[3] = {kOP, kOK, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    r = tensor_map_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)X, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[2] = {(cuuint64_t)I, (cuuint64_t)P};
+    cuuint64_t strides[1] = {(cuuint64_t)I * 4};
+    cuuint32_t box[2] = {kOK, kOP};
+    cuuint32_t es[2] = {1, 1};
+    r = tensor_map_encoder()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)X, dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   if (r != CUDA_SUCCESS) throw Error(RTUCKER_ECUDA, "cuTensorMapEncodeTiled failed for the Ozaki B-pass");
   const size_t smem = 1024 + (size_t)kONSS * kXStB + (size_t)kONQ * kQChB + sizeof(double) * kON * kOTP +
                       8 * (2 * kONSS + 2 * kONQ + 2 * kOXB + 2) + 16 + 8 * kON;
-  RT_CUDA(cudaFuncSetAttribute(bpass_ozaki_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kern = lg ? bpass_ozaki_kernel<true> : bpass_ozaki_kernel<false>;
+  RT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   static const bool prof = getenv("RTUCKER_OZ_PROF") != nullptr;
   DevBuf<long long> pbuf;
   if (prof) {
@@ -567,7 +637,7 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
     RT_CUDA(cudaMemsetAsync(pbuf.p, 0, 128, c.stream));
     prm.prof = pbuf.p;
   }
-  RT_LAUNCH(c, bpass_ozaki_kernel, grid, kOThreads, smem, tm, prm);
+  RT_LAUNCH(c, kern, grid, kOThreads, smem, tm, prm);
   if (prof) {
     long long h[16];
     RT_CUDA(cudaMemcpyAsync(h, pbuf.p, 128, cudaMemcpyDeviceToHost, c.stream));
