@@ -549,8 +549,14 @@ __global__ void oz_gram_reduce_kernel(const double *__restrict__ part, int nblk,
 
 }  // namespace
 
-void column_maxima(Ctx &c, const float *X, int64_t I, int64_t P, uint32_t *cm) {
-  RT_LAUNCH(c, colmax_kernel, std::max(1, std::min(c.num_sms * 16, (int)((P + 7) / 8))), 256, 0, X, I, P, cm);
+void column_maxima(Ctx &c, const float *X, ModeView v, uint32_t *cm) {
+  const int64_t P = v.L * v.R;
+  if (v.L > 1) {
+    RT_LAUNCH(c, colmax_l_kernel, (int)std::min<int64_t>((P + 255) / 256, (int64_t)c.num_sms * 32), 256, 0, X, v.L,
+              v.I, P, cm);
+  } else {
+    RT_LAUNCH(c, colmax_kernel, std::max(1, std::min(c.num_sms * 16, (int)((P + 7) / 8))), 256, 0, X, v.I, P, cm);
+  }
 }
 
 bool ozaki_bpass_enabled() {
@@ -576,12 +582,7 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
   RT_LAUNCH(c, qslice_kernel, kON, 256, 0, A, I, lda, J, nchunk, qs.p, fexp.p);
   if (!colmax) {
     cmown.alloc(c, (size_t)P);
-    if (lg) {
-      RT_LAUNCH(c, colmax_l_kernel, (int)std::min<int64_t>((P + 255) / 256, (int64_t)c.num_sms * 32), 256, 0, X, v.L,
-                I, P, cmown.p);
-    } else {
-      RT_LAUNCH(c, colmax_kernel, std::max(1, std::min(c.num_sms * 16, (int)((P + 7) / 8))), 256, 0, X, I, P, cmown.p);
-    }
+    column_maxima(c, X, v, cmown.p);
     colmax = cmown.p;
   }
   const int64_t tpr = (v.L + kOP - 1) / kOP;

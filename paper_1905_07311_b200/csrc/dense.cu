@@ -243,9 +243,9 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
     const bool last_sharded = in.sharded && n == d - 1;
     const int64_t Ig = in.gdims[n];
     DevBuf<double> Y(c, (size_t)Ig * ell + 1);
-    DevBuf<uint32_t> colmax;  // column maxima for the Ozaki B-pass (mode 1, fp32, HYBRID)
-    if (in.dt == DT::F32 && !pol.mul_f64 && v.L == 1 && !last_sharded && ozaki_bpass_enabled()) {
-      colmax.alloc(c, (size_t)v.R);
+    DevBuf<uint32_t> colmax;  // column maxima for the Ozaki B-pass (fp32, HYBRID), recorded by the sketch
+    if (in.dt == DT::F32 && !pol.mul_f64 && (v.L == 1 || (v.L % 4) == 0) && !last_sharded && ozaki_bpass_enabled()) {
+      colmax.alloc(c, (size_t)(v.L * v.R));
       colmax.zero();
     }
     PhaseScope ps(c, PH_SKETCH, n);

@@ -55,7 +55,7 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
                const uint32_t *colmax = nullptr);
 bool ozaki_bpass_enabled();
 // cm[p] = fp32 bits of max_i |X(i, p)| for X (I x P, column-major) - the Ozaki column scales.
-void column_maxima(Ctx &c, const float *X, int64_t I, int64_t P, uint32_t *cm);
+void column_maxima(Ctx &c, const float *X, ModeView v, uint32_t *cm);  // max_i |X(l, i, r)| per l + L r
 void ttm_dense(Ctx &c, const void *X, DT in, ModeView v, const double *A, int64_t lda, int J,
                void *out, DT outT, bool mul_f64, double *gram, const uint32_t *colmax = nullptr);
 

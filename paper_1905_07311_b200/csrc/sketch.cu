@@ -353,7 +353,7 @@ void sketch_dispatch(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int64_
     double *ns = kb == 0 ? normsq : nullptr;
     if constexpr (std::is_same<Tin, float>::value && std::is_same<Tmul, float>::value) {
       if (sketch_tc_mn(c, X, v, mode, e, k0 + kb, seed, col_offset, Yb, ns, kb == 0 ? colmax : nullptr)) continue;
-      if (kb == 0 && colmax) column_maxima(c, (const float *)X, v.I, v.R, colmax);  // TC path declined
+      if (kb == 0 && colmax) column_maxima(c, (const float *)X, v, colmax);  // TC path declined
     }
     if (e <= 16)
       launch_sketch<Tin, Tmul, 16>(c, X, v, mode, e, k0 + kb, seed, col_offset, Yb, ns);
@@ -372,8 +372,8 @@ void sketch_dense(Ctx &c, const void *X, DT in, ModeView v, int mode, int ell, i
   // the column maxima must be valid whenever requested: the tcgen05 mode-1 sketch records them
   // on the fly; any other path computes them here
   if (colmax && (in != DT::F32 || mul_f64)) {
-    RT_REQUIRE(in == DT::F32 && v.L == 1, "sketch: column maxima need fp32 data with L == 1");
-    column_maxima(c, (const float *)X, v.I, v.R, colmax);
+    RT_REQUIRE(in == DT::F32, "sketch: column maxima need fp32 data");
+    column_maxima(c, (const float *)X, v, colmax);
     colmax = nullptr;
   }
   if (in == DT::F64 || mul_f64) {

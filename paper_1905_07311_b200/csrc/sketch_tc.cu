@@ -60,7 +60,7 @@ struct SketchTcParams {
   int64_t col_offset;    // global unfolding-column offset of this shard
   double *partial;       // [grid][ell][I]
   double *norm_partial;  // [grid] or null
-  uint32_t *colmax;      // [C] fp32 bits of max_i |X(i, c)| (atomic max), or null (L == 1 only)
+  uint32_t *colmax;      // [C] fp32 bits of max_i |X(i, c)| (atomic max), or null
 };
 
 __device__ __forceinline__ int kmaj_off(int r, int k) {  // byte offset in a K-major tile
@@ -231,10 +231,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float *st = (const float *)(sb + (size_t)ss * sbytes);
       unsigned char *hs = hb + (size_t)so * abytes, *ls = lb + (size_t)so * abytes;
       float acc = 0.f;
+      float cm[8];  // this thread's column maxima of the stage's 8 columns c0 .. c0+7
+#pragma unroll
+      for (int u = 0; u < 8; ++u) cm[u] = 0.f;
       if (KM) {  // staging and operand planes share the K-major layout: elementwise split
         const int nun = p.nbox * p.BR * kBK / 4;  // float4 units
         for (int u = wt; u < nun; u += 32 * kWorkers) {
           const float4 x = *(const float4 *)(st + 4 * u);
+          if (p.colmax) {  // unit u = (i % 8) + 8 (l / 4) + 16 (i / 8): columns 4 (l / 4) + 0..3
+            const float m0 = fabsf(x.x), m1 = fabsf(x.y), m2 = fabsf(x.z), m3 = fabsf(x.w);
+            if ((u >> 3) & 1) {
+              cm[4] = fmaxf(cm[4], m0); cm[5] = fmaxf(cm[5], m1); cm[6] = fmaxf(cm[6], m2); cm[7] = fmaxf(cm[7], m3);
+            } else {
+              cm[0] = fmaxf(cm[0], m0); cm[1] = fmaxf(cm[1], m1); cm[2] = fmaxf(cm[2], m2); cm[3] = fmaxf(cm[3], m3);
+            }
+          }
           float4 h, l;
           h.x = tc::tf32_hi(x.x); h.y = tc::tf32_hi(x.y); h.z = tc::tf32_hi(x.z); h.w = tc::tf32_hi(x.w);
           l.x = tc::tf32_lo(x.x, h.x); l.y = tc::tf32_lo(x.y, h.y); l.z = tc::tf32_lo(x.z, h.z); l.w = tc::tf32_lo(x.w, h.w);
@@ -243,9 +254,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           acc = fmaf(x.x, x.x, acc); acc = fmaf(x.y, x.y, acc); acc = fmaf(x.z, x.z, acc); acc = fmaf(x.w, x.w, acc);
         }
       }
-      float cm[8];  // this thread's column maxima of the stage (L == 1: 8 columns c0 .. c0+7)
-#pragma unroll
-      for (int u = 0; u < 8; ++u) cm[u] = 0.f;
 #pragma unroll
       for (int j = 0; j < kRJ; ++j) {
         if (!KM && wt + 32 * kWorkers * j < rows_st) {
@@ -270,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (!KM && p.colmax) {
+      if (p.colmax) {
         // warp max per column by a transposing butterfly: at distance 16, 8, 4 each lane keeps
         // half of its columns and takes the partner's maxima of them (4 + 2 + 1 shuffles), so
         // lane l ends with column l / 4 over 8 lanes; distances 2, 1 finish the warp.  Then
@@ -814,7 +822,7 @@ bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t
   if (normsq) npart.alloc(c, g);
   p.partial = part.p;
   p.norm_partial = normsq ? npart.p : nullptr;
-  p.colmax = km ? nullptr : colmax;
+  p.colmax = colmax;
 
   CUtensorMap tm;
   CUresult r;
