@@ -182,6 +182,31 @@ def test_ozaki_bpass(ctx, shape, J, graded):
     assert np.linalg.norm(g - gref) <= 2e-9 * np.linalg.norm(gref)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,mode,J,graded", [((96, 64, 30), 1, 60, False), ((200, 24, 8), 1, 13, True),
+                                                 ((20, 64, 36), 2, 36, True), ((8, 16, 12), 2, 5, False)])
+def test_ozaki_bpass_strided(ctx, shape, mode, J, graded):
+    """Gram-only HYBRID B-pass of a strided mode (L > 1: the Ozaki kernel's 3-D-box variant,
+    R-HOSVD modes n > 1) against the fp64 Gram of Q^T X_(n) on the same fp32 bits, 2e-9
+    relative (DESIGN R18).  Ragged 128-column tiles (L = 200, 96, 1280, 128) and, with `graded`,
+    per-column scales over 12 decades with one zero column."""
+    rng = np.random.default_rng(sum(shape) + J + mode)
+    x = rng.standard_normal(shape)
+    if graded:  # scale the unfolding columns (indices other than `mode`)
+        other = [k for k in range(3) if k != mode]
+        x *= np.logspace(0, -12, shape[other[0]]).reshape([-1 if k == other[0] else 1 for k in range(3)])
+        idx = [0, 0, 0]
+        idx[mode] = slice(None)
+        x[tuple(idx)] = 0.0
+    x = np.asfortranarray(x.astype(np.float32))
+    q, _ = np.linalg.qr(rng.standard_normal((shape[mode], J)))
+    _, g = ctx.debug_ttm(x, x.shape, mode, q, want_out=False)
+    bref = q.T @ O.unfold(np.asarray(x, dtype=np.float64), mode)
+    gref = bref @ bref.T
+    g = g.cpu().numpy().reshape(J, J) if hasattr(g, "cpu") else np.asarray(g).reshape(J, J)
+    assert np.linalg.norm(g - gref) <= 2e-9 * np.linalg.norm(gref)
+
+
 @pytest.mark.parametrize("kind,n,k", [("c4like", 60, 50), ("hilbert", 60, 5), ("rankdef", 40, 7), ("small", 10, 5),
                                       ("odd", 33, 20), ("one", 1, 1)])
 def test_gram_eig(ctx, kind, n, k):
