@@ -361,7 +361,15 @@ def main():
                         "int8_tops": i8_ops / (t_k * 1e-3) / 1e12,
                         "int8_peak_tops": i8_peak,
                         "int8_peak_source": i8_src})
-    dom = max(kernels, key=lambda k: k["ms"]) if kernels else None
+    eig = [phases[("eig", m)] for m in range(3) if ("eig", m) in phases]
+    if eig and args.algo == "sthosvd":
+        # the three 60x60 eigensolves: one CTA each, bound by the dependent latency chain of the
+        # Jacobi rounds, no bandwidth or tensor roofline; listed for the step share
+        t_e = sum(v[0] / max(v[1], 1) for v in eig)
+        kernels.append({"kernel": "gram_eig_kernel x3 (pivoted Cholesky + one-sided Jacobi, one CTA)",
+                        "bound": "latency", "ms": t_e / len(eig), "ms_per_step": t_e,
+                        "share_of_step": t_e / ms_local, "launches_per_step": len(eig)})
+    dom = max((k for k in kernels if k["bound"] != "latency"), key=lambda k: k["ms"]) if kernels else None
     roofline = None
     if dom:
         roofline = {k: dom[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
