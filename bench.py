@@ -119,6 +119,14 @@ class Clocks:
         except Exception:
             self.p = None
 
+    def mark(self):
+        """Start of the timed region: only samples written after this point are summarised."""
+        try:
+            self.f.flush()
+            self.off = os.path.getsize(self.f.name)
+        except Exception:
+            self.off = 0
+
     def stop(self):
         if self.p is None:
             return None
@@ -129,7 +137,7 @@ class Clocks:
         except Exception:
             self.p.kill()
         self.f.flush()
-        self.f.seek(0)
+        self.f.seek(getattr(self, "off", 0))
         sm, smax, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.f.read().splitlines():
@@ -284,6 +292,12 @@ def main():
             return ctx.sthosvd(inp, (I, I, I), RANKS, P, SEED, ORDER, flags | args.flags, shard=shard)
         return ctx.hosvd(inp, (I, I, I), RANKS, P, SEED, flags | args.flags, shard=shard)
 
+    # the clock sampler (nvidia-smi -lms 100) starts before the warm-up: its process start and
+    # NVML initialisation take driver locks that stalled kernel launches when they overlapped
+    # the timed region (host enqueue 11 ms/step instead of 0.6 on one box)
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(1.0)
     for _ in range(args.warmup):
         step(x).free()
     torch.cuda.synchronize()
@@ -291,8 +305,7 @@ def main():
     # ---- timed region: K steps, barrier + sync on both sides, CUDA events on the ctx stream
     ctx.set_profiling(not args.no_phases)
     ctx.phase_times(reset=True)
-    clocks = Clocks(local)
-    clocks.start()
+    clocks.mark()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()

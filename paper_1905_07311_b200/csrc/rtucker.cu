@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <numeric>
 #include <functional>
+#include <mutex>
+#include <vector>
 
 #include "comm.h"
 #include "kernels_extra.h"
@@ -94,9 +96,23 @@ void rank_caps(const int64_t *dims, int d, int n, int64_t r, int p, bool strict,
 }
 
 // --------------------------------------------------------------------- result ------
+// Result structs live in pinned memory (device-to-host scalar copies land in them
+// asynchronously).  They are recycled through a process-wide free list: cudaMallocHost takes
+// driver locks and stalled concurrent kernel launches when called once per call in a
+// throughput loop; cudaFreeHost would synchronise the device.
+std::mutex g_result_mu;
+std::vector<rtucker_result *> g_result_free;
+
 rtucker_result *new_result(int d) {
   rtucker_result *r = nullptr;
-  if (cudaMallocHost((void **)&r, sizeof(rtucker_result)) != cudaSuccess)
+  {
+    std::lock_guard<std::mutex> lk(g_result_mu);
+    if (!g_result_free.empty()) {
+      r = g_result_free.back();
+      g_result_free.pop_back();
+    }
+  }
+  if (!r && cudaMallocHost((void **)&r, sizeof(rtucker_result)) != cudaSuccess)
     throw Error(RTUCKER_ENOMEM, "cudaMallocHost(result)");
   memset(r, 0, sizeof *r);
   r->d = d;
@@ -119,7 +135,11 @@ void free_result(Ctx &c, rtucker_result *r) {
     fr(r->selection[k]);
   }
   fr(r->core_vals);
-  cudaFreeHost(r);
+  // asynchronous copies into the struct must land before it is handed out again (cudaFreeHost,
+  // used before, synchronised the whole device here)
+  cudaStreamSynchronize(c.stream);
+  std::lock_guard<std::mutex> lk(g_result_mu);
+  g_result_free.push_back(r);
 }
 
 // Moves device result buffers to pinned host memory when RTUCKER_RESULT_HOST is set.
