@@ -425,7 +425,8 @@ def main():
             cpu = {"value": v, "unit": "Gelem/s", "cores": os.cpu_count(), "kind": "oracle", "sample": sample,
                    "seconds": dt}
         line = {
-            "metric": METRIC, "value": value, "unit": "Gelem/s", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC if args.algo == "sthosvd" else METRIC.replace("R-STHOSVD", "R-HOSVD"),
+            "value": value, "unit": "Gelem/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(args.algo, world),
             "roofline": roofline, "kernels": kernels,
