@@ -38,6 +38,12 @@ METRIC = "R-STHOSVD Gelem/s (C4 800^3 fp32, r=50, p=10)"
 
 
 def workload_config(algo, n):
+    if algo == "adaptive":
+        return {"workload": "C4 odeco 800x800x800 fp32 adaptive R-STHOSVD tol=1e-3 block=10 rho=[1,2,3] seed=0",
+                "algorithm": "adaptive R-STHOSVD (Alg 5)", "dims": [I, I, I], "dtype": "fp32", "tol": 1e-3,
+                "block": 10, "order": [1, 2, 3], "parallelism": "single GPU",
+                "l2": "input 2.05 GB > 126 MB L2: every step streams X from HBM (no flush needed)",
+                "data": "synthetic (workloads.odeco, data seed 4)"}
     return {"workload": f"C4 odeco 800x800x800 fp32 R-{algo.upper()} r=(50,50,50) p=10 rho=[1,2,3] seed=0",
             "algorithm": f"R-{algo.upper()}", "dims": [I, I, I], "dtype": "fp32", "ranks": list(RANKS), "p": P,
             "order": [1, 2, 3], "parallelism": f"mode-3 slabs x{n}" if n > 1 else "single GPU",
@@ -252,7 +258,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--algo", default="sthosvd", choices=["sthosvd", "hosvd", "sparse"])
+    ap.add_argument("--algo", default="sthosvd", choices=["sthosvd", "hosvd", "adaptive", "sparse"])
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -290,6 +296,9 @@ def main():
     def step(inp, flags=0):
         if args.algo == "sthosvd":
             return ctx.sthosvd(inp, (I, I, I), RANKS, P, SEED, ORDER, flags | args.flags, shard=shard)
+        if args.algo == "adaptive":  # C4 adaptive R-STHOSVD (Alg 5), block 10, tol 1e-3 (single GPU)
+            assert world == 1, "the adaptive variant is benchmarked on one GPU"
+            return ctx.adaptive(inp, (I, I, I), 1e-3, 10, order=ORDER, seed=SEED, flags=flags | args.flags)
         return ctx.hosvd(inp, (I, I, I), RANKS, P, SEED, flags | args.flags, shard=shard)
 
     # the clock sampler (nvidia-smi -lms 100) starts before the warm-up: its process start and
@@ -425,7 +434,8 @@ def main():
             cpu = {"value": v, "unit": "Gelem/s", "cores": os.cpu_count(), "kind": "oracle", "sample": sample,
                    "seconds": dt}
         line = {
-            "metric": METRIC if args.algo == "sthosvd" else METRIC.replace("R-STHOSVD", "R-HOSVD"),
+            "metric": {"sthosvd": METRIC, "hosvd": METRIC.replace("R-STHOSVD", "R-HOSVD"),
+                       "adaptive": "adaptive R-STHOSVD Gelem/s (C4 800^3 fp32, tol 1e-3, block 10)"}[args.algo],
             "value": value, "unit": "Gelem/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(args.algo, world),
