@@ -419,6 +419,102 @@ __global__ void __launch_bounds__(kL == 8 ? 256 : (kL == 16 ? 512 : kEigT)) jaco
   }
 }
 
+// Large-n variant of jacobi_kernel (matrices in global memory / L2) on the whole GPU: a
+// cooperative grid, one warp per column pair of a round (pairs strided over all warps of the
+// grid), grid.sync() between rounds.  A one-CTA sweep over n ~ 700 took ~0.3 s (3 s per
+// eigensolve in the adaptive C4 run, ranks ~700); the arithmetic and the round-robin order are
+// jacobi_kernel's, so the result is the same up to the order of the column-norm refreshes.
+// The convergence flag rotates over three slots (reset for sweep s while sweep s - 1's slot is
+// still being read).
+constexpr int kEigGT = 256;
+__global__ void __launch_bounds__(kEigGT) jacobi_grid_kernel(const double *__restrict__ Ain, int n,
+                                                          double *__restrict__ w, double *__restrict__ Vout,
+                                                          double *__restrict__ gws, int *__restrict__ conv,
+                                                          double tol, int max_sweeps, int *__restrict__ info,
+                                                          const int *__restrict__ gate) {
+  if (gate && *gate == 0) return;
+  cg::grid_group grid = cg::this_grid();
+  const int np = n + (n & 1);
+  double *__restrict__ M = gws;                    // np x np, column-major
+  double *__restrict__ V = M + (size_t)np * np;
+  double *__restrict__ lam = V + (size_t)np * np;  // np
+  const int lane = threadIdx.x & 31;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gthr = (int64_t)gridDim.x * blockDim.x;
+  const int gw = (int)(gtid >> 5), nw = (int)(gthr >> 5);
+  const int npairs = np / 2;
+  for (int64_t e = gtid; e < (int64_t)np * np; e += gthr) {
+    const int i = (int)(e % np), j = (int)(e / np);
+    M[e] = (i < n && j < n) ? 0.5 * (Ain[i + (size_t)n * j] + Ain[j + (size_t)n * i]) : 0.0;
+    V[e] = (i == j) ? 1.0 : 0.0;
+  }
+  const double tol2 = tol * tol;
+  int sweeps = 0;
+  grid.sync();
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    for (int k = gw; k < np; k += nw) {  // column norms^2 (fresh every sweep)
+      double d = 0.0;
+      for (int r = lane; r < np; r += 32) { const double x = M[r + (size_t)np * k]; d = fma(x, x, d); }
+      d = warp_sum(d);
+      if (lane == 0) lam[k] = d;
+    }
+    if (gtid == 0) conv[sweep % 3] = 1;
+    grid.sync();
+    for (int t = 0; t < np - 1; ++t) {
+      for (int k = gw; k < npairs; k += nw) {
+        int p, q;
+        rr_pair(k, t, np, p, q);
+        double *__restrict__ mp = M + (size_t)np * p;
+        double *__restrict__ mq = M + (size_t)np * q;
+        double g = 0.0;
+        for (int r = lane; r < np; r += 32) g = fma(mp[r], mq[r], g);
+        g = warp_sum(g);
+        const double a = lam[p], b = lam[q];
+        if (g != 0.0 && g * g > tol2 * a * b) {  // warp-uniform
+          if (lane == 0) conv[sweep % 3] = 0;
+          const double zeta = (b - a) / (2.0 * g);
+          const double tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double c = rsqrt(fma(tt, tt, 1.0)), s = tt * c;
+          double *__restrict__ vp = V + (size_t)np * p;
+          double *__restrict__ vq = V + (size_t)np * q;
+          for (int r = lane; r < np; r += 32) {
+            const double x = mp[r], y = mq[r];
+            const double u = vp[r], z = vq[r];
+            mp[r] = c * x - s * y;
+            mq[r] = s * x + c * y;
+            vp[r] = c * u - s * z;
+            vq[r] = s * u + c * z;
+          }
+          if (lane == 0) {
+            lam[p] = a - tt * g;
+            lam[q] = b + tt * g;
+          }
+        }
+      }
+      grid.sync();
+    }
+    sweeps = sweep + 1;
+    if (*(volatile int *)&conv[sweep % 3]) break;  // identical in every thread after the sync
+  }
+  if (gtid == 0 && info) *info = sweeps;
+  for (int k = gw; k < np; k += nw) {  // lambda_k = v_k^T m_k
+    double d = 0.0;
+    for (int r = lane; r < np; r += 32) d = fma(V[r + (size_t)np * k], M[r + (size_t)np * k], d);
+    d = warp_sum(d);
+    if (lane == 0) lam[k] = d;
+  }
+  grid.sync();
+  for (int64_t i = gtid; i < n; i += gthr) {  // sort descending (ties by index)
+    const double di = lam[i];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double dj = lam[j];
+      if (dj > di || (dj == di && j < i)) ++rank;
+    }
+    w[rank] = di;
+    for (int r = 0; r < n; ++r) Vout[r + (int64_t)n * rank] = V[r + (size_t)np * i];
+  }
+}
+
 // Eigenpairs of a PSD Gram G (n <= 64), preconditioned one-sided Jacobi (Drmac-Veselic
 // style): pivoted Cholesky G = M M^T with M = P L (diagonal pivoting, ties to the smallest
 // index, stops at rank when the largest remaining diagonal is <= n eps max diag(G); rows are
@@ -1187,9 +1283,25 @@ void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps, 
   RT_LAUNCH(c, (jacobi_kernel<KL, true>), 1, thr, need, A, n, w, V, (double *)nullptr, tol, max_sweeps, sweeps, gate)
     if (np <= 64) { RT_EIG(8); } else { RT_EIG(32); }
 #undef RT_EIG
-  } else {  // matrices and vectors in global memory, pairs computed on the fly
+  } else {  // matrices in global memory (L2): the whole GPU, one warp per pair, grid-synchronised
+    static const bool one_cta = getenv("RTUCKER_EIG_ONE_CTA") != nullptr;
     DevBuf<double> ws(c, 2 * (size_t)np * np + np);
-    RT_LAUNCH(c, (jacobi_kernel<32, false>), 1, kEigT, 0, A, n, w, V, ws.p, tol, max_sweeps, sweeps, gate);
+    if (one_cta) {
+      RT_LAUNCH(c, (jacobi_kernel<32, false>), 1, kEigT, 0, A, n, w, V, ws.p, tol, max_sweeps, sweeps, gate);
+    } else {
+      DevBuf<int> conv(c, 3);
+      int nb = 0;
+      RT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, jacobi_grid_kernel, kEigGT, 0));
+      const int grid = std::max(1, std::min(c.num_sms * std::max(nb, 1), (np / 2 + 7) / 8));
+      double *wsp = ws.p;
+      int *convp = conv.p;
+      double tl = tol;
+      int ms = max_sweeps;
+      void *args[] = {(void *)&A, (void *)&n, (void *)&w, (void *)&V, (void *)&wsp, (void *)&convp,
+                      (void *)&tl, (void *)&ms, (void *)&sweeps, (void *)&gate};
+      RT_CUDA(cudaLaunchCooperativeKernel((const void *)jacobi_grid_kernel, dim3(grid), dim3(kEigGT), args, 0, c.stream));
+      c.launches++;
+    }
   }
 }
 

@@ -108,8 +108,11 @@ def test_householder_qr(ctx, m, n):
         assert np.linalg.norm(y - q @ (q.T @ y)) <= 1e-12 * np.linalg.norm(y)
 
 
-@pytest.mark.parametrize("n", [1, 2, 7, 10, 30, 60, 64, 65])
+@pytest.mark.parametrize("n", [1, 2, 7, 10, 30, 60, 64, 65, 150])
 def test_sym_eig(ctx, n):
+    """Unpreconditioned one-sided Jacobi on the Gram against LAPACK eigh.  n <= ~110: one CTA
+    with the matrices in shared memory; n = 150: the grid-synchronised variant
+    (jacobi_grid_kernel, one warp per pair) used by the adaptive variant's large ranks."""
     rng = np.random.default_rng(n)
     u, _ = np.linalg.qr(rng.standard_normal((n, n)))
     lam = np.sort(np.logspace(0, -12, n) * (1 + 0.1 * rng.random(n)))[::-1]
