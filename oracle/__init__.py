@@ -19,12 +19,12 @@ in their docstring.
 from .philox import philox4x32_10, philox_words, omega_rows  # noqa: F401
 from .tensor import (  # noqa: F401
     unfold, fold, mode_product, multi_mode_product, frob, reconstruct, rel_error,
-    approx_distance, unfold_columns,
+    approx_distance, unfold_columns, projector_distance, spectral_gap_kappa,
 )
 from .algorithms import (  # noqa: F401
     TuckerResult, SpTuckerResult, randsvd, r_hosvd, r_sthosvd, adapt_range_finder,
     adaptive_r_sthosvd, adaptive_r_hosvd, hosvd, sthosvd, sp_sthosvd, sp_hosvd,
-    auto_order, rank_caps,
+    auto_order, rank_caps, canonical_signs,
 )
 from .srrqr import cpqr_select, srrqr_select, oblique_factor  # noqa: F401
 from .bounds import delta_tail, bound_expected_error, bound_sp, g_cond, f_p  # noqa: F401

@@ -103,15 +103,17 @@ def r_hosvd(x: np.ndarray, ranks, p: int, seed: int = 0) -> TuckerResult:
     then G = X x_1 A_1^T ... x_d A_d^T."""
     x = np.asarray(x, dtype=np.float64)
     d = x.ndim
-    factors, rr, ells = [None] * d, [0] * d, [0] * d
+    factors, rr, ells, svals = [None] * d, [0] * d, [0] * d, [None] * d
     for j in range(d):                                    # for j = 1:d
         ell, r = rank_caps(x.shape, j, ranks[j], p)
         xj = unfold(x, j)
         om = _omega_for(seed, j, xj.shape[1], ell)        # draw Omega_j
-        u, _, _, _ = randsvd(xj, r, ell - r, om)          # RandSVD(X_(j), r_j, p, Omega_j)
+        u, _, _, info = randsvd(xj, r, ell - r, om)       # RandSVD(X_(j), r_j, p, Omega_j)
         factors[j], rr[j], ells[j] = u, r, ell            # A_j <- U_hat
+        svals[j] = info["s_all"]                          # (diagnostic: projector-test gate)
     core = multi_mode_product(x, factors, transpose=True) # G = X x_j A_j^T
-    return TuckerResult(core, factors, tuple(rr), tuple(ells), tuple(range(d)), seed)
+    return TuckerResult(core, factors, tuple(rr), tuple(ells), tuple(range(d)), seed,
+                        extra=dict(s_all=svals))
 
 
 def r_sthosvd(x: np.ndarray, ranks, p: int, seed: int = 0, order=None) -> TuckerResult:
@@ -121,17 +123,18 @@ def r_sthosvd(x: np.ndarray, ranks, p: int, seed: int = 0, order=None) -> Tucker
     d = x.ndim
     order = auto_order(x.shape) if order is None else tuple(order)
     g = x                                                 # G = X
-    factors, rr, ells, res = [None] * d, [0] * d, [0] * d, {}
+    factors, rr, ells, res, svals = [None] * d, [0] * d, [0] * d, {}, [None] * d
     for j in order:
         ell, r = rank_caps(g.shape, j, ranks[j], p)
         gj = unfold(g, j)
         om = _omega_for(seed, j, gj.shape[1], ell)        # Omega_{rho_j}, current dims
-        u, s, vt, _ = randsvd(gj, r, ell - r, om)
+        u, s, vt, info = randsvd(gj, r, ell - r, om)
+        svals[j] = info["s_all"]                          # (diagnostic: projector-test gate)
         factors[j], rr[j], ells[j] = u, r, ell            # A_{rho_j} <- U_hat
         g_new = fold(s[:, None] * vt, j, g.shape)         # G_(rho_j) <- Sigma_hat V_hat^T
         res[j] = float(np.sum(g * g) - np.sum(g_new * g_new))
         g = g_new
-    return TuckerResult(g, factors, tuple(rr), tuple(ells), order, seed, res)
+    return TuckerResult(g, factors, tuple(rr), tuple(ells), order, seed, res, dict(s_all=svals))
 
 
 def adapt_range_finder(xm: np.ndarray, tau_sq: float, b: int, seed: int, mode: int,

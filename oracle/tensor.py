@@ -75,7 +75,33 @@ def rel_error(x: np.ndarray, core: np.ndarray, factors) -> float:
 
 
 def approx_distance(x: np.ndarray, t1, t2) -> float:
-    """delta = ||X_hat1 - X_hat2||_F / ||X||_F (DESIGN §5 parity metric)."""
+    """delta = ||X_hat1 - X_hat2||_F / ||X||_F (DESIGN §5 parity metric; SURVEY c.4: a
+    direct elementwise difference of the two reconstructions, not core algebra).
+    Pinned by closed forms in tests/test_oracle_tensor.py (2/sqrt(14) between the rank-2
+    and rank-1 truncations of the S:105 superdiagonal tensor)."""
     a = reconstruct(t1[0], t1[1])
     b = reconstruct(t2[0], t2[1])
     return frob(a - b) / frob(np.asarray(x, dtype=np.float64))
+
+
+def projector_distance(a: np.ndarray, b: np.ndarray) -> float:
+    """||A A^T - B B^T||_2 for two orthonormal bases of equal width (north_star parity
+    criterion, SURVEY c.4).  For equal dimensions this is the sine of the largest principal
+    angle, evaluated as ||(I - B B^T) A||_2 (no cancellation for small angles).  Pinned by
+    the closed form sin(theta) for planes rotated by theta (tests/test_oracle_tensor.py)."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if a.shape != b.shape:
+        raise ValueError("projector_distance: bases of different shapes")
+    return float(np.linalg.norm(a - b @ (b.T @ a), 2))
+
+
+def spectral_gap_kappa(s, r: int, u: float) -> float:
+    """Gate of the projector criterion (SURVEY c.4): kappa = u * s_1 / (s_r - s_{r+1}) for the
+    singular values s of B (descending) and the working unit roundoff u; the criterion
+    applies when kappa <= 1e-5.  r = len(s) (no s_{r+1}) gives kappa = 0."""
+    s = np.asarray(s, dtype=np.float64)
+    if r >= s.size:
+        return 0.0
+    gap = s[r - 1] - s[r]
+    return float("inf") if gap <= 0 else float(u * s[0] / gap)

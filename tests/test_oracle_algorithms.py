@@ -157,3 +157,24 @@ def test_ordering_invariance_of_bound_and_rsthosvd_orders():
     for order in itertools.permutations(range(3)):
         t = O.r_sthosvd(x, r, p, 0, order)
         assert O.rel_error(x, t.core, t.factors) * O.frob(x) <= 1.5 * bound
+
+
+def test_canonical_signs_rule():
+    """Reading R4b: the entry of largest magnitude of each column becomes positive; on a tie
+    of magnitudes the FIRST such row decides; a zero column keeps sign +1."""
+    u = np.array([[0.1, -3.0, 0.0, 2.0],
+                  [-0.5, 2.0, 0.0, -2.0],
+                  [0.5, 1.0, 0.0, 1.0]])
+    s = O.canonical_signs(u)
+    np.testing.assert_array_equal(s, [-1.0, -1.0, 1.0, 1.0])
+    # applied by randsvd: every returned column has a positive largest-magnitude entry
+    rng = np.random.default_rng(5)
+    xm = rng.standard_normal((30, 40))
+    omega = rng.standard_normal((40, 8))
+    uu, _, vt, _ = O.randsvd(xm, 5, 3, omega)
+    idx = np.argmax(np.abs(uu), axis=0)
+    assert np.all(uu[idx, np.arange(5)] > 0)
+    # the sign is applied to (U, V) together, so U S V^T is unchanged
+    u0, s0, vt0 = np.linalg.svd(np.linalg.qr(xm @ omega)[0].T @ xm, full_matrices=False)
+    q = np.linalg.qr(xm @ omega)[0]
+    np.testing.assert_allclose((uu * s0[:5]) @ vt, (q @ u0[:, :5] * s0[:5]) @ vt0[:5], atol=1e-12)

@@ -1,5 +1,9 @@
 """Pins for oracle/tensor.py (unfolding order, mode products, norms)."""
+import math
+
 import numpy as np
+
+import oracle as O
 
 from oracle.tensor import unfold, fold, mode_product, multi_mode_product, frob, unfold_columns
 from workloads import from_first_mode_fastest, to_first_mode_fastest
@@ -69,3 +73,57 @@ def test_mode_product_definition_bruteforce():
             for i3 in range(4):
                 s = sum(x[i1, i2, i3] * a[k, i2] for i2 in range(3))
                 assert abs(y[i1, k, i3] - s) < 1e-12
+
+
+def test_approx_distance_closed_form():
+    """delta between two DIFFERENT Tuckers has a closed form (the metric was only
+    ever checked at 0).  Superdiagonal (3,2,1) of S:105: its rank-(2,2,2) truncation is
+    diag(3,2,0) and its rank-(1,1,1) truncation diag(3,0,0), so
+    ||X_hat2 - X_hat1||_F / ||X||_F = 2 / sqrt(14)."""
+    from workloads import superdiagonal
+    x = superdiagonal([3.0, 2.0, 1.0])
+    e = np.eye(3)
+    g2 = np.zeros((2, 2, 2))
+    g2[0, 0, 0], g2[1, 1, 1] = 3.0, 2.0
+    t2 = (g2, [e[:, :2]] * 3)
+    t1 = (np.full((1, 1, 1), 3.0), [e[:, :1]] * 3)
+    assert abs(O.approx_distance(x, t2, t1) - 2 / math.sqrt(14)) < 1e-15
+    assert abs(O.approx_distance(x, t1, t2) - 2 / math.sqrt(14)) < 1e-15
+    # the full tensor against its rank-1 truncation: sqrt(2^2 + 1^2) / sqrt(14)
+    t3 = (x, [e] * 3)
+    assert abs(O.approx_distance(x, t3, t1) - math.sqrt(5 / 14)) < 1e-15
+    # sign/basis invariance: flipping a factor column and the matching core slice is the
+    # same approximation (distance 0), flipping only the factor is not (distance 2*2/sqrt(14))
+    f = [e[:, :2].copy() for _ in range(3)]
+    f[1][:, 1] *= -1
+    g = g2.copy()
+    g[:, 1, :] *= -1
+    assert O.approx_distance(x, t2, (g, f)) < 1e-15
+    assert abs(O.approx_distance(x, t2, (g2, f)) - 4 / math.sqrt(14)) < 1e-15
+
+
+def test_projector_distance_closed_form():
+    """||A A^T - B B^T||_2 = sin(theta) for two planes in R^4 sharing one direction and
+    rotated by theta in the other (largest principal angle theta); 0 for a rotated basis of
+    the same subspace; 1 for orthogonal complements."""
+    for th in (1e-9, 1e-5, 0.3, 1.2):
+        a = np.zeros((4, 2))
+        a[0, 0] = a[1, 1] = 1.0
+        b = np.zeros((4, 2))
+        b[0, 0] = 1.0
+        b[1, 1], b[2, 1] = math.cos(th), math.sin(th)
+        assert abs(O.projector_distance(a, b) - math.sin(th)) <= 1e-15 + 1e-13 * math.sin(th)
+    rng = np.random.default_rng(0)
+    q = np.linalg.qr(rng.standard_normal((9, 3)))[0]
+    rot = np.linalg.qr(rng.standard_normal((3, 3)))[0]
+    assert O.projector_distance(q, q @ rot) < 1e-15
+    full = np.linalg.qr(rng.standard_normal((6, 6)))[0]
+    assert abs(O.projector_distance(full[:, :3], full[:, 3:]) - 1.0) < 1e-14
+
+
+def test_spectral_gap_kappa():
+    """kappa = u s_1 / (s_r - s_{r+1}) (SURVEY c.4 gate)."""
+    s = np.array([4.0, 2.0, 1.5, 1.0])
+    assert abs(O.spectral_gap_kappa(s, 2, 1e-16) - 1e-16 * 4.0 / 0.5) < 1e-30
+    assert O.spectral_gap_kappa(s, 4, 1e-16) == 0.0
+    assert O.spectral_gap_kappa(np.array([1.0, 1.0]), 1, 1e-16) == float("inf")
