@@ -39,6 +39,22 @@ def _oracle(algo, x, ranks, p, seed, order=None):
     return O.r_hosvd(x, ranks, p, seed)
 
 
+def _check_projectors(g, o, fp64):
+    """North-star projector criterion (SURVEY c.4): ||A_g A_g^T - A_o A_o^T||_2 <= 1e-4 (fp32
+    data) / 1e-10 (fp64 data) for every mode whose spectral gap allows it, i.e. where the
+    oracle's kappa = u s_1 / (s_r - s_{r+1}) of B is <= 1e-5.  Returns the gated modes."""
+    u = 2.0 ** -53 if fp64 else 2.0 ** -24
+    gated = []
+    for j, (ag, ao) in enumerate(zip(g.factors, o.factors)):
+        s = o.extra["s_all"][j]
+        if O.spectral_gap_kappa(s, ao.shape[1], u) > 1e-5:
+            continue
+        pd = O.projector_distance(ag, ao)
+        assert pd <= (1e-10 if fp64 else 1e-4), (j, pd)
+        gated.append(j)
+    return gated
+
+
 def _check(x, g, o, fp64):
     delta = O.approx_distance(x, (g.core, g.factors), (o.core, o.factors))
     eg = O.rel_error(x, g.core, g.factors)
@@ -51,6 +67,8 @@ def _check(x, g, o, fp64):
         assert abs(eg - eo) <= 1e-5 * eo, (eg, eo)
     for a in g.factors:
         assert np.linalg.norm(a.T @ a - np.eye(a.shape[1])) <= 1e-12 * a.shape[1]
+    if "s_all" in o.extra:
+        _check_projectors(g, o, fp64)
     return delta, eg, eo
 
 
@@ -99,6 +117,18 @@ def test_fp32_parity(ctx, algo, name, make, ranks, p, order):
     g = _run(ctx, algo, x, ranks, p, seed=1, order=order)
     o = _oracle(algo, x, ranks, p, 1, order)
     _check(x, g, o, False)
+
+
+def test_projector_criterion_c2(ctx):
+    """C2 (BASELINE configs[1]) R-STHOSVD/R-HOSVD: the projector criterion is applied on every
+    mode the gap allows, and it must allow at least one (the oracle's kappa for mode 3 is
+    5.4e-6; SURVEY c.4 expects distances of 2-5e-5)."""
+    x = tucker_c2()
+    for algo in ("sthosvd", "hosvd"):
+        g = _run(ctx, algo, x, (20, 20, 40), 10, seed=0)
+        o = _oracle(algo, x, (20, 20, 40), 10, 0)
+        _check(x, g, o, False)
+        assert len(_check_projectors(g, o, False)) >= 1
 
 
 def test_fp32_fp64_policy_is_tighter(ctx):
@@ -213,6 +243,39 @@ def test_c4_full_size_rsthosvd(ctx):
         t = O.mode_product(t, g.factors[j].T @ o.factors[j], j)
     d2 = np.sum(g.core ** 2) + np.sum(o.core ** 2) - 2 * np.sum(g.core * t)
     assert np.sqrt(max(d2, 0.0) / nx2) <= 1e-5
+    # projector criterion where the gap allows (SURVEY c.4).  At C4 the kappa gate excludes
+    # every mode (s_50 - s_51 ~ 8.5e-5 s_1, kappa ~ 7e-4); the distances are printed
+    _check_projectors(g, o, False)
+    print("C4 R-STHOSVD projector distances",
+          [O.projector_distance(a, b) for a, b in zip(g.factors, o.factors)])
+
+
+@pytest.mark.slow
+def test_c4_full_size_rhosvd(ctx):
+    """BASELINE configs[3] R-HOSVD at full size (800^3 fp32, r=50, p=10) in bench.py's
+    launch configuration (--algo hosvd) against the full oracle run on the same bits:
+    |e_gpu - e_or| <= 1e-5 e_or, delta <= 1e-5, projector criterion where the gap allows."""
+    import torch
+    xd = odeco(800, seed=4, dtype=np.float32, device="cuda")
+    from paper_1905_07311_b200.rtucker import RESULT_HOST
+    g = ctx.hosvd(xd, (800, 800, 800), (50, 50, 50), 10, 0, RESULT_HOST).numpy()
+    x = xd.cpu().numpy().reshape((800, 800, 800), order="F")
+    del xd
+    torch.cuda.empty_cache()
+    o = O.r_hosvd(x, (50, 50, 50), 10, 0)
+    nx2 = float(np.sum(x.astype(np.float64) ** 2))
+    # R-HOSVD factors are orthonormal and G = X x_j A_j^T, so ||X - X_hat||^2 = ||X||^2 - ||G||^2
+    eg = np.sqrt(max(0.0, 1 - np.sum(g.core ** 2) / nx2))
+    eo = np.sqrt(max(0.0, 1 - np.sum(o.core ** 2) / nx2))
+    assert abs(eg - eo) <= 1e-5 * eo, (eg, eo)
+    t = o.core
+    for j in range(3):
+        t = O.mode_product(t, g.factors[j].T @ o.factors[j], j)
+    d2 = np.sum(g.core ** 2) + np.sum(o.core ** 2) - 2 * np.sum(g.core * t)
+    assert np.sqrt(max(d2, 0.0) / nx2) <= 1e-5
+    _check_projectors(g, o, False)
+    print("C4 R-HOSVD projector distances",
+          [O.projector_distance(a, b) for a, b in zip(g.factors, o.factors)])
 
 
 @pytest.mark.parametrize("algo", ["sthosvd", "hosvd"])

@@ -54,6 +54,18 @@ def _sketch_ref(x, mode, ell, seed, k0=0):
     return xm @ O.omega_rows(seed, mode, np.arange(xm.shape[1]), ell, k0=k0)
 
 
+def _check_elementwise(got, x, mode, ell, seed, k0, rel):
+    """Element-by-element check of a sketch against the oracle product: every entry within
+    rel * (|X_(n)| |Omega|)_ik, the scale of the rounding-error bound of that entry's dot
+    product (a wrong or missing element cannot hide in a Frobenius norm)."""
+    xm = O.unfold(np.asarray(x, dtype=np.float64), mode)
+    om = O.omega_rows(seed, mode, np.arange(xm.shape[1]), ell, k0=k0)
+    ref = xm @ om
+    scale = np.abs(xm) @ np.abs(om)
+    bad = np.abs(got - ref) > rel * scale + 1e-300
+    assert not bad.any(), (int(bad.sum()), np.argwhere(bad)[:5])
+
+
 CASES = [
     ("hilbert50", lambda: hilbert((50, 50, 50), "shifted"), [10, 64, 70]),
     ("ragged", lambda: np.asfortranarray(np.random.default_rng(1).standard_normal((37, 41, 29))), [13, 33]),
@@ -74,6 +86,7 @@ def test_sketch_all_modes(ctx, name, make, ells):
             ref = _sketch_ref(x, mode, ell, 11)
             err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
             assert err <= tol, (name, mode, ell, err)
+            _check_elementwise(got, x, mode, ell, 11, 0, 1e-14 if x.dtype == np.float64 else 1e-6)
 
 
 def test_sketch_fp32_with_fp64_policy(ctx):
@@ -90,6 +103,7 @@ def test_sketch_block_offset(ctx):
     got = ctx.debug_sketch(x, x.shape, 1, 6, seed=9, k0=13)
     ref = _sketch_ref(x, 1, 6, 9, k0=13)
     np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+    _check_elementwise(got, x, 1, 6, 9, 13, 1e-14)
 
 
 @pytest.mark.parametrize("m,n", [(800, 60), (50, 10), (25, 10), (1000, 1), (64, 64), (4096, 15)])
@@ -142,6 +156,7 @@ def test_sketch_tc_mode1(ctx, shape, ell, k0):
     err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     colerr = np.max(np.linalg.norm(got - ref, axis=0) / np.linalg.norm(ref, axis=0))
     assert err <= 1e-5 and colerr <= 2e-5, (err, colerr)
+    _check_elementwise(got, x, 0, ell, 5, k0, 1e-6)
 
 
 @pytest.mark.parametrize("shape,mode,ell,k0", [((80, 800, 30), 1, 60, 0), ((16, 96, 9), 1, 33, 4), ((40, 24, 200), 2, 20, 0),
@@ -157,6 +172,7 @@ def test_sketch_tc_kmajor(ctx, shape, mode, ell, k0):
     err = np.linalg.norm(got - ref) / np.linalg.norm(ref)
     colerr = np.max(np.linalg.norm(got - ref, axis=0) / np.linalg.norm(ref, axis=0))
     assert err <= 1e-5 and colerr <= 2e-5, (err, colerr)
+    _check_elementwise(got, x, mode, ell, 7, k0, 1e-6)
 
 
 @pytest.mark.parametrize("shape,J,graded", [((800, 300, 5), 60, False), ((96, 1001, 3), 17, True), ((64, 50, 7), 64, True),
