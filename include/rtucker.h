@@ -26,13 +26,32 @@
  *  - Input descriptors are BORROWED and never modified.  Device inputs must stay alive
  *    until the work enqueued on the context stream has completed; host inputs
  *    (memory = RTUCKER_HOST) are copied to the device inside the call.
- *  - Results are owned by the library and released with rtucker_result_free().  With
- *    RTUCKER_RESULT_HOST the core/factors are host (pinned) memory, else device memory.
- *  - Calls enqueue work on the context stream.  Every call that returns host metadata
- *    (realised ranks of the adaptive variant, nnz of the sparse variant, any
- *    RTUCKER_RESULT_HOST result) synchronises that stream before returning.
+ *  - Device workspace and device results are allocated stream-ordered on the context
+ *    stream through the context's allocator: the caller's rtucker_alloc_fn/rtucker_free_fn
+ *    hooks when given to rtucker_ctx_create (the Python binding routes them to torch's
+ *    caching allocator), else a memory pool owned by the library (created per context;
+ *    the device's default pool and its attributes are not touched).
+ *  - Results are owned by the library and released with rtucker_result_free(), which
+ *    synchronises the context stream (asynchronous copies into the result struct must land
+ *    before it is recycled).  With RTUCKER_RESULT_HOST the core/factors are host (pinned)
+ *    memory, else device memory.
+ *  - Calls enqueue work on the context stream.  The fixed-rank calls (rtucker_hosvd,
+ *    rtucker_sthosvd) on device results do NOT synchronise: the device buffers are valid in
+ *    stream order, and the host fields norm_sq / mode_residual_sq are filled by asynchronous
+ *    copies, valid only after rtucker_sync() (or any synchronising call).  Every call that
+ *    returns host metadata (realised ranks of the adaptive variant, nnz of the sparse
+ *    variant, any RTUCKER_RESULT_HOST result) synchronises the stream before returning.
+ *
+ * Multi-GPU (one context per rank, NCCL communicator of the library): every rank calls the
+ * same function with identical scalar arguments.  Dense inputs must be SHARDED along the
+ * last mode on every rank (shard_extent >= 1, so I_d >= nranks), the shards of all ranks
+ * tiling [0, I_d) in rank order; the sparse variant takes each rank's own nonzeros (a
+ * partition of the tensor's nonzeros).  Results are replicated on every rank.
  *
  * Errors: every call returns an rtucker_status; rtucker_last_error() gives a message.
+ *  Kernel-side conditions (a Jacobi eigensolve that did not converge within its sweep cap,
+ *  shards that do not tile the last mode) are recorded in a device status word and
+ *  returned as RTUCKER_ENUMERIC / RTUCKER_EINVAL by the next synchronising call.
  *  RTUCKER_EINVAL       invalid argument (d<1, dim<1, r_n not in [1, I_n], p<0, tol not in
  *                       (0,1), block<1, order not a permutation, eta<1, strict-cap
  *                       violation, SP cap r_n+p >= min(I_n, prod others), ...)
@@ -84,6 +103,13 @@ typedef enum { RTUCKER_DEVICE = 0, RTUCKER_HOST = 1 } rtucker_memory;
 #define RTUCKER_ADAPT_HOSVD       (1u << 4)  /* adaptive: Alg 4 (modes independent) instead of Alg 5 */
 #define RTUCKER_RESULT_HOST       (1u << 5)  /* copy core/factors to host memory */
 #define RTUCKER_NO_CORE           (1u << 6)  /* R-HOSVD: factors only */
+/* Determinism: every path uses fixed-order reductions and no floating-point
+ * atomics, so reruns with the same inputs and GPU count are bit-identical.  The flag is
+ * the default behaviour and is accepted for clarity. */
+#define RTUCKER_DETERMINISTIC     (1u << 7)
+/* Debug checks: index-range and finite-value checks of the inputs, and a stream
+ * synchronisation with error check after every step (slow; for debugging). */
+#define RTUCKER_DEBUG_CHECKS      (1u << 8)
 
 /* Dense tensor, first-mode-fastest.  When the tensor is sharded across ranks along its
  * LAST mode, dims[] are the GLOBAL dims and this rank holds the contiguous slab of
@@ -111,6 +137,12 @@ typedef struct {
 } rtucker_coo_desc;
 
 typedef struct rtucker_ctx rtucker_ctx; /* one per GPU / rank; not thread-safe */
+
+/* Allocation hooks: alloc returns `bytes` of device memory usable in stream order on
+ * `stream` (a cudaStream_t), or NULL on failure (-> RTUCKER_ENOMEM); free releases it in
+ * stream order.  `user` is passed through. */
+typedef void *(*rtucker_alloc_fn)(size_t bytes, void *stream, void *user);
+typedef void (*rtucker_free_fn)(void *ptr, void *stream, void *user);
 
 /* Result of a decomposition.  core / factors are fp64 (dtype field) for dense
  * algorithms; the SP core keeps the input value dtype (values copied exactly). */
@@ -140,9 +172,11 @@ typedef struct {
 
 /* Context.  device: CUDA ordinal.  cuda_stream: cudaStream_t to enqueue on (NULL =
  * a library-created stream).  nccl_unique_id: NULL for single-GPU, else the 128-byte
- * ncclUniqueId shared by all ranks (NCCL is loaded at run time). */
+ * ncclUniqueId shared by all ranks (NCCL is loaded at run time).  alloc_fn / free_fn:
+ * allocation hooks (both NULL = library-owned pool; both or neither must be given). */
 rtucker_status rtucker_ctx_create(int device, void *cuda_stream, const void *nccl_unique_id,
-                                  int rank, int nranks, rtucker_ctx **out);
+                                  int rank, int nranks, rtucker_alloc_fn alloc_fn,
+                                  rtucker_free_fn free_fn, void *alloc_user, rtucker_ctx **out);
 void rtucker_ctx_destroy(rtucker_ctx *ctx);
 rtucker_status rtucker_ctx_set_stream(rtucker_ctx *ctx, void *cuda_stream);
 const char *rtucker_last_error(const rtucker_ctx *ctx);
@@ -181,7 +215,9 @@ void rtucker_result_free(rtucker_ctx *ctx, rtucker_result *res);
 /* Stream-ordered copy on the context stream (plumbing for bindings): kind as in
  * cudaMemcpyKind (0 H2H, 1 H2D, 2 D2H, 3 D2D, 4 default). */
 rtucker_status rtucker_memcpy(rtucker_ctx *ctx, void *dst, const void *src, size_t bytes, int kind);
-/* Blocks until all work enqueued on the context stream has completed. */
+/* Blocks until all work enqueued on the context stream has completed; then reports (and
+ * clears) the device status word: RTUCKER_ENUMERIC for a non-converged eigensolve,
+ * RTUCKER_EINVAL for a shard layout that does not tile the last mode. */
 rtucker_status rtucker_sync(rtucker_ctx *ctx);
 
 /* Phase timing for measurement: when enabled, CUDA events are recorded on the context

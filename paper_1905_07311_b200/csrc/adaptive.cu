@@ -127,7 +127,7 @@ ModeOut adapt_mode(Ctx &c, const void *G, DT gt, const int64_t *cur, int d, int 
   const ModeView vb{v.L, k, v.R};
   if (!truncate || k == 0) {
     out.r = k;
-    RT_CUDA(cudaMallocAsync((void **)&out.A, sizeof(double) * I * std::max(k, 1), c.stream));
+    out.A = (double *)dev_alloc(c, sizeof(double) * I * std::max(k, 1));
     if (k > 0) RT_CUDA(cudaMemcpyAsync(out.A, Q.p, sizeof(double) * I * k, cudaMemcpyDeviceToDevice, c.stream));
     out.G = std::move(B);
     out.gt = store;
@@ -152,7 +152,7 @@ ModeOut adapt_mode(Ctx &c, const void *G, DT gt, const int64_t *cur, int d, int 
     }
   }
   out.r = r;
-  RT_CUDA(cudaMallocAsync((void **)&out.A, sizeof(double) * I * r, c.stream));
+  out.A = (double *)dev_alloc(c, sizeof(double) * I * r);
   gemm_small(c, false, Q.p, I, U.p, k, out.A, I, I, r, k);
   canonical_signs(c, out.A, I, r, U.p, k, k);
   if (want_core) {
@@ -225,7 +225,7 @@ rtucker_result *run_adaptive(Ctx &c, const rtucker_dense_desc *X, double tol, in
     res->order[jj] = n;
     if (eps[n] == 0.0) {  // mode not compressed: A = I (reading R8)
       double *A = nullptr;
-      RT_CUDA(cudaMallocAsync((void **)&A, sizeof(double) * cur[n] * cur[n], c.stream));
+      A = (double *)dev_alloc(c, sizeof(double) * cur[n] * cur[n]);
       std::vector<double> eye((size_t)cur[n] * cur[n], 0.0);
       for (int64_t i = 0; i < cur[n]; ++i) eye[i + cur[n] * i] = 1.0;
       RT_CUDA(cudaMemcpyAsync(A, eye.data(), sizeof(double) * eye.size(), cudaMemcpyHostToDevice, c.stream));
@@ -277,7 +277,7 @@ rtucker_result *run_adaptive(Ctx &c, const rtucker_dense_desc *X, double tol, in
     gt = gc;
   }
   const int64_t ncore = prod(cur, d);
-  RT_CUDA(cudaMallocAsync(&res->core, sizeof(double) * std::max<int64_t>(ncore, 1), c.stream));
+  res->core = dev_alloc(c, sizeof(double) * std::max<int64_t>(ncore, 1));
   convert(c, G, gt, res->core, DT::F64, ncore);
   finish_result(c, res, flags);
   RT_CUDA(cudaStreamSynchronize(c.stream));

@@ -560,7 +560,7 @@ void column_maxima(Ctx &c, const float *X, ModeView v, uint32_t *cm) {
 }
 
 bool ozaki_bpass_enabled() {
-  static const bool off = getenv("RTUCKER_NO_OZAKI") != nullptr;
+  static const bool off = RT_EXP_GETENV("RTUCKER_NO_OZAKI") != nullptr;
   return !off;
 }
 
@@ -572,7 +572,7 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
   if (!ozaki_bpass_enabled() || J < 1 || J > kON || (v.I % 4) != 0 || v.I > 26000 ||
       (((uintptr_t)X) & 15) != 0 || v.R > (int64_t)INT32_MAX - kOP)
     return false;
-  if (lg && (out || !gram || (v.L % 4) != 0 || v.L > (int64_t)INT32_MAX - kOP || getenv("RTUCKER_NO_OZAKI_LG")))
+  if (lg && (out || !gram || (v.L % 4) != 0 || v.L > (int64_t)INT32_MAX - kOP || RT_EXP_GETENV("RTUCKER_NO_OZAKI_LG")))
     return false;
   const int64_t I = v.I, P = v.L * v.R;
   const int nchunk = (int)((I + kOK - 1) / kOK);
@@ -603,7 +603,7 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
   // Gram of B in the epilogue (DMMA, 36 upper 8x8 tiles per 128-column tile).  The alternative,
   // a separate pass over B (gram64_kernel, RTUCKER_OZ_GRAM_SEPARATE), measured slower at C4
   // (B-pass + Gram 1.37 vs 0.82 ms).
-  static const bool gsep_env = getenv("RTUCKER_OZ_GRAM_SEPARATE") != nullptr;
+  static const bool gsep_env = RT_EXP_GETENV("RTUCKER_OZ_GRAM_SEPARATE") != nullptr;
   const bool gsep = gram && out && gsep_env;
   if (gram && !gsep) part.alloc(c, (size_t)grid * 4096);
   prm.gram_partial = (gram && !gsep) ? part.p : nullptr;
@@ -630,8 +630,8 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
   const size_t smem = 1024 + (size_t)kONSS * kXStB + (size_t)kONQ * kQChB + sizeof(double) * kON * kOTP +
                       8 * (2 * kONSS + 2 * kONQ + 2 * kOXB + 2) + 16 + 8 * kON;
   auto kern = lg ? bpass_ozaki_kernel<true> : bpass_ozaki_kernel<false>;
-  RT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  static const bool prof = getenv("RTUCKER_OZ_PROF") != nullptr;
+  smem_attr(kern, smem);
+  static const bool prof = RT_EXP_GETENV("RTUCKER_OZ_PROF") != nullptr;
   DevBuf<long long> pbuf;
   if (prof) {
     pbuf.alloc(c, 16);

@@ -234,7 +234,7 @@ __global__ void prep_q_kernel(const double *__restrict__ Q, int64_t ldq, int64_t
 // B = Q^T X_(n) for fp32 X with L == 1 (B[k + ell c]); Q fp64 I x ell (ld = ldq).  Returns
 // false outside the kernel's envelope (caller falls back to the SIMT TTM).
 bool bpass_tc_mn(Ctx &c, const float *X, ModeView v, const double *Q, int64_t ldq, int ell, void *B, bool out_f64) {
-  static const bool off = getenv("RTUCKER_NO_TC_BPASS") != nullptr;
+  static const bool off = RT_EXP_GETENV("RTUCKER_NO_TC_BPASS") != nullptr;
   if (off || !sketch_tc_enabled() || v.L != 1 || (v.I % 4) != 0 || (v.R % 8) != 0 || ell > 64 || ell < 1) return false;
   if ((((uintptr_t)X) & 15) != 0 || v.R / 8 > (int64_t)INT32_MAX / 2) return false;
   BpassParams p{};
@@ -264,10 +264,10 @@ bool bpass_tc_mn(Ctx &c, const float *X, ModeView v, const double *Q, int64_t ld
   const size_t smem = 1024 + kNS * (2 * kXBytes + 2 * kQBytes) + 256;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(c.num_sms, p.nunits));
   if (out_f64) {
-    RT_CUDA(cudaFuncSetAttribute(bpass_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_attr(bpass_tc_kernel<true>, smem);
     RT_LAUNCH(c, bpass_tc_kernel<true>, grid, kThreads, smem, tm, p);
   } else {
-    RT_CUDA(cudaFuncSetAttribute(bpass_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_attr(bpass_tc_kernel<false>, smem);
     RT_LAUNCH(c, bpass_tc_kernel<false>, grid, kThreads, smem, tm, p);
   }
   return true;

@@ -38,7 +38,23 @@ struct Error : std::runtime_error {
     }                                                                                  \
   } while (0)
 
+// Experimental kernel variants and probes are selected by environment variables only in an
+// experiments build (-DRTUCKER_EXPERIMENTS, e.g. RTUCKER_NVCC_EXTRA=-DRTUCKER_EXPERIMENTS);
+// the shipped library ignores them and always runs the tested path.
+#ifdef RTUCKER_EXPERIMENTS
+#define RT_EXP_GETENV(name) getenv(name)
+#else
+#define RT_EXP_GETENV(name) ((const char *)nullptr)
+#endif
+
 struct Comm;  // comm.cpp
+
+// Device status bits, set by kernels and reported at the next synchronisation point
+// (rtucker_sync or any call that synchronises) as RTUCKER_ENUMERIC.
+enum StatusBit : unsigned {
+  ST_EIG_NOT_CONVERGED = 1u,   // a Jacobi eigensolve hit its sweep cap
+  ST_SHARD_LAYOUT = 2u,        // the shards of a multi-rank call do not tile the last mode
+};
 
 // Phase timing (measurement only): CUDA events recorded on the context stream around
 // each step of the path; resolved lazily by rtucker_phase_times().
@@ -50,6 +66,15 @@ struct PhaseEvent {
 };
 
 struct Ctx {
+  // workspace and result allocations: the caller's hooks (e.g. torch's caching allocator)
+  // when given, else a library-owned stream-ordered pool (the device's default pool is not
+  // touched)
+  rtucker_alloc_fn alloc_fn = nullptr;
+  rtucker_free_fn free_fn = nullptr;
+  void *alloc_user = nullptr;
+  cudaMemPool_t pool = nullptr;
+  unsigned *status = nullptr;       // device status word (StatusBit)
+  bool deterministic = true;        // fixed-order reductions (RTUCKER_NONDETERMINISTIC clears)
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -98,6 +123,37 @@ struct PhaseScope {
   ~PhaseScope() { stop(); }
 };
 
+// Stream-ordered device allocation on the context stream through the context's allocator.
+inline void *dev_alloc(Ctx &c, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  void *p = nullptr;
+  if (c.alloc_fn) {
+    p = c.alloc_fn(bytes, (void *)c.stream, c.alloc_user);
+    if (!p) throw Error(RTUCKER_ENOMEM, "allocation hook returned NULL");
+    return p;
+  }
+  cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, c.pool, c.stream);
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    throw Error(e == cudaErrorMemoryAllocation ? RTUCKER_ENOMEM : RTUCKER_ECUDA,
+                std::string("device allocation failed: ") + cudaGetErrorString(e));
+  }
+  return p;
+}
+inline void dev_free(Ctx &c, void *p) {
+  if (!p) return;
+  if (c.free_fn) c.free_fn(p, (void *)c.stream, c.alloc_user);
+  else cudaFreeAsync(p, c.stream);
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size (host-side cache:
+// the attribute call is not free and most kernels are launched with the same size every call).
+void set_smem_attr(const void *func, size_t bytes);
+template <typename F>
+inline void smem_attr(F *func, size_t bytes) {
+  set_smem_attr((const void *)func, bytes);
+}
+
 // Count every library kernel launch (reported as gpu_launches by bench.py).
 #define RT_LAUNCH(ctx, kern, grid, block, smem, ...)                                   \
   do {                                                                                 \
@@ -112,13 +168,15 @@ struct DevBuf {
   T *p = nullptr;
   size_t n = 0;
   cudaStream_t s = nullptr;
+  Ctx *c = nullptr;
   DevBuf() = default;
-  DevBuf(Ctx &c, size_t count) { alloc(c, count); }
-  void alloc(Ctx &c, size_t count) {
+  DevBuf(Ctx &ctx, size_t count) { alloc(ctx, count); }
+  void alloc(Ctx &ctx, size_t count) {
     release();
-    s = c.stream;
+    c = &ctx;
+    s = ctx.stream;
     n = count;
-    if (count) RT_CUDA(cudaMallocAsync((void **)&p, count * sizeof(T), s));
+    if (count) p = (T *)dev_alloc(ctx, count * sizeof(T));
   }
   void zero() {
     if (n) RT_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
@@ -130,16 +188,16 @@ struct DevBuf {
     return q;
   }
   void release() {
-    if (p) cudaFreeAsync(p, s);
+    if (p) dev_free(*c, p);
     p = nullptr;
     n = 0;
   }
   ~DevBuf() { release(); }
   DevBuf(const DevBuf &) = delete;
   DevBuf &operator=(const DevBuf &) = delete;
-  DevBuf(DevBuf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+  DevBuf(DevBuf &&o) noexcept : p(o.p), n(o.n), s(o.s), c(o.c) { o.p = nullptr; o.n = 0; }
   DevBuf &operator=(DevBuf &&o) noexcept {
-    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; o.p = nullptr; o.n = 0; }
+    if (this != &o) { release(); p = o.p; n = o.n; s = o.s; c = o.c; o.p = nullptr; o.n = 0; }
     return *this;
   }
 };

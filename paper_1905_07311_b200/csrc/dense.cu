@@ -53,47 +53,27 @@ void fill_header(rtucker_result *r, const DenseIn &in, const int32_t *ord, uint6
   r->flags = flags;
 }
 
-// Sketch of the sharded last mode: local rows are complete; gather the row blocks of
-// all ranks into Y (I_glob x ell, column-major).  normsq gets the global ||G||^2.
+// Sketch of the sharded last mode: local rows are complete.  Every rank writes its rows (and
+// a coverage column of ones) into a zeroed global-size buffer at its own offset and the
+// buffers are summed over the ranks: the rows come out bit-exact (x + 0 = x) with no host
+// synchronisation or metadata exchange, and a device check flags shards that do not tile
+// [0, I_d) (status word, reported as EINVAL at the next synchronising call).  normsq gets the
+// global ||G||^2.
 void sketch_last_sharded(Ctx &c, const DenseIn &in, const void *G, DT gt, const int64_t *cur, int ell,
                          uint64_t seed, bool mulf64, double *Y, double *normsq, bool n32) {
   const int d = in.d, n = d - 1;
   const ModeView v = mode_view(cur, d, n);  // v.I = local extent
-  const int64_t ext = v.I;
-  // exchange (offset, extent) of every rank
-  DevBuf<double> meta(c, 2), all(c, 2 * (size_t)c.nranks);
-  double hm[2] = {(double)in.offset, (double)ext};
-  RT_CUDA(cudaMemcpyAsync(meta.p, hm, sizeof hm, cudaMemcpyHostToDevice, c.stream));
-  allgather_f64(c, meta.p, all.p, 2);
-  std::vector<double> ha(2 * c.nranks);
-  RT_CUDA(cudaMemcpyAsync(ha.data(), all.p, sizeof(double) * 2 * c.nranks, cudaMemcpyDeviceToHost, c.stream));
-  RT_CUDA(cudaStreamSynchronize(c.stream));
-  int64_t maxext = 0;
-  std::vector<int64_t> offs(c.nranks), exts(c.nranks);
-  for (int r = 0; r < c.nranks; ++r) {
-    offs[r] = (int64_t)ha[2 * r];
-    exts[r] = (int64_t)ha[2 * r + 1];
-    maxext = std::max(maxext, exts[r]);
-  }
-  DevBuf<double> yl(c, (size_t)maxext * ell + 1);
-  yl.zero();
+  const int64_t ext = v.I, I = in.gdims[n];
+  // [Y (I x ell) | ||G||^2 | coverage (I)]
+  DevBuf<double> buf(c, (size_t)I * ell + 1 + (size_t)I);
+  buf.zero();
   DevBuf<double> ytmp(c, (size_t)ext * ell);
-  sketch_dense(c, G, gt, v, n, ell, 0, seed, 0, mulf64, ytmp.p, yl.p + (size_t)maxext * ell, n32);
-  RT_CUDA(cudaMemcpy2DAsync(yl.p, maxext * sizeof(double), ytmp.p, ext * sizeof(double), ext * sizeof(double),
-                            ell, cudaMemcpyDeviceToDevice, c.stream));
-  RT_CUDA(cudaMemcpyAsync(normsq, yl.p + (size_t)maxext * ell, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
-  allreduce_sum_f64(c, normsq, 1);
-  DevBuf<double> g(c, (size_t)c.nranks * (maxext * ell + 1));
-  allgather_f64(c, yl.p, g.p, (size_t)maxext * ell + 1);
-  // drop the per-rank norm slot: blocks are (maxext*ell + 1) long
-  DevBuf<double> gp(c, (size_t)c.nranks * maxext * ell);
-  RT_CUDA(cudaMemcpy2DAsync(gp.p, maxext * ell * sizeof(double), g.p, (maxext * ell + 1) * sizeof(double),
-                            maxext * ell * sizeof(double), c.nranks, cudaMemcpyDeviceToDevice, c.stream));
-  DevBuf<int64_t> doffs(c, c.nranks), dexts(c, c.nranks);
-  RT_CUDA(cudaMemcpyAsync(doffs.p, offs.data(), sizeof(int64_t) * c.nranks, cudaMemcpyHostToDevice, c.stream));
-  RT_CUDA(cudaMemcpyAsync(dexts.p, exts.data(), sizeof(int64_t) * c.nranks, cudaMemcpyHostToDevice, c.stream));
-  rows_scatter(c, gp.p, c.nranks, maxext, ell, doffs.p, dexts.p, in.gdims[n], Y);
-  RT_CUDA(cudaStreamSynchronize(c.stream));  // host vectors above go out of scope
+  sketch_dense(c, G, gt, v, n, ell, 0, seed, 0, mulf64, ytmp.p, buf.p + (size_t)I * ell, n32);
+  place_rows(c, ytmp.p, ext, ell, in.offset, I, buf.p, buf.p + (size_t)I * ell + 1);
+  allreduce_sum_f64(c, buf.p, buf.n);
+  check_cover(c, buf.p + (size_t)I * ell + 1, I);
+  RT_CUDA(cudaMemcpyAsync(Y, buf.p, sizeof(double) * I * ell, cudaMemcpyDeviceToDevice, c.stream));
+  RT_CUDA(cudaMemcpyAsync(normsq, buf.p + (size_t)I * ell, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
 }
 
 void copy_residuals(Ctx &c, rtucker_result *r, const double *scal, int d, int first_mode) {
@@ -188,7 +168,7 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
     gram_eig(c, gram.p, ell, w.p, V.p, nullptr, rr);
     // ---- Alg 1 line 5: A_n = Q U_B(:, 1:r)
     double *A = nullptr;
-    RT_CUDA(cudaMallocAsync((void **)&A, sizeof(double) * Ig * rr, c.stream));
+    A = (double *)dev_alloc(c, sizeof(double) * Ig * rr);
     res->factors[n] = A;
     gemm_small(c, false, Q.p, Ig, V.p, ell, A, Ig, Ig, rr, ell);
     canonical_signs(c, A, Ig, rr, V.p, ell, ell);  // reading R4b (shrink uses the signed U_B)
@@ -208,7 +188,7 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
     res->ell[n] = ell;
   }
   const int64_t ncore = prod(cur, d);
-  RT_CUDA(cudaMallocAsync(&res->core, sizeof(double) * ncore, c.stream));
+  res->core = dev_alloc(c, sizeof(double) * ncore);
   convert(c, G, gt, res->core, DT::F64, ncore);
   copy_residuals(c, res, scal.p, d, ord[0]);
   finish_result(c, res, flags);
@@ -282,7 +262,7 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
     DevBuf<double> w(c, ell), V(c, (size_t)ell * ell);
     gram_eig(c, gram.p, ell, w.p, V.p, nullptr, rr);
     double *A = nullptr;
-    RT_CUDA(cudaMallocAsync((void **)&A, sizeof(double) * Ig * rr, c.stream));
+    A = (double *)dev_alloc(c, sizeof(double) * Ig * rr);
     res->factors[n] = A;
     gemm_small(c, false, Q.p, Ig, V.p, ell, A, Ig, Ig, rr, ell);
     canonical_signs(c, A, Ig, rr, V.p, ell, ell);  // reading R4b (shrink uses the signed U_B)
@@ -333,7 +313,7 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
       cur[n] = rr;
     }
     const int64_t ncore = prod(cur, d);
-    RT_CUDA(cudaMallocAsync(&res->core, sizeof(double) * ncore, c.stream));
+    res->core = dev_alloc(c, sizeof(double) * ncore);
     convert(c, G, gt, res->core, DT::F64, ncore);
   }
   copy_residuals(c, res, scal.p, d, 0);

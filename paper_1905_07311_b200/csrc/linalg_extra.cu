@@ -24,20 +24,23 @@ __global__ void ttm_expand_kernel(const Tin *__restrict__ X, int64_t L, int64_t 
   }
 }
 
-// Allgathered row blocks [rank][ext][ell] (each block column-major ext x ell) ->
-// column-major (I x ell) with rank blocks at row offsets off[rank].
-__global__ void rows_scatter_kernel(const double *__restrict__ g, int nranks, int64_t ext,
-                                    int ell, const int64_t *__restrict__ offs,
-                                    const int64_t *__restrict__ exts, int64_t I,
-                                    double *__restrict__ Y) {
-  const int64_t n = (int64_t)nranks * ext * ell;
+// Local rows y (ext x ell, column-major) into the zeroed global buffer Y (I x ell) at row
+// offset off, and the coverage column cov[off .. off + ext) = 1.
+__global__ void place_rows_kernel(const double *__restrict__ y, int64_t ext, int ell, int64_t off, int64_t I,
+                                  double *__restrict__ Y, double *__restrict__ cov) {
+  const int64_t n = ext * (ell + 1);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t rk = e / (ext * ell);
-    const int64_t t = e % (ext * ell);
-    const int64_t i = t % ext, k = t / ext;
-    if (i < exts[rk]) Y[offs[rk] + i + I * k] = g[e];
+    const int64_t i = e % ext, k = e / ext;
+    if (k < ell) Y[off + i + I * k] = y[i + ext * k];
+    else cov[off + i] = 1.0;
   }
+}
+
+// After the sum over ranks every row must be covered exactly once.
+__global__ void check_cover_kernel(const double *__restrict__ cov, int64_t I, unsigned *__restrict__ status) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x)
+    if (cov[i] != 1.0) atomicOr(status, (unsigned)ST_SHARD_LAYOUT);
 }
 
 __global__ void sum_first_kernel(const double *__restrict__ w, int r, const double *__restrict__ nsq,
@@ -59,11 +62,14 @@ void ttm_expand(Ctx &c, const void *X, DT in, ModeView v, const double *M, int64
     RT_LAUNCH(c, ttm_expand_kernel<float>, g, 256, 0, (const float *)X, v.L, v.I, v.R, M, ldm, J, out);
 }
 
-void rows_scatter(Ctx &c, const double *g, int nranks, int64_t ext, int ell, const int64_t *offs,
-                  const int64_t *exts, int64_t I, double *Y) {
-  const int64_t n = (int64_t)nranks * ext * ell;
+void place_rows(Ctx &c, const double *y, int64_t ext, int ell, int64_t off, int64_t I, double *Y, double *cov) {
+  const int64_t n = ext * (ell + 1);
   const int gr = std::max(1, std::min(4096, ceil_div(n, 256)));
-  RT_LAUNCH(c, rows_scatter_kernel, gr, 256, 0, g, nranks, ext, ell, offs, exts, I, Y);
+  RT_LAUNCH(c, place_rows_kernel, gr, 256, 0, y, ext, ell, off, I, Y, cov);
+}
+
+void check_cover(Ctx &c, const double *cov, int64_t I) {
+  RT_LAUNCH(c, check_cover_kernel, std::max(1, std::min(64, ceil_div(I, 256))), 256, 0, cov, I, c.status);
 }
 
 void residual_from_eigs(Ctx &c, const double *w, int r, const double *normsq, double *out) {

@@ -22,6 +22,9 @@ void rank_caps(const int64_t *dims, int d, int n, int64_t r, int p, bool strict,
 rtucker_result *new_result(int d);
 void free_result(Ctx &c, rtucker_result *r);
 void finish_result(Ctx &c, rtucker_result *r, uint32_t flags);
+// Synchronises the context stream, reads and clears the device status word (StatusBit) and
+// throws the matching error.
+void check_status(Ctx &c);
 
 // Global unfolding-column offset of this rank's slab for mode n < d-1 (the last mode is
 // sharded): c_glob = c_loc + offset * prod_{k != n, k < d-1} dims_k.

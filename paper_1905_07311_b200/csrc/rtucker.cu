@@ -22,6 +22,34 @@ struct rtucker_ctx {
 
 namespace rt {
 
+void set_smem_attr(const void *func, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void *, size_t>> done;  // largest size set per kernel
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto &e : done)
+    if (e.first == func) {
+      if (e.second >= bytes) return;
+      smem_attr(func, bytes);
+      e.second = bytes;
+      return;
+    }
+  smem_attr(func, bytes);
+  done.emplace_back(func, bytes);
+}
+
+// Reads and clears the device status word (synchronising calls only).
+void check_status(Ctx &c) {
+  unsigned h = 0;
+  RT_CUDA(cudaMemcpyAsync(&h, c.status, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+  RT_CUDA(cudaStreamSynchronize(c.stream));
+  if (!h) return;
+  RT_CUDA(cudaMemsetAsync(c.status, 0, sizeof(unsigned), c.stream));
+  if (h & ST_SHARD_LAYOUT)
+    throw Error(RTUCKER_EINVAL, "the shards of the ranks do not tile the last mode [0, I_d) (rank order)");
+  if (h & ST_EIG_NOT_CONVERGED)
+    throw Error(RTUCKER_ENUMERIC, "a Jacobi eigensolve did not converge within its sweep cap");
+}
+
 // ---------------------------------------------------------------- argument checks --
 static DT to_dt(rtucker_dtype t) {
   if (t == RTUCKER_F32) return DT::F32;
@@ -41,6 +69,9 @@ void prepare_dense(Ctx &c, const rtucker_dense_desc *X, DenseIn &in) {
     in.gdims[k] = X->dims[k];
     in.ldims[k] = X->dims[k];
   }
+  // multi-rank contract (rtucker.h): every rank holds a non-empty slab of the last mode
+  RT_REQUIRE(c.nranks == 1 || X->shard_extent >= 1,
+             "multi-rank calls need a sharded input (shard_extent >= 1 on every rank, so I_d >= nranks)");
   in.sharded = X->shard_extent > 0 && (X->shard_extent != X->dims[in.d - 1] || c.nranks > 1 || c.loopback_sharding);
   in.offset = 0;
   if (X->shard_extent > 0) {
@@ -126,7 +157,7 @@ void free_result(Ctx &c, rtucker_result *r) {
   auto fr = [&](void *p) {
     if (!p) return;
     if (r->memory == RTUCKER_HOST) cudaFreeHost(p);
-    else cudaFreeAsync(p, c.stream);
+    else dev_free(c, p);
   };
   fr(r->core);
   for (int k = 0; k < kMaxModes; ++k) {
@@ -150,7 +181,7 @@ void finish_result(Ctx &c, rtucker_result *r, uint32_t flags) {
     void *h = nullptr;
     RT_CUDA(cudaMallocHost(&h, std::max<size_t>(bytes, 1)));
     RT_CUDA(cudaMemcpyAsync(h, p, bytes, cudaMemcpyDeviceToHost, c.stream));
-    RT_CUDA(cudaFreeAsync(p, c.stream));
+    dev_free(c, p);
     p = h;
   };
   const size_t vs = r->dtype == RTUCKER_F64 ? 8 : 4;
@@ -164,7 +195,7 @@ void finish_result(Ctx &c, rtucker_result *r, uint32_t flags) {
   }
   if (r->core_vals) mv(r->core_vals, r->core_nnz * vs);
   r->memory = RTUCKER_HOST;
-  RT_CUDA(cudaStreamSynchronize(c.stream));
+  check_status(c);  // synchronises
 }
 
 }  // namespace rt
@@ -197,7 +228,7 @@ rtucker_status rtucker_memcpy(rtucker_ctx *ctx, void *dst, const void *src, size
 
 rtucker_status rtucker_sync(rtucker_ctx *ctx) {
   if (!ctx) return RTUCKER_EINVAL;
-  return guard(ctx, [&] { RT_CUDA(cudaStreamSynchronize(ctx->c.stream)); });
+  return guard(ctx, [&] { check_status(ctx->c); });
 }
 
 rtucker_status rtucker_debug_loopback_sharding(rtucker_ctx *ctx, int enabled) {
@@ -236,12 +267,17 @@ rtucker_status rtucker_phase_times(rtucker_ctx *ctx, double *ms, int64_t *counts
 }
 
 rtucker_status rtucker_ctx_create(int device, void *cuda_stream, const void *nccl_unique_id, int rank,
-                                  int nranks, rtucker_ctx **out) {
+                                  int nranks, rtucker_alloc_fn alloc_fn, rtucker_free_fn free_fn,
+                                  void *alloc_user, rtucker_ctx **out) {
   if (!out) return RTUCKER_EINVAL;
   *out = nullptr;
   if (nranks < 1 || rank < 0 || rank >= nranks) return RTUCKER_EINVAL;
   if (nranks > 1 && !nccl_unique_id) return RTUCKER_EINVAL;
+  if ((alloc_fn == nullptr) != (free_fn == nullptr)) return RTUCKER_EINVAL;
   rtucker_ctx *ctx = new rtucker_ctx;
+  ctx->c.alloc_fn = alloc_fn;
+  ctx->c.free_fn = free_fn;
+  ctx->c.alloc_user = alloc_user;
   rtucker_status st = guard(ctx, [&] {
     RT_CUDA(cudaSetDevice(device));
     ctx->c.device = device;
@@ -252,17 +288,25 @@ rtucker_status rtucker_ctx_create(int device, void *cuda_stream, const void *ncc
       ctx->c.own_stream = true;
     }
     RT_CUDA(cudaDeviceGetAttribute(&ctx->c.num_sms, cudaDevAttrMultiProcessorCount, device));
-    // keep freed stream-ordered workspace in the pool between calls (no re-mapping of the
-    // large B / shrunk-core buffers on every decomposition)
-    cudaMemPool_t pool;
-    RT_CUDA(cudaDeviceGetMemPool(&pool, device));
+    // library-owned stream-ordered pool (used when no allocation hooks are given); freed
+    // workspace stays in it between calls (no re-mapping of the large B / shrunk-core
+    // buffers on every decomposition).  The device's default pool is not modified.
+    cudaMemPoolProps pp = {};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = device;
+    RT_CUDA(cudaMemPoolCreate(&ctx->c.pool, &pp));
     uint64_t thr = UINT64_MAX;
-    RT_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    RT_CUDA(cudaMemPoolSetAttribute(ctx->c.pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    RT_CUDA(cudaMalloc((void **)&ctx->c.status, sizeof(unsigned)));
+    RT_CUDA(cudaMemset(ctx->c.status, 0, sizeof(unsigned)));
     ctx->c.rank = rank;
     ctx->c.nranks = nranks;
     if (nranks > 1) ctx->c.comm = comm_create(nccl_unique_id, rank, nranks);
   });
   if (st != RTUCKER_OK) {
+    if (ctx->c.status) cudaFree(ctx->c.status);
+    if (ctx->c.pool) cudaMemPoolDestroy(ctx->c.pool);
     delete ctx;
     return st;
   }
@@ -274,8 +318,13 @@ void rtucker_ctx_destroy(rtucker_ctx *ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->c.stream);
   if (ctx->c.sk_flags) cudaFree(ctx->c.sk_flags);
+  if (ctx->c.status) cudaFree(ctx->c.status);
   comm_destroy(ctx->c.comm);
   if (ctx->c.own_stream) cudaStreamDestroy(ctx->c.stream);
+  if (ctx->c.pool) {
+    cudaDeviceSynchronize();
+    cudaMemPoolDestroy(ctx->c.pool);
+  }
   delete ctx;
 }
 

@@ -351,6 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+#ifdef RTUCKER_EXPERIMENTS  // TMEM-A variant: measured slower, kept for experiments builds only
 // ---------------------------------------------------------------------------------------------
 // L == 1 variant with the A operand in TMEM (sketch_tc_ta_kernel).  The smem-operand kernel
 // above spends ~70 % of the shared-memory bandwidth on the X operand (hi / lo planes written
@@ -662,6 +663,8 @@ __global__ void __launch_bounds__(kTaThreads, 1)
   }
 }
 
+#endif  // RTUCKER_EXPERIMENTS
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -683,10 +686,11 @@ __global__ void reduce_partials_kernel(const double *__restrict__ partial, int n
   }
 }
 
+#ifdef RTUCKER_EXPERIMENTS
 template <int N>
 void launch_ta(Ctx &c, const CUtensorMap &tm, SketchTaParams &p, int grid, size_t smem) {
   auto k = sketch_tc_ta_kernel<N>;
-  RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  smem_attr(k, smem);
   RT_LAUNCH(c, k, grid, kTaThreads, smem, tm, p);
 }
 
@@ -699,7 +703,7 @@ bool sketch_ta(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0
   p.I = v.I;
   p.C = v.R;
   p.ng = (NT + 3) / 4;
-  if (const char *e = getenv("RTUCKER_TA_NG")) p.ng = std::max(p.ng, atoi(e));  // experiments
+  if (const char *e = RT_EXP_GETENV("RTUCKER_TA_NG")) p.ng = std::max(p.ng, atoi(e));  // experiments
   p.RG = (int)(((v.I + p.ng - 1) / p.ng + 7) / 8 * 8);
   p.NTg = (p.RG + 127) / 128;
   p.nbox = (p.RG + 255) / 256;
@@ -707,7 +711,7 @@ bool sketch_ta(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0
   p.acol = p.NTg * N;
   p.NSA = std::min(8, (512 - p.acol) / (16 * p.NTg));
   p.gsplit = kTaGen / 4;
-  static const bool prof = getenv("RTUCKER_TA_PROF") != nullptr;
+  static const bool prof = RT_EXP_GETENV("RTUCKER_TA_PROF") != nullptr;
   DevBuf<long long> pbuf;
   if (prof) {
     pbuf.alloc(c, 8);
@@ -759,10 +763,12 @@ bool sketch_ta(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0
   return true;
 }
 
+#endif  // RTUCKER_EXPERIMENTS
+
 template <int N, bool KM>
 void launch(Ctx &c, const CUtensorMap &tm, SketchTcParams &p, int grid, size_t smem) {
   auto k = sketch_tc_mn_kernel<N, KM>;
-  RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  smem_attr(k, smem);
   RT_LAUNCH(c, k, grid, kThreads, smem, tm, p);
 }
 
@@ -771,7 +777,7 @@ void launch(Ctx &c, const CUtensorMap &tm, SketchTcParams &p, int grid, size_t s
 PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() { return encode_fn(); }
 
 bool sketch_tc_enabled() {
-  static const bool off = getenv("RTUCKER_NO_TC") != nullptr;
+  static const bool off = RT_EXP_GETENV("RTUCKER_NO_TC") != nullptr;
   return !off;
 }
 
@@ -780,14 +786,16 @@ bool sketch_tc_enabled() {
 // Returns false when the shape is outside this kernel's envelope (caller falls back).
 bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0, uint64_t seed,
                   int64_t col_offset, double *Y, double *normsq, uint32_t *colmax) {
-  static const bool off = getenv("RTUCKER_NO_TC_SKETCH") != nullptr;
+  static const bool off = RT_EXP_GETENV("RTUCKER_NO_TC_SKETCH") != nullptr;
   if (off || !sketch_tc_enabled() || ell > 64 || ell < 1) return false;
   const bool km = v.L > 1;  // K-major variant: l contiguous (5-D TMA box, no transposition)
   if (!km && (v.I % 4) != 0) return false;
   if (km && ((v.L % 8) != 0 || (v.I % 8) != 0 || v.I / 8 > 256)) return false;
-  static const bool ta = getenv("RTUCKER_SKETCH_TA") != nullptr;  // TMEM-A variant (experimental)
+#ifdef RTUCKER_EXPERIMENTS
+  static const bool ta = RT_EXP_GETENV("RTUCKER_SKETCH_TA") != nullptr;  // TMEM-A variant (experimental)
   if (!km && ta && (((uintptr_t)X) & 15) == 0 && v.I <= 2048 && v.L * v.R <= (int64_t)INT32_MAX - 64)
     return sketch_ta(c, X, v, mode, ell, k0, seed, col_offset, Y, normsq, colmax);
+#endif
   const int N = ell <= 32 ? 32 : 64;
   const int NT = (int)((v.I + 127) / 128);
   if (NT * N > 512 || (((uintptr_t)X) & 15) != 0) return false;

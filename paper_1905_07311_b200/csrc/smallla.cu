@@ -254,7 +254,7 @@ template <int kL, bool kSmem>
 __global__ void __launch_bounds__(kL == 8 ? 256 : (kL == 16 ? 512 : kEigT)) jacobi_kernel(const double *__restrict__ Ain, int n, double *__restrict__ w,
                                                        double *__restrict__ Vout, double *__restrict__ gws,
                                                        double tol, int max_sweeps, int *__restrict__ info,
-                                                       const int *__restrict__ gate) {
+                                                       const int *__restrict__ gate, unsigned *__restrict__ status) {
   if (gate && *gate == 0) return;  // the preconditioned solver's result was accurate enough
   extern __shared__ double esm[];
   const int np = n + (n & 1);
@@ -294,6 +294,7 @@ __global__ void __launch_bounds__(kL == 8 ? 256 : (kL == 16 ? 512 : kEigT)) jaco
   const double tol2 = tol * tol;
   const int kstride = kGroups * nw;
   int sweeps = 0;
+  bool converged = false;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     // column norms^2 (fresh every sweep)
     for (int k = warp; k < np; k += nw) {
@@ -395,9 +396,13 @@ __global__ void __launch_bounds__(kL == 8 ? 256 : (kL == 16 ? 512 : kEigT)) jaco
     sweeps = sweep + 1;
     const int done = sconv;
     __syncthreads();
-    if (done) break;
+    if (done) {
+      converged = true;
+      break;
+    }
   }
   if (tid == 0 && info) *info = sweeps;
+  if (tid == 0 && !converged && status) atomicOr(status, (unsigned)ST_EIG_NOT_CONVERGED);
   // lambda_k = v_k^T m_k
   for (int k = warp; k < np; k += nw) {
     double d = 0.0;
@@ -431,7 +436,7 @@ __global__ void __launch_bounds__(kEigGT) jacobi_grid_kernel(const double *__res
                                                           double *__restrict__ w, double *__restrict__ Vout,
                                                           double *__restrict__ gws, int *__restrict__ conv,
                                                           double tol, int max_sweeps, int *__restrict__ info,
-                                                          const int *__restrict__ gate) {
+                                                          const int *__restrict__ gate, unsigned *__restrict__ status) {
   if (gate && *gate == 0) return;
   cg::grid_group grid = cg::this_grid();
   const int np = n + (n & 1);
@@ -449,6 +454,7 @@ __global__ void __launch_bounds__(kEigGT) jacobi_grid_kernel(const double *__res
   }
   const double tol2 = tol * tol;
   int sweeps = 0;
+  bool converged = false;
   grid.sync();
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     for (int k = gw; k < np; k += nw) {  // column norms^2 (fresh every sweep)
@@ -493,9 +499,13 @@ __global__ void __launch_bounds__(kEigGT) jacobi_grid_kernel(const double *__res
       grid.sync();
     }
     sweeps = sweep + 1;
-    if (*(volatile int *)&conv[sweep % 3]) break;  // identical in every thread after the sync
+    if (*(volatile int *)&conv[sweep % 3]) {  // identical in every thread after the sync
+      converged = true;
+      break;
+    }
   }
   if (gtid == 0 && info) *info = sweeps;
+  if (gtid == 0 && !converged && status) atomicOr(status, (unsigned)ST_EIG_NOT_CONVERGED);
   for (int k = gw; k < np; k += nw) {  // lambda_k = v_k^T m_k
     double d = 0.0;
     for (int r = lane; r < np; r += 32) d = fma(V[r + (size_t)np * k], M[r + (size_t)np * k], d);
@@ -640,7 +650,8 @@ __device__ __forceinline__ void jac_half(double (&own)[kV], const double (&oth)[
 template <int kV, int LPS>
 __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restrict__ Ain, int n, double *__restrict__ w,
                                                           double *__restrict__ Vout, double tol, int max_sweeps,
-                                                          int *__restrict__ info, int r_need, int *__restrict__ refine) {
+                                                          int *__restrict__ info, int r_need, int *__restrict__ refine,
+                                                          unsigned *__restrict__ status) {
   extern __shared__ double gsm2[];
 #ifdef RTUCKER_EIG_PROF_BUILD
   long long et_[6];
@@ -762,6 +773,7 @@ __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restri
   const int slot = lane / LPS, q = lane % LPS;
   const int nwk = nb / 2;  // working warps
   int sweeps = 0;
+  bool converged = false;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     if (tid == 0) sflag = 0;
     __syncthreads();
@@ -813,10 +825,14 @@ __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restri
     sweeps = sweep + 1;
     const int more = sflag;
     __syncthreads();
-    if (!more) break;
+    if (!more) {
+      converged = true;
+      break;
+    }
   }
   EGP();
   if (tid == 0 && info) *info = sweeps;
+  if (tid == 0 && !converged && status) atomicOr(status, (unsigned)ST_EIG_NOT_CONVERGED);
   for (int k = warp; k < np; k += kGramT / 32) {  // exact column norms
     double d = 0.0;
     for (int r = lane; r < np; r += 32) { const double x = M[r + ldm * k]; d = fma(x, x, d); }
@@ -1151,7 +1167,7 @@ void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q, const 
   // smallest cluster whose row slabs fit in shared memory (RTUCKER_QR_NCTA forces a size,
   // for testing the multi-CTA path on small inputs)
   static const int forced = [] {
-    const char *e = getenv("RTUCKER_QR_NCTA");
+    const char *e = RT_EXP_GETENV("RTUCKER_QR_NCTA");
     return e ? atoi(e) : 0;
   }();
   for (int ncta : {1, 2, 4, 8, 16}) {
@@ -1173,7 +1189,7 @@ void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q, const 
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    RT_CUDA(cudaFuncSetAttribute(qr_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_attr(qr_cluster_kernel, smem);
     if (ncta > 8)
       RT_CUDA(cudaFuncSetAttribute(qr_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     RT_CUDA(cudaLaunchKernelEx(&cfg, qr_cluster_kernel, Y, m, n, rows, Q, gate));
@@ -1184,7 +1200,7 @@ void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q, const 
   RT_CUDA(cudaMemcpyAsync(W.p, Y, sizeof(double) * m * n, cudaMemcpyDeviceToDevice, c.stream));
   const size_t smem = sizeof(double) * 2 * (size_t)n;
   if (smem > 48 * 1024)
-    RT_CUDA(cudaFuncSetAttribute(qr_global_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_attr(qr_global_kernel, smem);
   RT_LAUNCH(c, qr_global_kernel, 1, kQRG, smem, W.p, m, n, Q, gate);
 }
 
@@ -1195,7 +1211,7 @@ void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps,
   // 8 lanes (blocks of 4, all 8 warps busy, 8 rows per lane) measured no faster at n = 60
   // (405 vs 412 us): a round is bound by its dependent latency chain (reductions, angle),
   // not by the per-lane work.
-  static const bool lps8 = getenv("RTUCKER_EIG_LPS8") != nullptr;
+  static const bool lps8 = RT_EXP_GETENV("RTUCKER_EIG_LPS8") != nullptr;
   const int lps = (np > 32 && lps8) ? 8 : 4, spw = 32 / lps;
   const int nb = ((n + 2 * spw - 1) / (2 * spw)) * 2, ncol = spw * nb;
   const int kv = (np + lps - 1) / lps <= 4 ? 4 : ((np + lps - 1) / lps <= 8 ? 8 : 16);
@@ -1205,8 +1221,8 @@ void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps,
   const double tol = 3e-15 * std::sqrt((double)n);
   const int rn = std::max(1, std::min(r_need, n));
 #define RT_GE(KV, L)                                                                                      \
-  RT_CUDA(cudaFuncSetAttribute(gram_eig_kernel<KV, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need)); \
-  RT_LAUNCH(c, (gram_eig_kernel<KV, L>), 1, kGramT, need, A, n, w, V, tol, 40, sweeps, rn, refine.p)
+  smem_attr(gram_eig_kernel<KV, L>, need);                                                                 \
+  RT_LAUNCH(c, (gram_eig_kernel<KV, L>), 1, kGramT, need, A, n, w, V, tol, 40, sweeps, rn, refine.p, c.status)
   if (lps == 8) {
     RT_GE(8, 8);
   } else if (kv == 4) {
@@ -1223,7 +1239,7 @@ void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps,
 void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
   RT_REQUIRE(m >= n && n >= 1, "qr: need m >= n >= 1");
   if (n > 64) return householder_qr(c, Y, m, n, Q, nullptr);
-  static const bool no_chol = getenv("RTUCKER_QR_HOUSEHOLDER") != nullptr;
+  static const bool no_chol = RT_EXP_GETENV("RTUCKER_QR_HOUSEHOLDER") != nullptr;
   if (no_chol) return householder_qr(c, Y, m, n, Q, nullptr);
   DevBuf<int> bad(c, 1);
   bad.zero();
@@ -1249,14 +1265,14 @@ void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    RT_CUDA(cudaFuncSetAttribute(cholqr2_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    smem_attr(cholqr2_cluster_kernel, smem);
     RT_CUDA(cudaLaunchKernelEx(&cfg, cholqr2_cluster_kernel, Y, m, n, rows, ldY, ldG, ldE, Q, bad.p));
     c.launches++;
   } else {
     // tall sketches (sparse modes, I_n ~ 1e5): CholeskyQR2 over the whole grid
     DevBuf<double> G(c, (size_t)n * n), Ri(c, (size_t)n * n), Q1(c, (size_t)m * n);
     const size_t csm = sizeof(double) * ((size_t)n * n + n);
-    RT_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+    smem_attr(chol_inv_kernel, csm);
     const double *src = Y;
     for (int pass = 0; pass < 2; ++pass) {
       double *dst = pass == 0 ? Q1.p : Q;
@@ -1279,15 +1295,16 @@ void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps, 
   const int thr = np <= 64 ? std::max(64, ((np / 2) * 8 + 31) / 32 * 32) : kEigT;
   if (need <= 200 * 1024) {
 #define RT_EIG(KL)                                                                                   \
-  RT_CUDA(cudaFuncSetAttribute(jacobi_kernel<KL, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need)); \
-  RT_LAUNCH(c, (jacobi_kernel<KL, true>), 1, thr, need, A, n, w, V, (double *)nullptr, tol, max_sweeps, sweeps, gate)
+  smem_attr(jacobi_kernel<KL, true>, need);                                                                 \
+  RT_LAUNCH(c, (jacobi_kernel<KL, true>), 1, thr, need, A, n, w, V, (double *)nullptr, tol, max_sweeps, sweeps, gate, \
+            c.status)
     if (np <= 64) { RT_EIG(8); } else { RT_EIG(32); }
 #undef RT_EIG
   } else {  // matrices in global memory (L2): the whole GPU, one warp per pair, grid-synchronised
-    static const bool one_cta = getenv("RTUCKER_EIG_ONE_CTA") != nullptr;
+    static const bool one_cta = RT_EXP_GETENV("RTUCKER_EIG_ONE_CTA") != nullptr;
     DevBuf<double> ws(c, 2 * (size_t)np * np + np);
     if (one_cta) {
-      RT_LAUNCH(c, (jacobi_kernel<32, false>), 1, kEigT, 0, A, n, w, V, ws.p, tol, max_sweeps, sweeps, gate);
+      RT_LAUNCH(c, (jacobi_kernel<32, false>), 1, kEigT, 0, A, n, w, V, ws.p, tol, max_sweeps, sweeps, gate, c.status);
     } else {
       DevBuf<int> conv(c, 3);
       int nb = 0;
@@ -1297,8 +1314,9 @@ void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps, 
       int *convp = conv.p;
       double tl = tol;
       int ms = max_sweeps;
+      unsigned *stp = c.status;
       void *args[] = {(void *)&A, (void *)&n, (void *)&w, (void *)&V, (void *)&wsp, (void *)&convp,
-                      (void *)&tl, (void *)&ms, (void *)&sweeps, (void *)&gate};
+                      (void *)&tl, (void *)&ms, (void *)&sweeps, (void *)&gate, (void *)&stp};
       RT_CUDA(cudaLaunchCooperativeKernel((const void *)jacobi_grid_kernel, dim3(grid), dim3(kEigGT), args, 0, c.stream));
       c.launches++;
     }

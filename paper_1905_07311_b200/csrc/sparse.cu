@@ -424,8 +424,7 @@ void sketch_coo(Ctx &c, const CooDev &g, int mode, int ell, uint64_t seed, bool 
   const int64_t nper = (g.nnz + blocks - 1) / blocks;
 #define RT_COO(TV, TN)                                                                                     \
   do {                                                                                                     \
-    RT_CUDA(cudaFuncSetAttribute(sketch_coo_kernel<TV, TN>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
-                                 (int)smem));                                                              \
+    smem_attr(sketch_coo_kernel<TV, TN>, smem);                                                            \
     RT_LAUNCH(c, (sketch_coo_kernel<TV, TN>), (int)blocks, kCooT, smem, g, mode, ell, seed, nper, Y);      \
   } while (0)
   if (g.vt == DT::F64) {
@@ -461,7 +460,7 @@ void srrqr(Ctx &c, const double *Q, int64_t m, int l, double eta, int64_t *sel_d
   DevBuf<int> st(c, 1), insel(c, m);
   DevBuf<int64_t> dsel(c, l), mi(c, 1);
   const size_t qsm = sizeof(double) * l * 2 * l;
-  if (qsm > 48 * 1024) RT_CUDA(cudaFuncSetAttribute(qs_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsm));
+  if (qsm > 48 * 1024) smem_attr(qs_inverse, qsm);
   int swaps = 0;
   auto compute_A = [&](bool want_max) -> std::pair<double, int64_t> {
     RT_CUDA(cudaMemcpyAsync(dsel.p, sel.data(), sizeof(int64_t) * l, cudaMemcpyHostToDevice, c.stream));
@@ -585,10 +584,10 @@ rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int6
       thin_qr(c, Y.p, I, ell, Q.p);
     }
     double *A = nullptr;
-    RT_CUDA(cudaMallocAsync((void **)&A, sizeof(double) * I * ell, c.stream));
+    A = (double *)dev_alloc(c, sizeof(double) * I * ell);
     res->factors[n] = A;
     int64_t *S = nullptr;
-    RT_CUDA(cudaMallocAsync((void **)&S, sizeof(int64_t) * ell, c.stream));
+    S = (int64_t *)dev_alloc(c, sizeof(int64_t) * ell);
     res->selection[n] = S;
     {
       PhaseScope ps(c, PH_EIG, jj);
@@ -611,12 +610,12 @@ rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int6
   }
   res->core_nnz = nnz;
   for (int k = 0; k < d; ++k) {
-    RT_CUDA(cudaMallocAsync((void **)&res->core_idx[k], sizeof(int32_t) * std::max<int64_t>(nnz, 1), c.stream));
+    res->core_idx[k] = (int32_t *)dev_alloc(c, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
     if (nnz)
       RT_CUDA(cudaMemcpyAsync(res->core_idx[k], ib[cb].p + (size_t)k * nnz0, sizeof(int32_t) * nnz,
                               cudaMemcpyDeviceToDevice, c.stream));
   }
-  RT_CUDA(cudaMallocAsync(&res->core_vals, vs * std::max<int64_t>(nnz, 1), c.stream));
+  res->core_vals = dev_alloc(c, vs * std::max<int64_t>(nnz, 1));
   if (nnz) RT_CUDA(cudaMemcpyAsync(res->core_vals, vb[cb].p, vs * nnz, cudaMemcpyDeviceToDevice, c.stream));
   finish_result(c, res, flags);
   RT_CUDA(cudaStreamSynchronize(c.stream));

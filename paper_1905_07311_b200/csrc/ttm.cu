@@ -173,7 +173,7 @@ void launch_ttm(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t lda, 
 #define RT_TTM_CASE(ST, GR)                                                                   \
   do {                                                                                        \
     auto k = ttm_simt_kernel<Tin, Tout, Tmul, JP, ST, GR>;                                    \
-    RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+    smem_attr(k, smem); \
     RT_LAUNCH(c, k, nblk, kThreads, smem, X, v.L, v.I, v.R, A, lda, J, Jst, out, part.p);     \
   } while (0)
   if (out && gram) RT_TTM_CASE(true, true);
@@ -1004,7 +1004,7 @@ void launch_ttm_dfma(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t 
   const int64_t P = v.L * v.R;
   const int64_t ntiles = (P + kDP - 1) / kDP;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, c.num_sms));
-  static const bool use_dfma = getenv("RTUCKER_NO_DMMA") != nullptr;
+  static const bool use_dfma = RT_EXP_GETENV("RTUCKER_NO_DMMA") != nullptr;
   DevBuf<double> part;
   if (gram) part.alloc(c, (size_t)grid * 4096);
   // cp.async pipeline for L == 1 with 16-byte aligned rows of X and A
@@ -1015,7 +1015,7 @@ void launch_ttm_dfma(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t 
 #define RT_DL(ST, GR)                                                                                 \
   do {                                                                                                \
     auto k = ttm_dmma_l1_kernel<Tin, ST, GR>;                                                         \
-    RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));         \
+    smem_attr(k, smem);         \
     RT_LAUNCH(c, k, grid, kDT, smem, X, v.I, P, A, lda, J, out, part.p);                              \
   } while (0)
     if (out && gram) RT_DL(true, true);
@@ -1027,7 +1027,7 @@ void launch_ttm_dfma(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t 
 #define RT_DF(ST, GR)                                                                                 \
   do {                                                                                                \
     auto k = ttm_dfma_kernel<Tin, ST, GR>;                                                            \
-    RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));         \
+    smem_attr(k, smem);         \
     RT_LAUNCH(c, k, grid, kDT, smem, X, v.L, v.I, v.R, A, lda, J, out, part.p);                       \
   } while (0)
     if (out && gram) RT_DF(true, true);
@@ -1050,7 +1050,7 @@ void launch_ttm_dfma(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t 
 #define RT_DM(ST, GR)                                                                                 \
   do {                                                                                                \
     auto k = ttm_dmma_kernel<Tin, ST, GR>;                                                            \
-    RT_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));         \
+    smem_attr(k, smem);         \
     RT_LAUNCH(c, k, sk_grid, kDT, smem, X, v.L, v.I, v.R, A, lda, J, out, part.p, fix.p, c.sk_flags, c.sk_epoch); \
   } while (0)
     if (out && gram) RT_DM(true, true);

@@ -29,6 +29,11 @@ ADAPT_NO_TRUNCATE = 1 << 3
 ADAPT_HOSVD = 1 << 4
 RESULT_HOST = 1 << 5
 NO_CORE = 1 << 6
+DETERMINISTIC = 1 << 7
+DEBUG_CHECKS = 1 << 8
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
 
 STATUS = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ENUMERIC", 4: "ECUDA", 5: "ENCCL", 6: "EUNSUPPORTED"}
 
@@ -87,7 +92,7 @@ def load_library(path: str = LIB_PATH):
     P, I32, I64, U32, U64, D = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double
     RP = C.POINTER(C.POINTER(ResultStruct))
     sig = {
-        "rtucker_ctx_create": (C.c_int, [C.c_int, P, P, C.c_int, C.c_int, C.POINTER(P)]),
+        "rtucker_ctx_create": (C.c_int, [C.c_int, P, P, C.c_int, C.c_int, ALLOC_FN, FREE_FN, P, C.POINTER(P)]),
         "rtucker_ctx_destroy": (None, [P]),
         "rtucker_ctx_set_stream": (C.c_int, [P, P]),
         "rtucker_last_error": (C.c_char_p, [P]),
@@ -237,10 +242,13 @@ class Context:
     """One library context per GPU / rank.
 
     device: CUDA ordinal; stream: a torch.cuda.Stream (default: torch's current stream);
-    group: optional torch.distributed process group for the multi-rank (NCCL) path."""
+    group: optional torch.distributed process group for the multi-rank (NCCL) path;
+    allocator: "torch" (default) routes the library's device workspace and results through
+    torch's caching allocator (rtucker_alloc_fn hooks), "library" uses the library's own
+    stream-ordered pool."""
 
     def __init__(self, device: int = 0, stream=None, group=None, rank: int | None = None,
-                 world: int | None = None, nccl_id: bytes | None = None):
+                 world: int | None = None, nccl_id: bytes | None = None, allocator: str = "torch"):
         self.lib = load_library()
         torch = _torch()
         if stream is None and torch.cuda.is_available():
@@ -260,7 +268,12 @@ class Context:
                     nccl_id = bootstrap_nccl_id(group, r)
                 idbuf = C.create_string_buffer(bytes(nccl_id), 128)
         h = C.c_void_p()
-        st = self.lib.rtucker_ctx_create(device, sp, idbuf, r, n, C.byref(h))
+        self._alloc_cb, self._free_cb = ALLOC_FN(), FREE_FN()   # NULL hooks: library pool
+        if allocator == "torch":
+            self._alloc_cb, self._free_cb = _torch_hooks(device)
+        elif allocator != "library":
+            raise ValueError("allocator must be 'torch' or 'library'")
+        st = self.lib.rtucker_ctx_create(device, sp, idbuf, r, n, self._alloc_cb, self._free_cb, None, C.byref(h))
         if st != 0:
             raise RTuckerError(st, "rtucker_ctx_create failed")
         self.h = h
@@ -494,6 +507,24 @@ class Context:
                                                  a.data_ptr(), C.byref(sw)))
         self.sync()
         return sel.cpu().numpy(), a.cpu().numpy().reshape((m, l), order="F"), int(sw.value)
+
+
+def _torch_hooks(device: int):
+    """rtucker_alloc_fn / rtucker_free_fn routed to torch's caching allocator (stream-ordered
+    on the library's stream, so freed blocks are reused in stream order)."""
+    torch = _torch()
+
+    def _alloc(nbytes, stream, user):
+        try:
+            return int(torch.cuda.caching_allocator_alloc(int(nbytes), device, int(stream or 0)))
+        except Exception:  # out of memory or any allocator error: NULL -> RTUCKER_ENOMEM
+            return None
+
+    def _free(ptr, stream, user):
+        if ptr:
+            torch.cuda.caching_allocator_delete(int(ptr))
+
+    return ALLOC_FN(_alloc), FREE_FN(_free)
 
 
 def _buffer_int32(x):

@@ -54,9 +54,13 @@ def test_version(lib):
 
 def test_invalid_arguments_without_gpu(lib):
     h = C.c_void_p()
-    assert lib.rtucker_ctx_create(0, None, None, 0, 0, C.byref(h)) == 1      # nranks < 1
-    assert lib.rtucker_ctx_create(0, None, None, 2, 2, C.byref(h)) == 1      # rank >= nranks
-    assert lib.rtucker_ctx_create(0, None, None, 0, 2, C.byref(h)) == 1      # no NCCL id for 2 ranks
+    na, nf = R.ALLOC_FN(), R.FREE_FN()
+    assert lib.rtucker_ctx_create(0, None, None, 0, 0, na, nf, None, C.byref(h)) == 1      # nranks < 1
+    assert lib.rtucker_ctx_create(0, None, None, 2, 2, na, nf, None, C.byref(h)) == 1      # rank >= nranks
+    assert lib.rtucker_ctx_create(0, None, None, 0, 2, na, nf, None, C.byref(h)) == 1      # no NCCL id for 2 ranks
+    # allocation hooks come in pairs
+    a_only = R.ALLOC_FN(lambda n, s, u: None)
+    assert lib.rtucker_ctx_create(0, None, None, 0, 1, a_only, nf, None, C.byref(h)) == 1
     out = C.POINTER(R.ResultStruct)()
     desc = R.DenseDesc()
     ranks = (C.c_int64 * 3)(1, 1, 1)

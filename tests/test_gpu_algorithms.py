@@ -169,6 +169,21 @@ def test_host_input_and_determinism(ctx):
         np.testing.assert_array_equal(fa, fb)
 
 
+def test_allocator_hooks_bit_identical():
+    """Workspace and results through torch's caching allocator (rtucker_alloc_fn hooks, the
+    binding's default) or through the library's own pool give bit-identical results."""
+    from paper_1905_07311_b200.rtucker import Context
+    x = hilbert((30, 26, 22), "paper")
+    out = []
+    for alloc in ("torch", "library"):
+        c = Context(0, allocator=alloc)
+        out.append(_run(c, "sthosvd", x, (4, 4, 4), 3, 1))
+        c.close()
+    np.testing.assert_array_equal(out[0].core, out[1].core)
+    for fa, fb in zip(out[0].factors, out[1].factors):
+        np.testing.assert_array_equal(fa, fb)
+
+
 def test_rel_error_on_device(ctx):
     import torch
     x = hilbert((50, 50, 50), "shifted")
