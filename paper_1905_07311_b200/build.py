@@ -18,7 +18,7 @@ BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "librtucker.so")
 
 SOURCES = ["rtucker.cu", "dense.cu", "adaptive.cu", "sparse.cu", "sketch.cu", "sketch_tc.cu", "bpass_tc.cu", "bpass_ozaki.cu", "ttm.cu",
-           "linalg.cu", "smallla.cu", "linalg_extra.cu", "comm.cpp"]
+           "linalg.cu", "smallla.cu", "trideig.cu", "linalg_extra.cu", "comm.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
                      "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]

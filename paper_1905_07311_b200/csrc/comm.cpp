@@ -105,4 +105,31 @@ void allgather_f64(Ctx &ctx, const double *send, double *recv, size_t n) {
   check(api().AllGather(send, recv, n, ncclFloat64, ctx.comm->comm, ctx.stream), "ncclAllGather");
 }
 
+void allreduce_i64_sum(Ctx &ctx, void *buf, size_t n) {
+  if (ctx.nranks <= 1 || n == 0) return;
+  check(api().AllReduce(buf, buf, n, ncclInt64, ncclSum, ctx.comm->comm, ctx.stream), "ncclAllReduce(int64)");
+}
+
+void allreduce_u64_max(Ctx &ctx, void *buf, size_t n) {
+  if (ctx.nranks <= 1 || n == 0) return;
+  check(api().AllReduce(buf, buf, n, ncclUint64, ncclMax, ctx.comm->comm, ctx.stream), "ncclAllReduce(max)");
+}
+
+void allgather_i64(Ctx &ctx, const void *send, void *recv, size_t n) {
+  if (ctx.nranks <= 1) {
+    if (send != recv)
+      RT_CUDA(cudaMemcpyAsync(recv, send, n * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+    return;
+  }
+  check(api().AllGather(send, recv, n, ncclInt64, ctx.comm->comm, ctx.stream), "ncclAllGather(int64)");
+}
+
+void allgather_bytes(Ctx &ctx, const void *send, void *recv, size_t bytes) {
+  if (ctx.nranks <= 1) {
+    if (send != recv) RT_CUDA(cudaMemcpyAsync(recv, send, bytes, cudaMemcpyDeviceToDevice, ctx.stream));
+    return;
+  }
+  check(api().AllGather(send, recv, bytes, ncclUint8, ctx.comm->comm, ctx.stream), "ncclAllGather(bytes)");
+}
+
 }  // namespace rt

@@ -54,6 +54,8 @@ struct Comm;  // comm.cpp
 enum StatusBit : unsigned {
   ST_EIG_NOT_CONVERGED = 1u,   // a Jacobi eigensolve hit its sweep cap
   ST_SHARD_LAYOUT = 2u,        // the shards of a multi-rank call do not tile the last mode
+  ST_SINGULAR_PQ = 4u,         // SP-STHOSVD: singular P^T Q (fewer than l independent rows)
+  ST_BAD_INDEX = 8u,           // RTUCKER_DEBUG_CHECKS: a COO index out of range
 };
 
 // Phase timing (measurement only): CUDA events recorded on the context stream around

@@ -74,6 +74,9 @@ void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps =
 // ~eps sqrt(w_0 / w_k).  When the r_need-th eigenvalue is below 1e-8 w_0 the unpreconditioned
 // sym_eig recomputes the result (device-side gate, no host sync).  n > 64 uses sym_eig.
 void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps = nullptr, int r_need = 1 << 30);
+// Symmetric eigensolver for n <= 64 (trideig.cu): Householder tridiagonalisation, multisection,
+// twisted-factorisation eigenvectors, one CTA; eigenvalues descending.  Returns false if n > 64.
+bool trid_eig(Ctx &c, const double *A, int n, double *w, double *V, int *info = nullptr);
 // Sign convention of reading R4b: for each column k < r of A (m x r) make the entry of
 // largest magnitude positive (first on ties); the same sign is applied to column k of U
 // (ell x r, leading dim ldu) so that the shrink U^T B stays consistent.
@@ -81,6 +84,9 @@ void canonical_signs(Ctx &c, double *A, int64_t m, int r, double *U, int64_t ldu
 // C (m x n) = op(A) (m x k) * B (k x n), fp64 col-major with leading dims.
 void gemm_small(Ctx &c, bool transA, const double *A, int64_t lda, const double *B, int64_t ldb,
                 double *C, int64_t ldc, int64_t m, int64_t n, int64_t k);
+// C (m x n) = beta C + alpha op(A) B on the fp64 tensor cores (tiled, deterministic), column-major.
+void gemm_f64(Ctx &c, bool transA, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+              int64_t ldc, int64_t m, int64_t n, int64_t k, double beta = 0.0, double alpha = 1.0);
 void convert(Ctx &c, const void *src, DT s, void *dst, DT d, int64_t n);
 void sumsq(Ctx &c, const void *X, DT t, int64_t n, double *out);             // deterministic
 void diff_sumsq(Ctx &c, const void *X, DT t, const double *Y, int64_t n, double *out);
@@ -96,15 +102,18 @@ struct CooDev {
   const void *vals;
   DT vt;
 };
-// Y (I_n x ell, fp64) = G_(n) Omega_n for a COO tensor.
-// normals_f64: fp64 Box-Muller normals (else fp32 normals; products and sums in fp64).
-void sketch_coo(Ctx &c, const CooDev &g, int mode, int ell, uint64_t seed, bool normals_f64, double *Y);
-// Strong-RRQR (CPQR + maxvol, eta) on Q (m x l): sel sorted (device int64), A (m x l).
-void srrqr(Ctx &c, const double *Q, int64_t m, int l, double eta, int64_t *sel, double *A,
-           int *swaps_host);
-// Keep entries whose mode-n index is in sel (sorted, length l) and renumber it.
-// Returns new nnz (host sync).
-int64_t coo_select(Ctx &c, const CooDev &in, int mode, const int64_t *sel, int l,
-                   int32_t *const *out_idx, void *out_vals);
+// Y (I_n x ell, fp64) = G_(n) Omega_n for a COO tensor, summed in fixed point (deterministic)
+// and over the ranks.  nnz_dev (optional): live nnz on the device (g.nnz is then an upper
+// bound).  fs_dev (optional): the call's fixed-point scale (computed from g when null).
+// normals_f64: fp64 Box-Muller normals (else fp32 normals; products in fp64).
+void sketch_coo(Ctx &c, const CooDev &g, int mode, int ell, uint64_t seed, bool normals_f64, double *Y,
+                const int64_t *nnz_dev = nullptr, const void *fs_dev = nullptr);
+// Strong-RRQR (CPQR + maxvol, eta) on Q (m x l) in one cooperative kernel: sel sorted (device
+// int64), A (m x l), swaps (device int); singular P^T Q sets the status word.
+void srrqr(Ctx &c, const double *Q, int64_t m, int l, double eta, int64_t *sel, double *A, int *swaps_dev);
+// Keep entries whose mode-n index is in sel (sorted, length l) and renumber it; the live input
+// nnz is read from nnz_dev, the new nnz written to nnz_out (device).
+void coo_select(Ctx &c, const CooDev &in, const int64_t *nnz_dev, int mode, const int64_t *sel, int l,
+                int32_t *const *out_idx, void *out_vals, int64_t *nnz_out);
 
 }  // namespace rt

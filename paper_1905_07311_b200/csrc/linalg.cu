@@ -30,6 +30,73 @@ __global__ void gemm_small_kernel(bool transA, const double *__restrict__ A, int
   }
 }
 
+// C (m x n) = beta C + op(A) (m x k) B (k x n), column-major fp64 on the fp64 tensor cores
+// (mma.sync m8n8k4): CTA tile 64 x 64, K steps of 16 staged in shared memory, 8 warps of
+// 32 x 16; fixed summation order (deterministic).
+constexpr int kGm = 64, kGk = 16;
+__global__ void __launch_bounds__(256) gemm_f64_kernel(bool transA, const double *__restrict__ A, int64_t lda,
+                                                       const double *__restrict__ B, int64_t ldb,
+                                                       double *__restrict__ C, int64_t ldc, int64_t m, int64_t n,
+                                                       int64_t k, double beta, double alpha) {
+  __shared__ double As[kGk][kGm + 1], Bs[kGk][kGm + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t i0 = (int64_t)blockIdx.x * kGm, j0 = (int64_t)blockIdx.y * kGm;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  double acc[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int64_t k0 = 0; k0 < k; k0 += kGk) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      if (!transA) {
+        const int ii = tid & 63, kk = (tid >> 6) + 4 * s;
+        const int64_t gi = i0 + ii, gk = k0 + kk;
+        As[kk][ii] = (gi < m && gk < k) ? A[gi + lda * gk] : 0.0;
+      } else {
+        const int kk = tid & 15, ii = (tid >> 4) + 16 * s;
+        const int64_t gi = i0 + ii, gk = k0 + kk;
+        As[kk][ii] = (gi < m && gk < k) ? A[gk + lda * gi] : 0.0;
+      }
+      const int kk = tid & 15, jj = (tid >> 4) + 16 * s;
+      const int64_t gj = j0 + jj, gk = k0 + kk;
+      Bs[kk][jj] = (gj < n && gk < k) ? B[gk + ldb * gj] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < kGk; ks += 4) {
+      const int kk = ks + (lane & 3);
+      double bv[2];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) bv[b] = Bs[kk][wn + 8 * b + (lane >> 2)];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const double av = As[kk][wm + 8 * a + (lane >> 2)];
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
+                       : "d"(av), "d"(bv[b]));
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gi = i0 + wm + 8 * a + (lane >> 2), gj = j0 + wn + 8 * b + 2 * (lane & 3) + h;
+        if (gi < m && gj < n) {
+          double *cp = C + gi + ldc * gj;
+          const double v = alpha * acc[a][b][h];
+          *cp = beta == 0.0 ? v : fma(beta, *cp, v);
+        }
+      }
+}
+
 template <typename S, typename D>
 __global__ void convert_kernel(const S *__restrict__ s, D *__restrict__ d, int64_t n) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
@@ -79,8 +146,16 @@ __global__ void sub_scalar_kernel(const double *a, const double *b, double *out)
 
 void gemm_small(Ctx &c, bool transA, const double *A, int64_t lda, const double *B, int64_t ldb,
                 double *C, int64_t ldc, int64_t m, int64_t n, int64_t k) {
+  if (m * n * k >= (1 << 20)) return gemm_f64(c, transA, A, lda, B, ldb, C, ldc, m, n, k, 0.0, 1.0);
   const int g = std::max(1, std::min(2048, ceil_div(m * n, 256)));
   RT_LAUNCH(c, gemm_small_kernel, g, 256, 0, transA, A, lda, B, ldb, C, ldc, m, n, k);
+}
+
+void gemm_f64(Ctx &c, bool transA, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
+              int64_t ldc, int64_t m, int64_t n, int64_t k, double beta, double alpha) {
+  if (m <= 0 || n <= 0) return;
+  const dim3 grid((unsigned)((m + kGm - 1) / kGm), (unsigned)((n + kGm - 1) / kGm));
+  RT_LAUNCH(c, gemm_f64_kernel, grid, 256, 0, transA, A, lda, B, ldb, C, ldc, m, n, k, beta, alpha);
 }
 
 void convert(Ctx &c, const void *src, DT s, void *dst, DT d, int64_t n) {

@@ -46,6 +46,8 @@ void check_status(Ctx &c) {
   RT_CUDA(cudaMemsetAsync(c.status, 0, sizeof(unsigned), c.stream));
   if (h & ST_SHARD_LAYOUT)
     throw Error(RTUCKER_EINVAL, "the shards of the ranks do not tile the last mode [0, I_d) (rank order)");
+  if (h & ST_BAD_INDEX) throw Error(RTUCKER_EINVAL, "a COO index lies outside its mode's range");
+  if (h & ST_SINGULAR_PQ) throw Error(RTUCKER_ENUMERIC, "SP-STHOSVD: singular P^T Q (fewer than l independent rows)");
   if (h & ST_EIG_NOT_CONVERGED)
     throw Error(RTUCKER_ENUMERIC, "a Jacobi eigensolve did not converge within its sweep cap");
 }
@@ -467,9 +469,12 @@ rtucker_status rtucker_debug_srrqr(rtucker_ctx *ctx, int64_t m, int32_t l, const
                                    int64_t *sel, double *A, int32_t *swaps_out) {
   if (!ctx || !Q || !sel || !A || l < 1 || m < l || !(eta >= 1.0)) return RTUCKER_EINVAL;
   return guard(ctx, [&] {
-    int sw = 0;
-    srrqr(ctx->c, Q, m, l, eta, sel, A, &sw);
-    if (swaps_out) *swaps_out = sw;
+    DevBuf<int> sw(ctx->c, 1);
+    srrqr(ctx->c, Q, m, l, eta, sel, A, sw.p);
+    int h = 0;
+    RT_CUDA(cudaMemcpyAsync(&h, sw.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->c.stream));
+    check_status(ctx->c);
+    if (swaps_out) *swaps_out = h;
   });
 }
 

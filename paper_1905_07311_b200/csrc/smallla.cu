@@ -1206,6 +1206,9 @@ void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q, const 
 
 void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps, int r_need) {
   const int np = n + (n & 1);
+  // hot path: Householder tridiagonalisation + multisection + twisted eigenvectors (trideig.cu,
+  // one CTA for n <= 64, the whole GPU above); the Jacobi solvers below are experiments only
+  if (!RT_EXP_GETENV("RTUCKER_EIG_JACOBI") && trid_eig(c, A, n, w, V, sweeps)) return;
   if (np > 64) return sym_eig(c, A, n, w, V, sweeps);
   // 4 lanes per column slot (blocks of 8 columns, nb / 2 busy warps).  RTUCKER_EIG_LPS8 (n > 32):
   // 8 lanes (blocks of 4, all 8 warps busy, 8 rows per lane) measured no faster at n = 60
@@ -1287,6 +1290,7 @@ void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
 }
 
 void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps, const int *gate) {
+  if (!gate && !RT_EXP_GETENV("RTUCKER_EIG_JACOBI") && trid_eig(c, A, n, w, V, sweeps)) return;
   const int np = n + (n & 1);
   const size_t tab = sizeof(short2) * (size_t)(np - 1) * (np / 2) + 16;
   const size_t need = sizeof(double) * (2 * (size_t)np * np + np) + tab;

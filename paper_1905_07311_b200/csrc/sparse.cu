@@ -1,48 +1,117 @@
 // Structure-preserving SP-STHOSVD (Alg 6) for COO tensors:
 //   for j in rho:  Y = G_(j) Omega_j                 (sketch over the nonzeros)
-//                  Q = qr(Y)                         (Householder)
+//                  Q = qr(Y)
 //                  S = strong RRQR on Q^T, eta       (DESIGN reading R9: CPQR + maxvol)
 //                  A_j = Q (P^T Q)^{-1}
 //                  G_(j) <- P^T G_(j)                (keep the selected slices, renumber)
-// The core keeps the input values bit-exactly.  The selection and the
-// new nnz are data dependent, so the call synchronises the stream after every mode.
+// The core keeps the input values bit-exactly.
+//
+// Determinism (RTUCKER_DETERMINISTIC): the sketch sums in FIXED POINT.  Every
+// product v * omega (exact or fp64-rounded, as in the oracle) is scaled by 2^S and split into
+// an integer part H (units of 2^32) and a 32-bit fraction L; all reductions (lanes, warps,
+// CTAs, and the ranks of a multi-GPU run through an integer allreduce) add int64 words, which
+// is associative, so Y is bit-identical for any launch shape, schedule or GPU count.  S is
+// chosen from max|v| and the global nnz so that no partial sum overflows (|omega| < 8 since
+// u >= 2^-33): the resolution is 2^-65 of the largest term, below fp64 rounding.
+//
+// Nothing here synchronises the host until the end of the call: the current nnz stays on
+// the device (kernels are sized for the input nnz and read the live count), the sRRQR
+// selection runs in one cooperative kernel, and the final sizes are read back once.
+//
+// Multi-GPU: nnz-partitioned.  Each rank sketches its own nonzeros, the
+// integer partial sketches are allreduced (exact), QR and sRRQR run redundantly (identical
+// inputs, deterministic kernels -> identical selections), each rank filters its own nonzeros,
+// and the core nonzeros are gathered in rank order at the end (= the single-GPU order when
+// the partition is contiguous in the input order).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <vector>
+
+#include <cooperative_groups.h>
 
 #include "comm.h"
 #include "kernels_extra.h"
 #include "orchestrate.h"
 #include "philox.cuh"
 
+namespace cg = cooperative_groups;
+
 namespace rt {
 
 namespace {
 
-constexpr int kHot = 32;      // hottest rows (smallest indices) kept warp-private per CTA
 constexpr int kCooT = 256;
 constexpr int kMaxEll = 64;
 
+// ------------------------------------------------------------ fixed-point scale --
+struct FixScale {
+  double mul;    // 2^S: product -> fixed point (units of 2^-S... split at 2^32 below)
+  double outH;   // 2^(32 - S): weight of the H word
+  double outL;   // 2^-S: weight of the L word
+  int S;
+};
+
+template <typename TV>
+__global__ void abs_max_kernel(const TV *__restrict__ v, int64_t n, unsigned long long *__restrict__ out) {
+  double m = 0.0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs((double)v[e]));
+  // a non-negative double orders like its bit pattern: the maximum is order-independent
+  unsigned long long b = (unsigned long long)__double_as_longlong(m);
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, b, o);
+    b = t > b ? t : b;
+  }
+  if ((threadIdx.x & 31) == 0 && b) atomicMax(out, b);
+}
+
+// S = 91 - ceil(log2 N) - e with max|v| < 2^e: |v omega 2^S| < 2^(94 - ceil(log2 N)), so the
+// H words (|H| < 2^(62 - ceil(log2 N))) and the L words (< 2^32 each) of N terms never overflow.
+__global__ void fix_scale_kernel(const unsigned long long *__restrict__ maxbits, const int64_t *__restrict__ nglob,
+                                 FixScale *__restrict__ fs) {
+  const double m = __longlong_as_double((long long)*maxbits);
+  int e = 0;
+  if (m > 0.0) frexp(m, &e);
+  const int64_t N = *nglob > 1 ? *nglob : 1;
+  const int lg = N > 1 ? 64 - __clzll((unsigned long long)(N - 1)) : 0;
+  int S = 91 - lg - e;
+  S = S > 1000 ? 1000 : (S < -1000 ? -1000 : S);
+  fs->S = S;
+  fs->mul = ldexp(1.0, S);
+  fs->outH = ldexp(1.0, 32 - S);
+  fs->outL = ldexp(1.0, -S);
+}
+
+__device__ __forceinline__ void to_fixed(double prod, double mul, long long &H, long long &L) {
+  const double T = prod * mul;                 // exact power-of-two scaling
+  const double hf = floor(T * 0x1p-32);
+  H = (long long)hf;
+  L = __double2ll_rn(T - hf * 0x1p32);         // exact difference in [0, 2^32), fraction rounded
+}
+
 // ---------------------------------------------------------------- COO sketch (a8) --
-// Y[i_j, k] += v * Omega_j[c, k0 + k], c = sum_{m != j} i_m prod_{m' < m, m' != j} I_m'.
-// Products and sums in fp64.  Count tensors are heavy-tailed (BASELINE configs[4]: Zipf(1.1)
-// indices, the heaviest mode-3 row holds ~9 % of the nonzeros), so naive atomics serialise
-// on a few addresses.  Per warp instruction, lanes holding the same row are first combined
-// with __match_any_sync + a leader reduction (one update per distinct row and warp); rows
-// < kHot (the heavy rows of these tensors) then go to a warp-private shared-memory
-// accumulator (no atomics: one writer lane per row per instruction), flushed once per CTA;
-// other rows use one fp64 global atomic per distinct row and warp.  Global fp64 atomics make
-// the sum order run-dependent (rounding-level differences only).
+// Y[i_j, k] += v * Omega_j[c, k], c = sum_{m != j} i_m prod_{m' < m, m' != j} I_m', in fixed
+// point (see the file header).  Count tensors are heavy-tailed (BASELINE configs[4]: Zipf(1.1)
+// indices; the heaviest mode-3 row holds ~9 % of the nonzeros), so lanes holding the same row
+// are first combined (__match_any_sync + a shuffle tree over the group), rows < hot (the heavy
+// rows of these tensors) go to warp-private shared-memory accumulators (one writer lane per
+// row and instruction) flushed once per CTA, other rows to global int64 atomics (one per
+// distinct row and warp).  Integer adds make every one of these orders give the same sum.
 template <typename TV, typename TN>
-__global__ void __launch_bounds__(kCooT) sketch_coo_kernel(CooDev g, int mode, int ell, uint64_t seed,
-                                                           int64_t nper, double *__restrict__ Y) {
-  extern __shared__ double hot[];  // [warps][kHot][ell]
+__global__ void __launch_bounds__(kCooT) sketch_coo_kernel(CooDev g, const int64_t *__restrict__ nnz_dev, int mode,
+                                                           int ell, int hot, uint64_t seed,
+                                                           const FixScale *__restrict__ fs,
+                                                           unsigned long long *__restrict__ YH,
+                                                           unsigned long long *__restrict__ YL) {
+  extern __shared__ long long hsm[];  // [warps][hot][ell] H, then the same for L
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int kW = kCooT / 32;
   const int64_t I = g.dims[mode];
-  const int hrows = (int)(I < kHot ? I : kHot);
-  double *myhot = hot + (size_t)warp * kHot * ell;
-  for (int e = threadIdx.x; e < (kCooT / 32) * kHot * ell; e += kCooT) hot[e] = 0.0;
+  const int hrows = (int)(I < hot ? I : hot);
+  long long *hH = hsm + (size_t)warp * hot * ell;
+  long long *hL = hsm + (size_t)(kW + warp) * hot * ell;
+  for (int e = threadIdx.x; e < 2 * kW * hot * ell; e += kCooT) hsm[e] = 0;
   __syncthreads();
   int64_t stride[kMaxModes];
   int64_t s = 1;
@@ -50,11 +119,13 @@ __global__ void __launch_bounds__(kCooT) sketch_coo_kernel(CooDev g, int mode, i
     stride[k] = (k == mode) ? 0 : s;
     if (k != mode) s *= g.dims[k];
   }
+  const double mul = fs->mul;
   const TV *vals = (const TV *)g.vals;
   const int nb = (ell + 3) >> 2;
-  const int64_t e0 = (int64_t)blockIdx.x * nper, e1 = min(g.nnz, e0 + nper);
-  // warp-strided loop with uniform trip count (inactive lanes carry row = -1)
-  for (int64_t base = e0 + (int64_t)warp * 32; base < e1; base += kCooT) {
+  const int64_t nnz = nnz_dev ? *nnz_dev : g.nnz;
+  const int64_t nper = (nnz + gridDim.x - 1) / gridDim.x;
+  const int64_t e0 = (int64_t)blockIdx.x * nper, e1 = min(nnz, e0 + nper);
+  for (int64_t base = e0 + (int64_t)warp * 32; base < e1; base += kCooT) {  // uniform trip count per warp
     const int64_t e = base + lane;
     const bool act = e < e1;
     int64_t c = 0;
@@ -67,9 +138,6 @@ __global__ void __launch_bounds__(kCooT) sketch_coo_kernel(CooDev g, int mode, i
     }
     const unsigned grp = __match_any_sync(0xffffffffu, row);
     const int leader = __ffs(grp) - 1;
-    // rows shared by more than two lanes (the heavy rows of Zipf-like data): tree reduction over
-    // the group in 5 shuffle steps (partner = the member 2^k ranks further, __fns) instead of
-    // a serial loop over up to 32 members
     const bool big = __any_sync(0xffffffffu, __popc(grp) > 2);
     unsigned src[5];
     const int rank = __popc(grp & ((1u << lane) - 1u));
@@ -78,37 +146,40 @@ __global__ void __launch_bounds__(kCooT) sketch_coo_kernel(CooDev g, int mode, i
       for (int k = 0; k < 5; ++k) src[k] = __fns(grp, lane, 1 + (1 << k));
     }
     for (int jb = 0; jb < nb; ++jb) {
-      float4 dummy;
-      (void)dummy;
-      double pr[4] = {0.0, 0.0, 0.0, 0.0};
+      long long h[4] = {0, 0, 0, 0}, l[4] = {0, 0, 0, 0};
       if (act) {
         const uint4 w = omega_words(seed, mode, 0, (uint64_t)c, (uint32_t)jb);
         Normal4<TN> z(w);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) pr[q] = v * (double)z.v[q];
+        for (int q = 0; q < 4; ++q) to_fixed(v * (double)z.v[q], mul, h[q], l[q]);
       }
-      // sum over the lanes of this row group (into the group's first lane)
-      if (!big) {
+      if (!big) {  // groups of <= 2 lanes: every member adds the others' words
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          double t = 0.0;
+          long long th = 0, tl = 0;
           unsigned m = grp;
           while (m) {
             const int sl = __ffs(m) - 1;
-            t += __shfl_sync(grp, pr[q], sl);
+            th += __shfl_sync(grp, h[q], sl);
+            tl += __shfl_sync(grp, l[q], sl);
             m &= m - 1;
           }
-          pr[q] = t;
+          h[q] = th;
+          l[q] = tl;
         }
-      } else {
+      } else {  // tree over the group: partner = the member 2^k ranks further (__fns)
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
           const bool take = src[k] != 0xffffffffu && (rank & ((2 << k) - 1)) == 0;
           const int sl = (src[k] != 0xffffffffu) ? (int)src[k] : lane;
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            const double o = __shfl_sync(0xffffffffu, pr[q], sl);
-            if (take) pr[q] += o;
+            const long long oh = __shfl_sync(0xffffffffu, h[q], sl);
+            const long long ol = __shfl_sync(0xffffffffu, l[q], sl);
+            if (take) {
+              h[q] += oh;
+              l[q] += ol;
+            }
           }
         }
       }
@@ -117,8 +188,13 @@ __global__ void __launch_bounds__(kCooT) sketch_coo_kernel(CooDev g, int mode, i
         for (int q = 0; q < 4; ++q) {
           const int k = 4 * jb + q;
           if (k < ell) {
-            if (row < hrows) myhot[row * ell + k] += pr[q];
-            else atomicAdd(&Y[row + I * k], pr[q]);
+            if (row < hrows) {
+              hH[row * ell + k] += h[q];
+              hL[row * ell + k] += l[q];
+            } else {
+              atomicAdd(&YH[row + I * k], (unsigned long long)h[q]);
+              atomicAdd(&YL[row + I * k], (unsigned long long)l[q]);
+            }
           }
         }
       }
@@ -126,15 +202,25 @@ __global__ void __launch_bounds__(kCooT) sketch_coo_kernel(CooDev g, int mode, i
   }
   __syncthreads();
   for (int e = threadIdx.x; e < hrows * ell; e += kCooT) {
-    double t = 0.0;
-    for (int w = 0; w < kCooT / 32; ++w) t += hot[(size_t)w * kHot * ell + e];
-    if (t != 0.0) atomicAdd(&Y[(e / ell) + I * (e % ell)], t);
+    long long th = 0, tl = 0;
+    for (int w = 0; w < kW; ++w) {
+      th += hsm[(size_t)w * hot * ell + e];
+      tl += hsm[(size_t)(kW + w) * hot * ell + e];
+    }
+    const int r = e / ell, k = e % ell;
+    if (th) atomicAdd(&YH[r + I * k], (unsigned long long)th);
+    if (tl) atomicAdd(&YL[r + I * k], (unsigned long long)tl);
   }
 }
 
-// ------------------------------------------------------ CPQR on Q^T (a9, step 1) --
-// r: I rows of length ell (row-major copy of Q); per step j the residual norms
-// sum_{t >= j} r_i[t]^2 (fixed order), argmax with ties to the smallest index.
+__global__ void y_from_fixed_kernel(const long long *__restrict__ YH, const long long *__restrict__ YL, int64_t n,
+                                    const FixScale *__restrict__ fs, double *__restrict__ Y) {
+  const double oh = fs->outH, ol = fs->outL;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    Y[e] = fma((double)YH[e], oh, (double)YL[e] * ol);
+}
+
+// ------------------------------------------------------------- argmax helpers --
 struct ArgMax {
   double v;
   int64_t i;
@@ -142,13 +228,16 @@ struct ArgMax {
 __device__ __forceinline__ ArgMax better(ArgMax a, ArgMax b) {
   return (b.v > a.v || (b.v == a.v && b.i < a.i)) ? b : a;
 }
-__device__ ArgMax block_argmax(ArgMax m) {
+// CTA-wide argmax (ties to the smallest index); the result is returned to every thread.
+__device__ ArgMax block_argmax_all(ArgMax m) {
   __shared__ double sv[32];
   __shared__ int64_t si[32];
+  __shared__ ArgMax res;
   for (int o = 16; o; o >>= 1) {
     ArgMax t{__shfl_xor_sync(0xffffffffu, m.v, o), __shfl_xor_sync(0xffffffffu, m.i, o)};
     m = better(m, t);
   }
+  __syncthreads();  // sv/si/res may still be read by a previous call
   if ((threadIdx.x & 31) == 0) {
     sv[threadIdx.x >> 5] = m.v;
     si[threadIdx.x >> 5] = m.i;
@@ -156,112 +245,50 @@ __device__ ArgMax block_argmax(ArgMax m) {
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = better(m, ArgMax{sv[w], si[w]});
-  }
-  return m;
-}
-
-__global__ void cpqr_norm_argmax(const double *__restrict__ r, int64_t I, int ell, int j,
-                                 const int *__restrict__ chosen, double *__restrict__ pv, int64_t *__restrict__ pi) {
-  ArgMax m{-1.0, INT64_MAX};
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x) {
-    if (chosen[i]) continue;
-    double s = 0.0;
-    for (int t = j; t < ell; ++t) s += r[i * ell + t] * r[i * ell + t];
-    m = better(m, ArgMax{s, i});
-  }
-  m = block_argmax(m);
-  if (threadIdx.x == 0) {
-    pv[blockIdx.x] = m.v;
-    pi[blockIdx.x] = m.i;
-  }
-}
-
-__global__ void argmax_finish(const double *__restrict__ pv, const int64_t *__restrict__ pi, int n,
-                              int64_t *__restrict__ out_i, double *__restrict__ out_v, int *__restrict__ chosen) {
-  ArgMax m{-1.0, INT64_MAX};
-  for (int b = threadIdx.x; b < n; b += blockDim.x) m = better(m, ArgMax{pv[b], pi[b]});
-  m = block_argmax(m);
-  if (threadIdx.x == 0) {
-    *out_i = m.i;
-    if (out_v) *out_v = m.v;
-    if (chosen && m.i != INT64_MAX) chosen[m.i] = 1;
-  }
-}
-
-// Householder reflector from column p's rows j..ell-1 (oracle form: alpha = -sign(v0)||v||,
-// v0 -= alpha, v /= ||v||), applied to every column: r_i[j:] -= 2 (v . r_i[j:]) v.
-__global__ void cpqr_reflect(double *__restrict__ r, int64_t I, int ell, int j, const int64_t *__restrict__ pivot) {
-  __shared__ double v[256];
-  __shared__ double scale;
-  const int64_t p = *pivot;
-  if (threadIdx.x == 0) {
-    double nv = 0.0;
-    for (int t = j; t < ell; ++t) { v[t] = r[p * ell + t]; nv += v[t] * v[t]; }
-    nv = sqrt(nv);
-    if (nv == 0.0) {
-      scale = 0.0;
-    } else {
-      const double alpha = v[j] >= 0.0 ? -nv : nv;
-      v[j] -= alpha;
-      double vn = 0.0;
-      for (int t = j; t < ell; ++t) vn += v[t] * v[t];
-      vn = sqrt(vn);
-      if (vn == 0.0) {
-        scale = 0.0;
-      } else {
-        for (int t = j; t < ell; ++t) v[t] /= vn;
-        scale = 1.0;
-      }
-    }
+    res = m;
   }
   __syncthreads();
-  if (scale == 0.0) return;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x) {
-    if (i == p) continue;  // the pivot column is read by every CTA above and never used again
-    double s = 0.0;
-    for (int t = j; t < ell; ++t) s += v[t] * r[i * ell + t];
-    for (int t = j; t < ell; ++t) r[i * ell + t] -= 2.0 * s * v[t];
-  }
+  return res;
 }
 
-__global__ void transpose_q(const double *__restrict__ Q, int64_t I, int ell, double *__restrict__ r) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < I * ell; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / ell;
-    const int t = (int)(e % ell);
-    r[e] = Q[i + I * t];
-  }
-}
+// ------------------------------------------ sRRQR selection (a9), one cooperative kernel --
+// Reading R9 (oracle/srrqr.py): Businger-Golub CPQR on Q^T (pivot = largest residual column
+// norm sum_{t >= j} r_i[t]^2, ties to the smallest index; Householder reflector in the oracle's
+// form) gives the initial S; then, while max_{i not in S, k} |A_ik| > eta with A = Q Q_S^{-1}
+// (ties: smallest i, then smallest k), swap S_k <- i; finally S is sorted and A is formed for
+// the sorted selection.  Each step's reduction is over all rows of the grid (per-CTA argmax,
+// grid.sync, every CTA reduces the partials in the same order -> identical decisions).
+// Q_S^{-1} by Gauss-Jordan with partial pivoting, redundantly in every CTA; a pivot below
+// l eps max|Q_S| marks P^T Q singular (status ST_SINGULAR_PQ -> ENUMERIC).
+constexpr int kSrT = 256;
 
-// --------------------------------------- oblique factor A = Q Q_S^{-1} (a9, step 2) --
-// Inverse of Q_S (ell x ell, rows sel of Q) by Gauss-Jordan with partial pivoting (one CTA).
-// status = 1 when a pivot is below ell * eps * max|Q_S| (singular P^T Q, ENUMERIC).
-__global__ void qs_inverse(const double *__restrict__ Q, int64_t I, int ell, const int64_t *__restrict__ sel,
-                           double *__restrict__ inv, int *__restrict__ status) {
-  extern __shared__ double sm[];
-  double *M = sm;                 // ell x 2 ell, row-major
-  const int w = 2 * ell;
+// Gauss-Jordan inverse of Q[sel, :] (l x l) into inv (column-major), M scratch (l x 2l row-major).
+// Returns false when singular.  All threads of the CTA call it.
+__device__ bool gj_inverse(const double *__restrict__ Q, int64_t m, int l, const int64_t *sel, double *M, double *inv) {
   __shared__ int piv;
   __shared__ double amax;
-  for (int e = threadIdx.x; e < ell * w; e += blockDim.x) {
+  __shared__ int bad;
+  const int w = 2 * l;
+  for (int e = threadIdx.x; e < l * w; e += blockDim.x) {
     const int r = e / w, cc = e % w;
-    M[e] = cc < ell ? Q[sel[r] + I * cc] : (cc - ell == r ? 1.0 : 0.0);
+    M[e] = cc < l ? Q[sel[r] + m * cc] : (cc - l == r ? 1.0 : 0.0);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
     double a = 0.0;
-    for (int r = 0; r < ell; ++r)
-      for (int cc = 0; cc < ell; ++cc) a = fmax(a, fabs(M[r * w + cc]));
+    for (int r = 0; r < l; ++r)
+      for (int cc = 0; cc < l; ++cc) a = fmax(a, fabs(M[r * w + cc]));
     amax = a;
-    *status = 0;
+    bad = 0;
   }
   __syncthreads();
-  for (int col = 0; col < ell; ++col) {
+  for (int col = 0; col < l; ++col) {
     if (threadIdx.x == 0) {
       int best = col;
-      for (int r = col + 1; r < ell; ++r)
+      for (int r = col + 1; r < l; ++r)
         if (fabs(M[r * w + col]) > fabs(M[best * w + col])) best = r;
       piv = best;
-      if (!(fabs(M[best * w + col]) > ell * 2.2e-16 * amax)) *status = 1;
+      if (!(fabs(M[best * w + col]) > l * 2.2e-16 * amax)) bad = 1;
     }
     __syncthreads();
     const int pr = piv;
@@ -272,65 +299,179 @@ __global__ void qs_inverse(const double *__restrict__ Q, int64_t I, int ell, con
         M[pr * w + cc] = t;
       }
     __syncthreads();
-    const double d = M[col * w + col];
+    const double dinv = 1.0 / M[col * w + col];
     __syncthreads();
-    for (int cc = threadIdx.x; cc < w; cc += blockDim.x) M[col * w + cc] /= d;
+    for (int cc = threadIdx.x; cc < w; cc += blockDim.x) M[col * w + cc] *= dinv;
     __syncthreads();
-    for (int e = threadIdx.x; e < ell * w; e += blockDim.x) {
+    for (int e = threadIdx.x; e < l * w; e += blockDim.x) {
       const int r = e / w, cc = e % w;
-      if (r != col) {
-        const double f = M[r * w + col];
-        if (cc != col) M[e] -= f * M[col * w + cc];
-      }
+      if (r != col && cc != col) M[e] -= M[r * w + col] * M[col * w + cc];
     }
     __syncthreads();
-    for (int r = threadIdx.x; r < ell; r += blockDim.x)
+    for (int r = threadIdx.x; r < l; r += blockDim.x)
       if (r != col) M[r * w + col] = 0.0;
     __syncthreads();
   }
-  // M[:, ell:] = Q_S^{-1}; store column-major inv[a + ell b]
-  for (int e = threadIdx.x; e < ell * ell; e += blockDim.x) {
-    const int a = e % ell, b = e / ell;
-    inv[e] = M[a * w + ell + b];
+  for (int e = threadIdx.x; e < l * l; e += blockDim.x) {
+    const int a = e % l, b = e / l;
+    inv[e] = M[a * w + l + b];
   }
+  __syncthreads();
+  return bad == 0;
 }
 
-// A = Q inv (I x ell), and the argmax of |A_ik| over rows not in the selection (row-major
-// flat order: smallest i, then smallest k on ties).
-__global__ void oblique_apply(const double *__restrict__ Q, int64_t I, int ell, const double *__restrict__ inv,
-                              const int *__restrict__ insel, double *__restrict__ A, double *__restrict__ pv,
-                              int64_t *__restrict__ pi) {
-  ArgMax m{-1.0, INT64_MAX};
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < I; i += (int64_t)gridDim.x * blockDim.x) {
-    for (int k = 0; k < ell; ++k) {
-      double s = 0.0;
-      for (int t = 0; t < ell; ++t) s += Q[i + I * t] * inv[t + ell * k];
-      A[i + I * k] = s;
-      if (!insel[i]) m = better(m, ArgMax{fabs(s), i * ell + k});
+__global__ void __launch_bounds__(kSrT) srrqr_coop_kernel(const double *__restrict__ Q, int64_t m, int l, double eta,
+                                                          int max_swaps, double *__restrict__ r, int *__restrict__ mark,
+                                                          double *__restrict__ pv, int64_t *__restrict__ pi,
+                                                          int64_t *__restrict__ sel_out, double *__restrict__ A,
+                                                          int *__restrict__ swaps_out, unsigned *__restrict__ status) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double sh[];
+  double *M = sh;                        // l x 2l
+  double *inv = M + 2 * l * l;           // l x l
+  double *hv = inv + l * l;              // Householder vector (l)
+  __shared__ int64_t ssel[kMaxEll];
+  __shared__ int hv_ok;
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = gt; e < m * l; e += gs) {
+    const int64_t i = e / l;
+    const int t = (int)(e % l);
+    r[e] = Q[i + m * t];
+  }
+  for (int64_t i = gt; i < m; i += gs) mark[i] = 0;
+  grid.sync();
+  auto global_argmax = [&](ArgMax b) -> ArgMax {
+    b = block_argmax_all(b);
+    if (threadIdx.x == 0) {
+      pv[blockIdx.x] = b.v;
+      pi[blockIdx.x] = b.i;
     }
+    grid.sync();
+    ArgMax gb{-1.0, INT64_MAX};
+    for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) gb = better(gb, ArgMax{pv[q], pi[q]});
+    gb = block_argmax_all(gb);
+    grid.sync();  // every CTA has read pv/pi before they are rewritten
+    return gb;
+  };
+  // ---- Businger-Golub CPQR on Q^T
+  for (int j = 0; j < l; ++j) {
+    ArgMax b{-1.0, INT64_MAX};
+    for (int64_t i = gt; i < m; i += gs) {
+      if (mark[i]) continue;
+      double s2 = 0.0;
+      for (int t = j; t < l; ++t) s2 += r[i * l + t] * r[i * l + t];
+      b = better(b, ArgMax{s2, i});
+    }
+    const int64_t p = global_argmax(b).i;
+    if (threadIdx.x == 0) {
+      ssel[j] = p;
+      // reflector from row p, rows j..l-1 (alpha = -sign(v0) ||v||, v0 -= alpha, v /= ||v||)
+      double nv = 0.0;
+      for (int t = j; t < l; ++t) {
+        hv[t] = r[p * l + t];
+        nv += hv[t] * hv[t];
+      }
+      nv = sqrt(nv);
+      hv_ok = 0;
+      if (nv != 0.0) {
+        const double alpha = hv[j] >= 0.0 ? -nv : nv;
+        hv[j] -= alpha;
+        double vn = 0.0;
+        for (int t = j; t < l; ++t) vn += hv[t] * hv[t];
+        vn = sqrt(vn);
+        if (vn != 0.0) {
+          for (int t = j; t < l; ++t) hv[t] /= vn;
+          hv_ok = 1;
+        }
+      }
+    }
+    __syncthreads();
+    if (hv_ok)
+      for (int64_t i = gt; i < m; i += gs) {
+        if (i == p) continue;  // read by every CTA above; never used again
+        double s2 = 0.0;
+        for (int t = j; t < l; ++t) s2 += hv[t] * r[i * l + t];
+        for (int t = j; t < l; ++t) r[i * l + t] -= 2.0 * s2 * hv[t];
+      }
+    if (gt == 0) mark[p] = 1;
+    grid.sync();
   }
-  m = block_argmax(m);
-  if (threadIdx.x == 0) {
-    pv[blockIdx.x] = m.v;
-    pi[blockIdx.x] = m.i;
+  // ---- maxvol swaps while max_{i not in S} |A_ik| > eta
+  int swaps = 0;
+  bool singular = false;
+  while (true) {
+    if (!gj_inverse(Q, m, l, ssel, M, inv)) {
+      singular = true;
+      break;
+    }
+    ArgMax b{-1.0, INT64_MAX};
+    for (int64_t i = gt; i < m; i += gs) {
+      if (mark[i]) continue;
+      for (int k = 0; k < l; ++k) {
+        double s2 = 0.0;
+        for (int t = 0; t < l; ++t) s2 = fma(Q[i + m * t], inv[t + l * k], s2);
+        b = better(b, ArgMax{fabs(s2), i * l + k});
+      }
+    }
+    const ArgMax gb = global_argmax(b);
+    if (!(gb.v > eta) || swaps >= max_swaps) break;
+    const int64_t i = gb.i / l;
+    const int k = (int)(gb.i % l);
+    const int64_t old = ssel[k];
+    __syncthreads();
+    if (threadIdx.x == 0) ssel[k] = i;
+    if (gt == 0) {
+      mark[old] = 0;
+      mark[i] = 1;
+    }
+    ++swaps;
+    grid.sync();
   }
+  if (singular) {
+    if (gt == 0) atomicOr(status, (unsigned)ST_SINGULAR_PQ);
+    return;  // uniform over the grid (every CTA computed the same inverse)
+  }
+  // ---- sort S ascending; A = Q Q_S^{-1} for the sorted selection
+  if (threadIdx.x == 0)
+    for (int a = 1; a < l; ++a)
+      for (int b2 = a; b2 > 0 && ssel[b2 - 1] > ssel[b2]; --b2) {
+        const int64_t t = ssel[b2];
+        ssel[b2] = ssel[b2 - 1];
+        ssel[b2 - 1] = t;
+      }
+  __syncthreads();
+  gj_inverse(Q, m, l, ssel, M, inv);
+  for (int64_t i = gt; i < m; i += gs)
+    for (int k = 0; k < l; ++k) {
+      double s2 = 0.0;
+      for (int t = 0; t < l; ++t) s2 = fma(Q[i + m * t], inv[t + l * k], s2);
+      A[i + m * k] = s2;
+    }
+  if (gt == 0) *swaps_out = swaps;
+  if (blockIdx.x == 0)
+    for (int t = threadIdx.x; t < l; t += blockDim.x) sel_out[t] = ssel[t];
 }
 
 // ------------------------------------------------------- selection / compaction (a10) --
-__global__ void mark_sel(const int64_t *__restrict__ sel, int ell, int *__restrict__ mark) {
-  for (int t = threadIdx.x; t < ell; t += blockDim.x) mark[sel[t]] = 1;
-}
-
+// Keep the nonzeros whose mode-n index is selected and renumber it to its position in the
+// sorted selection; order-preserving (per-block counts, one exclusive scan, scatter).  The
+// live nnz is read from the device; grids are sized for the input nnz (an upper bound) and
+// blocks past the live count exit.
 __global__ void build_lookup(const int64_t *__restrict__ sel, int ell, int32_t *__restrict__ lut) {
   for (int t = threadIdx.x; t < ell; t += blockDim.x) lut[sel[t]] = t;
 }
 
 constexpr int kCompactB = 1024;
 
-__global__ void compact_count(const int32_t *__restrict__ idx, int64_t nnz, const int32_t *__restrict__ lut,
-                              int64_t *__restrict__ counts) {
+__global__ void compact_count(const int32_t *__restrict__ idx, const int64_t *__restrict__ nnz_dev,
+                              const int32_t *__restrict__ lut, int64_t *__restrict__ counts) {
   __shared__ int64_t sc[32];
+  const int64_t nnz = *nnz_dev;
   const int64_t e = (int64_t)blockIdx.x * kCompactB + threadIdx.x;
+  if ((int64_t)blockIdx.x * kCompactB >= nnz) {
+    if (threadIdx.x == 0) counts[blockIdx.x] = 0;
+    return;
+  }
   const int keep = (e < nnz && lut[idx[e]] >= 0) ? 1 : 0;
   const unsigned bal = __ballot_sync(0xffffffffu, keep);
   if ((threadIdx.x & 31) == 0) sc[threadIdx.x >> 5] = __popc(bal);
@@ -342,8 +483,8 @@ __global__ void compact_count(const int32_t *__restrict__ idx, int64_t nnz, cons
   }
 }
 
+// One CTA: per-thread chunk sums, a serial scan of the chunk sums, then the chunks.
 __global__ void exclusive_scan_single(int64_t *__restrict__ v, int64_t n, int64_t *__restrict__ total) {
-  // one CTA: chunked sequential scan with a per-thread chunk then a CTA scan of chunk sums
   __shared__ int64_t part[1024];
   const int64_t per = (n + blockDim.x - 1) / blockDim.x;
   const int64_t b = threadIdx.x * per, e = min(n, b + per);
@@ -370,12 +511,15 @@ __global__ void exclusive_scan_single(int64_t *__restrict__ v, int64_t n, int64_
 }
 
 template <typename TV>
-__global__ void compact_scatter(CooDev in, int mode, const int32_t *__restrict__ lut, const int64_t *__restrict__ offs,
+__global__ void compact_scatter(CooDev in, const int64_t *__restrict__ nnz_dev, int mode,
+                                const int32_t *__restrict__ lut, const int64_t *__restrict__ offs,
                                 int32_t *const *__restrict__ oidx, TV *__restrict__ ovals) {
   __shared__ int wsum[32];
+  const int64_t nnz = *nnz_dev;
+  if ((int64_t)blockIdx.x * kCompactB >= nnz) return;
   const int64_t e = (int64_t)blockIdx.x * kCompactB + threadIdx.x;
   int32_t pos = -1;
-  if (e < in.nnz) pos = lut[in.idx[mode][e]];
+  if (e < nnz) pos = lut[in.idx[mode][e]];
   const int keep = pos >= 0;
   const unsigned bal = __ballot_sync(0xffffffffu, keep);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -400,113 +544,138 @@ __global__ void fill_i32(int32_t *p, int64_t n, int32_t v) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) p[e] = v;
 }
 
-template <typename T>
-T fetch1(Ctx &c, const T *dev) {
-  T h;
-  RT_CUDA(cudaMemcpyAsync(&h, dev, sizeof(T), cudaMemcpyDeviceToHost, c.stream));
-  RT_CUDA(cudaStreamSynchronize(c.stream));
-  return h;
+// Debug-checks flag: every index of the COO input in range (status bit on failure).
+__global__ void check_indices(const int32_t *__restrict__ idx, int64_t n, int64_t dim, unsigned *__restrict__ status) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    if (idx[e] < 0 || idx[e] >= dim) atomicOr(status, (unsigned)ST_BAD_INDEX);
+}
+
+// Rank-order gather of the core nonzeros: rank q's block [q * cap, q * cap + cnt[q]) of the
+// allgathered arrays goes to offset sum_{q' < q} cnt[q'].
+template <typename TV>
+__global__ void gather_core(const int32_t *__restrict__ gidx, const TV *__restrict__ gvals, int d, int nranks,
+                            int64_t cap, const int64_t *__restrict__ cnt, int32_t *const *__restrict__ oidx,
+                            TV *__restrict__ ovals) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < (int64_t)nranks * cap;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int q = (int)(e / cap);
+    const int64_t t = e % cap;
+    if (t >= cnt[q]) continue;
+    int64_t o = t;
+    for (int q2 = 0; q2 < q; ++q2) o += cnt[q2];
+    for (int k = 0; k < d; ++k) oidx[k][o] = gidx[((int64_t)q * d + k) * cap + t];
+    ovals[o] = gvals[(int64_t)q * cap + t];
+  }
 }
 
 int grid_for(Ctx &c, int64_t n, int threads = 256) {
   return (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c.num_sms * 8, (n + threads - 1) / threads));
 }
 
+// Fixed-point scale of a sketch: max|v| over this rank's values, maximum and nnz over the
+// ranks, then S (device-side; no host synchronisation).
+void fix_scale(Ctx &c, const void *vals, DT vt, int64_t nnz, FixScale *fs) {
+  DevBuf<unsigned long long> mb(c, 1);
+  DevBuf<int64_t> nb(c, 1);
+  mb.zero();
+  if (nnz > 0) {
+    const int g = grid_for(c, nnz);
+    if (vt == DT::F64) RT_LAUNCH(c, abs_max_kernel<double>, g, 256, 0, (const double *)vals, nnz, mb.p);
+    else RT_LAUNCH(c, abs_max_kernel<float>, g, 256, 0, (const float *)vals, nnz, mb.p);
+  }
+  RT_CUDA(cudaMemcpyAsync(nb.p, &nnz, sizeof(int64_t), cudaMemcpyHostToDevice, c.stream));
+  allreduce_u64_max(c, mb.p, 1);
+  allreduce_i64_sum(c, nb.p, 1);
+  RT_LAUNCH(c, fix_scale_kernel, 1, 1, 0, mb.p, nb.p, fs);
+}
+
 }  // namespace
 
-void sketch_coo(Ctx &c, const CooDev &g, int mode, int ell, uint64_t seed, bool normals_f64, double *Y) {
+// Y (I x ell, fp64) = G_(n) Omega_n over the (live) nonzeros of g, summed over the ranks.
+void sketch_coo(Ctx &c, const CooDev &g, int mode, int ell, uint64_t seed, bool normals_f64, double *Y,
+                const int64_t *nnz_dev, const void *fs_dev) {
   const int64_t I = g.dims[mode];
   RT_REQUIRE(ell <= kMaxEll, "sparse sketch: l > 64 is not supported");
-  RT_CUDA(cudaMemsetAsync(Y, 0, sizeof(double) * I * ell, c.stream));
-  if (g.nnz == 0) return;
-  const size_t smem = sizeof(double) * (kCooT / 32) * kHot * ell;
-  const int64_t blocks = std::min<int64_t>((int64_t)c.num_sms * 4, (g.nnz + 1023) / 1024);
-  const int64_t nper = (g.nnz + blocks - 1) / blocks;
+  const FixScale *fs = (const FixScale *)fs_dev;
+  DevBuf<FixScale> own;
+  if (!fs) {  // standalone use: scale from this tensor
+    own.alloc(c, 1);
+    fix_scale(c, g.vals, g.vt, g.nnz, own.p);
+    fs = own.p;
+  }
+  DevBuf<long long> Yf(c, 2 * (size_t)I * ell);  // [H | L]
+  Yf.zero();
+  if (g.nnz > 0) {
+    constexpr int kW = kCooT / 32;
+    const int hot = (int)std::max<int64_t>(1, std::min<int64_t>(32, (200 * 1024) / (2 * kW * ell * 8)));
+    const size_t smem = (size_t)2 * kW * hot * ell * sizeof(long long);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c.num_sms * 4, (g.nnz + 1023) / 1024));
+    unsigned long long *yh = (unsigned long long *)Yf.p, *yl = yh + (size_t)I * ell;
 #define RT_COO(TV, TN)                                                                                     \
   do {                                                                                                     \
     smem_attr(sketch_coo_kernel<TV, TN>, smem);                                                            \
-    RT_LAUNCH(c, (sketch_coo_kernel<TV, TN>), (int)blocks, kCooT, smem, g, mode, ell, seed, nper, Y);      \
+    RT_LAUNCH(c, (sketch_coo_kernel<TV, TN>), blocks, kCooT, smem, g, nnz_dev, mode, ell, hot, seed, fs, yh, yl); \
   } while (0)
-  if (g.vt == DT::F64) {
-    RT_COO(double, double);
-  } else if (normals_f64) {
-    RT_COO(float, double);
-  } else {
-    RT_COO(float, float);
-  }
+    if (g.vt == DT::F64) {
+      RT_COO(double, double);
+    } else if (normals_f64) {
+      RT_COO(float, double);
+    } else {
+      RT_COO(float, float);
+    }
 #undef RT_COO
+  }
+  allreduce_i64_sum(c, Yf.p, Yf.n);  // exact: integer words
+  RT_LAUNCH(c, y_from_fixed_kernel, grid_for(c, I * ell), 256, 0, Yf.p, Yf.p + (size_t)I * ell, I * ell, fs, Y);
 }
 
-void srrqr(Ctx &c, const double *Q, int64_t m, int l, double eta, int64_t *sel_dev, double *A, int *swaps_host) {
-  RT_REQUIRE(l >= 1 && l <= 256 && m >= l, "srrqr: need 1 <= l <= 256 and m >= l");
-  DevBuf<double> r(c, (size_t)m * l);
-  RT_LAUNCH(c, transpose_q, grid_for(c, m * l), 256, 0, Q, m, l, r.p);
-  DevBuf<int> chosen(c, m);
-  chosen.zero();
-  const int g = grid_for(c, m);
-  DevBuf<double> pv(c, g);
-  DevBuf<int64_t> pi(c, g), piv(c, l);
-  // Businger-Golub CPQR pivots (initial S)
-  for (int j = 0; j < l; ++j) {
-    RT_LAUNCH(c, cpqr_norm_argmax, g, 256, 0, r.p, m, l, j, chosen.p, pv.p, pi.p);
-    RT_LAUNCH(c, argmax_finish, 1, 256, 0, pv.p, pi.p, g, piv.p + j, (double *)nullptr, chosen.p);
-    RT_LAUNCH(c, cpqr_reflect, g, 256, 0, r.p, m, l, j, piv.p + j);
+void srrqr(Ctx &c, const double *Q, int64_t m, int l, double eta, int64_t *sel_dev, double *A, int *swaps_dev) {
+  RT_REQUIRE(l >= 1 && l <= kMaxEll && m >= l, "srrqr: need 1 <= l <= 64 and m >= l");
+  const size_t smem = sizeof(double) * (3 * (size_t)l * l + l);
+  smem_attr(srrqr_coop_kernel, smem);
+  int per_sm = 0;
+  RT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srrqr_coop_kernel, kSrT, smem));
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c.num_sms * std::max(per_sm, 1),
+                                                               (m + kSrT - 1) / kSrT));
+  DevBuf<double> r(c, (size_t)m * l), pv(c, grid);
+  DevBuf<int> mark(c, m);
+  DevBuf<int64_t> pi(c, grid);
+  DevBuf<int> swl;
+  if (!swaps_dev) {
+    swl.alloc(c, 1);
+    swaps_dev = swl.p;
   }
-  std::vector<int64_t> sel(l);
-  RT_CUDA(cudaMemcpyAsync(sel.data(), piv.p, sizeof(int64_t) * l, cudaMemcpyDeviceToHost, c.stream));
-  RT_CUDA(cudaStreamSynchronize(c.stream));
-  // maxvol swaps while max_{i not in S} |A_ik| > eta
-  DevBuf<double> inv(c, (size_t)l * l), mv(c, 1);
-  DevBuf<int> st(c, 1), insel(c, m);
-  DevBuf<int64_t> dsel(c, l), mi(c, 1);
-  const size_t qsm = sizeof(double) * l * 2 * l;
-  if (qsm > 48 * 1024) smem_attr(qs_inverse, qsm);
-  int swaps = 0;
-  auto compute_A = [&](bool want_max) -> std::pair<double, int64_t> {
-    RT_CUDA(cudaMemcpyAsync(dsel.p, sel.data(), sizeof(int64_t) * l, cudaMemcpyHostToDevice, c.stream));
-    RT_LAUNCH(c, fill_i32, grid_for(c, m), 256, 0, insel.p, m, 0);
-    RT_LAUNCH(c, mark_sel, 1, 256, 0, dsel.p, l, insel.p);
-    RT_LAUNCH(c, qs_inverse, 1, 256, qsm, Q, m, l, dsel.p, inv.p, st.p);
-    RT_LAUNCH(c, oblique_apply, g, 256, 0, Q, m, l, inv.p, insel.p, A, pv.p, pi.p);
-    RT_LAUNCH(c, argmax_finish, 1, 256, 0, pv.p, pi.p, g, mi.p, mv.p, (int *)nullptr);
-    const int status = fetch1(c, st.p);
-    if (status) throw Error(RTUCKER_ENUMERIC, "SP-STHOSVD: singular P^T Q (fewer than l independent rows)");
-    if (!want_max) return {0.0, 0};
-    return {fetch1(c, mv.p), fetch1(c, mi.p)};
-  };
-  while (swaps < 10000) {
-    auto best = compute_A(true);
-    if (!(best.first > eta)) break;
-    const int64_t i = best.second / l;
-    const int k = (int)(best.second % l);
-    sel[k] = i;
-    ++swaps;
-  }
-  std::sort(sel.begin(), sel.end());
-  compute_A(false);  // A for the sorted selection (its column order defines the renumbering)
-  RT_CUDA(cudaMemcpyAsync(sel_dev, sel.data(), sizeof(int64_t) * l, cudaMemcpyHostToDevice, c.stream));
-  RT_CUDA(cudaStreamSynchronize(c.stream));
-  if (swaps_host) *swaps_host = swaps;
+  double *rp = r.p, *pvp = pv.p;
+  int *mp = mark.p;
+  int64_t *pip = pi.p;
+  int ms = 10000;
+  unsigned *stp = c.status;
+  void *args[] = {(void *)&Q, (void *)&m, (void *)&l, (void *)&eta, (void *)&ms, (void *)&rp, (void *)&mp,
+                  (void *)&pvp, (void *)&pip, (void *)&sel_dev, (void *)&A, (void *)&swaps_dev, (void *)&stp};
+  RT_CUDA(cudaLaunchCooperativeKernel((const void *)srrqr_coop_kernel, dim3(grid), dim3(kSrT), args, smem, c.stream));
+  c.launches++;
 }
 
-int64_t coo_select(Ctx &c, const CooDev &in, int mode, const int64_t *sel, int l, int32_t *const *out_idx,
-                   void *out_vals) {
+// Keep entries whose mode-n index is in sel (sorted, length l) and renumber it; the new nnz
+// is written to nnz_out (device).
+void coo_select(Ctx &c, const CooDev &in, const int64_t *nnz_dev, int mode, const int64_t *sel, int l,
+                int32_t *const *out_idx, void *out_vals, int64_t *nnz_out) {
   const int64_t I = in.dims[mode];
   DevBuf<int32_t> lut(c, I);
   RT_LAUNCH(c, fill_i32, grid_for(c, I), 256, 0, lut.p, I, -1);
   RT_LAUNCH(c, build_lookup, 1, 256, 0, sel, l, lut.p);
-  if (in.nnz == 0) return 0;
-  const int64_t nblk = (in.nnz + kCompactB - 1) / kCompactB;
-  DevBuf<int64_t> offs(c, nblk), total(c, 1);
-  RT_LAUNCH(c, compact_count, (int)nblk, kCompactB, 0, in.idx[mode], in.nnz, lut.p, offs.p);
-  RT_LAUNCH(c, exclusive_scan_single, 1, 1024, 0, offs.p, nblk, total.p);
+  const int64_t nblk = std::max<int64_t>(1, (in.nnz + kCompactB - 1) / kCompactB);
+  DevBuf<int64_t> offs(c, nblk);
+  RT_LAUNCH(c, compact_count, (int)nblk, kCompactB, 0, in.idx[mode], nnz_dev, lut.p, offs.p);
+  RT_LAUNCH(c, exclusive_scan_single, 1, 1024, 0, offs.p, nblk, nnz_out);
   DevBuf<int32_t *> optr(c, kMaxModes);
   RT_CUDA(cudaMemcpyAsync(optr.p, out_idx, sizeof(int32_t *) * kMaxModes, cudaMemcpyHostToDevice, c.stream));
   if (in.vt == DT::F64)
-    RT_LAUNCH(c, compact_scatter<double>, (int)nblk, kCompactB, 0, in, mode, lut.p, offs.p, optr.p, (double *)out_vals);
+    RT_LAUNCH(c, compact_scatter<double>, (int)nblk, kCompactB, 0, in, nnz_dev, mode, lut.p, offs.p, optr.p,
+              (double *)out_vals);
   else
-    RT_LAUNCH(c, compact_scatter<float>, (int)nblk, kCompactB, 0, in, mode, lut.p, offs.p, optr.p, (float *)out_vals);
-  return fetch1(c, total.p);
+    RT_LAUNCH(c, compact_scatter<float>, (int)nblk, kCompactB, 0, in, nnz_dev, mode, lut.p, offs.p, optr.p,
+              (float *)out_vals);
 }
 
 rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int64_t *ranks, int p, uint64_t seed,
@@ -514,11 +683,10 @@ rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int6
   RT_REQUIRE(X != nullptr, "null tensor descriptor");
   if (X->d > kMaxModes) throw Error(RTUCKER_EUNSUPPORTED, "d > RTUCKER_MAX_MODES");
   RT_REQUIRE(X->d >= 1, "d must be >= 1");
-  RT_REQUIRE(X->nnz >= 0, "nnz must be >= 0");
+  RT_REQUIRE(X->nnz >= 0 && X->nnz < INT32_MAX, "nnz must lie in [0, 2^31)");
   RT_REQUIRE(p >= 0, "p must be >= 0");
   RT_REQUIRE(eta >= 1.0, "eta must be >= 1 (P:379)");
   RT_REQUIRE(X->dtype == RTUCKER_F32 || X->dtype == RTUCKER_F64, "dtype must be RTUCKER_F32 or RTUCKER_F64");
-  RT_REQUIRE(c.nranks == 1, "rtucker_sparse_sthosvd: multi-rank contexts are not supported yet");
   const int d = X->d;
   const DT vt = X->dtype == RTUCKER_F64 ? DT::F64 : DT::F32;
   const size_t vs = dt_size(vt);
@@ -531,6 +699,7 @@ rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int6
   int32_t ord[kMaxModes];
   check_order(order, d, ord, cur, false);
   const bool nf64 = vt == DT::F64 || (flags & RTUCKER_ACCUM_MASK) == RTUCKER_ACCUM_FP64;
+  const bool dbg = flags & RTUCKER_DEBUG_CHECKS;
   ResultGuard rg{c, new_result(d)};
   rtucker_result *res = rg.r;
   res->dtype = X->dtype;
@@ -540,7 +709,7 @@ rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int6
   }
   res->seed = seed;
   res->flags = flags;
-  // working COO (ping-pong), device resident
+  // working COO (ping-pong), device resident; nnz and its history live on the device
   const int64_t nnz0 = X->nnz;
   DevBuf<int32_t> ib[2];
   DevBuf<unsigned char> vb[2];
@@ -552,12 +721,19 @@ rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int6
   for (int k = 0; k < d; ++k) {
     RT_REQUIRE(nnz0 == 0 || X->idx[k] != nullptr, "null index array");
     if (nnz0) RT_CUDA(cudaMemcpyAsync(ib[0].p + (size_t)k * nnz0, X->idx[k], sizeof(int32_t) * nnz0, kind, c.stream));
+    if (dbg && nnz0)
+      RT_LAUNCH(c, check_indices, grid_for(c, nnz0), 256, 0, ib[0].p + (size_t)k * nnz0, nnz0, cur[k], c.status);
   }
   RT_REQUIRE(nnz0 == 0 || X->vals != nullptr, "null value array");
   if (nnz0) RT_CUDA(cudaMemcpyAsync(vb[0].p, X->vals, vs * nnz0, kind, c.stream));
+  if (dbg) check_status(c);
+  DevBuf<int64_t> hist(c, kMaxModes + 1);  // nnz after each mode (device)
+  DevBuf<int> swaps(c, kMaxModes);
+  swaps.zero();
+  RT_CUDA(cudaMemcpyAsync(hist.p, &nnz0, sizeof(int64_t), cudaMemcpyHostToDevice, c.stream));
+  DevBuf<FixScale> fs(c, 1);
+  fix_scale(c, vb[0].p, vt, nnz0, fs.p);  // max|v| bounds every later (filtered) mode too
   int cb = 0;
-  int64_t nnz = nnz0;
-  res->nnz_history[0] = nnz0;
   for (int jj = 0; jj < d; ++jj) {
     const int n = ord[jj];
     int64_t others = 1;
@@ -572,51 +748,88 @@ rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int6
       g.dims[k] = cur[k];
       g.idx[k] = ib[cb].p + (size_t)k * nnz0;
     }
-    g.nnz = nnz;
+    g.nnz = nnz0;  // upper bound; the live count is hist[jj]
     g.vals = vb[cb].p;
     g.vt = vt;
     const int64_t I = cur[n];
     DevBuf<double> Y(c, (size_t)I * ell), Q(c, (size_t)I * ell);
     {
       PhaseScope ps(c, PH_SKETCH, jj);
-      sketch_coo(c, g, n, ell, seed, nf64, Y.p);
+      sketch_coo(c, g, n, ell, seed, nf64, Y.p, hist.p + jj, fs.p);
       ps.next(PH_QR);
       thin_qr(c, Y.p, I, ell, Q.p);
     }
-    double *A = nullptr;
-    A = (double *)dev_alloc(c, sizeof(double) * I * ell);
+    double *A = (double *)dev_alloc(c, sizeof(double) * I * ell);
     res->factors[n] = A;
-    int64_t *S = nullptr;
-    S = (int64_t *)dev_alloc(c, sizeof(int64_t) * ell);
+    int64_t *S = (int64_t *)dev_alloc(c, sizeof(int64_t) * ell);
     res->selection[n] = S;
     {
       PhaseScope ps(c, PH_EIG, jj);
-      int sw = 0;
-      srrqr(c, Q.p, I, ell, eta, S, A, &sw);
-      res->swaps[n] = sw;
+      srrqr(c, Q.p, I, ell, eta, S, A, swaps.p + n);
     }
-    // G_(n) <- P^T G_(n): keep the selected slices and renumber them 0..ell-1
+    // G_(n) <- P^T G_(n): keep the selected slices and renumber them 0..ell-1 (local nonzeros)
     int32_t *oidx[kMaxModes] = {nullptr};
     for (int k = 0; k < d; ++k) oidx[k] = ib[1 - cb].p + (size_t)k * nnz0;
     {
       PhaseScope ps(c, PH_SHRINK, jj);
-      nnz = coo_select(c, g, n, S, ell, oidx, vb[1 - cb].p);
+      coo_select(c, g, hist.p + jj, n, S, ell, oidx, vb[1 - cb].p, hist.p + jj + 1);
     }
     cb = 1 - cb;
     cur[n] = ell;
     res->ranks[n] = ell;
     res->ell[n] = ell;
-    res->nnz_history[jj + 1] = nnz;
   }
+  // ---- one host synchronisation: nnz history (summed over the ranks), swaps, status
+  DevBuf<int64_t> hsum(c, kMaxModes + 1);
+  RT_CUDA(cudaMemcpyAsync(hsum.p, hist.p, sizeof(int64_t) * (d + 1), cudaMemcpyDeviceToDevice, c.stream));
+  allreduce_i64_sum(c, hsum.p, d + 1);
+  std::vector<int64_t> hh(2 * (d + 1));
+  int hsw[kMaxModes];
+  RT_CUDA(cudaMemcpyAsync(hh.data(), hsum.p, sizeof(int64_t) * (d + 1), cudaMemcpyDeviceToHost, c.stream));
+  RT_CUDA(cudaMemcpyAsync(hh.data() + d + 1, hist.p, sizeof(int64_t) * (d + 1), cudaMemcpyDeviceToHost, c.stream));
+  RT_CUDA(cudaMemcpyAsync(hsw, swaps.p, sizeof(int) * d, cudaMemcpyDeviceToHost, c.stream));
+  check_status(c);  // synchronises; ENUMERIC on a singular P^T Q
+  for (int k = 0; k <= d; ++k) res->nnz_history[k] = hh[k];
+  for (int k = 0; k < d; ++k) res->swaps[k] = hsw[k];
+  const int64_t nnz_local = hh[d + 1 + d], nnz = hh[d];
   res->core_nnz = nnz;
-  for (int k = 0; k < d; ++k) {
-    res->core_idx[k] = (int32_t *)dev_alloc(c, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
-    if (nnz)
-      RT_CUDA(cudaMemcpyAsync(res->core_idx[k], ib[cb].p + (size_t)k * nnz0, sizeof(int32_t) * nnz,
-                              cudaMemcpyDeviceToDevice, c.stream));
-  }
+  for (int k = 0; k < d; ++k) res->core_idx[k] = (int32_t *)dev_alloc(c, sizeof(int32_t) * std::max<int64_t>(nnz, 1));
   res->core_vals = dev_alloc(c, vs * std::max<int64_t>(nnz, 1));
-  if (nnz) RT_CUDA(cudaMemcpyAsync(res->core_vals, vb[cb].p, vs * nnz, cudaMemcpyDeviceToDevice, c.stream));
+  if (c.nranks == 1) {
+    for (int k = 0; k < d; ++k)
+      if (nnz)
+        RT_CUDA(cudaMemcpyAsync(res->core_idx[k], ib[cb].p + (size_t)k * nnz0, sizeof(int32_t) * nnz,
+                                cudaMemcpyDeviceToDevice, c.stream));
+    if (nnz) RT_CUDA(cudaMemcpyAsync(res->core_vals, vb[cb].p, vs * nnz, cudaMemcpyDeviceToDevice, c.stream));
+  } else {
+    // gather the core nonzeros of all ranks in rank order (padded blocks of cap entries)
+    DevBuf<int64_t> cnt(c, 1), cnts(c, c.nranks), capd(c, 1);
+    RT_CUDA(cudaMemcpyAsync(cnt.p, hist.p + d, sizeof(int64_t), cudaMemcpyDeviceToDevice, c.stream));
+    allgather_i64(c, cnt.p, cnts.p, 1);
+    std::vector<int64_t> hc(c.nranks);
+    RT_CUDA(cudaMemcpyAsync(hc.data(), cnts.p, sizeof(int64_t) * c.nranks, cudaMemcpyDeviceToHost, c.stream));
+    RT_CUDA(cudaStreamSynchronize(c.stream));
+    int64_t cap = 1;
+    for (int64_t v : hc) cap = std::max(cap, v);
+    DevBuf<int32_t> sidx(c, (size_t)d * cap), gidx(c, (size_t)c.nranks * d * cap);
+    DevBuf<unsigned char> sval(c, (size_t)cap * vs), gval(c, (size_t)c.nranks * cap * vs);
+    for (int k = 0; k < d; ++k)
+      if (nnz_local)
+        RT_CUDA(cudaMemcpyAsync(sidx.p + (size_t)k * cap, ib[cb].p + (size_t)k * nnz0, sizeof(int32_t) * nnz_local,
+                                cudaMemcpyDeviceToDevice, c.stream));
+    if (nnz_local) RT_CUDA(cudaMemcpyAsync(sval.p, vb[cb].p, vs * nnz_local, cudaMemcpyDeviceToDevice, c.stream));
+    allgather_bytes(c, sidx.p, gidx.p, sizeof(int32_t) * d * cap);
+    allgather_bytes(c, sval.p, gval.p, vs * cap);
+    DevBuf<int32_t *> optr(c, kMaxModes);
+    RT_CUDA(cudaMemcpyAsync(optr.p, res->core_idx, sizeof(int32_t *) * kMaxModes, cudaMemcpyHostToDevice, c.stream));
+    const int g = grid_for(c, (int64_t)c.nranks * cap);
+    if (vt == DT::F64)
+      RT_LAUNCH(c, gather_core<double>, g, 256, 0, gidx.p, (const double *)gval.p, d, c.nranks, cap, cnts.p, optr.p,
+                (double *)res->core_vals);
+    else
+      RT_LAUNCH(c, gather_core<float>, g, 256, 0, gidx.p, (const float *)gval.p, d, c.nranks, cap, cnts.p, optr.p,
+                (float *)res->core_vals);
+  }
   finish_result(c, res, flags);
   RT_CUDA(cudaStreamSynchronize(c.stream));
   return rg.release();

@@ -199,3 +199,26 @@ def test_c4_adaptive_full_size(ctx):
             assert min(abs(v) for v in m["trunc_margin"] if v is not None) <= 1e-3, (j, m)
     print("C4 adaptive: ranks", h.ranks, "oracle", gold["ranks"], "columns", h.ell, "rel_err", err,
           "oracle", gold["rel_err_identity"])
+
+
+@pytest.mark.parametrize("algo_flags", [0, "hosvd"])
+def test_adaptive_sharded_path_loopback(ctx, algo_flags):
+    """The multi-rank adaptive path (W and ||B_i||^2 allreduced for modes < d, the
+    last mode's rows placed and summed, B_i of the last mode reduced over the sharded index,
+    replicated core) run on one rank with the collectives degenerate must reproduce the oracle."""
+    import torch
+    from paper_1905_07311_b200.rtucker import RESULT_HOST, ADAPT_HOSVD
+    x = hilbert((30, 24, 20), "paper")
+    flags = ADAPT_HOSVD if algo_flags == "hosvd" else 0
+    xd = torch.as_tensor(to_first_mode_fastest(x), device="cuda")
+    ctx.loopback_sharding(True)
+    try:
+        g = ctx.adaptive(xd, x.shape, 1e-5, 2, order=None if flags else (0, 1, 2), seed=3,
+                         flags=flags | RESULT_HOST, shard=(0, x.shape[-1])).numpy()
+    finally:
+        ctx.loopback_sharding(False)
+    o = (O.adaptive_r_hosvd(x, 1e-5, 2, seed=3) if flags else
+         O.adaptive_r_sthosvd(x, 1e-5, 2, seed=3, order=(0, 1, 2)))
+    assert g.ranks == o.ranks
+    assert _delta(x, g, o) <= 1e-12
+    assert O.rel_error(x, g.core, g.factors) <= 1e-5

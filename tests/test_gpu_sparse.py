@@ -102,6 +102,25 @@ def test_srrqr_on_oracle_q(ctx):
         np.testing.assert_allclose(a, O.oblique_factor(q, osel), rtol=0, atol=1e-10)
 
 
+def test_sparse_bit_reproducible_and_debug_checks(ctx):
+    """The sparse sketch sums in fixed point (int64 words, sparse.cu): reruns are bit-identical
+    (RTUCKER_DETERMINISTIC) although the reduction order of the CTAs, warps and
+    atomics varies between runs; RTUCKER_DEBUG_CHECKS rejects an out-of-range index."""
+    from paper_1905_07311_b200.rtucker import DEBUG_CHECKS, RTuckerError
+    idx, vals = sparse_zipf(ndraws=300_000, seed=9)
+    dims = (8000, 8000, 200000, 1200)
+    a = _run(ctx, idx, vals, dims, (10, 10, 10, 10), 5, seed=3)
+    b = _run(ctx, idx, vals, dims, (10, 10, 10, 10), 5, seed=3, flags=DEBUG_CHECKS)
+    for fa, fb in zip(a.factors, b.factors):
+        np.testing.assert_array_equal(fa, fb)
+    np.testing.assert_array_equal(a.core_idx, b.core_idx)
+    bad = idx.copy()
+    bad[1, 7] = dims[1]
+    with pytest.raises(RTuckerError) as e:
+        _run(ctx, bad, vals, dims, (10, 10, 10, 10), 5, seed=3, flags=DEBUG_CHECKS)
+    assert e.value.name == "EINVAL"
+
+
 def test_sparse_invalid(ctx):
     from paper_1905_07311_b200.rtucker import RTuckerError
     idx = np.array([[0, 1, 2], [0, 1, 2], [0, 1, 2]])
