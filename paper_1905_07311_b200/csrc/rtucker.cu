@@ -29,11 +29,11 @@ void set_smem_attr(const void *func, size_t bytes) {
   for (auto &e : done)
     if (e.first == func) {
       if (e.second >= bytes) return;
-      smem_attr(func, bytes);
+      RT_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
       e.second = bytes;
       return;
     }
-  smem_attr(func, bytes);
+  RT_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   done.emplace_back(func, bytes);
 }
 

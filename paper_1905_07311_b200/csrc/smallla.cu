@@ -1119,6 +1119,222 @@ __global__ void __launch_bounds__(kCQT, 1) cholqr2_cluster_kernel(const double *
   }
 }
 
+// ------------------------------------- cluster CholeskyQR2, blocked Cholesky (dense) --------
+// Same data flow as cholqr2_cluster_kernel (row slabs in the CTAs of one cluster, partial Grams
+// on the fp64 tensor cores, fixed-order DSMEM sum so every CTA holds the bit-identical Gram),
+// but the factorisation is blocked in 8 x 8 tiles instead of 60 single-pivot elimination steps
+// with a CTA barrier each:
+//   for each diagonal block kb:  warp 0 factors the 8 x 8 block (8 shuffle-broadcast pivots)
+//                                and inverts its triangle (D_kb = R_kb,kb^{-1}, one column per lane);
+//                                the panel R_kb,jb = D_kb^T G_kb,jb and the trailing update
+//                                G_ib,jb -= R_kb,ib^T R_kb,jb run on the fp64 tensor cores, one
+//                                block per warp (3 CTA barriers per block row, 24 in all);
+//   slab <- slab R^{-1} by a blocked triangular solve on the tensor cores, one 8-row block per
+//   warp: X_kb = (Y_kb - sum_{jb < kb} X_jb R_jb,kb) D_kb.
+// A pivot <= 1e-13 of its original diagonal (or NaN) flags the sketch as too ill-conditioned
+// and the Householder kernel recomputes Q (device-side gate), as before.
+constexpr int kBQT = 512;
+__device__ __forceinline__ void mma_blk8(double &c0, double &c1, const double *A, int lda_r, int lda_c,
+                                         const double *B, int ldb_r, int ldb_c, int lane) {
+  // C(8x8) += A(8x8) B(8x8): A(i, k) = A[i * lda_r + k * lda_c], B(k, j) = B[k * ldb_r + j * ldb_c]
+#pragma unroll
+  for (int k0 = 0; k0 < 8; k0 += 4) {
+    const int kk = k0 + (lane & 3), r = lane >> 2;
+    dmma884(c0, c1, A[r * lda_r + kk * lda_c], B[kk * ldb_r + r * ldb_c]);
+  }
+}
+
+__global__ void __launch_bounds__(kBQT, 1) cholqr2_blk_kernel(const double *__restrict__ Y, int64_t m, int n,
+                                                              int rows, int ldY, int ldG, double *__restrict__ Q,
+                                                              int *__restrict__ bad) {
+  extern __shared__ __align__(16) double bq[];
+  cg::cluster_group cl = cg::this_cluster();
+  const int ncta = (int)cl.num_blocks();
+  const int me = (int)cl.block_rank();
+  const int64_t r0 = (int64_t)me * rows;
+  const int64_t left_ = m - r0;
+  const int nloc = left_ <= 0 ? 0 : (left_ < rows ? (int)left_ : rows);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kW = kBQT / 32;
+  const int n8 = (n + 7) & ~7, nbk = n8 >> 3;
+  double *Yl = bq;                 // ldY x n8 slab (column-major), zero padded
+  double *Gp = Yl + ldY * n8;      // n8 x ldG partial Gram (row-major)
+  double *G = Gp + n8 * ldG;       // n8 x ldG summed Gram, then R (upper) in place
+  double *D = G + n8 * ldG;        // nbk x 64: D_kb (8 x 8 row-major)
+  double *tmp = D + 8 * 64;        // kW x 64 scratch (one 8 x 8 tile per warp)
+  double *d0 = tmp + kW * 64;      // 64: original diagonal
+  __shared__ int sbad;
+  for (int e = tid; e < ldY * n8; e += kBQT) {
+    const int i = e % ldY, c = e / ldY;
+    Yl[e] = (i < nloc && c < n) ? Y[r0 + i + m * c] : 0.0;
+  }
+  if (tid == 0) sbad = 0;
+  const int kend = (nloc + 3) & ~3;
+  const int ntiles = nbk * (nbk + 1) / 2;
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) cluster_wait();  // every CTA has read the pass-0 partial Grams
+    // ---- 1. partial Gram, upper tiles (a <= b), mirrored
+    for (int tile = warp; tile < ntiles; tile += kW) {
+      int a = 0, rem = tile;
+      while (rem >= nbk - a) { rem -= nbk - a; ++a; }
+      const int b = a + rem;
+      const double *pa = Yl + (size_t)ldY * (8 * a + (lane >> 2)) + (lane & 3);
+      const double *pb = Yl + (size_t)ldY * (8 * b + (lane >> 2)) + (lane & 3);
+      double c0 = 0.0, c1 = 0.0, e0 = 0.0, e1 = 0.0;
+      int k0 = 0;
+      for (; k0 + 8 <= kend; k0 += 8) {
+        dmma884(c0, c1, pa[k0], pb[k0]);
+        dmma884(e0, e1, pa[k0 + 4], pb[k0 + 4]);
+      }
+      if (k0 < kend) dmma884(c0, c1, pa[k0], pb[k0]);
+      c0 += e0; c1 += e1;
+      const int gi = 8 * a + (lane >> 2), gj = 8 * b + 2 * (lane & 3);
+      Gp[gi * ldG + gj] = c0; Gp[gi * ldG + gj + 1] = c1;
+      if (a != b) { Gp[gj * ldG + gi] = c0; Gp[(gj + 1) * ldG + gi] = c1; }
+    }
+    cluster_arrive();
+    cluster_wait();
+    // ---- 2. cluster sum (fixed CTA order) into G
+    for (int e = tid; e < n8 * n8; e += kBQT) {
+      const int i = e / n8, j = e % n8;
+      double sum = 0.0;
+      for (int q = 0; q < ncta; ++q) sum += cl.map_shared_rank(Gp, q)[i * ldG + j];
+      G[i * ldG + j] = sum;
+      if (i == j) d0[i] = sum;
+    }
+    cluster_arrive();  // matched by the wait before the next Gram (or before exit)
+    __syncthreads();
+    // ---- 3. blocked Cholesky G = R^T R (upper R in place) with D_kb = R_kb,kb^{-1}
+    for (int kb = 0; kb < nbk; ++kb) {
+      if (warp == 0) {
+        // (a) 8 x 8 diagonal block: lane holds entries e = lane, lane + 32 (i = e >> 3, j = e & 7)
+        double bv[2];
+        int bi[2], bj[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int e = lane + 32 * h;
+          bi[h] = e >> 3;
+          bj[h] = e & 7;
+          bv[h] = G[(8 * kb + bi[h]) * ldG + 8 * kb + bj[h]];
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int gk = 8 * kb + k;
+          const int ek = 9 * k;  // entry (k, k)
+          double piv = __shfl_sync(0xffffffffu, bv[ek >> 5], ek & 31);
+          if (gk >= n) piv = 1.0;  // padding pivot: identity
+          else if (!(piv > 1e-13 * d0[gk])) {
+            if (lane == 0) sbad = 1;
+            piv = 1.0;
+          }
+          const double rinv = rsqrt(piv);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (bi[h] == k && bj[h] > k) bv[h] *= rinv;
+            if (bi[h] == k && bj[h] == k) bv[h] = piv * rinv;
+          }
+          // rank-1 update of the trailing entries (i, j), k < i <= j: R_ki R_kj from row k
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int ea = 8 * k + bi[h], eb = 8 * k + bj[h];
+            const double rki = __shfl_sync(0xffffffffu, bv[ea >> 5], ea & 31);
+            const double rkj = __shfl_sync(0xffffffffu, bv[eb >> 5], eb & 31);
+            if (bi[h] > k && bj[h] >= bi[h]) bv[h] = fma(-rki, rkj, bv[h]);
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double &g = G[(8 * kb + bi[h]) * ldG + 8 * kb + bj[h]];
+          g = bj[h] >= bi[h] ? bv[h] : 0.0;
+        }
+        __syncwarp();
+        // (b) D = R_kb,kb^{-1} (upper): lane j < 8 solves column j by back substitution
+        double *Dk = D + 64 * kb;
+        if (lane < 8) {
+          const int j = lane;
+          const double *Rb = G + (8 * kb) * ldG + 8 * kb;
+          double x[8];
+#pragma unroll
+          for (int i = 7; i >= 0; --i) {
+            double s2 = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+            for (int t = i + 1; t < 8; ++t) s2 = fma(-Rb[i * ldG + t], x[t], s2);
+            x[i] = (i <= j) ? s2 / Rb[i * ldG + i] : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) Dk[i * 8 + j] = x[i];
+        }
+      }
+      __syncthreads();
+      // (c) panel: R_kb,jb = D^T G_kb,jb for jb > kb (one block per warp)
+      const double *Dk = D + 64 * kb;
+      for (int jb = kb + 1 + warp; jb < nbk; jb += kW) {
+        double c0 = 0.0, c1 = 0.0;
+        // A(i, k) = D^T(i, k) = D[k][i];  B(k, j) = G[8kb + k][8jb + j]
+        mma_blk8(c0, c1, Dk, 1, 8, G + (8 * kb) * ldG + 8 * jb, ldG, 1, lane);
+        __syncwarp();
+        const int r = lane >> 2, cc = 2 * (lane & 3);
+        G[(8 * kb + r) * ldG + 8 * jb + cc] = c0;
+        G[(8 * kb + r) * ldG + 8 * jb + cc + 1] = c1;
+      }
+      __syncthreads();
+      // (d) trailing update G_ib,jb -= R_kb,ib^T R_kb,jb for kb < ib <= jb
+      const int rem = nbk - kb - 1;
+      for (int t = warp; t < rem * (rem + 1) / 2; t += kW) {
+        int ib = 0, r2 = t;
+        while (r2 >= rem - ib) { r2 -= rem - ib; ++ib; }
+        const int jb = ib + r2;
+        ib += kb + 1;
+        const int jj = jb + kb + 1;
+        const int r = lane >> 2, cc = 2 * (lane & 3);
+        double c0 = G[(8 * ib + r) * ldG + 8 * jj + cc], c1 = G[(8 * ib + r) * ldG + 8 * jj + cc + 1];
+        // A(i, k) = -R_kb,ib^T(i, k) = -G[8kb + k][8ib + i] (negated via the B operand sign below)
+        double n0 = 0.0, n1 = 0.0;
+        mma_blk8(n0, n1, G + (8 * kb) * ldG + 8 * ib, 1, ldG, G + (8 * kb) * ldG + 8 * jj, ldG, 1, lane);
+        G[(8 * ib + r) * ldG + 8 * jj + cc] = c0 - n0;
+        G[(8 * ib + r) * ldG + 8 * jj + cc + 1] = c1 - n1;
+      }
+      __syncthreads();
+    }
+    // ---- 4. slab <- slab R^{-1}: X_kb = (Y_kb - sum_{jb<kb} X_jb R_jb,kb) D_kb per 8-row block
+    double *tw = tmp + 64 * warp;
+    for (int rb = warp; 8 * rb < nloc; rb += kW) {
+      double *yr = Yl + 8 * rb;  // rows 8rb.., column c at yr[ldY * c]
+      for (int kb = 0; kb < nbk; ++kb) {
+        const int r = lane >> 2, cc = 2 * (lane & 3);
+        double c0 = yr[r + (size_t)ldY * (8 * kb + cc)], c1 = yr[r + (size_t)ldY * (8 * kb + cc + 1)];
+        for (int jb = 0; jb < kb; ++jb) {
+          double n0 = 0.0, n1 = 0.0;
+          // A(i, k) = X[8rb + i][8jb + k];  B(k, j) = R[8jb + k][8kb + j]
+          mma_blk8(n0, n1, yr + (size_t)ldY * 8 * jb, 1, ldY, G + (8 * jb) * ldG + 8 * kb, ldG, 1, lane);
+          c0 -= n0;
+          c1 -= n1;
+        }
+        tw[r * 8 + cc] = c0;
+        tw[r * 8 + cc + 1] = c1;
+        __syncwarp();
+        double x0 = 0.0, x1 = 0.0;
+        mma_blk8(x0, x1, tw, 8, 1, D + 64 * kb, 8, 1, lane);  // (Y - ...) D_kb
+        __syncwarp();
+        yr[r + (size_t)ldY * (8 * kb + cc)] = x0;
+        yr[r + (size_t)ldY * (8 * kb + cc + 1)] = x1;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+  }
+  cluster_wait();  // no CTA leaves while others may still read its partial Gram
+  if (sbad) {
+    if (me == 0 && tid == 0) *bad = 1;
+    return;
+  }
+  for (int e = tid; e < nloc * n; e += kBQT) {
+    const int i = e % nloc, c = e / nloc;
+    Q[r0 + i + m * c] = Yl[i + (size_t)ldY * c];
+  }
+}
+
 // One CTA per column k: argmax |A[:, k]| (first index on ties); flip A[:, k] and U[:, k]
 // when that entry is negative (DESIGN reading R4b).
 __global__ void canonical_signs_kernel(double *__restrict__ A, int64_t m, double *__restrict__ U, int64_t ldu,
@@ -1254,11 +1470,13 @@ void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
     const int n8 = (n + 7) & ~7;
     const int ldY = ((rows + 7) / 8 * 8 + 11) / 16 * 16 + 4;  // >= rows rounded to 8, = 4 mod 16
     const int ldG = (n8 + 15) / 16 * 16 + 8, ldE = (n8 + 15) / 16 * 16 + 4;
-    const size_t smem = sizeof(double) * ((size_t)ldY * n8 + (size_t)n8 * ldG + (size_t)n8 * ldE + 4 * kCQN + kCQN);
+    const bool blk = !RT_EXP_GETENV("RTUCKER_QR_ELIM");  // blocked Cholesky (default) or the elimination kernel
+    const size_t smem = blk ? sizeof(double) * ((size_t)ldY * n8 + 2 * (size_t)n8 * ldG + 8 * 64 + (kBQT / 32) * 64 + 64)
+                            : sizeof(double) * ((size_t)ldY * n8 + (size_t)n8 * ldG + (size_t)n8 * ldE + 4 * kCQN + kCQN);
     RT_REQUIRE(smem <= kCQSmem, "qr: CholeskyQR2 slab does not fit shared memory");
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ncta);
-    cfg.blockDim = dim3(kCQT);
+    cfg.blockDim = dim3(blk ? kBQT : kCQT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute at[1];
@@ -1268,8 +1486,13 @@ void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    smem_attr(cholqr2_cluster_kernel, smem);
-    RT_CUDA(cudaLaunchKernelEx(&cfg, cholqr2_cluster_kernel, Y, m, n, rows, ldY, ldG, ldE, Q, bad.p));
+    if (blk) {
+      smem_attr(cholqr2_blk_kernel, smem);
+      RT_CUDA(cudaLaunchKernelEx(&cfg, cholqr2_blk_kernel, Y, m, n, rows, ldY, ldG, Q, bad.p));
+    } else {
+      smem_attr(cholqr2_cluster_kernel, smem);
+      RT_CUDA(cudaLaunchKernelEx(&cfg, cholqr2_cluster_kernel, Y, m, n, rows, ldY, ldG, ldE, Q, bad.p));
+    }
     c.launches++;
   } else {
     // tall sketches (sparse modes, I_n ~ 1e5): CholeskyQR2 over the whole grid

@@ -87,6 +87,12 @@ __device__ __forceinline__ int sturm_count(const double *d, const double *e2, in
   return cnt;
 }
 
+#ifdef RT_TRID_PROGRESS
+__device__ volatile int *g_trid_progress;
+#define TPROG(v) do { if (threadIdx.x == 0) { g_trid_progress[0] = (v); __threadfence_system(); } } while (0)
+#else
+#define TPROG(v)
+#endif
 __global__ void __launch_bounds__(kTeT, 1) trid_eig_kernel(const double *__restrict__ Ain, int n,
                                                          double *__restrict__ w, double *__restrict__ Vout,
                                                          int *__restrict__ info) {
@@ -129,7 +135,9 @@ __global__ void __launch_bounds__(kTeT, 1) trid_eig_kernel(const double *__restr
   __syncthreads();
 
   // ---- A. tridiagonalisation
+  TPROG(1);
   for (int k = 0; k + 2 < n; ++k) {
+    TPROG(100 + k);
     const int c0 = k + 1;                        // x = A[c0.., k]
     // fused matvecs over the columns j >= c0: y_i = sum_j A[i][j] x_j (rows i >= c0),
     // u_i = sum_j Q[i][j] x_j (all rows)
@@ -213,6 +221,7 @@ __global__ void __launch_bounds__(kTeT, 1) trid_eig_kernel(const double *__restr
   __syncthreads();
   for (int i = tid; i < kNP; i += kTeT) e2[i] = (i + 1 < n) ? e[i] * e[i] : 0.0;
   // ---- B. eigenvalues: Gershgorin interval, multisection (16 threads per eigenvalue)
+  TPROG(2);
   double glo = 1e300, ghi = -1e300;
   for (int i = 0; i < n; ++i) {
     const double r = (i > 0 ? fabs(e[i - 1]) : 0.0) + (i + 1 < n ? fabs(e[i]) : 0.0);
@@ -245,6 +254,7 @@ __global__ void __launch_bounds__(kTeT, 1) trid_eig_kernel(const double *__restr
   // reciprocals 1/D_i, 1/R_i of the recurrences are kept for the eigenvector recurrences.
   // Storage (A and Z2 are free now): column q of A holds D (rows 0..63) ... as [q][i] planes.
   double *Dq = A, *Rq = Z2;  // Dq[q * kLd + i] = 1/D_i, Rq[q * kLd + i] = 1/R_i
+  TPROG(3);
   if (tid < 2 * n) {
     const int q = tid >> 1;
     const double l = lam[q];
@@ -337,6 +347,7 @@ __global__ void __launch_bounds__(kTeT, 1) trid_eig_kernel(const double *__restr
     }
   }
   __syncthreads();
+  TPROG(4);
   // Newton-Schulz: Z <- Z (3 I - Z^T Z) / 2 (S = Z^T Z in A's storage)
   double *S = A;
   gemm64(Z, Z, S, true);
@@ -357,6 +368,7 @@ __global__ void __launch_bounds__(kTeT, 1) trid_eig_kernel(const double *__restr
   }
   for (int i = tid; i < n; i += kTeT) w[i] = lam[n - 1 - i] * scale;
   if (tid == 0 && info) *info = 1;
+  TPROG(5);
 }
 
 
