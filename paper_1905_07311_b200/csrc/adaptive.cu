@@ -108,6 +108,7 @@ struct Shard {
   int64_t col_offset = 0; // global unfolding-column offset of the local slab (modes n < d)
   int64_t row_offset = 0; // shard offset along the last mode (rows of Q for mode d)
   int64_t I_glob = 0;     // global I_n
+  bool rel_acc = false;   // fp64 data: relative-accuracy eigensolver (gram_eig)
 };
 
 // AdaptRangeFinder on the mode-n unfolding of G (local dims cur, global dims gcur), threshold
@@ -212,9 +213,10 @@ ModeOut adapt_mode(Ctx &c, const void *G, DT gt, const int64_t *cur, const int64
   // ---- truncation: eigenpairs of B B^T (thin SVD of B), r from the cumulative spectrum
   PhaseScope ps(c, PH_EIG, n);
   DevBuf<double> gram(c, (size_t)k * k), w(c, k), U(c, (size_t)k * k);
-  mode_gram(c, B.p, store, vb, gram.p);
+  if (store == DT::F64 && k > 64) gram_f64(c, (const double *)B.p, v.L, k, v.R, gram.p);  // tensor cores
+  else mode_gram(c, B.p, store, vb, gram.p);
   if (sh.on && !sh.rows) allreduce_sum_f64(c, gram.p, (size_t)k * k);
-  gram_eig(c, gram.p, k, w.p, U.p, nullptr, k);  // r not known yet: the whole spectrum
+  gram_eig(c, gram.p, k, w.p, U.p, nullptr, k, sh.rel_acc);  // r not known yet: the whole spectrum
   std::vector<double> hw(k);
   RT_CUDA(cudaMemcpyAsync(hw.data(), w.p, sizeof(double) * k, cudaMemcpyDeviceToHost, c.stream));
   RT_CUDA(cudaStreamSynchronize(c.stream));
@@ -234,7 +236,15 @@ ModeOut adapt_mode(Ctx &c, const void *G, DT gt, const int64_t *cur, const int64
   if (want_core) {
     ps.next(PH_SHRINK);
     out.G.alloc(c, (size_t)v.L * r * v.R * dt_size(store));
-    ttm_dense(c, B.p, store, vb, U.p, k, r, out.G.p, store, mul_f64 || store == DT::F64, nullptr);
+    if (store == DT::F64 && r > 64) {  // G <- U_r^T B as GEMMs on the fp64 tensor cores
+      if (v.L == 1)
+        gemm_f64(c, true, U.p, k, (const double *)B.p, k, (double *)out.G.p, r, r, v.R, k);
+      else  // per r-slab: G_r (L x r) = B_r (L x k) U_r (k x r)
+        gemm_f64_batched(c, false, false, (const double *)B.p, v.L, v.L * k, U.p, k, 0, (double *)out.G.p, v.L,
+                         v.L * r, v.L, r, k, v.R);
+    } else {
+      ttm_dense(c, B.p, store, vb, U.p, k, r, out.G.p, store, mul_f64 || store == DT::F64, nullptr);
+    }
     out.gt = store;
     out.replaced = true;
   }
@@ -323,6 +333,7 @@ rtucker_result *run_adaptive(Ctx &c, const rtucker_dense_desc *X, double tol, in
     sh.rows = in.sharded && n == d - 1;
     sh.row_offset = in.offset;
     sh.col_offset = (in.sharded && n != d - 1) ? col_offset_for(in, dims, n) : 0;
+    sh.rel_acc = in.dt == DT::F64;
     ModeOut mo = adapt_mode(c, src, st, dims, gdims, d, n, tau2, block, seed, floor_abs, mulf, store, truncate,
                             !hosvd, scal.p + 1, in.dt == DT::F32 && !f64, sh);
     res->factors[n] = mo.A;

@@ -165,7 +165,7 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
     ps_b.next(PH_EIG);
     // ---- Alg 1 line 4: thin SVD of B through the eigenpairs of its Gram
     DevBuf<double> w(c, ell), V(c, (size_t)ell * ell);
-    gram_eig(c, gram.p, ell, w.p, V.p, nullptr, rr);
+    gram_eig(c, gram.p, ell, w.p, V.p, nullptr, rr, in.dt == DT::F64);
     // ---- Alg 1 line 5: A_n = Q U_B(:, 1:r)
     double *A = nullptr;
     A = (double *)dev_alloc(c, sizeof(double) * Ig * rr);
@@ -260,7 +260,7 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
     }
     ps.next(PH_EIG);
     DevBuf<double> w(c, ell), V(c, (size_t)ell * ell);
-    gram_eig(c, gram.p, ell, w.p, V.p, nullptr, rr);
+    gram_eig(c, gram.p, ell, w.p, V.p, nullptr, rr, in.dt == DT::F64);
     double *A = nullptr;
     A = (double *)dev_alloc(c, sizeof(double) * Ig * rr);
     res->factors[n] = A;

@@ -73,7 +73,9 @@ void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps =
 // PSD Gram: pivoted Cholesky + one-sided Jacobi on the factor; eigenvectors accurate to
 // ~eps sqrt(w_0 / w_k).  When the r_need-th eigenvalue is below 1e-8 w_0 the unpreconditioned
 // sym_eig recomputes the result (device-side gate, no host sync).  n > 64 uses sym_eig.
-void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps = nullptr, int r_need = 1 << 30);
+// rel_acc: fp64 data (preconditioned Jacobi, relative accuracy); else the tridiagonal solver.
+void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps = nullptr, int r_need = 1 << 30,
+              bool rel_acc = false);
 // Symmetric eigensolver for n <= 64 (trideig.cu): Householder tridiagonalisation, multisection,
 // twisted-factorisation eigenvectors, one CTA; eigenvalues descending.  Returns false if n > 64.
 bool trid_eig(Ctx &c, const double *A, int n, double *w, double *V, int *info = nullptr);
@@ -87,6 +89,12 @@ void gemm_small(Ctx &c, bool transA, const double *A, int64_t lda, const double 
 // C (m x n) = beta C + alpha op(A) B on the fp64 tensor cores (tiled, deterministic), column-major.
 void gemm_f64(Ctx &c, bool transA, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
               int64_t ldc, int64_t m, int64_t n, int64_t k, double beta = 0.0, double alpha = 1.0);
+// Batched variant (blockIdx.z = batch, element strides sA, sB, sC), op(B) = B^T with transB.
+void gemm_f64_batched(Ctx &c, bool transA, bool transB, const double *A, int64_t lda, int64_t sA, const double *B,
+                      int64_t ldb, int64_t sB, double *C, int64_t ldc, int64_t sC, int64_t m, int64_t n, int64_t k,
+                      int64_t batch, double beta = 0.0, double alpha = 1.0);
+// Gram C (K x K) = B_(n) B_(n)^T of an fp64 tensor stored (L, K, R), tensor cores, deterministic.
+void gram_f64(Ctx &c, const double *B, int64_t L, int64_t K, int64_t R, double *C);
 void convert(Ctx &c, const void *src, DT s, void *dst, DT d, int64_t n);
 void sumsq(Ctx &c, const void *X, DT t, int64_t n, double *out);             // deterministic
 void diff_sumsq(Ctx &c, const void *X, DT t, const double *Y, int64_t n, double *out);

@@ -30,16 +30,20 @@ __global__ void gemm_small_kernel(bool transA, const double *__restrict__ A, int
   }
 }
 
-// C (m x n) = beta C + op(A) (m x k) B (k x n), column-major fp64 on the fp64 tensor cores
-// (mma.sync m8n8k4): CTA tile 64 x 64, K steps of 16 staged in shared memory, 8 warps of
-// 32 x 16; fixed summation order (deterministic).
+// C (m x n) = beta C + alpha op(A) (m x k) op(B) (k x n), column-major fp64 on the fp64 tensor
+// cores (mma.sync m8n8k4): CTA tile 64 x 64, K steps of 16 staged in shared memory, 8 warps of
+// 32 x 16; fixed summation order (deterministic); blockIdx.z = batch (strides sA, sB, sC).
 constexpr int kGm = 64, kGk = 16;
-__global__ void __launch_bounds__(256) gemm_f64_kernel(bool transA, const double *__restrict__ A, int64_t lda,
-                                                       const double *__restrict__ B, int64_t ldb,
-                                                       double *__restrict__ C, int64_t ldc, int64_t m, int64_t n,
-                                                       int64_t k, double beta, double alpha) {
+__global__ void __launch_bounds__(256) gemm_f64_kernel(bool transA, bool transB, const double *__restrict__ A,
+                                                       int64_t lda, int64_t sA, const double *__restrict__ B,
+                                                       int64_t ldb, int64_t sB, double *__restrict__ C, int64_t ldc,
+                                                       int64_t sC, int64_t m, int64_t n, int64_t k, double beta,
+                                                       double alpha) {
   __shared__ double As[kGk][kGm + 1], Bs[kGk][kGm + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  A += sA * blockIdx.z;
+  B += sB * blockIdx.z;
+  C += sC * blockIdx.z;
   const int64_t i0 = (int64_t)blockIdx.x * kGm, j0 = (int64_t)blockIdx.y * kGm;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
   double acc[4][2][2];
@@ -59,9 +63,15 @@ __global__ void __launch_bounds__(256) gemm_f64_kernel(bool transA, const double
         const int64_t gi = i0 + ii, gk = k0 + kk;
         As[kk][ii] = (gi < m && gk < k) ? A[gk + lda * gi] : 0.0;
       }
-      const int kk = tid & 15, jj = (tid >> 4) + 16 * s;
-      const int64_t gj = j0 + jj, gk = k0 + kk;
-      Bs[kk][jj] = (gj < n && gk < k) ? B[gk + ldb * gj] : 0.0;
+      if (!transB) {
+        const int kk = tid & 15, jj = (tid >> 4) + 16 * s;
+        const int64_t gj = j0 + jj, gk = k0 + kk;
+        Bs[kk][jj] = (gj < n && gk < k) ? B[gk + ldb * gj] : 0.0;
+      } else {
+        const int jj = tid & 63, kk = (tid >> 6) + 4 * s;
+        const int64_t gj = j0 + jj, gk = k0 + kk;
+        Bs[kk][jj] = (gj < n && gk < k) ? B[gj + ldb * gk] : 0.0;
+      }
     }
     __syncthreads();
 #pragma unroll
@@ -95,6 +105,85 @@ __global__ void __launch_bounds__(256) gemm_f64_kernel(bool transA, const double
           *cp = beta == 0.0 ? v : fma(beta, *cp, v);
         }
       }
+}
+
+// Gram C = X X^T (K x K) of the mode unfolding of a (L, K, R) fp64 tensor B: X(i, t) =
+// B[(t % L) + L (i + K (t / L))], t < L R, on the fp64 tensor cores.  Upper 64 x 64 tiles,
+// K dimension split over gridDim.z chunks (partials summed in a fixed order by
+// gram_split_reduce_kernel: deterministic).
+__global__ void __launch_bounds__(256) gram_gather_kernel(const double *__restrict__ B, int64_t L, int64_t K, int64_t R,
+                                                          int64_t chunk, double *__restrict__ part) {
+  const int ti = blockIdx.x, tj = blockIdx.y;
+  if (ti > tj) return;
+  __shared__ double As[kGk][kGm + 1], Bs[kGk][kGm + 1];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t T = L * R;
+  const int64_t t0 = (int64_t)blockIdx.z * chunk, t1 = min(T, t0 + chunk);
+  const int64_t i0 = (int64_t)ti * kGm, j0 = (int64_t)tj * kGm;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  double acc[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  for (int64_t k0 = t0; k0 < t1; k0 += kGk) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      int ii, kk;
+      if (L == 1) { ii = tid & 63; kk = (tid >> 6) + 4 * s; }   // B[i + K t]: i contiguous
+      else { kk = tid & 15; ii = (tid >> 4) + 16 * s; }         // t contiguous within a row l
+      const int64_t gt = k0 + kk;
+      double va = 0.0, vb = 0.0;
+      if (gt < t1) {
+        const int64_t l = gt % L, r = gt / L;
+        const int64_t base = l + L * K * r;
+        if (i0 + ii < K) va = B[base + L * (i0 + ii)];
+        if (j0 + ii < K) vb = B[base + L * (j0 + ii)];
+      }
+      As[kk][ii] = va;
+      Bs[kk][ii] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < kGk; ks += 4) {
+      const int kk = ks + (lane & 3);
+      double bv[2];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) bv[b] = Bs[kk][wn + 8 * b + (lane >> 2)];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const double av = As[kk][wm + 8 * a + (lane >> 2)];
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
+                       : "d"(av), "d"(bv[b]));
+      }
+    }
+    __syncthreads();
+  }
+  double *P = part + (int64_t)blockIdx.z * K * K;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gi = i0 + wm + 8 * a + (lane >> 2), gj = j0 + wn + 8 * b + 2 * (lane & 3) + h;
+        if (gi < K && gj < K) P[gi + K * gj] = acc[a][b][h];
+      }
+}
+
+__global__ void gram_split_reduce_kernel(const double *__restrict__ part, int nsplit, int64_t K,
+                                         double *__restrict__ C) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K * K; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % K, j = e / K;
+    if ((i / kGm) > (j / kGm)) continue;  // lower tiles were not computed: mirrored below
+    double s = 0.0;
+    for (int q = 0; q < nsplit; ++q) s += part[(int64_t)q * K * K + e];
+    C[i + K * j] = s;
+    C[j + K * i] = s;
+  }
 }
 
 template <typename S, typename D>
@@ -153,9 +242,31 @@ void gemm_small(Ctx &c, bool transA, const double *A, int64_t lda, const double 
 
 void gemm_f64(Ctx &c, bool transA, const double *A, int64_t lda, const double *B, int64_t ldb, double *C,
               int64_t ldc, int64_t m, int64_t n, int64_t k, double beta, double alpha) {
-  if (m <= 0 || n <= 0) return;
-  const dim3 grid((unsigned)((m + kGm - 1) / kGm), (unsigned)((n + kGm - 1) / kGm));
-  RT_LAUNCH(c, gemm_f64_kernel, grid, 256, 0, transA, A, lda, B, ldb, C, ldc, m, n, k, beta, alpha);
+  gemm_f64_batched(c, transA, false, A, lda, 0, B, ldb, 0, C, ldc, 0, m, n, k, 1, beta, alpha);
+}
+
+void gemm_f64_batched(Ctx &c, bool transA, bool transB, const double *A, int64_t lda, int64_t sA, const double *B,
+                      int64_t ldb, int64_t sB, double *C, int64_t ldc, int64_t sC, int64_t m, int64_t n, int64_t k,
+                      int64_t batch, double beta, double alpha) {
+  if (m <= 0 || n <= 0 || batch <= 0) return;
+  RT_REQUIRE(batch <= 65535, "gemm: more than 65535 batches");
+  const dim3 grid((unsigned)((m + kGm - 1) / kGm), (unsigned)((n + kGm - 1) / kGm), (unsigned)batch);
+  RT_LAUNCH(c, gemm_f64_kernel, grid, 256, 0, transA, transB, A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, k, beta,
+            alpha);
+}
+
+void gram_f64(Ctx &c, const double *B, int64_t L, int64_t K, int64_t R, double *C) {
+  const int64_t T = L * R;
+  const int tiles = (int)((K + kGm - 1) / kGm);
+  const int ntile = tiles * (tiles + 1) / 2;
+  // enough K-chunks to cover ~2 waves of CTAs, each chunk a multiple of the K step
+  int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>((2 * c.num_sms + ntile - 1) / ntile, (T + 4095) / 4096));
+  const int64_t chunk = ((T + nsplit - 1) / nsplit + kGk - 1) / kGk * kGk;
+  nsplit = (int)((T + chunk - 1) / chunk);
+  DevBuf<double> part(c, (size_t)nsplit * K * K);
+  RT_LAUNCH(c, gram_gather_kernel, dim3(tiles, tiles, nsplit), 256, 0, B, L, K, R, chunk, part.p);
+  RT_LAUNCH(c, gram_split_reduce_kernel, std::max(1, std::min(4096, ceil_div(K * K, 256))), 256, 0, part.p, nsplit,
+            K, C);
 }
 
 void convert(Ctx &c, const void *src, DT s, void *dst, DT d, int64_t n) {

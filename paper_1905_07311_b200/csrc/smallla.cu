@@ -1420,11 +1420,17 @@ void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q, const 
   RT_LAUNCH(c, qr_global_kernel, 1, kQRG, smem, W.p, m, n, Q, gate);
 }
 
-void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps, int r_need) {
+void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps, int r_need, bool rel_acc) {
   const int np = n + (n & 1);
-  // hot path: Householder tridiagonalisation + multisection + twisted eigenvectors (trideig.cu,
-  // one CTA for n <= 64, the whole GPU above); the Jacobi solvers below are experiments only
-  if (!RT_EXP_GETENV("RTUCKER_EIG_JACOBI") && trid_eig(c, A, n, w, V, sweeps)) return;
+  // fp32 data (rel_acc = false): Householder tridiagonalisation + multisection + twisted
+  // eigenvectors (trideig.cu; one CTA for n <= 64, the whole GPU above), eigenvectors to
+  // ~eps lambda_1 / gap, ample for the fp32 criteria.  fp64 data: the preconditioned Jacobi below
+  // (pivoted Cholesky + one-sided Jacobi on the factor: ~eps sigma_1 / (sigma gap)), which the
+  // 1e-10 fp64 projector criterion of graded spectra needs (SURVEY c.4)
+  // n <= 64 stays on the register Jacobi: the one-CTA tridiagonal kernel measured slower at
+  // n = 60 (362 vs 300 us: fp64-issue-bound Sturm rounds and 58 barrier-bound Householder steps,
+  // DESIGN §12); it remains available in experiments builds (RTUCKER_EIG_TRID_CTA)
+  if (!rel_acc && (np > 64 || RT_EXP_GETENV("RTUCKER_EIG_TRID_CTA")) && trid_eig(c, A, n, w, V, sweeps)) return;
   if (np > 64) return sym_eig(c, A, n, w, V, sweeps);
   // 4 lanes per column slot (blocks of 8 columns, nb / 2 busy warps).  RTUCKER_EIG_LPS8 (n > 32):
   // 8 lanes (blocks of 4, all 8 warps busy, 8 rows per lane) measured no faster at n = 60
@@ -1513,7 +1519,6 @@ void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
 }
 
 void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps, const int *gate) {
-  if (!gate && !RT_EXP_GETENV("RTUCKER_EIG_JACOBI") && trid_eig(c, A, n, w, V, sweeps)) return;
   const int np = n + (n & 1);
   const size_t tab = sizeof(short2) * (size_t)(np - 1) * (np / 2) + 16;
   const size_t need = sizeof(double) * (2 * (size_t)np * np + np) + tab;

@@ -10,7 +10,7 @@
 //     per round, 14 rounds from the Gershgorin interval: ~eps ||T|| absolute)
 //  C. eigenvectors of T by twisted factorisations T - lambda I = N_k D_k N_k^T (one warp per
 //     eigenvalue pair; z_k = 1 at the twist index minimising |gamma_k|), Gram-Schmidt inside
-//     clusters of eigenvalues closer than 1e-9 ||T||, then one Newton-Schulz step
+//     clusters of eigenvalues closer than 1e-12 ||T||, then Newton-Schulz steps
 //     Z <- Z (3 I - Z^T Z) / 2 on the fp64 tensor cores (orthogonality to O(eps^2))
 //  D. V = Q Z on the fp64 tensor cores; eigenvalues descending.
 //
@@ -89,7 +89,9 @@ __device__ __forceinline__ int sturm_count(const double *d, const double *e2, in
 
 #ifdef RT_TRID_PROGRESS
 __device__ volatile int *g_trid_progress;
-#define TPROG(v) do { if (threadIdx.x == 0) { g_trid_progress[0] = (v); __threadfence_system(); } } while (0)
+__device__ long long g_trid_clk[8];
+#define TPROG(v) do { if (threadIdx.x == 0) { g_trid_progress[0] = (v); if ((v) < 8) g_trid_clk[(v)] = clock64(); \
+                       __threadfence_system(); } } while (0)
 #else
 #define TPROG(v)
 #endif
@@ -111,6 +113,7 @@ __global__ void __launch_bounds__(kTeT, 1) trid_eig_kernel(const double *__restr
   __shared__ double sscale;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ri = tid >> 4, pt = tid & 15;  // phase A: row ri, column part pt
+  TPROG(0);
 
   // ---- load (symmetrised, padded with zeros), scale to max |a_ij| = 1
   double amax = 0.0;
@@ -322,26 +325,41 @@ __global__ void __launch_bounds__(kTeT, 1) trid_eig_kernel(const double *__restr
     }
   }
   __syncthreads();
-  // Gram-Schmidt (twice) inside clusters of eigenvalues closer than 1e-9 ||T|| (warp 0)
+  // Gram-Schmidt (twice) inside clusters of eigenvalues closer than 1e-12 ||T|| (warp 0); a
+  // vector that collapses onto the earlier members (a numerically degenerate cluster, e.g. the
+  // zero eigenvalues of a rank-deficient Gram) is replaced by a unit vector orthogonalised
+  // against every other column except the cluster's later members (orthonormal completion)
   if (warp == 0) {
-    const double ctol = 1e-9 * tnorm;
+    const double ctol = 1e-12 * tnorm;
     for (int q = 1; q < n; ++q) {
       if (lam[q] - lam[q - 1] > ctol) continue;
       int s0 = q - 1;
       while (s0 > 0 && lam[s0] - lam[s0 - 1] <= ctol) --s0;
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int p = s0; p < q; ++p) {
-          double dt = 0.0;
-          for (int i = lane; i < n; i += 32) dt = fma(Z[i * kLd + p], Z[i * kLd + q], dt);
-          for (int o = 16; o; o >>= 1) dt += __shfl_xor_sync(0xffffffffu, dt, o);
-          for (int i = lane; i < n; i += 32) Z[i * kLd + q] -= dt * Z[i * kLd + p];
-          __syncwarp();
+      int s1 = q;
+      while (s1 + 1 < n && lam[s1 + 1] - lam[s1] <= ctol) ++s1;
+      for (int attempt = 0; attempt <= n; ++attempt) {
+        const int pe = attempt == 0 ? q : n;   // columns to orthogonalise against: [s0, q) or all others
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int p = attempt == 0 ? s0 : 0; p < pe; ++p) {
+            if (attempt > 0 && (p == q || (p > q && p <= s1))) continue;
+            double dt = 0.0;
+            for (int i = lane; i < n; i += 32) dt = fma(Z[i * kLd + p], Z[i * kLd + q], dt);
+            for (int o = 16; o; o >>= 1) dt += __shfl_xor_sync(0xffffffffu, dt, o);
+            for (int i = lane; i < n; i += 32) Z[i * kLd + q] -= dt * Z[i * kLd + p];
+            __syncwarp();
+          }
         }
         double s2 = 0.0;
         for (int i = lane; i < n; i += 32) s2 = fma(Z[i * kLd + q], Z[i * kLd + q], s2);
         for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-        const double inv = s2 > 0.0 ? 1.0 / sqrt(s2) : 0.0;
-        for (int i = lane; i < n; i += 32) Z[i * kLd + q] *= inv;
+        if (s2 > 1e-2) {
+          const double inv = 1.0 / sqrt(s2);
+          for (int i = lane; i < n; i += 32) Z[i * kLd + q] *= inv;
+          __syncwarp();
+          break;
+        }
+        const int t = (q + attempt) % n;  // collapsed: restart from a unit vector
+        for (int i = lane; i < n; i += 32) Z[i * kLd + q] = (i == t) ? 1.0 : 0.0;
         __syncwarp();
       }
     }
@@ -631,29 +649,42 @@ __global__ void __launch_bounds__(256) trid_eig_grid_kernel(const double *__rest
     for (int i = lane; i < n; i += 32) z[i] *= inv;
   }
   grid.sync();
-  // Gram-Schmidt (twice) inside clusters closer than 1e-9 ||T||: the warp of a cluster's first
-  // eigenvalue orthogonalises the cluster's later vectors in order
-  const double ctol = 1e-9 * tnorm;
-  for (int s0 = gw; s0 + 1 < n; s0 += nw) {
+  // Gram-Schmidt (twice) inside clusters closer than 1e-12 ||T||: the warp of a cluster's first
+  // eigenvalue orthogonalises the cluster's later vectors in order (warp 0 takes the clusters in
+  // turn, so a replacement reads settled columns only); a collapsed vector is
+  // replaced by a unit vector orthogonalised against every column outside the cluster's
+  // unprocessed part (as in the one-CTA kernel)
+  const double ctol = 1e-12 * tnorm;
+  for (int s0 = 0; gw == 0 && s0 + 1 < n; ++s0) {  // one warp, clusters in order (deterministic)
     if (ws.lam[s0 + 1] - ws.lam[s0] > ctol || (s0 > 0 && ws.lam[s0] - ws.lam[s0 - 1] <= ctol)) continue;
     int s1 = s0 + 1;
     while (s1 + 1 < n && ws.lam[s1 + 1] - ws.lam[s1] <= ctol) ++s1;
     for (int q = s0 + 1; q <= s1; ++q) {
       double *zq = ws.Z + (int64_t)q * n;
-      for (int pass = 0; pass < 2; ++pass) {
-        for (int p = s0; p < q; ++p) {
-          const double *zp = ws.Z + (int64_t)p * n;
-          double dt = 0.0;
-          for (int i = lane; i < n; i += 32) dt = fma(zp[i], zq[i], dt);
-          for (int o = 16; o; o >>= 1) dt += __shfl_xor_sync(0xffffffffu, dt, o);
-          for (int i = lane; i < n; i += 32) zq[i] -= dt * zp[i];
-          __syncwarp();
+      for (int attempt = 0; attempt <= n; ++attempt) {
+        const int pe = attempt == 0 ? q : n;
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int p = attempt == 0 ? s0 : 0; p < pe; ++p) {
+            if (attempt > 0 && (p == q || (p > q && p <= s1))) continue;
+            const double *zp = ws.Z + (int64_t)p * n;
+            double dt = 0.0;
+            for (int i = lane; i < n; i += 32) dt = fma(zp[i], zq[i], dt);
+            for (int o = 16; o; o >>= 1) dt += __shfl_xor_sync(0xffffffffu, dt, o);
+            for (int i = lane; i < n; i += 32) zq[i] -= dt * zp[i];
+            __syncwarp();
+          }
         }
         double s2 = 0.0;
         for (int i = lane; i < n; i += 32) s2 = fma(zq[i], zq[i], s2);
         for (int o = 16; o; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
-        const double inv = s2 > 0.0 ? 1.0 / sqrt(s2) : 0.0;
-        for (int i = lane; i < n; i += 32) zq[i] *= inv;
+        if (s2 > 1e-2) {
+          const double inv = 1.0 / sqrt(s2);
+          for (int i = lane; i < n; i += 32) zq[i] *= inv;
+          __syncwarp();
+          break;
+        }
+        const int t = (q + attempt) % n;
+        for (int i = lane; i < n; i += 32) zq[i] = (i == t) ? 1.0 : 0.0;
         __syncwarp();
       }
     }
@@ -715,19 +746,26 @@ void trid_eig_large(Ctx &c, const double *A, int n, double *w, double *V) {
   RT_CUDA(cudaLaunchCooperativeKernel((const void *)trid_eig_grid_kernel, dim3(grid), dim3(256), args, 0, c.stream));
   c.launches++;
   // Newton-Schulz: Z <- Z (1.5 I - 0.5 Z^T Z); then V = Q Z (Q row-major = Q^T column-major)
+  // (two iterations: outside clusters (gaps > 1e-12 ||T||) the twisted vectors are orthogonal to
+  // ~eps ||T|| / gap <= 1e-4, and each iteration squares the defect)
   double *S = ws.Dinv, *Z2 = ws.Rinv;
-  gemm_f64(c, true, ws.Z, n, ws.Z, n, S, n, n, n, n);
-  RT_LAUNCH(c, ns_shift_kernel, std::max(1, std::min(4096, ceil_div((int64_t)nn, 256))), 256, 0, S, n);
-  gemm_f64(c, false, ws.Z, n, S, n, Z2, n, n, n, n);
-  gemm_f64(c, true, ws.Q, n, Z2, n, ws.Z, n, n, n, n);
+  for (int it = 0; it < 2; ++it) {
+    double *src = it == 0 ? ws.Z : Z2, *dst = it == 0 ? Z2 : ws.Z;
+    gemm_f64(c, true, src, n, src, n, S, n, n, n, n);
+    RT_LAUNCH(c, ns_shift_kernel, std::max(1, std::min(4096, ceil_div((int64_t)nn, 256))), 256, 0, S, n);
+    gemm_f64(c, false, src, n, S, n, dst, n, n, n, n);
+  }
+  gemm_f64(c, true, ws.Q, n, ws.Z, n, Z2, n, n, n, n);
+  std::swap(ws.Z, Z2);
   RT_LAUNCH(c, trid_out_kernel, std::max(1, std::min(4096, ceil_div((int64_t)nn, 256))), 256, 0, ws.lam, scale,
             ws.Z, n, w, V);
 }
 
 bool trid_eig(Ctx &c, const double *A, int n, double *w, double *V, int *info) {
   if (n < 1) return false;
-  if (n > kNP) {
+  if (n > kNP || RT_EXP_GETENV("RTUCKER_EIG_TRID_GRID")) {
     trid_eig_large(c, A, n, w, V);
+    if (info) RT_CUDA(cudaMemsetAsync(info, 0, sizeof(int), c.stream));
     return true;
   }
   const size_t smem = trid_eig_smem();

@@ -152,14 +152,21 @@ def test_adaptive_large_ranks_odeco300(ctx):
     columns and truncates to ranks (153, 125, 97), so the Gram eigensolves of sizes 180 and
     130 run on the grid-synchronised Jacobi and 110 on the shared-memory one."""
     from workloads import odeco
+    from paper_1905_07311_b200.rtucker import ACCUM_FP64
     x = odeco(300, seed=4, dtype=np.float32)
-    g = _run(ctx, x, 1e-2, 10, seed=0, order=(0, 1, 2))
     o = O.adaptive_r_sthosvd(x, 1e-2, 10, seed=0, order=(0, 1, 2), floor_rel=1e-6)
     assert max(o.ell) > 112
+    # FP64 policy: fp64 normals and products, so only rounding separates GPU and oracle
+    g = _run(ctx, x, 1e-2, 10, seed=0, order=(0, 1, 2), flags=ACCUM_FP64)
+    assert g.ranks == o.ranks and g.ell == o.ell, (g.ranks, o.ranks)
+    assert _delta(x, g, o) <= 1e-8
+    # default (HYBRID): fp32 normals (Omega within ~1e-7 of the oracle's, reading R3); at ranks
+    # ~150 of this slowly decaying spectrum the truncated basis amplifies that to ~1e-5
+    g = _run(ctx, x, 1e-2, 10, seed=0, order=(0, 1, 2))
     tie = _check_blocks_fp32(x, g, o, 1e-2)
     if not tie:
         assert g.ranks == o.ranks, (g.ranks, o.ranks)
-        assert _delta(x, g, o) <= 1e-5
+        assert _delta(x, g, o) <= 1e-4
     assert O.rel_error(x, g.core, g.factors) <= 1e-2
 
 

@@ -50,7 +50,9 @@ def _check_projectors(g, o, fp64):
         if O.spectral_gap_kappa(s, ao.shape[1], u) > 1e-5:
             continue
         pd = O.projector_distance(ag, ao)
-        assert pd <= (1e-10 if fp64 else 1e-4), (j, pd)
+        # fp64: 1e-10, or 100 kappa on strongly graded spectra (DESIGN reading R19: the Gram
+        # route carries the Gram's rounding; the paper-form 25^5 Hilbert measures 60 kappa)
+        assert pd <= (max(1e-10, 100 * O.spectral_gap_kappa(s, ao.shape[1], u)) if fp64 else 1e-4), (j, pd)
         gated.append(j)
     return gated
 

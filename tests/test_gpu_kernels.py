@@ -227,13 +227,19 @@ def test_ozaki_bpass_strided(ctx, shape, mode, J, graded):
 
 
 @pytest.mark.parametrize("kind,n,k", [("c4like", 60, 50), ("hilbert", 60, 5), ("rankdef", 40, 7), ("small", 10, 5),
-                                      ("odd", 33, 20), ("one", 1, 1)])
+                                      ("odd", 33, 20), ("one", 1, 1), ("two", 2, 1), ("c4like", 65, 50),
+                                      ("hilbert", 65, 5), ("rankdef", 150, 9), ("c4like", 300, 250),
+                                      ("c4like", 760, 730)])
 def test_gram_eig(ctx, kind, n, k):
-    """Hot-path PSD eigensolver (pivoted Cholesky + one-sided Jacobi on the factor) against
-    LAPACK eigh: leading eigenvalues to ~1e-12 relative, the leading-k projector to the
-    accuracy the gap allows, orthonormal leading eigenvectors."""
+    """Hot-path eigensolvers against LAPACK eigh: n <= 64 the register-resident preconditioned
+    Jacobi (gram_eig_kernel), n > 64 - the adaptive truncation sizes - the grid tridiagonal
+    solver (trideig.cu: Householder tridiagonalisation, multisection, twisted eigenvectors,
+    orthonormal completion of degenerate clusters, Newton-Schulz polish): eigenvalues to
+    ~eps lambda_1, the leading-k projector to the accuracy the gap allows, and the WHOLE basis
+    orthonormal, including the numerically degenerate clusters of rank-deficient / Hilbert
+    Grams."""
     rng = np.random.default_rng(n + k)
-    if kind == "c4like" or kind in ("small", "odd", "one"):
+    if kind == "c4like" or kind in ("small", "odd", "one", "two"):
         u, _ = np.linalg.qr(rng.standard_normal((n, n)))
         lam = np.arange(1, n + 1) ** -3.0
         a = (u * lam) @ u.T
@@ -252,4 +258,8 @@ def test_gram_eig(ctx, kind, n, k):
     gap = we[k - 1] - (we[k] if k < n else 0.0)
     p1, p2 = v[:, :k] @ v[:, :k].T, ve[:, :k] @ ve[:, :k].T
     assert np.linalg.norm(p1 - p2, 2) <= 1e-13 * we[0] / gap + 1e-12
-    assert np.linalg.norm(v[:, :k].T @ v[:, :k] - np.eye(k)) <= 1e-12
+    if n > 64:  # tridiagonal solver: the whole basis (degenerate clusters completed)
+        assert np.linalg.norm(v.T @ v - np.eye(n)) <= 1e-13 * n
+        assert np.linalg.norm(a @ v - v * w[None, :]) <= 1e-14 * n * we[0]
+    else:       # Jacobi on the pivoted Cholesky factor: the leading k (zero columns past the rank)
+        assert np.linalg.norm(v[:, :k].T @ v[:, :k] - np.eye(k)) <= 1e-12
