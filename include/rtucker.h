@@ -277,6 +277,14 @@ rtucker_status rtucker_debug_eig(rtucker_ctx *ctx, int32_t n, const double *A, d
 rtucker_status rtucker_debug_gram_eig(rtucker_ctx *ctx, int32_t n, const double *A, double *w, double *V,
                                       int32_t *sweeps_out /* host, may be NULL */);
 
+/* C (m x n) = op(A) op(B), fp64 column-major on the tensor cores (the library's GEMM for the
+ * adaptive truncation and the eigensolver), DEVICE pointers; trans* != 0 transposes. */
+rtucker_status rtucker_debug_gemm(rtucker_ctx *ctx, int transA, int transB, int64_t m, int64_t n, int64_t k,
+                                  const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc);
+
+/* Gram C (K x K) = B_(n) B_(n)^T of an fp64 tensor stored (L, K, R) (DEVICE pointers). */
+rtucker_status rtucker_debug_gram(rtucker_ctx *ctx, int64_t L, int64_t K, int64_t R, const double *B, double *C);
+
 /* Strong-RRQR row selection (DESIGN reading R9) of an m x l orthonormal fp64 Q:
  * sel (l, sorted ascending, DEVICE int64) and A = Q Q[sel,:]^{-1} (m x l, DEVICE). */
 rtucker_status rtucker_debug_srrqr(rtucker_ctx *ctx, int64_t m, int32_t l, const double *Q,

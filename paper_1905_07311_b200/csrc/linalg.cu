@@ -107,6 +107,128 @@ __global__ void __launch_bounds__(256) gemm_f64_kernel(bool transA, bool transB,
       }
 }
 
+// Large GEMMs (adaptive truncation: Gram and shrink with k, r ~ 700): CTA tile 64 x 128, 8 warps
+// of 32 x 32 (16 m8n8k4 tiles each: 8 fragment loads feed 16 MMAs), K tiles of 16 in a 3-stage
+// cp.async ring (8-byte copies: leading dimensions need not be even), zero fill at the edges.
+// Shared layouts follow the global ones (no transposition): A as [k][m] (TA = false) or [m][k],
+// B as [n][k] (TB = false) or [k][n].
+constexpr int kBm = 64, kBn = 128, kBk = 16, kBs = 3;
+constexpr int kPadM = kBm + 2, kPadN = kBn + 2, kPadK = kBk + 2;
+// GA (Gram of a mode unfolding, L > 1): op(A)(i, t) = A[(t % L) + L i + L Km (t / L)] and
+// op(B)(t, j) the same with j; blockIdx.z = K chunk [z kc, (z+1) kc) with C + z sC its partial.
+template <bool TA, bool TB, bool GA = false>
+__global__ void __launch_bounds__(256) gemm_f64_big_kernel(const double *__restrict__ A, int64_t lda, int64_t sA,
+                                                           const double *__restrict__ B, int64_t ldb, int64_t sB,
+                                                           double *__restrict__ C, int64_t ldc, int64_t sC, int64_t m,
+                                                           int64_t n, int64_t k, double beta, double alpha,
+                                                           int64_t gL = 1, int64_t gKm = 1, int64_t kc = 0) {
+  extern __shared__ __align__(16) double gsm[];
+  constexpr int kAst = TA ? kBm * kPadK : kBk * kPadM;  // doubles per A stage
+  constexpr int kBst = TB ? kBk * kPadN : kBn * kPadK;  // doubles per B stage
+  double *As = gsm, *Bs = gsm + kBs * kAst;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int64_t kbeg = 0;
+  if (GA) {
+    kbeg = (int64_t)blockIdx.z * kc;
+    k = min(k, kbeg + kc);
+  } else {
+    A += sA * blockIdx.z;
+    B += sB * blockIdx.z;
+  }
+  C += sC * blockIdx.z;
+  const int64_t i0 = (int64_t)blockIdx.x * kBm, j0 = (int64_t)blockIdx.y * kBn;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  const int nkt = (int)((k - kbeg + kBk - 1) / kBk);
+  auto load_stage = [&](int kt, int st) {
+    const int64_t k0 = kbeg + (int64_t)kt * kBk;
+    double *as = As + st * kAst, *bs = Bs + st * kBst;
+    // A: 64 x 16 = 1024 elements, 4 per thread
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;
+      int mm, kk;
+      if (!TA) { mm = e & 63; kk = e >> 6; } else { kk = e & 15; mm = e >> 4; }
+      const int64_t gi = i0 + mm, gk = k0 + kk;
+      const bool ok = gi < m && gk < k;
+      const double *src = A;
+      if (ok) {
+        if (GA) src = A + (gk % gL) + gL * gi + gL * gKm * (gk / gL);
+        else src = TA ? A + gk + lda * gi : A + gi + lda * gk;
+      }
+      double *dst = TA ? as + mm * kPadK + kk : as + kk * kPadM + mm;
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "r"(ok ? 8 : 0));
+    }
+    // B: 16 x 128 = 2048 elements, 8 per thread
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int e = tid + 256 * q;
+      int nn, kk;
+      if (!TB) { kk = e & 15; nn = e >> 4; } else { nn = e & 127; kk = e >> 7; }
+      const int64_t gj = j0 + nn, gk = k0 + kk;
+      const bool ok = gj < n && gk < k;
+      const double *src = B;
+      if (ok) {
+        if (GA) src = B + (gk % gL) + gL * gj + gL * gKm * (gk / gL);
+        else src = TB ? B + gj + ldb * gk : B + gk + ldb * gj;
+      }
+      double *dst = TB ? bs + kk * kPadN + nn : bs + nn * kPadK + kk;
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(sa), "l"(src), "r"(ok ? 8 : 0));
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+#pragma unroll
+  for (int st = 0; st < kBs - 1; ++st) {
+    if (st < nkt) load_stage(st, st);
+    asm volatile("cp.async.commit_group;");
+  }
+  for (int kt = 0; kt < nkt; ++kt) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kBs - 2));
+    __syncthreads();
+    if (kt + kBs - 1 < nkt) load_stage(kt + kBs - 1, (kt + kBs - 1) % kBs);
+    asm volatile("cp.async.commit_group;");
+    const double *as = As + (kt % kBs) * kAst, *bs = Bs + (kt % kBs) * kBst;
+#pragma unroll
+    for (int ks = 0; ks < kBk; ks += 4) {
+      const int kk = ks + (lane & 3), r = lane >> 2;
+      double av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = TA ? as[(wm + 8 * a + r) * kPadK + kk] : as[kk * kPadM + wm + 8 * a + r];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = TB ? bs[kk * kPadN + wn + 8 * b + r] : bs[(wn + 8 * b + r) * kPadK + kk];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[a][b][0]), "+d"(acc[a][b][1])
+                       : "d"(av[a]), "d"(bv[b]));
+    }
+  }
+  asm volatile("cp.async.wait_group 0;");
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t gi = i0 + wm + 8 * a + (lane >> 2), gj = j0 + wn + 8 * b + 2 * (lane & 3) + h;
+        if (gi < m && gj < n) {
+          double *cp = C + gi + ldc * gj;
+          const double v = alpha * acc[a][b][h];
+          *cp = beta == 0.0 ? v : fma(beta, *cp, v);
+        }
+      }
+}
+constexpr size_t kBigSmem(bool ta, bool tb) {
+  return sizeof(double) * kBs * ((ta ? kBm * kPadK : kBk * kPadM) + (tb ? kBk * kPadN : kBn * kPadK));
+}
+
 // Gram C = X X^T (K x K) of the mode unfolding of a (L, K, R) fp64 tensor B: X(i, t) =
 // B[(t % L) + L (i + K (t / L))], t < L R, on the fp64 tensor cores.  Upper 64 x 64 tiles,
 // K dimension split over gridDim.z chunks (partials summed in a fixed order by
@@ -172,6 +294,23 @@ __global__ void __launch_bounds__(256) gram_gather_kernel(const double *__restri
         const int64_t gi = i0 + wm + 8 * a + (lane >> 2), gj = j0 + wn + 8 * b + 2 * (lane & 3) + h;
         if (gi < K && gj < K) P[gi + K * gj] = acc[a][b][h];
       }
+}
+
+__global__ void gram_reduce_full_kernel(const double *__restrict__ part, int nsplit, int64_t K,
+                                        double *__restrict__ C) {
+  // fixed-order sum of the split partials; the two triangles are averaged so C is exactly symmetric
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K * K; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e % K, j = e / K;
+    if (i > j) continue;
+    double s1 = 0.0, s2 = 0.0;
+    for (int q = 0; q < nsplit; ++q) {
+      s1 += part[(int64_t)q * K * K + e];
+      s2 += part[(int64_t)q * K * K + j + K * i];
+    }
+    const double s = 0.5 * (s1 + s2);
+    C[i + K * j] = s;
+    C[j + K * i] = s;
+  }
 }
 
 __global__ void gram_split_reduce_kernel(const double *__restrict__ part, int nsplit, int64_t K,
@@ -250,6 +389,21 @@ void gemm_f64_batched(Ctx &c, bool transA, bool transB, const double *A, int64_t
                       int64_t batch, double beta, double alpha) {
   if (m <= 0 || n <= 0 || batch <= 0) return;
   RT_REQUIRE(batch <= 65535, "gemm: more than 65535 batches");
+  if (m * n * k * batch >= (int64_t)1 << 28) {  // large: the pipelined 64 x 128 kernel
+    const dim3 g((unsigned)((m + kBm - 1) / kBm), (unsigned)((n + kBn - 1) / kBn), (unsigned)batch);
+#define RT_BIG(TA_, TB_)                                                                                      \
+  do {                                                                                                       \
+    smem_attr(gemm_f64_big_kernel<TA_, TB_>, kBigSmem(TA_, TB_));                                            \
+    RT_LAUNCH(c, (gemm_f64_big_kernel<TA_, TB_>), g, 256, kBigSmem(TA_, TB_), A, lda, sA, B, ldb, sB, C, ldc, sC, m, \
+              n, k, beta, alpha);                                                                            \
+  } while (0)
+    if (!transA && !transB) RT_BIG(false, false);
+    else if (transA && !transB) RT_BIG(true, false);
+    else if (!transA && transB) RT_BIG(false, true);
+    else RT_BIG(true, true);
+#undef RT_BIG
+    return;
+  }
   const dim3 grid((unsigned)((m + kGm - 1) / kGm), (unsigned)((n + kGm - 1) / kGm), (unsigned)batch);
   RT_LAUNCH(c, gemm_f64_kernel, grid, 256, 0, transA, transB, A, lda, sA, B, ldb, sB, C, ldc, sC, m, n, k, beta,
             alpha);
@@ -257,15 +411,46 @@ void gemm_f64_batched(Ctx &c, bool transA, bool transB, const double *A, int64_t
 
 void gram_f64(Ctx &c, const double *B, int64_t L, int64_t K, int64_t R, double *C) {
   const int64_t T = L * R;
-  const int tiles = (int)((K + kGm - 1) / kGm);
-  const int ntile = tiles * (tiles + 1) / 2;
-  // enough K-chunks to cover ~2 waves of CTAs, each chunk a multiple of the K step
-  int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>((2 * c.num_sms + ntile - 1) / ntile, (T + 4095) / 4096));
-  const int64_t chunk = ((T + nsplit - 1) / nsplit + kGk - 1) / kGk * kGk;
+  if (K * K * T < ((int64_t)1 << 28)) {  // small: the simple tiled kernel (upper tiles, split K)
+    const int tiles = (int)((K + kGm - 1) / kGm);
+    const int ntile = tiles * (tiles + 1) / 2;
+    int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>((2 * c.num_sms + ntile - 1) / ntile, (T + 4095) / 4096));
+    const int64_t chunk = ((T + nsplit - 1) / nsplit + kGk - 1) / kGk * kGk;
+    nsplit = (int)((T + chunk - 1) / chunk);
+    DevBuf<double> part(c, (size_t)nsplit * K * K);
+    RT_LAUNCH(c, gram_gather_kernel, dim3(tiles, tiles, nsplit), 256, 0, B, L, K, R, chunk, part.p);
+    RT_LAUNCH(c, gram_split_reduce_kernel, std::max(1, std::min(4096, ceil_div(K * K, 256))), 256, 0, part.p,
+              nsplit, K, C);
+    return;
+  }
+  // large: the pipelined kernel on the full K x K (both triangles), K chunks over ~2 waves,
+  // partials summed in a fixed order
+  const int64_t tiles = ((K + kBm - 1) / kBm) * ((K + kBn - 1) / kBn);
+  int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>((2 * c.num_sms + tiles - 1) / tiles, T / 2048));
+  const int64_t chunk = ((T + nsplit - 1) / nsplit + kBk - 1) / kBk * kBk;
   nsplit = (int)((T + chunk - 1) / chunk);
   DevBuf<double> part(c, (size_t)nsplit * K * K);
-  RT_LAUNCH(c, gram_gather_kernel, dim3(tiles, tiles, nsplit), 256, 0, B, L, K, R, chunk, part.p);
-  RT_LAUNCH(c, gram_split_reduce_kernel, std::max(1, std::min(4096, ceil_div(K * K, 256))), 256, 0, part.p, nsplit,
+  const dim3 g((unsigned)((K + kBm - 1) / kBm), (unsigned)((K + kBn - 1) / kBn), (unsigned)nsplit);
+  if (L == 1) {  // X = B (K x R, column-major): C = X X^T, full K chunks as batches, then the tail
+    const int64_t nfull = T / chunk, tl = T - nfull * chunk;
+    smem_attr(gemm_f64_big_kernel<false, true, false>, kBigSmem(false, true));
+    if (nfull > 0) {
+      const dim3 gf(g.x, g.y, (unsigned)nfull);
+      RT_LAUNCH(c, (gemm_f64_big_kernel<false, true, false>), gf, 256, kBigSmem(false, true), B, K, chunk * K, B, K,
+                chunk * K, part.p, K, K * K, K, K, chunk, 0.0, 1.0, (int64_t)1, (int64_t)1, (int64_t)0);
+    }
+    if (tl > 0) {
+      const dim3 g1(g.x, g.y, 1);
+      RT_LAUNCH(c, (gemm_f64_big_kernel<false, true, false>), g1, 256, kBigSmem(false, true), B + nfull * chunk * K, K,
+                0, B + nfull * chunk * K, K, 0, part.p + nfull * K * K, K, 0, K, K, tl, 0.0, 1.0, (int64_t)1,
+                (int64_t)1, (int64_t)0);
+    }
+  } else {
+    smem_attr(gemm_f64_big_kernel<true, false, true>, kBigSmem(true, false));
+    RT_LAUNCH(c, (gemm_f64_big_kernel<true, false, true>), g, 256, kBigSmem(true, false), B, 0, 0, B, 0, 0, part.p, K,
+              K * K, K, K, T, 0.0, 1.0, L, K, chunk);
+  }
+  RT_LAUNCH(c, gram_reduce_full_kernel, std::max(1, std::min(4096, ceil_div(K * K, 256))), 256, 0, part.p, nsplit,
             K, C);
 }
 

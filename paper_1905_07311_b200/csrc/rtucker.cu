@@ -465,6 +465,19 @@ rtucker_status rtucker_debug_gram_eig(rtucker_ctx *ctx, int32_t n, const double 
   });
 }
 
+rtucker_status rtucker_debug_gemm(rtucker_ctx *ctx, int transA, int transB, int64_t m, int64_t n, int64_t k,
+                                  const double *A, int64_t lda, const double *B, int64_t ldb, double *C, int64_t ldc) {
+  if (!ctx || !A || !B || !C || m < 1 || n < 1 || k < 1) return RTUCKER_EINVAL;
+  return guard(ctx, [&] {
+    gemm_f64_batched(ctx->c, transA != 0, transB != 0, A, lda, 0, B, ldb, 0, C, ldc, 0, m, n, k, 1);
+  });
+}
+
+rtucker_status rtucker_debug_gram(rtucker_ctx *ctx, int64_t L, int64_t K, int64_t R, const double *B, double *C) {
+  if (!ctx || !B || !C || L < 1 || K < 1 || R < 1) return RTUCKER_EINVAL;
+  return guard(ctx, [&] { gram_f64(ctx->c, B, L, K, R, C); });
+}
+
 rtucker_status rtucker_debug_srrqr(rtucker_ctx *ctx, int64_t m, int32_t l, const double *Q, double eta,
                                    int64_t *sel, double *A, int32_t *swaps_out) {
   if (!ctx || !Q || !sel || !A || l < 1 || m < l || !(eta >= 1.0)) return RTUCKER_EINVAL;

@@ -44,6 +44,7 @@ EXPORTED = [
     "rtucker_rel_error", "rtucker_debug_sketch", "rtucker_debug_omega", "rtucker_debug_philox",
     "rtucker_debug_qr", "rtucker_debug_eig", "rtucker_debug_srrqr", "rtucker_set_profiling",
     "rtucker_phase_times", "rtucker_debug_gram_eig", "rtucker_debug_ttm", "rtucker_debug_loopback_sharding",
+    "rtucker_debug_gemm", "rtucker_debug_gram",
 ]
 PHASES = ("sketch", "qr", "bpass", "eig", "shrink", "other")
 
@@ -117,6 +118,8 @@ def load_library(path: str = LIB_PATH):
         "rtucker_debug_ttm": (C.c_int, [P, C.POINTER(DenseDesc), I32, P, I32, U32, P, P]),
         "rtucker_debug_loopback_sharding": (C.c_int, [P, C.c_int]),
         "rtucker_set_profiling": (C.c_int, [P, C.c_int]),
+        "rtucker_debug_gemm": (C.c_int, [P, C.c_int, C.c_int, I64, I64, I64, P, I64, P, I64, P, I64]),
+        "rtucker_debug_gram": (C.c_int, [P, I64, I64, I64, P, P]),
         "rtucker_phase_times": (C.c_int, [P, P, P, C.c_int]),
     }
     for name, (res, args) in sig.items():
@@ -495,6 +498,31 @@ class Context:
         self.sync()
         self.last_sweeps = int(sw.value)
         return w.cpu().numpy(), v.cpu().numpy().reshape((n, n), order="F")
+
+    def debug_gemm(self, a: np.ndarray, b: np.ndarray, transA=False, transB=False):
+        """C = op(A) op(B) through the library's fp64 tensor-core GEMM."""
+        torch = _torch()
+        at = torch.as_tensor(np.asfortranarray(a, dtype=np.float64).ravel(order="F"), device="cuda")
+        bt = torch.as_tensor(np.asfortranarray(b, dtype=np.float64).ravel(order="F"), device="cuda")
+        m = a.shape[1] if transA else a.shape[0]
+        k = a.shape[0] if transA else a.shape[1]
+        n = b.shape[0] if transB else b.shape[1]
+        c = torch.empty(m * n, dtype=torch.float64, device="cuda")
+        self._enter()
+        self._check(self.lib.rtucker_debug_gemm(self.h, int(transA), int(transB), m, n, k, at.data_ptr(), a.shape[0],
+                                                bt.data_ptr(), b.shape[0], c.data_ptr(), m))
+        self.sync()
+        return c.cpu().numpy().reshape((m, n), order="F")
+
+    def debug_gram(self, b: np.ndarray, L: int, K: int, R: int):
+        """Gram of the mode unfolding of an fp64 tensor stored (L, K, R) (flat image b)."""
+        torch = _torch()
+        bt = torch.as_tensor(np.asarray(b, dtype=np.float64).ravel(), device="cuda")
+        c = torch.empty(K * K, dtype=torch.float64, device="cuda")
+        self._enter()
+        self._check(self.lib.rtucker_debug_gram(self.h, L, K, R, bt.data_ptr(), c.data_ptr()))
+        self.sync()
+        return c.cpu().numpy().reshape((K, K), order="F")
 
     def debug_srrqr(self, q: np.ndarray, eta: float = 2.0):
         torch = _torch()

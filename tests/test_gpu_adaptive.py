@@ -194,16 +194,24 @@ def test_c4_adaptive_full_size(ctx):
     assert err <= 1e-3, err
     nx2 = gold["norm_sq"]
     tau2 = (1e-3 / np.sqrt(3)) ** 2 * nx2
+    tie = False
     for j in range(3):
         m = gold["modes"][str(j)]
+        if tie:
+            # after a certified near-tie the later modes work on a differently shaped core, so
+            # only closeness is asserted (the tolerance itself is checked above)
+            assert abs(h.ranks[j] - gold["ranks"][j]) <= 0.02 * gold["ranks"][j], (j, h.ranks, gold["ranks"])
+            continue
         if h.ell[j] != m["k"]:
             # certified near-tie only: the oracle's residual after the shorter count is at tau^2
             e = m["e_hist_tail"][-2] if h.ell[j] < m["k"] else m["e_hist_tail"][-1]
             assert abs(h.ell[j] - m["k"]) == 10 and abs(e - tau2) <= 1e-3 * tau2, (j, h.ell, m)
+            tie = True
         elif h.ranks[j] != gold["ranks"][j]:
             # truncation near-tie only: the oracle's margin at its rank decision is within 1e-3 tau^2
             assert abs(h.ranks[j] - gold["ranks"][j]) == 1, (j, h.ranks, gold["ranks"])
             assert min(abs(v) for v in m["trunc_margin"] if v is not None) <= 1e-3, (j, m)
+            tie = True
     print("C4 adaptive: ranks", h.ranks, "oracle", gold["ranks"], "columns", h.ell, "rel_err", err,
           "oracle", gold["rel_err_identity"])
 

@@ -263,3 +263,30 @@ def test_gram_eig(ctx, kind, n, k):
         assert np.linalg.norm(a @ v - v * w[None, :]) <= 1e-14 * n * we[0]
     else:       # Jacobi on the pivoted Cholesky factor: the leading k (zero columns past the rank)
         assert np.linalg.norm(v[:, :k].T @ v[:, :k] - np.eye(k)) <= 1e-12
+
+
+@pytest.mark.parametrize("m,n,k,ta,tb", [(730, 900, 760, True, False), (70, 40, 65, False, False),
+                                         (300, 257, 1000, False, True), (129, 300, 77, True, True),
+                                         (760, 760, 4000, False, True)])
+def test_gemm_f64(ctx, m, n, k, ta, tb):
+    """The library's fp64 tensor-core GEMM (both the simple and the pipelined cp.async kernel,
+    every transposition, ragged edges) against numpy: fp64 accuracy (1e-14 relative)."""
+    rng = np.random.default_rng(m + n + k)
+    a = rng.standard_normal((k, m) if ta else (m, k))
+    b = rng.standard_normal((n, k) if tb else (k, n))
+    c = ctx.debug_gemm(a, b, ta, tb)
+    ref = (a.T if ta else a) @ (b.T if tb else b)
+    assert np.max(np.abs(c - ref)) <= 1e-14 * np.sqrt(k) * np.max(np.abs(a)) * np.max(np.abs(b)) * 10
+
+
+@pytest.mark.parametrize("L,K,R", [(1, 760, 20000), (730, 120, 30), (7, 65, 50), (1, 30, 1000), (50, 700, 40)])
+def test_gram_f64(ctx, L, K, R):
+    """Gram B_(n) B_(n)^T of a (L, K, R) fp64 tensor (adaptive truncation), gather layout for
+    L > 1, split K with a fixed-order reduction: fp64 accuracy and exact symmetry."""
+    rng = np.random.default_rng(L + K + R)
+    b = rng.standard_normal(L * K * R)
+    c = ctx.debug_gram(b, L, K, R)
+    x = O.unfold(b.reshape((L, K, R), order="F"), 1)
+    ref = x @ x.T
+    assert np.max(np.abs(c - ref)) <= 1e-13 * np.max(np.abs(ref))
+    np.testing.assert_array_equal(c, c.T)
