@@ -110,6 +110,10 @@ typedef enum { RTUCKER_DEVICE = 0, RTUCKER_HOST = 1 } rtucker_memory;
 /* Debug checks: index-range and finite-value checks of the inputs, and a stream
  * synchronisation with error check after every step (slow; for debugging). */
 #define RTUCKER_DEBUG_CHECKS      (1u << 8)
+/* rtucker_sparse_sthosvd: SP-HOSVD instead of SP-STHOSVD (the paper's first variant):
+ * every mode is sketched and selected on X itself, and the core is X x_1 P_1^T ... x_d P_d^T,
+ * one filter by all selections (order is ignored; nnz_history = [nnz(X), nnz(core)]). */
+#define RTUCKER_SP_HOSVD          (1u << 9)
 
 /* Dense tensor, first-mode-fastest.  When the tensor is sharded across ranks along its
  * LAST mode, dims[] are the GLOBAL dims and this rank holds the contiguous slab of

@@ -463,8 +463,20 @@ __global__ void build_lookup(const int64_t *__restrict__ sel, int ell, int32_t *
 
 constexpr int kCompactB = 1024;
 
-__global__ void compact_count(const int32_t *__restrict__ idx, const int64_t *__restrict__ nnz_dev,
-                              const int32_t *__restrict__ lut, int64_t *__restrict__ counts) {
+// Per-mode lookup tables of a selection: lut[m][i] = position of i in S_m, or -1; a null table
+// keeps every index of that mode (single-mode filter of SP-STHOSVD, all-mode filter of SP-HOSVD).
+struct LutSet {
+  const int32_t *lut[kMaxModes];
+};
+
+__device__ __forceinline__ bool keep_entry(const CooDev &in, const LutSet &ls, int64_t e) {
+  for (int k = 0; k < in.d; ++k)
+    if (ls.lut[k] && ls.lut[k][in.idx[k][e]] < 0) return false;
+  return true;
+}
+
+__global__ void compact_count(CooDev in, const int64_t *__restrict__ nnz_dev, LutSet ls,
+                              int64_t *__restrict__ counts) {
   __shared__ int64_t sc[32];
   const int64_t nnz = *nnz_dev;
   const int64_t e = (int64_t)blockIdx.x * kCompactB + threadIdx.x;
@@ -472,7 +484,7 @@ __global__ void compact_count(const int32_t *__restrict__ idx, const int64_t *__
     if (threadIdx.x == 0) counts[blockIdx.x] = 0;
     return;
   }
-  const int keep = (e < nnz && lut[idx[e]] >= 0) ? 1 : 0;
+  const int keep = (e < nnz && keep_entry(in, ls, e)) ? 1 : 0;
   const unsigned bal = __ballot_sync(0xffffffffu, keep);
   if ((threadIdx.x & 31) == 0) sc[threadIdx.x >> 5] = __popc(bal);
   __syncthreads();
@@ -511,16 +523,14 @@ __global__ void exclusive_scan_single(int64_t *__restrict__ v, int64_t n, int64_
 }
 
 template <typename TV>
-__global__ void compact_scatter(CooDev in, const int64_t *__restrict__ nnz_dev, int mode,
-                                const int32_t *__restrict__ lut, const int64_t *__restrict__ offs,
-                                int32_t *const *__restrict__ oidx, TV *__restrict__ ovals) {
+__global__ void compact_scatter(CooDev in, const int64_t *__restrict__ nnz_dev, LutSet ls,
+                                const int64_t *__restrict__ offs, int32_t *const *__restrict__ oidx,
+                                TV *__restrict__ ovals) {
   __shared__ int wsum[32];
   const int64_t nnz = *nnz_dev;
   if ((int64_t)blockIdx.x * kCompactB >= nnz) return;
   const int64_t e = (int64_t)blockIdx.x * kCompactB + threadIdx.x;
-  int32_t pos = -1;
-  if (e < nnz) pos = lut[in.idx[mode][e]];
-  const int keep = pos >= 0;
+  const int keep = (e < nnz && keep_entry(in, ls, e)) ? 1 : 0;
   const unsigned bal = __ballot_sync(0xffffffffu, keep);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (lane == 0) wsum[w] = __popc(bal);
@@ -536,7 +546,10 @@ __global__ void compact_scatter(CooDev in, const int64_t *__restrict__ nnz_dev, 
   __syncthreads();
   if (!keep) return;
   const int64_t o = offs[blockIdx.x] + wsum[w] + __popc(bal & ((1u << lane) - 1u));
-  for (int k = 0; k < in.d; ++k) oidx[k][o] = (k == mode) ? pos : in.idx[k][e];
+  for (int k = 0; k < in.d; ++k) {
+    const int32_t i = in.idx[k][e];
+    oidx[k][o] = ls.lut[k] ? ls.lut[k][i] : i;
+  }
   ovals[o] = ((const TV *)in.vals)[e];
 }
 
@@ -656,26 +669,40 @@ void srrqr(Ctx &c, const double *Q, int64_t m, int l, double eta, int64_t *sel_d
   c.launches++;
 }
 
-// Keep entries whose mode-n index is in sel (sorted, length l) and renumber it; the new nnz
-// is written to nnz_out (device).
-void coo_select(Ctx &c, const CooDev &in, const int64_t *nnz_dev, int mode, const int64_t *sel, int l,
-                int32_t *const *out_idx, void *out_vals, int64_t *nnz_out) {
-  const int64_t I = in.dims[mode];
-  DevBuf<int32_t> lut(c, I);
-  RT_LAUNCH(c, fill_i32, grid_for(c, I), 256, 0, lut.p, I, -1);
-  RT_LAUNCH(c, build_lookup, 1, 256, 0, sel, l, lut.p);
+// Keep the entries whose index is selected in every mode m with sel[m] != null (sorted, length
+// l[m]) and renumber those modes; the live input nnz is read from nnz_dev, the new nnz written to
+// nnz_out (device).  Order-preserving.
+void coo_select_modes(Ctx &c, const CooDev &in, const int64_t *nnz_dev, const int64_t *const *sel, const int *l,
+                      int32_t *const *out_idx, void *out_vals, int64_t *nnz_out) {
+  LutSet ls{};
+  DevBuf<int32_t> lut[kMaxModes];
+  for (int m = 0; m < in.d; ++m) {
+    if (!sel[m]) continue;
+    const int64_t I = in.dims[m];
+    lut[m].alloc(c, I);
+    RT_LAUNCH(c, fill_i32, grid_for(c, I), 256, 0, lut[m].p, I, -1);
+    RT_LAUNCH(c, build_lookup, 1, 256, 0, sel[m], l[m], lut[m].p);
+    ls.lut[m] = lut[m].p;
+  }
   const int64_t nblk = std::max<int64_t>(1, (in.nnz + kCompactB - 1) / kCompactB);
   DevBuf<int64_t> offs(c, nblk);
-  RT_LAUNCH(c, compact_count, (int)nblk, kCompactB, 0, in.idx[mode], nnz_dev, lut.p, offs.p);
+  RT_LAUNCH(c, compact_count, (int)nblk, kCompactB, 0, in, nnz_dev, ls, offs.p);
   RT_LAUNCH(c, exclusive_scan_single, 1, 1024, 0, offs.p, nblk, nnz_out);
   DevBuf<int32_t *> optr(c, kMaxModes);
   RT_CUDA(cudaMemcpyAsync(optr.p, out_idx, sizeof(int32_t *) * kMaxModes, cudaMemcpyHostToDevice, c.stream));
   if (in.vt == DT::F64)
-    RT_LAUNCH(c, compact_scatter<double>, (int)nblk, kCompactB, 0, in, nnz_dev, mode, lut.p, offs.p, optr.p,
-              (double *)out_vals);
+    RT_LAUNCH(c, compact_scatter<double>, (int)nblk, kCompactB, 0, in, nnz_dev, ls, offs.p, optr.p, (double *)out_vals);
   else
-    RT_LAUNCH(c, compact_scatter<float>, (int)nblk, kCompactB, 0, in, nnz_dev, mode, lut.p, offs.p, optr.p,
-              (float *)out_vals);
+    RT_LAUNCH(c, compact_scatter<float>, (int)nblk, kCompactB, 0, in, nnz_dev, ls, offs.p, optr.p, (float *)out_vals);
+}
+
+void coo_select(Ctx &c, const CooDev &in, const int64_t *nnz_dev, int mode, const int64_t *sel, int l,
+                int32_t *const *out_idx, void *out_vals, int64_t *nnz_out) {
+  const int64_t *sels[kMaxModes] = {nullptr};
+  int ls[kMaxModes] = {0};
+  sels[mode] = sel;
+  ls[mode] = l;
+  coo_select_modes(c, in, nnz_dev, sels, ls, out_idx, out_vals, nnz_out);
 }
 
 rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int64_t *ranks, int p, uint64_t seed,
@@ -696,8 +723,11 @@ rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int6
     RT_REQUIRE(ranks[k] >= 1, "r_n must be >= 1");
     cur[k] = X->dims[k];
   }
+  const bool hosvd = flags & RTUCKER_SP_HOSVD;  // SP-HOSVD: modes on X, one final filter
   int32_t ord[kMaxModes];
-  check_order(order, d, ord, cur, false);
+  check_order(hosvd ? nullptr : order, d, ord, cur, false);
+  if (hosvd)
+    for (int k = 0; k < d; ++k) ord[k] = k;
   const bool nf64 = vt == DT::F64 || (flags & RTUCKER_ACCUM_MASK) == RTUCKER_ACCUM_FP64;
   const bool dbg = flags & RTUCKER_DEBUG_CHECKS;
   ResultGuard rg{c, new_result(d)};
@@ -755,7 +785,7 @@ rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int6
     DevBuf<double> Y(c, (size_t)I * ell), Q(c, (size_t)I * ell);
     {
       PhaseScope ps(c, PH_SKETCH, jj);
-      sketch_coo(c, g, n, ell, seed, nf64, Y.p, hist.p + jj, fs.p);
+      sketch_coo(c, g, n, ell, seed, nf64, Y.p, hist.p + (hosvd ? 0 : jj), fs.p);
       ps.next(PH_QR);
       thin_qr(c, Y.p, I, ell, Q.p);
     }
@@ -767,6 +797,9 @@ rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int6
       PhaseScope ps(c, PH_EIG, jj);
       srrqr(c, Q.p, I, ell, eta, S, A, swaps.p + n);
     }
+    res->ranks[n] = ell;
+    res->ell[n] = ell;
+    if (hosvd) continue;  // X itself is sketched for every mode; filtered once below
     // G_(n) <- P^T G_(n): keep the selected slices and renumber them 0..ell-1 (local nonzeros)
     int32_t *oidx[kMaxModes] = {nullptr};
     for (int k = 0; k < d; ++k) oidx[k] = ib[1 - cb].p + (size_t)k * nnz0;
@@ -776,8 +809,31 @@ rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int6
     }
     cb = 1 - cb;
     cur[n] = ell;
-    res->ranks[n] = ell;
-    res->ell[n] = ell;
+  }
+  if (hosvd) {  // core = X x_1 P_1^T ... x_d P_d^T: keep entries selected in every mode
+    PhaseScope ps(c, PH_SHRINK, 0);
+    CooDev g;
+    g.d = d;
+    for (int k = 0; k < d; ++k) {
+      g.dims[k] = X->dims[k];
+      g.idx[k] = ib[0].p + (size_t)k * nnz0;
+    }
+    g.nnz = nnz0;
+    g.vals = vb[0].p;
+    g.vt = vt;
+    const int64_t *sels[kMaxModes] = {nullptr};
+    int ls[kMaxModes] = {0};
+    int32_t *oidx[kMaxModes] = {nullptr};
+    for (int k = 0; k < d; ++k) {
+      sels[k] = res->selection[k];
+      ls[k] = (int)res->ranks[k];
+      oidx[k] = ib[1].p + (size_t)k * nnz0;
+      cur[k] = res->ranks[k];
+    }
+    coo_select_modes(c, g, hist.p, sels, ls, oidx, vb[1].p, hist.p + 1);
+    for (int k = 2; k <= d; ++k)
+      RT_CUDA(cudaMemcpyAsync(hist.p + k, hist.p + 1, sizeof(int64_t), cudaMemcpyDeviceToDevice, c.stream));
+    cb = 1;
   }
   // ---- one host synchronisation: nnz history (summed over the ranks), swaps, status
   DevBuf<int64_t> hsum(c, kMaxModes + 1);

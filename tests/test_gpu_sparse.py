@@ -121,6 +121,26 @@ def test_sparse_bit_reproducible_and_debug_checks(ctx):
     assert e.value.name == "EINVAL"
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_sp_hosvd(ctx, dtype):
+    """SP-HOSVD (NEXT-2): every mode selected on X, core = X x_j P_j^T (one filter by all
+    selections), against the oracle's sp_hosvd: selections, factors, core entries bit-exact."""
+    from paper_1905_07311_b200.rtucker import SP_HOSVD
+    idx, vals = sparse_zipf(dims=(800, 700, 20000, 120), ndraws=200_000, seed=6)
+    vals = vals.astype(dtype)
+    dims = (800, 700, 20000, 120)
+    g = _run(ctx, idx, vals, dims, (6, 6, 6, 6), 4, seed=2, flags=SP_HOSVD)
+    o = O.sp_hosvd(idx, vals, dims, (6, 6, 6, 6), 4, seed=2)
+    for j in range(4):
+        assert list(g.selections[j]) == list(o.selections[j]), j
+        err = np.linalg.norm(g.factors[j] - o.factors[j]) / np.linalg.norm(o.factors[j])
+        assert err <= (1e-9 if dtype == np.float64 else 1e-4), (j, err)
+    assert g.nnz_history[:2] == tuple(o.nnz_history)
+    gk, ok = np.lexsort(g.core_idx[::-1]), np.lexsort(o.core_idx[::-1])
+    np.testing.assert_array_equal(g.core_idx[:, gk], o.core_idx[:, ok])
+    np.testing.assert_array_equal(g.core_vals[gk], np.asarray(o.core_vals)[ok])
+
+
 def test_sparse_invalid(ctx):
     from paper_1905_07311_b200.rtucker import RTuckerError
     idx = np.array([[0, 1, 2], [0, 1, 2], [0, 1, 2]])
