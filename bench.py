@@ -51,6 +51,24 @@ def workload_config(algo, n):
             "data": "synthetic (workloads.odeco, data seed 4)"}
 
 
+def step_bytes(algo: str) -> int:
+    """Algorithmic HBM bytes of one step (SURVEY §8(d) d.4 conventions: one read per pass, B
+    written once and read once by the shrink; HYBRID policy: B and every shrunk intermediate in
+    fp64).  C4, r = 50, l = 60, rho = [1, 2, 3]."""
+    r, ell, n = RANKS[0], RANKS[0] + P, I
+    x = 4 * n ** 3
+    if algo == "sthosvd":
+        b1, g1 = 8 * ell * n * n, 8 * r * n * n           # mode 1: B (l, I, I), G1 (r, I, I)
+        b2, g2 = 8 * r * ell * n, 8 * r * r * n           # mode 2 on G1
+        b3, g3 = 8 * r * r * ell, 8 * r ** 3               # mode 3 on G2
+        return (2 * x + 2 * b1 + g1) + (2 * g1 + 2 * b2 + g2) + (2 * g2 + 2 * b3 + g3)
+    if algo == "hosvd":
+        b1, g1, g2, core = 8 * ell * n * n, 8 * r * n * n, 8 * r * r * n, 8 * r ** 3
+        # 3 sketches + 3 B-passes over X (B_1 written), core chain U_B1^T B_1 -> x_2 A_2^T -> x_3 A_3^T
+        return 6 * x + b1 + (b1 + g1) + (g1 + g2) + (g2 + core)
+    return 0
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -262,7 +280,8 @@ def main():
     ap.add_argument("--flags", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-phases", action="store_true", help="time without the per-phase events")
+    ap.add_argument("--no-phases", action="store_true", help="skip the separate per-phase profiling pass")
+    ap.add_argument("--no-graph", action="store_true", help="time eager calls instead of CUDA-graph replays")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -273,7 +292,7 @@ def main():
     import numpy as np
     import torch
     import torch.distributed as dist
-    from paper_1905_07311_b200.rtucker import Context, RESULT_HOST
+    from paper_1905_07311_b200.rtucker import Context, RESULT_HOST, GRAPH
     from workloads import odeco
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -307,13 +326,14 @@ def main():
     clocks = Clocks(local)
     clocks.start()
     time.sleep(1.0)
+    # fixed-rank calls replay one CUDA graph per step (RTUCKER_GRAPH: captured during the warm-up;
+    # the adaptive variant's ranks are data dependent, so it stays eager)
+    gflag = GRAPH if (args.algo in ("sthosvd", "hosvd") and not args.no_graph) else 0
     for _ in range(args.warmup):
-        step(x).free()
+        step(x, gflag).free()
     torch.cuda.synchronize()
 
     # ---- timed region: K steps, barrier + sync on both sides, CUDA events on the ctx stream
-    ctx.set_profiling(not args.no_phases)
-    ctx.phase_times(reset=True)
     clocks.mark()
     if world > 1:
         dist.barrier()
@@ -325,7 +345,7 @@ def main():
     results = []
     th0 = time.perf_counter()
     for _ in range(args.steps):
-        results.append(step(x))
+        results.append(step(x, gflag))
     host_ms = (time.perf_counter() - th0) * 1e3 / args.steps
     e1.record(stream)
     torch.cuda.synchronize()
@@ -335,10 +355,47 @@ def main():
     ms_local = e0.elapsed_time(e1) / args.steps
     print(f"[bench] host enqueue {host_ms:.3f} ms/step, device {ms_local:.3f} ms/step", file=sys.stderr)
     clk = clocks.stop()
-    phases = ctx.phase_times(reset=True)
-    ctx.set_profiling(False)
     for r in results:
         r.free()
+    # ---- the other fixed-rank algorithm of the BASELINE metric ("R-HOSVD/R-STHOSVD Gelem/s"):
+    # R-HOSVD on the same resident input, timed the same way (graph replays, events, max over ranks)
+    also = {}
+    if args.algo == "sthosvd":
+        hstep = lambda f: ctx.hosvd(x, (I, I, I), RANKS, P, SEED, f | args.flags, shard=shard)
+        for _ in range(args.warmup):
+            hstep(gflag).free()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        hres = [hstep(gflag) for _ in range(args.steps)]
+        h1.record(stream)
+        torch.cuda.synchronize()
+        for r in hres:
+            r.free()
+        hms = h0.elapsed_time(h1) / args.steps
+        if world > 1:
+            t = torch.tensor([hms], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            hms = float(t.item())
+        hb = step_bytes("hosvd") // world
+        also["R-HOSVD"] = {"metric": METRIC.replace("R-STHOSVD", "R-HOSVD"), "value": N_ELEM / (hms * 1e-3) / 1e9,
+                           "unit": "Gelem/s", "ms_per_step": hms,
+                           "step_roofline": {"bytes_per_step": hb, "achieved": hb / (hms * 1e-3) / 1e9,
+                                             "peak": peaks()[0], "unit": "GB/s",
+                                             "frac": hb / (hms * 1e-3) / 1e9 / peaks()[0]}}
+
+    # ---- per-phase CUDA events: a separate eager pass after the timed region (phase events
+    # cannot sit inside a graph replay); these give the per-kernel rooflines below
+    phases = {}
+    if not args.no_phases:
+        ctx.set_profiling(True)
+        ctx.phase_times(reset=True)
+        for _ in range(min(args.steps, 5)):
+            step(x).free()
+        phases = ctx.phase_times(reset=True)
+        ctx.set_profiling(False)
     ms = ms_local
     if world > 1:
         t = torch.tensor([ms_local], device="cuda")
@@ -392,6 +449,13 @@ def main():
                         "bound": "latency", "ms": t_e / len(eig), "ms_per_step": t_e,
                         "share_of_step": t_e / ms_local, "launches_per_step": len(eig)})
     dom = max((k for k in kernels if k["bound"] != "latency"), key=lambda k: k["ms"]) if kernels else None
+    sb = step_bytes(args.algo) // world
+    step_roof = None
+    if sb:
+        step_roof = {"bound": "hbm", "bytes_per_step": sb, "achieved": sb / (ms * 1e-3) / 1e9, "peak": hbm,
+                     "unit": "GB/s", "frac": sb / (ms * 1e-3) / 1e9 / hbm, "ideal_ms": sb / (hbm * 1e9) * 1e3,
+                     "model": "SURVEY d.4: one read of every input per pass, B written once / read once, "
+                              "HYBRID fp64 intermediates; small solves (QR, eig) not counted"}
     roofline = None
     if dom:
         roofline = {k: dom[k] for k in ("bound", "achieved", "peak", "unit", "frac", "traffic")}
@@ -439,8 +503,9 @@ def main():
             "value": value, "unit": "Gelem/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload_config(args.algo, world),
-            "roofline": roofline, "kernels": kernels,
-            "phase_ms": step_phase_ms,
+            "roofline": roofline, "step_roofline": step_roof, "kernels": kernels,
+            "phase_ms": step_phase_ms, "host_enqueue_ms_per_step": host_ms,
+            "graph_replay": bool(gflag), "also": also,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         }
         print(json.dumps(line), flush=True)

@@ -114,6 +114,13 @@ typedef enum { RTUCKER_DEVICE = 0, RTUCKER_HOST = 1 } rtucker_memory;
  * every mode is sketched and selected on X itself, and the core is X x_1 P_1^T ... x_d P_d^T,
  * one filter by all selections (order is ignored; nnz_history = [nnz(X), nnz(core)]). */
 #define RTUCKER_SP_HOSVD          (1u << 9)
+/* Fixed-rank calls (rtucker_hosvd / rtucker_sthosvd, device result): replay the whole call as one
+ * CUDA graph.  The first call with a given (input pointer, shape, ranks, p, seed, order, flags)
+ * runs eagerly, sizes a workspace arena and captures the call; later identical calls launch the
+ * graph and copy core, factors and residuals into a fresh result (host enqueue ~ one graph launch
+ * plus a few copies).  The context keeps the arena and the graph until it is destroyed.
+ * Ignored with RTUCKER_RESULT_HOST or while phase profiling is on. */
+#define RTUCKER_GRAPH             (1u << 10)
 
 /* Dense tensor, first-mode-fastest.  When the tensor is sharded across ranks along its
  * LAST mode, dims[] are the GLOBAL dims and this rank holds the contiguous slab of

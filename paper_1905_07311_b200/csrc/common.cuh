@@ -76,6 +76,15 @@ struct Ctx {
   void *alloc_user = nullptr;
   cudaMemPool_t pool = nullptr;
   unsigned *status = nullptr;       // device status word (StatusBit)
+  // CUDA-graph mode of the fixed-rank calls (RTUCKER_GRAPH): while a call is captured, device
+  // allocations come from a bump arena sized by a counting eager run, and frees are no-ops
+  struct Arena {
+    char *base = nullptr;
+    size_t size = 0, off = 0, counted = 0;
+    bool on = false, counting = false;
+  } arena;
+  bool capturing = false;
+  void *graphs = nullptr;           // graph plan cache (rtucker.cu)
   bool deterministic = true;        // fixed-order reductions (RTUCKER_NONDETERMINISTIC clears)
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -129,6 +138,14 @@ struct PhaseScope {
 inline void *dev_alloc(Ctx &c, size_t bytes) {
   if (bytes == 0) bytes = 16;
   void *p = nullptr;
+  const size_t aligned = (bytes + 255) & ~(size_t)255;
+  if (c.arena.on) {
+    if (c.arena.off + aligned > c.arena.size) throw Error(RTUCKER_ENOMEM, "graph arena exhausted");
+    p = c.arena.base + c.arena.off;
+    c.arena.off += aligned;
+    return p;
+  }
+  if (c.arena.counting) c.arena.counted += aligned;
   if (c.alloc_fn) {
     p = c.alloc_fn(bytes, (void *)c.stream, c.alloc_user);
     if (!p) throw Error(RTUCKER_ENOMEM, "allocation hook returned NULL");
@@ -144,6 +161,7 @@ inline void *dev_alloc(Ctx &c, size_t bytes) {
 }
 inline void dev_free(Ctx &c, void *p) {
   if (!p) return;
+  if (c.arena.base && (char *)p >= c.arena.base && (char *)p < c.arena.base + c.arena.size) return;
   if (c.free_fn) c.free_fn(p, (void *)c.stream, c.alloc_user);
   else cudaFreeAsync(p, c.stream);
 }

@@ -191,6 +191,7 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
   res->core = dev_alloc(c, sizeof(double) * ncore);
   convert(c, G, gt, res->core, DT::F64, ncore);
   copy_residuals(c, res, scal.p, d, ord[0]);
+  if (c.capturing) res->internal = scal.p;  // graph template: the residual block lives in the arena
   finish_result(c, res, flags);
   return rg.release();
 }
@@ -317,6 +318,7 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
     convert(c, G, gt, res->core, DT::F64, ncore);
   }
   copy_residuals(c, res, scal.p, d, 0);
+  if (c.capturing) res->internal = scal.p;
   finish_result(c, res, flags);
   return rg.release();
 }

@@ -25,6 +25,10 @@ void finish_result(Ctx &c, rtucker_result *r, uint32_t flags);
 // Synchronises the context stream, reads and clears the device status word (StatusBit) and
 // throws the matching error.
 void check_status(Ctx &c);
+// Fixed-rank entry (algo 0 = R-STHOSVD, 1 = R-HOSVD), with the RTUCKER_GRAPH replay path.
+rtucker_result *run_fixed_rank(Ctx &c, int algo, const rtucker_dense_desc *X, const int64_t *ranks, int p,
+                               uint64_t seed, const int32_t *order, uint32_t flags);
+void destroy_graphs(Ctx &c);
 
 // Global unfolding-column offset of this rank's slab for mode n < d-1 (the last mode is
 // sharded): c_glob = c_loc + offset * prod_{k != n, k < d-1} dims_k.

@@ -200,6 +200,161 @@ void finish_result(Ctx &c, rtucker_result *r, uint32_t flags) {
   check_status(c);  // synchronises
 }
 
+// ------------------------------------------------------------- CUDA-graph plans ----
+// RTUCKER_GRAPH for the fixed-rank calls (include/rtucker.h).  A plan is keyed by everything the
+// enqueued work depends on; its template result points into the plan's arena (core, factors)
+// and its `internal` field at the device residual block (2 d doubles: ||G||^2, residual per mode).
+struct GraphPlan {
+  std::vector<int64_t> key;
+  cudaGraphExec_t exec = nullptr;
+  char *arena = nullptr;
+  size_t arena_size = 0;
+  rtucker_result *tmpl = nullptr;
+  uint64_t launches = 0;
+};
+struct GraphCache {
+  std::vector<GraphPlan *> plans;
+};
+
+static std::vector<int64_t> plan_key(int algo, const rtucker_dense_desc *X, const int64_t *ranks, int p, uint64_t seed,
+                                     const int32_t *order, uint32_t flags, const Ctx &c) {
+  std::vector<int64_t> k = {algo, (int64_t)(uintptr_t)X->data, X->dtype, X->d, X->shard_offset, X->shard_extent,
+                            X->memory, p, (int64_t)seed, (int64_t)(flags & ~RTUCKER_GRAPH), c.nranks,
+                            c.loopback_sharding ? 1 : 0};
+  for (int i = 0; i < X->d && i < kMaxModes; ++i) {
+    k.push_back(X->dims[i]);
+    k.push_back(ranks[i]);
+    k.push_back(order ? order[i] : -1);
+  }
+  return k;
+}
+
+void destroy_graphs(Ctx &c) {
+  auto *gc = (GraphCache *)c.graphs;
+  if (!gc) return;
+  for (GraphPlan *pl : gc->plans) {
+    if (pl->exec) cudaGraphExecDestroy(pl->exec);
+    if (pl->arena) cudaFree(pl->arena);
+    if (pl->tmpl) {
+      std::lock_guard<std::mutex> lk(g_result_mu);
+      g_result_free.push_back(pl->tmpl);
+    }
+    delete pl;
+  }
+  delete gc;
+  c.graphs = nullptr;
+}
+
+rtucker_result *run_fixed_rank(Ctx &c, int algo, const rtucker_dense_desc *X, const int64_t *ranks, int p,
+                               uint64_t seed, const int32_t *order, uint32_t flags) {
+  auto body = [&]() {
+    return algo == 0 ? run_sthosvd(c, X, ranks, p, seed, order, flags) : run_hosvd(c, X, ranks, p, seed, flags);
+  };
+  if (!(flags & RTUCKER_GRAPH) || (flags & RTUCKER_RESULT_HOST) || c.profiling || !X || !ranks ||
+      X->memory != RTUCKER_DEVICE || X->d < 1 || X->d > kMaxModes)
+    return body();
+  if (!c.graphs) c.graphs = new GraphCache;
+  auto *gc = (GraphCache *)c.graphs;
+  const std::vector<int64_t> key = plan_key(algo, X, ranks, p, seed, order, flags, c);
+  GraphPlan *pl = nullptr;
+  for (GraphPlan *q : gc->plans)
+    if (q->key == key) pl = q;
+  if (pl && !pl->exec) return body();  // capture failed earlier for this key
+  if (!pl) {
+    // 1. eager call (its result is returned) counting the workspace it allocates
+    c.arena = Ctx::Arena{};
+    c.arena.counting = true;
+    rtucker_result *res = nullptr;
+    try {
+      res = body();
+    } catch (...) {
+      c.arena = Ctx::Arena{};
+      throw;
+    }
+    const size_t need = c.arena.counted + (1 << 20);
+    c.arena = Ctx::Arena{};
+    // 2. capture the same call with the arena allocator
+    auto *np = new GraphPlan;
+    np->key = key;
+    np->arena_size = need;
+    cudaError_t e = cudaMalloc((void **)&np->arena, need);
+    if (e != cudaSuccess) {  // no room for a plan: stay eager
+      (void)cudaGetLastError();
+      delete np;
+      return res;
+    }
+    c.arena.base = np->arena;
+    c.arena.size = need;
+    c.arena.on = true;
+    c.capturing = true;
+    const uint64_t l0 = c.launches;
+    cudaGraph_t g = nullptr;
+    rtucker_result *tmpl = nullptr;
+    try {
+      RT_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeRelaxed));
+      tmpl = body();
+      RT_CUDA(cudaStreamEndCapture(c.stream, &g));
+      RT_CUDA(cudaGraphInstantiate(&np->exec, g, 0));
+    } catch (const std::exception &ex) {
+      cudaGraph_t junk = nullptr;
+      cudaStreamEndCapture(c.stream, &junk);
+      if (junk) cudaGraphDestroy(junk);
+      if (g) cudaGraphDestroy(g);
+      c.capturing = false;
+      c.arena = Ctx::Arena{};
+      cudaFree(np->arena);
+      np->arena = nullptr;
+      (void)cudaGetLastError();
+      // capture failed: the eager result stands; the key stays as an eager-only plan (no retry)
+      fprintf(stderr, "[rtucker] RTUCKER_GRAPH: capture failed, calls with this key stay eager: %s\n", ex.what());
+      gc->plans.push_back(np);
+      return res;
+    }
+    cudaGraphDestroy(g);
+    np->launches = c.launches - l0;
+    c.launches = l0;
+    c.capturing = false;
+    c.arena = Ctx::Arena{};
+    np->tmpl = tmpl;
+    gc->plans.push_back(np);
+    return res;
+  }
+  // 3. replay: one graph launch, then the outputs are copied into a fresh result
+  RT_CUDA(cudaGraphLaunch(pl->exec, c.stream));
+  c.launches += pl->launches;
+  const rtucker_result *t = pl->tmpl;
+  ResultGuard rg{c, new_result(t->d)};
+  rtucker_result *r = rg.r;
+  memcpy(r->dims, t->dims, sizeof r->dims);
+  memcpy(r->ranks, t->ranks, sizeof r->ranks);
+  memcpy(r->ell, t->ell, sizeof r->ell);
+  memcpy(r->order, t->order, sizeof r->order);
+  r->seed = t->seed;
+  r->flags = flags;
+  r->dtype = t->dtype;
+  int64_t ncore = 1;
+  for (int k = 0; k < t->d; ++k) ncore *= t->ranks[k];
+  if (t->core) {
+    r->core = dev_alloc(c, sizeof(double) * ncore);
+    RT_CUDA(cudaMemcpyAsync(r->core, t->core, sizeof(double) * ncore, cudaMemcpyDeviceToDevice, c.stream));
+  }
+  for (int k = 0; k < t->d; ++k) {
+    if (!t->factors[k]) continue;
+    const size_t b = sizeof(double) * t->dims[k] * t->ranks[k];
+    r->factors[k] = dev_alloc(c, b);
+    RT_CUDA(cudaMemcpyAsync(r->factors[k], t->factors[k], b, cudaMemcpyDeviceToDevice, c.stream));
+  }
+  if (t->internal) {  // residual block: [||G||^2 at 2n, residual at 2n+1]
+    const double *scal = (const double *)t->internal;
+    for (int k = 0; k < t->d; ++k)
+      RT_CUDA(cudaMemcpyAsync(&r->mode_residual_sq[k], scal + 2 * k + 1, sizeof(double), cudaMemcpyDeviceToHost,
+                              c.stream));
+    const int first = algo == 0 ? t->order[0] : 0;
+    RT_CUDA(cudaMemcpyAsync(&r->norm_sq, scal + 2 * first, sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  }
+  return rg.release();
+}
+
 }  // namespace rt
 
 // ======================================================================= C ABI ======
@@ -319,6 +474,7 @@ rtucker_status rtucker_ctx_create(int device, void *cuda_stream, const void *ncc
 void rtucker_ctx_destroy(rtucker_ctx *ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->c.stream);
+  destroy_graphs(ctx->c);
   if (ctx->c.sk_flags) cudaFree(ctx->c.sk_flags);
   if (ctx->c.status) cudaFree(ctx->c.status);
   comm_destroy(ctx->c.comm);
@@ -356,7 +512,7 @@ rtucker_status rtucker_hosvd(rtucker_ctx *ctx, const rtucker_dense_desc *X, cons
                              int32_t p, uint64_t seed, uint32_t flags, rtucker_result **out) {
   if (!ctx || !out || !ranks) return RTUCKER_EINVAL;
   *out = nullptr;
-  return guard(ctx, [&] { *out = run_hosvd(ctx->c, X, ranks, p, seed, flags); });
+  return guard(ctx, [&] { *out = run_fixed_rank(ctx->c, 1, X, ranks, p, seed, nullptr, flags); });
 }
 
 rtucker_status rtucker_sthosvd(rtucker_ctx *ctx, const rtucker_dense_desc *X, const int64_t *ranks,
@@ -364,7 +520,7 @@ rtucker_status rtucker_sthosvd(rtucker_ctx *ctx, const rtucker_dense_desc *X, co
                                rtucker_result **out) {
   if (!ctx || !out || !ranks) return RTUCKER_EINVAL;
   *out = nullptr;
-  return guard(ctx, [&] { *out = run_sthosvd(ctx->c, X, ranks, p, seed, order, flags); });
+  return guard(ctx, [&] { *out = run_fixed_rank(ctx->c, 0, X, ranks, p, seed, order, flags); });
 }
 
 rtucker_status rtucker_adaptive(rtucker_ctx *ctx, const rtucker_dense_desc *X, double tol, int32_t block,

@@ -1044,6 +1044,8 @@ void launch_ttm_dfma(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t 
       c.sk_n = sk_grid;
     }
     if (++c.sk_epoch == 0) ++c.sk_epoch;  // 0 is the initial flag value
+    // a captured launch replays with the same epoch: reset the flags inside the graph
+    if (c.capturing) RT_CUDA(cudaMemsetAsync(c.sk_flags, 0, sizeof(unsigned) * sk_grid, c.stream));
     DevBuf<double> fix(c, (size_t)sk_grid * 64 * kDT);
     if (gram) part.alloc(c, (size_t)sk_grid * 4096);
     const size_t smem = std::max(sizeof(double) * (kDP * kMX + kDK * kMA), sizeof(double) * 128 * kTS);

@@ -32,6 +32,7 @@ NO_CORE = 1 << 6
 DETERMINISTIC = 1 << 7
 DEBUG_CHECKS = 1 << 8
 SP_HOSVD = 1 << 9
+GRAPH = 1 << 10
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)

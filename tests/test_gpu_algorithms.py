@@ -186,6 +186,30 @@ def test_allocator_hooks_bit_identical():
         np.testing.assert_array_equal(fa, fb)
 
 
+@pytest.mark.parametrize("algo", ["sthosvd", "hosvd"])
+def test_graph_replay_bit_identical(ctx, algo):
+    """RTUCKER_GRAPH: the first call runs eagerly and captures the call; replays launch the CUDA
+    graph and copy the outputs out.  Every replay must equal the eager result bit for bit, the
+    residuals included; a different input pointer builds its own plan."""
+    import torch
+    from paper_1905_07311_b200.rtucker import GRAPH
+    x = odeco(96, seed=4, dtype=np.float32)          # HYBRID path incl. the stream-K fp64 kernels
+    xd = torch.as_tensor(to_first_mode_fastest(x), device="cuda")
+    call = (lambda f: ctx.sthosvd(xd, x.shape, (12, 12, 12), 10, 1, (0, 1, 2), f)) if algo == "sthosvd" else \
+           (lambda f: ctx.hosvd(xd, x.shape, (12, 12, 12), 10, 1, f))
+    ref = call(0).numpy()
+    outs = [call(GRAPH).numpy() for _ in range(3)]
+    for o in outs:
+        np.testing.assert_array_equal(o.core, ref.core)
+        for a, b in zip(o.factors, ref.factors):
+            np.testing.assert_array_equal(a, b)
+        assert o.mode_residual_sq == ref.mode_residual_sq and o.norm_sq == ref.norm_sq
+    x2 = xd.clone() * 2
+    o2 = (ctx.sthosvd(x2, x.shape, (12, 12, 12), 10, 1, (0, 1, 2), GRAPH) if algo == "sthosvd" else
+          ctx.hosvd(x2, x.shape, (12, 12, 12), 10, 1, GRAPH)).numpy()
+    np.testing.assert_allclose(o2.core, 2 * ref.core, rtol=1e-12, atol=1e-14)
+
+
 def test_rel_error_on_device(ctx):
     import torch
     x = hilbert((50, 50, 50), "shifted")
