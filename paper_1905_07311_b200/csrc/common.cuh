@@ -85,6 +85,7 @@ struct Ctx {
   } arena;
   bool capturing = false;
   void *graphs = nullptr;           // graph plan cache (rtucker.cu)
+  cudaStream_t aux = nullptr;       // side stream for the small solves of R-HOSVD (overlap)
   bool deterministic = true;        // fixed-order reductions (RTUCKER_NONDETERMINISTIC clears)
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -172,6 +173,22 @@ void set_smem_attr(const void *func, size_t bytes);
 template <typename F>
 inline void smem_attr(F *func, size_t bytes) {
   set_smem_attr((const void *)func, bytes);
+}
+
+// Runs the enclosed work on another stream of the context (restores the main stream on exit).
+struct OnStream {
+  Ctx &c;
+  cudaStream_t saved;
+  OnStream(Ctx &ctx, cudaStream_t s) : c(ctx), saved(ctx.stream) { c.stream = s; }
+  ~OnStream() { c.stream = saved; }
+};
+// Event recorded on `from`, waited on by `to` (fork / join; captured into graphs as edges).
+inline void stream_dep(cudaStream_t from, cudaStream_t to) {
+  cudaEvent_t e;
+  RT_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  RT_CUDA(cudaEventRecord(e, from));
+  RT_CUDA(cudaStreamWaitEvent(to, e, 0));
+  RT_CUDA(cudaEventDestroy(e));
 }
 
 // Count every library kernel launch (reported as gpu_launches by bench.py).

@@ -217,7 +217,88 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
   DevBuf<double> U1;
   int ell1 = 0;
 
-  for (int n = 0; n < d; ++n) {
+  // Unsharded: the d modes are independent (Alg 2), so the small solves of mode n (QR after its
+  // sketch, eigensolve after its B-pass: one CTA / cluster each) run on the context's side
+  // stream while the main stream streams the next mode's sketch / B-pass over X.  Only the last
+  // mode's QR and eigensolve stay exposed.  Event edges order the two streams (and become graph
+  // edges under RTUCKER_GRAPH).
+  const bool overlap = !in.sharded && d > 1 && c.aux;
+  if (overlap) {
+    // the persistent streaming kernels size their grids by c.num_sms: leave 4 SMs to the side
+    // stream (a QR cluster of <= 4 CTAs, or one eigensolver CTA), restored at the join
+    struct SmReserve {
+      Ctx &c;
+      int saved;
+      explicit SmReserve(Ctx &cc) : c(cc), saved(cc.num_sms) { c.num_sms = std::max(8, c.num_sms - 4); }
+      ~SmReserve() { c.num_sms = saved; }
+    } reserve(c);
+    DevBuf<double> Ys[kMaxModes], Qs[kMaxModes], grams[kMaxModes], ws[kMaxModes], Vs[kMaxModes];
+    DevBuf<uint32_t> cms[kMaxModes];
+    int ells[kMaxModes], rrs[kMaxModes];
+    cudaEvent_t qdone[kMaxModes];  // Q_n ready on the side stream
+    for (int n = 0; n < d; ++n) RT_CUDA(cudaEventCreateWithFlags(&qdone[n], cudaEventDisableTiming));
+    for (int n = 0; n < d; ++n) {  // sketches on the main stream, QRs on the side stream
+      rank_caps(in.gdims, d, n, ranks[n], p, flags & RTUCKER_STRICT, ells[n], rrs[n]);
+      const int ell = ells[n];
+      const ModeView v = mode_view(in.ldims, d, n);
+      const int64_t Ig = in.gdims[n];
+      Ys[n].alloc(c, (size_t)Ig * ell + 1);
+      if (in.dt == DT::F32 && !pol.mul_f64 && (v.L == 1 || (v.L % 4) == 0) && ozaki_bpass_enabled()) {
+        cms[n].alloc(c, (size_t)(v.L * v.R));
+        cms[n].zero();
+      }
+      Qs[n].alloc(c, (size_t)Ig * ell);
+      grams[n].alloc(c, (size_t)ell * ell);
+      ws[n].alloc(c, ell);
+      Vs[n].alloc(c, (size_t)ell * ell);
+      {
+        PhaseScope ps(c, PH_SKETCH, n);
+        sketch_dense(c, in.ptr, in.dt, v, n, ell, 0, seed, 0, pol.mul_f64, Ys[n].p, Ys[n].p + Ig * ell,
+                     in.dt == DT::F32 && !pol.mul_f64, cms[n].p);
+        RT_CUDA(cudaMemcpyAsync(scal.p + 2 * n, Ys[n].p + Ig * ell, sizeof(double), cudaMemcpyDeviceToDevice,
+                                c.stream));
+      }
+      stream_dep(c.stream, c.aux);
+      OnStream os(c, c.aux);
+      PhaseScope ps(c, PH_QR, n);
+      thin_qr(c, Ys[n].p, Ig, ell, Qs[n].p);
+      RT_CUDA(cudaEventRecord(qdone[n], c.stream));
+    }
+    for (int n = 0; n < d; ++n) {  // B-passes on the main stream, eigensolves on the side stream
+      const int ell = ells[n], rr = rrs[n];
+      const ModeView v = mode_view(in.ldims, d, n);
+      const int64_t Ig = in.gdims[n];
+      RT_CUDA(cudaStreamWaitEvent(c.stream, qdone[n], 0));  // Q_n ready (not the earlier eigensolves)
+      {
+        PhaseScope ps(c, PH_BPASS, n);
+        if (n == 0 && keep_b1) {
+          B1.alloc(c, (size_t)v.L * ell * v.R * dt_size(pol.store));
+          ttm_dense(c, in.ptr, in.dt, v, Qs[n].p, Ig, ell, B1.p, pol.store, pol.mul_f64, grams[n].p, cms[n].p);
+        } else {
+          ttm_dense(c, in.ptr, in.dt, v, Qs[n].p, Ig, ell, nullptr, pol.store, pol.mul_f64, grams[n].p, cms[n].p);
+        }
+      }
+      double *A = (double *)dev_alloc(c, sizeof(double) * Ig * rr);
+      res->factors[n] = A;
+      if (n == 0 && keep_b1) U1.alloc(c, (size_t)ell * rr);
+      stream_dep(c.stream, c.aux);
+      OnStream os(c, c.aux);
+      PhaseScope ps(c, PH_EIG, n);
+      gram_eig(c, grams[n].p, ell, ws[n].p, Vs[n].p, nullptr, rr, in.dt == DT::F64);
+      gemm_small(c, false, Qs[n].p, Ig, Vs[n].p, ell, A, Ig, Ig, rr, ell);
+      canonical_signs(c, A, Ig, rr, Vs[n].p, ell, ell);  // reading R4b (shrink uses the signed U_B)
+      residual_from_eigs(c, ws[n].p, rr, scal.p + 2 * n, scal.p + 2 * n + 1);
+      if (n == 0 && keep_b1) {
+        RT_CUDA(cudaMemcpyAsync(U1.p, Vs[n].p, sizeof(double) * ell * rr, cudaMemcpyDeviceToDevice, c.stream));
+        ell1 = ell;
+      }
+      res->ranks[n] = rr;
+      res->ell[n] = ell;
+    }
+    stream_dep(c.aux, c.stream);  // join: factors, U_B1 and residuals ready; buffers freed after
+    for (int n = 0; n < d; ++n) RT_CUDA(cudaEventDestroy(qdone[n]));
+  }
+  for (int n = 0; n < d && !overlap; ++n) {
     int ell, rr;
     rank_caps(in.gdims, d, n, ranks[n], p, flags & RTUCKER_STRICT, ell, rr);
     const ModeView v = mode_view(in.ldims, d, n);

@@ -445,6 +445,7 @@ rtucker_status rtucker_ctx_create(int device, void *cuda_stream, const void *ncc
       ctx->c.own_stream = true;
     }
     RT_CUDA(cudaDeviceGetAttribute(&ctx->c.num_sms, cudaDevAttrMultiProcessorCount, device));
+    RT_CUDA(cudaStreamCreateWithFlags(&ctx->c.aux, cudaStreamNonBlocking));
     // library-owned stream-ordered pool (used when no allocation hooks are given); freed
     // workspace stays in it between calls (no re-mapping of the large B / shrunk-core
     // buffers on every decomposition).  The device's default pool is not modified.
@@ -475,6 +476,10 @@ void rtucker_ctx_destroy(rtucker_ctx *ctx) {
   if (!ctx) return;
   cudaStreamSynchronize(ctx->c.stream);
   destroy_graphs(ctx->c);
+  if (ctx->c.aux) {
+    cudaStreamSynchronize(ctx->c.aux);
+    cudaStreamDestroy(ctx->c.aux);
+  }
   if (ctx->c.sk_flags) cudaFree(ctx->c.sk_flags);
   if (ctx->c.status) cudaFree(ctx->c.status);
   comm_destroy(ctx->c.comm);
