@@ -190,6 +190,17 @@ def oracle_sample_input(slabs: int):
     return x.reshape((I, I, slabs), order="F")
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def cpu_oracle_sample(slabs: int = 300, x=None):
     """The oracle (oracle/, fp64 numpy) as it stands on a bounded sample of the workload:
     R-STHOSVD of the first `slabs` mode-3 slabs of C4 (800 x 800 x slabs), same ranks."""
@@ -198,7 +209,9 @@ def cpu_oracle_sample(slabs: int = 300, x=None):
     t0 = time.perf_counter()
     O.r_sthosvd(x, (50, 50, min(50, slabs)), P, SEED, ORDER)
     dt = time.perf_counter() - t0
-    return x.size / dt / 1e9, dt, f"oracle r_sthosvd on C4[:, :, :{slabs}] (800x800x{slabs}, {x.size} elem)"
+    return x.size / dt / 1e9, dt, (f"oracle r_sthosvd on C4[:, :, :{slabs}] (800x800x{slabs}, {x.size} elem); "
+                                   "reported as elements/s of the sample (every pass of the oracle is linear in "
+                                   "the number of mode-3 slabs, so the rate extrapolates to the full 800^3)")
 
 
 def run_reference(args):
@@ -220,27 +233,36 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args.algo, args.gpus),
-            "cpu_baseline": {"value": v, "unit": "Gelem/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "Gelem/s", "cores": cores, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": "Gelem/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def bench_sparse(args):
     """SP-STHOSVD (Alg 6) of BASELINE configs[4] (C5: 4-mode Zipf(1.1) counts, 50M draws ->
-    ~40.7M nnz, r = 10, p = 5), COO resident in HBM; metric = input nnz / step time.  Single GPU
-    (the nnz-partitioned multi-GPU path is not built yet: DESIGN §12)."""
+    ~40.7M nnz, r = 10, p = 5), COO resident in HBM; metric = input nnz / step time.  With N > 1
+    ranks the nonzeros are partitioned into N contiguous ranges; the partial
+    sketches are summed exactly (integer allreduce), the selection runs redundantly, every rank
+    filters its own nonzeros."""
     import numpy as np
     import torch
+    import torch.distributed as dist
     from paper_1905_07311_b200.rtucker import Context
     from workloads import sparse_zipf
-    if int(os.environ.get("RANK", "0")) != 0:
-        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dims = (8000, 8000, 200000, 1200)
     idx, vals = sparse_zipf()
-    it = torch.as_tensor(idx, device="cuda")
-    vt = torch.as_tensor(vals, device="cuda")
+    lo, hi = rank * idx.shape[1] // world, (rank + 1) * idx.shape[1] // world
+    it = torch.as_tensor(np.ascontiguousarray(idx[:, lo:hi]), device="cuda")
+    vt = torch.as_tensor(np.ascontiguousarray(vals[lo:hi]), device="cuda")
     stream = torch.cuda.Stream()
-    ctx = Context(0, stream=stream)
+    ctx = Context(local, stream=stream, group=dist.group.WORLD if world > 1 else None)
     step = lambda: ctx.sparse_sthosvd(it, vt, dims, (10, 10, 10, 10), 5, SEED, None, 2.0)
     for _ in range(args.warmup):
         step().free()
@@ -249,6 +271,9 @@ def bench_sparse(args):
     ctx.phase_times(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = ctx.launches
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
     e0.record(stream)
     hist = None
     for _ in range(args.steps):
@@ -258,16 +283,25 @@ def bench_sparse(args):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank != 0:
+        dist.destroy_process_group()
+        return
     phases = {f"{k[0]}{k[1] + 1}": round(v[0] / max(v[1], 1), 4) for k, v in sorted(ctx.phase_times().items())}
     nnz = idx.shape[1]
     line = {"metric": "SP-STHOSVD Gnnz/s (C5 8000x8000x200000x1200, 50M Zipf(1.1) draws, r=10, p=5)",
-            "value": nnz / (ms * 1e-3) / 1e9, "unit": "Gnnz/s", "n_gpus": 1, "steps": args.steps,
+            "value": nnz / (ms * 1e-3) / 1e9, "unit": "Gnnz/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32 values, fp64 sketch sums", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f32 values, fixed-point (int64) sketch sums", "data": "synthetic",
             "config": {"workload": "C5 sparse_zipf data seed 5, SP-STHOSVD rho=auto [3,1,2,4], eta=2",
                        "nnz": nnz, "nnz_chain": hist},
             "phase_ms": phases, "gpu_launches": (ctx.launches - l0) // args.steps}
     print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
@@ -496,7 +530,8 @@ def main():
         if not args.no_cpu_baseline:
             v, dt, sample = cpu_oracle_sample(300)
             cpu = {"value": v, "unit": "Gelem/s", "cores": os.cpu_count(), "kind": "oracle", "sample": sample,
-                   "seconds": dt}
+                   "seconds": dt, "cpu_model": cpu_model(),
+                   "threads": "numpy/OpenBLAS default (all host cores)"}
         line = {
             "metric": {"sthosvd": METRIC, "hosvd": METRIC.replace("R-STHOSVD", "R-HOSVD"),
                        "adaptive": "adaptive R-STHOSVD Gelem/s (C4 800^3 fp32, tol 1e-3, block 10)"}[args.algo],

@@ -475,82 +475,91 @@ __device__ __forceinline__ bool keep_entry(const CooDev &in, const LutSet &ls, i
   return true;
 }
 
-__global__ void compact_count(CooDev in, const int64_t *__restrict__ nnz_dev, LutSet ls,
-                              int64_t *__restrict__ counts) {
-  __shared__ int64_t sc[32];
-  const int64_t nnz = *nnz_dev;
-  const int64_t e = (int64_t)blockIdx.x * kCompactB + threadIdx.x;
-  if ((int64_t)blockIdx.x * kCompactB >= nnz) {
-    if (threadIdx.x == 0) counts[blockIdx.x] = 0;
-    return;
-  }
-  const int keep = (e < nnz && keep_entry(in, ls, e)) ? 1 : 0;
-  const unsigned bal = __ballot_sync(0xffffffffu, keep);
-  if ((threadIdx.x & 31) == 0) sc[threadIdx.x >> 5] = __popc(bal);
+// Order-preserving compaction with a fixed grid: CTA b owns the contiguous range
+// [b chunk, (b+1) chunk) of the live nonzeros (chunk from the live nnz on the device), counts its
+// survivors, a one-CTA scan turns the per-CTA counts into offsets, and the scatter pass re-walks
+// the range in 1024-entry steps with a running offset.  The grid does not depend on the live nnz,
+// so nothing waits for the host.
+constexpr int kCompactG = 1024;  // max CTAs
+__device__ __forceinline__ void compact_range(int64_t nnz, int64_t &b0, int64_t &b1) {
+  const int64_t chunk = ((nnz + gridDim.x - 1) / gridDim.x + kCompactB - 1) / kCompactB * kCompactB;
+  b0 = min(nnz, (int64_t)blockIdx.x * chunk);
+  b1 = min(nnz, b0 + chunk);
+}
+
+__global__ void __launch_bounds__(kCompactB) compact_count(CooDev in, const int64_t *__restrict__ nnz_dev, LutSet ls,
+                                                           int64_t *__restrict__ counts) {
+  __shared__ int sc[32];
+  int64_t b0, b1;
+  compact_range(*nnz_dev, b0, b1);
+  int mine = 0;
+  for (int64_t e = b0 + threadIdx.x; e < b1; e += kCompactB) mine += keep_entry(in, ls, e) ? 1 : 0;
+  for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0) sc[threadIdx.x >> 5] = mine;
   __syncthreads();
   if (threadIdx.x == 0) {
-    int64_t s = 0;
-    for (int w = 0; w < kCompactB / 32; ++w) s += sc[w];
-    counts[blockIdx.x] = s;
+    int64_t t = 0;
+    for (int w = 0; w < kCompactB / 32; ++w) t += sc[w];
+    counts[blockIdx.x] = t;
   }
 }
 
-// One CTA: per-thread chunk sums, a serial scan of the chunk sums, then the chunks.
+// One CTA: exclusive scan of n <= kCompactG values (thread t owns entry t), total to *total.
 __global__ void exclusive_scan_single(int64_t *__restrict__ v, int64_t n, int64_t *__restrict__ total) {
-  __shared__ int64_t part[1024];
-  const int64_t per = (n + blockDim.x - 1) / blockDim.x;
-  const int64_t b = threadIdx.x * per, e = min(n, b + per);
-  int64_t s = 0;
-  for (int64_t k = b; k < e; ++k) s += v[k];
-  part[threadIdx.x] = s;
+  __shared__ int64_t sh[kCompactG];
+  const int t = threadIdx.x;
+  const int64_t x = t < n ? v[t] : 0;
+  sh[t] = x;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int64_t acc = 0;
-    for (int t = 0; t < (int)blockDim.x; ++t) {
-      const int64_t x = part[t];
-      part[t] = acc;
-      acc += x;
-    }
-    *total = acc;
+  for (int o = 1; o < (int)blockDim.x; o <<= 1) {  // Hillis-Steele inclusive scan
+    const int64_t y = t >= o ? sh[t - o] : 0;
+    __syncthreads();
+    sh[t] += y;
+    __syncthreads();
   }
-  __syncthreads();
-  int64_t acc = part[threadIdx.x];
-  for (int64_t k = b; k < e; ++k) {
-    const int64_t x = v[k];
-    v[k] = acc;
-    acc += x;
-  }
+  if (t < n) v[t] = sh[t] - x;
+  if (t == (int)blockDim.x - 1) *total = sh[t];
 }
 
 template <typename TV>
-__global__ void compact_scatter(CooDev in, const int64_t *__restrict__ nnz_dev, LutSet ls,
-                                const int64_t *__restrict__ offs, int32_t *const *__restrict__ oidx,
-                                TV *__restrict__ ovals) {
+__global__ void __launch_bounds__(kCompactB) compact_scatter(CooDev in, const int64_t *__restrict__ nnz_dev, LutSet ls,
+                                                             const int64_t *__restrict__ offs,
+                                                             int32_t *const *__restrict__ oidx, TV *__restrict__ ovals) {
   __shared__ int wsum[32];
-  const int64_t nnz = *nnz_dev;
-  if ((int64_t)blockIdx.x * kCompactB >= nnz) return;
-  const int64_t e = (int64_t)blockIdx.x * kCompactB + threadIdx.x;
-  const int keep = (e < nnz && keep_entry(in, ls, e)) ? 1 : 0;
-  const unsigned bal = __ballot_sync(0xffffffffu, keep);
+  __shared__ int64_t base;
+  int64_t b0, b1;
+  compact_range(*nnz_dev, b0, b1);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  if (lane == 0) wsum[w] = __popc(bal);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int k = 0; k < kCompactB / 32; ++k) {
-      const int x = wsum[k];
-      wsum[k] = acc;
-      acc += x;
+  if (threadIdx.x == 0) base = offs[blockIdx.x];
+  for (int64_t s0 = b0; s0 < b1; s0 += kCompactB) {
+    const int64_t e = s0 + threadIdx.x;
+    const int keep = (e < b1 && keep_entry(in, ls, e)) ? 1 : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    __syncthreads();  // base / wsum of the previous step consumed
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int k = 0; k < kCompactB / 32; ++k) {
+        const int x = wsum[k];
+        wsum[k] = acc;
+        acc += x;
+      }
+      wsum[31] += 0;
     }
+    __syncthreads();
+    const int64_t o = base + wsum[w] + __popc(bal & ((1u << lane) - 1u));
+    if (keep) {
+      for (int k = 0; k < in.d; ++k) {
+        const int32_t i = in.idx[k][e];
+        oidx[k][o] = ls.lut[k] ? ls.lut[k][i] : i;
+      }
+      ovals[o] = ((const TV *)in.vals)[e];
+    }
+    __syncthreads();
+    if (threadIdx.x == kCompactB - 1) base = o + (keep ? 1 : 0);  // last thread: offset after this step
+    __syncthreads();
   }
-  __syncthreads();
-  if (!keep) return;
-  const int64_t o = offs[blockIdx.x] + wsum[w] + __popc(bal & ((1u << lane) - 1u));
-  for (int k = 0; k < in.d; ++k) {
-    const int32_t i = in.idx[k][e];
-    oidx[k][o] = ls.lut[k] ? ls.lut[k][i] : i;
-  }
-  ovals[o] = ((const TV *)in.vals)[e];
 }
 
 __global__ void fill_i32(int32_t *p, int64_t n, int32_t v) {
@@ -684,10 +693,11 @@ void coo_select_modes(Ctx &c, const CooDev &in, const int64_t *nnz_dev, const in
     RT_LAUNCH(c, build_lookup, 1, 256, 0, sel[m], l[m], lut[m].p);
     ls.lut[m] = lut[m].p;
   }
-  const int64_t nblk = std::max<int64_t>(1, (in.nnz + kCompactB - 1) / kCompactB);
+  const int nblk = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)c.num_sms * 4, (int64_t)kCompactG,
+                                                                 (in.nnz + kCompactB - 1) / kCompactB}));
   DevBuf<int64_t> offs(c, nblk);
-  RT_LAUNCH(c, compact_count, (int)nblk, kCompactB, 0, in, nnz_dev, ls, offs.p);
-  RT_LAUNCH(c, exclusive_scan_single, 1, 1024, 0, offs.p, nblk, nnz_out);
+  RT_LAUNCH(c, compact_count, nblk, kCompactB, 0, in, nnz_dev, ls, offs.p);
+  RT_LAUNCH(c, exclusive_scan_single, 1, kCompactG, 0, offs.p, nblk, nnz_out);
   DevBuf<int32_t *> optr(c, kMaxModes);
   RT_CUDA(cudaMemcpyAsync(optr.p, out_idx, sizeof(int32_t *) * kMaxModes, cudaMemcpyHostToDevice, c.stream));
   if (in.vt == DT::F64)
