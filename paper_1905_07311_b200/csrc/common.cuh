@@ -8,6 +8,8 @@
 #include <vector>
 #include <stdexcept>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: no-ops unless a profiler is attached
+
 #include "../../include/rtucker.h"
 
 namespace rt {
@@ -107,14 +109,29 @@ struct Ctx {
   unsigned sk_epoch = 0;
 };
 
-// RAII scope that records a start/stop event pair when profiling is on.
+// RAII scope that records a start/stop event pair when profiling is on, and always an NVTX
+// range ("sketch m2", ...) for timeline tools (nsys / ncu --nvtx); NVTX calls are no-ops
+// without an attached tool.
+inline const char *phase_name(int phase, int pos) {
+  static const char *names[PH_COUNT][kMaxModes] = {
+      {"sketch m1", "sketch m2", "sketch m3", "sketch m4", "sketch m5", "sketch m6", "sketch m7", "sketch m8"},
+      {"qr m1", "qr m2", "qr m3", "qr m4", "qr m5", "qr m6", "qr m7", "qr m8"},
+      {"bpass m1", "bpass m2", "bpass m3", "bpass m4", "bpass m5", "bpass m6", "bpass m7", "bpass m8"},
+      {"eig m1", "eig m2", "eig m3", "eig m4", "eig m5", "eig m6", "eig m7", "eig m8"},
+      {"shrink m1", "shrink m2", "shrink m3", "shrink m4", "shrink m5", "shrink m6", "shrink m7", "shrink m8"},
+      {"other m1", "other m2", "other m3", "other m4", "other m5", "other m6", "other m7", "other m8"}};
+  return names[phase][pos < 0 ? 0 : (pos < kMaxModes ? pos : kMaxModes - 1)];
+}
+
 struct PhaseScope {
   Ctx &c;
   PhaseEvent ev{};
-  bool on, open = false;
+  bool on, open = false, nvtx_open = false;
   int pos;
   PhaseScope(Ctx &ctx, int phase, int position) : c(ctx), on(ctx.profiling), pos(position) { start(phase); }
   void start(int phase) {
+    nvtxRangePushA(phase_name(phase, pos));
+    nvtx_open = true;
     if (!on) return;
     ev.slot = phase * kMaxModes + (pos < kMaxModes ? pos : kMaxModes - 1);
     cudaEventCreate(&ev.a);
@@ -123,6 +140,10 @@ struct PhaseScope {
     open = true;
   }
   void stop() {
+    if (nvtx_open) {
+      nvtxRangePop();
+      nvtx_open = false;
+    }
     if (!on || !open) return;
     cudaEventRecord(ev.b, c.stream);
     c.events.push_back(ev);
