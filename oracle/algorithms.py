@@ -81,11 +81,17 @@ def canonical_signs(u: np.ndarray) -> np.ndarray:
     return s
 
 
-def randsvd(xm: np.ndarray, r: int, p: int, omega: np.ndarray):
+def randsvd(xm: np.ndarray, r: int, p: int, omega: np.ndarray, power: int = 0):
     """Alg 1 RandSVD(X, r, p, Omega).  Returns (U_hat, Sigma_hat, V_hat^T)
-    plus the diagnostics (Q, B, U_B, all singular values of B).  Signs per reading R4b."""
+    plus the diagnostics (Q, B, U_B, all singular values of B).  Signs per reading R4b.
+    power = q >= 1 adds q steps of randomized subspace iteration after line 2 (the paper's
+    remedy for slow spectral decay, "see Halko et al."): Z = X^T Q,
+    re-orthonormalised, then Y = X Z and Q = qr(Y) again, so range(Q) = range((X X^T)^q X Omega)."""
     y = xm @ omega                                        # line 1: Y = X Omega
     q, _ = np.linalg.qr(y, mode="reduced")                # line 2: Y = QR (Householder, LAPACK)
+    for _ in range(power):                                # subspace iteration (P:553)
+        z, _ = np.linalg.qr(xm.T @ q, mode="reduced")     #   Z = orth(X^T Q)
+        q, _ = np.linalg.qr(xm @ z, mode="reduced")       #   Q = orth(X Z)
     b = q.T @ xm                                          # line 3: B = Q^T X
     ub, s, vt = np.linalg.svd(b, full_matrices=False)     # line 4: thin SVD of B
     u = q @ ub[:, :r]                                     # line 5: U_hat = Q U_B(:, 1:r)
@@ -98,7 +104,7 @@ def _omega_for(seed, j, ncols, ell, k0=0):
     return omega_rows(seed, j, np.arange(ncols, dtype=np.int64), ell, k0=k0)
 
 
-def r_hosvd(x: np.ndarray, ranks, p: int, seed: int = 0) -> TuckerResult:
+def r_hosvd(x: np.ndarray, ranks, p: int, seed: int = 0, power: int = 0) -> TuckerResult:
     """Alg 2: A_j from RandSVD of every X_(j) with independent Omega_j,
     then G = X x_1 A_1^T ... x_d A_d^T."""
     x = np.asarray(x, dtype=np.float64)
@@ -108,7 +114,7 @@ def r_hosvd(x: np.ndarray, ranks, p: int, seed: int = 0) -> TuckerResult:
         ell, r = rank_caps(x.shape, j, ranks[j], p)
         xj = unfold(x, j)
         om = _omega_for(seed, j, xj.shape[1], ell)        # draw Omega_j
-        u, _, _, info = randsvd(xj, r, ell - r, om)       # RandSVD(X_(j), r_j, p, Omega_j)
+        u, _, _, info = randsvd(xj, r, ell - r, om, power) # RandSVD(X_(j), r_j, p, Omega_j)
         factors[j], rr[j], ells[j] = u, r, ell            # A_j <- U_hat
         svals[j] = info["s_all"]                          # (diagnostic: projector-test gate)
     core = multi_mode_product(x, factors, transpose=True) # G = X x_j A_j^T
@@ -116,7 +122,7 @@ def r_hosvd(x: np.ndarray, ranks, p: int, seed: int = 0) -> TuckerResult:
                         extra=dict(s_all=svals))
 
 
-def r_sthosvd(x: np.ndarray, ranks, p: int, seed: int = 0, order=None) -> TuckerResult:
+def r_sthosvd(x: np.ndarray, ranks, p: int, seed: int = 0, order=None, power: int = 0) -> TuckerResult:
     """Alg 3: sequential over rho; RandSVD of the current core unfolding,
     then G_(rho_j) <- Sigma_hat V_hat^T (line 6)."""
     x = np.asarray(x, dtype=np.float64)
@@ -128,7 +134,7 @@ def r_sthosvd(x: np.ndarray, ranks, p: int, seed: int = 0, order=None) -> Tucker
         ell, r = rank_caps(g.shape, j, ranks[j], p)
         gj = unfold(g, j)
         om = _omega_for(seed, j, gj.shape[1], ell)        # Omega_{rho_j}, current dims
-        u, s, vt, info = randsvd(gj, r, ell - r, om)
+        u, s, vt, info = randsvd(gj, r, ell - r, om, power)
         svals[j] = info["s_all"]                          # (diagnostic: projector-test gate)
         factors[j], rr[j], ells[j] = u, r, ell            # A_{rho_j} <- U_hat
         g_new = fold(s[:, None] * vt, j, g.shape)         # G_(rho_j) <- Sigma_hat V_hat^T

@@ -178,3 +178,37 @@ def test_canonical_signs_rule():
     u0, s0, vt0 = np.linalg.svd(np.linalg.qr(xm @ omega)[0].T @ xm, full_matrices=False)
     q = np.linalg.qr(xm @ omega)[0]
     np.testing.assert_allclose((uu * s0[:5]) @ vt, (q @ u0[:, :5] * s0[:5]) @ vt0[:5], atol=1e-12)
+
+
+def test_subspace_iteration_pins():
+    """Randomized subspace iteration (NEXT-3; SPEC S:254-262 examples):
+    q = 0 is the plain range finder; range(Q_q) = range((X X^T)^q X Omega) computed directly
+    (no intermediate orthonormalisation, a different route); exact low rank is still recovered;
+    on a slowly decaying spectrum one step does not increase the error (20 paired seeds)."""
+    rng = np.random.default_rng(2)
+    xm = rng.standard_normal((40, 60)) * (0.8 ** np.arange(60))[None, :]
+    om = rng.standard_normal((60, 8))
+    u0, _, _, i0 = O.randsvd(xm, 5, 3, om, 0)
+    u1, _, _, i1 = O.randsvd(xm, 5, 3, om, 1)
+    ua, _, _, _ = O.randsvd(xm, 5, 3, om)
+    np.testing.assert_array_equal(u0, ua)
+    direct = np.linalg.qr(xm @ (xm.T @ (xm @ om)))[0]
+    assert O.projector_distance(i1["q"], direct) <= 1e-10
+    x = exact_rank((9, 10, 11), (2, 3, 2), seed=4)
+    for t in (O.r_hosvd(x, (2, 3, 2), 2, 1, power=1), O.r_sthosvd(x, (2, 3, 2), 2, 1, power=2)):
+        assert O.rel_error(x, t.core, t.factors) <= 1e-12
+    s = 1.0 / np.arange(1, 31) ** 0.3                        # slow decay
+    u, _ = np.linalg.qr(rng.standard_normal((30, 30)))
+    v, _ = np.linalg.qr(rng.standard_normal((50, 30)))
+    a = (u * s) @ v.T
+    e0 = e1 = 0.0
+    for seed in range(20):
+        om = np.random.default_rng(100 + seed).standard_normal((50, 6))
+        for q, acc in ((0, 0), (1, 1)):
+            uu, _, _, inf = O.randsvd(a, 4, 2, om, q)
+            err = np.linalg.norm(a - inf["q"] @ (inf["q"].T @ a))
+            if q == 0:
+                e0 += err
+            else:
+                e1 += err
+    assert e1 <= e0
