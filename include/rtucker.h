@@ -121,6 +121,12 @@ typedef enum { RTUCKER_DEVICE = 0, RTUCKER_HOST = 1 } rtucker_memory;
  * plus a few copies).  The context keeps the arena and the graph until it is destroyed.
  * Ignored with RTUCKER_RESULT_HOST or while phase profiling is on. */
 #define RTUCKER_GRAPH             (1u << 10)
+/* Randomized subspace iteration (the paper's remedy for slowly decaying spectra, P:550-553;
+ * NEXT-3): RTUCKER_POWER(q), q = 0..15, adds q steps Z = orth(X_(n)^T Q), Q = orth(X_(n) Z)
+ * after each range finder's QR in rtucker_hosvd / rtucker_sthosvd (unsharded inputs; two extra
+ * passes over the mode's tensor per step). */
+#define RTUCKER_POWER(q)          (((uint32_t)(q) & 15u) << 12)
+#define RTUCKER_POWER_MASK        (15u << 12)
 
 /* Dense tensor, first-mode-fastest.  When the tensor is sharded across ranks along its
  * LAST mode, dims[] are the GLOBAL dims and this rank holds the contiguous slab of

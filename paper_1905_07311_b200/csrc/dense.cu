@@ -76,6 +76,26 @@ void sketch_last_sharded(Ctx &c, const DenseIn &in, const void *G, DT gt, const 
   RT_CUDA(cudaMemcpyAsync(normsq, buf.p + (size_t)I * ell, sizeof(double), cudaMemcpyDeviceToDevice, c.stream));
 }
 
+// q steps of randomized subspace iteration on the range basis Q (I x ell) of G_(n) (P:550-553,
+// Halko et al.'s scheme as the paper cites it): B = Q^T G_(n) (the B-pass, with its Gram),
+// Z = B^T re-orthonormalised by the Cholesky factor of that Gram (B' = R^{-T} B), Y = G_(n) Z
+// (the sketch kernel with Z in place of Omega), Q = qr(Y).  fp64 throughout.
+void power_iterate(Ctx &c, const void *G, DT gt, ModeView v, int ell, int q, bool mul_f64, double *Q,
+                   const uint32_t *colmax) {
+  const int64_t I = v.I;
+  for (int it = 0; it < q; ++it) {
+    DevBuf<double> B(c, (size_t)v.L * ell * v.R), B2(c, (size_t)v.L * ell * v.R), gram(c, (size_t)ell * ell),
+        Rinv(c, (size_t)ell * ell), Y(c, (size_t)I * ell);
+    DevBuf<int> bad(c, 1);
+    bad.zero();
+    ttm_dense(c, G, gt, v, Q, I, ell, B.p, DT::F64, mul_f64, gram.p, colmax);
+    chol_rinv(c, gram.p, ell, Rinv.p, bad.p);
+    ttm_dense(c, B.p, DT::F64, ModeView{v.L, ell, v.R}, Rinv.p, ell, ell, B2.p, DT::F64, true, nullptr);
+    sketch_explicit(c, G, gt, v, B2.p, ell, Y.p);
+    thin_qr(c, Y.p, I, ell, Q);
+  }
+}
+
 void copy_residuals(Ctx &c, rtucker_result *r, const double *scal, int d, int first_mode) {
   for (int k = 0; k < d; ++k)
     RT_CUDA(cudaMemcpyAsync(&r->mode_residual_sq[k], scal + 2 * k + 1, sizeof(double), cudaMemcpyDeviceToHost,
@@ -94,6 +114,8 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
   check_order(order, in.d, ord, in.gdims, in.sharded);
   const Policy pol = policy_for(in.dt, flags, max_ell(in, ranks, p));
   const int d = in.d;
+  const int power = (int)((flags & RTUCKER_POWER_MASK) >> 12);
+  if (power > 0 && in.sharded) throw Error(RTUCKER_EUNSUPPORTED, "subspace iteration: unsharded inputs only");
   ResultGuard rg{c, new_result(d)};
   rtucker_result *res = rg.r;
   fill_header(res, in, ord, seed, flags);
@@ -143,6 +165,10 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
       thin_qr(c, Y.p, Ig, ell, Q.p);
     }
     Y.release();
+    if (power > 0) {  // subspace iteration (NEXT-3)
+      PhaseScope ps(c, PH_OTHER, jj);
+      power_iterate(c, G, gt, v, ell, power, pol.mul_f64 || gt == DT::F64, Q.p, colmax.p);
+    }
     // ---- Alg 1 line 3: B = Q^T G_(n)   (+ Gram B B^T)
     DevBuf<unsigned char> B(c, (size_t)v.L * ell * v.R * dt_size(pol.store));
     DevBuf<double> gram(c, (size_t)ell * ell);
@@ -222,7 +248,9 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
   // stream while the main stream streams the next mode's sketch / B-pass over X.  Only the last
   // mode's QR and eigensolve stay exposed.  Event edges order the two streams (and become graph
   // edges under RTUCKER_GRAPH).
-  const bool overlap = !in.sharded && d > 1 && c.aux;
+  const int power = (int)((flags & RTUCKER_POWER_MASK) >> 12);
+  if (power > 0 && in.sharded) throw Error(RTUCKER_EUNSUPPORTED, "subspace iteration: unsharded inputs only");
+  const bool overlap = !in.sharded && d > 1 && c.aux && power == 0;
   if (overlap) {
     // the persistent streaming kernels size their grids by c.num_sms: leave 4 SMs to the side
     // stream (a QR cluster of <= 4 CTAs, or one eigensolver CTA), restored at the join
@@ -323,6 +351,7 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
     ps.next(PH_QR);
     DevBuf<double> Q(c, (size_t)Ig * ell);
     thin_qr(c, Y.p, Ig, ell, Q.p);
+    if (power > 0) power_iterate(c, in.ptr, in.dt, v, ell, power, pol.mul_f64 || in.dt == DT::F64, Q.p, colmax.p);
     DevBuf<double> gram(c, (size_t)ell * ell);
     ps.next(PH_BPASS);
     if (!last_sharded) {

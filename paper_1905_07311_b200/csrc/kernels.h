@@ -40,6 +40,12 @@ bool sketch_tc_enabled();
 // bpass_tc.cu: B = Q^T X_(n) (B[k + ell c]) for fp32 X with L == 1 on tcgen05 (3xTF32).
 bool bpass_tc_mn(Ctx &c, const float *X, ModeView v, const double *Q, int64_t ldq, int ell, void *B, bool out_f64);
 
+// Y (I x ell) = X_(n) Om_(n)^T with an explicit fp64 (L, ell, R) tensor Om in place of Omega
+// (subspace iteration: Y = X_(n) Z with Z = B'^T), fp64 products, ell <= 64.
+void sketch_explicit(Ctx &c, const void *X, DT in, ModeView v, const double *Om, int ell, double *Y);
+// Rinv (n x n, column-major upper) = R^{-1} of the Cholesky factor G = R^T R of an SPD Gram
+// (subspace iteration's re-orthonormalisation); *bad = 1 on a non-positive pivot.
+void chol_rinv(Ctx &c, const double *G, int n, double *Rinv, int *bad);
 // Generates Omega rows for given columns (debug / parity).
 void omega_rows(Ctx &c, DT out, uint64_t seed, int mode, const int64_t *cols, int64_t n,
                 int ell, int64_t k0, void *dst);

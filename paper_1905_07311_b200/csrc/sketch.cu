@@ -209,7 +209,8 @@ template <typename Tin, typename TN>
 __global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict__ X, int64_t L, int64_t I, int64_t R,
                                                           int64_t cols_per_split, uint64_t seed, int mode, int ell,
                                                           int64_t k0, int64_t col_offset, double *__restrict__ partial,
-                                                          double *__restrict__ norm_partial) {
+                                                          double *__restrict__ norm_partial,
+                                                          const double *__restrict__ Om = nullptr) {
   __shared__ __align__(16) double Xs[kSP * kSX];
   __shared__ __align__(16) double Os[kSP * kSO];
   __shared__ double sred[8];
@@ -264,8 +265,21 @@ __global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict_
       nsq = fma(v, v, nsq);
       Xs[pp * kSX + ii] = v;
     }
-    // Omega chunk: rows p0.., columns k0.. (Philox block granularity); rows past pend are 0
-    for (int e = tid; e < kSP * nb; e += 256) {
+    // Omega chunk: rows p0.., columns k0.. (Philox block granularity); rows past pend are 0.
+    // Explicit Omega (subspace iteration): Om stored (L, ell, R), Omega(p, k) = Om(l, k, r).
+    if (Om) {
+      for (int e = tid; e < kSP * ell; e += 256) {
+        const int pp = e / ell, kk = e % ell;
+        const int64_t p = p0 + pp;
+        double v = 0.0;
+        if (p < pend) {
+          const int64_t r = p / L, l = p - r * L;
+          v = Om[l + L * (kk + (int64_t)ell * r)];
+        }
+        Os[pp * kSO + kk] = v;
+      }
+    }
+    for (int e = tid; e < kSP * nb && !Om; e += 256) {
       const int pp = e / nb, jb = e % nb;
       const int64_t p = p0 + pp;
       const uint4 w = omega_words(seed, mode, 0, (uint64_t)(p + col_offset), (uint32_t)(jb0 + jb));
@@ -322,7 +336,7 @@ __global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict_
 
 template <typename Tin, typename TN>
 void launch_sketch_dfma(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int64_t k0, uint64_t seed,
-                        int64_t col_offset, double *Y, double *normsq) {
+                        int64_t col_offset, double *Y, double *normsq, const double *Om = nullptr) {
   const int gx = ceil_div(v.I, 128);
   const int64_t P = v.L * v.R;
   // one full wave: 2 CTAs of 256 threads per SM (126 registers per thread)
@@ -336,7 +350,7 @@ void launch_sketch_dfma(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int
   if (normsq) npart.alloc(c, (size_t)nsplit * gx);
   dim3 grid(gx, (unsigned)nsplit);
   RT_LAUNCH(c, (sketch_dfma_kernel<Tin, TN>), grid, 256, 0, X, v.L, v.I, v.R, cps, seed, mode, ell, k0, col_offset,
-            part.p, normsq ? npart.p : nullptr);
+            part.p, normsq ? npart.p : nullptr, Om);
   const int64_t n = v.I * ell;
   RT_LAUNCH(c, reduce_splits_kernel, ceil_div(n, 256) > 1024 ? 1024 : ceil_div(n, 256), 256, 0, part.p, (int)nsplit, n,
             Y);
@@ -395,6 +409,12 @@ void sketch_dense(Ctx &c, const void *X, DT in, ModeView v, int mode, int ell, i
   sketch_dispatch<float, float>(c, (const float *)X, v, mode, ell, k0, seed, col_offset, Y, normsq, colmax);
 }
 
+
+void sketch_explicit(Ctx &c, const void *X, DT in, ModeView v, const double *Om, int ell, double *Y) {
+  RT_REQUIRE(ell >= 1 && ell <= 64, "explicit sketch: 1 <= l <= 64");
+  if (in == DT::F64) launch_sketch_dfma<double, double>(c, (const double *)X, v, 0, ell, 0, 0, 0, Y, nullptr, Om);
+  else launch_sketch_dfma<float, double>(c, (const float *)X, v, 0, ell, 0, 0, 0, Y, nullptr, Om);
+}
 
 void omega_rows(Ctx &c, DT out, uint64_t seed, int mode, const int64_t *cols, int64_t n, int ell,
                 int64_t k0, void *dst) {

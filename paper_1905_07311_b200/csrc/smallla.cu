@@ -912,6 +912,27 @@ __global__ void __launch_bounds__(256) chol_inv_kernel(const double *__restrict_
   }
 }
 
+// Inverse of an upper-triangular n x n matrix (column-major, n <= 256): thread j solves column j
+// of R X = I by back substitution (R in shared memory).
+__global__ void tri_inv_upper_kernel(const double *__restrict__ Rg, int n, double *__restrict__ X,
+                                     const int *__restrict__ bad) {
+  if (*bad) return;
+  extern __shared__ double rs2[];
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) rs2[e] = Rg[e];
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    for (int i = n - 1; i >= 0; --i) {
+      double s = (i == j) ? 1.0 : 0.0;
+      if (i > j) {
+        X[i + (int64_t)n * j] = 0.0;
+        continue;
+      }
+      for (int t = i + 1; t <= j; ++t) s = fma(-rs2[i + n * t], X[t + (int64_t)n * j], s);
+      X[i + (int64_t)n * j] = s / rs2[i + n * i];
+    }
+  }
+}
+
 // Q = Y R^{-1} by forward substitution, one row of Y per thread (x R = y), R in shared memory.
 __global__ void __launch_bounds__(128) trsm_rows_kernel(const double *__restrict__ Y, int64_t m, int n,
                                                         const double *__restrict__ Rg, double *__restrict__ Q,
@@ -1459,6 +1480,16 @@ void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps,
   }
 #undef RT_GE
   sym_eig(c, A, n, w, V, nullptr, refine.p);  // no-op unless the gate asks for it
+}
+
+void chol_rinv(Ctx &c, const double *G, int n, double *Rinv, int *bad) {
+  RT_REQUIRE(n >= 1 && n <= 256, "chol_rinv: 1 <= n <= 256");
+  DevBuf<double> R(c, (size_t)n * n);
+  const size_t csm = sizeof(double) * ((size_t)n * n + n);
+  smem_attr(chol_inv_kernel, csm);
+  RT_LAUNCH(c, chol_inv_kernel, 1, 256, csm, G, n, R.p, bad);
+  smem_attr(tri_inv_upper_kernel, sizeof(double) * n * n);
+  RT_LAUNCH(c, tri_inv_upper_kernel, 1, 256, sizeof(double) * n * n, R.p, n, Rinv, bad);
 }
 
 void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {

@@ -34,6 +34,13 @@ DEBUG_CHECKS = 1 << 8
 SP_HOSVD = 1 << 9
 GRAPH = 1 << 10
 
+
+def POWER(q: int) -> int:
+    """RTUCKER_POWER(q): q steps of randomized subspace iteration."""
+    return (int(q) & 15) << 12
+
+
+
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
 

@@ -343,3 +343,25 @@ def test_sharded_path_loopback(ctx, algo, name, make, ranks, p):
         ctx.loopback_sharding(False)
     o = _oracle(algo, x, ranks, p, 1, tuple(range(d)))
     _check(x, g, o, x.dtype == np.float64)
+
+
+@pytest.mark.parametrize("algo", ["sthosvd", "hosvd"])
+@pytest.mark.parametrize("name,make,ranks,p,q", [
+    ("c1_q1", lambda: hilbert((50, 50, 50), "shifted"), (5, 5, 5), 5, 1),
+    ("ragged_q2", lambda: np.asfortranarray(np.random.default_rng(3).standard_normal((37, 19, 41))), (7, 3, 11), 4, 2),
+    ("odeco96_f32_q1", lambda: odeco(96, seed=4, dtype=np.float32), (12, 12, 12), 10, 1),
+    ("c2_q1", lambda: tucker_c2(), (20, 20, 40), 10, 1),
+])
+def test_subspace_iteration_parity(ctx, algo, name, make, ranks, p, q):
+    """RTUCKER_POWER(q): q steps of randomized subspace iteration (NEXT-3) on every
+    mode, against the oracle's randsvd(power=q) on the same Omega: fixed-rank criteria."""
+    from paper_1905_07311_b200.rtucker import POWER
+    x = make()
+    order = tuple(range(x.ndim)) if algo == "sthosvd" else None
+    g = _run(ctx, algo, x, ranks, p, seed=2, order=order, flags=POWER(q))
+    o = (O.r_sthosvd(x, ranks, p, 2, order, power=q) if algo == "sthosvd" else O.r_hosvd(x, ranks, p, 2, power=q))
+    _check(x, g, o, x.dtype == np.float64)
+    # one step helps on the slowly decaying random tensor (paired with q = 0 on the same Omega)
+    if name == "ragged_q2":
+        g0 = _run(ctx, algo, x, ranks, p, seed=2, order=order)
+        assert O.rel_error(x, g.core, g.factors) <= O.rel_error(x, g0.core, g0.factors) + 1e-12
