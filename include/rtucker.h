@@ -127,6 +127,11 @@ typedef enum { RTUCKER_DEVICE = 0, RTUCKER_HOST = 1 } rtucker_memory;
  * passes over the mode's tensor per step). */
 #define RTUCKER_POWER(q)          (((uint32_t)(q) & 15u) << 12)
 #define RTUCKER_POWER_MASK        (15u << 12)
+/* Deterministic comparators (NEXT-4; the paper's baselines of Table 6.2): with this
+ * flag rtucker_hosvd / rtucker_sthosvd compute the deterministic HOSVD / STHOSVD
+ * (P:74-92): the leading r_n eigenvectors of the full unfolding's Gram G_(n) G_(n)^T instead of
+ * a sketch (p and seed are ignored; single GPU; fp64 products and intermediates). */
+#define RTUCKER_EXACT_SVD         (1u << 16)
 
 /* Dense tensor, first-mode-fastest.  When the tensor is sharded across ranks along its
  * LAST mode, dims[] are the GLOBAL dims and this rank holds the contiguous slab of

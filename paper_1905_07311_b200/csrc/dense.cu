@@ -105,8 +105,93 @@ void copy_residuals(Ctx &c, rtucker_result *r, const double *scal, int d, int fi
 
 }  // namespace
 
+// Deterministic comparators (RTUCKER_EXACT_SVD, NEXT-4): HOSVD and STHOSVD from
+// the eigenpairs of the full unfolding's Gram G_(n) G_(n)^T (the Gram route of Alg 1 line 4 with
+// Q = I): no sketch, fp64 products and intermediates, signs per R4b.
+rtucker_result *run_exact(Ctx &c, const rtucker_dense_desc *X, const int64_t *ranks, const int32_t *order,
+                          uint32_t flags, bool st) {
+  DenseIn in;
+  prepare_dense(c, X, in);
+  RT_REQUIRE(!in.sharded, "RTUCKER_EXACT_SVD: unsharded inputs only");
+  check_ranks(in, ranks, 0);
+  const int d = in.d;
+  int32_t ord[kMaxModes];
+  if (st) check_order(order, d, ord, in.gdims, false);
+  else for (int k = 0; k < d; ++k) ord[k] = k;
+  ResultGuard rg{c, new_result(d)};
+  rtucker_result *res = rg.r;
+  fill_header(res, in, ord, 0, flags);
+  DevBuf<double> scal(c, 2 * (size_t)d);
+  scal.zero();
+  int64_t cur[kMaxModes];
+  memcpy(cur, in.gdims, sizeof cur);
+  const void *G = in.ptr;
+  DT gt = in.dt;
+  DevBuf<unsigned char> gown;
+  for (int jj = 0; jj < d; ++jj) {
+    const int n = ord[jj];
+    const int64_t *dims = st ? cur : in.gdims;
+    const void *src = st ? G : in.ptr;
+    const DT stt = st ? gt : in.dt;
+    const ModeView v = mode_view(dims, d, n);
+    const int I = (int)v.I, r = (int)std::min<int64_t>(ranks[n], v.I);
+    DevBuf<double> gram(c, (size_t)I * I), w(c, I), V(c, (size_t)I * I);
+    {
+      PhaseScope ps(c, PH_BPASS, jj);
+      sumsq(c, src, stt, v.L * v.I * v.R, scal.p + 2 * n);
+      if (stt == DT::F64 && I > 64) gram_f64(c, (const double *)src, v.L, I, v.R, gram.p);
+      else mode_gram(c, src, stt, v, gram.p);
+    }
+    double *A = (double *)dev_alloc(c, sizeof(double) * I * r);
+    res->factors[n] = A;
+    {
+      PhaseScope ps(c, PH_EIG, jj);
+      // relative-accuracy Jacobi for small fp64 Grams; the tridiagonal solver above 64 (the
+      // unpreconditioned grid Jacobi can miss its sweep cap on these nearly singular Grams)
+      gram_eig(c, gram.p, I, w.p, V.p, nullptr, r, in.dt == DT::F64 && I <= 64);
+      RT_CUDA(cudaMemcpyAsync(A, V.p, sizeof(double) * I * r, cudaMemcpyDeviceToDevice, c.stream));
+      canonical_signs(c, A, I, r, V.p, I, I);
+      residual_from_eigs(c, w.p, r, scal.p + 2 * n, scal.p + 2 * n + 1);
+    }
+    res->ranks[n] = r;
+    res->ell[n] = I;
+    if (st) {  // G_(n) <- U(:, 1:r)^T G_(n)
+      PhaseScope ps(c, PH_SHRINK, jj);
+      DevBuf<unsigned char> Gn(c, (size_t)v.L * r * v.R * sizeof(double));
+      ttm_dense(c, G, gt, v, V.p, I, r, Gn.p, DT::F64, true, nullptr);
+      gown = std::move(Gn);
+      G = gown.p;
+      gt = DT::F64;
+      cur[n] = r;
+    }
+  }
+  if (!st) {  // G = X x_1 A_1^T ... x_d A_d^T
+    PhaseScope ps(c, PH_SHRINK, 0);
+    DevBuf<unsigned char> g0, g1;
+    for (int n = 0; n < d; ++n) {
+      const ModeView v = mode_view(cur, d, n);
+      const int rr = (int)res->ranks[n];
+      DevBuf<unsigned char> &dst = (G == g0.p) ? g1 : g0;
+      dst.alloc(c, (size_t)v.L * rr * v.R * sizeof(double));
+      ttm_dense(c, G, gt, v, (const double *)res->factors[n], in.gdims[n], rr, dst.p, DT::F64, true, nullptr);
+      G = dst.p;
+      gt = DT::F64;
+      cur[n] = rr;
+    }
+    gown = std::move(G == g0.p ? g0 : g1);
+    G = gown.p;
+  }
+  const int64_t ncore = prod(cur, d);
+  res->core = dev_alloc(c, sizeof(double) * ncore);
+  convert(c, G, gt, res->core, DT::F64, ncore);
+  copy_residuals(c, res, scal.p, d, ord[0]);
+  finish_result(c, res, flags);
+  return rg.release();
+}
+
 rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ranks, int p, uint64_t seed,
                             const int32_t *order, uint32_t flags) {
+  if (flags & RTUCKER_EXACT_SVD) return run_exact(c, X, ranks, order, flags, true);
   DenseIn in;
   prepare_dense(c, X, in);
   check_ranks(in, ranks, p);
@@ -224,6 +309,7 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
 
 rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ranks, int p, uint64_t seed,
                           uint32_t flags) {
+  if (flags & RTUCKER_EXACT_SVD) return run_exact(c, X, ranks, nullptr, flags, false);
   DenseIn in;
   prepare_dense(c, X, in);
   check_ranks(in, ranks, p);

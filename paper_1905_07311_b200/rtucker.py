@@ -33,6 +33,7 @@ DETERMINISTIC = 1 << 7
 DEBUG_CHECKS = 1 << 8
 SP_HOSVD = 1 << 9
 GRAPH = 1 << 10
+EXACT_SVD = 1 << 16
 
 
 def POWER(q: int) -> int:

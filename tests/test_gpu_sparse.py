@@ -166,3 +166,27 @@ def test_zipf_full_scale_c5(ctx):
     t2 = time.perf_counter()
     print(f"C5 nnz={idx.shape[1]} gpu {t1 - t0:.3f}s (incl. H2D) oracle {t2 - t1:.1f}s nnz chain {g.nnz_history}")
     _check(g, o, 2.0, 1e-4)
+
+
+def test_gamma_tensor_error_ordering(ctx):
+    """NEXT-4 (Fig 6.4): on the synthetic sparse gamma-tensor (gamma = 10, 200^3,
+    ~185k nonzeros) SP-STHOSVD at target rank r (rank r + p) is no better than R-STHOSVD and
+    STHOSVD at rank r + p, and stays within a small factor of them ("slightly higher")."""
+    import torch
+    from paper_1905_07311_b200.rtucker import EXACT_SVD, RESULT_HOST
+    from workloads import synthetic_sparse_gamma, to_first_mode_fastest
+    x = synthetic_sparse_gamma(10.0, seed=1)
+    idx = np.array(np.nonzero(x), dtype=np.int32)
+    vals = x[tuple(idx)]
+    r, ell = 10, 15
+    sp = _run(ctx, idx, vals, x.shape, (r, r, r), 5, seed=0, order=(0, 1, 2))
+    o = O.sp_sthosvd(idx, vals, x.shape, (r, r, r), 5, seed=0, order=(0, 1, 2))
+    _check(sp, o, 2.0, 1e-9)
+    core = np.zeros((ell,) * 3)
+    core[tuple(sp.core_idx)] = sp.core_vals
+    e_sp = np.linalg.norm(x - O.reconstruct(core, sp.factors)) / np.linalg.norm(x)
+    xd = torch.as_tensor(to_first_mode_fastest(x), device="cuda")
+    rs = ctx.sthosvd(xd, x.shape, (ell,) * 3, 5, 0, (0, 1, 2), RESULT_HOST).numpy()
+    st = ctx.sthosvd(xd, x.shape, (ell,) * 3, 0, 0, (0, 1, 2), EXACT_SVD | RESULT_HOST).numpy()
+    e_rs, e_st = O.rel_error(x, rs.core, rs.factors), O.rel_error(x, st.core, st.factors)
+    assert e_st <= e_rs * (1 + 1e-9) and e_rs <= e_sp * (1 + 1e-9) and e_sp <= 10 * e_rs, (e_st, e_rs, e_sp)
