@@ -307,6 +307,13 @@ rtucker_status rtucker_debug_gemm(rtucker_ctx *ctx, int transA, int transB, int6
 /* Gram C (K x K) = B_(n) B_(n)^T of an fp64 tensor stored (L, K, R) (DEVICE pointers). */
 rtucker_status rtucker_debug_gram(rtucker_ctx *ctx, int64_t L, int64_t K, int64_t R, const double *B, double *C);
 
+/* Sparse sketch Y = X_(mode) Omega_mode(:, 0:ell) of a COO tensor (Alg 6 line 4), summed
+ * in fixed point over the nonzeros (DESIGN reading R20), fp64 I_mode x ell column-major, written
+ * to Y_out (DEVICE).  flags: RTUCKER_ACCUM_FP64 draws fp64 normals for fp32 values (fp64
+ * values always use fp64 normals).  ell <= 64. */
+rtucker_status rtucker_debug_coo_sketch(rtucker_ctx *ctx, const rtucker_coo_desc *X, int32_t mode, int32_t ell,
+                                        uint64_t seed, uint32_t flags, double *Y_out);
+
 /* Strong-RRQR row selection (DESIGN reading R9) of an m x l orthonormal fp64 Q:
  * sel (l, sorted ascending, DEVICE int64) and A = Q Q[sel,:]^{-1} (m x l, DEVICE). */
 rtucker_status rtucker_debug_srrqr(rtucker_ctx *ctx, int64_t m, int32_t l, const double *Q,

@@ -24,7 +24,7 @@ from .tensor import (  # noqa: F401
 from .algorithms import (  # noqa: F401
     TuckerResult, SpTuckerResult, randsvd, r_hosvd, r_sthosvd, adapt_range_finder,
     adaptive_r_sthosvd, adaptive_r_hosvd, hosvd, sthosvd, sp_sthosvd, sp_hosvd,
-    auto_order, rank_caps, canonical_signs,
+    auto_order, rank_caps, canonical_signs, sp_sketch,
 )
 from .srrqr import cpqr_select, srrqr_select, oblique_factor  # noqa: F401
 from .bounds import delta_tail, bound_expected_error, bound_sp, g_cond, f_p  # noqa: F401

@@ -281,14 +281,20 @@ def sthosvd(x: np.ndarray, ranks, order=None) -> TuckerResult:
     return TuckerResult(g, factors, tuple(ranks), tuple(ranks), order, -1)
 
 
-def _sp_mode(idx, vals, cur_dims, j, ell, seed, eta):
-    """One pass of Alg 6 lines 3-7 on the current sparse core (COO)."""
+def sp_sketch(idx, vals, cur_dims, j, ell, seed):
+    """Alg 6 line 4: Y = G_(j) Omega_j for a COO tensor, with only the Omega rows of
+    the occupied columns of the unfolding drawn."""
     cols = unfold_columns(cur_dims, j, idx)
     ucols, inv = np.unique(cols, return_inverse=True)
     om = omega_rows(seed, j, ucols, ell)                  # Omega rows of occupied columns
-    gj = sp.coo_matrix((vals.astype(np.float64), (idx[j].astype(np.int64), inv)),
+    gj = sp.coo_matrix((np.asarray(vals).astype(np.float64), (np.asarray(idx[j]).astype(np.int64), inv)),
                        shape=(int(cur_dims[j]), ucols.size)).tocsr()
-    y = np.asarray(gj @ om)                               # line 4: Y = G_(j) Omega
+    return np.asarray(gj @ om)
+
+
+def _sp_mode(idx, vals, cur_dims, j, ell, seed, eta):
+    """One pass of Alg 6 lines 3-7 on the current sparse core (COO)."""
+    y = sp_sketch(idx, vals, cur_dims, j, ell, seed)      # line 4: Y = G_(j) Omega
     q, _ = np.linalg.qr(y, mode="reduced")                # line 5: thin QR
     sel, swaps = srrqr_select(q, eta)                     # line 6: strong RRQR on Q^T
     a = oblique_factor(q, sel)                            # line 7: A = Q (P^T Q)^{-1}

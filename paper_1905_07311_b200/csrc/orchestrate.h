@@ -59,6 +59,8 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
                           uint32_t flags);
 rtucker_result *run_adaptive(Ctx &c, const rtucker_dense_desc *X, double tol, int block, const double *mode_tol,
                              const int32_t *order, uint64_t seed, uint32_t flags);
+void debug_coo_sketch(Ctx &c, const rtucker_coo_desc *X, int mode, int ell, uint64_t seed, bool normals_f64,
+                      double *Y);
 rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int64_t *ranks, int p,
                                    uint64_t seed, const int32_t *order, double eta, uint32_t flags);
 double run_rel_error(Ctx &c, const rtucker_dense_desc *X, const rtucker_result *res);

@@ -639,6 +639,17 @@ rtucker_status rtucker_debug_gram(rtucker_ctx *ctx, int64_t L, int64_t K, int64_
   return guard(ctx, [&] { gram_f64(ctx->c, B, L, K, R, C); });
 }
 
+rtucker_status rtucker_debug_coo_sketch(rtucker_ctx *ctx, const rtucker_coo_desc *X, int32_t mode, int32_t ell,
+                                        uint64_t seed, uint32_t flags, double *Y_out) {
+  if (!ctx || !X || !Y_out || X->d < 1 || X->d > RTUCKER_MAX_MODES || mode < 0 || mode >= X->d || ell < 1 ||
+      ell > 64 || X->nnz < 0 || (X->dtype != RTUCKER_F32 && X->dtype != RTUCKER_F64))
+    return RTUCKER_EINVAL;
+  return guard(ctx, [&] {
+    debug_coo_sketch(ctx->c, X, mode, ell, seed, (flags & RTUCKER_ACCUM_MASK) == RTUCKER_ACCUM_FP64, Y_out);
+    check_status(ctx->c);
+  });
+}
+
 rtucker_status rtucker_debug_srrqr(rtucker_ctx *ctx, int64_t m, int32_t l, const double *Q, double eta,
                                    int64_t *sel, double *A, int32_t *swaps_out) {
   if (!ctx || !Q || !sel || !A || l < 1 || m < l || !(eta >= 1.0)) return RTUCKER_EINVAL;

@@ -213,6 +213,371 @@ __global__ void __launch_bounds__(kCooT) sketch_coo_kernel(CooDev g, const int64
   }
 }
 
+// ------------------------------------------- bucketed COO sketch (default, a8) --
+// Count tensors are heavy-tailed (BASELINE configs[4]: Zipf(1.1) indices; in mode 3 the
+// heaviest row holds ~9 % of the nonzeros and every one of the 200000 rows a few), so a
+// per-nonzero global atomic (2 words x ell columns) is what bounds a direct scatter into Y.
+// Instead:
+//   pass 0  bucket_hist     nonzeros per bucket of kBR consecutive rows (per-CTA shared-
+//                           memory counters, one global atomic per CTA and bucket)
+//   scan    bucket_scan     bucket offsets and the work units (<= unit nonzeros of one bucket)
+//   pass 1  bucket_scatter  every nonzero to its bucket: key = Omega column index c | local row
+//                           << 56, value; per chunk one cursor atomic per bucket reserves a
+//                           contiguous range (the write frontiers, one per bucket, stay in L2)
+//   pass 2  bucket_sketch   one work item per CTA iteration: Y rows of the bucket accumulate in
+//                           shared memory (int64 fixed point) with ONE writer per address: warp
+//                           w owns columns 4(w & 3) .. +3 of copy (w >> 2), lanes of a warp
+//                           holding the same row are combined by a shuffle tree first; then one
+//                           global atomic pair per touched (row, column) of the item.
+// Integer additions make the result independent of every order involved (R20).
+constexpr int kBR = 128;          // rows per bucket (local row: 7 bits of the key)
+constexpr int kMaxBk = 8192;      // buckets (I <= 2^20)
+constexpr int kBT = 256;          // threads of the bucket kernels
+constexpr int kBChunk = 8192;     // nonzeros per scatter chunk
+constexpr int kItemMax = 65536;   // nonzeros per sketch work unit (at most; see bucket_scan)
+constexpr int kSub = 2048, kRun = kSub / kBT;  // bucket_sketch sub-chunk, nonzeros per lane
+constexpr uint64_t kKeyMask = (1ull << 56) - 1;
+
+__global__ void __launch_bounds__(kBT) bucket_hist(CooDev g, const int64_t *__restrict__ nnz_dev, int mode, int nbk,
+                                                  unsigned *__restrict__ gcnt) {
+  __shared__ unsigned cnt[kMaxBk];
+  for (int t = threadIdx.x; t < nbk; t += kBT) cnt[t] = 0;
+  __syncthreads();
+  const int64_t nnz = nnz_dev ? *nnz_dev : g.nnz;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = ((int64_t)blockIdx.x * kBT + threadIdx.x) & ~(int64_t)31; base < nnz;
+       base += (int64_t)gridDim.x * kBT) {
+    const int64_t e = base + lane;
+    const int bk = e < nnz ? g.idx[mode][e] / kBR : -1;
+    const unsigned grp = __match_any_sync(0xffffffffu, bk);
+    if (bk >= 0 && lane == __ffs(grp) - 1) atomicAdd(&cnt[bk], (unsigned)__popc(grp));
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nbk; t += kBT)
+    if (cnt[t]) atomicAdd(&gcnt[t], cnt[t]);
+}
+
+// One CTA: bstart[b] (exclusive scan of the counts, bstart[nbk] = nnz), cursor = bstart, and
+// istart[b] = first work unit of bucket b (ceil(cnt / unit) of them), istart[nbk] = units.
+__device__ __forceinline__ int64_t block_excl_scan(int64_t x, int64_t *sh, int64_t &total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int64_t inc = x;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += y;
+  }
+  if (lane == 31) sh[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    const int64_t s = lane < (int)(blockDim.x >> 5) ? sh[lane] : 0;
+    int64_t si = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, si, o);
+      if (lane >= o) si += y;
+    }
+    sh[lane] = si - s;
+    if (lane == 31) sh[32] = si;
+  }
+  __syncthreads();
+  const int64_t r = sh[w] + inc - x;
+  total = sh[32];
+  __syncthreads();
+  return r;
+}
+constexpr int kScanT = 1024, kScanPer = kMaxBk / kScanT;
+__global__ void __launch_bounds__(kScanT) bucket_scan(const unsigned *__restrict__ cnt, int nbk,
+                                                     unsigned *__restrict__ bstart, unsigned *__restrict__ cur,
+                                                     int *__restrict__ istart, int *__restrict__ work, int grid) {
+  __shared__ int64_t sh[33];
+  unsigned v[kScanPer];
+  int64_t s = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    const int i = threadIdx.x * kScanPer + k;
+    v[k] = i < nbk ? cnt[i] : 0u;
+    s += v[k];
+  }
+  int64_t tot, itot;
+  int64_t run = block_excl_scan(s, sh, tot);
+  // work-unit size from the live nonzero count: ~4 units per CTA of bucket_sketch, a multiple
+  // of its sub-chunk, at most kItemMax
+  const int64_t u = (tot / (4 * (int64_t)grid) + kSub - 1) / kSub * kSub;
+  const int unit = (int)(u < kSub ? kSub : (u > kItemMax ? kItemMax : u));
+  int64_t si = 0;
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) si += (v[k] + unit - 1) / unit;
+  int64_t irun = block_excl_scan(si, sh, itot);
+#pragma unroll
+  for (int k = 0; k < kScanPer; ++k) {
+    const int i = threadIdx.x * kScanPer + k;
+    if (i < nbk) {
+      bstart[i] = (unsigned)run;
+      cur[i] = (unsigned)run;
+      istart[i] = (int)irun;
+    }
+    run += v[k];
+    irun += (v[k] + unit - 1) / unit;
+  }
+  if (threadIdx.x == 0) {
+    bstart[nbk] = (unsigned)tot;
+    istart[nbk] = (int)itot;
+    work[0] = 0;
+    work[1] = unit;
+  }
+}
+
+template <typename TV>
+__global__ void __launch_bounds__(kBT) bucket_scatter(CooDev g, const int64_t *__restrict__ nnz_dev, int mode, int nbk,
+                                                     unsigned *__restrict__ cur, uint64_t *__restrict__ skey,
+                                                     TV *__restrict__ sval) {
+  extern __shared__ unsigned bsc[];
+  unsigned *lcnt = bsc, *lbase = bsc + nbk;
+  const int64_t nnz = nnz_dev ? *nnz_dev : g.nnz;
+  const int lane = threadIdx.x & 31;
+  int64_t stride[kMaxModes];
+  int64_t s = 1;
+  for (int k = 0; k < g.d; ++k) {
+    stride[k] = (k == mode) ? 0 : s;
+    if (k != mode) s *= g.dims[k];
+  }
+  const TV *vals = (const TV *)g.vals;
+  for (int64_t c0 = (int64_t)blockIdx.x * kBChunk; c0 < nnz; c0 += (int64_t)gridDim.x * kBChunk) {
+    const int64_t c1 = min(nnz, c0 + kBChunk);
+    for (int t = threadIdx.x; t < nbk; t += kBT) lcnt[t] = 0;
+    __syncthreads();
+    for (int64_t b0 = c0 + (threadIdx.x & ~31); b0 < c1; b0 += kBT) {
+      const int64_t e = b0 + lane;
+      const int bk = e < c1 ? g.idx[mode][e] / kBR : -1;
+      const unsigned grp = __match_any_sync(0xffffffffu, bk);
+      if (bk >= 0 && lane == __ffs(grp) - 1) atomicAdd(&lcnt[bk], (unsigned)__popc(grp));
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < nbk; t += kBT) {
+      if (lcnt[t]) lbase[t] = atomicAdd(&cur[t], lcnt[t]);
+      lcnt[t] = 0;
+    }
+    __syncthreads();
+    for (int64_t b0 = c0 + (threadIdx.x & ~31); b0 < c1; b0 += kBT) {
+      const int64_t e = b0 + lane;
+      const bool act = e < c1;
+      int row = -1, bk = -1;
+      uint64_t c = 0;
+      TV v = TV(0);
+      if (act) {
+        for (int k = 0; k < g.d; ++k) c += (uint64_t)((int64_t)g.idx[k][e] * stride[k]);
+        row = g.idx[mode][e];
+        bk = row / kBR;
+        v = vals[e];
+      }
+      const unsigned grp = __match_any_sync(0xffffffffu, bk);
+      const int leader = __ffs(grp) - 1;
+      unsigned pos = 0;
+      if (act && lane == leader) pos = lbase[bk] + atomicAdd(&lcnt[bk], (unsigned)__popc(grp));
+      pos = __shfl_sync(0xffffffffu, pos, leader) + (unsigned)__popc(grp & ((1u << lane) - 1u));
+      if (act) {
+        skey[pos] = c | ((uint64_t)(row - bk * kBR) << 56);
+        sval[pos] = v;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// Pass 2 work unit: <= unit consecutive nonzeros of one bucket, taken by a CTA from a global
+// counter.  The unit's Y rows (kBR x 16 columns x (H, L) int64) accumulate in shared memory
+// and are flushed once (one global atomic pair per touched word).  The unit is processed in
+// sub-chunks of kSub nonzeros, each first counting-sorted by local row in shared memory; then
+// every lane sums a run of kRun consecutive sorted nonzeros in registers and emits per row
+// segment: segments strictly inside its run belong to this lane alone (plain add), its first
+// segment may continue the previous lane's (shared-memory atomic), and the runs' last segments
+// are combined across the warp by a segmented shuffle reduction (rows are sorted, so equal rows
+// sit in consecutive lanes) whose head lane adds atomically.
+constexpr size_t kBSmem = sizeof(long long) * 2 * kBR * 16   // accumulators
+                          + sizeof(uint64_t) * kSub + sizeof(double) * kSub  // sorted keys, values
+                          + sizeof(int) * 2 * kBR + 16;                     // row counts, offsets
+
+__device__ __forceinline__ void seg_add(long long *aH, long long *aL, int lr, int nq, const long long (&H)[16],
+                                        const long long (&L)[16]) {
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    if (q < nq) {
+      aH[lr * 16 + q] += H[q];
+      aL[lr * 16 + q] += L[q];
+    }
+  }
+}
+
+template <typename TV, typename TN>
+__global__ void __launch_bounds__(kBT, 2) bucket_sketch(const uint64_t *__restrict__ skey, const TV *__restrict__ sval,
+                                                       const unsigned *__restrict__ bstart,
+                                                       const int *__restrict__ istart, int nbk, int64_t I, int mode,
+                                                       int ell, uint64_t seed, const FixScale *__restrict__ fs,
+                                                       int *__restrict__ work, unsigned long long *__restrict__ YH,
+                                                       unsigned long long *__restrict__ YL) {
+  extern __shared__ __align__(16) long long bsm[];
+  long long *aH = bsm, *aL = aH + kBR * 16;
+  uint64_t *sk = (uint64_t *)(aL + kBR * 16);
+  double *sv = (double *)(sk + kSub);
+  int *lcnt = (int *)(sv + kSub), *loff = lcnt + kBR;
+  __shared__ int sunit;
+  __shared__ int brow[kBT / 32];
+  __shared__ long long bH[kBT / 32 * 16], bL[kBT / 32 * 16];
+  const int lane = threadIdx.x & 31, tid = threadIdx.x;
+  const double mul = fs->mul;
+  const int nunits = istart[nbk];
+  const int unit = work[1];
+  while (true) {
+    if (tid == 0) sunit = atomicAdd(work, 1);
+    __syncthreads();
+    const int it = sunit;
+    __syncthreads();
+    if (it >= nunits) break;
+    int lo = 0, hi = nbk - 1;  // bucket of unit it: largest b with istart[b] <= it
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (istart[mid] <= it) lo = mid;
+      else hi = mid - 1;
+    }
+    const int b = lo;
+    const int64_t u0 = (int64_t)bstart[b] + (int64_t)(it - istart[b]) * unit;
+    const int64_t u1 = min((int64_t)bstart[b + 1], u0 + unit);
+    for (int cb = 0; cb < ell; cb += 16) {
+      const int nq = min(16, ell - cb);
+      for (int t = tid; t < 2 * kBR * 16; t += kBT) aH[t] = 0;  // aH and aL are contiguous
+      for (int64_t s0 = u0; s0 < u1; s0 += kSub) {
+        const int n = (int)min((int64_t)kSub, u1 - s0);
+        for (int t = tid; t < kBR; t += kBT) lcnt[t] = 0;
+        __syncthreads();
+        // local counting sort by row (rank inside a row from warp-aggregated smem atomics)
+        uint64_t kk[kRun];
+        double vv[kRun];
+        int rk[kRun];
+#pragma unroll
+        for (int k = 0; k < kRun; ++k) {
+          const int i = tid + kBT * k;
+          const bool act = i < n;
+          kk[k] = act ? skey[s0 + i] : 0;
+          vv[k] = act ? (double)sval[s0 + i] : 0.0;
+          const int lr = act ? (int)(kk[k] >> 56) : -1;
+          const unsigned grp = __match_any_sync(0xffffffffu, lr);
+          const int leader = __ffs(grp) - 1;
+          int base = 0;
+          if (act && lane == leader) base = atomicAdd(&lcnt[lr], __popc(grp));
+          rk[k] = __shfl_sync(0xffffffffu, base, leader) + __popc(grp & ((1u << lane) - 1u));
+        }
+        __syncthreads();
+        if (tid < 32) {  // exclusive scan of the kBR = 128 counts, 4 per lane
+          int c4[4], t4 = 0;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) { c4[j] = lcnt[4 * lane + j]; t4 += c4[j]; }
+          int inc = t4;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+          }
+          int run = inc - t4;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) { loff[4 * lane + j] = run; run += c4[j]; }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < kRun; ++k) {
+          if (tid + kBT * k < n) {
+            const int o = loff[(int)(kk[k] >> 56)] + rk[k];
+            sk[o] = kk[k];
+            sv[o] = vv[k];
+          }
+        }
+        __syncthreads();
+        // lane-serial segments over the sorted sub-chunk.  Rows a lane completes inside its run
+        // (its first segment included) are distinct across all lanes of the CTA, so they are
+        // added without atomics; the runs' last segments are added after a barrier.
+        const int i0 = tid * kRun, i1 = min(n, i0 + kRun);
+        long long H[16], L[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) H[q] = L[q] = 0;
+        int cur = i0 < i1 ? (int)(sk[i0] >> 56) : -1;
+        for (int i = i0; i < i1; ++i) {
+          const uint64_t key = sk[i];
+          const int r = (int)(key >> 56);
+          if (r != cur) {
+            seg_add(aH, aL, cur, nq, H, L);
+#pragma unroll
+            for (int q = 0; q < 16; ++q) H[q] = L[q] = 0;
+            cur = r;
+          }
+          const double v = sv[i];
+#pragma unroll
+          for (int jb = 0; jb < 4; ++jb) {
+            if (4 * jb < nq) {
+              const uint4 w = omega_words(seed, mode, 0, key & kKeyMask, (uint32_t)(cb / 4 + jb));
+              Normal4<TN> z(w);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                long long h, l;
+                to_fixed(v * (double)z.v[q], mul, h, l);
+                H[4 * jb + q] += h;
+                L[4 * jb + q] += l;
+              }
+            }
+          }
+        }
+        // last segments: suffix sums over consecutive lanes holding the same row (sorted)
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int ro = __shfl_down_sync(0xffffffffu, cur, o);
+          const bool take = lane + o < 32 && ro == cur;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const long long oh = __shfl_down_sync(0xffffffffu, H[q], o);
+            const long long ol = __shfl_down_sync(0xffffffffu, L[q], o);
+            if (take) {
+              H[q] += oh;
+              L[q] += ol;
+            }
+          }
+        }
+        const int rp = __shfl_up_sync(0xffffffffu, cur, 1);
+        __syncthreads();  // every in-run segment added
+        // group heads: the group of lane 0 may continue the previous warp's last group -> its
+        // warp's boundary slot; every other group's row is this warp's alone
+        const int warp = tid >> 5;
+        if (lane == 0) {
+          brow[warp] = cur;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            bH[warp * 16 + q] = H[q];
+            bL[warp * 16 + q] = L[q];
+          }
+        } else if (cur >= 0 && rp != cur) {
+          seg_add(aH, aL, cur, nq, H, L);
+        }
+        __syncthreads();
+        if (tid < 32) {  // boundary slots in warp order, one thread per word
+          const int q = tid & 15;
+          long long *dst = tid < 16 ? aH : aL;
+          const long long *src = tid < 16 ? bH : bL;
+          for (int w = 0; w < kBT / 32; ++w)
+            if (brow[w] >= 0 && q < nq) dst[brow[w] * 16 + q] += src[w * 16 + q];
+        }
+        __syncthreads();
+      }
+      for (int t = tid; t < kBR * 16; t += kBT) {
+        const int r = t >> 4, q = t & 15;
+        const int64_t row = (int64_t)b * kBR + r;
+        if (q >= nq || row >= I) continue;
+        const int64_t o = row + I * (cb + q);
+        if (aH[t]) atomicAdd(&YH[o], (unsigned long long)aH[t]);
+        if (aL[t]) atomicAdd(&YL[o], (unsigned long long)aL[t]);
+      }
+      __syncthreads();
+    }
+  }
+}
+
 __global__ void y_from_fixed_kernel(const long long *__restrict__ YH, const long long *__restrict__ YL, int64_t n,
                                     const FixScale *__restrict__ fs, double *__restrict__ Y) {
   const double oh = fs->outH, ol = fs->outL;
@@ -627,7 +992,45 @@ void sketch_coo(Ctx &c, const CooDev &g, int mode, int ell, uint64_t seed, bool 
   }
   DevBuf<long long> Yf(c, 2 * (size_t)I * ell);  // [H | L]
   Yf.zero();
-  if (g.nnz > 0) {
+  static const bool unsorted = RT_EXP_GETENV("RTUCKER_COO_UNSORTED") != nullptr;
+  bool key_fits = true;  // Omega column index c < prod_{k != mode} I_k must fit 56 bits of the key
+  int64_t others = 1;
+  for (int k = 0; k < g.d; ++k) {
+    if (k == mode) continue;
+    if (others > (int64_t)(kKeyMask / (uint64_t)g.dims[k])) key_fits = false;
+    else others *= g.dims[k];
+  }
+  const int64_t nbk64 = (I + kBR - 1) / kBR;
+  if (g.nnz > 0 && !unsorted && nbk64 <= kMaxBk && key_fits && g.nnz < INT32_MAX) {
+    const int nbk = (int)nbk64;
+    DevBuf<unsigned> cnt(c, (size_t)nbk), bstart(c, (size_t)nbk + 1), cur(c, (size_t)nbk);
+    DevBuf<int> istart(c, (size_t)nbk + 3);  // + bucket_sketch's work-unit counter and unit size
+    DevBuf<uint64_t> skey(c, (size_t)g.nnz);
+    DevBuf<char> sval(c, (size_t)g.nnz * (g.vt == DT::F64 ? 8 : 4));
+    cnt.zero();
+    const int gs = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c.num_sms * 2, (g.nnz + kBChunk - 1) / kBChunk));
+    RT_LAUNCH(c, bucket_hist, gs, kBT, 0, g, nnz_dev, mode, nbk, cnt.p);
+    const int gk = c.num_sms * 2;
+    RT_LAUNCH(c, bucket_scan, 1, kScanT, 0, cnt.p, nbk, bstart.p, cur.p, istart.p, istart.p + nbk + 1, gk);
+    unsigned long long *yh = (unsigned long long *)Yf.p, *yl = yh + (size_t)I * ell;
+#define RT_BUCKETED(TV, TN)                                                                                  \
+  do {                                                                                                       \
+    smem_attr(bucket_scatter<TV>, 2 * sizeof(unsigned) * nbk);                                               \
+    RT_LAUNCH(c, bucket_scatter<TV>, gs, kBT, 2 * sizeof(unsigned) * nbk, g, nnz_dev, mode, nbk, cur.p, skey.p,  \
+              (TV *)sval.p);                                                                                 \
+    smem_attr(bucket_sketch<TV, TN>, kBSmem);                                                                \
+    RT_LAUNCH(c, (bucket_sketch<TV, TN>), gk, kBT, kBSmem, skey.p, (const TV *)sval.p, bstart.p, istart.p, nbk, \
+              I, mode, ell, seed, fs, istart.p + nbk + 1, yh, yl);                                           \
+  } while (0)
+    if (g.vt == DT::F64) {
+      RT_BUCKETED(double, double);
+    } else if (normals_f64) {
+      RT_BUCKETED(float, double);
+    } else {
+      RT_BUCKETED(float, float);
+    }
+#undef RT_BUCKETED
+  } else if (g.nnz > 0) {
     constexpr int kW = kCooT / 32;
     const int hot = (int)std::max<int64_t>(1, std::min<int64_t>(32, (200 * 1024) / (2 * kW * ell * 8)));
     const size_t smem = (size_t)2 * kW * hot * ell * sizeof(long long);
@@ -713,6 +1116,38 @@ void coo_select(Ctx &c, const CooDev &in, const int64_t *nnz_dev, int mode, cons
   sels[mode] = sel;
   ls[mode] = l;
   coo_select_modes(c, in, nnz_dev, sels, ls, out_idx, out_vals, nnz_out);
+}
+
+void debug_coo_sketch(Ctx &c, const rtucker_coo_desc *X, int mode, int ell, uint64_t seed, bool normals_f64,
+                      double *Y) {
+  const int d = X->d;
+  const DT vt = X->dtype == RTUCKER_F64 ? DT::F64 : DT::F32;
+  const int64_t nnz = X->nnz;
+  CooDev g;
+  g.d = d;
+  g.nnz = nnz;
+  g.vt = vt;
+  for (int k = 0; k < d; ++k) {
+    RT_REQUIRE(X->dims[k] >= 1 && X->dims[k] <= INT32_MAX, "every dim must lie in [1, 2^31)");
+    RT_REQUIRE(nnz == 0 || X->idx[k] != nullptr, "null index array");
+    g.dims[k] = X->dims[k];
+  }
+  RT_REQUIRE(nnz == 0 || X->vals != nullptr, "null value array");
+  DevBuf<int32_t> ib;
+  DevBuf<unsigned char> vb;
+  if (X->memory == RTUCKER_HOST && nnz > 0) {
+    ib.alloc(c, (size_t)nnz * d);
+    vb.alloc(c, (size_t)nnz * dt_size(vt));
+    for (int k = 0; k < d; ++k)
+      RT_CUDA(cudaMemcpyAsync(ib.p + (size_t)k * nnz, X->idx[k], sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, c.stream));
+    RT_CUDA(cudaMemcpyAsync(vb.p, X->vals, dt_size(vt) * nnz, cudaMemcpyHostToDevice, c.stream));
+    for (int k = 0; k < d; ++k) g.idx[k] = ib.p + (size_t)k * nnz;
+    g.vals = vb.p;
+  } else {
+    for (int k = 0; k < d; ++k) g.idx[k] = X->idx[k];
+    g.vals = X->vals;
+  }
+  sketch_coo(c, g, mode, ell, seed, vt == DT::F64 || normals_f64, Y, nullptr, nullptr);
 }
 
 rtucker_result *run_sparse_sthosvd(Ctx &c, const rtucker_coo_desc *X, const int64_t *ranks, int p, uint64_t seed,

@@ -54,7 +54,7 @@ EXPORTED = [
     "rtucker_rel_error", "rtucker_debug_sketch", "rtucker_debug_omega", "rtucker_debug_philox",
     "rtucker_debug_qr", "rtucker_debug_eig", "rtucker_debug_srrqr", "rtucker_set_profiling",
     "rtucker_phase_times", "rtucker_debug_gram_eig", "rtucker_debug_ttm", "rtucker_debug_loopback_sharding",
-    "rtucker_debug_gemm", "rtucker_debug_gram",
+    "rtucker_debug_gemm", "rtucker_debug_gram", "rtucker_debug_coo_sketch",
 ]
 PHASES = ("sketch", "qr", "bpass", "eig", "shrink", "other")
 
@@ -124,6 +124,7 @@ def load_library(path: str = LIB_PATH):
         "rtucker_debug_qr": (C.c_int, [P, I64, I32, P, P]),
         "rtucker_debug_eig": (C.c_int, [P, I32, P, P, P, C.POINTER(I32)]),
         "rtucker_debug_srrqr": (C.c_int, [P, I64, I32, P, D, P, P, C.POINTER(I32)]),
+        "rtucker_debug_coo_sketch": (C.c_int, [P, C.POINTER(CooDesc), I32, I32, U64, U32, P]),
         "rtucker_debug_gram_eig": (C.c_int, [P, I32, P, P, P, C.POINTER(I32)]),
         "rtucker_debug_ttm": (C.c_int, [P, C.POINTER(DenseDesc), I32, P, I32, U32, P, P]),
         "rtucker_debug_loopback_sharding": (C.c_int, [P, C.c_int]),
@@ -398,8 +399,7 @@ class Context:
                                               self._i32(order), int(seed), int(flags), C.byref(out)))
         return Result(self, out)
 
-    def sparse_sthosvd(self, idx, vals, dims, ranks, p, seed=0, order=None, eta=2.0, flags=0) -> Result:
-        """SP-STHOSVD (Alg 6).  idx: (d, nnz) int32 (torch or numpy, 0-based); vals: values."""
+    def _coo_desc(self, idx, vals, dims):
         d = len(dims)
         desc = CooDesc()
         keep = []
@@ -415,6 +415,11 @@ class Context:
             desc.idx[k] = iptr
             keep.append(ki)
         desc.nnz = int(len(vals))
+        return desc, keep
+
+    def sparse_sthosvd(self, idx, vals, dims, ranks, p, seed=0, order=None, eta=2.0, flags=0) -> Result:
+        """SP-STHOSVD (Alg 6).  idx: (d, nnz) int32 (torch or numpy, 0-based); vals: values."""
+        desc, keep = self._coo_desc(idx, vals, dims)
         self._enter()
         out = C.POINTER(ResultStruct)()
         self._check(self.lib.rtucker_sparse_sthosvd(self.h, C.byref(desc), self._i64(ranks), int(p), int(seed),
@@ -434,6 +439,16 @@ class Context:
         y = torch.empty(int(ell) * int(dims[mode]), dtype=torch.float64, device="cuda")
         self._check(self.lib.rtucker_debug_sketch(self.h, C.byref(desc), int(mode), int(ell), int(k0), int(seed),
                                                   int(flags), y.data_ptr()))
+        self.sync()
+        return y.cpu().numpy().reshape((int(dims[mode]), int(ell)), order="F")
+
+    def debug_coo_sketch(self, idx, vals, dims, mode, ell, seed=0, flags=0):
+        """Y = X_(mode) Omega_mode[:, :ell] of a COO tensor (Alg 6 line 4), fp64 (I_mode x ell)."""
+        torch = _torch()
+        desc, keep = self._coo_desc(idx, vals, dims)
+        y = torch.empty(int(ell) * int(dims[mode]), dtype=torch.float64, device="cuda")
+        self._check(self.lib.rtucker_debug_coo_sketch(self.h, C.byref(desc), int(mode), int(ell), int(seed),
+                                                      int(flags), y.data_ptr()))
         self.sync()
         return y.cpu().numpy().reshape((int(dims[mode]), int(ell)), order="F")
 

@@ -50,6 +50,52 @@ def _check(g, o, eta, a_tol):
     np.testing.assert_array_equal(g.core_vals[gk], np.asarray(o.core_vals)[ok])
 
 
+def _col_err(y, yo):
+    return np.max(np.linalg.norm(y - yo, axis=0) / np.maximum(np.linalg.norm(yo, axis=0), 1e-300))
+
+
+@pytest.mark.parametrize("dtype,flags", [(np.float64, 0), (np.float32, "fp64"), (np.float32, 0)])
+def test_coo_sketch_elementwise(ctx, dtype, flags):
+    """Alg 6 line 4 element by element against the oracle: the row-sorted, lane-segmented
+    fixed-point sketch (sparse.cu) on C5-shaped Zipf counts at 1/100 of the draws (heavy rows
+    spanning many lanes and warps, ragged tails), every mode.  fp64 normals: the fixed-point sum
+    is the exact sum rounded once (R20), so ~1e-13 per column; fp32 normals (R3, RMS 3e-7)."""
+    from paper_1905_07311_b200.rtucker import ACCUM_FP64
+    idx, vals = sparse_zipf(ndraws=500_000, seed=4)
+    vals = vals.astype(dtype)
+    dims = (8000, 8000, 200000, 1200)
+    f = ACCUM_FP64 if flags == "fp64" else 0
+    tol = 1e-6 if (dtype == np.float32 and not f) else 1e-12
+    for j in range(4):
+        y = ctx.debug_coo_sketch(idx, vals, dims, j, 15, seed=5, flags=f)
+        yo = O.sp_sketch(idx, vals, dims, j, 15, seed=5)
+        assert _col_err(y, yo) <= tol, (j, _col_err(y, yo))
+        assert np.all(y[np.abs(yo).sum(axis=1) == 0] == 0.0)      # empty rows stay exactly zero
+
+
+def test_coo_sketch_degenerate(ctx):
+    """Edge cases of the sorted sketch: one row holding every nonzero (one segment across all
+    lanes and warps), a single nonzero, a ragged nnz, ell = 1, 16, 17 and 29 (column passes)."""
+    rng = np.random.default_rng(12)
+    dims = (50, 40, 30)
+    n = 40 * 30
+    heavy = np.array([np.full(n, 7), np.repeat(np.arange(40), 30), np.tile(np.arange(30), 40)])
+    hv = rng.standard_normal(n)
+    cases = [(heavy, hv), (np.array([[3], [2], [1]]), np.array([2.5])),
+             (np.array([rng.integers(0, d_, 1037) for d_ in dims]), rng.standard_normal(1037))]
+    for idx, vals in cases:
+        key = np.ravel_multi_index(idx, dims)
+        _, first = np.unique(key, return_index=True)
+        idx, vals = idx[:, np.sort(first)], vals[np.sort(first)]
+        for ell in (1, 16, 17, 29):
+            for j in range(3):
+                y = ctx.debug_coo_sketch(idx, vals, dims, j, ell, seed=1)
+                yo = O.sp_sketch(idx, vals, dims, j, ell, seed=1)
+                assert _col_err(y, yo) <= 1e-12, (idx.shape, ell, j)
+    y = ctx.debug_coo_sketch(np.zeros((3, 0), np.int32), np.zeros(0), dims, 1, 5, seed=1)
+    assert y.shape == (40, 5) and np.all(y == 0.0)
+
+
 def test_superdiagonal_spec_example(ctx):
     """Superdiagonal 5^3 with (5,4,3,2,1), r=(2,2,2), p=2 -> the 4x4x4 leading sub-tensor."""
     x = superdiagonal([5, 4, 3, 2, 1])

@@ -100,6 +100,24 @@ def test_sp_sparse_matches_dense_route():
             np.testing.assert_allclose(a, b, atol=1e-12)
 
 
+def test_sp_sketch_equals_dense_unfolding_product():
+    """Alg 6 line 4: the COO sketch (Omega rows drawn only for occupied columns, summed per
+    row) equals X_(j) Omega_j with the full dense unfolding and every Omega row; a tensor with
+    an empty slice and a single heavy row covers the degenerate rows."""
+    rng = np.random.default_rng(8)
+    x = rng.standard_normal((7, 6, 5)) * (rng.random((7, 6, 5)) < 0.25)
+    x[3] = 0.0                                               # empty mode-0 row
+    x[5] = rng.standard_normal((6, 5))                       # dense (heavy) mode-0 row
+    idx, vals = _coo(x)
+    for j in range(3):
+        y = O.sp_sketch(idx, vals, x.shape, j, 4, seed=2)
+        xj = O.unfold(x, j)
+        om = O.omega_rows(2, j, np.arange(xj.shape[1]), 4)
+        np.testing.assert_allclose(y, xj @ om, rtol=0, atol=1e-12)
+        if j == 0:
+            assert np.all(y[3] == 0.0)
+
+
 def test_sp_structure_on_zipf_counts():
     """Scaled-down C5 (BASELINE configs[4] recipe): every core entry is an entry of X
     bit-exactly, nnz never increases, A_j[S_j] = I, 1 <= ||A_j||_2 <= g(I_j, l_j)."""
