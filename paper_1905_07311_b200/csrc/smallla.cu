@@ -974,6 +974,79 @@ __device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
+// Gram G = Y^T Y of a tall m x n fp64 matrix (column-major, ld m), n <= 8 NA, on the fp64
+// tensor cores: warp = a run of rows, fragments F_a = Y[k0 + (lane & 3), 8a + (lane >> 2)]
+// serve as both operands of the NA(NA+1)/2 upper 8 x 8 tiles (m8n8k4: A = F_a, B = F_b);
+// the 8 warps of a CTA add into shared memory in warp order, CTA partials are summed in block
+// order by tall_gram_reduce_kernel (deterministic).
+template <int NA>
+__global__ void __launch_bounds__(256) tall_gram_kernel(const double *__restrict__ Y, int64_t m, int n,
+                                                       int64_t rpw, double *__restrict__ part) {
+  constexpr int N8 = 8 * NA, NT = NA * (NA + 1) / 2;
+  __shared__ double buf[N8 * N8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < N8 * N8; t += 256) buf[t] = 0.0;
+  const int64_t r0 = ((int64_t)blockIdx.x * 8 + warp) * rpw, r1 = min(m, r0 + rpw);
+  double acc[NT][2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+  const int kr = lane & 3, cr = lane >> 2;
+#pragma unroll 4
+  for (int64_t k0 = r0; k0 < r1; k0 += 4) {
+    const int64_t row = k0 + kr;
+    double f[NA];
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      const int col = 8 * a + cr;
+      f[a] = (row < r1 && col < n) ? Y[(int64_t)col * m + row] : 0.0;
+    }
+    int t = 0;
+#pragma unroll
+    for (int a = 0; a < NA; ++a)
+#pragma unroll
+      for (int b = a; b < NA; ++b, ++t) dmma884(acc[t][0], acc[t][1], f[a], f[b]);
+  }
+  for (int w = 0; w < 8; ++w) {
+    __syncthreads();
+    if (warp == w) {
+      int t = 0;
+#pragma unroll
+      for (int a = 0; a < NA; ++a)
+#pragma unroll
+        for (int b = a; b < NA; ++b, ++t) {
+          const int i = 8 * a + cr, j = 8 * b + 2 * kr;  // C fragment: row lane >> 2, cols 2 (lane & 3) + {0, 1}
+          buf[i * N8 + j] += acc[t][0];
+          buf[i * N8 + j + 1] += acc[t][1];
+        }
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < N8 * N8; t += 256) part[(int64_t)blockIdx.x * N8 * N8 + t] = buf[t];
+}
+// G (n x n, column-major, both triangles) = sum over the CTA partials in block order
+__global__ void tall_gram_reduce_kernel(const double *__restrict__ part, int nblk, int n, int n8,
+                                        double *__restrict__ G) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n * n) return;
+  int i = e % n, j = e / n;
+  if (i > j) { const int t = i; i = j; j = t; }  // upper tile entry (i <= j)
+  double s = 0.0;
+  for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * n8 * n8 + i * n8 + j];
+  G[e] = s;
+}
+
+void tall_gram(Ctx &c, const double *Y, int64_t m, int n, double *G) {
+  RT_REQUIRE(n >= 1 && n <= 64, "tall_gram: 1 <= n <= 64");
+  const int64_t rpw = std::max<int64_t>(64, ((m + (int64_t)c.num_sms * 64 - 1) / ((int64_t)c.num_sms * 64) + 3) / 4 * 4);
+  const int nblk = (int)((m + 8 * rpw - 1) / (8 * rpw));
+  const int na = (n + 7) / 8, n8 = 8 * (na <= 2 ? 2 : (na <= 4 ? 4 : 8));
+  DevBuf<double> part(c, (size_t)nblk * n8 * n8);
+  if (na <= 2) RT_LAUNCH(c, tall_gram_kernel<2>, nblk, 256, 0, Y, m, n, rpw, part.p);
+  else if (na <= 4) RT_LAUNCH(c, tall_gram_kernel<4>, nblk, 256, 0, Y, m, n, rpw, part.p);
+  else RT_LAUNCH(c, tall_gram_kernel<8>, nblk, 256, 0, Y, m, n, rpw, part.p);
+  RT_LAUNCH(c, tall_gram_reduce_kernel, ceil_div(n * n, 256), 256, 0, part.p, nblk, n, n8, G);
+}
+
 __device__ __forceinline__ void cluster_arrive() {
   asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 }
@@ -1539,7 +1612,7 @@ void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
     const double *src = Y;
     for (int pass = 0; pass < 2; ++pass) {
       double *dst = pass == 0 ? Q1.p : Q;
-      mode_gram(c, src, DT::F64, ModeView{m, n, 1}, G.p);
+      tall_gram(c, src, m, n, G.p);
       RT_LAUNCH(c, chol_inv_kernel, 1, 256, csm, G.p, n, Ri.p, bad.p);
       RT_LAUNCH(c, trsm_rows_kernel, std::max(1, std::min(c.num_sms * 8, ceil_div(m, 128))), 128,
                 sizeof(double) * n * n, src, m, n, Ri.p, dst, bad.p);

@@ -240,7 +240,7 @@ constexpr uint64_t kKeyMask = (1ull << 56) - 1;
 
 __global__ void __launch_bounds__(kBT) bucket_hist(CooDev g, const int64_t *__restrict__ nnz_dev, int mode, int nbk,
                                                   unsigned *__restrict__ gcnt) {
-  __shared__ unsigned cnt[kMaxBk];
+  extern __shared__ unsigned cnt[];  // nbk
   for (int t = threadIdx.x; t < nbk; t += kBT) cnt[t] = 0;
   __syncthreads();
   const int64_t nnz = nnz_dev ? *nnz_dev : g.nnz;
@@ -890,40 +890,59 @@ template <typename TV>
 __global__ void __launch_bounds__(kCompactB) compact_scatter(CooDev in, const int64_t *__restrict__ nnz_dev, LutSet ls,
                                                              const int64_t *__restrict__ offs,
                                                              int32_t *const *__restrict__ oidx, TV *__restrict__ ovals) {
-  __shared__ int wsum[32];
+  // steps of 4 kCompactB entries, thread t owning the 4 consecutive entries 4t .. 4t + 3 of
+  // the step: survivors' offsets from a warp scan of the per-thread counts and a scan of the
+  // 32 warp totals (2 barriers per step)
+  __shared__ int wsum[33];
   __shared__ int64_t base;
   int64_t b0, b1;
   compact_range(*nnz_dev, b0, b1);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) base = offs[blockIdx.x];
-  for (int64_t s0 = b0; s0 < b1; s0 += kCompactB) {
-    const int64_t e = s0 + threadIdx.x;
-    const int keep = (e < b1 && keep_entry(in, ls, e)) ? 1 : 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    __syncthreads();  // base / wsum of the previous step consumed
-    if (lane == 0) wsum[w] = __popc(bal);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int acc = 0;
-      for (int k = 0; k < kCompactB / 32; ++k) {
-        const int x = wsum[k];
-        wsum[k] = acc;
-        acc += x;
+  for (int64_t s0 = b0; s0 < b1; s0 += 4 * kCompactB) {
+    const int64_t e0 = s0 + 4 * (int64_t)threadIdx.x;
+    bool keep[4];
+    int cnt = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      keep[k] = e0 + k < b1 && keep_entry(in, ls, e0 + k);
+      cnt += keep[k] ? 1 : 0;
+    }
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();  // wsum written; base of this step visible
+    if (w == 0) {
+      const int x = wsum[lane];
+      int xi = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, xi, o);
+        if (lane >= o) xi += y;
       }
-      wsum[31] += 0;
+      wsum[lane] = xi - x;
+      if (lane == 31) wsum[32] = xi;
     }
     __syncthreads();
-    const int64_t o = base + wsum[w] + __popc(bal & ((1u << lane) - 1u));
-    if (keep) {
-      for (int k = 0; k < in.d; ++k) {
-        const int32_t i = in.idx[k][e];
-        oidx[k][o] = ls.lut[k] ? ls.lut[k][i] : i;
+    int64_t o = base + wsum[w] + inc - cnt;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (keep[k]) {
+        const int64_t e = e0 + k;
+        for (int m = 0; m < in.d; ++m) {
+          const int32_t i = in.idx[m][e];
+          oidx[m][o] = ls.lut[m] ? ls.lut[m][i] : i;
+        }
+        ovals[o] = ((const TV *)in.vals)[e];
+        ++o;
       }
-      ovals[o] = ((const TV *)in.vals)[e];
     }
-    __syncthreads();
-    if (threadIdx.x == kCompactB - 1) base = o + (keep ? 1 : 0);  // last thread: offset after this step
-    __syncthreads();
+    __syncthreads();  // base and wsum consumed
+    if (threadIdx.x == 0) base += wsum[32];
   }
 }
 
@@ -1008,8 +1027,10 @@ void sketch_coo(Ctx &c, const CooDev &g, int mode, int ell, uint64_t seed, bool 
     DevBuf<uint64_t> skey(c, (size_t)g.nnz);
     DevBuf<char> sval(c, (size_t)g.nnz * (g.vt == DT::F64 ? 8 : 4));
     cnt.zero();
-    const int gs = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c.num_sms * 2, (g.nnz + kBChunk - 1) / kBChunk));
-    RT_LAUNCH(c, bucket_hist, gs, kBT, 0, g, nnz_dev, mode, nbk, cnt.p);
+    // latency-bound streaming passes: 8 CTAs (64 warps) per SM in flight
+    const int gs = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c.num_sms * 8, (g.nnz + kBChunk - 1) / kBChunk));
+    smem_attr(bucket_hist, sizeof(unsigned) * nbk);
+    RT_LAUNCH(c, bucket_hist, gs, kBT, sizeof(unsigned) * nbk, g, nnz_dev, mode, nbk, cnt.p);
     const int gk = c.num_sms * 2;
     RT_LAUNCH(c, bucket_scan, 1, kScanT, 0, cnt.p, nbk, bstart.p, cur.p, istart.p, istart.p + nbk + 1, gk);
     unsigned long long *yh = (unsigned long long *)Yf.p, *yl = yh + (size_t)I * ell;
