@@ -1023,16 +1023,20 @@ __global__ void __launch_bounds__(256) tall_gram_kernel(const double *__restrict
   __syncthreads();
   for (int t = threadIdx.x; t < N8 * N8; t += 256) part[(int64_t)blockIdx.x * N8 * N8 + t] = buf[t];
 }
-// G (n x n, column-major, both triangles) = sum over the CTA partials in block order
+// G (n x n, column-major, both triangles) = sum over the CTA partials: one CTA per entry, a fixed
+// partition of the partials over its threads and a fixed-shape tree (deterministic)
 __global__ void tall_gram_reduce_kernel(const double *__restrict__ part, int nblk, int n, int n8,
                                         double *__restrict__ G) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n * n) return;
+  __shared__ double sr[4];
+  const int e = blockIdx.x;
   int i = e % n, j = e / n;
   if (i > j) { const int t = i; i = j; j = t; }  // upper tile entry (i <= j)
   double s = 0.0;
-  for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * n8 * n8 + i * n8 + j];
-  G[e] = s;
+  for (int b = threadIdx.x; b < nblk; b += 128) s += part[(int64_t)b * n8 * n8 + i * n8 + j];
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sr[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) G[e] = (sr[0] + sr[1]) + (sr[2] + sr[3]);
 }
 
 void tall_gram(Ctx &c, const double *Y, int64_t m, int n, double *G) {
@@ -1044,7 +1048,7 @@ void tall_gram(Ctx &c, const double *Y, int64_t m, int n, double *G) {
   if (na <= 2) RT_LAUNCH(c, tall_gram_kernel<2>, nblk, 256, 0, Y, m, n, rpw, part.p);
   else if (na <= 4) RT_LAUNCH(c, tall_gram_kernel<4>, nblk, 256, 0, Y, m, n, rpw, part.p);
   else RT_LAUNCH(c, tall_gram_kernel<8>, nblk, 256, 0, Y, m, n, rpw, part.p);
-  RT_LAUNCH(c, tall_gram_reduce_kernel, ceil_div(n * n, 256), 256, 0, part.p, nblk, n, n8, G);
+  RT_LAUNCH(c, tall_gram_reduce_kernel, n * n, 128, 0, part.p, nblk, n, n8, G);
 }
 
 __device__ __forceinline__ void cluster_arrive() {

@@ -1081,11 +1081,13 @@ void srrqr(Ctx &c, const double *Q, int64_t m, int l, double eta, int64_t *sel_d
   smem_attr(srrqr_coop_kernel, smem);
   int per_sm = 0;
   RT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, srrqr_coop_kernel, kSrT, smem));
+  // every resident CTA: a maxvol round recomputes A = Q Q_S^{-1} (m l^2 flops); one CTA per SM
+  // (cheaper grid barriers) measured slower on C5's 200000-row mode (0.98 vs 0.59 ms)
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c.num_sms * std::max(per_sm, 1),
                                                                (m + kSrT - 1) / kSrT));
-  DevBuf<double> r(c, (size_t)m * l), pv(c, grid);
+  DevBuf<double> r(c, (size_t)m * l), pv(c, 2 * (size_t)grid);
   DevBuf<int> mark(c, m);
-  DevBuf<int64_t> pi(c, grid);
+  DevBuf<int64_t> pi(c, 2 * (size_t)grid);
   DevBuf<int> swl;
   if (!swaps_dev) {
     swl.alloc(c, 1);
