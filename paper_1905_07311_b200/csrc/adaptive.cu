@@ -31,6 +31,7 @@
 #include "comm.h"
 #include "kernels_extra.h"
 #include "orchestrate.h"
+#include "philox.cuh"
 
 namespace rt {
 
@@ -59,6 +60,290 @@ __global__ void sub_gemm_kernel(double *__restrict__ W, int64_t m, int b, const 
     for (int t = 0; t < k; ++t) s += Q[i + m * t] * T[t + (int64_t)k * j];
     W[e] -= s;
   }
+}
+
+// ---------------------------------------------------------------------------------------
+// Fused block pass for fp64 cores (SURVEY §3.3 "B_i + next sketch"): ONE read of G_(n) gives
+//   B_i     = Q_i^T G_(n)                      (b x P, stored (L, b, R)) and its Gram, and
+//   W_{i+1} = G_(n) Omega(:, k1 : k1 + b1)     (I x b1, the next block's sketch)
+// where the next sketch is formed before the stop test of block i decides whether it is needed
+// (a wasted product on the last block of a mode).  G is (L, I, R), column p = l + L r; a tile is
+// 32 consecutive l of one r, streamed in chunks of 32 rows i through a cp.async ring.  Per chunk
+// (fp64 tensor cores, m8n8k4, one 8 x 8 output tile per warp and product):
+//   B tile (16 j x 32 l) += Q_c^T (16 x 32 i) G_c (32 i x 32 l)    accumulated over the tile
+//   W rows (32 i x 16 j') += G_c (32 i x 32 l) Omega_t (32 l x 16 j') into shared W (I x 16)
+// Omega_t is generated per tile by the sketch's Philox stream (same counter layout as
+// sketch_dfma_kernel).  Per-CTA W and Gram partials are summed in a fixed order afterwards.
+constexpr int kFT = 256;              // threads
+constexpr int kFS = 5;                // ring stages
+constexpr int kFL = 64;               // columns l per tile
+constexpr int kFG = kFL + 4;          // G chunk row stride (doubles, = 4 mod 16: conflict-free fragments)
+constexpr int kFQ = 20;               // Q chunk / Omega row stride (= 4 mod 16)
+constexpr int kFStage = 32 * kFG + 32 * kFQ;  // doubles per stage (G chunk + Q chunk)
+__host__ __device__ constexpr int fused_ys(int bb1) { return bb1 <= 12 ? 12 : 16; }  // W row stride
+__host__ __device__ constexpr size_t fused_smem(int64_t I, int ys) {
+  return sizeof(double) * ((size_t)kFS * kFStage + kFL * kFQ + 16 * (kFL + 1) + (size_t)I * ys);
+}
+
+__device__ __forceinline__ void cp_async8(unsigned d, const double *src, bool ok) {
+  const int n = ok ? 8 : 0;  // src-size 0: zero fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(ok ? src : nullptr), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async16(unsigned d, const double *src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(bytes ? src : nullptr), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void dmma(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <typename TN, bool V16>
+__global__ void __launch_bounds__(kFT, 1) adapt_fused_kernel(const double *__restrict__ G, int64_t L, int64_t I, int64_t R,
+                                                           const double *__restrict__ Q, int bb, uint64_t seed, int mode,
+                                                           int64_t k1, int bb1, int64_t col_offset, int ys,
+                                                           double *__restrict__ Bi, double *__restrict__ ypart,
+                                                           double *__restrict__ gpart) {
+  extern __shared__ __align__(16) double fsm[];
+  double *ring = fsm;                        // kFS x (G chunk [32][kFG], Q chunk [32][kFQ])
+  double *Om = ring + kFS * kFStage;         // [kFL l][kFQ]
+  double *Bs = Om + kFL * kFQ;               // [16 j][kFL + 1]
+  double *Ys = Bs + 16 * (kFL + 1);          // [I][ys]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fa = lane & 3, fb = lane >> 2;
+  const int64_t ntl = (L + kFL - 1) / kFL, ntiles = ntl * R, nch = (I + 31) / 32;
+  for (int64_t e = tid; e < I * ys; e += kFT) Ys[e] = 0.0;
+  // this CTA's tiles: blockIdx.x + t gridDim.x; steps = tiles x chunks.  Tile and chunk of the
+  // consumed and of the issued step advance incrementally (no 64-bit divisions per step).
+  const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const int64_t nsteps = my_tiles * nch;
+  struct Cursor {
+    int64_t t, r, l0, ch;
+  };
+  auto set_tile = [&](Cursor &cu, int64_t t) {
+    cu.t = t;
+    cu.r = t / ntl;
+    cu.l0 = (t - cu.r * ntl) * kFL;
+    cu.ch = 0;
+  };
+  auto advance = [&](Cursor &cu) {
+    if (++cu.ch == nch) set_tile(cu, cu.t + gridDim.x);
+  };
+  // G chunk copies: V16 (L even, G 16-byte aligned): pairs of l per 16-byte cp.async, else 8-byte
+  constexpr int kGW = V16 ? 2 : 1;                 // doubles per copy
+  constexpr int kGQ = 32 * kFL / (kFT * kGW);      // copies per thread and chunk
+  int64_t goff[kGQ];
+  int gll[kGQ], gii[kGQ];
+  const unsigned ring_s = (unsigned)__cvta_generic_to_shared(ring);
+#pragma unroll
+  for (int q = 0; q < kGQ; ++q) {
+    const int e = (tid + kFT * q) * kGW;
+    gii[q] = e / kFL;
+    gll[q] = e % kFL;
+    goff[q] = gll[q] + L * gii[q];
+  }
+  const int qii0 = tid >> 4, qj = tid & 15;  // Q chunk elements (qii0, qj) and (qii0 + 16, qj)
+  Cursor ic;  // issue cursor
+  set_tile(ic, blockIdx.x);
+  int64_t is = 0;
+  auto issue = [&]() {
+    if (is < nsteps) {
+      const int64_t i0 = ic.ch * 32;
+      const unsigned st = ring_s + (unsigned)((is % kFS) * kFStage * sizeof(double));
+      const double *gb = G + ic.l0 + L * (i0 + I * ic.r);
+      const int64_t lrem = L - ic.l0, irem = I - i0;
+#pragma unroll
+      for (int q = 0; q < kGQ; ++q) {  // G chunk: 32 rows i x kFL l, coalesced along l
+        const unsigned d = st + (unsigned)((gii[q] * kFG + gll[q]) * sizeof(double));
+        if constexpr (V16) {
+          const int nv = gii[q] < irem ? (int)min((int64_t)2, max((int64_t)0, lrem - gll[q])) : 0;
+          cp_async16(d, gb + goff[q], 8 * nv);
+        } else {
+          cp_async8(d, gb + goff[q], gii[q] < irem && gll[q] < lrem);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {  // Q chunk: 32 rows i x 16 j
+        const int ii = qii0 + 16 * q;
+        const bool ok = (ii < irem) && (qj < bb);
+        cp_async8(st + (unsigned)((32 * kFG + ii * kFQ + qj) * sizeof(double)), Q + (i0 + ii) + I * qj, ok);
+      }
+      advance(ic);
+    }
+    ++is;
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (int s = 0; s < kFS - 1; ++s) issue();
+  // Work split (every G element is read from shared memory once per product):
+  //   B: warp w takes rows 4w .. 4w + 3 of the chunk (one k-step) for all 64 l and both j
+  //      blocks; the 8 partial B tiles are summed in warp order at the tile's end
+  //   W: warp w takes the 8-row block (w & 3) and the l half (w >> 2) for both j' blocks; the
+  //      second half adds its partial after the next barrier (other rows: no conflict), Omega's
+  //      fragments stay in registers for the whole tile
+  double bacc[2][8][2];
+#pragma unroll
+  for (int m = 0; m < 2; ++m)
+#pragma unroll
+    for (int u = 0; u < 8; ++u) bacc[m][u][0] = bacc[m][u][1] = 0.0;
+  double gacc = 0.0;                          // Gram entry (tid >> 4, tid & 15)
+  const int ymt = warp & 3, yh = warp >> 2;   // W: row block, l half
+  double omr[8][2];                           // Omega fragments of this warp's l half
+  double ypend[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  int64_t ypend_i = -1;
+  auto add_y = [&](int64_t i, const double (&y)[2][2]) {
+    if (i < 0 || i >= I) return;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      const int jc = 8 * nt + 2 * fa;
+      if (jc < bb1) Ys[i * ys + jc] += y[nt][0];
+      if (jc + 1 < bb1) Ys[i * ys + jc + 1] += y[nt][1];
+    }
+  };
+  Cursor cc;  // consume cursor
+  set_tile(cc, blockIdx.x);
+  for (int64_t s = 0; s < nsteps; ++s, advance(cc)) {
+    const int64_t r = cc.r, l0 = cc.l0, ch = cc.ch, i0 = ch * 32;
+    asm volatile("cp.async.wait_group %0;" ::"n"(kFS - 2) : "memory");
+    __syncthreads();     // chunk s visible to all; every warp is past step s - 1
+    issue();             // into the stage consumed at step s - 1
+    if (yh == 1) {       // the second l half's partial of step s - 1 (rows differ from step s's: nch >= 2)
+      add_y(ypend_i, ypend);
+      ypend_i = -1;
+    }
+    if (ch == 0 && bb1 > 0) {  // Omega rows of this tile: p = l0 + ll + L r, columns k1 .. k1 + bb1
+      const int64_t jb0 = k1 >> 2;
+      const int nb = (int)(((k1 + bb1 - 1) >> 2) - jb0 + 1);
+      for (int e = tid; e < kFL * nb; e += kFT) {
+        const int ll = e / nb, jb = e % nb;
+        const bool lok = l0 + ll < L;
+        const uint64_t p = (uint64_t)(l0 + ll + L * r + col_offset);
+        const uint4 w = omega_words(seed, mode, 0, p, (uint32_t)(jb0 + jb));
+        Normal4<TN> z(w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t kk = 4 * (jb0 + jb) + q - k1;
+          if (kk >= 0 && kk < bb1) Om[ll * kFQ + kk] = lok ? (double)z.v[q] : 0.0;
+        }
+      }
+      for (int e = tid; e < kFL * 16; e += kFT)  // unused columns stay zero (disjoint entries)
+        if ((e & 15) >= bb1) Om[(e >> 4) * kFQ + (e & 15)] = 0.0;
+      __syncthreads();
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) omr[ks][nt] = Om[(4 * (8 * yh + ks) + fa) * kFQ + 8 * nt + fb];
+    }
+    const double *Gc = ring + (s % kFS) * kFStage, *Qc = Gc + 32 * kFG;
+    {  // B partial += Q_c(rows 4w..)^T G_c(rows 4w.., all l)
+      const double a0 = Qc[(4 * warp + fa) * kFQ + fb], a1 = Qc[(4 * warp + fa) * kFQ + 8 + fb];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const double b = Gc[(4 * warp + fa) * kFG + 8 * u + fb];
+        dmma(bacc[0][u][0], bacc[0][u][1], a0, b);
+        dmma(bacc[1][u][0], bacc[1][u][1], a1, b);
+      }
+    }
+    if (bb1 > 0) {  // W rows (8 ymt ..) += G_c(rows, l half) Omega(l half, :)
+      double y[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const double a = Gc[(8 * ymt + fb) * kFG + 4 * (8 * yh + ks) + fa];
+        dmma(y[0][0], y[0][1], a, omr[ks][0]);
+        dmma(y[1][0], y[1][1], a, omr[ks][1]);
+      }
+      const int64_t i = i0 + 8 * ymt + fb;
+      if (yh == 0) {
+        add_y(i, y);
+      } else {
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) { ypend[nt][0] = y[nt][0]; ypend[nt][1] = y[nt][1]; }
+        ypend_i = i;
+      }
+    }
+    if (ch == nch - 1) {  // tile complete: sum the warps' B partials, store B_i, its Gram
+      const int LB = kFL + 1;
+      for (int w = 0; w < kFT / 32; ++w) {
+        if (warp == w) {
+#pragma unroll
+          for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                double &d = Bs[(8 * m + fb) * LB + 8 * u + 2 * fa + h];
+                d = (w == 0 ? 0.0 : d) + bacc[m][u][h];
+                bacc[m][u][h] = 0.0;
+              }
+        }
+        __syncthreads();
+      }
+      for (int e = tid; e < 16 * kFL; e += kFT) {
+        const int j = e / kFL, ll = e % kFL;
+        if (j < bb && l0 + ll < L) Bi[(l0 + ll) + L * (j + (int64_t)bb * r)] = Bs[j * LB + ll];
+      }
+      const int gj = tid >> 4, gk = tid & 15;
+      double sacc = 0.0;
+#pragma unroll 8
+      for (int ll = 0; ll < kFL; ++ll) sacc = fma(Bs[gj * LB + ll], Bs[gk * LB + ll], sacc);
+      gacc += sacc;
+      // Bs is rewritten at the next tile's end, >= 1 barrier later
+    }
+  }
+  __syncthreads();
+  if (yh == 1) add_y(ypend_i, ypend);
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  double *yp = ypart + (int64_t)blockIdx.x * I * ys;
+  for (int64_t e = tid; e < I * ys; e += kFT) yp[e] = Ys[e];
+  gpart[(int64_t)blockIdx.x * 256 + tid] = gacc;
+}
+
+// W (I x b1, column-major) and gram (bb x bb) from the per-CTA partials, summed in CTA order
+__global__ void fused_reduce_kernel(const double *__restrict__ ypart, const double *__restrict__ gpart, int nblk,
+                                    int64_t I, int bb1, int bb, int ys, double *__restrict__ W, double *__restrict__ gram) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < I * bb1) {
+    const int64_t i = e % I;
+    const int j = (int)(e / I);
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += ypart[((int64_t)b * I + i) * ys + j];
+    W[e] = s;
+  } else if (e < I * bb1 + bb * bb) {
+    const int f = (int)(e - I * bb1), j = f % bb, k = f / bb;
+    double s = 0.0;
+    for (int b = 0; b < nblk; ++b) s += gpart[(int64_t)b * 256 + j * 16 + k];
+    gram[f] = s;
+  }
+}
+
+bool fused_ok(const ModeView &v, int bb) {
+  static const bool off = RT_EXP_GETENV("RTUCKER_ADAPT_UNFUSED") != nullptr;
+  return !off && v.L >= 32 && v.I > 32 && bb <= 16 && fused_smem(v.I, fused_ys(bb)) <= 225 * 1024;
+}
+
+// B_i (and its Gram) and, when bb1 > 0, the next block's sketch W1 in one pass over G (fp64)
+void fused_block(Ctx &c, const double *G, const ModeView &v, int n, const double *Qi, int bb, uint64_t seed,
+                 int64_t k1, int bb1, int64_t col_offset, bool normals_f32, double *Bi, double *gram, double *W1) {
+  const int grid = c.num_sms;
+  const int ys = fused_ys(bb1);
+  const size_t smem = fused_smem(v.I, ys);
+  DevBuf<double> yp(c, (size_t)grid * v.I * ys), gp(c, (size_t)grid * 256);
+  const bool v16 = (v.L % 2 == 0) && ((uintptr_t)G % 16 == 0);
+#define RT_FUSED(TN, V)                                                                                     \
+  do {                                                                                                      \
+    smem_attr(adapt_fused_kernel<TN, V>, smem);                                                             \
+    RT_LAUNCH(c, (adapt_fused_kernel<TN, V>), grid, kFT, smem, G, v.L, v.I, v.R, Qi, bb, seed, n, k1, bb1,  \
+              col_offset, ys, Bi, yp.p, gp.p);                                                              \
+  } while (0)
+  if (normals_f32) {
+    if (v16) RT_FUSED(float, true); else RT_FUSED(float, false);
+  } else {
+    if (v16) RT_FUSED(double, true); else RT_FUSED(double, false);
+  }
+#undef RT_FUSED
+  const int64_t tot = v.I * bb1 + (int64_t)bb * bb;
+  RT_LAUNCH(c, fused_reduce_kernel, ceil_div(tot, 256), 256, 0, yp.p, gp.p, grid, v.I, bb1, bb, ys, W1, gram);
 }
 
 struct ModeOut {
@@ -139,13 +424,21 @@ ModeOut adapt_mode(Ctx &c, const void *G, DT gt, const int64_t *cur, const int64
   DevBuf<double> scal(c, 4), T(c, (size_t)cap * block);
   double E = gn2;
   int k = 0;
+  // fp64 cores: B_i and the next block's sketch in one pass over G (fused_block)
+  const bool fused = gt == DT::F64 && store == DT::F64 && !sh.rows && fused_ok(v, block);
+  DevBuf<double> Wn;  // next block's sketch from the fused pass (local partial when sharded)
+  int wn_cols = 0;
   while (true) {
     if (E <= tau2 || k >= cap) break;
     const int bb = std::min(block, cap - k);
     DevBuf<double> W(c, (size_t)I * bb + 1);
     {
       PhaseScope ps(c, PH_SKETCH, n);
-      if (!sh.rows) {
+      if (wn_cols == bb) {  // formed by the previous block's fused pass
+        std::swap(W, Wn);
+        wn_cols = 0;
+        if (sh.on) allreduce_sum_f64(c, W.p, (size_t)I * bb);
+      } else if (!sh.rows) {
         sketch_dense(c, G, gt, v, n, bb, k, seed, sh.col_offset, mul_f64, W.p, nullptr, fp32_data);
         if (sh.on) allreduce_sum_f64(c, W.p, (size_t)I * bb);
       } else {
@@ -171,7 +464,14 @@ ModeOut adapt_mode(Ctx &c, const void *G, DT gt, const int64_t *cur, const int64
     // B_i = Q_i^T G_(n) written into rows k..k+bb of B (L, cap, R) via a strided copy
     DevBuf<double> gram(c, (size_t)bb * bb);
     DevBuf<unsigned char> Bi(c, (size_t)v.L * bb * v.R * dt_size(store));
-    if (!sh.rows) {
+    if (fused) {
+      const int bb1 = std::max(0, std::min(block, cap - (k + bb)));
+      Wn.alloc(c, (size_t)I * std::max(bb1, 1) + 1);
+      fused_block(c, (const double *)G, v, n, Qi, bb, seed, k + bb, bb1, sh.col_offset, fp32_data, (double *)Bi.p,
+                  gram.p, Wn.p);
+      wn_cols = bb1;
+      if (sh.on) allreduce_sum_f64(c, gram.p, (size_t)bb * bb);
+    } else if (!sh.rows) {
       ttm_dense(c, G, gt, v, Qi, I, bb, Bi.p, store, mul_f64, gram.p, colmax.p);
       if (sh.on) allreduce_sum_f64(c, gram.p, (size_t)bb * bb);
     } else {
