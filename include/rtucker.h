@@ -299,6 +299,16 @@ rtucker_status rtucker_debug_eig(rtucker_ctx *ctx, int32_t n, const double *A, d
 rtucker_status rtucker_debug_gram_eig(rtucker_ctx *ctx, int32_t n, const double *A, double *w, double *V,
                                       int32_t *sweeps_out /* host, may be NULL */);
 
+/* The same eigensolver as the hot path selects it for a Gram of fp32 data (rel_acc = 0) or fp64
+ * data (rel_acc = 1), the wanted rank r_need deciding its fallback (Alg 1 line 4).  For
+ * rel_acc = 0 and 32 < n <= 64 this is the mixed-precision solver (fp32 Jacobi on the pivoted
+ * Cholesky factor, then fp64 Newton refinement on the tensor cores), eigenvectors to
+ * ~eps w_0 / gap; *sweeps_out = fp32 sweeps + 1000 x refinement steps, or the fp64 Jacobi's
+ * sweep count when the fallback ran (DEVICE pointers; EINVAL for n < 1 or r_need < 1). */
+rtucker_status rtucker_debug_gram_eig_ex(rtucker_ctx *ctx, int32_t n, const double *A, double *w, double *V,
+                                         int32_t *sweeps_out /* host, may be NULL */, int32_t rel_acc,
+                                         int32_t r_need);
+
 /* C (m x n) = op(A) op(B), fp64 column-major on the tensor cores (the library's GEMM for the
  * adaptive truncation and the eigensolver), DEVICE pointers; trans* != 0 transposes. */
 rtucker_status rtucker_debug_gemm(rtucker_ctx *ctx, int transA, int transB, int64_t m, int64_t n, int64_t k,

@@ -647,11 +647,104 @@ __device__ __forceinline__ void jac_half(double (&own)[kV], const double (&oth)[
   }
 }
 
+// Pivoted Cholesky of the np x np Gram G (column-major, shared memory) without row exchanges,
+// left-looking, one CTA barrier per step (256 threads: 4 per row):
+//   p = argmax of the remaining diagonal d (first index on ties; every warp evaluates it
+//   redundantly from d in shared memory, so no barrier publishes it), stop once d_p <= n eps
+//   max diag(G);  M[i, k] = (G[i, p] - sum_{k' < k} M[i, k'] M[p, k']) / sqrt(d_p) on the rows
+//   not yet pivoted (4 threads per row split the dot product), d_i -= M[i, k]^2.
+//   M = P L (P the pivot permutation): its columns have the preconditioning of L, and
+//   M M^T = G in the original index order.  (Right-looking with a rank-1 update of G and a
+//   separate pivot pass cost 3 barriers and ~2100 cycles per step: 125k cycles at n = 60.)
+// M (ldm x >= np) must be zero on entry; lc, lam: np-double scratch each.  Returns the number
+// of pivots taken (the numerical rank); the columns of M beyond it stay zero.
+__device__ int chol_pivoted_left(const double *__restrict__ G, int np, int n, double *__restrict__ M, int ldm,
+                                 double *__restrict__ lc, double *__restrict__ lam, int ldg) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  // remaining diagonal, double-buffered (step k reads lc / lam by parity, writes the other); -inf
+  // marks a pivoted (or padding) row; a remaining diagonal that rounds below zero stays live
+  for (int i = tid; i < np; i += blockDim.x) lc[i] = i < n ? G[i + ldg * i] : -INFINITY;
+  double dmax = 0.0;
+  for (int i = lane; i < n; i += 32) dmax = fmax(dmax, G[i + ldg * i]);
+  for (int o = 16; o; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+  const double thresh = n * 2.2e-16 * dmax;
+  __syncthreads();
+  const int ci = tid >> 2, cs = tid & 3;  // row ci, dot-product quarter cs
+#ifdef RTUCKER_EIG_PROF_BUILD
+  long long cpa[5] = {0, 0, 0, 0, 0}, cpt = clock64();
+#define CHP(i) { const long long t_ = clock64(); cpa[i] += t_ - cpt; cpt = t_; }
+#else
+#define CHP(i)
+#endif
+  int k = 0;
+  for (; k < n; ++k) {
+    CHP(0);
+    const double *dc = (k & 1) ? lam : lc;
+    double *dnx = (k & 1) ? lc : lam;
+    // pivot = argmax of the remaining diagonal to fp32 resolution by ONE warp reduction: key =
+    // fp32 bits of d_i (non-negative floats order like their bit patterns) with the low 6 bits
+    // replaced by 63 - i (ties, and values equal to 2^-17 relative, go to the smallest index);
+    // the pivot only has to be near-maximal (for the grading), and the choice is deterministic.
+    // Negative entries (pivoted rows, diagonals rounded below 0) count as 0.  (Three dependent
+    // redux.sync for the exact fp64 maximum cost ~700 cycles per step.)
+    uint32_t key = 0;
+    for (int i = lane; i < n; i += 32) {
+      const double v = dc[i];
+      const uint32_t kb = v > 0.0 ? ((__float_as_uint((float)v) & ~63u) | (uint32_t)(63 - i)) : 0u;
+      key = max(key, kb);
+    }
+    key = __reduce_max_sync(0xffffffffu, key);
+    const int bi = 63 - (int)(key & 63u);
+    const double bv = key ? dc[bi] : 0.0;
+    if (!(bv > thresh)) break;  // rank reached (same decision in every warp): the rest of M is zero
+    const int p = bi;
+    double inv;  // bv^{-1/2}: approximate rsqrt + two Newton steps (no slow-path subroutine)
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(bv));
+    inv = inv * fma(-0.5 * bv * inv, inv, 1.5);
+    inv = inv * fma(-0.5 * bv * inv, inv, 1.5);
+    CHP(1);
+    double dot = 0.0;
+    if (ci < np) {  // four independent chains (loads of 4 steps in flight)
+      double d1 = 0.0, d2 = 0.0, d3 = 0.0;
+      int kk = cs;
+      for (; kk + 12 < k; kk += 16) {
+        dot = fma(M[ci + ldm * kk], M[p + ldm * kk], dot);
+        d1 = fma(M[ci + ldm * (kk + 4)], M[p + ldm * (kk + 4)], d1);
+        d2 = fma(M[ci + ldm * (kk + 8)], M[p + ldm * (kk + 8)], d2);
+        d3 = fma(M[ci + ldm * (kk + 12)], M[p + ldm * (kk + 12)], d3);
+      }
+      for (; kk < k; kk += 4) dot = fma(M[ci + ldm * kk], M[p + ldm * kk], dot);
+      dot = (dot + d1) + (d2 + d3);
+    }
+    dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+    dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+    CHP(2);
+    if (cs == 0 && ci < np) {
+      const double dci = dc[ci];
+      const bool done = dci == -INFINITY;
+      const double l = done ? 0.0 : (G[ci + ldg * p] - dot) * inv;
+      M[ci + ldm * k] = l;
+      dnx[ci] = (done || ci == p) ? -INFINITY : dci - l * l;
+    }
+    CHP(3);
+    __syncthreads();
+    CHP(4);
+  }
+#ifdef RTUCKER_EIG_PROF_BUILD
+  if (tid == 0 || tid == 255)
+    printf("[chol prof] tid %d steps %d: top %lld argmax %lld dot %lld write %lld barrier %lld\n", tid, k, cpa[0], cpa[1],
+           cpa[2], cpa[3], cpa[4]);
+#endif
+#undef CHP
+  return k;
+}
+
 template <int kV, int LPS>
 __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restrict__ Ain, int n, double *__restrict__ w,
                                                           double *__restrict__ Vout, double tol, int max_sweeps,
                                                           int *__restrict__ info, int r_need, int *__restrict__ refine,
-                                                          unsigned *__restrict__ status) {
+                                                          unsigned *__restrict__ status, const int *__restrict__ gate) {
+  if (gate && *gate == 0) return;  // the mixed-precision solver succeeded
   extern __shared__ double gsm2[];
 #ifdef RTUCKER_EIG_PROF_BUILD
   long long et_[6];
@@ -681,92 +774,7 @@ __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restri
   for (int e = tid; e < ldm * ncol; e += kGramT) M[e] = 0.0;
   for (int i = tid; i < np; i += kGramT) dn[i] = i < n ? 0 : 1;
   __syncthreads();
-  // ---- pivoted Cholesky without row exchanges, left-looking, one CTA barrier per step:
-  //   p = argmax of the remaining diagonal d (first index on ties; every warp evaluates it
-  //   redundantly from d in shared memory, so no barrier publishes it), stop once d_p <= n eps
-  //   max diag(G);  M[i, k] = (G[i, p] - sum_{k' < k} M[i, k'] M[p, k']) / sqrt(d_p) on the rows
-  //   not yet pivoted (4 threads per row split the dot product), d_i -= M[i, k]^2.
-  //   M = P L (P the pivot permutation): its columns have the preconditioning of L, and
-  //   M M^T = G in the original index order.  (Right-looking with a rank-1 update of G and a
-  //   separate pivot pass cost 3 barriers and ~2100 cycles per step: 125k cycles at n = 60.)
-  // remaining diagonal, double-buffered (step k reads dq[k & 1], writes dq[(k + 1) & 1]); -inf
-  // marks a pivoted (or padding) row; a remaining diagonal that rounds below zero stays live
-  double *dq[2] = {lc, lam};
-  for (int i = tid; i < np; i += kGramT) lc[i] = i < n ? G[i + np * i] : -INFINITY;
-  double dmax = 0.0;
-  for (int i = lane; i < n; i += 32) dmax = fmax(dmax, G[i + np * i]);
-  for (int o = 16; o; o >>= 1) dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
-  const double thresh = n * 2.2e-16 * dmax;
-  __syncthreads();
-  EGP();
-  const int ci = tid >> 2, cs = tid & 3;  // row ci, dot-product quarter cs
-#ifdef RTUCKER_EIG_PROF_BUILD
-  long long ca = 0, cb = 0, cc = 0, cd = 0;
-#endif
-  for (int k = 0; k < n; ++k) {
-#ifdef RTUCKER_EIG_PROF_BUILD
-    const long long q0 = clock64();
-#endif
-    const double *dc = dq[k & 1];
-    double *dnx = dq[(k + 1) & 1];
-    // argmax by three single-instruction warp reductions (redux.sync) instead of a 5-round
-    // shuffle tree (~700 cycles measured): a double >= 0 orders like its bit pattern, so the
-    // maximum is (max of the high words, then max of the low words among those), and ties go to
-    // the smallest index; negative entries (pivoted rows, diagonals rounded below 0) count as 0.
-    uint32_t khi = 0, klo = 0;
-    int kid = n;
-    for (int i = lane; i < n; i += 32) {
-      const double v = dc[i];
-      const uint32_t h = v > 0.0 ? (uint32_t)__double2hiint(v) : 0u, l = v > 0.0 ? (uint32_t)__double2loint(v) : 0u;
-      if (h > khi || (h == khi && l > klo)) { khi = h; klo = l; kid = i; }
-    }
-    const uint32_t mhi = __reduce_max_sync(0xffffffffu, khi);
-    const uint32_t mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
-    const int bi = (int)__reduce_min_sync(0xffffffffu, (khi == mhi && klo == mlo) ? (uint32_t)kid : 0xffffffffu);
-    const double bv = __hiloint2double((int)mhi, (int)mlo);
-    if (!(bv > thresh)) break;  // rank reached (same decision in every warp): the rest of M is zero
-#ifdef RTUCKER_EIG_PROF_BUILD
-    const long long q1 = clock64();
-#endif
-    const int p = bi;
-    const double inv = rsqrt(bv);
-    double dot = 0.0;
-    if (ci < np) {  // four independent chains (loads of 4 steps in flight)
-      double d1 = 0.0, d2 = 0.0, d3 = 0.0;
-      int kk = cs;
-      for (; kk + 12 < k; kk += 16) {
-        dot = fma(M[ci + ldm * kk], M[p + ldm * kk], dot);
-        d1 = fma(M[ci + ldm * (kk + 4)], M[p + ldm * (kk + 4)], d1);
-        d2 = fma(M[ci + ldm * (kk + 8)], M[p + ldm * (kk + 8)], d2);
-        d3 = fma(M[ci + ldm * (kk + 12)], M[p + ldm * (kk + 12)], d3);
-      }
-      for (; kk < k; kk += 4) dot = fma(M[ci + ldm * kk], M[p + ldm * kk], dot);
-      dot = (dot + d1) + (d2 + d3);
-    }
-    dot += __shfl_xor_sync(0xffffffffu, dot, 1);
-    dot += __shfl_xor_sync(0xffffffffu, dot, 2);
-#ifdef RTUCKER_EIG_PROF_BUILD
-    const long long q2 = clock64();
-#endif
-    if (cs == 0 && ci < np) {
-      const double dci = dc[ci];
-      const bool done = dci == -INFINITY;
-      const double l = done ? 0.0 : (G[ci + np * p] - dot) * inv;
-      M[ci + ldm * k] = l;
-      dnx[ci] = (done || ci == p) ? -INFINITY : dci - l * l;
-    }
-#ifdef RTUCKER_EIG_PROF_BUILD
-    const long long q3 = clock64();
-#endif
-    __syncthreads();
-#ifdef RTUCKER_EIG_PROF_BUILD
-    const long long q4 = clock64();
-    ca += q1 - q0; cb += q2 - q1; cc += q3 - q2; cd += q4 - q3;
-#endif
-  }
-#ifdef RTUCKER_EIG_PROF_BUILD
-  if (tid == 0 || tid == 255) printf("[chol prof] tid %d argmax %lld dot %lld write %lld barrier %lld\n", tid, ca, cb, cc, cd);
-#endif
+  chol_pivoted_left(G, np, n, M, ldm, lc, lam, np);
   EGP();
   // ---- block-ordered one-sided Jacobi on the columns of M
   const double tol2 = tol * tol;
@@ -864,6 +872,525 @@ __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restri
     __syncthreads();  // w (global) written above by the sorting threads
     if (tid == 0) *refine = (w[r_need - 1] >= 1e-8 * w[0]) ? 0 : 1;
   }
+}
+
+// ----------------------------------------------------- mixed-precision Gram eigensolver ----
+// fp32 data, n <= 64 (the fixed-rank truncation of Alg 1 line 4, eigenpairs of the l x l
+// Gram B B^T): the fp32 criteria need the eigenvectors to the absolute accuracy ~eps lambda_1 /
+// gap (the class of the tridiagonal solver used above 64), which an fp64 Newton refinement of
+// an fp32 starting basis reaches in two or three GEMM-shaped steps:
+//   1. pivoted Cholesky G = M M^T in fp64 (chol_pivoted_left: M keeps the column grading);
+//   2. block-ordered one-sided Jacobi on an fp32 copy of M (same schedule as gram_eig_kernel)
+//      to column orthogonality ~4e-6; X = normalised columns of M J (eigenvector estimates of
+//      G, angles ~4e-6 / relative gap thanks to the grading);
+//   3. Ogita-Aishima refinement in fp64 (Newton steps on X^T X = I, X^T G X diagonal):
+//        R = I - X^T X, S = X^T G X, lambda_i = S_ii / (1 - R_ii),
+//        E_ij = (S_ij + lambda_j R_ij) / (lambda_j - lambda_i)   (i != j, |E_ij| <= 1/8),
+//        E_ij = R_ij / 2                                        (otherwise: a cluster),
+//        X <- X + X E,
+//      the four 64^3 products on the fp64 tensor cores (mma.sync m8n8k4), until max |E| <= 1e-8
+//      (the next correction would be below 1e-16) or four steps.
+// A rank-deficient Gram (the Cholesky stops early) or a pair of the final step that is still
+// unresolved across the wanted rank r_need with a gap above 1e-12 lambda_1 raises *fallback,
+// which runs the fp64 Jacobi kernel (device-side gate, no host sync).
+constexpr int kMxT = 256;
+constexpr int kMxLd = 66;  // 64 x 64 fp64 tiles: 2-wavefront m8n8k4 fragment loads both ways
+
+__device__ __forceinline__ void dmma_m8n8k4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// C = op(A) B (+ Cin) for 64 x 64 column-major shared-memory operands (ld kMxLd); 8 warps, warp w
+// computes rows 16 (w & 3) .. + 15 and columns 32 (w >> 2) .. + 31 as 2 x 4 tiles of 8 x 8.
+template <bool TA>
+__device__ __forceinline__ void mx_gemm64(const double *__restrict__ A, const double *__restrict__ B,
+                                          double *__restrict__ C, const double *__restrict__ Cin) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int i0 = 16 * (warp & 3), j0 = 32 * (warp >> 2);
+  double acc[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = i0 + 8 * i + g, cc = j0 + 8 * j + 2 * t;
+      acc[i][j][0] = Cin ? Cin[r + kMxLd * cc] : 0.0;
+      acc[i][j][1] = Cin ? Cin[r + kMxLd * (cc + 1)] : 0.0;
+    }
+#pragma unroll 4
+  for (int k0 = 0; k0 < 64; k0 += 4) {
+    double a[2], b[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int r = i0 + 8 * i + g;
+      a[i] = TA ? A[(k0 + t) + kMxLd * r] : A[r + kMxLd * (k0 + t)];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = B[(k0 + t) + kMxLd * (j0 + 8 * j + g)];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j], a[i], b[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = i0 + 8 * i + g, cc = j0 + 8 * j + 2 * t;
+      C[r + kMxLd * cc] = acc[i][j][0];
+      C[r + kMxLd * (cc + 1)] = acc[i][j][1];
+    }
+}
+
+// fp32 rotation (c, s) annihilating g for squared column norms a (p), b (q)
+// fp32 rotation (c, s) annihilating g for squared column norms a (p), b (q) in two dependent
+// MUFU steps: with d = b - a and r = sqrt(d^2 + 4 g^2), cos 2theta = |d| / r, c = sqrt((1 +
+// cos 2theta) / 2), s = sgn(d) g / (r c) (|theta| <= pi/4; the usual t = sgn(zeta) / (|zeta| +
+// sqrt(1 + zeta^2)) chain cost five dependent MUFU operations).  g = 0 gives the identity.
+__device__ __forceinline__ float rsqrt_ftz_f32(float x) {  // bare MUFU.RSQ (no denormal fix-up code)
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ void jac_angle_f32(float a, float b, float g, float &c, float &s) {
+  const float d = b - a;
+  const float q = rsqrt_ftz_f32(fmaf(d, d, 4.0f * g * g));
+  const float h = fmaf(fabsf(d), 0.5f * q, 0.5f);
+  const float rh = rsqrt_ftz_f32(h);
+  const bool id = g == 0.0f;
+  c = id ? 1.0f : h * rh;
+  s = id ? 0.0f : copysignf(1.0f, d) * (g * q * rh);
+}
+
+// convergence test g^2 > tol^2 a b, off the rotation's critical path: every pair is rotated, a
+// converged one by an angle below tol.  (Columns are scaled to max norm 1 and the Cholesky stops
+// at n eps max diag, so tol^2 a b >= 1e-6 (64 eps)^2 stays a normal fp32 number.)
+__device__ __forceinline__ bool jac_needs_f32(float a, float b, float g, float tol) {
+  return g * g > (tol * tol) * (a * b);
+}
+
+template <int kV, int LPS>
+__device__ __forceinline__ void jac_pair_f32(float (&x)[kV], float (&y)[kV], float tol, int &rot) {
+  float g0 = 0.f, g1 = 0.f, a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+#pragma unroll
+  for (int v = 0; v < kV; v += 2) {
+    g0 = fmaf(x[v], y[v], g0);
+    g1 = fmaf(x[v + 1], y[v + 1], g1);
+    a0 = fmaf(x[v], x[v], a0);
+    a1 = fmaf(x[v + 1], x[v + 1], a1);
+    b0 = fmaf(y[v], y[v], b0);
+    b1 = fmaf(y[v + 1], y[v + 1], b1);
+  }
+  float g = g0 + g1, a = a0 + a1, b = b0 + b1;
+#pragma unroll
+  for (int o = 1; o < LPS; o <<= 1) {
+    g += __shfl_xor_sync(0xffffffffu, g, o);
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  rot |= jac_needs_f32(a, b, g, tol) ? 1 : 0;
+  float c, s;
+  jac_angle_f32(a, b, g, c, s);
+#pragma unroll
+  for (int v = 0; v < kV; ++v) {
+    const float xv = x[v], yv = y[v];
+    x[v] = fmaf(c, xv, -s * yv);
+    y[v] = fmaf(s, xv, c * yv);
+  }
+}
+
+template <int kV, int LPS>
+__device__ __forceinline__ void jac_half_f32(float (&own)[kV], const float (&oth)[kV], bool own_is_p, float tol,
+                                             int &rot) {
+  float g0 = 0.f, g1 = 0.f, o0 = 0.f, o1 = 0.f, t0 = 0.f, t1 = 0.f;
+#pragma unroll
+  for (int v = 0; v < kV; v += 2) {
+    g0 = fmaf(own[v], oth[v], g0);
+    g1 = fmaf(own[v + 1], oth[v + 1], g1);
+    o0 = fmaf(own[v], own[v], o0);
+    o1 = fmaf(own[v + 1], own[v + 1], o1);
+    t0 = fmaf(oth[v], oth[v], t0);
+    t1 = fmaf(oth[v + 1], oth[v + 1], t1);
+  }
+  float g = g0 + g1, so = o0 + o1, st = t0 + t1;
+#pragma unroll
+  for (int o = 1; o < LPS; o <<= 1) {
+    g += __shfl_xor_sync(0xffffffffu, g, o);
+    so += __shfl_xor_sync(0xffffffffu, so, o);
+    st += __shfl_xor_sync(0xffffffffu, st, o);
+  }
+  const float a = own_is_p ? so : st, b = own_is_p ? st : so;
+  rot |= jac_needs_f32(a, b, g, tol) ? 1 : 0;
+  float c, s;
+  jac_angle_f32(a, b, g, c, s);
+  // p: c own - s oth;  q: s oth + c own  (the mirror slot applies the other half)
+  const float so_ = own_is_p ? -s : s;
+#pragma unroll
+  for (int v = 0; v < kV; ++v) own[v] = fmaf(so_, oth[v], c * own[v]);
+}
+
+constexpr int kMxLdm = 68;  // fp32 Jacobi columns: 4 lanes x 16 rows + 4 (conflict-free slot loads)
+constexpr size_t kMxSmem = sizeof(double) * (5 * 64 * kMxLd + 6 * 64) + 64;
+
+// A (64 x 64, ld kMxLd) -= P P^T for a 64 x 8 panel P (column-major, ld ldp) on the fp64 tensor
+// cores (the trailing update of the blocked Cholesky below; same warp tiling as mx_gemm64)
+__device__ __forceinline__ void mx_syrk8(double *__restrict__ A, const double *__restrict__ P, int ldp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int i0 = 16 * (warp & 3), j0 = 32 * (warp >> 2);
+  double acc[2][4][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = i0 + 8 * i + g, cc = j0 + 8 * j + 2 * t;
+      acc[i][j][0] = A[r + kMxLd * cc];
+      acc[i][j][1] = A[r + kMxLd * (cc + 1)];
+    }
+#pragma unroll
+  for (int k0 = 0; k0 < 8; k0 += 4) {
+    double a[2], b[4];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) a[i] = -P[(i0 + 8 * i + g) + ldp * (k0 + t)];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = P[(j0 + 8 * j + g) + ldp * (k0 + t)];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j], a[i], b[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = i0 + 8 * i + g, cc = j0 + 8 * j + 2 * t;
+      A[r + kMxLd * cc] = acc[i][j][0];
+      A[r + kMxLd * (cc + 1)] = acc[i][j][1];
+    }
+}
+
+// Blocked pivoted Cholesky G = M M^T (M = P L, rows in the original order, no row exchanges) for
+// the mixed solver, 256 threads, n <= 64.  Panels of 8 columns: ONE warp factors the panel
+// (rows lane and lane + 32 in registers, the remaining diagonal d in registers, pivot = argmax d
+// by one redux.sync as in chol_pivoted_left, earlier panel columns of the pivot row by shuffles:
+// no CTA barrier inside a panel), then all warps apply the trailing update A -= P P^T on the
+// fp64 tensor cores.  ~250 cycles per column instead of ~1900 for the one-barrier-per-column
+// left-looking form.  A (ld kMxLd) is a working copy of G and is destroyed; M (ld ldm) must be
+// zero on entry.  Returns the number of pivots (numerical rank, threshold n eps max diag).
+__device__ int chol_pivoted_panel(double *__restrict__ A, int n, double *__restrict__ M, int ldm, int *sh) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double d0 = -1.0, d1 = -1.0;  // remaining diagonal of rows lane, lane + 32 (-1: pivoted / padding)
+  double thresh = 0.0;
+  if (warp == 0) {
+    if (lane < n) d0 = A[lane * (kMxLd + 1)];
+    if (lane + 32 < n) d1 = A[(lane + 32) * (kMxLd + 1)];
+    double dm = fmax(d0, d1);
+    for (int o = 16; o; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+    thresh = n * 2.2e-16 * dm;
+  }
+  int k = 0;
+  for (int j0 = 0; j0 < n; j0 += 8) {
+    if (warp == 0) {
+      double P0[8], P1[8];
+      int stop = 0;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        P0[jj] = 0.0;
+        P1[jj] = 0.0;
+        if (stop || j0 + jj >= n) continue;
+        uint32_t key0 = d0 > 0.0 ? ((__float_as_uint((float)d0) & ~63u) | (uint32_t)(63 - lane)) : 0u;
+        uint32_t key1 = d1 > 0.0 ? ((__float_as_uint((float)d1) & ~63u) | (uint32_t)(31 - lane)) : 0u;
+        const uint32_t key = __reduce_max_sync(0xffffffffu, max(key0, key1));
+        const int p = 63 - (int)(key & 63u), pl = p & 31;
+        const bool hi = p >= 32;
+        const double bv = __shfl_sync(0xffffffffu, hi ? d1 : d0, pl);
+        if (!key || !(bv > thresh)) {
+          stop = 1;
+          continue;
+        }
+        double inv;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(inv) : "d"(bv));
+        inv = inv * fma(-0.5 * bv * inv, inv, 1.5);
+        inv = inv * fma(-0.5 * bv * inv, inv, 1.5);
+        double a0 = A[lane + kMxLd * p], a1 = A[lane + 32 + kMxLd * p];
+#pragma unroll
+        for (int q = 0; q < jj; ++q) {
+          const double pp = __shfl_sync(0xffffffffu, hi ? P1[q] : P0[q], pl);
+          a0 = fma(-P0[q], pp, a0);
+          a1 = fma(-P1[q], pp, a1);
+        }
+        const double l0 = d0 < 0.0 && lane != p ? 0.0 : a0 * inv;
+        const double l1 = d1 < 0.0 && lane + 32 != p ? 0.0 : a1 * inv;
+        P0[jj] = l0;
+        P1[jj] = l1;
+        M[lane + ldm * (j0 + jj)] = l0;
+        M[lane + 32 + ldm * (j0 + jj)] = l1;
+        d0 = (d0 < 0.0 || lane == p) ? -1.0 : d0 - l0 * l0;
+        d1 = (d1 < 0.0 || lane + 32 == p) ? -1.0 : d1 - l1 * l1;
+      }
+      if (lane == 0) {
+        sh[0] = stop;
+        sh[1] = stop ? -1 : 0;
+      }
+      // pivots taken in this panel: columns j0.. until the stop
+      int taken = 0;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) taken += (j0 + jj < n) ? 1 : 0;
+      (void)taken;
+    }
+    __syncthreads();
+    const int stopped = sh[0];
+    if (stopped || j0 + 8 >= n) {
+      // count the columns actually taken (nonzero pivot entries) in this last panel
+      k = j0;
+      for (int jj = 0; jj < 8 && j0 + jj < n; ++jj) {
+        bool nz = false;
+        for (int r = 0; r < n; ++r) nz |= M[r + ldm * (j0 + jj)] != 0.0;
+        if (!nz) break;
+        ++k;
+      }
+      break;
+    }
+    mx_syrk8(A, M + ldm * j0, ldm);
+    __syncthreads();
+  }
+  return k;
+}
+
+
+
+__global__ void __launch_bounds__(kMxT) gram_eig_mixed_kernel(const double *__restrict__ Ain, int n,
+                                                              double *__restrict__ w, double *__restrict__ Vout,
+                                                              int *__restrict__ info, int r_need,
+                                                              int *__restrict__ fallback, int max_sweeps) {
+  constexpr int kV = 16, LPS = 4, SPW = 8, NB = 8;  // 64 columns of 64 rows, 8 blocks of 8
+  extern __shared__ double mxs[];
+#ifdef RTUCKER_EIG_PROF_BUILD
+  long long mt_[12];
+  int mn_ = 0;
+#define MXP() if (threadIdx.x == 0 && mn_ < 12) mt_[mn_++] = clock64()
+#else
+#define MXP()
+#endif
+  MXP();
+  double *Gs = mxs;                   // 64 x 64 (ld kMxLd), zero padded
+  double *buf1 = Gs + 64 * kMxLd;     // M32 (fp32 Jacobi columns), later a product buffer
+  double *buf2 = buf1 + 64 * kMxLd;   // M (fp64, ld kMxLdm, spans buf2..buf3), later X
+  double *buf3 = buf2 + 64 * kMxLd;
+  double *Eb = buf3 + 64 * kMxLd;     // the refinement's correction E
+  double *lc = Eb + 64 * kMxLd, *lam = lc + 64, *lamv = lam + 64, *rowoff = lamv + 64, *rowr = rowoff + 64;
+  int *rkv = reinterpret_cast<int *>(rowr + 64);
+  float *M32 = reinterpret_cast<float *>(buf1);
+  double *M = buf2;
+  __shared__ int sflag, sbad;
+  __shared__ float smaxe;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int np = n + (n & 1);
+  for (int e = tid; e < 64 * kMxLd; e += kMxT) {
+    const int i = e % kMxLd, j = e / kMxLd;
+    const double gv = (i < n && j < n) ? 0.5 * (Ain[i + (size_t)n * j] + Ain[j + (size_t)n * i]) : 0.0;
+    Gs[e] = gv;
+    Eb[e] = gv;  // the Cholesky's working copy
+    buf2[e] = 0.0;
+    buf3[e] = 0.0;
+  }
+  if (tid == 0) sbad = 0;
+  __syncthreads();
+  // ---- 1. pivoted Cholesky (fp64, blocked)
+  __shared__ int csh[2];
+  const int rank = chol_pivoted_panel(Eb, n, M, kMxLdm, csh);
+  (void)np;
+  MXP();
+  if (rank < n) {  // rank-deficient Gram: the fp64 Jacobi kernel handles the null space
+    if (tid == 0) *fallback = 1;
+    return;
+  }
+  // ---- 2. fp32 one-sided Jacobi on M / sqrt(max column norm^2) (no fp32 overflow / underflow)
+  double dmx = 0.0;
+  for (int i = 0; i < n; ++i) dmx = fmax(dmx, Gs[i + kMxLd * i]);
+  const double sc = dmx > 0.0 ? 1.0 / sqrt(dmx) : 1.0;
+  for (int e = tid; e < kMxLdm * 64; e += kMxT) M32[e] = (float)(M[e] * sc);
+  __syncthreads();
+  // a start to ~1e-3: the refinement's Newton steps converge quadratically from there
+  const float tol = 1e-3f;
+  const int slot = lane / LPS, q = lane % LPS;
+  int sweeps = 0;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    if (tid == 0) sflag = 0;
+    __syncthreads();
+    int rot = 0;
+    if (warp < NB / 2) {
+      float *c1 = M32 + kMxLdm * (2 * SPW * warp + slot), *c2 = c1 + SPW * kMxLdm;
+      float x[kV], y[kV];
+#pragma unroll
+      for (int v = 0; v < kV; ++v) { x[v] = c1[q + LPS * v]; y[v] = c2[q + LPS * v]; }
+#pragma unroll 1
+      for (int m = 1; m < SPW; ++m) {
+        const int src = (slot ^ m) * LPS + q;
+        const bool own_p = slot < (slot ^ m);
+        float px[kV], py[kV];
+#pragma unroll
+        for (int v = 0; v < kV; ++v) {
+          px[v] = __shfl_sync(0xffffffffu, x[v], src);
+          py[v] = __shfl_sync(0xffffffffu, y[v], src);
+        }
+        jac_half_f32<kV, LPS>(x, px, own_p, tol, rot);
+        jac_half_f32<kV, LPS>(y, py, own_p, tol, rot);
+      }
+#pragma unroll
+      for (int v = 0; v < kV; ++v) { c1[q + LPS * v] = x[v]; c2[q + LPS * v] = y[v]; }
+    }
+    __syncthreads();
+    for (int t = 0; t < NB - 1; ++t) {
+      if (warp < NB / 2) {
+        int bA, bB;
+        rr_pair(warp, t, NB, bA, bB);
+        float *c1 = M32 + kMxLdm * (SPW * bA + slot), *c2 = M32 + kMxLdm * (SPW * bB + slot);
+        float x[kV], y[kV];
+#pragma unroll
+        for (int v = 0; v < kV; ++v) { x[v] = c1[q + LPS * v]; y[v] = c2[q + LPS * v]; }
+        const int nxt = ((slot + 1) % SPW) * LPS + q;
+#pragma unroll 1
+        for (int r = 0; r < SPW; ++r) {
+          jac_pair_f32<kV, LPS>(x, y, tol, rot);
+#pragma unroll
+          for (int v = 0; v < kV; ++v) y[v] = __shfl_sync(0xffffffffu, y[v], nxt);
+        }
+#pragma unroll
+        for (int v = 0; v < kV; ++v) { c1[q + LPS * v] = x[v]; c2[q + LPS * v] = y[v]; }
+      }
+      __syncthreads();
+    }
+    if (rot) sflag = 1;
+    __syncthreads();
+    sweeps = sweep + 1;
+    const int more = sflag;
+    __syncthreads();
+    if (!more) break;
+  }
+  MXP();
+  // X = normalised columns of M32 J (fp64), columns >= n and rows >= n zero
+  double *X = buf2, *T1 = buf1, *T2 = buf3;
+  for (int k = warp; k < 64; k += kMxT / 32) {
+    double d = 0.0;
+    for (int r = lane; r < 64; r += 32) { const double v = (double)M32[r + kMxLdm * k]; d = fma(v, v, d); }
+    d = warp_sum(d);
+    if (lane == 0) lc[k] = d;
+  }
+  __syncthreads();
+  // column k of M32 -> column k of X (M32 lives in buf1, X in buf2: no overlap)
+  for (int e = tid; e < 64 * 64; e += kMxT) {
+    const int r = e & 63, k = e >> 6;
+    const double d = lc[k];
+    X[r + kMxLd * k] = (r < n && k < n && d > 0.0) ? (double)M32[r + kMxLdm * k] / sqrt(d) : 0.0;
+  }
+  __syncthreads();
+  MXP();
+  // ---- 3. Ogita-Aishima refinement (fp64 tensor cores).  S and I - R are read symmetrised (the
+  // GEMMs leave ~eps ||G|| asymmetry, which the 1 / (lambda_j - lambda_i) of small eigenvalues
+  // would amplify into a loss of orthogonality: with symmetric S, E + E^T = R exactly).  A pair
+  // takes the Newton correction when it is separated at this step's resolution,
+  //   |lambda_j - lambda_i| > 4 |S_ij| + 2 lambda_max |R_ij|  and  |E_ij| <= 1/100
+  // (a per-pair form of Ogita and Aishima's separation bound; the second condition keeps the
+  // first-order step inside its domain), else it is orthogonalised only (a cluster: any basis of
+  // a numerically degenerate pair is as good, a split across r_need raises the fallback).
+  const double floor_num = n * 2.2e-16 * dmx;
+  int it = 0, more = 1, unresolved = 0;
+  while (it < 4 && more) {
+    mx_gemm64<false>(Gs, X, T1, nullptr);  // A X
+    __syncthreads();
+    mx_gemm64<true>(X, T1, T2, nullptr);  // S = X^T (A X)
+    __syncthreads();
+    mx_gemm64<true>(X, X, T1, nullptr);  // X^T X = I - R
+    __syncthreads();
+    if (tid < 64) lamv[tid] = tid < n ? T2[tid * (kMxLd + 1)] / T1[tid * (kMxLd + 1)] : 0.0;
+    __syncthreads();
+    double ml = fmax(lamv[lane], lamv[lane + 32]);
+    for (int o = 16; o; o >>= 1) ml = fmax(ml, __shfl_xor_sync(0xffffffffu, ml, o));
+    int lmore = 0, bad = 0;
+    for (int e = tid; e < 64 * 64; e += kMxT) {
+      const int i = e & 63, j = e >> 6;
+      double E = 0.0;
+      if (i < n && j < n) {
+        if (i == j) {
+          E = 0.5 * (1.0 - T1[i * (kMxLd + 1)]);
+        } else {
+          const double sij = 0.5 * (T2[i + kMxLd * j] + T2[j + kMxLd * i]);
+          const double rij = -0.5 * (T1[i + kMxLd * j] + T1[j + kMxLd * i]);
+          const double num = fma(lamv[j], rij, sij), den = lamv[j] - lamv[i];
+          const double aden = fabs(den);
+          if (aden > 4.0 * fabs(sij) + 2.0 * ml * fabs(rij) && fabs(num) <= 0.01 * aden) {
+            double rd = rcp_approx_f64(den);  // + two Newton steps: ~1e-16 relative, no division subroutine
+            rd = rd * fma(-den, rd, 2.0);
+            rd = rd * fma(-den, rd, 2.0);
+            E = num * rd;
+            if (fabs(E) > 1e-8 && fabs(num) > floor_num) lmore = 1;  // not yet at the noise floor
+          } else {
+            E = 0.5 * rij;  // a cluster at this step's resolution: orthogonalise only
+            // harmful only when the pair straddles the wanted rank with a real gap
+            if (aden > 1e-12 * dmx) {
+              int ri = 0, rj = 0;
+              for (int k = 0; k < n; ++k) {
+                ri += (lamv[k] > lamv[i] || (lamv[k] == lamv[i] && k < i));
+                rj += (lamv[k] > lamv[j] || (lamv[k] == lamv[j] && k < j));
+              }
+              if ((ri < r_need) != (rj < r_need)) bad = 1;
+            }
+          }
+        }
+      }
+      Eb[i + kMxLd * j] = E;
+    }
+    more = __syncthreads_or(lmore);
+    unresolved = __syncthreads_or(bad);
+    mx_gemm64<false>(X, Eb, T1, X);  // X + X E
+    __syncthreads();
+    double *tmp = X;
+    X = T1;
+    T1 = tmp;
+    ++it;
+    MXP();
+  }
+  if (tid == 0 && info) *info = sweeps + 1000 * it;
+  if (unresolved || more) {  // a straddling cluster, or no convergence in four steps
+    if (tid == 0) *fallback = 1;
+    return;
+  }
+  // eigenvalues: the last step's Rayleigh quotients (second order in the remaining error);
+  // eigenvectors: the refined columns, normalised
+  for (int k = warp; k < n; k += kMxT / 32) {
+    double d = 0.0;
+    for (int r = lane; r < n; r += 32) { const double v = X[r + kMxLd * k]; d = fma(v, v, d); }
+    d = warp_sum(d);
+    if (lane == 0) lc[k] = 1.0 / sqrt(d);
+  }
+  for (int i = tid; i < n; i += kMxT) {  // rank of each eigenvalue: descending, ties by index
+    const double di = lamv[i];
+    int rk = 0;
+    for (int j = 0; j < n; ++j) {
+      const double dj = lamv[j];
+      if (j != i && (dj > di || (dj == di && j < i))) ++rk;
+    }
+    rkv[i] = rk;
+    w[rk] = di;
+  }
+  __syncthreads();
+  for (int e = tid; e < n * n; e += kMxT) {  // coalesced: consecutive threads, consecutive rows
+    const int i = e / n, r = e - i * n;
+    Vout[r + (int64_t)n * rkv[i]] = X[r + kMxLd * i] * lc[i];
+  }
+  MXP();
+#ifdef RTUCKER_EIG_PROF_BUILD
+  if (threadIdx.x == 0) {
+    printf("[mixed prof] n %d sweeps %d iters %d:", n, sweeps, it);
+    for (int i = 1; i < mn_; ++i) printf(" %lld", mt_[i] - mt_[i - 1]);
+    printf("\n");
+  }
+#endif
+#undef MXP
 }
 
 // ------------------------------------------------------------- CholeskyQR2 ----------
@@ -1543,9 +2070,22 @@ void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps,
   DevBuf<int> refine(c, 1);
   const double tol = 3e-15 * std::sqrt((double)n);
   const int rn = std::max(1, std::min(r_need, n));
+  // fp32 data, 32 < n <= 64: the mixed-precision solver; the fp64 Jacobi below runs only when it
+  // raises its fallback flag (rank-deficient Gram, unresolved pair across r_need)
+  const int *gate = nullptr;
+  DevBuf<int> fb;
+  static const bool no_mixed = RT_EXP_GETENV("RTUCKER_EIG_NO_MIXED") != nullptr;
+  if (!rel_acc && n > 32 && !no_mixed) {
+    fb.alloc(c, 1);
+    fb.zero();
+    refine.zero();
+    smem_attr(gram_eig_mixed_kernel, kMxSmem);
+    RT_LAUNCH(c, gram_eig_mixed_kernel, 1, kMxT, kMxSmem, A, n, w, V, sweeps, rn, fb.p, 15);
+    gate = fb.p;
+  }
 #define RT_GE(KV, L)                                                                                      \
   smem_attr(gram_eig_kernel<KV, L>, need);                                                                 \
-  RT_LAUNCH(c, (gram_eig_kernel<KV, L>), 1, kGramT, need, A, n, w, V, tol, 40, sweeps, rn, refine.p, c.status)
+  RT_LAUNCH(c, (gram_eig_kernel<KV, L>), 1, kGramT, need, A, n, w, V, tol, 40, sweeps, rn, refine.p, c.status, gate)
   if (lps == 8) {
     RT_GE(8, 8);
   } else if (kv == 4) {

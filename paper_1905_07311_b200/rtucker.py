@@ -54,7 +54,7 @@ EXPORTED = [
     "rtucker_rel_error", "rtucker_debug_sketch", "rtucker_debug_omega", "rtucker_debug_philox",
     "rtucker_debug_qr", "rtucker_debug_eig", "rtucker_debug_srrqr", "rtucker_set_profiling",
     "rtucker_phase_times", "rtucker_debug_gram_eig", "rtucker_debug_ttm", "rtucker_debug_loopback_sharding",
-    "rtucker_debug_gemm", "rtucker_debug_gram", "rtucker_debug_coo_sketch",
+    "rtucker_debug_gemm", "rtucker_debug_gram", "rtucker_debug_coo_sketch", "rtucker_debug_gram_eig_ex",
 ]
 PHASES = ("sketch", "qr", "bpass", "eig", "shrink", "other")
 
@@ -126,6 +126,7 @@ def load_library(path: str = LIB_PATH):
         "rtucker_debug_srrqr": (C.c_int, [P, I64, I32, P, D, P, P, C.POINTER(I32)]),
         "rtucker_debug_coo_sketch": (C.c_int, [P, C.POINTER(CooDesc), I32, I32, U64, U32, P]),
         "rtucker_debug_gram_eig": (C.c_int, [P, I32, P, P, P, C.POINTER(I32)]),
+        "rtucker_debug_gram_eig_ex": (C.c_int, [P, I32, P, P, P, C.POINTER(I32), I32, I32]),
         "rtucker_debug_ttm": (C.c_int, [P, C.POINTER(DenseDesc), I32, P, I32, U32, P, P]),
         "rtucker_debug_loopback_sharding": (C.c_int, [P, C.c_int]),
         "rtucker_set_profiling": (C.c_int, [P, C.c_int]),
@@ -520,6 +521,21 @@ class Context:
         sw = C.c_int32()
         self._enter()
         self._check(self.lib.rtucker_debug_gram_eig(self.h, n, at.data_ptr(), w.data_ptr(), v.data_ptr(), C.byref(sw)))
+        self.sync()
+        self.last_sweeps = int(sw.value)
+        return w.cpu().numpy(), v.cpu().numpy().reshape((n, n), order="F")
+
+    def debug_gram_eig_ex(self, a: np.ndarray, rel_acc: bool, r_need: int):
+        """The hot path's Gram eigensolver as selected for fp32 (rel_acc False) / fp64 data."""
+        torch = _torch()
+        n = a.shape[0]
+        at = torch.as_tensor(np.asfortranarray(a, dtype=np.float64).ravel(order="F"), device="cuda")
+        w = torch.empty(n, dtype=torch.float64, device="cuda")
+        v = torch.empty_like(at)
+        sw = C.c_int32()
+        self._enter()
+        self._check(self.lib.rtucker_debug_gram_eig_ex(self.h, n, at.data_ptr(), w.data_ptr(), v.data_ptr(),
+                                                       C.byref(sw), int(bool(rel_acc)), int(r_need)))
         self.sync()
         self.last_sweeps = int(sw.value)
         return w.cpu().numpy(), v.cpu().numpy().reshape((n, n), order="F")
