@@ -96,6 +96,11 @@ void power_iterate(Ctx &c, const void *G, DT gt, ModeView v, int ell, int q, boo
   }
 }
 
+// fp32 data: the sketch's range basis may stop at one CholeskyQR pass when Q^T Q is within 1e-10
+// of I (reading R22: 1e-10 is far below the 1e-5 criteria and fp32's own 6e-8); fp64 data keeps
+// both passes (orthonormal to working precision).
+double qr_orth_tol(const DenseIn &in) { return in.dt == DT::F32 ? 1e-10 : 0.0; }
+
 void copy_residuals(Ctx &c, rtucker_result *r, const double *scal, int d, int first_mode) {
   for (int k = 0; k < d; ++k)
     RT_CUDA(cudaMemcpyAsync(&r->mode_residual_sq[k], scal + 2 * k + 1, sizeof(double), cudaMemcpyDeviceToHost,
@@ -247,7 +252,7 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
     DevBuf<double> Q(c, (size_t)Ig * ell);
     {
       PhaseScope ps(c, PH_QR, jj);
-      thin_qr(c, Y.p, Ig, ell, Q.p);
+      thin_qr(c, Y.p, Ig, ell, Q.p, qr_orth_tol(in));
     }
     Y.release();
     if (power > 0) {  // subspace iteration (NEXT-3)
@@ -281,9 +286,8 @@ rtucker_result *run_sthosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *
     double *A = nullptr;
     A = (double *)dev_alloc(c, sizeof(double) * Ig * rr);
     res->factors[n] = A;
-    gemm_small(c, false, Q.p, Ig, V.p, ell, A, Ig, Ig, rr, ell);
-    canonical_signs(c, A, Ig, rr, V.p, ell, ell);  // reading R4b (shrink uses the signed U_B)
-    residual_from_eigs(c, w.p, rr, scal.p + 2 * n, scal.p + 2 * n + 1);
+    // A_n = Q U_B(:, 1:r), signs (reading R4b; the shrink uses the signed U_B), residual
+    factor_epilogue(c, Q.p, Ig, ell, V.p, rr, A, w.p, scal.p + 2 * n, scal.p + 2 * n + 1);
     ps_b.next(PH_SHRINK);
     // ---- Alg 3 line 6: G_(n) <- Sigma_hat V_hat^T = U_B(:, 1:r)^T B
     const ModeView vb{v.L, ell, v.R};
@@ -375,7 +379,7 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
       stream_dep(c.stream, c.aux);
       OnStream os(c, c.aux);
       PhaseScope ps(c, PH_QR, n);
-      thin_qr(c, Ys[n].p, Ig, ell, Qs[n].p);
+      thin_qr(c, Ys[n].p, Ig, ell, Qs[n].p, qr_orth_tol(in));
       RT_CUDA(cudaEventRecord(qdone[n], c.stream));
     }
     for (int n = 0; n < d; ++n) {  // B-passes on the main stream, eigensolves on the side stream
@@ -399,9 +403,7 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
       OnStream os(c, c.aux);
       PhaseScope ps(c, PH_EIG, n);
       gram_eig(c, grams[n].p, ell, ws[n].p, Vs[n].p, nullptr, rr, in.dt == DT::F64);
-      gemm_small(c, false, Qs[n].p, Ig, Vs[n].p, ell, A, Ig, Ig, rr, ell);
-      canonical_signs(c, A, Ig, rr, Vs[n].p, ell, ell);  // reading R4b (shrink uses the signed U_B)
-      residual_from_eigs(c, ws[n].p, rr, scal.p + 2 * n, scal.p + 2 * n + 1);
+      factor_epilogue(c, Qs[n].p, Ig, ell, Vs[n].p, rr, A, ws[n].p, scal.p + 2 * n, scal.p + 2 * n + 1);
       if (n == 0 && keep_b1) {
         RT_CUDA(cudaMemcpyAsync(U1.p, Vs[n].p, sizeof(double) * ell * rr, cudaMemcpyDeviceToDevice, c.stream));
         ell1 = ell;
@@ -436,7 +438,7 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
     }
     ps.next(PH_QR);
     DevBuf<double> Q(c, (size_t)Ig * ell);
-    thin_qr(c, Y.p, Ig, ell, Q.p);
+    thin_qr(c, Y.p, Ig, ell, Q.p, qr_orth_tol(in));
     if (power > 0) power_iterate(c, in.ptr, in.dt, v, ell, power, pol.mul_f64 || in.dt == DT::F64, Q.p, colmax.p);
     DevBuf<double> gram(c, (size_t)ell * ell);
     ps.next(PH_BPASS);
@@ -461,9 +463,8 @@ rtucker_result *run_hosvd(Ctx &c, const rtucker_dense_desc *X, const int64_t *ra
     double *A = nullptr;
     A = (double *)dev_alloc(c, sizeof(double) * Ig * rr);
     res->factors[n] = A;
-    gemm_small(c, false, Q.p, Ig, V.p, ell, A, Ig, Ig, rr, ell);
-    canonical_signs(c, A, Ig, rr, V.p, ell, ell);  // reading R4b (shrink uses the signed U_B)
-    residual_from_eigs(c, w.p, rr, scal.p + 2 * n, scal.p + 2 * n + 1);
+    // A_n = Q U_B(:, 1:r), signs (reading R4b; the shrink uses the signed U_B), residual
+    factor_epilogue(c, Q.p, Ig, ell, V.p, rr, A, w.p, scal.p + 2 * n, scal.p + 2 * n + 1);
     if (n == 0 && keep_b1) {
       U1.alloc(c, (size_t)ell * rr);
       RT_CUDA(cudaMemcpyAsync(U1.p, V.p, sizeof(double) * ell * rr, cudaMemcpyDeviceToDevice, c.stream));

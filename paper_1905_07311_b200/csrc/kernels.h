@@ -72,7 +72,9 @@ void mode_gram(Ctx &c, const void *B, DT t, ModeView v, double *gram);
 // gate (device int, optional): the kernels return immediately when *gate == 0.
 void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q, const int *gate = nullptr);
 // Hot-path thin QR: CholeskyQR2, with Householder recomputation when ill-conditioned.
-void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q);
+// orth_tol > 0 (fp32 data): the one-cluster CholeskyQR2 stops after its first pass when the
+// second pass's Gram shows ||Q^T Q - I||_max <= orth_tol (DESIGN reading R22).
+void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q, double orth_tol = 0.0);
 // w descending; sweeps (optional, device int) <- Jacobi sweeps used
 // gate (device int, optional): the kernel returns immediately when *gate == 0.
 void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps = nullptr, const int *gate = nullptr);
@@ -80,6 +82,10 @@ void sym_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps =
 // ~eps sqrt(w_0 / w_k).  When the r_need-th eigenvalue is below 1e-8 w_0 the unpreconditioned
 // sym_eig recomputes the result (device-side gate, no host sync).  n > 64 uses sym_eig.
 // rel_acc: fp64 data (preconditioned Jacobi, relative accuracy); else the tridiagonal solver.
+// A = Q U(:, 1:r) (m x r), canonical signs on A and U (reading R4b), and, when w is given,
+// residual = normsq - sum_{i<r} w_i: one launch for ell <= 64.
+void factor_epilogue(Ctx &c, const double *Q, int64_t m, int ell, double *U, int r, double *A, const double *w,
+                     const double *normsq, double *residual);
 void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps = nullptr, int r_need = 1 << 30,
               bool rel_acc = false);
 // Symmetric eigensolver for n <= 64 (trideig.cu): Householder tridiagonalisation, multisection,

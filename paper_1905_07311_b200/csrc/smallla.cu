@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 
 #include "kernels.h"
+#include "kernels_extra.h"
 
 namespace cg = cooperative_groups;
 
@@ -740,12 +741,10 @@ __device__ int chol_pivoted_left(const double *__restrict__ G, int np, int n, do
 }
 
 template <int kV, int LPS>
-__global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restrict__ Ain, int n, double *__restrict__ w,
-                                                          double *__restrict__ Vout, double tol, int max_sweeps,
-                                                          int *__restrict__ info, int r_need, int *__restrict__ refine,
-                                                          unsigned *__restrict__ status, const int *__restrict__ gate) {
-  if (gate && *gate == 0) return;  // the mixed-precision solver succeeded
-  extern __shared__ double gsm2[];
+__device__ void gram_eig_body(double *__restrict__ gsm2, const double *__restrict__ Ain, int n,
+                              double *__restrict__ w, double *__restrict__ Vout, double tol, int max_sweeps,
+                              int *__restrict__ info, int r_need, int *__restrict__ refine,
+                              unsigned *__restrict__ status) {
 #ifdef RTUCKER_EIG_PROF_BUILD
   long long et_[6];
   int en_ = 0;
@@ -872,6 +871,15 @@ __global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restri
     __syncthreads();  // w (global) written above by the sorting threads
     if (tid == 0) *refine = (w[r_need - 1] >= 1e-8 * w[0]) ? 0 : 1;
   }
+}
+
+template <int kV, int LPS>
+__global__ void __launch_bounds__(kGramT) gram_eig_kernel(const double *__restrict__ Ain, int n, double *__restrict__ w,
+                                                          double *__restrict__ Vout, double tol, int max_sweeps,
+                                                          int *__restrict__ info, int r_need, int *__restrict__ refine,
+                                                          unsigned *__restrict__ status) {
+  extern __shared__ double gsm_dyn[];
+  gram_eig_body<kV, LPS>(gsm_dyn, Ain, n, w, Vout, tol, max_sweeps, info, r_need, refine, status);
 }
 
 // ----------------------------------------------------- mixed-precision Gram eigensolver ----
@@ -1164,8 +1172,9 @@ __device__ int chol_pivoted_panel(double *__restrict__ A, int n, double *__restr
 
 __global__ void __launch_bounds__(kMxT) gram_eig_mixed_kernel(const double *__restrict__ Ain, int n,
                                                               double *__restrict__ w, double *__restrict__ Vout,
-                                                              int *__restrict__ info, int r_need,
-                                                              int *__restrict__ fallback, int max_sweeps) {
+                                                              int *__restrict__ info, int r_need, int max_sweeps,
+                                                              double tol64, int *__restrict__ refine,
+                                                              unsigned *__restrict__ status) {
   constexpr int kV = 16, LPS = 4, SPW = 8, NB = 8;  // 64 columns of 64 rows, 8 blocks of 8
   extern __shared__ double mxs[];
 #ifdef RTUCKER_EIG_PROF_BUILD
@@ -1197,15 +1206,19 @@ __global__ void __launch_bounds__(kMxT) gram_eig_mixed_kernel(const double *__re
     buf2[e] = 0.0;
     buf3[e] = 0.0;
   }
-  if (tid == 0) sbad = 0;
+  if (tid == 0) {
+    sbad = 0;
+    if (refine) *refine = 0;  // set again by the fp64 fallback when it needs the unpreconditioned solver
+  }
   __syncthreads();
   // ---- 1. pivoted Cholesky (fp64, blocked)
   __shared__ int csh[2];
   const int rank = chol_pivoted_panel(Eb, n, M, kMxLdm, csh);
   (void)np;
   MXP();
-  if (rank < n) {  // rank-deficient Gram: the fp64 Jacobi kernel handles the null space
-    if (tid == 0) *fallback = 1;
+  if (rank < n) {  // rank-deficient Gram: the fp64 Jacobi (null space as zero columns)
+    __syncthreads();
+    gram_eig_body<16, 4>(mxs, Ain, n, w, Vout, tol64, 40, info, r_need, refine, status);
     return;
   }
   // ---- 2. fp32 one-sided Jacobi on M / sqrt(max column norm^2) (no fp32 overflow / underflow)
@@ -1327,7 +1340,8 @@ __global__ void __launch_bounds__(kMxT) gram_eig_mixed_kernel(const double *__re
             rd = rd * fma(-den, rd, 2.0);
             rd = rd * fma(-den, rd, 2.0);
             E = num * rd;
-            if (fabs(E) > 1e-8 && fabs(num) > floor_num) lmore = 1;  // not yet at the noise floor
+            // another step unless this correction already leaves ~|E|^2 <= 1e-14 (or sits at the noise floor)
+            if (fabs(E) > 1e-7 && fabs(num) > floor_num) lmore = 1;
           } else {
             E = 0.5 * rij;  // a cluster at this step's resolution: orthogonalise only
             // harmful only when the pair straddles the wanted rank with a real gap
@@ -1355,8 +1369,9 @@ __global__ void __launch_bounds__(kMxT) gram_eig_mixed_kernel(const double *__re
     MXP();
   }
   if (tid == 0 && info) *info = sweeps + 1000 * it;
-  if (unresolved || more) {  // a straddling cluster, or no convergence in four steps
-    if (tid == 0) *fallback = 1;
+  if (unresolved || more) {  // a straddling cluster, or no convergence in four steps: fp64 Jacobi
+    __syncthreads();
+    gram_eig_body<16, 4>(mxs, Ain, n, w, Vout, tol64, 40, info, r_need, refine, status);
     return;
   }
   // eigenvalues: the last step's Rayleigh quotients (second order in the remaining error);
@@ -1771,7 +1786,7 @@ __device__ __forceinline__ void mma_blk8(double &c0, double &c1, const double *A
 
 __global__ void __launch_bounds__(kBQT, 1) cholqr2_blk_kernel(const double *__restrict__ Y, int64_t m, int n,
                                                               int rows, int ldY, int ldG, double *__restrict__ Q,
-                                                              int *__restrict__ bad) {
+                                                              int *__restrict__ bad, double orth_tol) {
   extern __shared__ __align__(16) double bq[];
   cg::cluster_group cl = cg::this_cluster();
   const int ncta = (int)cl.num_blocks();
@@ -1821,15 +1836,18 @@ __global__ void __launch_bounds__(kBQT, 1) cholqr2_blk_kernel(const double *__re
     cluster_arrive();
     cluster_wait();
     // ---- 2. cluster sum (fixed CTA order) into G
+    int far = 0;  // pass 1: an entry of Q^T Q - I above orth_tol
     for (int e = tid; e < n8 * n8; e += kBQT) {
       const int i = e / n8, j = e % n8;
       double sum = 0.0;
       for (int q = 0; q < ncta; ++q) sum += cl.map_shared_rank(Gp, q)[i * ldG + j];
       G[i * ldG + j] = sum;
       if (i == j) d0[i] = sum;
+      if (i < n && j < n) far |= !(fabs(sum - (i == j ? 1.0 : 0.0)) <= orth_tol);
     }
     cluster_arrive();  // matched by the wait before the next Gram (or before exit)
-    __syncthreads();
+    // the Gram is bit-identical in every CTA of the cluster, so every CTA takes the same decision
+    if (__syncthreads_or(far) == 0 && pass == 1) break;  // the first pass is orthonormal enough
     // ---- 3. blocked Cholesky G = R^T R (upper R in place) with D_kb = R_kb,kb^{-1}
     for (int kb = 0; kb < nbk; ++kb) {
       if (warp == 0) {
@@ -1996,10 +2014,73 @@ __global__ void canonical_signs_kernel(double *__restrict__ A, int64_t m, double
     for (int i = threadIdx.x; i < ell; i += blockDim.x) U[i + ldu * k] = -U[i + ldu * k];
 }
 
+// Alg 1 line 5 + reading R4b + the residual of the truncation in one launch (ell <= 64): CTA j
+// forms column j of A = Q U_B(:, 1:r) (fixed summation order over the ell columns of Q), flips it
+// and U_B's column j so that its largest-|entry| element (first index on ties) is positive, and
+// CTA 0 writes ||G||^2 - sum_{i<r} w_i (the truncated mode's residual, P:133 / Alg 3).
+__global__ void __launch_bounds__(256) factor_epilogue_kernel(const double *__restrict__ Q, int64_t m, int ell,
+                                                              double *__restrict__ U, double *__restrict__ A,
+                                                              const double *__restrict__ w, int r,
+                                                              const double *__restrict__ nsq, double *__restrict__ res) {
+  const int j = blockIdx.x;
+  __shared__ double u[64];
+  __shared__ double sv[8];
+  __shared__ int64_t si[8];
+  __shared__ double sgn;
+  if (threadIdx.x < ell) u[threadIdx.x] = U[threadIdx.x + (int64_t)ell * j];
+  if (res && j == 0 && threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < r; ++i) s += w[i];
+    *res = *nsq - s;
+  }
+  __syncthreads();
+  double *a = A + m * j;
+  double best = -1.0;
+  int64_t bi = 0;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    double acc = 0.0;
+    for (int t = 0; t < ell; ++t) acc = fma(Q[i + m * t], u[t], acc);
+    a[i] = acc;
+    const double v = fabs(acc);
+    if (v > best) { best = v; bi = i; }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+  }
+  if ((threadIdx.x & 31) == 0) { sv[threadIdx.x >> 5] = best; si[threadIdx.x >> 5] = bi; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double b = sv[0];
+    int64_t i0 = si[0];
+    for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww)
+      if (sv[ww] > b || (sv[ww] == b && si[ww] < i0)) { b = sv[ww]; i0 = si[ww]; }
+    sgn = a[i0] < 0.0 ? -1.0 : 1.0;  // (the thread that wrote a[i0] is in this CTA: visible after the barrier)
+  }
+  __syncthreads();
+  if (sgn > 0.0) return;
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) a[i] = -a[i];
+  if (threadIdx.x < ell) U[threadIdx.x + (int64_t)ell * j] = -u[threadIdx.x];
+}
+
 }  // namespace
 
 void canonical_signs(Ctx &c, double *A, int64_t m, int r, double *U, int64_t ldu, int ell) {
   RT_LAUNCH(c, canonical_signs_kernel, r, 256, 0, A, m, U, ldu, ell);
+}
+
+void factor_epilogue(Ctx &c, const double *Q, int64_t m, int ell, double *U, int r, double *A, const double *w,
+                     const double *normsq, double *residual) {
+  if (ell > 64) {  // the adaptive truncation's large bases: tensor-core GEMM + separate passes
+    gemm_small(c, false, Q, m, U, ell, A, m, m, r, ell);
+    canonical_signs(c, A, m, r, U, ell, ell);
+    if (w) residual_from_eigs(c, w, r, normsq, residual);
+    return;
+  }
+  const double *wz = w ? w : U;  // (r = 0 residual terms when w is null: the loop reads nothing)
+  RT_LAUNCH(c, factor_epilogue_kernel, r, 256, 0, Q, m, ell, U, A, wz, w ? r : 0, w ? normsq : U,
+            w ? residual : nullptr);
 }
 
 void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q, const int *gate) {
@@ -2072,20 +2153,17 @@ void gram_eig(Ctx &c, const double *A, int n, double *w, double *V, int *sweeps,
   const int rn = std::max(1, std::min(r_need, n));
   // fp32 data, 32 < n <= 64: the mixed-precision solver; the fp64 Jacobi below runs only when it
   // raises its fallback flag (rank-deficient Gram, unresolved pair across r_need)
-  const int *gate = nullptr;
-  DevBuf<int> fb;
   static const bool no_mixed = RT_EXP_GETENV("RTUCKER_EIG_NO_MIXED") != nullptr;
-  if (!rel_acc && n > 32 && !no_mixed) {
-    fb.alloc(c, 1);
-    fb.zero();
-    refine.zero();
+  if (!rel_acc && n > 32 && !no_mixed && lps == 4 && kv == 16) {
+    // the fp64 Jacobi runs inside the same launch when the solver falls back
     smem_attr(gram_eig_mixed_kernel, kMxSmem);
-    RT_LAUNCH(c, gram_eig_mixed_kernel, 1, kMxT, kMxSmem, A, n, w, V, sweeps, rn, fb.p, 15);
-    gate = fb.p;
+    RT_LAUNCH(c, gram_eig_mixed_kernel, 1, kMxT, kMxSmem, A, n, w, V, sweeps, rn, 15, tol, refine.p, c.status);
+    sym_eig(c, A, n, w, V, nullptr, refine.p);  // no-op unless the fallback's gate asks for it
+    return;
   }
 #define RT_GE(KV, L)                                                                                      \
   smem_attr(gram_eig_kernel<KV, L>, need);                                                                 \
-  RT_LAUNCH(c, (gram_eig_kernel<KV, L>), 1, kGramT, need, A, n, w, V, tol, 40, sweeps, rn, refine.p, c.status, gate)
+  RT_LAUNCH(c, (gram_eig_kernel<KV, L>), 1, kGramT, need, A, n, w, V, tol, 40, sweeps, rn, refine.p, c.status)
   if (lps == 8) {
     RT_GE(8, 8);
   } else if (kv == 4) {
@@ -2109,7 +2187,7 @@ void chol_rinv(Ctx &c, const double *G, int n, double *Rinv, int *bad) {
   RT_LAUNCH(c, tri_inv_upper_kernel, 1, 256, sizeof(double) * n * n, R.p, n, Rinv, bad);
 }
 
-void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
+void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q, double orth_tol) {
   RT_REQUIRE(m >= n && n >= 1, "qr: need m >= n >= 1");
   if (n > 64) return householder_qr(c, Y, m, n, Q, nullptr);
   static const bool no_chol = RT_EXP_GETENV("RTUCKER_QR_HOUSEHOLDER") != nullptr;
@@ -2142,7 +2220,7 @@ void thin_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q) {
     cfg.numAttrs = 1;
     if (blk) {
       smem_attr(cholqr2_blk_kernel, smem);
-      RT_CUDA(cudaLaunchKernelEx(&cfg, cholqr2_blk_kernel, Y, m, n, rows, ldY, ldG, Q, bad.p));
+      RT_CUDA(cudaLaunchKernelEx(&cfg, cholqr2_blk_kernel, Y, m, n, rows, ldY, ldG, Q, bad.p, orth_tol));
     } else {
       smem_attr(cholqr2_cluster_kernel, smem);
       RT_CUDA(cudaLaunchKernelEx(&cfg, cholqr2_cluster_kernel, Y, m, n, rows, ldY, ldG, ldE, Q, bad.p));
