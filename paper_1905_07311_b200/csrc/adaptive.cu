@@ -62,6 +62,82 @@ __global__ void sub_gemm_kernel(double *__restrict__ W, int64_t m, int b, const 
   }
 }
 
+// Skinny projection W <- W - Q (Q^T W) of one block (m x b, b <= 16) against the basis so far
+// (Q: m x k), fp64, fixed summation order (deterministic).  The tensor-core GEMM tiles of
+// 64 x 64 left these k x b / m x b products at 12-25 CTAs and ~68 us each (4 per block, 59 ms
+// of the C4 adaptive call); here:
+//   proj_t_kernel:   T = Q^T W, one warp per row j of T (lanes stride the m rows, b running
+//                    sums each, fixed-order warp tree); W staged once per CTA in shared memory;
+//   proj_sub_kernel: W -= Q T, one CTA per 32 rows, its 8 warps split the k columns of Q, and
+//                    the 8 partial sums are added in warp order through shared memory.
+constexpr int kProjB = 16;
+__global__ void __launch_bounds__(256) proj_t_kernel(const double *__restrict__ Q, int64_t m, int k,
+                                                     const double *__restrict__ W, int b, double *__restrict__ T) {
+  extern __shared__ double wsm[];  // m x b (column-major, ld m)
+  for (int64_t e = threadIdx.x; e < m * b; e += blockDim.x) wsm[e] = W[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (j >= k) return;
+  double acc[kProjB];
+#pragma unroll
+  for (int c = 0; c < kProjB; ++c) acc[c] = 0.0;
+  const double *qj = Q + m * j;
+  for (int64_t i = lane; i < m; i += 32) {
+    const double q = qj[i];
+#pragma unroll
+    for (int c = 0; c < kProjB; ++c)
+      if (c < b) acc[c] = fma(q, wsm[i + m * c], acc[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < kProjB; ++c) {
+    double v = acc[c];
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0 && c < b) T[j + (int64_t)k * c] = v;
+  }
+}
+
+__global__ void __launch_bounds__(256) proj_sub_kernel(double *__restrict__ W, int64_t m, int b,
+                                                       const double *__restrict__ Q, int k,
+                                                       const double *__restrict__ T) {
+  __shared__ double part[8][32][kProjB + 1];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+  const int per = (k + 7) / 8, j0 = warp * per, j1 = min(k, j0 + per);
+  double acc[kProjB];
+#pragma unroll
+  for (int c = 0; c < kProjB; ++c) acc[c] = 0.0;
+  if (i < m)
+    for (int j = j0; j < j1; ++j) {
+      const double q = Q[i + m * j];
+#pragma unroll
+      for (int c = 0; c < kProjB; ++c)
+        if (c < b) acc[c] = fma(q, T[j + (int64_t)k * c], acc[c]);
+    }
+#pragma unroll
+  for (int c = 0; c < kProjB; ++c) part[warp][lane][c] = acc[c];
+  __syncthreads();
+  if (warp == 0 && i < m) {
+    for (int c = 0; c < b; ++c) {
+      double s = 0.0;
+      for (int w = 0; w < 8; ++w) s += part[w][lane][c];
+      W[i + m * c] -= s;
+    }
+  }
+}
+
+void project_out(Ctx &c, const double *Q, int64_t m, int k, double *W, int b, double *T) {
+  const size_t sm = sizeof(double) * (size_t)m * b;
+  if (b > kProjB || sm > 200 * 1024) {  // outside the skinny kernels' envelope: the GEMMs
+    gemm_f64(c, true, Q, m, W, m, T, k, k, b, m);
+    gemm_f64(c, false, Q, m, T, k, W, m, m, b, k, 1.0, -1.0);
+    return;
+  }
+  if (sm > 48 * 1024) smem_attr(proj_t_kernel, sm);
+  RT_LAUNCH(c, proj_t_kernel, (k + 7) / 8, 256, sm, Q, m, k, (const double *)W, b, T);
+  RT_LAUNCH(c, proj_sub_kernel, (int)((m + 31) / 32), 256, 0, W, m, b, Q, k, (const double *)T);
+}
+
 // ---------------------------------------------------------------------------------------
 // Fused block pass for fp64 cores (SURVEY §3.3 "B_i + next sketch"): ONE read of G_(n) gives
 //   B_i     = Q_i^T G_(n)                      (b x P, stored (L, b, R)) and its Gram, and
@@ -453,10 +529,7 @@ ModeOut adapt_mode(Ctx &c, const void *G, DT gt, const int64_t *cur, const int64
     }
     PhaseScope ps(c, PH_QR, n);
     if (k > 0) {  // W <- (I - Q Q^T) W, twice (re-orthogonalisation)
-      for (int rep = 0; rep < 2; ++rep) {
-        gemm_f64(c, true, Q.p, I, W.p, I, T.p, k, k, bb, I);                 // T = Q^T W
-        gemm_f64(c, false, Q.p, I, T.p, k, W.p, I, I, bb, k, 1.0, -1.0);     // W -= Q T
-      }
+      for (int rep = 0; rep < 2; ++rep) project_out(c, Q.p, I, k, W.p, bb, T.p);  // T = Q^T W, W -= Q T
     }
     double *Qi = Q.p + (size_t)I * k;
     householder_qr(c, W.p, I, bb, Qi);  // the basis of Q is the core basis with ADAPT_NO_TRUNCATE

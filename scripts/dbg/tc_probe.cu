@@ -11,6 +11,9 @@ __global__ void probe(const float *A, const float *B, float *D, int mode, int va
   __shared__ uint64_t bar;
   __shared__ uint32_t slot;
   int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  // zero the operand area first (an earlier version zeroed it AFTER writing A: every mode read 0)
+  for (int idx = t; idx < 190 * 1024 / 4; idx += blockDim.x) ((float *)sa)[idx] = 0.f;
+  __syncthreads();
   // A(m, k) m<128, k<8: atom a = m/32, row r = k, 16B chunk j = (m%32)/4, within-chunk e = m%4
   for (int idx = t; idx < 128 * 8; idx += blockDim.x) {
     int m = idx % 128, k = idx / 128;
@@ -47,13 +50,27 @@ __global__ void probe(const float *A, const float *B, float *D, int mode, int va
       *(float *)(sb + k * 128 + (((n / 4) ^ (k % 8)) * 16) + (n % 4) * 4) = B[n + 32 * k];
     }
   }
-  if (mode >= 9) {  // A K-major no swizzle
+  if (mode == 15) {  // A MN-major SWIZZLE_128B_BASE32B (CUTLASS Layout_MN_SW128_32B_Atom): atom = 4 k-rows x
+    // 128 B (32 m), 32-byte chunk c = (m % 32) / 8 stored at c ^ (k % 4); atoms along m at LBO = 512,
+    // k-groups of 4 at SBO = 2048
+    for (int idx = t; idx < 128 * 8; idx += blockDim.x) {
+      int m = idx % 128, k = idx / 128;
+      int off = (m / 32) * 512 + (k / 4) * 2048 + (k % 4) * 128 + ((((m % 32) / 8) ^ (k % 4)) * 32) + (m % 8) * 4;
+      *(float *)(sa + off) = A[m + 128 * k];
+    }
+  }
+  if (mode == 16) {  // B MN-major SWIZZLE_128B_BASE32B: n < 32 = one atom along n, k-groups at SBO = 512
+    for (int idx = t; idx < 32 * 8; idx += blockDim.x) {
+      int n = idx % 32, k = idx / 32;
+      *(float *)(sb + (k / 4) * 512 + (k % 4) * 128 + ((((n % 32) / 8) ^ (k % 4)) * 32) + (n % 8) * 4) = B[n + 32 * k];
+    }
+  }
+  if (mode >= 9 && mode != 15) {  // A K-major no swizzle
     for (int idx = t; idx < 128 * 8; idx += blockDim.x) {
       int m = idx % 128, k = idx / 128;
       *(float *)(sa + (m / 8) * 256 + (k / 4) * 128 + (m % 8) * 16 + (k % 4) * 4) = A[m + 128 * k];
     }
   }
-  for (int idx = t; idx < 190 * 1024 / 4; idx += blockDim.x) ((float *)sa)[idx] = 0.f;
   __syncthreads();
   if (mode == 14) {  // truncation test, K-major no swizzle: A(0,0) = 1+2^-11+2^-13, B(n,0) = 1
     for (int idx = t; idx < 128 * 8; idx += blockDim.x) {
@@ -103,7 +120,16 @@ __global__ void probe(const float *A, const float *B, float *D, int mode, int va
     if (mode == 5) ad = tc::smem_desc(tc::smem_u32(sa), 1024, 128, tc::kSwNone);
     if (mode == 6) ad = tc::smem_desc(tc::smem_u32(sa), 128, 1024, tc::kSwNone);
     if (mode == 7) ad = tc::smem_desc(tc::smem_u32(sa), 1024, 1024, tc::kSw128);
-    if (mode >= 9) {
+    if (mode == 15) {
+      ad = tc::smem_desc(tc::smem_u32(sa), 512, 2048, 1u);
+      tc::mma_tf32(tm, ad, bd, tc::idesc_tf32(128, 32, true, false), 0);
+    }
+    if (mode == 16) {
+      ad = tc::smem_desc(tc::smem_u32(sa), 128, 256, tc::kSwNone);
+      bd = tc::smem_desc(tc::smem_u32(sb), 512, 512, 1u);
+      tc::mma_tf32(tm, ad, bd, tc::idesc_tf32(128, 32, false, true), 0);
+    }
+    if (mode >= 9 && mode <= 10) {
       ad = tc::smem_desc(tc::smem_u32(sa), 128, 256, tc::kSwNone);
       bd = mode == 9 ? tc::smem_desc(tc::smem_u32(sb), 1024, 128, tc::kSwNone) : tc::smem_desc(tc::smem_u32(sb), 1024, 1024, tc::kSw128);
       tc::mma_tf32(tm, ad, bd, tc::idesc_tf32(128, 32, false, true), 0);
