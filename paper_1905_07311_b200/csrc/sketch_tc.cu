@@ -13,10 +13,10 @@
 //                hi/lo tf32 K-major tiles (NSG stages deep, so the long RNG dependency chain
 //                runs ahead of the X pipeline)
 //   warps 6-13   X workers: split X = hi + lo (both rounded to the tf32 grid, R15) and
-//                write both TRANSPOSED into K-major operand tiles (the tensor core reads tf32
-//                operands K-major only: MN-major tf32 A or B measured as all-zero output on
-//                this B200, scripts/dbg/tc_probe.cu); accumulate ||X||^2; after the last
-//                stage: TMEM -> fp64 partial Y.
+//                write both TRANSPOSED into K-major no-swizzle operand tiles (MN-major tf32
+//                operands need the SWIZZLE_128B_BASE32B layout; this kernel keeps
+//                the K-major split); accumulate ||X||^2; after the last stage: TMEM -> fp64
+//                partial Y.
 //   The accumulator of M-tile mt (rows 128 mt ..) lives in TMEM columns [mt N, mt N + N):
 //   3 MMAs per M-tile and stage, D += Xhi*Ohi + Xhi*Olo + Xlo*Ohi (M=128, N, K=8), fp32
 //   accumulation in TMEM (BASELINE "3xTF32"; the dropped Xlo*Olo term is 2^-22 relative).

@@ -2014,54 +2014,84 @@ __global__ void canonical_signs_kernel(double *__restrict__ A, int64_t m, double
     for (int i = threadIdx.x; i < ell; i += blockDim.x) U[i + ldu * k] = -U[i + ldu * k];
 }
 
-// Alg 1 line 5 + reading R4b + the residual of the truncation in one launch (ell <= 64): CTA j
-// forms column j of A = Q U_B(:, 1:r) (fixed summation order over the ell columns of Q), flips it
-// and U_B's column j so that its largest-|entry| element (first index on ties) is positive, and
-// CTA 0 writes ||G||^2 - sum_{i<r} w_i (the truncated mode's residual, P:133 / Alg 3).
-__global__ void __launch_bounds__(256) factor_epilogue_kernel(const double *__restrict__ Q, int64_t m, int ell,
-                                                              double *__restrict__ U, double *__restrict__ A,
-                                                              const double *__restrict__ w, int r,
-                                                              const double *__restrict__ nsq, double *__restrict__ res) {
-  const int j = blockIdx.x;
-  __shared__ double u[64];
-  __shared__ double sv[8];
-  __shared__ int64_t si[8];
-  __shared__ double sgn;
-  if (threadIdx.x < ell) u[threadIdx.x] = U[threadIdx.x + (int64_t)ell * j];
-  if (res && j == 0 && threadIdx.x == 0) {
+// Alg 1 line 5 + reading R4b + the residual of the truncation (ell, r <= 64), two launches:
+//   factor_gemm_kernel: CTA b forms rows 16b .. 16b + 15 of A = Q U(:, 1:r) from shared-memory
+//     copies of its Q slab and of U (fixed summation order over the ell columns of Q) and
+//     records, per column, the largest |A_ij| of its rows and its first row index;
+//   factor_sign_kernel: CTA j reduces those partials in block order (largest value, smallest
+//     row on ties), flips A(:, j) and U(:, j) when that entry is negative, and CTA 0 writes
+//     ||G||^2 - sum_{i<r} w_i (the truncated mode's residual, P:133 / Alg 3).
+// (One CTA per column reading all of Q measured 61 us: dependent L2 loads per thread.)
+constexpr int kFeRows = 16;
+__global__ void __launch_bounds__(256) factor_gemm_kernel(const double *__restrict__ Q, int64_t m, int ell,
+                                                          const double *__restrict__ U, int r, double *__restrict__ A,
+                                                          double *__restrict__ pmax, int *__restrict__ pidx) {
+  __shared__ double us[64][64], qs[kFeRows][64];  // (row reads broadcast, column reads consecutive)
+  __shared__ double bm[4][64];
+  __shared__ int bi[4][64];
+  const int tid = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.x * kFeRows;
+  for (int e = tid; e < ell * r; e += 256) us[e % ell][e / ell] = U[(e % ell) + (int64_t)ell * (e / ell)];
+  for (int e = tid; e < kFeRows * ell; e += 256) {
+    const int i = e % kFeRows, t = e / kFeRows;
+    qs[i][t] = r0 + i < m ? Q[r0 + i + m * t] : 0.0;
+  }
+  __syncthreads();
+  const int j = tid & 63, g = tid >> 6;
+  double best = -1.0;
+  int besti = 0;
+  if (j < r) {
+    for (int k = 0; k < kFeRows / 4; ++k) {
+      const int i = g + 4 * k;
+      double acc = 0.0;
+      for (int t = 0; t < ell; ++t) acc = fma(qs[i][t], us[t][j], acc);
+      if (r0 + i < m) {
+        A[r0 + i + m * j] = acc;
+        const double v = fabs(acc);
+        if (v > best) { best = v; besti = (int)(r0 + i); }  // rows ascending: first index kept on ties
+      }
+    }
+  }
+  bm[g][j] = best;
+  bi[g][j] = besti;
+  __syncthreads();
+  if (g == 0 && j < r) {
+    double b = bm[0][j];
+    int ii = bi[0][j];
+    for (int q = 1; q < 4; ++q)
+      if (bm[q][j] > b || (bm[q][j] == b && bi[q][j] < ii)) { b = bm[q][j]; ii = bi[q][j]; }
+    pmax[(int64_t)blockIdx.x * r + j] = b;
+    pidx[(int64_t)blockIdx.x * r + j] = ii;
+  }
+}
+
+__global__ void __launch_bounds__(32) factor_sign_kernel(double *__restrict__ A, int64_t m, int ell,
+                                                         double *__restrict__ U, int r, int nblk,
+                                                         const double *__restrict__ pmax, const int *__restrict__ pidx,
+                                                         const double *__restrict__ w, const double *__restrict__ nsq,
+                                                         double *__restrict__ res) {
+  const int j = blockIdx.x, lane = threadIdx.x;
+  if (res && j == 0 && lane == 0) {
     double s = 0.0;
     for (int i = 0; i < r; ++i) s += w[i];
     *res = *nsq - s;
   }
-  __syncthreads();
-  double *a = A + m * j;
   double best = -1.0;
-  int64_t bi = 0;
-  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-    double acc = 0.0;
-    for (int t = 0; t < ell; ++t) acc = fma(Q[i + m * t], u[t], acc);
-    a[i] = acc;
-    const double v = fabs(acc);
-    if (v > best) { best = v; bi = i; }
+  int bi = 0;
+  for (int b = lane; b < nblk; b += 32) {  // blocks ascending per lane
+    const double v = pmax[(int64_t)b * r + j];
+    const int ii = pidx[(int64_t)b * r + j];
+    if (v > best) { best = v; bi = ii; }
   }
   for (int o = 16; o; o >>= 1) {
     const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-    const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
     if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
   }
-  if ((threadIdx.x & 31) == 0) { sv[threadIdx.x >> 5] = best; si[threadIdx.x >> 5] = bi; }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double b = sv[0];
-    int64_t i0 = si[0];
-    for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww)
-      if (sv[ww] > b || (sv[ww] == b && si[ww] < i0)) { b = sv[ww]; i0 = si[ww]; }
-    sgn = a[i0] < 0.0 ? -1.0 : 1.0;  // (the thread that wrote a[i0] is in this CTA: visible after the barrier)
-  }
-  __syncthreads();
-  if (sgn > 0.0) return;
-  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) a[i] = -a[i];
-  if (threadIdx.x < ell) U[threadIdx.x + (int64_t)ell * j] = -u[threadIdx.x];
+  double *a = A + m * j;
+  if (a[bi] >= 0.0) return;
+  for (int64_t i = lane; i < m; i += 32) a[i] = -a[i];
+  for (int t = lane; t < ell; t += 32) U[t + (int64_t)ell * j] = -U[t + (int64_t)ell * j];
 }
 
 }  // namespace
@@ -2078,9 +2108,12 @@ void factor_epilogue(Ctx &c, const double *Q, int64_t m, int ell, double *U, int
     if (w) residual_from_eigs(c, w, r, normsq, residual);
     return;
   }
-  const double *wz = w ? w : U;  // (r = 0 residual terms when w is null: the loop reads nothing)
-  RT_LAUNCH(c, factor_epilogue_kernel, r, 256, 0, Q, m, ell, U, A, wz, w ? r : 0, w ? normsq : U,
-            w ? residual : nullptr);
+  const int nblk = (int)((m + kFeRows - 1) / kFeRows);
+  DevBuf<double> pmax(c, (size_t)nblk * r);
+  DevBuf<int> pidx(c, (size_t)nblk * r);
+  RT_LAUNCH(c, factor_gemm_kernel, nblk, 256, 0, Q, m, ell, (const double *)U, r, A, pmax.p, pidx.p);
+  RT_LAUNCH(c, factor_sign_kernel, r, 32, 0, A, m, ell, U, r, nblk, (const double *)pmax.p, (const int *)pidx.p, w,
+            normsq, w ? residual : nullptr);
 }
 
 void householder_qr(Ctx &c, const double *Y, int64_t m, int n, double *Q, const int *gate) {
