@@ -262,7 +262,9 @@ def bench_sparse(args):
     it = torch.as_tensor(np.ascontiguousarray(idx[:, lo:hi]), device="cuda")
     vt = torch.as_tensor(np.ascontiguousarray(vals[lo:hi]), device="cuda")
     stream = torch.cuda.Stream()
-    ctx = Context(local, stream=stream, group=dist.group.WORLD if world > 1 else None)
+    # the library's own stream-ordered pool: no Python allocator callbacks (and no torch cache
+    # trims) inside the timed region; torch's allocator stays the binding's default for users
+    ctx = Context(local, stream=stream, group=dist.group.WORLD if world > 1 else None, allocator="library")
     step = lambda: ctx.sparse_sthosvd(it, vt, dims, (10, 10, 10, 10), 5, SEED, None, 2.0)
     for _ in range(args.warmup):
         step().free()
@@ -344,7 +346,9 @@ def main():
     shard = (off, ext[rank]) if world > 1 else None
     torch.cuda.synchronize()
     stream = torch.cuda.Stream()  # the library enqueues every kernel of a step on this stream
-    ctx = Context(local, stream=stream, group=dist.group.WORLD if world > 1 else None)
+    # the library's own stream-ordered pool: no Python allocator callbacks (and no torch cache
+    # trims) inside the timed region; torch's allocator stays the binding's default for users
+    ctx = Context(local, stream=stream, group=dist.group.WORLD if world > 1 else None, allocator="library")
 
     def step(inp, flags=0):
         if args.algo == "sthosvd":

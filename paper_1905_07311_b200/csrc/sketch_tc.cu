@@ -351,6 +351,268 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// L == 1, MN-major A (sketch_tc_mna_kernel, round 2): X_(1) tiles go from TMA straight into the
+// MMA's A-operand layout.  tcgen05 kind::tf32 reads an MN-major operand in the SWIZZLE_128B_BASE32B
+// layout (atoms of 4 K-rows x 128 B along M, 32-byte chunk j of K-row k stored at j ^ (k % 4)),
+// and TMA's CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B writes exactly that for a box of 32 rows i x 8
+// columns c (measured, scripts/dbg/tma_swz_probe.cu).  So one stage = ceil(I / 32) boxes of 1 KB,
+// M-tile mt = 4 boxes (LBO = 1 KB between 32-row atoms, SBO = 512 B between the two 4-column
+// groups), and the raw fp32 X IS the hi operand: the tensor core truncates it to tf32, x_t =
+// trunc(x).  The X workers no longer transpose: they write X_lo = rn_tf32(x - x_t) elementwise
+// in the same layout (exact difference, rounded to the tf32 grid: residual <= 2^-11 |x - x_t|
+// <= 2^-21 |x|, unbiased), and keep ||X||^2 and the Ozaki column maxima (a thread's chunks all
+// lie in one column c of the stage).  D += x_t Ohi + x_t Olo + X_lo Ohi as in R15 (hi split by
+// truncation instead of rounding; same tf32 grid).  Shared-memory traffic per X byte: TMA write,
+// one worker read, the lo write and three operand reads (the K-major kernel also wrote the hi
+// plane and transposed through shared memory).
+//   warp 0 TMA producer, warp 1 TMEM + MMA issuer, warps 2-5 Omega generators (as in
+//   sketch_tc_mn_kernel), warps 6-13 X workers; stage s = (x plane, lo plane), NS deep.
+constexpr int kMnaJ = 7;  // 16-byte chunks per worker thread and stage (NT <= 7: 28 KB / 4 KB)
+
+template <int N>
+__global__ void __launch_bounds__(kThreads, 1)
+    sketch_tc_mna_kernel(const __grid_constant__ CUtensorMap tmap, const SketchTcParams p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
+  unsigned char *base = smem_raw + pad;
+  const int NT = p.NT, NS = p.NSS, nbox = p.nbox;
+  const int abytes = NT * 4096;                    // one plane: NT M-tiles x (128 rows x 8 K fp32)
+  constexpr int obytes = N * kBK * 4;
+  unsigned char *xb = base;                        // [NS][abytes] X as loaded (the hi operand)
+  unsigned char *lb = xb + (size_t)NS * abytes;    // [NS][abytes] X_lo
+  unsigned char *ohb = lb + (size_t)NS * abytes;   // [kNSG][obytes]
+  unsigned char *olb = ohb + (size_t)kNSG * obytes;// [kNSG][obytes]
+  uint64_t *full = (uint64_t *)(olb + (size_t)kNSG * obytes);
+  uint64_t *sfree = full + NS;    // the MMAs of stage s finished reading both planes
+  uint64_t *xready = sfree + NS;  // workers wrote X_lo of stage s
+  uint64_t *oready = xready + NS;
+  uint64_t *oempty = oready + kNSG;
+  uint64_t *done = oempty + kNSG;
+  uint32_t *tslot = (uint32_t *)(done + 1);
+  double *wsum = (double *)(tslot + 2);            // [kWorkers]
+
+#ifdef RTUCKER_SK_PROF_BUILD
+  long long skp[5] = {0, 0, 0, 0, 0}, skp_t = 0;
+  const long long skp_start = clock64();
+#define SKP_T0() skp_t = clock64()
+#define SKP_ACC(i) skp[i] += clock64() - skp_t
+#else
+#define SKP_T0()
+#define SKP_ACC(i)
+#endif
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t cbeg = (int64_t)blockIdx.x * p.cps;
+  const int64_t cend = min(p.C, cbeg + p.cps);
+  const int nst = (int)((cend - cbeg + kBK - 1) / kBK);
+  const uint32_t tcols = NT * N <= 32 ? 32 : NT * N <= 64 ? 64 : NT * N <= 128 ? 128 : NT * N <= 256 ? 256 : 512;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&sfree[s], 1);
+      tc::mbar_init(&xready[s], 32 * kWorkers);
+    }
+    for (int s = 0; s < kNSG; ++s) {
+      tc::mbar_init(&oready[s], 32 * kGen);
+      tc::mbar_init(&oempty[s], 1);
+    }
+    tc::mbar_init(done, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tslot, tcols);
+  // Omega tiles: columns n >= ell stay zero; atoms past the last TMA box (rows >= 32 nbox, only
+  // ever read into D rows >= I, which are discarded) are zeroed once in both planes
+  for (int e = threadIdx.x; e < 2 * kNSG * obytes / 4; e += kThreads) ((float *)ohb)[e] = 0.f;
+  {
+    const int pad_f = (4 * NT - nbox) * 256;  // floats per plane past the boxes
+    for (int e = threadIdx.x; e < 2 * NS * pad_f; e += kThreads) {
+      const int pl = e / pad_f, f = e % pad_f;
+      ((float *)(xb + (size_t)pl * abytes + (size_t)nbox * 1024))[f] = 0.f;
+    }
+  }
+  tc::fence_proxy_async_smem();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------- TMA producer
+    if (lane == 0 && nst > 0) {
+      tc::tma_prefetch_desc(&tmap);
+      const uint32_t bytes = (uint32_t)nbox * 1024u;
+      for (int it = 0; it < nst; ++it) {
+        const int s = it % NS;
+        SKP_T0();
+        if (it >= NS) tc::mbar_wait(&sfree[s], ((it / NS) & 1) ^ 1);
+        SKP_ACC(0);
+        tc::mbar_arrive_expect_tx(&full[s], bytes);
+        const int c0 = (int)(cbeg + (int64_t)it * kBK);
+        unsigned char *dst = xb + (size_t)s * abytes;
+        if (p.L == 3)  // 3-D map (32 rows, columns, row blocks): all nbox boxes in one instruction
+          tc::tma_load_3d(dst, &tmap, &full[s], 0, c0, 0);
+        else  // (one TMA instruction per 1 KB box: the producer's issue rate bounds the kernel)
+          for (int b = 0; b < nbox; ++b) tc::tma_load_2d(dst + b * 1024, &tmap, &full[s], 32 * b, c0);
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------- MMA issuer (warp-wide)
+    if (nst > 0) {
+      constexpr uint32_t idesc = tc::idesc_tf32(128, N, true, false);
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint32_t xb0 = __shfl_sync(0xffffffffu, tc::smem_u32(xb), 0);
+      const uint32_t lb0 = __shfl_sync(0xffffffffu, tc::smem_u32(lb), 0);
+      const uint32_t obh = __shfl_sync(0xffffffffu, tc::smem_u32(ohb), 0);
+      const uint32_t obl = __shfl_sync(0xffffffffu, tc::smem_u32(olb), 0);
+      for (int it = 0; it < nst; ++it) {
+        const int s = it % NS, g = it % kNSG;
+        SKP_T0();
+        tc::mbar_wait(&oready[g], (it / kNSG) & 1);
+        SKP_ACC(1);
+        tc::mbar_wait(&xready[s], (it / NS) & 1);
+        SKP_ACC(2);
+        tc::tc_fence_after();
+        const uint32_t xa = xb0 + s * abytes, la = lb0 + s * abytes;
+        const uint64_t bh = tc::smem_desc(obh + g * obytes, 128, 256, tc::kSwNone);
+        const uint64_t bl = tc::smem_desc(obl + g * obytes, 128, 256, tc::kSwNone);
+        for (int mt = 0; mt < NT; ++mt) {
+          const uint64_t ah = tc::smem_desc(xa + mt * 4096, 1024, 512, tc::kSw128Base32);
+          const uint64_t al = tc::smem_desc(la + mt * 4096, 1024, 512, tc::kSw128Base32);
+          const uint32_t d = tm + mt * N;
+          tc::mma_tf32_w(d, ah, bh, idesc, it > 0 ? 1u : 0u);
+          tc::mma_tf32_w(d, ah, bl, idesc, 1u);
+          tc::mma_tf32_w(d, al, bh, idesc, 1u);
+        }
+        tc::mma_commit_w(&sfree[s]);
+        tc::mma_commit_w(&oempty[g]);
+      }
+      tc::mma_commit_w(done);
+    }
+  } else if (warp < 2 + kGen) {
+    // ------------------------------------------------------------- Omega generators
+    const int gt = threadIdx.x - 64;  // 0 .. 32*kGen-1
+    const int64_t jb0 = p.k0 >> 2;
+    const int nb = (int)(((p.k0 + p.ell - 1) >> 2) - jb0 + 1);
+    for (int it = 0; it < nst; ++it) {
+      const int g = it % kNSG;
+      const int64_t c0 = cbeg + (int64_t)it * kBK;
+      SKP_T0();
+      if (it >= kNSG) tc::mbar_wait(&oempty[g], ((it / kNSG) & 1) ^ 1);
+      SKP_ACC(3);
+      float *oh = (float *)(ohb + (size_t)g * obytes), *ol = (float *)(olb + (size_t)g * obytes);
+      for (int t = gt; t < kBK * nb; t += 32 * kGen) {
+        const int kk = t & (kBK - 1), jb = t >> 3;
+        const int64_t c = c0 + kk;
+        const bool valid = c < cend;
+        const uint4 w = omega_words(p.seed, p.mode, 0, (uint64_t)(c + p.col_offset), (uint32_t)(jb0 + jb));
+        Normal4<float> z(w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t n = 4 * (jb0 + jb) + q - p.k0;
+          if (n >= 0 && n < p.ell) {
+            const float v = valid ? z.v[q] : 0.f;
+            const float hi = tc::tf32_hi(v);
+            const int off = kmaj_off((int)n, kk) >> 2;
+            oh[off] = hi;
+            ol[off] = tc::tf32_lo(v, hi);
+          }
+        }
+      }
+      tc::fence_proxy_async_smem();
+      tc::mbar_arrive(&oready[g]);
+    }
+  } else {
+    // ------------------------------------------------------------- X workers
+    const int wt = threadIdx.x - 32 * (2 + kGen);  // 0 .. 32*kWorkers-1
+    const int nch = nbox * 64;                     // 16-byte chunks per stage
+    const int ccol = (wt & 63) >> 3;               // the stage column all of this thread's chunks hold
+    double nsq = 0.0;
+    for (int it = 0; it < nst; ++it) {
+      const int s = it % NS;
+      SKP_T0();
+      tc::mbar_wait(&full[s], (it / NS) & 1);  // (TMA refilled stage s only after its MMAs finished)
+      SKP_ACC(4);
+      const unsigned char *xs = xb + (size_t)s * abytes;
+      unsigned char *ls = lb + (size_t)s * abytes;
+      float acc = 0.f, cm = 0.f;
+      // all of the thread's chunks (<= kMnaJ) loaded first, then split and stored: the loads
+      // are independent, so their latency overlaps instead of chaining per chunk
+      float4 xv[kMnaJ];
+#pragma unroll
+      for (int j = 0; j < kMnaJ; ++j) {
+        const int q = wt + 32 * kWorkers * j;
+        xv[j] = q < nch ? *(const float4 *)(xs + 16 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int j = 0; j < kMnaJ; ++j) {
+        const int q = wt + 32 * kWorkers * j;
+        const float4 x = xv[j];
+        float4 l;
+        l.x = tc::tf32_rn(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u));
+        l.y = tc::tf32_rn(x.y - __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u));
+        l.z = tc::tf32_rn(x.z - __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u));
+        l.w = tc::tf32_rn(x.w - __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u));
+        if (q < nch) *(float4 *)(ls + 16 * q) = l;
+        acc = fmaf(x.x, x.x, acc); acc = fmaf(x.y, x.y, acc); acc = fmaf(x.z, x.z, acc); acc = fmaf(x.w, x.w, acc);
+        cm = fmaxf(cm, fmaxf(fmaxf(fabsf(x.x), fabsf(x.y)), fmaxf(fabsf(x.z), fabsf(x.w))));
+      }
+      if (p.colmax) {  // lanes 8g .. 8g + 7 of a warp share one column: 3 shuffles, one atomic
+        cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 1));
+        cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 2));
+        cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, 4));
+        const int64_t c = cbeg + (int64_t)it * kBK + ccol;
+        if ((lane & 7) == 0 && c < cend) atomicMax(p.colmax + c, __float_as_uint(cm));
+      }
+      nsq += (double)acc;
+      tc::fence_proxy_async_smem();
+      tc::mbar_arrive(&xready[s]);
+    }
+    // ---- epilogue: TMEM -> fp64 partial[blockIdx.x][k * I + i]
+    const int q4 = warp & 3;                       // TMEM lane quadrant of this warp
+    const int half = (warp - 2 - kGen) >> 2;       // 0 / 1: which 32 of the N columns
+    if (nst > 0) {
+      tc::mbar_wait(done, 0);
+      tc::tc_fence_after();
+    }
+    double *dst = p.partial + (int64_t)blockIdx.x * p.ell * p.I;
+    if (half * 32 < N) {
+      for (int mt = 0; mt < NT; ++mt) {
+        uint32_t rr[32];
+        if (nst > 0) tc::tmem_ld32(tmem + ((uint32_t)(32 * q4) << 16) + mt * N + half * 32, rr);
+        const int64_t i = (int64_t)mt * 128 + 32 * q4 + lane;
+        if (i < p.I) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int k = half * 32 + j;
+            if (k < p.ell) dst[(int64_t)k * p.I + i] = nst > 0 ? (double)__uint_as_float(rr[j]) : 0.0;
+          }
+        }
+      }
+    }
+    if (p.norm_partial) {
+      for (int o = 16; o; o >>= 1) nsq += __shfl_xor_sync(0xffffffffu, nsq, o);
+      if (lane == 0) wsum[warp - 2 - kGen] = nsq;
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (p.norm_partial && threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < kWorkers; ++w) s += wsum[w];
+    p.norm_partial[blockIdx.x] = s;
+  }
+  if (warp == 1) {
+    tc::tc_fence_after();
+    tc::tmem_dealloc(tmem, tcols);
+  }
+#ifdef RTUCKER_SK_PROF_BUILD
+  if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 32 || threadIdx.x == 64 || threadIdx.x == 192))
+    printf("[mna prof] tid %d nst %d: wait sfree %lld oready %lld xready %lld oempty %lld full %lld total %lld\n",
+           threadIdx.x, nst, skp[0], skp[1], skp[2], skp[3], skp[4], clock64() - skp_start);
+#endif
+}
+
 #ifdef RTUCKER_EXPERIMENTS  // TMEM-A variant: measured slower, kept for experiments builds only
 // ---------------------------------------------------------------------------------------------
 // L == 1 variant with the A operand in TMEM (sketch_tc_ta_kernel).  The smem-operand kernel
@@ -765,6 +1027,79 @@ bool sketch_ta(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0
 
 #endif  // RTUCKER_EXPERIMENTS
 
+template <int N>
+void launch_mna(Ctx &c, const CUtensorMap &tm, SketchTcParams &p, int grid, size_t smem) {
+  auto k = sketch_tc_mna_kernel<N>;
+  smem_attr(k, smem);
+  RT_LAUNCH(c, k, grid, kThreads, smem, tm, p);
+}
+
+// The MN-major-A route for L == 1 (sketch_tc_mna_kernel).  Returns false outside its envelope.
+bool sketch_tc_mna(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t k0, uint64_t seed,
+                   int64_t col_offset, double *Y, double *normsq, uint32_t *colmax) {
+  const int N = ell <= 32 ? 32 : 64;
+  const int NT = (int)((v.I + 127) / 128);
+  if (NT * N > 512 || NT > kMnaJ || (v.I % 4) != 0 || (((uintptr_t)X) & 15) != 0) return false;
+  const int64_t C = v.L * v.R;
+  if (C > (int64_t)INT32_MAX - 64) return false;
+  SketchTcParams p{};
+  p.I = v.I;
+  p.C = C;
+  p.NT = NT;
+  p.nbox = (int)((v.I + 31) / 32);
+  const size_t abytes = (size_t)NT * 4096, obytes = (size_t)N * kBK * 4;
+  const size_t budget = 220 * 1024;
+  const size_t fixed = 1024 + 2 * kNSG * obytes + 512;
+  if (fixed + 2 * 2 * abytes > budget) return false;
+  p.NSS = (int)std::min<size_t>(4, (budget - fixed) / (2 * abytes));
+  const size_t smem = fixed + (size_t)p.NSS * 2 * abytes;
+  const int64_t nchunks = (C + kBK - 1) / kBK;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(c.num_sms, nchunks / 4));
+  p.cps = ((nchunks + grid - 1) / grid) * kBK;
+  const int g = (int)((C + p.cps - 1) / p.cps);
+  p.ell = ell;
+  p.k0 = k0;
+  p.seed = seed;
+  p.mode = mode;
+  p.col_offset = col_offset;
+  DevBuf<double> part(c, (size_t)g * ell * v.I);
+  DevBuf<double> npart;
+  if (normsq) npart.alloc(c, g);
+  p.partial = part.p;
+  p.norm_partial = normsq ? npart.p : nullptr;
+  p.colmax = colmax;
+  CUtensorMap tm;
+  CUresult r;
+  // p.L is reused as the map's rank: 3 when I % 32 == 0 and nbox <= 256 (dims: 32 rows i % 32,
+  // columns c, row blocks i / 32 at a 128-byte stride, one box = a whole stage), else 2
+  if (v.I % 32 == 0 && p.nbox <= 256) {
+    p.L = 3;
+    cuuint64_t dims[3] = {32, (cuuint64_t)C, (cuuint64_t)p.nbox};
+    cuuint64_t strides[2] = {(cuuint64_t)v.I * 4, 128};
+    cuuint32_t box[3] = {32, kBK, (cuuint32_t)p.nbox};
+    cuuint32_t es[3] = {1, 1, 1};
+    r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)X, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    p.L = 2;
+    cuuint64_t dims[2] = {(cuuint64_t)v.I, (cuuint64_t)C};
+    cuuint64_t strides[1] = {(cuuint64_t)v.I * 4};
+    cuuint32_t box[2] = {32, kBK};
+    cuuint32_t es[2] = {1, 1};
+    r = encode_fn()(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)X, dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (r != CUDA_SUCCESS) throw Error(RTUCKER_ECUDA, "cuTensorMapEncodeTiled failed for the MN-major sketch operand");
+  if (N == 32) launch_mna<32>(c, tm, p, g, smem);
+  else launch_mna<64>(c, tm, p, g, smem);
+  const int64_t n = v.I * ell;
+  RT_LAUNCH(c, reduce_partials_kernel, (int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, part.p, g, n, Y);
+  if (normsq) sum_vec(c, npart.p, g, normsq);
+  return true;
+}
+
 template <int N, bool KM>
 void launch(Ctx &c, const CUtensorMap &tm, SketchTcParams &p, int grid, size_t smem) {
   auto k = sketch_tc_mn_kernel<N, KM>;
@@ -791,6 +1126,10 @@ bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t
   const bool km = v.L > 1;  // K-major variant: l contiguous (5-D TMA box, no transposition)
   if (!km && (v.I % 4) != 0) return false;
   if (km && ((v.L % 8) != 0 || (v.I % 8) != 0 || v.I / 8 > 256)) return false;
+  // L == 1: X tiles straight into the MN-major A operand (RTUCKER_SKETCH_KMAJOR in experiments
+  // builds selects the transposing K-major kernel below)
+  static const bool kmajor = RT_EXP_GETENV("RTUCKER_SKETCH_KMAJOR") != nullptr;
+  if (!km && !kmajor && sketch_tc_mna(c, X, v, mode, ell, k0, seed, col_offset, Y, normsq, colmax)) return true;
 #ifdef RTUCKER_EXPERIMENTS
   static const bool ta = RT_EXP_GETENV("RTUCKER_SKETCH_TA") != nullptr;  // TMEM-A variant (experimental)
   if (!km && ta && (((uintptr_t)X) & 15) == 0 && v.I <= 2048 && v.L * v.R <= (int64_t)INT32_MAX - 64)

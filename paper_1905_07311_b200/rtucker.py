@@ -258,12 +258,14 @@ class Context:
 
     device: CUDA ordinal; stream: a torch.cuda.Stream (default: torch's current stream);
     group: optional torch.distributed process group for the multi-rank (NCCL) path;
-    allocator: "torch" (default) routes the library's device workspace and results through
-    torch's caching allocator (rtucker_alloc_fn hooks), "library" uses the library's own
-    stream-ordered pool."""
+    allocator: "library" (default) uses the library's own stream-ordered pool; "torch" routes
+    the library's device workspace and results through torch's caching allocator
+    (rtucker_alloc_fn hooks: memory shared with torch, at ~50 us of host time per allocation
+    for the Python callback -- 5.6 ms/step of host enqueue on eager C4 calls against 0.25 ms
+    with the pool)."""
 
     def __init__(self, device: int = 0, stream=None, group=None, rank: int | None = None,
-                 world: int | None = None, nccl_id: bytes | None = None, allocator: str = "torch"):
+                 world: int | None = None, nccl_id: bytes | None = None, allocator: str = "library"):
         self.lib = load_library()
         torch = _torch()
         if stream is None and torch.cuda.is_available():
