@@ -121,7 +121,10 @@ __global__ void __launch_bounds__(256) gemm_f64_big_kernel(const double *__restr
                                                            const double *__restrict__ B, int64_t ldb, int64_t sB,
                                                            double *__restrict__ C, int64_t ldc, int64_t sC, int64_t m,
                                                            int64_t n, int64_t k, double beta, double alpha,
-                                                           int64_t gL = 1, int64_t gKm = 1, int64_t kc = 0) {
+                                                           int64_t gL = 1, int64_t gKm = 1, int64_t kc = 0,
+                                                           int upper = 0) {
+  // upper (Grams): tiles entirely below the diagonal (every row > every column) are not computed
+  if (upper && (int64_t)blockIdx.x * kBm > (int64_t)blockIdx.y * kBn + kBn - 1) return;
   extern __shared__ __align__(16) double gsm[];
   constexpr int kAst = TA ? kBm * kPadK : kBk * kPadM;  // doubles per A stage
   constexpr int kBst = TB ? kBk * kPadN : kBn * kPadK;  // doubles per B stage
@@ -298,16 +301,13 @@ __global__ void __launch_bounds__(256) gram_gather_kernel(const double *__restri
 
 __global__ void gram_reduce_full_kernel(const double *__restrict__ part, int nsplit, int64_t K,
                                         double *__restrict__ C) {
-  // fixed-order sum of the split partials; the two triangles are averaged so C is exactly symmetric
+  // fixed-order sum of the split partials of the upper triangle (the GEMM computed only the tiles
+  // touching it), mirrored: C is exactly symmetric
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < K * K; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e % K, j = e / K;
     if (i > j) continue;
-    double s1 = 0.0, s2 = 0.0;
-    for (int q = 0; q < nsplit; ++q) {
-      s1 += part[(int64_t)q * K * K + e];
-      s2 += part[(int64_t)q * K * K + j + K * i];
-    }
-    const double s = 0.5 * (s1 + s2);
+    double s = 0.0;
+    for (int q = 0; q < nsplit; ++q) s += part[(int64_t)q * K * K + e];
     C[i + K * j] = s;
     C[j + K * i] = s;
   }
@@ -423,9 +423,11 @@ void gram_f64(Ctx &c, const double *B, int64_t L, int64_t K, int64_t R, double *
               nsplit, K, C);
     return;
   }
-  // large: the pipelined kernel on the full K x K (both triangles), K chunks over ~2 waves,
-  // partials summed in a fixed order
-  const int64_t tiles = ((K + kBm - 1) / kBm) * ((K + kBn - 1) / kBn);
+  // large: the pipelined kernel on the tiles touching the upper triangle (58 % of them at K = 760),
+  // K chunks over ~2 waves, partials summed in a fixed order and mirrored
+  int64_t tiles = 0;  // tiles touching the upper triangle
+  for (int64_t by = 0; by < (K + kBn - 1) / kBn; ++by)
+    for (int64_t bx = 0; bx < (K + kBm - 1) / kBm; ++bx) tiles += bx * kBm <= by * kBn + kBn - 1;
   int nsplit = (int)std::max<int64_t>(1, std::min<int64_t>((2 * c.num_sms + tiles - 1) / tiles, T / 2048));
   const int64_t chunk = ((T + nsplit - 1) / nsplit + kBk - 1) / kBk * kBk;
   nsplit = (int)((T + chunk - 1) / chunk);
@@ -437,18 +439,18 @@ void gram_f64(Ctx &c, const double *B, int64_t L, int64_t K, int64_t R, double *
     if (nfull > 0) {
       const dim3 gf(g.x, g.y, (unsigned)nfull);
       RT_LAUNCH(c, (gemm_f64_big_kernel<false, true, false>), gf, 256, kBigSmem(false, true), B, K, chunk * K, B, K,
-                chunk * K, part.p, K, K * K, K, K, chunk, 0.0, 1.0, (int64_t)1, (int64_t)1, (int64_t)0);
+                chunk * K, part.p, K, K * K, K, K, chunk, 0.0, 1.0, (int64_t)1, (int64_t)1, (int64_t)0, 1);
     }
     if (tl > 0) {
       const dim3 g1(g.x, g.y, 1);
       RT_LAUNCH(c, (gemm_f64_big_kernel<false, true, false>), g1, 256, kBigSmem(false, true), B + nfull * chunk * K, K,
                 0, B + nfull * chunk * K, K, 0, part.p + nfull * K * K, K, 0, K, K, tl, 0.0, 1.0, (int64_t)1,
-                (int64_t)1, (int64_t)0);
+                (int64_t)1, (int64_t)0, 1);
     }
   } else {
     smem_attr(gemm_f64_big_kernel<true, false, true>, kBigSmem(true, false));
     RT_LAUNCH(c, (gemm_f64_big_kernel<true, false, true>), g, 256, kBigSmem(true, false), B, 0, 0, B, 0, 0, part.p, K,
-              K * K, K, K, T, 0.0, 1.0, L, K, chunk);
+              K * K, K, K, T, 0.0, 1.0, L, K, chunk, 1);
   }
   RT_LAUNCH(c, gram_reduce_full_kernel, std::max(1, std::min(4096, ceil_div(K * K, 256))), 256, 0, part.p, nsplit,
             K, C);
