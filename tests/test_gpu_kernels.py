@@ -144,10 +144,14 @@ def test_sym_eig(ctx, n):
 
 
 @pytest.mark.parametrize("shape,ell,k0", [((800, 800, 40), 60, 0), ((800, 300, 7), 10, 0), ((96, 1001, 3), 64, 0),
-                                          ((800, 200, 11), 5, 10), ((128, 64, 8), 33, 4)])
+                                          ((800, 200, 11), 5, 10), ((128, 64, 8), 33, 4), ((100, 300, 5), 20, 0),
+                                          ((36, 500, 2), 7, 3), ((900, 64, 3), 60, 0)])
 def test_sketch_tc_mode1(ctx, shape, ell, k0):
     """Mode-1 fp32 sketch (the tcgen05 3xTF32 path: L == 1, I % 4 == 0) against the fp64
     oracle product on the same fp32 bits, incl. ragged column counts and block offsets k0.
+    Routes: MN-major A with one 3-D TMA per stage (I % 32 == 0: 800, 96, 128), MN-major A
+    with 32-row 2-D boxes (100, 36: the last box ragged), the transposing K-major kernel
+    (I = 900: more than 7 M-tiles).
     Tolerance: fp32 accumulation in TMEM over a CTA's column range (a few hundred to a few
     thousand terms, relative error ~ sqrt(K) u32) -> 1e-5 relative."""
     rng = np.random.default_rng(sum(shape) + ell)
