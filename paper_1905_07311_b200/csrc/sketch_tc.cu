@@ -368,10 +368,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 // plane and transposed through shared memory).
 //   warp 0 TMA producer, warp 1 TMEM + MMA issuer, warps 2-5 Omega generators (as in
 //   sketch_tc_mn_kernel), warps 6-13 X workers; stage s = (x plane, lo plane), NS deep.
-constexpr int kMnaJ = 7;  // 16-byte chunks per worker thread and stage (NT <= 7: 28 KB / 4 KB)
+constexpr int kMW = 12;   // X worker warps of the MN-major kernel (its longest pipeline stage)
+constexpr int kMThreads = 32 * (2 + kGen + kMW);
+constexpr int kMnaJ = (7 * 256 + 32 * kMW - 1) / (32 * kMW);  // 16-byte chunks per worker and stage (NT <= 7)
 
 template <int N>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kMThreads, 1)
     sketch_tc_mna_kernel(const __grid_constant__ CUtensorMap tmap, const SketchTcParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t pad = (1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u;
@@ -390,7 +392,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t *oempty = oready + kNSG;
   uint64_t *done = oempty + kNSG;
   uint32_t *tslot = (uint32_t *)(done + 1);
-  double *wsum = (double *)(tslot + 2);            // [kWorkers]
+  double *wsum = (double *)(tslot + 2);            // [kMW]
 
 #ifdef RTUCKER_SK_PROF_BUILD
   long long skp[5] = {0, 0, 0, 0, 0}, skp_t = 0;
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < NS; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&sfree[s], 1);
-      tc::mbar_init(&xready[s], 32 * kWorkers);
+      tc::mbar_init(&xready[s], 32 * kMW);
     }
     for (int s = 0; s < kNSG; ++s) {
       tc::mbar_init(&oready[s], 32 * kGen);
@@ -423,10 +425,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 1) tc::tmem_alloc(tslot, tcols);
   // Omega tiles: columns n >= ell stay zero; atoms past the last TMA box (rows >= 32 nbox, only
   // ever read into D rows >= I, which are discarded) are zeroed once in both planes
-  for (int e = threadIdx.x; e < 2 * kNSG * obytes / 4; e += kThreads) ((float *)ohb)[e] = 0.f;
+  for (int e = threadIdx.x; e < 2 * kNSG * obytes / 4; e += kMThreads) ((float *)ohb)[e] = 0.f;
   {
     const int pad_f = (4 * NT - nbox) * 256;  // floats per plane past the boxes
-    for (int e = threadIdx.x; e < 2 * NS * pad_f; e += kThreads) {
+    for (int e = threadIdx.x; e < 2 * NS * pad_f; e += kMThreads) {
       const int pl = e / pad_f, f = e % pad_f;
       ((float *)(xb + (size_t)pl * abytes + (size_t)nbox * 1024))[f] = 0.f;
     }
@@ -524,7 +526,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ------------------------------------------------------------- X workers
-    const int wt = threadIdx.x - 32 * (2 + kGen);  // 0 .. 32*kWorkers-1
+    const int wt = threadIdx.x - 32 * (2 + kGen);  // 0 .. 32*kMW-1
     const int nch = nbox * 64;                     // 16-byte chunks per stage
     const int ccol = (wt & 63) >> 3;               // the stage column all of this thread's chunks hold
     double nsq = 0.0;
@@ -541,12 +543,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       float4 xv[kMnaJ];
 #pragma unroll
       for (int j = 0; j < kMnaJ; ++j) {
-        const int q = wt + 32 * kWorkers * j;
+        const int q = wt + 32 * kMW * j;
         xv[j] = q < nch ? *(const float4 *)(xs + 16 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
       for (int j = 0; j < kMnaJ; ++j) {
-        const int q = wt + 32 * kWorkers * j;
+        const int q = wt + 32 * kMW * j;
         const float4 x = xv[j];
         float4 l;
         l.x = tc::tf32_rn(x.x - __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u));
@@ -599,7 +601,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   if (p.norm_partial && threadIdx.x == 0) {
     double s = 0.0;
-    for (int w = 0; w < kWorkers; ++w) s += wsum[w];
+    for (int w = 0; w < kMW; ++w) s += wsum[w];
     p.norm_partial[blockIdx.x] = s;
   }
   if (warp == 1) {
@@ -1031,7 +1033,7 @@ template <int N>
 void launch_mna(Ctx &c, const CUtensorMap &tm, SketchTcParams &p, int grid, size_t smem) {
   auto k = sketch_tc_mna_kernel<N>;
   smem_attr(k, smem);
-  RT_LAUNCH(c, k, grid, kThreads, smem, tm, p);
+  RT_LAUNCH(c, k, grid, kMThreads, smem, tm, p);
 }
 
 // The MN-major-A route for L == 1 (sketch_tc_mna_kernel).  Returns false outside its envelope.
@@ -1039,7 +1041,7 @@ bool sketch_tc_mna(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_
                    int64_t col_offset, double *Y, double *normsq, uint32_t *colmax) {
   const int N = ell <= 32 ? 32 : 64;
   const int NT = (int)((v.I + 127) / 128);
-  if (NT * N > 512 || NT > kMnaJ || (v.I % 4) != 0 || (((uintptr_t)X) & 15) != 0) return false;
+  if (NT * N > 512 || NT > 7 || (v.I % 4) != 0 || (((uintptr_t)X) & 15) != 0) return false;
   const int64_t C = v.L * v.R;
   if (C > (int64_t)INT32_MAX - 64) return false;
   SketchTcParams p{};

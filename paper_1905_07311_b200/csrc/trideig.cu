@@ -408,6 +408,13 @@ struct TridGridWs {
 __global__ void __launch_bounds__(256) trid_eig_grid_kernel(const double *__restrict__ Ain, int n, TridGridWs ws,
                                                           double *__restrict__ scale_out) {
   cg::grid_group grid = cg::this_grid();
+#ifdef RTUCKER_TRID_PROF_BUILD
+  long long tg_[4] = {0, 0, 0, 0};
+  const long long tg0_ = clock64();
+#define TGP(i) if (blockIdx.x == 0 && threadIdx.x == 0) tg_[i] = clock64() - tg0_
+#else
+#define TGP(i)
+#endif
   const int lane = threadIdx.x & 31;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, gthr = (int64_t)gridDim.x * blockDim.x;
   const int gw = (int)(gtid >> 5), nw = (int)(gthr >> 5);
@@ -440,6 +447,7 @@ __global__ void __launch_bounds__(256) trid_eig_grid_kernel(const double *__rest
   if (gtid == 0) *scale_out = scale;
   for (int64_t e0 = gtid; e0 < (int64_t)n * n; e0 += gthr) A[e0] *= iscale;
   grid.sync();
+  TGP(0);
   // ---- A. tridiagonalisation (x = row k of A, j >= k+1; A stays symmetric)
   for (int k = 0; k + 2 < n; ++k) {
     const int c0 = k + 1;
@@ -558,6 +566,7 @@ __global__ void __launch_bounds__(256) trid_eig_grid_kernel(const double *__rest
   }
   const double tnorm = fmax(fabs(glo), fabs(ghi));
   const double pm = 1e-280;
+  TGP(1);
   // ---- B. eigenvalues: one warp per eigenvalue, 33-section
   for (int q = gw; q < n; q += nw) {
     double lo = glo - 2.2e-16 * tnorm - 1e-300, hi = ghi + 2.2e-16 * tnorm + 1e-300;
@@ -575,6 +584,7 @@ __global__ void __launch_bounds__(256) trid_eig_grid_kernel(const double *__rest
     if (lane == 0) ws.lam[q] = 0.5 * (lo + hi);
   }
   grid.sync();
+  TGP(2);
   // ---- C. eigenvectors of T (twisted factorisations), eigenvector q in Z + q n
   for (int64_t t = gtid; t < 2 * (int64_t)n; t += gthr) {
     const int q = (int)(t >> 1);
@@ -689,6 +699,11 @@ __global__ void __launch_bounds__(256) trid_eig_grid_kernel(const double *__rest
       }
     }
   }
+#ifdef RTUCKER_TRID_PROF_BUILD
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    printf("[trid prof] n %d grid %d: load %lld tridiag %lld eigvals %lld eigvecs %lld cycles\n", n, (int)gridDim.x, tg_[0], tg_[1] - tg_[0], tg_[2] - tg_[1], clock64() - tg0_ - tg_[2]);
+#endif
+#undef TGP
 }
 
 // S <- 1.5 I - 0.5 S (n x n)
@@ -741,7 +756,12 @@ void trid_eig_large(Ctx &c, const double *A, int n, double *w, double *V) {
   ws.twist = tw.p;
   int per_sm = 0;
   RT_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, trid_eig_grid_kernel, 256, 0));
-  const int grid = std::max(1, std::min(c.num_sms * std::max(per_sm, 1), 4096));
+  // one warp per matrix row (ceil(n / 8) CTAs of 8 warps): the two grid barriers per Householder
+  // step dominate phase A and cost more with more CTAs; at n = 760 phase A measured 26 ms with
+  // 96 CTAs, 30 ms with 148, 38 ms with 48 and 53 ms with all 592 resident CTAs
+  static const int gover = RT_EXP_GETENV("RTUCKER_TRID_GRID") ? atoi(RT_EXP_GETENV("RTUCKER_TRID_GRID")) : 0;
+  const int gmax = std::max(1, std::min(c.num_sms * std::max(per_sm, 1), 4096));
+  const int grid = gover > 0 ? std::min(gover, gmax) : std::min(gmax, (n + 7) / 8);
   void *args[] = {(void *)&A, (void *)&n, (void *)&ws, (void *)&scale};
   RT_CUDA(cudaLaunchCooperativeKernel((const void *)trid_eig_grid_kernel, dim3(grid), dim3(256), args, 0, c.stream));
   c.launches++;
