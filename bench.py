@@ -453,9 +453,9 @@ def main():
         t_k = sk_ms / sk_n
         algo = BYTES_X // world  # X read once (Omega never touches HBM; Y partials stay in L2)
         ach = algo / (t_k * 1e-3) / 1e9
-        kernels.append({"kernel": "sketch_tc_mn_kernel (mode-1 sketch, tcgen05 3xTF32)", "bound": "hbm",
+        kernels.append({"kernel": "sketch_tc_mna_kernel (mode-1 sketch, tcgen05 3xTF32, MN-major A by TMA)", "bound": "hbm",
                         "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
-                        "traffic": traffic.get("sketch_tc_mn_kernel"), "ms": t_k,
+                        "traffic": traffic.get("sketch_tc_mna_kernel"), "ms": t_k,
                         "algorithmic": f"{algo} B per launch (800^3 fp32 read once)"})
     bp_ms, bp_n = phases.get(("bpass", 0), (0.0, 0))
     if bp_n and args.algo == "sthosvd":
@@ -480,10 +480,11 @@ def main():
                         "int8_peak_source": i8_src})
     eig = [phases[("eig", m)] for m in range(3) if ("eig", m) in phases]
     if eig and args.algo == "sthosvd":
-        # the three 60x60 eigensolves: one CTA each, bound by the dependent latency chain of the
-        # Jacobi rounds, no bandwidth or tensor roofline; listed for the step share
+        # the three 60x60 eigensolves (eig phase: the mixed-precision solver + the factor epilogue):
+        # one CTA each, bound by the dependent latency chain of the Cholesky steps and Jacobi
+        # rounds, no bandwidth or tensor roofline; listed for the step share
         t_e = sum(v[0] / max(v[1], 1) for v in eig)
-        kernels.append({"kernel": "gram_eig_kernel x3 (pivoted Cholesky + one-sided Jacobi, one CTA)",
+        kernels.append({"kernel": "gram_eig_mixed_kernel x3 (pivoted Cholesky + fp32 Jacobi + fp64 refinement, one CTA)",
                         "bound": "latency", "ms": t_e / len(eig), "ms_per_step": t_e,
                         "share_of_step": t_e / ms_local, "launches_per_step": len(eig)})
     dom = max((k for k in kernels if k["bound"] != "latency"), key=lambda k: k["ms"]) if kernels else None

@@ -13,5 +13,5 @@ CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline --no-graph 
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/p_launches.csv $CMD > gpurun_out/ncu_list.log 2>&1; echo list_exit=$?
 timeout 300 python scripts/run_c4_once.py 1 > gpurun_out/plain2.log 2>&1 && \
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"sketch_tc_mn|bpass_ozaki|ttm_dmma|gram_eig|cholqr2|sketch_dfma|factor_epilogue" -c 14 -o gpurun_out/p_c4_full -f python scripts/run_c4_once.py 1 > gpurun_out/ncu_full.log 2>&1; echo full_exit=$?
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"sketch_tc_mn|bpass_ozaki|ttm_dmma|gram_eig|cholqr2|sketch_dfma|factor_" -c 16 -o gpurun_out/p_c4_full -f python scripts/run_c4_once.py 1 > gpurun_out/ncu_full.log 2>&1; echo full_exit=$?
 for f in default sparse adaptive reference; do tail -c 300 gpurun_out/p_$f.json; echo; done
