@@ -92,6 +92,44 @@ __device__ __forceinline__ void slice5(float r, uint32_t (&q)[kOS]) {
   }
 }
 
+// Two values at a time on the paired fp32 pipe (FFMA2 / FADD2, sm_100): the same exact steps as
+// slice5, carried on the NEGATED residual r' = -r so that no operand needs a sign flip:
+//   u = fma(r', -k, M) = fl(r k + M),  t = u + (-M) = u - M,  r' <- fma(r', k, t) = -(r k - t).
+// Bit-identical slices; half the FP instructions of two slice5 calls (the slicers bound the
+// B-pass: DESIGN §7).
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  return (uint64_t)__float_as_uint(lo) | ((uint64_t)__float_as_uint(hi) << 32);
+}
+// slices of x0 * sc and x1 * sc into q0, q1 (raw bits of u, as slice5)
+__device__ __forceinline__ void slice5x2(float x0, float x1, float sc, uint32_t (&q0)[kOS], uint32_t (&q1)[kOS]) {
+  const uint64_t M2 = f2_pack(12582912.0f, 12582912.0f), nM2 = f2_pack(-12582912.0f, -12582912.0f);
+  uint64_t r = f2_mul(f2_pack(x0, x1), f2_pack(-sc, -sc));  // r' = -x sc (exact: sc is a power of 2)
+#pragma unroll
+  for (int s = 0; s < kOS; ++s) {
+    const float k = s == 0 ? 64.0f : 128.0f;
+    const uint64_t u = f2_fma(r, f2_pack(-k, -k), M2);
+    const uint64_t t = f2_add(u, nM2);
+    r = f2_fma(r, f2_pack(k, k), t);
+    q0[s] = (uint32_t)u;
+    q1[s] = (uint32_t)(u >> 32);
+  }
+}
+
 // m_p = max_i |X(i, p)| as fp32 bits (the scale exponent is taken from it), one warp per column.
 // The R-STHOSVD path gets these from the mode-1 sketch instead (sketch_tc.cu, colmax).
 __global__ void colmax_kernel(const float *__restrict__ X, int64_t I, int64_t P, uint32_t *__restrict__ cm) {
@@ -398,19 +436,20 @@ __global__ void __launch_bounds__(kOThreads, 1)
           v = *reinterpret_cast<const float4 *>(srow + ((j ^ (row & 7)) << 4));
         }
         uint32_t a[kOS], b[kOS], c[kOS], d[kOS];
-        slice5(v.x * sc, a);
-        slice5(v.y * sc, b);
-        slice5(v.z * sc, c);
-        slice5(v.w * sc, d);
+        slice5x2(v.x, v.y, sc, a, b);
+        slice5x2(v.z, v.w, sc, c, d);
 #pragma unroll
         for (int t = 0; t < kOS; ++t)
           w[t][cq] = __byte_perm(__byte_perm(a[t], b[t], 0x0040), __byte_perm(c[t], d[t], 0x0040), 0x5410);
       }
-      tc::mbar_arrive(&sfree[s]);  // staging slot may be refilled
       const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + kOAcol + 40 * x + 4 * half;
 #pragma unroll
       for (int t = 0; t < kOS; ++t) tmem_st4(ta + 8 * t, w[t][0], w[t][1], w[t][2], w[t][3]);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      // the staging slot is released only after every slice has been formed and stored: with
+      // the paired-pipe slicing, ptxas issued this arrive between the staging loads and their
+      // first use, and the refill raced with them (nondeterministic B, caught by rerunning C4)
+      tc::mbar_arrive(&sfree[s]);  // staging slot may be refilled
       tc::tc_fence_before();
       tc::mbar_arrive(&xready[x]);
       if (++ch == nchunk) { ch = 0; ++tk; }

@@ -292,6 +292,21 @@ def test_c4_full_size_rsthosvd(ctx):
 
 
 @pytest.mark.slow
+def test_c4_reruns_bit_identical(ctx):
+    """Determinism at full C4 size (every pipeline runs many stages per CTA there): three
+    R-STHOSVD calls on the same input give bit-identical cores and factors.  (A staging-slot
+    release that ptxas scheduled before the slicers had consumed their loads once made the
+    Ozaki B-pass race with the next TMA refill: e moved in the 5th digit between reruns.)"""
+    xd = odeco(800, seed=4, dtype=np.float32, device="cuda")
+    from paper_1905_07311_b200.rtucker import RESULT_HOST
+    runs = [ctx.sthosvd(xd, (800, 800, 800), (50, 50, 50), 10, 0, (0, 1, 2), RESULT_HOST).numpy() for _ in range(3)]
+    for r in runs[1:]:
+        assert np.array_equal(r.core, runs[0].core)
+        for a, b in zip(r.factors, runs[0].factors):
+            assert np.array_equal(a, b)
+
+
+@pytest.mark.slow
 def test_c4_full_size_rhosvd(ctx):
     """BASELINE configs[3] R-HOSVD at full size (800^3 fp32, r=50, p=10) in bench.py's
     launch configuration (--algo hosvd) against the full oracle run on the same bits:
