@@ -145,6 +145,18 @@ __global__ void __launch_bounds__(256) gemm_f64_big_kernel(const double *__restr
   auto load_stage = [&](int kt, int st) {
     const int64_t k0 = kbeg + (int64_t)kt * kBk;
     double *as = As + st * kAst, *bs = Bs + st * kBst;
+    // GA: the K index t = l + gL r of this tile, split once per stage (per-element 64-bit
+    // divisions were subroutine calls: 12 per thread and stage, the gather Gram ran at 12 TF/s)
+    int64_t r0 = 0, l0 = 0;
+    if (GA) {
+      r0 = k0 / gL;
+      l0 = k0 - r0 * gL;
+    }
+    auto gsplit = [&](int kk, int64_t &l, int64_t &r) {
+      l = l0 + kk;
+      r = r0;
+      while (l >= gL) { l -= gL; ++r; }
+    };
     // A: 64 x 16 = 1024 elements, 4 per thread
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -155,7 +167,11 @@ __global__ void __launch_bounds__(256) gemm_f64_big_kernel(const double *__restr
       const bool ok = gi < m && gk < k;
       const double *src = A;
       if (ok) {
-        if (GA) src = A + (gk % gL) + gL * gi + gL * gKm * (gk / gL);
+        if (GA) {
+          int64_t l, r;
+          gsplit(kk, l, r);
+          src = A + l + gL * gi + gL * gKm * r;
+        }
         else src = TA ? A + gk + lda * gi : A + gi + lda * gk;
       }
       double *dst = TA ? as + mm * kPadK + kk : as + kk * kPadM + mm;
@@ -172,7 +188,11 @@ __global__ void __launch_bounds__(256) gemm_f64_big_kernel(const double *__restr
       const bool ok = gj < n && gk < k;
       const double *src = B;
       if (ok) {
-        if (GA) src = B + (gk % gL) + gL * gj + gL * gKm * (gk / gL);
+        if (GA) {
+          int64_t l, r;
+          gsplit(kk, l, r);
+          src = B + l + gL * gj + gL * gKm * r;
+        }
         else src = TB ? B + gj + ldb * gk : B + gk + ldb * gj;
       }
       double *dst = TB ? bs + kk * kPadN + nn : bs + nn * kPadK + kk;

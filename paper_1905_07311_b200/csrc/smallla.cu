@@ -1871,7 +1871,10 @@ __global__ void __launch_bounds__(kBQT, 1) cholqr2_blk_kernel(const double *__re
             if (lane == 0) sbad = 1;
             piv = 1.0;
           }
-          const double rinv = rsqrt(piv);
+          double rinv;  // piv^{-1/2}: approximate rsqrt + two Newton steps (no slow-path subroutine)
+          asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rinv) : "d"(piv));
+          rinv = rinv * fma(-0.5 * piv * rinv, rinv, 1.5);
+          rinv = rinv * fma(-0.5 * piv * rinv, rinv, 1.5);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
             if (bi[h] == k && bj[h] > k) bv[h] *= rinv;
@@ -1903,7 +1906,11 @@ __global__ void __launch_bounds__(kBQT, 1) cholqr2_blk_kernel(const double *__re
             double s2 = (i == j) ? 1.0 : 0.0;
 #pragma unroll
             for (int t = i + 1; t < 8; ++t) s2 = fma(-Rb[i * ldG + t], x[t], s2);
-            x[i] = (i <= j) ? s2 / Rb[i * ldG + i] : 0.0;
+            const double di = Rb[i * ldG + i];
+            double rd = rcp_approx_f64(di);  // 1 / R_ii: approximate reciprocal + two Newton steps
+            rd = rd * fma(-di, rd, 2.0);
+            rd = rd * fma(-di, rd, 2.0);
+            x[i] = (i <= j) ? s2 * rd : 0.0;
           }
 #pragma unroll
           for (int i = 0; i < 8; ++i) Dk[i * 8 + j] = x[i];

@@ -499,14 +499,20 @@ __global__ void __launch_bounds__(256) trid_eig_grid_kernel(const double *__rest
       ws.pxy[blockIdx.x] = t;
     }
     grid.sync();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {  // the CTA partials by one warp: lane-strided sums, fixed-order tree
       double sxx = 0.0, sxy = 0.0;
-      for (int q = 0; q < (int)gridDim.x; ++q) {
+      for (int q = lane; q < (int)gridDim.x; q += 32) {
         sxx += ws.pxx[q];
         sxy += ws.pxy[q];
       }
-      bc[0] = sxx;
-      bc[1] = sxy;
+      for (int o = 16; o; o >>= 1) {
+        sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
+        sxy += __shfl_xor_sync(0xffffffffu, sxy, o);
+      }
+      if (lane == 0) {
+        bc[0] = sxx;
+        bc[1] = sxy;
+      }
     }
     __syncthreads();
     const double sxx = bc[0], sxy = bc[1];
