@@ -114,6 +114,9 @@ def int8_peak_tops():
     return sms * 8186 * 2 * mhz * 1e6 / 1e12, f"derived: {sms} SMs x 8186 int8 MAC/clk (measured) x 2 x {mhz:.0f} MHz"
 
 
+RNG_PEAK_GNORMALS = 500.0  # fp32 Philox4x32-10 + Box-Muller normals per second / 1e9, generator alone (rng_rate.cu)
+
+
 def load_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
     captures (profiles/traffic.json, written by scripts/ncu_traffic.py); {} if absent."""
@@ -266,9 +269,13 @@ def bench_sparse(args):
     # trims) inside the timed region; torch's allocator stays the binding's default for users
     ctx = Context(local, stream=stream, group=dist.group.WORLD if world > 1 else None, allocator="library")
     step = lambda: ctx.sparse_sthosvd(it, vt, dims, (10, 10, 10, 10), 5, SEED, None, 2.0)
+    clocks = Clocks(local)  # started before the warm-up (see the dense bench)
+    clocks.start()
+    time.sleep(1.0)
     for _ in range(args.warmup):
         step().free()
     torch.cuda.synchronize()
+    clocks.mark()
     ctx.set_profiling(True)
     ctx.phase_times(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -284,23 +291,86 @@ def bench_sparse(args):
         r.free()
     e1.record(stream)
     torch.cuda.synchronize()
+    launches_per_step = (ctx.launches - l0) // args.steps
+    clk = clocks.stop()
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
+    ctx.set_profiling(False)
+    # ---- end-to-end through the public API with HOST buffers: the COO (int32 indices, fp32
+    # values) copied from pinned memory by the library every step, the result read back
+    e2e = None
+    if not args.no_e2e:
+        ih = torch.empty(it.shape, dtype=it.dtype, pin_memory=True)
+        vh = torch.empty(vt.shape, dtype=vt.dtype, pin_memory=True)
+        ih.copy_(it)
+        vh.copy_(vt)
+        from paper_1905_07311_b200.rtucker import RESULT_HOST
+        hstep = lambda: ctx.sparse_sthosvd(ih, vh, dims, (10, 10, 10, 10), 5, SEED, None, 2.0, RESULT_HOST)
+        hstep().free()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d2h = 0
+        for _ in range(args.steps):
+            r = hstep()
+            sr = r.s
+            d2h = int(sr.core_nnz) * (4 * 4 + 8) + sum(int(sr.dims[k]) * int(sr.ranks[k]) * 8 + int(sr.ranks[k]) * 8
+                                                       for k in range(4))
+            r.free()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / args.steps
+        if world > 1:
+            t = torch.tensor([dt], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": idx.shape[1] / dt / 1e9, "unit": "Gnnz/s",
+               "h2d_bytes_per_step": int(ih.numel() * ih.element_size() + vh.numel() * vh.element_size()),
+               "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3}
     if rank != 0:
         dist.destroy_process_group()
         return
     phases = {f"{k[0]}{k[1] + 1}": round(v[0] / max(v[1], 1), 4) for k, v in sorted(ctx.phase_times().items())}
     nnz = idx.shape[1]
+    # ---- roofline of the dominant phase: the first mode's COO sketch (bucket sort + bucket_sketch
+    # + fixed-point readout), bound by generating Omega: every nonzero draws ceil(ell/4) Philox
+    # blocks of 4 normals (ell = r + p = 15: 16 normals), against the generator-only rate measured
+    # on this B200 (scripts/dbg/rng_rate.cu: 5.0e11 fp32 normals/s)
+    ell = 15
+    normals = nnz * 4 * ((ell + 3) // 4)
+    t_s = phases.get("sketch1")
+    roofline = None
+    if t_s:
+        ach = normals / (t_s * 1e-3) / 1e9
+        roofline = {"bound": "alu", "achieved": ach, "peak": RNG_PEAK_GNORMALS, "unit": "Gnormal/s",
+                    "frac": ach / RNG_PEAK_GNORMALS, "traffic": None, "kernel_ms": t_s,
+                    "kernel": "mode-3 COO sketch phase (bucket_hist/scatter + bucket_sketch: Philox4x32-10 + "
+                              "Box-Muller per nonzero, fixed-point row sums + readout)",
+                    "algorithmic": f"{normals} normals per launch ({nnz} nonzeros x 16)",
+                    "peak_source": "measured generator-only rate on this B200 (scripts/dbg/rng_rate.cu)"}
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle as O
+        ns = 8_000_000
+        t0 = time.perf_counter()
+        O.sp_sthosvd(idx[:, :ns], vals[:ns], dims, (10, 10, 10, 10), 5, SEED, None, 2.0)
+        dtc = time.perf_counter() - t0
+        cpu = {"value": ns / dtc / 1e9, "unit": "Gnnz/s", "cores": os.cpu_count(), "kind": "oracle",
+               "sample": f"oracle sp_sthosvd on the first {ns} of the {nnz} nonzeros (same dims, ranks, p, "
+                         "seed, eta); reported as nonzeros/s of the sample (the per-mode QR / sRRQR costs "
+                         "do not shrink with the sample, so the full-size rate is lower)",
+               "seconds": dtc, "cpu_model": cpu_model(), "threads": "numpy/OpenBLAS default (all host cores)"}
     line = {"metric": "SP-STHOSVD Gnnz/s (C5 8000x8000x200000x1200, 50M Zipf(1.1) draws, r=10, p=5)",
             "value": nnz / (ms * 1e-3) / 1e9, "unit": "Gnnz/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32 values, fixed-point (int64) sketch sums", "data": "synthetic",
             "config": {"workload": "C5 sparse_zipf data seed 5, SP-STHOSVD rho=auto [3,1,2,4], eta=2",
                        "nnz": nnz, "nnz_chain": hist},
-            "phase_ms": phases, "gpu_launches": (ctx.launches - l0) // args.steps}
+            "phase_ms": phases, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step, "clocks": clk}
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
