@@ -58,7 +58,7 @@ struct SketchTcParams {
   uint64_t seed;
   int mode;
   int64_t col_offset;    // global unfolding-column offset of this shard
-  double *partial;       // [grid][ell][I]
+  float *partial;        // [grid][ell][I]: the CTA's fp32 TMEM sums (exact copies; summed in fp64)
   double *norm_partial;  // [grid] or null
   uint32_t *colmax;      // [C] fp32 bits of max_i |X(i, c)| (atomic max), or null
 };
@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc::mbar_wait(done, 0);
       tc::tc_fence_after();
     }
-    double *dst = p.partial + (int64_t)blockIdx.x * p.ell * p.I;
+    float *dst = p.partial + (int64_t)blockIdx.x * p.ell * p.I;
     if (half * 32 < N) {
       for (int mt = 0; mt < NT; ++mt) {
         uint32_t rr[32];
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int k = half * 32 + j;
-            if (k < p.ell) dst[(int64_t)k * p.I + i] = nst > 0 ? (double)__uint_as_float(rr[j]) : 0.0;
+            if (k < p.ell) dst[(int64_t)k * p.I + i] = nst > 0 ? __uint_as_float(rr[j]) : 0.f;
           }
         }
       }
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(kMThreads, 1)
       tc::mbar_wait(done, 0);
       tc::tc_fence_after();
     }
-    double *dst = p.partial + (int64_t)blockIdx.x * p.ell * p.I;
+    float *dst = p.partial + (int64_t)blockIdx.x * p.ell * p.I;
     if (half * 32 < N) {
       for (int mt = 0; mt < NT; ++mt) {
         uint32_t rr[32];
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(kMThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int k = half * 32 + j;
-            if (k < p.ell) dst[(int64_t)k * p.I + i] = nst > 0 ? (double)__uint_as_float(rr[j]) : 0.0;
+            if (k < p.ell) dst[(int64_t)k * p.I + i] = nst > 0 ? __uint_as_float(rr[j]) : 0.f;
           }
         }
       }
@@ -904,7 +904,7 @@ __global__ void __launch_bounds__(kTaThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int k = h * 32 + j;
-            if (k < p.ell) dst[(int64_t)k * p.I + i] = nst > 0 ? (double)__uint_as_float(rr[j]) : 0.0;
+            if (k < p.ell) dst[(int64_t)k * p.I + i] = nst > 0 ? __uint_as_float(rr[j]) : 0.f;
           }
         }
       }
@@ -939,6 +939,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     fn = (PFN_cuTensorMapEncodeTiled_v12000)ptr;
   }
   return fn;
+}
+
+// Y = sum over the CTAs of their fp32 partials, in fp64 and in CTA order (deterministic; the fp32
+// partials are the TMEM values themselves, so this is the same sum as over fp64 copies at half
+// the bytes)
+__global__ void reduce_partials_f32_kernel(const float *__restrict__ partial, int nsplit, int64_t n,
+                                           double *__restrict__ Y) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < nsplit; ++k) s += (double)partial[(int64_t)k * n + e];
+    Y[e] = s;
+  }
 }
 
 __global__ void reduce_partials_kernel(const double *__restrict__ partial, int nsplit, int64_t n,
@@ -1064,7 +1076,7 @@ bool sketch_tc_mna(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_
   p.seed = seed;
   p.mode = mode;
   p.col_offset = col_offset;
-  DevBuf<double> part(c, (size_t)g * ell * v.I);
+  DevBuf<float> part(c, (size_t)g * ell * v.I);
   DevBuf<double> npart;
   if (normsq) npart.alloc(c, g);
   p.partial = part.p;
@@ -1097,7 +1109,7 @@ bool sketch_tc_mna(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_
   if (N == 32) launch_mna<32>(c, tm, p, g, smem);
   else launch_mna<64>(c, tm, p, g, smem);
   const int64_t n = v.I * ell;
-  RT_LAUNCH(c, reduce_partials_kernel, (int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, part.p, g, n, Y);
+  RT_LAUNCH(c, reduce_partials_f32_kernel, (int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, part.p, g, n, Y);
   if (normsq) sum_vec(c, npart.p, g, normsq);
   return true;
 }
@@ -1166,7 +1178,7 @@ bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t
   p.seed = seed;
   p.mode = mode;
   p.col_offset = col_offset;
-  DevBuf<double> part(c, (size_t)g * ell * v.I);
+  DevBuf<float> part(c, (size_t)g * ell * v.I);
   DevBuf<double> npart;
   if (normsq) npart.alloc(c, g);
   p.partial = part.p;
@@ -1202,7 +1214,7 @@ bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t
     else launch<64, false>(c, tm, p, g, smem);
   }
   const int64_t n = v.I * ell;
-  RT_LAUNCH(c, reduce_partials_kernel, (int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, part.p, g, n, Y);
+  RT_LAUNCH(c, reduce_partials_f32_kernel, (int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, part.p, g, n, Y);
   if (normsq) sum_vec(c, npart.p, g, normsq);
   return true;
 }
