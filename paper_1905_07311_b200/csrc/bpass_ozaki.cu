@@ -578,12 +578,17 @@ __global__ void __launch_bounds__(kOThreads, 1)
 }
 
 __global__ void oz_gram_reduce_kernel(const double *__restrict__ part, int nblk, int J, double *__restrict__ gram) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= J * J) return;
+  // four lanes per entry: lane q sums the CTA partials b = q, q + 4, ... in order, then
+  // (q0 + q1) + (q2 + q3) (a serial chain over ~148 partials per thread was latency-bound)
+  const int e4 = blockIdx.x * blockDim.x + threadIdx.x, q = threadIdx.x & 3, e = e4 >> 2;
+  if (e >= J * J) return;  // (J * J * 4 and the block size are multiples of 4: groups exit together)
   const int i = e % J, j = e / J;
   double s = 0.0;
-  for (int b = 0; b < nblk; ++b) s += part[(int64_t)b * 4096 + i * 64 + j];
-  gram[i + (int64_t)J * j] = s;
+  for (int b = q; b < nblk; b += 4) s += part[(int64_t)b * 4096 + i * 64 + j];
+  const unsigned gm = 0xFu << (threadIdx.x & 28);
+  s += __shfl_xor_sync(gm, s, 1);
+  s += __shfl_xor_sync(gm, s, 2);
+  if (q == 0) gram[i + (int64_t)J * j] = s;
 }
 
 }  // namespace
@@ -688,7 +693,7 @@ bool ttm_ozaki(Ctx &c, const float *X, ModeView v, const double *A, int64_t lda,
             h[15], h[0], h[1], h[2], h[3], h[4], h[5], h[6], h[7], h[8], h[9], h[10], h[11], h[12]);
   }
   if (gsep) mode_gram(c, out, DT::F64, ModeView{1, J, P}, gram);
-  else if (gram) RT_LAUNCH(c, oz_gram_reduce_kernel, (J * J + 127) / 128, 128, 0, part.p, grid, J, gram);
+  else if (gram) RT_LAUNCH(c, oz_gram_reduce_kernel, (4 * J * J + 127) / 128, 128, 0, part.p, grid, J, gram);
   return true;
 }
 

@@ -946,10 +946,17 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // the bytes)
 __global__ void reduce_partials_f32_kernel(const float *__restrict__ partial, int nsplit, int64_t n,
                                            double *__restrict__ Y) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+  // four lanes per output (a serial chain over ~148 CTAs per thread was latency-bound): lane q of
+  // the group sums the partials k = q, q + 4, ... in order, then (q0 + q1) + (q2 + q3)
+  const int q = threadIdx.x & 3;
+  for (int64_t e4 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e4 < 4 * n; e4 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = e4 >> 2;  // (4 n is a multiple of 4 and the stride is too: groups stay aligned)
     double s = 0.0;
-    for (int k = 0; k < nsplit; ++k) s += (double)partial[(int64_t)k * n + e];
-    Y[e] = s;
+    for (int k = q; k < nsplit; k += 4) s += (double)partial[(int64_t)k * n + e];
+    const unsigned gm = 0xFu << (threadIdx.x & 28);  // this group's four lanes (always all active)
+    s += __shfl_xor_sync(gm, s, 1);
+    s += __shfl_xor_sync(gm, s, 2);
+    if (q == 0) Y[e] = s;
   }
 }
 
@@ -1109,7 +1116,7 @@ bool sketch_tc_mna(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_
   if (N == 32) launch_mna<32>(c, tm, p, g, smem);
   else launch_mna<64>(c, tm, p, g, smem);
   const int64_t n = v.I * ell;
-  RT_LAUNCH(c, reduce_partials_f32_kernel, (int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, part.p, g, n, Y);
+  RT_LAUNCH(c, reduce_partials_f32_kernel, (int)std::min<int64_t>(4096, (4 * n + 255) / 256), 256, 0, part.p, g, n, Y);
   if (normsq) sum_vec(c, npart.p, g, normsq);
   return true;
 }
@@ -1214,7 +1221,7 @@ bool sketch_tc_mn(Ctx &c, const float *X, ModeView v, int mode, int ell, int64_t
     else launch<64, false>(c, tm, p, g, smem);
   }
   const int64_t n = v.I * ell;
-  RT_LAUNCH(c, reduce_partials_f32_kernel, (int)std::min<int64_t>(1024, (n + 255) / 256), 256, 0, part.p, g, n, Y);
+  RT_LAUNCH(c, reduce_partials_f32_kernel, (int)std::min<int64_t>(4096, (4 * n + 255) / 256), 256, 0, part.p, g, n, Y);
   if (normsq) sum_vec(c, npart.p, g, normsq);
   return true;
 }
