@@ -43,6 +43,12 @@ bool bpass_tc_mn(Ctx &c, const float *X, ModeView v, const double *Q, int64_t ld
 // Y (I x ell) = X_(n) Om_(n)^T with an explicit fp64 (L, ell, R) tensor Om in place of Omega
 // (subspace iteration: Y = X_(n) Z with Z = B'^T), fp64 products, ell <= 64.
 void sketch_explicit(Ctx &c, const void *X, DT in, ModeView v, const double *Om, int ell, double *Y);
+// Deferred shrink (R-STHOSVD): the explicit sketch tensor Om (L', ell, R') of the
+// mode-m unfolding of B (G's dims gdims except mode n, which B holds at ell_n) such that
+// B_(m) Om = G_(m) Omega_m for G = B x_n V(:, :gdims[n])^T, V (ell_n x ell_n, col-major),
+// Omega_m the on-the-fly Gaussian of mode m (columns 0..ell-1, unsharded).
+void omega_fold(Ctx &c, const int64_t *gdims, int d, int n, int m, int ell_n, const double *V, int ell, uint64_t seed,
+                bool normals_f32, double *Om);
 // Rinv (n x n, column-major upper) = R^{-1} of the Cholesky factor G = R^T R of an SPD Gram
 // (subspace iteration's re-orthonormalisation); *bad = 1 on a non-positive pivot.
 void chol_rinv(Ctx &c, const double *G, int n, double *Rinv, int *bad);
@@ -67,6 +73,8 @@ void ttm_dense(Ctx &c, const void *X, DT in, ModeView v, const double *A, int64_
 
 // Gram of the mode-n unfolding of B (mode size v.I): gram (v.I x v.I, fp64).
 void mode_gram(Ctx &c, const void *B, DT t, ModeView v, double *gram);
+// Same for fp64 B with v.L, v.I <= 64, slab by slab (B(:, :, r) contiguous).
+void slab_gram(Ctx &c, const double *B, ModeView v, double *gram);
 
 // ---- linalg.cu ---------------------------------------------------------------------
 // gate (device int, optional): the kernels return immediately when *gate == 0.

@@ -10,5 +10,7 @@ void place_rows(Ctx &c, const double *y, int64_t ext, int ell, int64_t off, int6
 // sets ST_SHARD_LAYOUT in the status word unless every cov[i] == 1
 void check_cover(Ctx &c, const double *cov, int64_t I);
 // out = *normsq - sum_{i<r} w[i]
+// out = sum_{i<r} w_i (||U_B(:, :r)^T B||^2 = ||G||^2 after the shrink, without forming G)
+void sum_top_eigs(Ctx &c, const double *w, int r, double *out);
 void residual_from_eigs(Ctx &c, const double *w, int r, const double *normsq, double *out);
 }  // namespace rt

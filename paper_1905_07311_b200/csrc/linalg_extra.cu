@@ -50,6 +50,12 @@ __global__ void sum_first_kernel(const double *__restrict__ w, int r, const doub
   *out = *nsq - s;
 }
 
+__global__ void sum_top_kernel(const double *__restrict__ w, int r, double *__restrict__ out) {
+  double s = 0.0;
+  for (int i = 0; i < r; ++i) s += w[i];  // the order of factor_sign_kernel's sum
+  *out = s;
+}
+
 }  // namespace
 
 void ttm_expand(Ctx &c, const void *X, DT in, ModeView v, const double *M, int64_t ldm, int64_t J,
@@ -70,6 +76,10 @@ void place_rows(Ctx &c, const double *y, int64_t ext, int ell, int64_t off, int6
 
 void check_cover(Ctx &c, const double *cov, int64_t I) {
   RT_LAUNCH(c, check_cover_kernel, std::max(1, std::min(64, ceil_div(I, 256))), 256, 0, cov, I, c.status);
+}
+
+void sum_top_eigs(Ctx &c, const double *w, int r, double *out) {
+  RT_LAUNCH(c, sum_top_kernel, 1, 1, 0, w, r, out);
 }
 
 void residual_from_eigs(Ctx &c, const double *w, int r, const double *normsq, double *out) {

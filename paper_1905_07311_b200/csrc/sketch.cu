@@ -232,6 +232,20 @@ __global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict_
   //   L == 1: element e = tid + 256 q: row ii = e & 127, column pp = e >> 7 (coalesced along i)
   //   L > 1 : element e: column pp = e % 16, row ii = e / 16 (coalesced along p = l)
   Tin pre[kSP * 128 / 256];
+  // explicit Omega (ell <= 64): 4 values per thread and chunk, prefetched like X; consecutive
+  // threads read consecutive p (coalesced), one division per chunk
+  double opre[4];
+  auto load_om = [&](int64_t p0) {
+    const int pp = tid % kSP;
+    const int64_t p = p0 + pp;
+    const int64_t r = p / L, l = p - r * L;
+    const double *om = Om + l + L * (int64_t)ell * r;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int kk = tid / kSP + 16 * t;
+      opre[t] = (p < pend && kk < ell) ? om[L * kk] : 0.0;
+    }
+  };
   auto load_x = [&](int64_t p0) {
     if (L == 1) {
 #pragma unroll
@@ -253,7 +267,10 @@ __global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict_
       }
     }
   };
-  if (pbeg < pend) load_x(pbeg);
+  if (pbeg < pend) {
+    load_x(pbeg);
+    if (Om) load_om(pbeg);
+  }
   for (int64_t p0 = pbeg; p0 < pend; p0 += kSP) {
     __syncthreads();
 #pragma unroll
@@ -268,15 +285,12 @@ __global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict_
     // Omega chunk: rows p0.., columns k0.. (Philox block granularity); rows past pend are 0.
     // Explicit Omega (subspace iteration): Om stored (L, ell, R), Omega(p, k) = Om(l, k, r).
     if (Om) {
-      for (int e = tid; e < kSP * ell; e += 256) {
-        const int pp = e / ell, kk = e % ell;
-        const int64_t p = p0 + pp;
-        double v = 0.0;
-        if (p < pend) {
-          const int64_t r = p / L, l = p - r * L;
-          v = Om[l + L * (kk + (int64_t)ell * r)];
-        }
-        Os[pp * kSO + kk] = v;
+      // prefetched with the X chunk (load_om): thread -> column pp = tid % 16, rows tid / 16 + 16 t
+      const int pp = tid % kSP;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int kk = tid / kSP + 16 * t;
+        if (kk < ell) Os[pp * kSO + kk] = opre[t];
       }
     }
     for (int e = tid; e < kSP * nb && !Om; e += 256) {
@@ -291,7 +305,10 @@ __global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict_
       }
     }
     __syncthreads();
-    if (p0 + kSP < pend) load_x(p0 + kSP);  // in flight during the MMA block
+    if (p0 + kSP < pend) {  // in flight during the MMA block
+      load_x(p0 + kSP);
+      if (Om) load_om(p0 + kSP);
+    }
 #pragma unroll
     for (int ks = 0; ks < kSP / 4; ++ks) {
       double af[4], bf[4];
@@ -409,6 +426,76 @@ void sketch_dense(Ctx &c, const void *X, DT in, ModeView v, int mode, int ell, i
   sketch_dispatch<float, float>(c, (const float *)X, v, mode, ell, k0, seed, col_offset, Y, normsq, colmax);
 }
 
+
+// Om(l', k, r') = sum_a V[k_n + ell_n a] Omega_m(p(a), k) for the mode-m unfolding columns
+// p' = l' + L' r' of B (mode n of size ell_n); p(a) is the column of G = B x_n V(:, :r)^T with
+// i_n = a (deferred shrink).  One CTA per (p_lo, p_hi): the r x ell block of
+// Omega_m it needs is generated once (the sketch kernels' stream: key (seed, m), counter
+// (k >> 2, m, p)), the ell_n x ell outputs are sums over a in index order (deterministic).
+template <typename TN>
+__global__ void __launch_bounds__(256) omega_fold_kernel(int64_t sn, int r, int ell_n, int ell, int64_t Lb,
+                                                         uint64_t seed, int mode, const double *__restrict__ V,
+                                                         double *__restrict__ Om) {
+  extern __shared__ double fsm[];
+  const int rp = r | 1;               // odd strides: conflict-free column reads
+  double *Os = fsm;                   // [a][kk], stride ell
+  double *Vs = Os + (size_t)r * ell;  // [k][a], stride rp
+  const int64_t plo = (int64_t)blockIdx.x % sn, phi = (int64_t)blockIdx.x / sn;
+  const int nb = (ell + 3) >> 2, tid = threadIdx.x;
+  for (int e = tid; e < r * nb; e += blockDim.x) {
+    const int a = e / nb, jb = e - a * nb;
+    const uint4 w = omega_words(seed, mode, 0, (uint64_t)(plo + sn * (a + (int64_t)r * phi)), (uint32_t)jb);
+    Normal4<TN> z(w);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (4 * jb + q < ell) Os[a * ell + 4 * jb + q] = (double)z.v[q];
+  }
+  for (int e = tid; e < ell_n * r; e += blockDim.x) {
+    const int a = e / ell_n, k = e - a * ell_n;
+    Vs[k * rp + a] = V[k + (int64_t)ell_n * a];
+  }
+  __syncthreads();
+  const int nq = (ell + 3) >> 2;  // four sketch columns per thread: four independent chains
+  for (int e = tid; e < ell_n * nq; e += blockDim.x) {
+    const int q = e / ell_n, k = e - q * ell_n;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int a = 0; a < r; ++a) {
+      const double vk = Vs[k * rp + a];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s[u] = fma(vk, Os[a * ell + min(4 * q + u, ell - 1)], s[u]);
+    }
+    const int64_t pq = plo + sn * (k + (int64_t)ell_n * phi);
+    const int64_t rq = pq / Lb, lq = pq - rq * Lb;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (4 * q + u < ell) Om[lq + Lb * (4 * q + u + (int64_t)ell * rq)] = s[u];
+  }
+}
+
+void omega_fold(Ctx &c, const int64_t *gdims, int d, int n, int m, int ell_n, const double *V, int ell, uint64_t seed,
+                bool normals_f32, double *Om) {
+  RT_REQUIRE(n != m && ell >= 1 && ell <= 64 && ell_n >= 1 && ell_n <= 64, "omega_fold: bad shape");
+  const int r = (int)gdims[n];
+  int64_t sn = 1, P = 1, Lb = 1;
+  for (int k = 0; k < d; ++k) {
+    if (k == m) continue;
+    P *= gdims[k];
+    if (k < n) sn *= gdims[k];
+  }
+  for (int k = 0; k < m; ++k) Lb *= (k == n ? ell_n : gdims[k]);
+  const int64_t nhi = P / (sn * r);
+  if (sn == 0 || nhi == 0) return;
+  RT_REQUIRE(sn * nhi < (1ll << 31) && r <= 64, "omega_fold: grid too large");
+  const size_t smem = sizeof(double) * ((size_t)r * ell + (size_t)ell_n * (r | 1));
+  const unsigned grid = (unsigned)(sn * nhi);
+  if (normals_f32) {
+    smem_attr(omega_fold_kernel<float>, smem);
+    RT_LAUNCH(c, omega_fold_kernel<float>, grid, 256, smem, sn, r, ell_n, ell, Lb, seed, m, V, Om);
+  } else {
+    smem_attr(omega_fold_kernel<double>, smem);
+    RT_LAUNCH(c, omega_fold_kernel<double>, grid, 256, smem, sn, r, ell_n, ell, Lb, seed, m, V, Om);
+  }
+}
 
 void sketch_explicit(Ctx &c, const void *X, DT in, ModeView v, const double *Om, int ell, double *Y) {
   RT_REQUIRE(ell >= 1 && ell <= 64, "explicit sketch: 1 <= l <= 64");

@@ -322,6 +322,46 @@ __global__ void gram_reduce2_kernel(const double *__restrict__ partial, int nblk
   if (threadIdx.x == 0) gram[e] = (sred[0] + sred[1]) + (sred[2] + sred[3]);
 }
 
+// Gram of the middle index for L, J <= 64 (B(l, j, r), slabs B(:, :, r) of L J contiguous
+// doubles): each CTA sums M_r^T M_r over its contiguous range of r, thread = 4 x 4 tile of the
+// 64 x 64 partial, one partial per CTA, reduced in a fixed order by gram_reduce2_kernel.
+constexpr int kSGs = 68;  // slab row stride (doubles)
+__global__ void __launch_bounds__(256) slab_gram_kernel(const double *__restrict__ B, int L, int J, int64_t R,
+                                                        double *__restrict__ partial) {
+  __shared__ __align__(16) double sM[64 * kSGs];
+  const int tid = threadIdx.x, ta = tid >> 4, tb = tid & 15;
+  const int64_t r0 = (int64_t)blockIdx.x * R / gridDim.x, r1 = (int64_t)(blockIdx.x + 1) * R / gridDim.x;
+  for (int e = tid; e < 64 * kSGs; e += 256) sM[e] = 0.0;
+  double acc[4][4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+  const int LJ = L * J;
+  for (int64_t r = r0; r < r1; ++r) {
+    __syncthreads();
+    const double *src = B + r * (int64_t)LJ;
+    for (int e = tid; e < LJ; e += 256) {
+      const int j = e / L, l = e - j * L;
+      sM[l * kSGs + j] = src[e];
+    }
+    __syncthreads();
+    for (int l = 0; l < L; ++l) {
+      const double2 x0 = *(const double2 *)&sM[l * kSGs + 4 * ta], x1 = *(const double2 *)&sM[l * kSGs + 4 * ta + 2];
+      const double2 y0 = *(const double2 *)&sM[l * kSGs + 4 * tb], y1 = *(const double2 *)&sM[l * kSGs + 4 * tb + 2];
+      const double x[4] = {x0.x, x0.y, x1.x, x1.y}, y[4] = {y0.x, y0.y, y1.x, y1.y};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = fma(x[u], y[v], acc[u][v]);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int v = 0; v < 4; ++v) partial[(int64_t)blockIdx.x * 4096 + (4 * ta + u) * 64 + 4 * tb + v] = acc[u][v];
+}
+
 template <typename T>
 void mode_gram_t(Ctx &c, const T *B, ModeView v, double *gram) {
   const int64_t P = v.L * v.R;
@@ -1084,6 +1124,14 @@ void ttm_dispatch(Ctx &c, const Tin *X, ModeView v, const double *A, int64_t lda
 }
 
 }  // namespace
+
+void slab_gram(Ctx &c, const double *B, ModeView v, double *gram) {
+  RT_REQUIRE(v.L <= 64 && v.I <= 64, "slab_gram: L, J <= 64");
+  const int g = (int)std::max<int64_t>(1, std::min<int64_t>(v.R, (int64_t)c.num_sms * 2));
+  DevBuf<double> part(c, (size_t)g * 4096);
+  RT_LAUNCH(c, slab_gram_kernel, g, 256, 0, B, (int)v.L, (int)v.I, v.R, part.p);
+  RT_LAUNCH(c, gram_reduce2_kernel, (int)(v.I * v.I), 128, 0, part.p, g, (int)v.I, gram);
+}
 
 void mode_gram(Ctx &c, const void *B, DT t, ModeView v, double *gram) {
   if (t == DT::F64) mode_gram_t<double>(c, (const double *)B, v, gram);

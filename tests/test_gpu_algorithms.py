@@ -81,6 +81,15 @@ FP64_CASES = [
     ("ragged", lambda: np.asfortranarray(np.random.default_rng(3).standard_normal((37, 19, 41))),
      (7, 3, 11), 4, (2, 0, 1)),
     ("d4_wide_ell", lambda: hilbert((70, 9, 13, 11), "paper"), (40, 3, 5, 4), 25, None),
+    # R-STHOSVD deferred shrink: B of the first mode has >= 2^22 entries and
+    # l r > 2 (l - r) l_next, so the next mode sketches B with U_B folded into Omega (C2-style
+    # Tucker tensors: decaying core, Haar factors, 1e-3 noise)
+    ("deferred_f64", lambda: tucker_c2(5, (64, 300, 300), (56, 56, 56), 1e-3, np.float64), (40, 20, 20), 10, (0, 1, 2)),
+    # mode 3 first: the folded index sits above the sketched mode (p_lo spans I_2)
+    ("deferred_hi", lambda: tucker_c2(6, (300, 300, 64), (56, 56, 56), 1e-3, np.float64), (20, 20, 40), 10, (2, 0, 1)),
+    # 4 modes, mode 2 deferred into mode 4 (the folded index below the sketched mode, p_lo spans I_1)
+    ("deferred_d4", lambda: tucker_c2(7, (60, 40, 50, 45), (20, 36, 20, 20), 1e-3, np.float64), (10, 30, 12, 10), 8,
+     (1, 3, 0, 2)),
 ]
 
 
@@ -109,6 +118,8 @@ FP32_CASES = [
     # gets its column maxima from the separate column_maxima pass
     ("tall_mode1", lambda: np.asfortranarray(np.random.default_rng(11).standard_normal((1100, 24, 20))
                                              .astype(np.float32)), (10, 8, 8), 6, (0, 1, 2)),
+    # deferred shrink with fp32 data (fp32 normals folded with U_B in fp64)
+    ("deferred_f32", lambda: tucker_c2(8, (64, 300, 300), (56, 56, 56), 1e-3, np.float32), (40, 20, 20), 10, (0, 1, 2)),
 ]
 
 
