@@ -436,39 +436,53 @@ template <typename TN>
 __global__ void __launch_bounds__(256) omega_fold_kernel(int64_t sn, int r, int ell_n, int ell, int64_t Lb,
                                                          uint64_t seed, int mode, const double *__restrict__ V,
                                                          double *__restrict__ Om) {
-  extern __shared__ double fsm[];
-  const int rp = r | 1;               // odd strides: conflict-free column reads
-  double *Os = fsm;                   // [a][kk], stride ell
-  double *Vs = Os + (size_t)r * ell;  // [k][a], stride rp
+  extern __shared__ __align__(16) double fsm[];
+  const int ep = (ell + 3) & ~3, kp = (ell_n + 3) & ~3;  // rows padded to 4 (zero-filled)
+  double *Os = fsm;                                      // [a][kk], stride ep
+  double *Vs = Os + (size_t)r * ep;                      // [a][k], stride kp
   const int64_t plo = (int64_t)blockIdx.x % sn, phi = (int64_t)blockIdx.x / sn;
-  const int nb = (ell + 3) >> 2, tid = threadIdx.x;
+  const int nb = ep >> 2, tid = threadIdx.x;
   for (int e = tid; e < r * nb; e += blockDim.x) {
     const int a = e / nb, jb = e - a * nb;
     const uint4 w = omega_words(seed, mode, 0, (uint64_t)(plo + sn * (a + (int64_t)r * phi)), (uint32_t)jb);
     Normal4<TN> z(w);
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (4 * jb + q < ell) Os[a * ell + 4 * jb + q] = (double)z.v[q];
+    for (int q = 0; q < 4; ++q) Os[a * ep + 4 * jb + q] = 4 * jb + q < ell ? (double)z.v[q] : 0.0;
   }
-  for (int e = tid; e < ell_n * r; e += blockDim.x) {
-    const int a = e / ell_n, k = e - a * ell_n;
-    Vs[k * rp + a] = V[k + (int64_t)ell_n * a];
+  for (int e = tid; e < kp * r; e += blockDim.x) {
+    const int a = e / kp, k = e - a * kp;
+    Vs[a * kp + k] = k < ell_n ? V[k + (int64_t)ell_n * a] : 0.0;
   }
   __syncthreads();
-  const int nq = (ell + 3) >> 2;  // four sketch columns per thread: four independent chains
-  for (int e = tid; e < ell_n * nq; e += blockDim.x) {
-    const int q = e / ell_n, k = e - q * ell_n;
-    double s[4] = {0.0, 0.0, 0.0, 0.0};
+  // thread = 4 k x 4 kk outputs: per a two 32-byte loads of each operand and 16 independent FMAs
+  const int nkb = kp >> 2;
+  for (int e = tid; e < nkb * nb; e += blockDim.x) {
+    const int q = e / nkb, kb = e - q * nkb;
+    double s[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) s[i][u] = 0.0;
+#pragma unroll 2
     for (int a = 0; a < r; ++a) {
-      const double vk = Vs[k * rp + a];
+      const double2 v0 = *(const double2 *)&Vs[a * kp + 4 * kb], v1 = *(const double2 *)&Vs[a * kp + 4 * kb + 2];
+      const double2 o0 = *(const double2 *)&Os[a * ep + 4 * q], o1 = *(const double2 *)&Os[a * ep + 4 * q + 2];
+      const double vv[4] = {v0.x, v0.y, v1.x, v1.y}, oo[4] = {o0.x, o0.y, o1.x, o1.y};
 #pragma unroll
-      for (int u = 0; u < 4; ++u) s[u] = fma(vk, Os[a * ell + min(4 * q + u, ell - 1)], s[u]);
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) s[i][u] = fma(vv[i], oo[u], s[i][u]);
     }
-    const int64_t pq = plo + sn * (k + (int64_t)ell_n * phi);
-    const int64_t rq = pq / Lb, lq = pq - rq * Lb;
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (4 * q + u < ell) Om[lq + Lb * (4 * q + u + (int64_t)ell * rq)] = s[u];
+    for (int i = 0; i < 4; ++i) {
+      const int k = 4 * kb + i;
+      if (k >= ell_n) break;
+      const int64_t pq = plo + sn * (k + (int64_t)ell_n * phi);
+      const int64_t rq = pq / Lb, lq = pq - rq * Lb;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (4 * q + u < ell) Om[lq + Lb * (4 * q + u + (int64_t)ell * rq)] = s[i][u];
+    }
   }
 }
 
@@ -486,7 +500,7 @@ void omega_fold(Ctx &c, const int64_t *gdims, int d, int n, int m, int ell_n, co
   const int64_t nhi = P / (sn * r);
   if (sn == 0 || nhi == 0) return;
   RT_REQUIRE(sn * nhi < (1ll << 31) && r <= 64, "omega_fold: grid too large");
-  const size_t smem = sizeof(double) * ((size_t)r * ell + (size_t)ell_n * (r | 1));
+  const size_t smem = sizeof(double) * (size_t)r * (((ell + 3) & ~3) + ((ell_n + 3) & ~3));
   const unsigned grid = (unsigned)(sn * nhi);
   if (normals_f32) {
     smem_attr(omega_fold_kernel<float>, smem);

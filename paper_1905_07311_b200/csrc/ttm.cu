@@ -338,14 +338,28 @@ __global__ void __launch_bounds__(256) slab_gram_kernel(const double *__restrict
 #pragma unroll
     for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
   const int LJ = L * J;
+  double pre[16];  // the next slab, prefetched into registers (L J <= 4096: 16 per thread)
+  auto load = [&](int64_t r) {
+    const double *src = B + r * (int64_t)LJ;
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int e = tid + 256 * t;
+      pre[t] = e < LJ ? src[e] : 0.0;
+    }
+  };
+  if (r0 < r1) load(r0);
   for (int64_t r = r0; r < r1; ++r) {
     __syncthreads();
-    const double *src = B + r * (int64_t)LJ;
-    for (int e = tid; e < LJ; e += 256) {
-      const int j = e / L, l = e - j * L;
-      sM[l * kSGs + j] = src[e];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int e = tid + 256 * t;
+      if (e < LJ) {
+        const int j = e / L, l = e - j * L;
+        sM[l * kSGs + j] = pre[t];
+      }
     }
     __syncthreads();
+    if (r + 1 < r1) load(r + 1);
     for (int l = 0; l < L; ++l) {
       const double2 x0 = *(const double2 *)&sM[l * kSGs + 4 * ta], x1 = *(const double2 *)&sM[l * kSGs + 4 * ta + 2];
       const double2 y0 = *(const double2 *)&sM[l * kSGs + 4 * tb], y1 = *(const double2 *)&sM[l * kSGs + 4 * tb + 2];
