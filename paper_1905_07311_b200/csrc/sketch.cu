@@ -205,14 +205,23 @@ void launch_sketch(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int64_t 
 constexpr int kSP = 16;   // p per chunk
 constexpr int kSX = 136;  // Xs row stride (doubles, = 8 mod 16): conflict-free A fragments
 constexpr int kSO = 72;   // Os row stride
-template <typename Tin, typename TN>
-__global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict__ X, int64_t L, int64_t I, int64_t R,
-                                                          int64_t cols_per_split, uint64_t seed, int mode, int ell,
-                                                          int64_t k0, int64_t col_offset, double *__restrict__ partial,
-                                                          double *__restrict__ norm_partial,
-                                                          const double *__restrict__ Om = nullptr) {
-  __shared__ __align__(16) double Xs[kSP * kSX];
-  __shared__ __align__(16) double Os[kSP * kSO];
+// Shared memory is double buffered (dynamic, kSketchDfmaSmem bytes): per chunk a warp stores the
+// NEXT chunk (register-prefetched X, generated or explicit Omega) into the other buffer, issues
+// the global loads of the chunk after it and then runs the MMAs of the current buffer: one CTA
+// barrier per chunk, and the loads are in flight during the MMA block.  L1 (mode-1 layout) is a
+// template parameter and CTAs whose 128 rows are all inside I take unpredicated loads (ncu on
+// the C4 mode-2 sketch of B: the single-buffered form issued ~20 instructions per DMMA).  The
+// (l, r) split of a thread's column p is advanced incrementally (one division per CTA).
+constexpr size_t kSketchDfmaSmem = (size_t)2 * kSP * (kSX + kSO) * sizeof(double);
+template <typename Tin, typename TN, bool L1>
+__global__ void __launch_bounds__(256, 2) sketch_dfma_kernel(const Tin *__restrict__ X, int64_t L, int64_t I, int64_t R,
+                                                             int64_t cols_per_split, uint64_t seed, int mode, int ell,
+                                                             int64_t k0, int64_t col_offset, double *__restrict__ partial,
+                                                             double *__restrict__ norm_partial,
+                                                             const double *__restrict__ Om = nullptr) {
+  extern __shared__ __align__(16) double sk_smem[];
+  double *const XsB = sk_smem;                  // [2][kSP * kSX]
+  double *const OsB = sk_smem + 2 * kSP * kSX;  // [2][kSP * kSO]
   __shared__ double sred[8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 3, wn = warp >> 2, fr = lane >> 2, fc = lane & 3;
@@ -221,94 +230,127 @@ __global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict_
   const int64_t pbeg = (int64_t)blockIdx.y * cols_per_split, pend = min(P, pbeg + cols_per_split);
   const int64_t jb0 = k0 >> 2;
   const int nb = (int)(((k0 + ell - 1) >> 2) - jb0 + 1);
+  const bool rows_full = i0 + 128 <= I;
+  const bool want_norm = norm_partial != nullptr;
   double acc[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int q = 0; q < 4; ++q) acc[a][q][0] = acc[a][q][1] = 0.0;
   double nsq = 0.0;
-  for (int e = tid; e < kSP * kSO; e += 256) Os[e] = 0.0;
-  // X staging with a register prefetch of the next chunk (8 values per thread and chunk)
-  //   L == 1: element e = tid + 256 q: row ii = e & 127, column pp = e >> 7 (coalesced along i)
-  //   L > 1 : element e: column pp = e % 16, row ii = e / 16 (coalesced along p = l)
-  Tin pre[kSP * 128 / 256];
-  // explicit Omega (ell <= 64): 4 values per thread and chunk, prefetched like X; consecutive
-  // threads read consecutive p (coalesced), one division per chunk
+  for (int e = tid; e < 2 * kSP * kSO; e += 256) OsB[e] = 0.0;
+  __syncthreads();  // the zero fill precedes every Omega store
+  // X staging with a register prefetch (8 values per thread and chunk)
+  //   L1 : element e = tid + 256 q: row ii = tid & 127, column pp = (tid >> 7) + 2 q (coalesced along i)
+  //   !L1: column pp = tid % 16, row ii = tid / 16 + 16 q (coalesced along p = l)
+  constexpr int NQ = kSP * 128 / 256;
+  Tin pre[NQ];
   double opre[4];
-  auto load_om = [&](int64_t p0) {
-    const int pp = tid % kSP;
-    const int64_t p = p0 + pp;
-    const int64_t r = p / L, l = p - r * L;
-    const double *om = Om + l + L * (int64_t)ell * r;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int kk = tid / kSP + 16 * t;
-      opre[t] = (p < pend && kk < ell) ? om[L * kk] : 0.0;
+  const int xoff = L1 ? (tid >> 7) * kSX + (tid & 127) : (tid % kSP) * kSX + tid / kSP;
+  constexpr int xstep = L1 ? 2 * kSX : 16;
+  // column (tid % 16) of the chunk: p = l + L r, advanced by kSP per chunk
+  const int ppc = tid % kSP;
+  int64_t cl = 0, cr = 0;
+  if (!L1 || Om) {
+    const int64_t p = pbeg + ppc;
+    cr = p / L;
+    cl = p - cr * L;
+  }
+  auto advance = [&]() {
+    if (L1) {
+      cr += kSP;  // l = 0, r = p
+    } else {
+      cl += kSP;
+      while (cl >= L) { cl -= L; ++cr; }
     }
   };
-  auto load_x = [&](int64_t p0) {
-    if (L == 1) {
+  // loads of the chunk at p0; (cl, cr) must describe column p0 + ppc
+  auto load_chunk = [&](int64_t p0) {
+    if (Om) {
+      const bool pok = p0 + ppc < pend;
+      const double *om = Om + cl + L * (int64_t)ell * cr;
 #pragma unroll
-      for (int q = 0; q < kSP * 128 / 256; ++q) {
-        const int e = tid + 256 * q, ii = e & 127, pp = e >> 7;
-        const int64_t i = i0 + ii, p = p0 + pp;
-        pre[q] = (i < I && p < pend) ? X[i + I * p] : Tin(0);
+      for (int t = 0; t < 4; ++t) {
+        const int kk = tid / kSP + 16 * t;
+        opre[t] = (pok && kk < ell) ? om[L * kk] : 0.0;
       }
-    } else {  // this thread's column pp = tid % 16 is the same for every q: one div per chunk
-      const int pp = tid % kSP;
-      const int64_t p = p0 + pp;
-      const bool pok = p < pend;
-      const int64_t r = p / L, l = p - r * L;
-      const Tin *base = X + l + L * I * r;
+    }
+    if (L1) {
+      const int64_t i = i0 + (tid & 127);
+      const int64_t pf = p0 + (tid >> 7);
+      const Tin *src = X + i + I * pf;
+      if (rows_full && p0 + kSP <= pend) {
 #pragma unroll
-      for (int q = 0; q < kSP * 128 / 256; ++q) {
-        const int64_t i = i0 + tid / kSP + 16 * q;
-        pre[q] = (pok && i < I) ? base[L * i] : Tin(0);
+        for (int q = 0; q < NQ; ++q) pre[q] = src[(int64_t)(2 * q) * I];
+      } else {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) pre[q] = (i < I && pf + 2 * q < pend) ? src[(int64_t)(2 * q) * I] : Tin(0);
+      }
+    } else {
+      const bool pok = p0 + ppc < pend;
+      const int64_t ib = i0 + tid / kSP;
+      const Tin *src = X + cl + L * I * cr + L * ib;
+      if (rows_full && p0 + kSP <= pend) {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) pre[q] = src[(int64_t)(16 * q) * L];
+      } else {
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) pre[q] = (pok && ib + 16 * q < I) ? src[(int64_t)(16 * q) * L] : Tin(0);
+      }
+    }
+  };
+  // stores of the prefetched chunk at p0 into buffer b (Omega generated here when not explicit)
+  auto store_chunk = [&](int64_t p0, int b) {
+    double *Xs = XsB + b * (kSP * kSX);
+    double *Os = OsB + b * (kSP * kSO);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const double v = (double)pre[q];
+      if (want_norm) nsq = fma(v, v, nsq);
+      Xs[xoff + q * xstep] = v;
+    }
+    // Omega chunk: rows p0.., columns k0.. (Philox block granularity); rows past pend are 0.
+    // Explicit Omega (subspace iteration, deferred shrink): Om stored (L, ell, R), Omega(p, k) = Om(l, k, r).
+    if (Om) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int kk = tid / kSP + 16 * t;
+        if (kk < ell) Os[ppc * kSO + kk] = opre[t];
+      }
+    } else {
+      for (int e = tid; e < kSP * nb; e += 256) {
+        const int pp = e / nb, jb = e - pp * nb;
+        const int64_t p = p0 + pp;
+        const uint4 w = omega_words(seed, mode, 0, (uint64_t)(p + col_offset), (uint32_t)(jb0 + jb));
+        Normal4<TN> z(w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t kk = 4 * (jb0 + jb) + q - k0;
+          if (kk >= 0 && kk < ell) Os[pp * kSO + kk] = p < pend ? (double)z.v[q] : 0.0;
+        }
       }
     }
   };
   if (pbeg < pend) {
-    load_x(pbeg);
-    if (Om) load_om(pbeg);
+    load_chunk(pbeg);
+    store_chunk(pbeg, 0);
+    if (pbeg + kSP < pend) {
+      advance();
+      load_chunk(pbeg + kSP);
+    }
   }
-  for (int64_t p0 = pbeg; p0 < pend; p0 += kSP) {
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < kSP * 128 / 256; ++q) {
-      const int e = tid + 256 * q;
-      int ii, pp;
-      if (L == 1) { ii = e & 127; pp = e >> 7; } else { pp = e % kSP; ii = e / kSP; }
-      const double v = (double)pre[q];
-      nsq = fma(v, v, nsq);
-      Xs[pp * kSX + ii] = v;
-    }
-    // Omega chunk: rows p0.., columns k0.. (Philox block granularity); rows past pend are 0.
-    // Explicit Omega (subspace iteration): Om stored (L, ell, R), Omega(p, k) = Om(l, k, r).
-    if (Om) {
-      // prefetched with the X chunk (load_om): thread -> column pp = tid % 16, rows tid / 16 + 16 t
-      const int pp = tid % kSP;
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int kk = tid / kSP + 16 * t;
-        if (kk < ell) Os[pp * kSO + kk] = opre[t];
+  __syncthreads();
+  int buf = 0;
+  for (int64_t p0 = pbeg; p0 < pend; p0 += kSP, buf ^= 1) {
+    if (p0 + kSP < pend) {
+      store_chunk(p0 + kSP, buf ^ 1);
+      if (p0 + 2 * kSP < pend) {  // in flight during the MMA block
+        advance();
+        load_chunk(p0 + 2 * kSP);
       }
     }
-    for (int e = tid; e < kSP * nb && !Om; e += 256) {
-      const int pp = e / nb, jb = e % nb;
-      const int64_t p = p0 + pp;
-      const uint4 w = omega_words(seed, mode, 0, (uint64_t)(p + col_offset), (uint32_t)(jb0 + jb));
-      Normal4<TN> z(w);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t kk = 4 * (jb0 + jb) + q - k0;
-        if (kk >= 0 && kk < ell) Os[pp * kSO + kk] = p < pend ? (double)z.v[q] : 0.0;
-      }
-    }
-    __syncthreads();
-    if (p0 + kSP < pend) {  // in flight during the MMA block
-      load_x(p0 + kSP);
-      if (Om) load_om(p0 + kSP);
-    }
+    const double *Xs = XsB + buf * (kSP * kSX);
+    const double *Os = OsB + buf * (kSP * kSO);
 #pragma unroll
     for (int ks = 0; ks < kSP / 4; ++ks) {
       double af[4], bf[4];
@@ -324,6 +366,7 @@ __global__ void __launch_bounds__(256) sketch_dfma_kernel(const Tin *__restrict_
                        : "+d"(acc[mt][nt][0]), "+d"(acc[mt][nt][1])
                        : "d"(af[mt]), "d"(bf[nt]));
     }
+    __syncthreads();
   }
   // C fragment: acc[mt][nt][h] = Y(i = 32 wm + 8 mt + fr, k = 32 wn + 8 nt + 2 fc + h)
   double *dst = partial + (int64_t)blockIdx.y * I * ell;
@@ -366,8 +409,15 @@ void launch_sketch_dfma(Ctx &c, const Tin *X, ModeView v, int mode, int ell, int
   DevBuf<double> npart;
   if (normsq) npart.alloc(c, (size_t)nsplit * gx);
   dim3 grid(gx, (unsigned)nsplit);
-  RT_LAUNCH(c, (sketch_dfma_kernel<Tin, TN>), grid, 256, 0, X, v.L, v.I, v.R, cps, seed, mode, ell, k0, col_offset,
-            part.p, normsq ? npart.p : nullptr, Om);
+  if (v.L == 1) {
+    smem_attr(sketch_dfma_kernel<Tin, TN, true>, kSketchDfmaSmem);
+    RT_LAUNCH(c, (sketch_dfma_kernel<Tin, TN, true>), grid, 256, kSketchDfmaSmem, X, v.L, v.I, v.R, cps, seed, mode, ell,
+              k0, col_offset, part.p, normsq ? npart.p : nullptr, Om);
+  } else {
+    smem_attr(sketch_dfma_kernel<Tin, TN, false>, kSketchDfmaSmem);
+    RT_LAUNCH(c, (sketch_dfma_kernel<Tin, TN, false>), grid, 256, kSketchDfmaSmem, X, v.L, v.I, v.R, cps, seed, mode, ell,
+              k0, col_offset, part.p, normsq ? npart.p : nullptr, Om);
+  }
   const int64_t n = v.I * ell;
   RT_LAUNCH(c, reduce_splits_kernel, ceil_div(n, 256) > 1024 ? 1024 : ceil_div(n, 256), 256, 0, part.p, (int)nsplit, n,
             Y);
