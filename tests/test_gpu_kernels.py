@@ -89,6 +89,26 @@ def test_sketch_all_modes(ctx, name, make, ells):
             _check_elementwise(got, x, mode, ell, 11, 0, 1e-14 if x.dtype == np.float64 else 1e-6)
 
 
+@pytest.mark.parametrize("shape", [(1, 5, 1), (2, 7, 3), (3, 130, 5), (16, 129, 2), (17, 257, 33), (5, 4, 1500),
+                                   (260, 3, 2), (1, 1, 40)])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_sketch_fp64_edge_shapes(ctx, shape, dtype):
+    """The double-buffered fp64 tensor-core sketch at its corner cases: fewer columns than one
+    16-column chunk, exactly one / two chunks per split, a contiguous lower extent L below the
+    chunk (the incremental (l, r) split wraps several times per chunk), ragged 128-row tiles,
+    and both input types (fp32 data under the FP64 policy takes the same kernel).  Tolerance
+    2e-13 (|X||Omega|)_ik: with one or a few terms per entry nothing averages the generator's
+    own accuracy (fp64 normals within 1e-13 of the oracle's, test_omega_*; seen: 7e-14 on the
+    single-column case)."""
+    from paper_1905_07311_b200.rtucker import ACCUM_FP64
+    rng = np.random.default_rng(sum(shape))
+    x = np.asfortranarray(rng.standard_normal(shape).astype(dtype))
+    for mode in range(3):
+        for ell in (1, 9, 64):
+            got = ctx.debug_sketch(x, x.shape, mode, ell, seed=21, flags=ACCUM_FP64)
+            _check_elementwise(got, x, mode, ell, 21, 0, 2e-13)
+
+
 def test_sketch_fp32_with_fp64_policy(ctx):
     from paper_1905_07311_b200.rtucker import ACCUM_FP64
     x = hilbert((25,) * 5, "shifted", dtype=np.float32)
