@@ -410,7 +410,7 @@ __device__ __forceinline__ void seg_add(long long *aH, long long *aL, int lr, in
 }
 
 template <typename TV, typename TN>
-__global__ void __launch_bounds__(kBT, 2) bucket_sketch(const uint64_t *__restrict__ skey, const TV *__restrict__ sval,
+__global__ void __launch_bounds__(kBT, 3) bucket_sketch(const uint64_t *__restrict__ skey, const TV *__restrict__ sval,
                                                        const unsigned *__restrict__ bstart,
                                                        const int *__restrict__ istart, int nbk, int64_t I, int mode,
                                                        int ell, uint64_t seed, const FixScale *__restrict__ fs,
@@ -1031,7 +1031,7 @@ void sketch_coo(Ctx &c, const CooDev &g, int mode, int ell, uint64_t seed, bool 
     const int gs = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)c.num_sms * 8, (g.nnz + kBChunk - 1) / kBChunk));
     smem_attr(bucket_hist, sizeof(unsigned) * nbk);
     RT_LAUNCH(c, bucket_hist, gs, kBT, sizeof(unsigned) * nbk, g, nnz_dev, mode, nbk, cnt.p);
-    const int gk = c.num_sms * 2;
+    const int gk = c.num_sms * 3;
     RT_LAUNCH(c, bucket_scan, 1, kScanT, 0, cnt.p, nbk, bstart.p, cur.p, istart.p, istart.p + nbk + 1, gk);
     unsigned long long *yh = (unsigned long long *)Yf.p, *yl = yh + (size_t)I * ell;
 #define RT_BUCKETED(TV, TN)                                                                                  \
