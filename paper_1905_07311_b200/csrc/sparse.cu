@@ -705,17 +705,24 @@ __global__ void __launch_bounds__(kSrT) srrqr_coop_kernel(const double *__restri
   }
   for (int64_t i = gt; i < m; i += gs) mark[i] = 0;
   grid.sync();
+  // Per-CTA candidates go to alternating halves of pv / pi (2 gridDim.x entries each): a CTA that
+  // runs ahead writes the other half, and it cannot reach the call after that (the same half
+  // again) before every CTA has passed this call's barrier, i.e. finished reading: one grid
+  // barrier per reduction instead of two.
+  int am_par = 0;
   auto global_argmax = [&](ArgMax b) -> ArgMax {
     b = block_argmax_all(b);
+    double *pvh = pv + (size_t)am_par * gridDim.x;
+    int64_t *pih = pi + (size_t)am_par * gridDim.x;
+    am_par ^= 1;
     if (threadIdx.x == 0) {
-      pv[blockIdx.x] = b.v;
-      pi[blockIdx.x] = b.i;
+      pvh[blockIdx.x] = b.v;
+      pih[blockIdx.x] = b.i;
     }
     grid.sync();
     ArgMax gb{-1.0, INT64_MAX};
-    for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) gb = better(gb, ArgMax{pv[q], pi[q]});
+    for (int q = threadIdx.x; q < (int)gridDim.x; q += blockDim.x) gb = better(gb, ArgMax{pvh[q], pih[q]});
     gb = block_argmax_all(gb);
-    grid.sync();  // every CTA has read pv/pi before they are rewritten
     return gb;
   };
   // ---- Businger-Golub CPQR on Q^T
